@@ -1,0 +1,170 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes binding of the CPU restatement of the
+reference fastsil hot path (oracle/fsil_oracle.cpp).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline and
+``--impl reference`` legs may import this package.  It is the parity checker
+and the CPU baseline, never the thing measured or shipped.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libfsil_oracle.so")
+_lib = None
+
+SQEUCLID, COSINE, EUCLID = 0, 1, 2
+FAST, NAIVE = 0, 1
+METRICS = {"sqeuclid": SQEUCLID, "squared_euclidean": SQEUCLID, "cosine": COSINE,
+           "euclid": EUCLID, "euclidean": EUCLID}
+
+
+class OracleValidationError(ValueError):
+    """fastsil::ValidationError (types.hpp:41-44)."""
+
+
+class OracleInvalidArgument(ValueError):
+    """std::invalid_argument raised by the reference."""
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB_PATH):
+        subprocess.run(["make", "-C", _HERE, "-s"], check=True)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB_PATH)
+        P = ctypes.c_void_p
+        i64, i32, dbl, sz, cp = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_size_t, ctypes.c_char_p
+        L.orc_silhouette_f32.argtypes = [i32, i32, P, P, i64, i64, i32, P, P, P, P, P, P, P, P, P, cp, sz]
+        L.orc_silhouette.argtypes = [i32, i32, P, P, i64, i64, i32, P, P, P, P, P, P, P, P, P, cp, sz]
+        L.orc_aggregate_f32.argtypes = [i32, P, P, i64, i64, i32, P, P, P, P, cp, sz]
+        L.orc_score_rows_f32.argtypes = [i32, P, P, i64, i64, i32, P, P, P, P, i64, P, P, P, P, cp, sz]
+        L.orc_plan_shards.argtypes = [i64, i32, P, P, cp, sz]
+        L.orc_assemble_score.argtypes = [dbl, dbl, P, cp, sz]
+        L.orc_default_shards.restype = i32
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _check(rc, err):
+    if rc == 0:
+        return
+    msg = err.value.decode()
+    if rc == 2:
+        raise OracleValidationError(msg)
+    if rc == 3:
+        raise OracleInvalidArgument(msg)
+    raise RuntimeError(f"oracle error {rc}: {msg}")
+
+
+@dataclass
+class OracleReport:
+    a: np.ndarray
+    b: np.ndarray
+    s: np.ndarray
+    own: np.ndarray
+    neighbour: np.ndarray
+    mean: float
+    k: int
+    dense_to_raw: np.ndarray
+    wall_ms: float
+
+
+def silhouette(X, labels, metric="sqeuclid", engine="fast", shards=0) -> OracleReport:
+    """compute_silhouette(validate_and_densify(X, labels), ...) (engine.cpp:76-92)."""
+    m = METRICS[metric] if isinstance(metric, str) else int(metric)
+    e = NAIVE if engine == "naive" else FAST
+    X = np.ascontiguousarray(X)
+    n = X.shape[0]
+    d = X.shape[1] if X.ndim == 2 else 0
+    labels = np.ascontiguousarray(labels, dtype=np.int32)
+    out = [np.zeros(n) for _ in range(3)] + [np.zeros(n, np.int32) for _ in range(2)]
+    mean, wall = ctypes.c_double(0), ctypes.c_double(0)
+    k = ctypes.c_int32(0)
+    d2r = np.zeros(max(n, 1), np.int32)
+    err = ctypes.create_string_buffer(512)
+    fn = lib().orc_silhouette_f32 if X.dtype == np.float32 else lib().orc_silhouette
+    if X.dtype not in (np.float32, np.float64):
+        X = X.astype(np.float64)
+        fn = lib().orc_silhouette
+    rc = fn(m, e, _ptr(X), _ptr(labels), n if labels.shape[0] == n else labels.shape[0], d, shards,
+            *[_ptr(o) for o in out], ctypes.byref(mean), ctypes.byref(k), _ptr(d2r),
+            ctypes.byref(wall), err, 512)
+    _check(rc, err)
+    return OracleReport(out[0], out[1], out[2], out[3], out[4], mean.value, k.value,
+                        d2r[: k.value].copy(), wall.value)
+
+
+def aggregate(X, labels, metric="sqeuclid", shards=0):
+    """Merged phase-1 statistics (engine.hpp:50-80): (counts, sums[K,D], psi|None)."""
+    m = METRICS[metric] if isinstance(metric, str) else int(metric)
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    n, d = X.shape
+    labels = np.ascontiguousarray(labels, dtype=np.int32)
+    kmax = len(np.unique(labels))
+    counts = np.zeros(kmax, np.int64)
+    sums = np.zeros((kmax, d))
+    psi = np.zeros(kmax)
+    k = ctypes.c_int32(0)
+    err = ctypes.create_string_buffer(512)
+    rc = lib().orc_aggregate_f32(m, _ptr(X), _ptr(labels), n, d, shards, _ptr(counts), _ptr(sums),
+                                 _ptr(psi), ctypes.byref(k), err, 512)
+    _check(rc, err)
+    return counts, sums, (psi if m == SQEUCLID else None)
+
+
+def score_rows(X, dense, counts, sums, psi, rows, metric="sqeuclid"):
+    """score_range on sampled rows against global stats -> (a, b, s, neighbour)."""
+    m = METRICS[metric] if isinstance(metric, str) else int(metric)
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    n, d = X.shape
+    dense = np.ascontiguousarray(dense, dtype=np.int32)
+    counts = np.ascontiguousarray(counts, dtype=np.int64)
+    sums = np.ascontiguousarray(sums, dtype=np.float64)
+    psi_a = None if psi is None else np.ascontiguousarray(psi, dtype=np.float64)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    mm = rows.shape[0]
+    a, b, s = np.zeros(mm), np.zeros(mm), np.zeros(mm)
+    nb = np.zeros(mm, np.int32)
+    err = ctypes.create_string_buffer(512)
+    rc = lib().orc_score_rows_f32(m, _ptr(X), _ptr(dense), n, d, counts.shape[0], _ptr(counts),
+                                  _ptr(sums), _ptr(psi_a), _ptr(rows), mm, _ptr(a), _ptr(b),
+                                  _ptr(s), _ptr(nb), err, 512)
+    _check(rc, err)
+    return a, b, s, nb
+
+
+def plan_shards(n, w):
+    """plan_shards (engine.cpp:8-25) -> list of (begin, end)."""
+    ranges = np.zeros(2 * max(1, min(max(w, 1), max(n, 1))), np.int64)
+    ns = ctypes.c_int(0)
+    err = ctypes.create_string_buffer(512)
+    rc = lib().orc_plan_shards(n, w, _ptr(ranges), ctypes.byref(ns), err, 512)
+    _check(rc, err)
+    return [(int(ranges[2 * i]), int(ranges[2 * i + 1])) for i in range(ns.value)]
+
+
+def assemble_score(a, b):
+    s = ctypes.c_double(0)
+    err = ctypes.create_string_buffer(512)
+    rc = lib().orc_assemble_score(a, b, ctypes.byref(s), err, 512)
+    _check(rc, err)
+    return s.value
+
+
+def default_shards():
+    return lib().orc_default_shards()

@@ -1,0 +1,494 @@
+// capi.cu -- the C ABI (include/fsil.h): context, validation in the reference's
+// order and wording, the single-GPU pipeline and the sharded protocol.
+//
+// Pipeline per call (all on ctx->stream; two host syncs: K after densify, and
+// the final scalar words):
+//   K0 densify (densify.cu) -> K1 aggregate (aggregate.cu) -> derive ->
+//   K2 score_ffma | K3 score_tc -> K4 refine -> K5 tile-group sum (finalize.cu)
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "fsil_internal.cuh"
+#include "score_common.cuh"
+
+namespace fsil {
+
+void score_ffma(fsil_context* c, const ScoreParams& p);
+int64_t ffma_tiles(int64_t n);
+bool ffma_supported(const fsil_context* c);
+void flag_all(fsil_context* c, const ScoreParams& p, int tile_rows);
+void refine(fsil_context* c, const ScoreParams& p);
+void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows);
+bool tc_supported(const fsil_context* c);
+int64_t tc_tiles(const fsil_context* c, int* tile_rows);
+void score_tc(fsil_context* c, const ScoreParams& p);
+
+namespace {
+
+void record(fsil_context* c, int i) {
+  if (c->timing) FSIL_CUDA(cudaEventRecord(c->ev[i], c->stream));
+}
+
+void check_metric(int metric) {
+  if (metric != FSIL_SQEUCLID && metric != FSIL_COSINE && metric != FSIL_EUCLID)
+    fail(FSIL_ERR_INVALID_ARGUMENT, "unknown metric code " + std::to_string(metric));
+}
+
+// validate_and_densify's shape checks (dataset.cpp:29-34).
+void check_shape(int64_t n_global, int64_t d) {
+  if (n_global < 2)
+    fail(FSIL_ERR_VALIDATION, "dataset needs at least 2 points, got " + std::to_string(n_global));
+  if (d < 1) fail(FSIL_ERR_VALIDATION, "dataset needs at least 1 feature dimension");
+}
+
+void begin(fsil_context* c, int metric, const float* dX, const int32_t* dlabels, int64_t n_local,
+           int32_t d, int64_t row_offset, int64_t n_global) {
+  check_metric(metric);
+  check_shape(n_global, d);
+  if (n_local < 0 || row_offset < 0 || row_offset + n_local > n_global)
+    fail(FSIL_ERR_INVALID_ARGUMENT, "shard rows outside the dataset");
+  if (n_local > 0 && (!dX || !dlabels)) fail(FSIL_ERR_INVALID_ARGUMENT, "null input pointer");
+  FSIL_CUDA(cudaSetDevice(c->device));
+  c->metric = metric;
+  c->X = dX;
+  c->labels = dlabels;
+  c->n = n_local;
+  c->n_global = n_global;
+  c->row_offset = row_offset;
+  c->d = d;
+  c->dp = (static_cast<int64_t>(d) + 3) / 4 * 4;
+  c->k = 0;
+  c->launches = 0;
+  c->stats = fsil_stats{};
+  record(c, 0);
+  densify_collect(c);
+  c->phase = 1;
+}
+
+void set_dictionary(fsil_context* c, const int32_t* raw, int32_t k) {
+  if (c->phase < 1) fail(FSIL_ERR_INVALID_ARGUMENT, "fsil_shard_begin must come first");
+  if (k < 1 || (k > 0 && !raw)) fail(FSIL_ERR_INVALID_ARGUMENT, "empty dictionary");
+  c->k = k;
+  densify_assign_and_map(c, raw, k);
+  record(c, 1);
+  c->phase = 2;
+}
+
+void do_aggregate(fsil_context* c) {
+  if (c->phase < 2) fail(FSIL_ERR_INVALID_ARGUMENT, "dictionary not set");
+  // Plain euclidean has no aggregable decomposition; the dataset is still
+  // validated first, as the reference builds the Dataset before dispatching.
+  const int saved = c->metric;
+  if (c->metric == FSIL_EUCLID) c->metric = FSIL_SQEUCLID;
+  aggregate(c);
+  c->metric = saved;
+  record(c, 2);
+  c->phase = 3;
+}
+
+ScoreParams make_params(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a,
+                        double* b) {
+  ScoreParams p{};
+  p.X = c->X;
+  p.dense = c->dense.as<int32_t>();
+  p.n = c->n;
+  p.d = c->d;
+  p.dp = static_cast<int>(c->dp);
+  p.k = c->k;
+  p.mu32 = c->mu32.as<float>();
+  p.p32 = c->p32.as<float>();
+  p.stats = c->stats_buf.as<double>();
+  p.nk = c->nk.as<double>();
+  p.bound = c->bound.as<float>();
+  if (!s) {
+    c->s_tmp.ensure(std::max<int64_t>(c->n, 1) * sizeof(double));
+    s = c->s_tmp.as<double>();
+  }
+  p.s = s;
+  p.nb = nb;
+  p.own = own;
+  p.a = a;
+  p.b = b;
+  return p;
+}
+
+void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, double* b) {
+  if (c->phase < 3) fail(FSIL_ERR_INVALID_ARGUMENT, "aggregate must come before score");
+  c->result.ensure(4 * sizeof(double));
+  FSIL_CUDA(cudaMemsetAsync(c->result.p, 0, 4 * sizeof(double), c->stream));
+  c->phase = 4;
+  if (c->k < 2 || c->metric == FSIL_EUCLID || c->n == 0) {  // reported by finish
+    record(c, 3); record(c, 4); record(c, 5);
+    return;
+  }
+  derive(c);
+  ScoreParams p = make_params(c, s, nb, own, a, b);
+  int use = c->path;
+  const bool tc_ok = tc_supported(c), ffma_ok = ffma_supported(c);
+  if (use == FSIL_PATH_AUTO) {
+    if (c->k <= 32 && ffma_ok) use = FSIL_PATH_FFMA;
+    else if (tc_ok) use = FSIL_PATH_TCGEN05;
+    else if (ffma_ok) use = FSIL_PATH_FFMA;
+    else use = FSIL_PATH_FP64;
+  }
+  if (use == FSIL_PATH_TCGEN05 && !tc_ok)
+    fail(FSIL_ERR_INVALID_ARGUMENT, "tcgen05 scoring path unavailable for this shape");
+  if (use == FSIL_PATH_FFMA && !ffma_ok)
+    fail(FSIL_ERR_INVALID_ARGUMENT, "FFMA scoring path unavailable for this shape (D too large)");
+  int tile_rows = 256;
+  const int64_t ntiles = use == FSIL_PATH_TCGEN05 ? tc_tiles(c, &tile_rows) : ffma_tiles(c->n);
+  c->tile_sum.ensure(std::max<int64_t>(ntiles, 1) * sizeof(double));
+  c->tile_flag.ensure(std::max<int64_t>(ntiles, 1) * sizeof(int32_t));
+  c->flag_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int32_t));
+  c->flag_count.ensure(sizeof(unsigned long long));
+  FSIL_CUDA(cudaMemsetAsync(c->flag_count.p, 0, sizeof(unsigned long long), c->stream));
+  p.tile_sum = c->tile_sum.as<double>();
+  p.tile_flag = c->tile_flag.as<int32_t>();
+  p.flag_rows = c->flag_rows.as<int32_t>();
+  p.flag_count = c->flag_count.as<unsigned long long>();
+  record(c, 3);
+  if (use == FSIL_PATH_TCGEN05) score_tc(c, p);
+  else if (use == FSIL_PATH_FFMA) score_ffma(c, p);
+  else flag_all(c, p, tile_rows);
+  c->score_path = use;
+  record(c, 4);
+  refine(c, p);
+  record(c, 5);
+  finalize_sum(c, p, ntiles, tile_rows);
+}
+
+// Reads the (all-reduced) validation word and sum; raises in the reference's order.
+double finish(fsil_context* c, double* flagged_out) {
+  if (c->phase < 4) fail(FSIL_ERR_INVALID_ARGUMENT, "score must come before finish");
+  int64_t checks[2] = {kNone, kNone};
+  double res[2] = {0, 0};
+  int missing = 0;
+  FSIL_CUDA(cudaMemcpyAsync(checks, c->checks.p, sizeof(checks), cudaMemcpyDeviceToHost, c->stream));
+  FSIL_CUDA(cudaMemcpyAsync(res, c->result.p, sizeof(res), cudaMemcpyDeviceToHost, c->stream));
+  FSIL_CUDA(cudaMemcpyAsync(&missing, c->counters.as<int>() + 4, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  record(c, 6);
+  FSIL_CUDA(cudaStreamSynchronize(c->stream));
+  FSIL_CUDA(cudaGetLastError());
+  c->phase = 0;
+  if (checks[0] != kNone) {
+    const int64_t row = checks[0] / c->d, dim = checks[0] % c->d;
+    fail(FSIL_ERR_VALIDATION, "non-finite feature value at point " + std::to_string(row) +
+                                  ", dimension " + std::to_string(dim));
+  }
+  if (c->k < 2)
+    fail(FSIL_ERR_VALIDATION, "silhouette undefined for a single cluster: need K >= 2, got K = " +
+                                  std::to_string(c->k));
+  if (c->metric == FSIL_EUCLID)
+    fail(FSIL_ERR_VALIDATION,
+         "no fast engine for plain euclidean distance (no aggregable decomposition); use the naive "
+         "engine");
+  if (checks[1] != kNone)
+    fail(FSIL_ERR_VALIDATION,
+         "cosine distance undefined for zero vector (point " + std::to_string(checks[1]) + ")");
+  if (missing) fail(FSIL_ERR_INTERNAL, "a row's label is missing from the dense dictionary");
+  c->stats.n = c->n;
+  c->stats.d = c->d;
+  c->stats.k = c->k;
+  c->stats.path = c->score_path;
+  c->stats.agg_path = c->agg_path;
+  c->stats.flagged_rows = static_cast<int64_t>(res[1]);
+  c->stats.kernel_launches = c->launches;
+  if (c->timing) {
+    float* ms[5] = {&c->stats.ms_densify, &c->stats.ms_aggregate, &c->stats.ms_score,
+                    &c->stats.ms_refine, &c->stats.ms_finalize};
+    const int from[5] = {0, 1, 3, 4, 5}, to[5] = {1, 2, 4, 5, 6};
+    for (int i = 0; i < 5; ++i) FSIL_CUDA(cudaEventElapsedTime(ms[i], c->ev[from[i]], c->ev[to[i]]));
+  }
+  if (flagged_out) *flagged_out = res[1];
+  return res[0] / static_cast<double>(c->n_global);
+}
+
+// Dense order = ascending first row (dataset.cpp:41-51).
+std::vector<int32_t> order_dictionary(std::vector<std::pair<int64_t, int32_t>>& rows_labels) {
+  std::sort(rows_labels.begin(), rows_labels.end());
+  std::vector<int32_t> raw(rows_labels.size());
+  for (size_t i = 0; i < raw.size(); ++i) raw[i] = rows_labels[i].second;
+  return raw;
+}
+
+std::vector<std::pair<int64_t, int32_t>> fetch_dictionary(fsil_context* c) {
+  std::vector<int32_t> labels(static_cast<size_t>(c->n_distinct));
+  std::vector<int64_t> rows(static_cast<size_t>(c->n_distinct));
+  if (c->n_distinct > 0) {
+    FSIL_CUDA(cudaMemcpyAsync(labels.data(), c->dict_labels.p, labels.size() * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, c->stream));
+    FSIL_CUDA(cudaMemcpyAsync(rows.data(), c->dict_rows.p, rows.size() * sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, c->stream));
+    FSIL_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  std::vector<std::pair<int64_t, int32_t>> out(labels.size());
+  for (size_t i = 0; i < labels.size(); ++i) out[i] = {rows[i], labels[i]};
+  return out;
+}
+
+double run_device(fsil_context* c, int metric, const float* dX, const int32_t* dlabels, int64_t n,
+                  int32_t d, double* ds, int32_t* dnb, int32_t* down, double* da, double* db,
+                  int32_t* k_out, int32_t* dense_to_raw) {
+  begin(c, metric, dX, dlabels, n, d, 0, n);
+  auto dict = fetch_dictionary(c);
+  const std::vector<int32_t> raw = order_dictionary(dict);
+  set_dictionary(c, raw.data(), static_cast<int32_t>(raw.size()));
+  do_aggregate(c);
+  do_score(c, ds, dnb, down, da, db);
+  const double mean = finish(c, nullptr);
+  if (k_out) *k_out = c->k;
+  if (dense_to_raw) std::copy(raw.begin(), raw.end(), dense_to_raw);
+  return mean;
+}
+
+template <typename F>
+fsil_status guarded(fsil_context* c, F&& f) {
+  try {
+    f();
+    if (c) c->last_error.clear();
+    return FSIL_OK;
+  } catch (const Error& e) {
+    if (c) {
+      c->last_error = e.what();
+      c->phase = 0;
+    }
+    return e.status;
+  } catch (const std::exception& e) {
+    if (c) {
+      c->last_error = e.what();
+      c->phase = 0;
+    }
+    return FSIL_ERR_INTERNAL;
+  }
+}
+
+}  // namespace
+}  // namespace fsil
+
+using namespace fsil;
+
+namespace {
+thread_local std::string g_create_error;
+}
+
+extern "C" {
+
+int fsil_abi_version(void) { return FSIL_ABI_VERSION; }
+
+fsil_status fsil_create(fsil_context** out, int device) {
+  if (!out) return FSIL_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  auto* c = new fsil_context();
+  const fsil_status st = guarded(c, [&] {
+    int count = 0;
+    FSIL_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count)
+      fail(FSIL_ERR_CUDA, "no CUDA device " + std::to_string(device) + " (have " + std::to_string(count) + ")");
+    cudaDeviceProp prop{};
+    FSIL_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      fail(FSIL_ERR_CUDA, std::string("libfsil is built for sm_100a (B200); device is ") + prop.name);
+    FSIL_CUDA(cudaSetDevice(device));
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
+    FSIL_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+    for (auto& e : c->ev) FSIL_CUDA(cudaEventCreate(&e));
+  });
+  if (st != FSIL_OK) {
+    g_create_error = c->last_error;  // reachable through fsil_last_error(NULL)
+    fsil_destroy(c);
+    return st;
+  }
+  *out = c;
+  return FSIL_OK;
+}
+
+void fsil_destroy(fsil_context* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  fsil::DevBuf* bufs[] = {&c->ht_keys, &c->ht_vals, &c->ht_dense, &c->dict_labels, &c->dict_rows,
+                          &c->counters, &c->dense, &c->stats_buf, &c->checks, &c->partials,
+                          &c->sort_tmp, &c->sort_keys, &c->sort_vals, &c->iota, &c->seg_start,
+                          &c->piece_start, &c->mu32, &c->p32, &c->nk, &c->bound, &c->s_tmp,
+                          &c->tile_sum, &c->tile_flag, &c->flag_rows, &c->flag_count, &c->result,
+                          &c->group_sum, &c->hX, &c->hL, &c->o_s, &c->o_nb, &c->o_own, &c->o_a,
+                          &c->o_b};
+  for (auto* b : bufs) b->release();
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* fsil_last_error(const fsil_context* c) {
+  return c ? c->last_error.c_str() : g_create_error.c_str();
+}
+
+fsil_status fsil_set_stream(fsil_context* c, void* stream) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    if (stream) {
+      if (c->own_stream && c->stream) FSIL_CUDA(cudaStreamDestroy(c->stream));
+      c->stream = static_cast<cudaStream_t>(stream);
+      c->own_stream = false;
+    } else if (!c->own_stream) {
+      FSIL_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+  });
+}
+
+fsil_status fsil_set_path(fsil_context* c, int path) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  if (path < FSIL_PATH_AUTO || path > FSIL_PATH_FP64) {
+    c->last_error = "unknown scoring path";
+    return FSIL_ERR_INVALID_ARGUMENT;
+  }
+  c->path = path;
+  return FSIL_OK;
+}
+
+fsil_status fsil_set_timing(fsil_context* c, int enabled) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  c->timing = enabled != 0;
+  return FSIL_OK;
+}
+
+fsil_status fsil_get_stats(const fsil_context* c, fsil_stats* out) {
+  if (!c || !out) return FSIL_ERR_INVALID_ARGUMENT;
+  *out = c->stats;
+  return FSIL_OK;
+}
+
+fsil_status fsil_silhouette_device(fsil_context* c, int metric, const float* dX,
+                                   const int32_t* dlabels, int64_t n, int32_t d, double* ds,
+                                   int32_t* dnb, int32_t* down, double* da, double* db,
+                                   double* mean, int32_t* k_out, int32_t* dense_to_raw) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    const double m = run_device(c, metric, dX, dlabels, n, d, ds, dnb, down, da, db, k_out, dense_to_raw);
+    if (mean) *mean = m;
+  });
+}
+
+fsil_status fsil_silhouette(fsil_context* c, int metric, const float* X, const int32_t* labels,
+                            int64_t n, int32_t d, double* s, int32_t* neighbour, int32_t* own,
+                            double* a, double* b, double* mean, int32_t* k_out,
+                            int32_t* dense_to_raw) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    check_metric(metric);
+    check_shape(n, d);
+    if (!X || !labels) fail(FSIL_ERR_INVALID_ARGUMENT, "null input pointer");
+    FSIL_CUDA(cudaSetDevice(c->device));
+    const size_t xb = static_cast<size_t>(n) * d * sizeof(float);
+    c->hX.ensure(xb);
+    c->hL.ensure(n * sizeof(int32_t));
+    FSIL_CUDA(cudaMemcpyAsync(c->hX.p, X, xb, cudaMemcpyHostToDevice, c->stream));
+    FSIL_CUDA(cudaMemcpyAsync(c->hL.p, labels, n * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+    double* ds = nullptr;
+    int32_t *dnb = nullptr, *down = nullptr;
+    double *da = nullptr, *db = nullptr;
+    if (s) { c->o_s.ensure(n * sizeof(double)); ds = c->o_s.as<double>(); }
+    if (neighbour) { c->o_nb.ensure(n * sizeof(int32_t)); dnb = c->o_nb.as<int32_t>(); }
+    if (own) { c->o_own.ensure(n * sizeof(int32_t)); down = c->o_own.as<int32_t>(); }
+    if (a) { c->o_a.ensure(n * sizeof(double)); da = c->o_a.as<double>(); }
+    if (b) { c->o_b.ensure(n * sizeof(double)); db = c->o_b.as<double>(); }
+    const double m = run_device(c, metric, c->hX.as<float>(), c->hL.as<int32_t>(), n, d, ds, dnb,
+                                down, da, db, k_out, dense_to_raw);
+    if (s) FSIL_CUDA(cudaMemcpyAsync(s, ds, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (neighbour) FSIL_CUDA(cudaMemcpyAsync(neighbour, dnb, n * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    if (own) FSIL_CUDA(cudaMemcpyAsync(own, down, n * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    if (a) FSIL_CUDA(cudaMemcpyAsync(a, da, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (b) FSIL_CUDA(cudaMemcpyAsync(b, db, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    FSIL_CUDA(cudaStreamSynchronize(c->stream));
+    if (mean) *mean = m;
+  });
+}
+
+fsil_status fsil_shard_begin(fsil_context* c, int metric, const float* dX, const int32_t* dlabels,
+                             int64_t n_local, int32_t d, int64_t row_offset, int64_t n_global,
+                             int64_t* n_distinct) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    begin(c, metric, dX, dlabels, n_local, d, row_offset, n_global);
+    if (n_distinct) *n_distinct = c->n_distinct;
+  });
+}
+
+fsil_status fsil_shard_get_dictionary(fsil_context* c, int32_t* raw_labels, int64_t* first_rows) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    if (c->phase < 1) fail(FSIL_ERR_INVALID_ARGUMENT, "fsil_shard_begin must come first");
+    auto dict = fetch_dictionary(c);
+    std::sort(dict.begin(), dict.end());
+    for (size_t i = 0; i < dict.size(); ++i) {
+      if (raw_labels) raw_labels[i] = dict[i].second;
+      if (first_rows) first_rows[i] = dict[i].first;
+    }
+  });
+}
+
+fsil_status fsil_shard_set_dictionary(fsil_context* c, const int32_t* raw, int32_t k) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] { set_dictionary(c, raw, k); });
+}
+
+fsil_status fsil_shard_aggregate(fsil_context* c, double** d_stats, int64_t* stats_len,
+                                 int64_t** d_checks) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    do_aggregate(c);
+    const int m = c->metric == FSIL_EUCLID ? FSIL_SQEUCLID : c->metric;
+    if (d_stats) *d_stats = c->stats_buf.as<double>();
+    if (stats_len) *stats_len = StatsLayout{m, c->k, c->d}.len();
+    if (d_checks) *d_checks = c->checks.as<int64_t>();
+  });
+}
+
+fsil_status fsil_shard_score(fsil_context* c, double* ds, int32_t* dnb, int32_t* down, double* da,
+                             double* db, double** d_partial) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    do_score(c, ds, dnb, down, da, db);
+    if (d_partial) *d_partial = c->result.as<double>();
+  });
+}
+
+fsil_status fsil_shard_finish(fsil_context* c, double* mean) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    const double m = finish(c, nullptr);
+    if (mean) *mean = m;
+  });
+}
+
+fsil_status fsil_plan_shards(int64_t n, int32_t requested, int64_t* ranges, int32_t* num_shards) {
+  if (n < 1 || requested < 1 || !ranges) return FSIL_ERR_INVALID_ARGUMENT;
+  const int64_t w = std::min<int64_t>(requested, n);
+  const int64_t base = n / w, extra = n % w;
+  int64_t begin = 0;
+  for (int64_t s = 0; s < w; ++s) {
+    const int64_t size = base + (s < extra ? 1 : 0);
+    ranges[2 * s] = begin;
+    ranges[2 * s + 1] = begin + size;
+    begin += size;
+  }
+  if (num_shards) *num_shards = static_cast<int32_t>(w);
+  return FSIL_OK;
+}
+
+fsil_status fsil_assemble_score(double a, double b, double* s) {
+  if (!s || a < 0.0 || b < 0.0) return FSIL_ERR_INVALID_ARGUMENT;
+  *s = (a == 0.0 && b == 0.0) ? 0.0 : (a <= b ? 1.0 - a / b : b / a - 1.0);
+  return FSIL_OK;
+}
+
+}  // extern "C"

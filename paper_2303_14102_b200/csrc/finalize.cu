@@ -1,0 +1,167 @@
+// finalize.cu -- K4 fp64 refinement of uncertified rows and K5 deterministic mean.
+//
+// K4 re-evaluates every foreign cluster of a flagged row in fp64 with the
+// reference formulas and the reference's argmin rule (ascending k, strict <,
+// so ties keep the lowest dense id: squared_euclidean.cpp:94-103,
+// cosine.cpp:103-112), then rewrites a_i, b_i, s_i and the neighbour.
+// K5 sums s_i in a fixed order (tile partials written by the scoring kernel,
+// tiles that held refined rows re-summed from s[]), replacing the reference's
+// serial left-to-right sum (report.cpp:36-40); the result is bit-identical run
+// to run, and within ~1e-16 relative of the serial sum.
+#include <algorithm>
+
+#include "score_common.cuh"
+
+namespace fsil {
+namespace {
+
+template <bool COS>
+__global__ void __launch_bounds__(256) refine_kernel(ScoreParams p) {
+  const unsigned long long count = *p.flag_count;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const double* sums = p.stats + (COS ? p.k : 2 * p.k);
+  for (int64_t i = warp; i < static_cast<int64_t>(count); i += nwarps) {
+    const int64_t row = p.flag_rows[i];
+    const float* x = p.X + row * p.d;
+    const int own = p.dense[row];
+    double ss = 0.0;
+    for (int l = lane; l < p.d; l += 32) {
+      const double v = x[l];
+      ss = fma(v, v, ss);
+    }
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    const double nrm = sqrt(ss);
+    double best = INFINITY;
+    int arg = -1;
+    for (int k = lane; k < p.k; k += 32) {  // ascending within the lane
+      if (k == own) continue;
+      const double* yk = sums + static_cast<int64_t>(k) * p.d;
+      double cross = 0.0;
+      for (int l = 0; l < p.d; ++l) cross = fma(yk[l], static_cast<double>(x[l]), cross);
+      const double m = COS ? cos_foreign(p.nk[k], cross / nrm)
+                           : sq_foreign(ss, p.stats[p.k + k], p.nk[k], cross);
+      if (m < best) {
+        best = m;
+        arg = k;
+      }
+    }
+    // warp argmin with ties broken towards the lowest k
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oa = __shfl_xor_sync(0xffffffffu, arg, off);
+      if (oa >= 0 && (arg < 0 || ob < best || (ob == best && oa < arg))) {
+        best = ob;
+        arg = oa;
+      }
+    }
+    // own-cluster mean, dims split over lanes
+    const double* yo = sums + static_cast<int64_t>(own) * p.d;
+    double co = 0.0;
+    for (int l = lane; l < p.d; l += 32) co = fma(yo[l], static_cast<double>(x[l]), co);
+    for (int off = 16; off > 0; off >>= 1) co += __shfl_xor_sync(0xffffffffu, co, off);
+    if (lane == 0) {
+      const double n_o = p.nk[own];
+      const bool singleton = n_o == 1.0;
+      double a = 0.0;
+      if (!singleton) a = COS ? cos_own(n_o, co / nrm) : sq_own(ss, p.stats[p.k + own], n_o, co);
+      const double s = singleton ? 0.0 : assemble_score(a, best);
+      p.s[row] = s;
+      if (p.nb) p.nb[row] = arg;
+      if (p.own) p.own[row] = own;
+      if (p.a) p.a[row] = a;
+      if (p.b) p.b[row] = best;
+    }
+  }
+}
+
+// Group partials: one thread per tile, fixed-order tree per block.
+__global__ void __launch_bounds__(256) tile_group_kernel(const double* __restrict__ tile_sum,
+                                                         const int32_t* __restrict__ tile_flag,
+                                                         const double* __restrict__ s,
+                                                         int64_t ntiles, int tile_rows, int64_t n,
+                                                         double* group_sum) {
+  __shared__ double sm[256];
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  double v = 0.0;
+  if (t < ntiles) {
+    if (tile_flag[t]) {
+      const int64_t r0 = t * tile_rows, r1 = min(n, r0 + tile_rows);
+      double acc = 0.0;
+      for (int64_t r = r0; r < r1; ++r) acc += s[r];
+      v = acc;
+    } else {
+      v = tile_sum[t];
+    }
+  }
+  sm[threadIdx.x] = v;
+  __syncthreads();
+  for (int stride = 128; stride > 0; stride >>= 1) {
+    if (threadIdx.x < stride) sm[threadIdx.x] += sm[threadIdx.x + stride];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) group_sum[blockIdx.x] = sm[0];
+}
+
+__global__ void __launch_bounds__(1024) total_kernel(const double* __restrict__ group_sum,
+                                                     int64_t ngroups,
+                                                     const unsigned long long* flag_count,
+                                                     double* result) {
+  __shared__ double sm[1024];
+  double acc = 0.0;
+  for (int64_t g = threadIdx.x; g < ngroups; g += 1024) acc += group_sum[g];
+  sm[threadIdx.x] = acc;
+  __syncthreads();
+  for (int stride = 512; stride > 0; stride >>= 1) {
+    if (threadIdx.x < stride) sm[threadIdx.x] += sm[threadIdx.x + stride];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    result[0] = sm[0];
+    result[1] = static_cast<double>(*flag_count);
+  }
+}
+
+// FSIL_PATH_FP64: every row goes through the fp64 re-evaluation.
+__global__ void flag_all_kernel(int64_t n, int tile_rows, int32_t* flag_rows, int32_t* tile_flag,
+                                double* tile_sum, unsigned long long* flag_count) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) flag_rows[i] = static_cast<int32_t>(i);
+  if (i < (n + tile_rows - 1) / tile_rows) {
+    tile_flag[i] = 1;
+    tile_sum[i] = 0.0;
+  }
+  if (i == 0) *flag_count = static_cast<unsigned long long>(n);
+}
+
+}  // namespace
+
+void flag_all(fsil_context* c, const ScoreParams& p, int tile_rows) {
+  flag_all_kernel<<<static_cast<unsigned>((p.n + 255) / 256), 256, 0, c->stream>>>(
+      p.n, tile_rows, p.flag_rows, p.tile_flag, p.tile_sum, p.flag_count);
+  FSIL_LAUNCHED(c);
+}
+
+void refine(fsil_context* c, const ScoreParams& p) {
+  const int grid = c->num_sms * 4;
+  if (c->metric == FSIL_COSINE) refine_kernel<true><<<grid, 256, 0, c->stream>>>(p);
+  else refine_kernel<false><<<grid, 256, 0, c->stream>>>(p);
+  FSIL_LAUNCHED(c);
+}
+
+void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows) {
+  const int64_t ngroups = (ntiles + 255) / 256;
+  c->group_sum.ensure(std::max<int64_t>(ngroups, 1) * sizeof(double));
+  c->result.ensure(4 * sizeof(double));
+  if (ngroups > 0) {
+    tile_group_kernel<<<static_cast<unsigned>(ngroups), 256, 0, c->stream>>>(
+        p.tile_sum, p.tile_flag, p.s, ntiles, tile_rows, p.n, c->group_sum.as<double>());
+    FSIL_LAUNCHED(c);
+  }
+  total_kernel<<<1, 1024, 0, c->stream>>>(c->group_sum.as<double>(), ngroups, p.flag_count,
+                                          c->result.as<double>());
+  FSIL_LAUNCHED(c);
+}
+
+}  // namespace fsil

@@ -1,0 +1,144 @@
+// fsil_internal.cuh -- shared device/host definitions for libfsil (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "fsil.h"
+
+namespace fsil {
+
+// ---- errors crossing the internal C++ layers (converted to fsil_status at the C ABI) ----
+struct Error : std::runtime_error {
+  fsil_status status;
+  Error(fsil_status st, const std::string& msg) : std::runtime_error(msg), status(st) {}
+};
+[[noreturn]] inline void fail(fsil_status st, const std::string& msg) { throw Error(st, msg); }
+
+#define FSIL_CUDA(call)                                                                    \
+  do {                                                                                     \
+    cudaError_t e__ = (call);                                                              \
+    if (e__ != cudaSuccess)                                                                \
+      ::fsil::fail(FSIL_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e__));    \
+  } while (0)
+
+#define FSIL_LAUNCHED(ctx)                                                                 \
+  do {                                                                                     \
+    cudaError_t e__ = cudaGetLastError();                                                  \
+    if (e__ != cudaSuccess)                                                                \
+      ::fsil::fail(FSIL_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e__)); \
+    ++(ctx)->launches;                                                                     \
+  } while (0)
+
+constexpr int kNumSMs = 148;  // B200; the context re-reads the real count
+
+// ---- grow-only device scratch -----------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+  void ensure(size_t want) {
+    if (want <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t cap = want < 4096 ? 4096 : want + want / 8;
+    FSIL_CUDA(cudaMalloc(&p, cap));
+    bytes = cap;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+// Layout of the fp64 cluster-statistics buffer (the all-reduce payload):
+//   sqeuclid: [count K][psi K][sums K*D]    -> K*(D+2)
+//   cosine  : [count K][sums K*D]           -> K*(D+1)
+struct StatsLayout {
+  int metric;
+  int64_t k, d;
+  int64_t count_off() const { return 0; }
+  int64_t psi_off() const { return k; }
+  int64_t sums_off() const { return metric == FSIL_SQEUCLID ? 2 * k : k; }
+  int64_t len() const { return sums_off() + k * d; }
+};
+
+// Derived per-cluster constants consumed by the scoring kernels.
+struct Derived {
+  float* mu32;       // [K][dp] fp32: Y_k/n_k (sqeuclid) or Omega_k/n_k (cosine), zero padded
+  float* p32;        // [K] sqeuclid: psi_k/n_k in fp32
+  double* nk;        // [K] counts as fp64
+  float* bound;      // [4]: max ||mu_k||, max p_k, 0, 0 (fp32, rounded up)
+};
+
+// Validation word, all-reduced with MIN across ranks.
+//   [0] first non-finite element as global row*D + dim (INT64_MAX if none)
+//   [1] first zero-norm row (cosine only; INT64_MAX if none)
+constexpr int64_t kNone = INT64_MAX;
+
+}  // namespace fsil
+
+// ---- context (C ABI handle) ----------------------------------------------------------------
+struct fsil_context {
+  int device = 0;
+  int num_sms = fsil::kNumSMs;
+  size_t smem_optin = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int path = FSIL_PATH_AUTO;
+  bool timing = false;
+  std::string last_error;
+  int64_t launches = 0;
+  fsil_stats stats{};
+
+  // shard/call state
+  int metric = FSIL_SQEUCLID;
+  const float* X = nullptr;
+  const int32_t* labels = nullptr;
+  int64_t n = 0, n_global = 0, row_offset = 0;
+  int32_t d = 0, k = 0;
+  int64_t dp = 0;  // d rounded up to a multiple of 4
+  int64_t n_distinct = 0;
+  int agg_path = 0;
+  int score_path = 0;
+  int phase = 0;  // 0 idle, 1 begun, 2 dictionary set, 3 aggregated, 4 scored
+
+  // scratch (grow-only)
+  fsil::DevBuf ht_keys, ht_vals, ht_dense, dict_labels, dict_rows, counters;
+  fsil::DevBuf dense;          // [n] int32 dense labels
+  fsil::DevBuf stats_buf;      // fp64 stats (all-reduce payload)
+  fsil::DevBuf checks;         // int64[2] validation word
+  fsil::DevBuf partials;       // aggregation block partials
+  fsil::DevBuf sort_tmp, sort_keys, sort_vals, iota;  // label-sorted aggregation
+  fsil::DevBuf seg_start, piece_start;
+  fsil::DevBuf mu32, p32, nk, bound;
+  fsil::DevBuf s_tmp;          // s when the caller passes no s pointer
+  fsil::DevBuf tile_sum, tile_flag, flag_rows, flag_count;
+  fsil::DevBuf result;         // double[4]: sum_s, flagged, ... (shard partial)
+  fsil::DevBuf group_sum;
+  // host staging for fsil_silhouette (pageable -> pinned)
+  fsil::DevBuf hX, hL;         // device copies of host inputs
+  fsil::DevBuf o_s, o_nb, o_own, o_a, o_b;
+  int64_t ht_cap = 0;
+  cudaEvent_t ev[8] = {};
+};
+
+namespace fsil {
+
+// kernels.cu entry points (host launchers), all async on ctx->stream
+void densify_collect(fsil_context* c);     // fills ctx->n_distinct (syncs)
+void densify_assign_and_map(fsil_context* c, const int32_t* raw_in_dense_order, int32_t k);
+void aggregate(fsil_context* c);           // stats_buf + checks
+void derive(fsil_context* c);              // mu32, p32, nk, bound
+void score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, double* b);
+void finalize_partial(fsil_context* c, double* s);  // result[0] = sum s, result[1] = flagged
+void score_tc(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, double* b);
+bool tc_supported(const fsil_context* c);
+
+}  // namespace fsil
