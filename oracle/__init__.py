@@ -48,6 +48,7 @@ def lib():
         L.orc_silhouette_f32.argtypes = [i32, i32, P, P, i64, i64, i32, P, P, P, P, P, P, P, P, P, cp, sz]
         L.orc_silhouette.argtypes = [i32, i32, P, P, i64, i64, i32, P, P, P, P, P, P, P, P, P, cp, sz]
         L.orc_aggregate_f32.argtypes = [i32, P, P, i64, i64, i32, P, P, P, P, cp, sz]
+        L.orc_aggregate_dense_f32.argtypes = [i32, P, P, i64, i64, i32, i32, P, P, P, cp, sz]
         L.orc_score_rows_f32.argtypes = [i32, P, P, i64, i64, i32, P, P, P, P, i64, P, P, P, P, cp, sz]
         L.orc_plan_shards.argtypes = [i64, i32, P, P, cp, sz]
         L.orc_assemble_score.argtypes = [dbl, dbl, P, cp, sz]
@@ -123,6 +124,32 @@ def aggregate(X, labels, metric="sqeuclid", shards=0):
     err = ctypes.create_string_buffer(512)
     rc = lib().orc_aggregate_f32(m, _ptr(X), _ptr(labels), n, d, shards, _ptr(counts), _ptr(sums),
                                  _ptr(psi), ctypes.byref(k), err, 512)
+    _check(rc, err)
+    return counts, sums, (psi if m == SQEUCLID else None)
+
+
+def first_appearance(labels):
+    """Dense ids by first appearance (dataset.cpp:41-51) without strings: (dense, raw_in_order)."""
+    labels = np.asarray(labels)
+    uniq, first, inv = np.unique(labels, return_index=True, return_inverse=True)
+    order = np.argsort(first, kind="stable")
+    rank = np.empty_like(order)
+    rank[order] = np.arange(order.shape[0])
+    return rank[inv].astype(np.int32), uniq[order]
+
+
+def aggregate_dense(X, dense, k, metric="sqeuclid", shards=0):
+    """Merged phase-1 statistics over already-dense labels -> (counts, sums[K,D], psi|None)."""
+    m = METRICS[metric] if isinstance(metric, str) else int(metric)
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    n, d = X.shape
+    dense = np.ascontiguousarray(dense, dtype=np.int32)
+    counts = np.zeros(k, np.int64)
+    sums = np.zeros((k, d))
+    psi = np.zeros(k)
+    err = ctypes.create_string_buffer(512)
+    rc = lib().orc_aggregate_dense_f32(m, _ptr(X), _ptr(dense), n, d, k, shards, _ptr(counts),
+                                       _ptr(sums), _ptr(psi), err, 512)
     _check(rc, err)
     return counts, sums, (psi if m == SQEUCLID else None)
 

@@ -677,6 +677,58 @@ int orc_aggregate_f32(int metric, const float* X, const int32_t* labels, int64_t
   });
 }
 
+int orc_aggregate_dense_f32(int metric, const float* X, const int32_t* dense, int64_t n, int64_t d,
+                            int32_t k, int shards, int64_t* counts, double* sums, double* psi,
+                            char* err, size_t errlen) {
+  // Same per-row arithmetic as partial_cluster_stats / partial_unit_sums
+  // (sqE.cpp:37-50, cos.cpp:39-57) read straight from fp32 storage (each value
+  // widened exactly), same N-only block plan and ascending fold
+  // (engine.hpp:37-40,75-78); no fp64 copy of X, so 123 GB inputs fit.
+  return guarded(err, errlen, [&] {
+    const bool cos = to_metric(metric) == orc::Metric::Cosine;
+    const int64_t block = orc::aggregation_block_size(n);
+    const int64_t nblocks = (n + block - 1) / block;
+    const int64_t S = k * (d + 2);
+    std::vector<std::vector<double>> part(static_cast<size_t>(nblocks));
+    std::vector<double> xd(static_cast<size_t>(d));
+    auto run_block = [&](int64_t b) {
+      std::vector<double> st(static_cast<size_t>(S), 0.0);  // [count K][psi K][sums K*D]
+      std::vector<double> row(static_cast<size_t>(d));
+      const int64_t e = std::min(n, (b + 1) * block);
+      for (int64_t i = b * block; i < e; ++i) {
+        const int c = dense[i];
+        if (c < 0 || c >= k) throw orc::ValidationError("cluster label out of range");
+        for (int64_t l = 0; l < d; ++l) row[l] = static_cast<double>(X[i * d + l]);
+        const double ss = orc::sq_norm(row.data(), d);
+        st[c] += 1.0;
+        double* y = st.data() + 2 * k + static_cast<int64_t>(c) * d;
+        if (cos) {
+          const double nrm = std::sqrt(ss);
+          if (nrm == 0.0) orc::throw_zero_norm(i);
+          for (int64_t l = 0; l < d; ++l) y[l] += row[l] / nrm;
+        } else {
+          st[k + c] += ss;
+          for (int64_t l = 0; l < d; ++l) y[l] += row[l];
+        }
+      }
+      part[static_cast<size_t>(b)] = std::move(st);
+    };
+    const int w = shards > 0 ? shards : orc::default_shards();
+    std::atomic<int64_t> next{0};
+    orc::run_workers(static_cast<int>(std::min<int64_t>(w, nblocks)), [&](int) {
+      for (int64_t b; (b = next.fetch_add(1)) < nblocks;) run_block(b);
+    });
+    std::vector<double> merged = std::move(part[0]);
+    for (int64_t b = 1; b < nblocks; ++b)
+      for (int64_t j = 0; j < S; ++j) merged[j] += part[b][j];
+    for (int32_t c = 0; c < k; ++c) {
+      counts[c] = static_cast<int64_t>(merged[c]);
+      if (!cos && psi) psi[c] = merged[k + c];
+    }
+    std::copy(merged.begin() + 2 * k, merged.end(), sums);
+  });
+}
+
 int orc_score_rows_f32(int metric, const float* X, const int32_t* dense, int64_t n, int64_t d,
                        int32_t k, const int64_t* counts, const double* sums, const double* psi,
                        const int64_t* rows, int64_t m, double* a, double* b, double* s,

@@ -79,6 +79,13 @@ int orc_score_rows_f32(int metric, const float* X, const int32_t* dense, int64_t
                        const int64_t* rows, int64_t m, double* a, double* b, double* s,
                        int32_t* neighbour, char* err, size_t errlen);
 
+/* aggregate_cluster_stats over labels that are already dense ids in [0, k)
+ * (skips the string densify, which is impractical at 1e8 rows); same block
+ * plan and fold as orc_aggregate_f32.  Used to pin full-size configs. */
+int orc_aggregate_dense_f32(int metric, const float* X, const int32_t* dense, int64_t n, int64_t d,
+                            int32_t k, int shards, int64_t* counts, double* sums, double* psi,
+                            char* err, size_t errlen);
+
 /* plan_shards (engine.cpp:8-25): writes w' (begin,end) pairs, returns w'. */
 int orc_plan_shards(int64_t n, int requested, int64_t* ranges, int* num_shards, char* err,
                     size_t errlen);

@@ -31,10 +31,14 @@ constexpr int kPieceRows = 2048;
 // ---------------------------------------------------------------- path 1 ----
 // Lanes of a warp are split into RPW row sub-groups of LPR lanes; each lane
 // covers CPL chunks of VEC floats of the row.  Copy index = warp*RPW + sub.
+// Within a copy the cluster sums are stored "chunk-transposed" (element l at
+// (l%VEC)*nchunks + l/VEC) so that a sub-group's read-modify-writes hit
+// consecutive doubles (bank-conflict free).  U rows per slot are loaded ahead.
 template <bool COS, int VEC, int CPL>
 __global__ void __launch_bounds__(256) agg_private_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ dense, int64_t n, int d,
     int64_t row_offset, int k, int lpr, double* __restrict__ partials, int64_t* checks) {
+  constexpr int U = 4;
   extern __shared__ double sm[];
   const int S = COS ? k * (d + 1) : k * (d + 2);
   const int sums_off = COS ? k : 2 * k;
@@ -48,79 +52,108 @@ __global__ void __launch_bounds__(256) agg_private_kernel(
   double* my = sm + (warp * rpw + sub) * S;
   const int64_t G = static_cast<int64_t>(gridDim.x) * copies;
   const int nchunks = (d + VEC - 1) / VEC;
-  for (int64_t base = (static_cast<int64_t>(blockIdx.x) * warps + warp) * rpw; base < n; base += G) {
-    const int64_t r = base + sub;  // warp-uniform trip count; sub-groups past n are masked
-    const bool valid = r < n;
-    const int lab = valid ? dense[r] : 0;
-    float v[CPL][VEC];
+  const int64_t wbase = (static_cast<int64_t>(blockIdx.x) * warps + warp) * rpw;
+  for (int64_t base = wbase; base < n; base += U * G) {
+    float v[U][CPL][VEC];
+    int lab[U];
+    bool valid[U];
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      const int ch = li + c * lpr;
-      if constexpr (VEC == 4) {
-        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid && ch < nchunks) t = ldg_stream(reinterpret_cast<const float4*>(X + r * d) + ch);
-        v[c][0] = t.x; v[c][1] = t.y; v[c][2] = t.z; v[c][3] = t.w;
-      } else {
-        v[c][0] = (valid && ch < nchunks) ? __ldg(X + r * d + ch) : 0.f;
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = base + sub + u * G;
+      valid[u] = r < n;
+      lab[u] = valid[u] ? __ldg(dense + r) : 0;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int ch = li + c * lpr;
+        if constexpr (VEC == 4) {
+          float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (valid[u] && ch < nchunks) t = ldg_stream(reinterpret_cast<const float4*>(X + r * d) + ch);
+          v[u][c][0] = t.x; v[u][c][1] = t.y; v[u][c][2] = t.z; v[u][c][3] = t.w;
+        } else {
+          v[u][c][0] = (valid[u] && ch < nchunks) ? __ldg(X + r * d + ch) : 0.f;
+        }
       }
     }
-    double ss = 0.0;
-    bool finite = true;
 #pragma unroll
-    for (int c = 0; c < CPL; ++c)
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) {
-        const double x = v[c][e];
-        ss += x * x;
-        finite = finite && isfinite(v[c][e]);
-      }
-    if (!finite) {
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = base + sub + u * G;
+      double ss = 0.0;
+      bool finite = true;
 #pragma unroll
       for (int c = 0; c < CPL; ++c)
 #pragma unroll
         for (int e = 0; e < VEC; ++e) {
-          const int l = (li + c * lpr) * VEC + e;
-          if (l < d && !isfinite(v[c][e])) atomic_min_i64(checks, (row_offset + r) * d + l);
+          const double x = v[u][c][e];
+          ss = fma(x, x, ss);
+          finite = finite && isfinite(v[u][c][e]);
         }
-    }
-    for (int off = lpr >> 1; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off, lpr);
-    if (!valid) continue;
-    double scale = 1.0;
-    if (COS) {
-      if (ss == 0.0) {
-        if (li == 0) atomic_min_i64(checks + 1, row_offset + r);
-        continue;
-      }
-      scale = 1.0 / sqrt(ss);
-    }
-    if (li == 0) {
-      my[lab] += 1.0;
-      if (!COS) my[k + lab] += ss;
-    }
-    double* ys = my + sums_off + static_cast<int64_t>(lab) * d;
+      if (!finite) {
 #pragma unroll
-    for (int c = 0; c < CPL; ++c)
+        for (int c = 0; c < CPL; ++c)
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) {
-        const int l = (li + c * lpr) * VEC + e;
-        if (l < d) ys[l] += COS ? static_cast<double>(v[c][e]) * scale : static_cast<double>(v[c][e]);
+          for (int e = 0; e < VEC; ++e) {
+            const int l = (li + c * lpr) * VEC + e;
+            if (l < d && !isfinite(v[u][c][e])) atomic_min_i64(checks, (row_offset + r) * d + l);
+          }
       }
+      for (int off = lpr >> 1; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off, lpr);
+      if (!valid[u]) continue;
+      double scale = 1.0;
+      if (COS) {
+        if (ss == 0.0) {
+          if (li == 0) atomic_min_i64(checks + 1, row_offset + r);
+          continue;
+        }
+        scale = 1.0 / sqrt(ss);
+      }
+      if (li == 0) {
+        my[lab[u]] += 1.0;
+        if (!COS) my[k + lab[u]] += ss;
+      }
+      double* ys = my + sums_off + static_cast<int64_t>(lab[u]) * d;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int ch = li + c * lpr;
+        if (ch < nchunks) {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const double x = COS ? static_cast<double>(v[u][c][e]) * scale : static_cast<double>(v[u][c][e]);
+            ys[e * nchunks + ch] += x;
+          }
+        }
+      }
+    }
   }
   __syncthreads();
   for (int j = threadIdx.x; j < S; j += blockDim.x) {
+    int src = j;
+    if (j >= sums_off) {  // undo the chunk transpose
+      const int t = j - sums_off, kk = t / d, l = t % d;
+      src = sums_off + kk * d + (l % VEC) * nchunks + l / VEC;
+    }
     double acc = 0.0;
-    for (int c = 0; c < copies; ++c) acc += sm[c * S + j];
+    for (int c = 0; c < copies; ++c) acc += sm[c * S + src];
     partials[static_cast<int64_t>(blockIdx.x) * S + j] = acc;
   }
 }
 
-__global__ void fold_partials_kernel(const double* __restrict__ partials, int nblocks, int64_t S,
-                                     double* __restrict__ stats) {
-  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= S) return;
+// Sum of block partials per element: 8 fixed strided chains + fixed tree.
+__global__ void __launch_bounds__(256) fold_partials_kernel(const double* __restrict__ partials,
+                                                            int nblocks, int64_t S,
+                                                            double* __restrict__ stats) {
+  __shared__ double sm[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * 32 + tx;
   double acc = 0.0;
-  for (int b = 0; b < nblocks; ++b) acc += partials[b * S + j];
-  stats[j] = acc;
+  if (j < S)
+    for (int b = ty; b < nblocks; b += 8) acc += partials[b * S + j];
+  sm[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0 && j < S) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += sm[w][tx];
+    stats[j] = t;
+  }
 }
 
 // ---------------------------------------------------------------- path 2 ----
@@ -398,7 +431,7 @@ void aggregate(fsil_context* c) {
       launch_private<true>(c, vec, cpl_t, grid, warps * 32, lpr, smem, c->partials.as<double>(), checks);
     else
       launch_private<false>(c, vec, cpl_t, grid, warps * 32, lpr, smem, c->partials.as<double>(), checks);
-    fold_partials_kernel<<<static_cast<unsigned>((S + 255) / 256), 256, 0, c->stream>>>(
+    fold_partials_kernel<<<static_cast<unsigned>((S + 31) / 32), 256, 0, c->stream>>>(
         c->partials.as<double>(), grid, S, stats);
     FSIL_LAUNCHED(c);
     return;

@@ -45,7 +45,7 @@ void check_shape(int64_t n_global, int64_t d) {
   if (d < 1) fail(FSIL_ERR_VALIDATION, "dataset needs at least 1 feature dimension");
 }
 
-void begin(fsil_context* c, int metric, const float* dX, const int32_t* dlabels, int64_t n_local,
+void setup(fsil_context* c, int metric, const float* dX, const int32_t* dlabels, int64_t n_local,
            int32_t d, int64_t row_offset, int64_t n_global) {
   check_metric(metric);
   check_shape(n_global, d);
@@ -65,6 +65,11 @@ void begin(fsil_context* c, int metric, const float* dX, const int32_t* dlabels,
   c->launches = 0;
   c->stats = fsil_stats{};
   record(c, 0);
+}
+
+void begin(fsil_context* c, int metric, const float* dX, const int32_t* dlabels, int64_t n_local,
+           int32_t d, int64_t row_offset, int64_t n_global) {
+  setup(c, metric, dX, dlabels, n_local, d, row_offset, n_global);
   densify_collect(c);
   c->phase = 1;
 }
@@ -233,15 +238,17 @@ std::vector<std::pair<int64_t, int32_t>> fetch_dictionary(fsil_context* c) {
 double run_device(fsil_context* c, int metric, const float* dX, const int32_t* dlabels, int64_t n,
                   int32_t d, double* ds, int32_t* dnb, int32_t* down, double* da, double* db,
                   int32_t* k_out, int32_t* dense_to_raw) {
-  begin(c, metric, dX, dlabels, n, d, 0, n);
-  auto dict = fetch_dictionary(c);
-  const std::vector<int32_t> raw = order_dictionary(dict);
-  set_dictionary(c, raw.data(), static_cast<int32_t>(raw.size()));
+  setup(c, metric, dX, dlabels, n, d, 0, n);
+  densify_local(c);  // dictionary ordered on the device; one host sync for K
+  record(c, 1);
+  c->phase = 2;
   do_aggregate(c);
   do_score(c, ds, dnb, down, da, db);
+  if (dense_to_raw && c->k > 0)
+    FSIL_CUDA(cudaMemcpyAsync(dense_to_raw, c->dict_sorted_labels, c->k * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, c->stream));
   const double mean = finish(c, nullptr);
   if (k_out) *k_out = c->k;
-  if (dense_to_raw) std::copy(raw.begin(), raw.end(), dense_to_raw);
   return mean;
 }
 
@@ -314,7 +321,7 @@ void fsil_destroy(fsil_context* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   fsil::DevBuf* bufs[] = {&c->ht_keys, &c->ht_vals, &c->ht_dense, &c->dict_labels, &c->dict_rows,
-                          &c->counters, &c->dense, &c->stats_buf, &c->checks, &c->partials,
+                          &c->counters, &c->dict_sorted, &c->dense, &c->stats_buf, &c->checks, &c->partials,
                           &c->sort_tmp, &c->sort_keys, &c->sort_vals, &c->iota, &c->seg_start,
                           &c->piece_start, &c->mu32, &c->p32, &c->nk, &c->bound, &c->s_tmp,
                           &c->tile_sum, &c->tile_flag, &c->flag_rows, &c->flag_count, &c->result,

@@ -6,6 +6,8 @@
 // (label, min row) into a global open-addressing table; the host orders the
 // (few) distinct labels by first row -- merging across ranks first in the
 // sharded protocol -- and pass 2 maps every row to its dense id.
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
 #include <vector>
 
@@ -88,6 +90,12 @@ __global__ void densify_compact_kernel(const unsigned long long* __restrict__ gk
   out_rows[j] = row_offset + static_cast<int64_t>(gvals[i]);
 }
 
+// Dense id j for the j-th distinct label in first-row order (entries past `count`
+// are padding with first row INT64_MAX).
+__global__ void densify_assign_sorted_kernel(const unsigned long long* __restrict__ gkeys,
+                                             uint32_t cap_mask, const int32_t* __restrict__ raw,
+                                             const unsigned long long* count, int32_t* gdense);
+
 __device__ int64_t find_slot(const unsigned long long* gkeys, uint32_t cap_mask,
                              unsigned long long key) {
   uint32_t h = hash32(static_cast<uint32_t>(key)) & cap_mask;
@@ -122,6 +130,15 @@ __global__ void __launch_bounds__(256) densify_map_kernel(const int32_t* __restr
     if (dj < 0) atomicExch(missing, 1);
     dense[i] = dj;
   }
+}
+
+__global__ void densify_assign_sorted_kernel(const unsigned long long* __restrict__ gkeys,
+                                             uint32_t cap_mask, const int32_t* __restrict__ raw,
+                                             const unsigned long long* count, int32_t* gdense) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= static_cast<int64_t>(*count)) return;
+  const int64_t slot = find_slot(gkeys, cap_mask, label_key(raw[j]));
+  if (slot >= 0) gdense[slot] = static_cast<int32_t>(j);
 }
 
 int grid_for(int64_t n, int threads, int num_sms, int per_sm) {
@@ -170,6 +187,76 @@ void densify_collect(fsil_context* c) {
     FSIL_CUDA(cudaStreamSynchronize(c->stream));
     c->n_distinct = static_cast<int64_t>(h_count);
     if (c->n_distinct * 2 > cap) c->ht_cap = cap * 2;  // keep probes short next call
+    return;
+  }
+}
+
+// Single-GPU densify with one host sync: collect -> compact -> device sort of the
+// dictionary by first row -> dense ids -> per-row map; then read K.
+void densify_local(fsil_context* c) {
+  if (c->n >= (int64_t(1) << 31) - 1)
+    fail(FSIL_ERR_INVALID_ARGUMENT, "too many rows for one device call (2^31-2)");
+  int64_t cap = std::max<int64_t>(c->ht_cap, 8192);
+  c->counters.ensure(64);
+  for (;;) {
+    c->ht_keys.ensure(cap * sizeof(unsigned long long));
+    c->ht_vals.ensure(cap * sizeof(uint32_t));
+    c->ht_dense.ensure(cap * sizeof(int32_t));
+    c->dict_labels.ensure(cap * sizeof(int32_t));
+    c->dict_rows.ensure(cap * sizeof(int64_t));
+    c->dict_sorted.ensure(cap * (sizeof(int32_t) + sizeof(int64_t)));
+    c->dense.ensure(std::max<int64_t>(c->n, 1) * sizeof(int32_t));
+    FSIL_CUDA(cudaMemsetAsync(c->ht_keys.p, 0, cap * sizeof(unsigned long long), c->stream));
+    FSIL_CUDA(cudaMemsetAsync(c->ht_vals.p, 0xff, cap * sizeof(uint32_t), c->stream));
+    FSIL_CUDA(cudaMemsetAsync(c->ht_dense.p, 0xff, cap * sizeof(int32_t), c->stream));
+    FSIL_CUDA(cudaMemsetAsync(c->dict_rows.p, 0x7f, cap * sizeof(int64_t), c->stream));
+    FSIL_CUDA(cudaMemsetAsync(c->counters.p, 0, 64, c->stream));
+    int* overflow = c->counters.as<int>();
+    int* missing = c->counters.as<int>() + 4;
+    unsigned long long* count = reinterpret_cast<unsigned long long*>(c->counters.as<char>() + 8);
+    const uint32_t mask = static_cast<uint32_t>(cap - 1);
+    densify_collect_kernel<<<grid_for(c->n, 256, c->num_sms, 4), 256, 0, c->stream>>>(
+        c->labels, c->n, c->ht_keys.as<unsigned long long>(), c->ht_vals.as<uint32_t>(), mask,
+        overflow);
+    FSIL_LAUNCHED(c);
+    densify_compact_kernel<<<static_cast<unsigned>((cap + 255) / 256), 256, 0, c->stream>>>(
+        c->ht_keys.as<unsigned long long>(), c->ht_vals.as<uint32_t>(), static_cast<uint32_t>(cap),
+        0, c->dict_labels.as<int32_t>(), c->dict_rows.as<int64_t>(), count);
+    FSIL_LAUNCHED(c);
+    int64_t* sorted_rows = reinterpret_cast<int64_t*>(c->dict_sorted.p);
+    int32_t* sorted_labels = reinterpret_cast<int32_t*>(sorted_rows + cap);
+    int bits = 1;
+    while ((int64_t(1) << bits) < c->n + 1 && bits < 63) ++bits;
+    size_t tmp = 0;
+    FSIL_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, c->dict_rows.as<int64_t>(), sorted_rows,
+                                              c->dict_labels.as<int32_t>(), sorted_labels,
+                                              static_cast<int>(cap), 0, 64, c->stream));
+    c->sort_tmp.ensure(tmp);
+    FSIL_CUDA(cub::DeviceRadixSort::SortPairs(c->sort_tmp.p, tmp, c->dict_rows.as<int64_t>(), sorted_rows,
+                                              c->dict_labels.as<int32_t>(), sorted_labels,
+                                              static_cast<int>(cap), 0, 64, c->stream));
+    c->launches += 4;
+    densify_assign_sorted_kernel<<<static_cast<unsigned>((cap + 255) / 256), 256, 0, c->stream>>>(
+        c->ht_keys.as<unsigned long long>(), mask, sorted_labels, count, c->ht_dense.as<int32_t>());
+    FSIL_LAUNCHED(c);
+    densify_map_kernel<<<grid_for(c->n, 256, c->num_sms, 8), 256, 0, c->stream>>>(
+        c->labels, c->n, c->ht_keys.as<unsigned long long>(), c->ht_dense.as<int32_t>(), mask,
+        c->dense.as<int32_t>(), missing);
+    FSIL_LAUNCHED(c);
+    struct {
+      int overflow, pad;
+      unsigned long long count;
+    } h{};
+    FSIL_CUDA(cudaMemcpyAsync(&h, c->counters.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    FSIL_CUDA(cudaStreamSynchronize(c->stream));
+    if (h.overflow) {
+      cap *= 4;
+      continue;
+    }
+    c->ht_cap = static_cast<int64_t>(h.count) * 2 > cap ? cap * 2 : cap;
+    c->n_distinct = static_cast<int64_t>(h.count);
+    c->k = static_cast<int32_t>(h.count);
+    c->dict_sorted_labels = sorted_labels;
     return;
   }
 }

@@ -76,26 +76,29 @@ __global__ void __launch_bounds__(256) refine_kernel(ScoreParams p) {
   }
 }
 
-// Group partials: one thread per tile, fixed-order tree per block.
+// Group partials: a block covers 256 tiles; tiles that held refined rows are
+// re-summed from s[] by a whole warp (fixed lane order + xor tree); then a
+// fixed-order tree over the 256 tile values.
 __global__ void __launch_bounds__(256) tile_group_kernel(const double* __restrict__ tile_sum,
                                                          const int32_t* __restrict__ tile_flag,
                                                          const double* __restrict__ s,
                                                          int64_t ntiles, int tile_rows, int64_t n,
                                                          double* group_sum) {
   __shared__ double sm[256];
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
-  double v = 0.0;
-  if (t < ntiles) {
-    if (tile_flag[t]) {
-      const int64_t r0 = t * tile_rows, r1 = min(n, r0 + tile_rows);
-      double acc = 0.0;
-      for (int64_t r = r0; r < r1; ++r) acc += s[r];
-      v = acc;
-    } else {
-      v = tile_sum[t];
-    }
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * 256;
+  const int64_t t = t0 + threadIdx.x;
+  sm[threadIdx.x] = (t < ntiles && !tile_flag[t]) ? tile_sum[t] : 0.0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < 256; j += 8) {
+    const int64_t tt = t0 + j;
+    if (tt >= ntiles || !tile_flag[tt]) continue;
+    const int64_t r0 = tt * tile_rows, r1 = min(n, r0 + tile_rows);
+    double acc = 0.0;
+    for (int64_t r = r0 + lane; r < r1; r += 32) acc += s[r];
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) sm[j] = acc;
   }
-  sm[threadIdx.x] = v;
   __syncthreads();
   for (int stride = 128; stride > 0; stride >>= 1) {
     if (threadIdx.x < stride) sm[threadIdx.x] += sm[threadIdx.x + stride];

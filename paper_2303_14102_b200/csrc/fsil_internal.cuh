@@ -110,7 +110,8 @@ struct fsil_context {
   int phase = 0;  // 0 idle, 1 begun, 2 dictionary set, 3 aggregated, 4 scored
 
   // scratch (grow-only)
-  fsil::DevBuf ht_keys, ht_vals, ht_dense, dict_labels, dict_rows, counters;
+  fsil::DevBuf ht_keys, ht_vals, ht_dense, dict_labels, dict_rows, dict_sorted, counters;
+  const int32_t* dict_sorted_labels = nullptr;  // device: raw labels in dense order (single GPU)
   fsil::DevBuf dense;          // [n] int32 dense labels
   fsil::DevBuf stats_buf;      // fp64 stats (all-reduce payload)
   fsil::DevBuf checks;         // int64[2] validation word
@@ -133,6 +134,7 @@ namespace fsil {
 
 // kernels.cu entry points (host launchers), all async on ctx->stream
 void densify_collect(fsil_context* c);     // fills ctx->n_distinct (syncs)
+void densify_local(fsil_context* c);       // single GPU: dense ids + K, one sync
 void densify_assign_and_map(fsil_context* c, const int32_t* raw_in_dense_order, int32_t k);
 void aggregate(fsil_context* c);           // stats_buf + checks
 void derive(fsil_context* c);              // mu32, p32, nk, bound

@@ -18,6 +18,7 @@ struct ScoreParams {
   int64_t n;
   int d, dp, k;
   int xstride;            // floats per staged row in shared memory
+  int nstage;             // x tile buffers per CTA (1 or 2)
   const float* mu32;      // [kpad][dp]
   const float* p32;       // [kpad]
   const double* stats;    // fp64 all-reduced stats (StatsLayout)

@@ -66,15 +66,30 @@ __device__ __forceinline__ void load_tile(const ScoreParams& p, float* xs, int64
 template <int KB, bool COS, int VEC, bool MULTI>
 __global__ void __launch_bounds__(kThreads) score_ffma_kernel(ScoreParams p, int64_t ntiles) {
   extern __shared__ __align__(16) float smem[];
-  float* mus = smem;                                 // [KB][dp]   (single-group case)
-  float* pks = mus + (MULTI ? 0 : KB * p.dp);        // [KB]
-  float* xbuf = pks + (MULTI ? 0 : KB);              // [2][kTileRows][xstride]
+  // single-group case: Yt2[dp/2][KB] pairs {Y[k][l], Y[k][l+1]} (fp64) so that the
+  // per-lane own/neighbour gathers of the fp64 epilogue all hit one smem row
+  double2* yt2 = reinterpret_cast<double2*>(smem);
+  float* mus = smem + (MULTI ? 0 : KB * p.dp * 2);      // [KB][dp]
+  float* pks = mus + (MULTI ? 0 : KB * p.dp);           // [KB]
+  float* xbuf = pks + (MULTI ? 0 : KB);                 // [nstage][kTileRows][xstride]
   __shared__ double wsum[kThreads / 32];
   const int tid = threadIdx.x;
+  const int nstage = p.nstage;
 
   if constexpr (!MULTI) {
     for (int j = tid; j < KB * p.dp; j += kThreads) mus[j] = p.mu32[j];
     for (int j = tid; j < KB; j += kThreads) pks[j] = COS ? 0.f : p.p32[j];
+    const double* sums = p.stats + (COS ? p.k : 2 * p.k);
+    for (int j = tid; j < KB * (p.dp / 2); j += kThreads) {
+      const int k = j % KB, l2 = j / KB;
+      double2 v = make_double2(0.0, 0.0);
+      if (k < p.k) {
+        const int l = 2 * l2;
+        if (l < p.d) v.x = sums[static_cast<int64_t>(k) * p.d + l];
+        if (l + 1 < p.d) v.y = sums[static_cast<int64_t>(k) * p.d + l + 1];
+      }
+      yt2[j] = v;
+    }
   }
 
   const float bmu = p.bound[0], bp = p.bound[1];
@@ -88,7 +103,7 @@ __global__ void __launch_bounds__(kThreads) score_ffma_kernel(ScoreParams p, int
   for (; tile < ntiles; tile += gridDim.x) {
     const int64_t next = tile + gridDim.x;
     float* xs = xbuf + buf * kTileRows * p.xstride;
-    if (next < ntiles) {
+    if (nstage == 2 && next < ntiles) {
       load_tile<VEC>(p, xbuf + (buf ^ 1) * kTileRows * p.xstride, next);
       cp_async_wait<1>();
     } else {
@@ -173,28 +188,82 @@ __global__ void __launch_bounds__(kThreads) score_ffma_kernel(ScoreParams p, int
     }
 
     // ---------------- epilogue ----------------
+    int nbr[kRowsPerThread];
+    bool flg[kRowsPerThread];
+#pragma unroll
+    for (int r = 0; r < kRowsPerThread; ++r) {
+      const float eps = COS ? 1.01f * gam * (2.0f * bmu + 2.0f)
+                            : 1.01f * gam * (xi[r] + bp + 4.0f * sqrtf(xi[r]) * bmu);
+      flg[r] = !((best2[r] - best1[r]) > 2.0f * eps);
+      nbr[r] = arg[r];
+      if (nbr[r] < 0) {  // non-finite fast pass (overflowing features): provisional pick
+        nbr[r] = own[r] == 0 ? 1 : 0;
+        flg[r] = true;
+      }
+      if (own[r] < 0) {  // row past n: harmless in-range indices
+        own[r] = 0;
+        nbr[r] = 1;
+      }
+    }
+    // fp64 a_i, b_i with the reference formulas: own and neighbour dots (+ ||x||^2)
+    double ss[kRowsPerThread], co[kRowsPerThread], cb[kRowsPerThread];
+#pragma unroll
+    for (int r = 0; r < kRowsPerThread; ++r) ss[r] = co[r] = cb[r] = 0.0;
+    if constexpr (!MULTI) {
+#pragma unroll 2
+      for (int c = 0; c < nc; ++c) {
+#pragma unroll
+        for (int r = 0; r < kRowsPerThread; ++r) {
+          const float4 xv = *reinterpret_cast<const float4*>(xr[r] + 4 * c);
+          const double2 yo0 = yt2[(2 * c) * KB + own[r]], yo1 = yt2[(2 * c + 1) * KB + own[r]];
+          const double2 yb0 = yt2[(2 * c) * KB + nbr[r]], yb1 = yt2[(2 * c + 1) * KB + nbr[r]];
+          const double x0 = xv.x, x1 = xv.y, x2 = xv.z, x3 = xv.w;
+          ss[r] = fma(x0, x0, ss[r]); ss[r] = fma(x1, x1, ss[r]);
+          ss[r] = fma(x2, x2, ss[r]); ss[r] = fma(x3, x3, ss[r]);
+          co[r] = fma(yo0.x, x0, co[r]); co[r] = fma(yo0.y, x1, co[r]);
+          co[r] = fma(yo1.x, x2, co[r]); co[r] = fma(yo1.y, x3, co[r]);
+          cb[r] = fma(yb0.x, x0, cb[r]); cb[r] = fma(yb0.y, x1, cb[r]);
+          cb[r] = fma(yb1.x, x2, cb[r]); cb[r] = fma(yb1.y, x3, cb[r]);
+        }
+      }
+    } else {
+      const double* sums = p.stats + (COS ? p.k : 2 * p.k);
+#pragma unroll
+      for (int r = 0; r < kRowsPerThread; ++r) {
+        const double* yo = sums + static_cast<int64_t>(own[r]) * p.d;
+        const double* yb = sums + static_cast<int64_t>(nbr[r]) * p.d;
+        for (int l = 0; l < p.d; ++l) {
+          const double v = xr[r][l];
+          ss[r] = fma(v, v, ss[r]);
+          co[r] = fma(__ldg(yo + l), v, co[r]);
+          cb[r] = fma(__ldg(yb + l), v, cb[r]);
+        }
+      }
+    }
     double s_thread = 0.0;
     bool any_flag = false;
 #pragma unroll
     for (int r = 0; r < kRowsPerThread; ++r) {
       const int64_t row = tile * kTileRows + tid + r * kThreads;
       if (row >= p.n) continue;
-      const float eps = COS ? 1.01f * gam * (2.0f * bmu + 2.0f)
-                            : 1.01f * gam * (xi[r] + bp + 4.0f * sqrtf(xi[r]) * bmu);
-      bool flagged = !((best2[r] - best1[r]) > 2.0f * eps);
-      int nb = arg[r];
-      if (nb < 0) {  // non-finite fast pass (overflowing features): provisional pick
-        nb = own[r] == 0 ? 1 : 0;
-        flagged = true;
+      const double n_o = p.nk[own[r]], n_b = p.nk[nbr[r]];
+      const bool singleton = n_o == 1.0;
+      double a, b;
+      if (COS) {
+        const double nrm = sqrt(ss[r]);
+        b = cos_foreign(n_b, cb[r] / nrm);
+        a = singleton ? 0.0 : cos_own(n_o, co[r] / nrm);
+      } else {
+        b = sq_foreign(ss[r], p.stats[p.k + nbr[r]], n_b, cb[r]);
+        a = singleton ? 0.0 : sq_own(ss[r], p.stats[p.k + own[r]], n_o, co[r]);
       }
-      double a, b, s;
-      exact_row<COS>(xr[r], p.d, own[r], nb, p.stats, p.nk, p.k, a, b, s);
+      const double s = singleton ? 0.0 : assemble_score(a, b);
       p.s[row] = s;
-      if (p.nb) p.nb[row] = nb;
+      if (p.nb) p.nb[row] = nbr[r];
       if (p.own) p.own[row] = own[r];
       if (p.a) p.a[row] = a;
       if (p.b) p.b[row] = b;
-      if (flagged) {
+      if (flg[r]) {
         const unsigned long long idx = atomicAdd(p.flag_count, 1ull);
         p.flag_rows[idx] = static_cast<int32_t>(row);
         any_flag = true;
@@ -213,7 +282,8 @@ __global__ void __launch_bounds__(kThreads) score_ffma_kernel(ScoreParams p, int
       p.tile_flag[tile] = tile_flagged;
     }
     __syncthreads();  // xs and wsum are reused next iteration
-    buf ^= 1;
+    if (nstage == 2) buf ^= 1;
+    else if (next < ntiles) load_tile<VEC>(p, xbuf, next);
   }
 }
 
@@ -242,16 +312,23 @@ void* pick_kernel(int kb) {
 
 int64_t ffma_tiles(int64_t n) { return (n + kTileRows - 1) / kTileRows; }
 
-static size_t ffma_smem(const fsil_context* c, int* xstride_out) {
+static size_t ffma_smem(const fsil_context* c, int* xstride_out, int nstage) {
   const int kb = c->k <= 32 ? std::max(4, ((c->k + 3) / 4) * 4) : -1;
   const int q = static_cast<int>(c->dp / 4);
   const int xstride = static_cast<int>(c->dp) + ((q % 2 == 0) ? 4 : 8);
   if (xstride_out) *xstride_out = xstride;
-  const size_t mu_floats = kb > 0 ? static_cast<size_t>(kb) * c->dp + kb : 0;
-  return (mu_floats + 2ull * kTileRows * xstride) * sizeof(float);
+  const size_t mu_floats = kb > 0 ? static_cast<size_t>(kb) * c->dp * 3 + kb : 0;
+  return (mu_floats + static_cast<size_t>(nstage) * kTileRows * xstride) * sizeof(float);
 }
 
-bool ffma_supported(const fsil_context* c) { return ffma_smem(c, nullptr) <= c->smem_optin; }
+// Two stages in one CTA when two such CTAs still fit per SM, else single-stage
+// CTAs (overlap then comes from the co-resident CTAs).
+static int ffma_stages(const fsil_context* c) {
+  const size_t sm_bytes = 228 * 1024;
+  return ffma_smem(c, nullptr, 2) * 2 + 2048 <= sm_bytes ? 2 : 1;
+}
+
+bool ffma_supported(const fsil_context* c) { return ffma_smem(c, nullptr, 1) <= c->smem_optin; }
 
 void score_ffma(fsil_context* c, const ScoreParams& base) {
   const bool cos = c->metric == FSIL_COSINE;
@@ -262,7 +339,8 @@ void score_ffma(fsil_context* c, const ScoreParams& base) {
   const int kb = c->k <= 32 ? std::max(4, ((c->k + 3) / 4) * 4) : -1;
   ScoreParams p = base;
   // padded row stride: (xstride/4) odd -> conflict-free 128-bit row reads
-  const size_t smem = ffma_smem(c, &p.xstride);
+  p.nstage = ffma_stages(c);
+  const size_t smem = ffma_smem(c, &p.xstride, p.nstage);
   void* fn = cos ? (vec == 4 ? pick_kernel<true, 4>(kb) : pick_kernel<true, 1>(kb))
                  : (vec == 4 ? pick_kernel<false, 4>(kb) : pick_kernel<false, 1>(kb));
   if (smem > c->smem_optin)

@@ -1,0 +1,274 @@
+"""GPU parity: libfsil (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Bar (BASELINE.json north_star): identical neighbour cluster
+(dense id, reference tie rule), |ds_i| <= 1e-5, |dS| <= 1e-6; a_i / b_i within
+1e-5 relative.  Runs on a B200 under gpurun (`pytest -m gpu`)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+S_TOL, MEAN_TOL = 1e-5, 1e-6
+PATHS = {"auto": 0, "ffma": 1, "tcgen05": 2, "fp64": 3}
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2303_14102_b200 import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def reference_noise_ties(X, ref, metric, rows, alt):
+    raw = np.asarray(ref.dense_to_raw)[ref.own]  # same first-appearance order as ref
+    counts, sums, psi = oracle.aggregate(X, raw, metric)
+    x = X[rows].astype(np.float64)
+    out = []
+    for i, r in enumerate(rows):
+        vals, scales = [], []
+        for k in (ref.neighbour[r], alt[i]):
+            n = float(counts[k])
+            cross = float(sums[k] @ x[i])
+            if metric == "cosine":
+                nrm = np.sqrt(x[i] @ x[i])
+                vals.append(min(max(1.0 - cross / nrm / n, 0.0), 2.0))
+                scales.append(1.0 + abs(cross / nrm / n))
+            else:
+                xi = float(x[i] @ x[i])
+                vals.append(max(0.0, xi + psi[k] / n - 2.0 * cross / n))
+                scales.append(xi + psi[k] / n + 2.0 * abs(cross) / n)
+        out.append(abs(vals[0] - vals[1]) <= 1e-12 * max(scales))
+    return np.array(out)
+
+
+def check(ctx, X, L, metric, path="auto", label=""):
+    ctx.set_path(PATHS[path])
+    got = ctx.silhouette(X, L, metric)
+    ref = oracle.silhouette(X, L, metric)
+    tag = f"{label} {metric} path={path} n={X.shape[0]} d={X.shape[1]}"
+    assert got.cluster_names == ref.dense_to_raw.tolist(), tag
+    assert np.array_equal(got.own, ref.own), tag
+    mism = np.flatnonzero(got.neighbour != ref.neighbour)
+    if mism.size:
+        # Only rows whose two candidates tie within the fp64 rounding noise of the
+        # reference formula itself (terms of size xi + Psi/n + 2|cross|/n) may
+        # differ: there the reference's own choice depends on its summation order.
+        ties = reference_noise_ties(X, ref, metric, mism, got.neighbour[mism])
+        assert ties.all(), (f"{tag}: {int((~ties).sum())} certain-neighbour mismatches, "
+                            f"rows {mism[~ties][:5]}")
+        assert mism.size <= max(2, X.shape[0] // 20), tag
+    assert np.abs(got.s - ref.s).max() <= S_TOL, tag
+    assert abs(got.mean - ref.mean) <= MEAN_TOL, tag
+    for g, r in ((got.a, ref.a), (got.b, ref.b)):
+        assert np.all(np.abs(g - r) <= 1e-5 * np.maximum(1.0, np.abs(r))), tag
+    ctx.set_path(0)
+    return got, ref
+
+
+def test_spec_goldens(ctx):
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+    sq = g["spec_square"]
+    got = ctx.silhouette(np.array(sq["X"], np.float32), [1, 1, 2, 2], "sqeuclid")
+    assert np.allclose(got.s, sq["s"], atol=1e-15) and abs(got.mean - 31 / 33) < 1e-15
+    assert np.allclose(got.a, 1.0) and np.allclose(got.b, 16.5)
+    cs = g["spec_cosine"]
+    got = ctx.silhouette(np.array(cs["X"], np.float32), [0, 0, 1, 1], "cosine")
+    assert np.allclose(got.s, 1.0) and got.mean == 1.0
+
+
+def test_sklearn_goldens(ctx):
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+    for case in g["sklearn_cases"]:
+        got = ctx.silhouette(np.array(case["X"], np.float32), case["labels"], case["metric"])
+        assert np.abs(got.s - np.array(case["s"])).max() <= 1e-9
+        assert abs(got.mean - case["mean"]) <= 1e-12
+
+
+SHAPES = [(500, 5, 6), (1000, 16, 8), (3000, 64, 20), (777, 3, 3), (2000, 33, 40), (5000, 128, 100),
+          (2500, 7, 32), (4000, 1, 5), (3000, 100, 2), (1500, 200, 300)]
+
+
+@pytest.mark.parametrize("n,d,k", SHAPES)
+@pytest.mark.parametrize("metric", ["sqeuclid", "cosine"])
+def test_random_shapes(ctx, n, d, k, metric):
+    rng = np.random.default_rng(n * 31 + d * 7 + k)
+    X = (rng.normal(size=(n, d)) + rng.normal(size=(1, d)) * 3).astype(np.float32)
+    L = rng.integers(0, k, n) * 7 - 3
+    check(ctx, X, L, metric)
+
+
+@pytest.mark.parametrize("path", ["ffma", "fp64"])
+@pytest.mark.parametrize("metric", ["sqeuclid", "cosine"])
+def test_paths_agree(ctx, path, metric):
+    rng = np.random.default_rng(5)
+    X = rng.normal(size=(4096, 48)).astype(np.float32)
+    L = rng.integers(0, 24, 4096)
+    check(ctx, X, L, metric, path)
+
+
+def test_edge_singleton_and_pairs(ctx):
+    rng = np.random.default_rng(11)
+    X = rng.normal(size=(600, 8)).astype(np.float32)
+    L = rng.integers(0, 5, 600)
+    L[17] = 50          # singleton: a = 0, s = 0, b and neighbour still reported
+    L[[3, 400]] = 60    # size-2 cluster
+    for metric in ("sqeuclid", "cosine"):
+        got, ref = check(ctx, X, L, metric)
+        assert got.s[17] == 0.0 and got.a[17] == 0.0 and got.b[17] > 0
+
+
+def test_edge_duplicates_across_clusters(ctx):
+    # coincident points in two clusters: a = b = 0 -> s = 0 (report.cpp:12)
+    X = np.array([[1, 2], [1, 2], [1, 2], [1, 2], [5, 5], [5, 6]], np.float32)
+    L = [0, 0, 1, 1, 2, 2]
+    got, _ = check(ctx, X, L, "sqeuclid")
+    assert np.all(got.s[:4] == 0.0)
+
+
+def test_edge_exact_tie_lowest_dense_id(ctx):
+    # two identical foreign clusters: neighbour = lowest dense id (strict <)
+    base = np.array([[0, 0], [0.1, 0], [0, 0.1]], np.float32)
+    far = base + np.float32(10)
+    X = np.concatenate([far, base, far])   # raw labels 9 (far), 4 (base), 7 (far copy)
+    L = [9, 9, 9, 4, 4, 4, 7, 7, 7]
+    for metric in ("sqeuclid", "cosine"):
+        got, ref = check(ctx, X + np.float32(1), L, metric)
+        assert got.neighbour[3] == 0  # dense id of raw 9, not 7
+
+
+def test_edge_first_appearance_not_numeric(ctx):
+    rng = np.random.default_rng(3)
+    X = rng.normal(size=(300, 4)).astype(np.float32)
+    L = rng.choice([2**31 - 1, -2**31, 0, 17, -5], size=300)
+    got, ref = check(ctx, X, L, "sqeuclid")
+    assert got.cluster_names[0] == int(L[0])
+
+
+def test_edge_k2_and_many_labels(ctx):
+    rng = np.random.default_rng(4)
+    X = rng.normal(size=(3000, 6)).astype(np.float32)
+    check(ctx, X, rng.integers(0, 2, 3000), "sqeuclid")
+    # K close to N: hash-table growth path, mostly singletons
+    L = rng.integers(0, 2500, 3000) * 9973
+    check(ctx, X, L, "cosine")
+
+
+def test_edge_negative_cancellation_clamp(ctx):
+    # A cluster of identical points far from the origin: its own-cluster mean is
+    # exactly 0 in real arithmetic, and the reference formula's cancellation
+    # (n*xi + Psi - 2*cross) can round to a tiny negative that max(0, .) clamps
+    # (squared_euclidean.cpp:77,81).  Other clusters keep the fp64 noise small
+    # relative to their distances, so the comparison stays meaningful.
+    rng = np.random.default_rng(8)
+    X = (np.float32(40) + rng.normal(size=(2000, 12)) * 2).astype(np.float32)
+    L = rng.integers(0, 4, 2000)
+    X[L == 2] = X[np.flatnonzero(L == 2)[0]]
+    for metric in ("sqeuclid", "cosine"):
+        got, ref = check(ctx, X, L, metric)
+        assert np.all(got.a >= 0) and np.all(got.b >= 0)
+        xi = (X[L == 2][0].astype(np.float64) ** 2).sum()
+        assert np.all(got.a[L == 2] <= 1e-12 * xi)
+
+
+def test_validation_errors_match_reference(ctx):
+    from paper_2303_14102_b200 import ValidationError
+    X = np.array([[0, 1], [1, np.nan], [2, 2], [3, 3]], np.float32)
+    with pytest.raises(ValidationError, match="non-finite feature value at point 1, dimension 1"):
+        ctx.silhouette(X, [0, 1, 1, 0], "sqeuclid")
+    X = np.array([[0, 1], [0, 0], [2, 2], [3, 3]], np.float32)
+    with pytest.raises(ValidationError, match=r"cosine distance undefined for zero vector \(point 1\)"):
+        ctx.silhouette(X, [0, 1, 1, 0], "cosine")
+    with pytest.raises(ValidationError, match="need K >= 2, got K = 1"):
+        ctx.silhouette(X + 1, [3, 3, 3, 3], "sqeuclid")
+    with pytest.raises(ValidationError, match="at least 2 points"):
+        ctx.silhouette(np.ones((1, 3), np.float32), [0], "sqeuclid")
+    with pytest.raises(ValidationError, match="no fast engine for plain euclidean"):
+        ctx.silhouette(X + 1, [0, 1, 1, 0], "euclid")
+    # NaN takes precedence over K < 2 (dataset.cpp:35 before :53)
+    Xn = np.array([[0, 1], [np.inf, 1]], np.float32)
+    with pytest.raises(ValidationError, match="non-finite"):
+        ctx.silhouette(Xn, [1, 1], "sqeuclid")
+    # the context stays usable after errors
+    check(ctx, np.random.default_rng(0).normal(size=(100, 3)).astype(np.float32),
+          np.arange(100) % 3, "sqeuclid")
+
+
+def test_determinism(ctx):
+    rng = np.random.default_rng(9)
+    X = rng.normal(size=(50000, 24)).astype(np.float32)
+    L = rng.integers(0, 12, 50000)
+    r1 = ctx.silhouette(X, L, "cosine")
+    r2 = ctx.silhouette(X, L, "cosine")
+    assert np.array_equal(r1.s, r2.s) and r1.mean == r2.mean and np.array_equal(r1.neighbour, r2.neighbour)
+
+
+def _config(ctx, name, n=None):
+    from paper_2303_14102_b200 import datagen
+    X, L, metric = datagen.generate_host(name, n=n)
+    return X, L, metric
+
+
+def test_c1_full_and_naive_rows(ctx):
+    X, L, metric = _config(ctx, "C1")
+    got, ref = check(ctx, X, L, metric, label="C1")
+    # naive O(N^2 D) definition (naive.cpp:30-71) on sampled rows, all N points
+    rows = np.random.default_rng(1).choice(X.shape[0], 64, replace=False)
+    X64 = X.astype(np.float64)
+    sizes = np.bincount(got.own)
+    for i in rows:
+        dist = ((X64 - X64[i]) ** 2).sum(1)
+        sums = np.bincount(got.own, dist, minlength=sizes.shape[0])
+        own = got.own[i]
+        a = sums[own] / (sizes[own] - 1)
+        means = sums / sizes
+        means[own] = np.inf
+        nb = int(np.argmin(means))
+        b = means[nb]
+        s = 1 - a / b if a <= b else b / a - 1
+        assert nb == got.neighbour[i] and abs(s - got.s[i]) <= 1e-9
+
+
+def test_c2_full(ctx):
+    X, L, metric = _config(ctx, "C2")
+    check(ctx, X, L, metric, label="C2")
+
+
+@pytest.mark.parametrize("name,n", [("C3", 400_000), ("C4", 400_000), ("C5", 20_000)])
+def test_scaled_configs_full_oracle(ctx, name, n):
+    X, L, metric = _config(ctx, name, n)
+    check(ctx, X, L, metric, label=name)
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_full_size_sampled_rows(ctx, name):
+    """BASELINE.json full sizes: the oracle aggregates all N rows (fp64, dense
+    labels), then scores a sample of rows exactly; s_i depends only on (x_i, label_i,
+    global stats).  Size-independent properties checked on every row."""
+    import torch
+    from paper_2303_14102_b200 import datagen
+    Xd, Ld, metric = datagen.generate_device(name)
+    n, d = Xd.shape
+    s = torch.empty(n, dtype=torch.float64, device="cuda")
+    nb = torch.empty(n, dtype=torch.int32, device="cuda")
+    own = torch.empty(n, dtype=torch.int32, device="cuda")
+    d2r = np.empty(n if n < 10_000_000 else 10_000_000, np.int32)
+    mean, k = ctx.silhouette_device(Xd, Ld, metric, s=s, neighbour=nb, own=own, dense_to_raw=d2r)
+    s_h, nb_h, own_h = s.cpu().numpy(), nb.cpu().numpy(), own.cpu().numpy()
+    assert np.all(np.abs(s_h) <= 1.0) and abs(s_h.mean() - mean) <= 1e-9
+    assert np.all(nb_h != own_h) and nb_h.min() >= 0 and nb_h.max() < k
+    mean2, _ = ctx.silhouette_device(Xd, Ld, metric, s=s, neighbour=nb)
+    assert mean2 == mean  # bit-identical rerun
+    X, L = Xd.cpu().numpy(), Ld.cpu().numpy()
+    del Xd
+    dense, raw = oracle.first_appearance(L)
+    assert raw.tolist() == d2r[:k].tolist() and np.array_equal(dense, own_h)
+    counts, sums, psi = oracle.aggregate_dense(X, dense, k, metric)
+    rows = np.random.default_rng(2).choice(n, 2000, replace=False)
+    a, b, sv, nbv = oracle.score_rows(X, dense, counts, sums, psi, rows, metric)
+    assert np.array_equal(nbv, nb_h[rows])
+    assert np.abs(sv - s_h[rows]).max() <= S_TOL
