@@ -73,7 +73,8 @@ typedef struct {
   int32_t k;               /* dense clusters */
   int32_t path;            /* fsil_path actually used */
   int32_t agg_path;        /* 1 = warp-private shared-memory, 2 = label-sorted segments */
-  int64_t flagged_rows;    /* rows re-evaluated by the fp64 refinement kernel */
+  int64_t flagged_rows;    /* rows re-evaluated by the fp64 argmin refinement kernel */
+  int64_t exact_rows;      /* rows whose a_i, b_i were recomputed exactly (tcgen05 path) */
   int64_t kernel_launches; /* kernels launched by the last call */
   float ms_densify, ms_aggregate, ms_score, ms_refine, ms_finalize; /* device time, 0 unless timing on */
 } fsil_stats;

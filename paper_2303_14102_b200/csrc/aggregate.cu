@@ -37,8 +37,10 @@ constexpr int kPieceRows = 2048;
 template <bool COS, int VEC, int CPL>
 __global__ void __launch_bounds__(256) agg_private_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ dense, int64_t n, int d,
-    int64_t row_offset, int k, int lpr, double* __restrict__ partials, int64_t* checks) {
+    int64_t row_offset, int k, int lpr, double* __restrict__ partials, int64_t* checks,
+    float* xmax) {
   constexpr int U = 4;
+  float amax = 0.f;
   extern __shared__ double sm[];
   const int S = COS ? k * (d + 1) : k * (d + 2);
   const int sums_off = COS ? k : 2 * k;
@@ -86,6 +88,7 @@ __global__ void __launch_bounds__(256) agg_private_kernel(
           const double x = v[u][c][e];
           ss = fma(x, x, ss);
           finite = finite && isfinite(v[u][c][e]);
+          amax = fmaxf(amax, fabsf(v[u][c][e]));
         }
       if (!finite) {
 #pragma unroll
@@ -124,6 +127,8 @@ __global__ void __launch_bounds__(256) agg_private_kernel(
       }
     }
   }
+  for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  if (lane == 0 && amax > 0.f) atomic_max_nonneg_f32(xmax, amax);
   __syncthreads();
   for (int j = threadIdx.x; j < S; j += blockDim.x) {
     int src = j;
@@ -187,7 +192,7 @@ __global__ void __launch_bounds__(256) agg_piece_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ rows, int64_t n, int d,
     int64_t row_offset, int k, int lpr, const int64_t* __restrict__ seg_begin,
     const int64_t* __restrict__ seg_end, const int64_t* __restrict__ piece_start,
-    double* __restrict__ piece_out, int64_t* checks) {
+    double* __restrict__ piece_out, int64_t* checks, float* xmax) {
   const int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t total = piece_start[k];
@@ -211,6 +216,7 @@ __global__ void __launch_bounds__(256) agg_piece_kernel(
 #pragma unroll
     for (int e = 0; e < VEC; ++e) acc[q][e] = 0.0;
   double psi = 0.0, cnt = 0.0;
+  float amax = 0.f;
   for (int64_t base = b0; base < b1; base += rpw) {
     const int64_t pos = base + sub;  // warp-uniform trip count
     const bool valid = pos < b1;
@@ -236,6 +242,7 @@ __global__ void __launch_bounds__(256) agg_piece_kernel(
         const double x = v[q][e];
         ss += x * x;
         finite = finite && isfinite(v[q][e]);
+        amax = fmaxf(amax, fabsf(v[q][e]));
       }
     if (!finite) {
 #pragma unroll
@@ -276,6 +283,8 @@ __global__ void __launch_bounds__(256) agg_piece_kernel(
   }
   if (!COS)
     for (int off = 16; off > 0; off >>= 1) psi += __shfl_xor_sync(0xffffffffu, psi, off);
+  for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  if (lane == 0 && amax > 0.f) atomic_max_nonneg_f32(xmax, amax);
   const int S1 = COS ? d + 1 : d + 2;
   double* out = piece_out + p * S1;
   if (lane == 0) {
@@ -317,11 +326,15 @@ __global__ void derive_kernel(const double* __restrict__ stats, int k, int d, in
   const double n = cnt > 0.0 ? cnt : 1.0;
   const double* sums = stats + (cos ? k : 2 * k) + static_cast<int64_t>(c) * d;
   double sq = 0.0;
+  float amax = 0.f;
   for (int l = threadIdx.x; l < dp; l += blockDim.x) {
     const double m = l < d ? sums[l] / n : 0.0;
     mu32[static_cast<int64_t>(c) * dp + l] = static_cast<float>(m);
     sq += m * m;
+    amax = fmaxf(amax, __double2float_ru(fabs(m)));
   }
+  for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  if ((threadIdx.x & 31) == 0 && amax > 0.f) atomic_max_nonneg_f32(bound + 2, amax);
   __shared__ double red[32];
   for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
@@ -354,7 +367,8 @@ void launch_private(fsil_context* c, int vec, int cpl, int grid, int threads, in
     auto kern = agg_private_kernel<COS, V, C>;                                                   \
     FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     kern<<<grid, threads, smem, c->stream>>>(c->X, c->dense.as<int32_t>(), c->n, c->d,          \
-                                             c->row_offset, c->k, lpr, partials, checks);        \
+                                             c->row_offset, c->k, lpr, partials, checks,         \
+                                             c->xmax.as<float>());                               \
     FSIL_LAUNCHED(c);                                                                            \
     return;                                                                                      \
   }
@@ -373,7 +387,7 @@ void launch_pieces(fsil_context* c, int vec, int cpl, int64_t max_pieces, int lp
   if (vec == V && cpl == C) {                                                                    \
     agg_piece_kernel<COS, V, C><<<grid, 256, 0, c->stream>>>(                                    \
         c->X, rows, c->n, c->d, c->row_offset, c->k, lpr, seg_begin, seg_end, piece_start,       \
-        piece_out, checks);                                                                      \
+        piece_out, checks, c->xmax.as<float>());                                                 \
     FSIL_LAUNCHED(c);                                                                            \
     return;                                                                                      \
   }
@@ -397,6 +411,8 @@ void aggregate(fsil_context* c) {
   const int64_t none[2] = {kNone, kNone};
   FSIL_CUDA(cudaMemcpyAsync(checks, none, sizeof(none), cudaMemcpyHostToDevice, c->stream));
   FSIL_CUDA(cudaMemsetAsync(stats, 0, S * sizeof(double), c->stream));
+  c->xmax.ensure(sizeof(float));
+  FSIL_CUDA(cudaMemsetAsync(c->xmax.p, 0, sizeof(float), c->stream));
   if (c->n == 0) {
     c->agg_path = 0;
     return;

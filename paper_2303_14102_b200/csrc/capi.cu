@@ -21,6 +21,7 @@ void score_ffma(fsil_context* c, const ScoreParams& p);
 int64_t ffma_tiles(int64_t n);
 bool ffma_supported(const fsil_context* c);
 void flag_all(fsil_context* c, const ScoreParams& p, int tile_rows);
+void exact_ab(fsil_context* c, const ScoreParams& p);
 void refine(fsil_context* c, const ScoreParams& p);
 void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows);
 bool tc_supported(const fsil_context* c);
@@ -156,11 +157,13 @@ void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, 
   p.flag_rows = c->flag_rows.as<int32_t>();
   p.flag_count = c->flag_count.as<unsigned long long>();
   record(c, 3);
+  c->tc_exact_used = false;
   if (use == FSIL_PATH_TCGEN05) score_tc(c, p);
   else if (use == FSIL_PATH_FFMA) score_ffma(c, p);
   else flag_all(c, p, tile_rows);
   c->score_path = use;
   record(c, 4);
+  if (c->tc_exact_used) exact_ab(c, p);
   refine(c, p);
   record(c, 5);
   finalize_sum(c, p, ntiles, tile_rows);
@@ -170,7 +173,7 @@ void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, 
 double finish(fsil_context* c, double* flagged_out) {
   if (c->phase < 4) fail(FSIL_ERR_INVALID_ARGUMENT, "score must come before finish");
   int64_t checks[2] = {kNone, kNone};
-  double res[2] = {0, 0};
+  double res[3] = {0, 0, 0};
   int missing = 0;
   FSIL_CUDA(cudaMemcpyAsync(checks, c->checks.p, sizeof(checks), cudaMemcpyDeviceToHost, c->stream));
   FSIL_CUDA(cudaMemcpyAsync(res, c->result.p, sizeof(res), cudaMemcpyDeviceToHost, c->stream));
@@ -201,6 +204,7 @@ double finish(fsil_context* c, double* flagged_out) {
   c->stats.path = c->score_path;
   c->stats.agg_path = c->agg_path;
   c->stats.flagged_rows = static_cast<int64_t>(res[1]);
+  c->stats.exact_rows = static_cast<int64_t>(res[2]);
   c->stats.kernel_launches = c->launches;
   if (c->timing) {
     float* ms[5] = {&c->stats.ms_densify, &c->stats.ms_aggregate, &c->stats.ms_score,
@@ -325,7 +329,7 @@ void fsil_destroy(fsil_context* c) {
                           &c->sort_tmp, &c->sort_keys, &c->sort_vals, &c->iota, &c->seg_start,
                           &c->piece_start, &c->mu32, &c->p32, &c->nk, &c->bound, &c->s_tmp,
                           &c->tile_sum, &c->tile_flag, &c->flag_rows, &c->flag_count, &c->result,
-                          &c->group_sum, &c->hX, &c->hL, &c->o_s, &c->o_nb, &c->o_own, &c->o_a,
+                          &c->group_sum, &c->xmax, &c->tc_b, &c->exact_rows, &c->exact_count, &c->hX, &c->hL, &c->o_s, &c->o_nb, &c->o_own, &c->o_a,
                           &c->o_b};
   for (auto* b : bufs) b->release();
   for (auto& e : c->ev)

@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(256) tile_group_kernel(const double* __restric
 __global__ void __launch_bounds__(1024) total_kernel(const double* __restrict__ group_sum,
                                                      int64_t ngroups,
                                                      const unsigned long long* flag_count,
+                                                     const unsigned long long* exact_count,
                                                      double* result) {
   __shared__ double sm[1024];
   double acc = 0.0;
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(1024) total_kernel(const double* __restrict__ 
   if (threadIdx.x == 0) {
     result[0] = sm[0];
     result[1] = static_cast<double>(*flag_count);
+    result[2] = exact_count ? static_cast<double>(*exact_count) : 0.0;
   }
 }
 
@@ -138,7 +140,65 @@ __global__ void flag_all_kernel(int64_t n, int tile_rows, int32_t* flag_rows, in
   if (i == 0) *flag_count = static_cast<unsigned long long>(n);
 }
 
+// Exact own/neighbour recompute for rows whose tensor-core a_i/b_i bound was too
+// loose (neighbour already certified): one warp per row, reference formulas.
+template <bool COS>
+__global__ void __launch_bounds__(256) exact_ab_kernel(ScoreParams p, const int2* __restrict__ rows,
+                                                       const unsigned long long* count) {
+  const unsigned long long cnt = *count;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const double* sums = p.stats + (COS ? p.k : 2 * p.k);
+  for (int64_t i = warp; i < static_cast<int64_t>(cnt); i += nwarps) {
+    const int2 rn = rows[i];
+    const int64_t row = rn.x;
+    const int nb = rn.y;
+    const int own = p.dense[row];
+    const float* x = p.X + row * p.d;
+    const double* yo = sums + static_cast<int64_t>(own) * p.d;
+    const double* yb = sums + static_cast<int64_t>(nb) * p.d;
+    double ss = 0.0, co = 0.0, cb = 0.0;
+    for (int l = lane; l < p.d; l += 32) {
+      const double v = x[l];
+      ss = fma(v, v, ss);
+      co = fma(yo[l], v, co);
+      cb = fma(yb[l], v, cb);
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      ss += __shfl_xor_sync(0xffffffffu, ss, off);
+      co += __shfl_xor_sync(0xffffffffu, co, off);
+      cb += __shfl_xor_sync(0xffffffffu, cb, off);
+    }
+    if (lane == 0) {
+      const double n_o = p.nk[own], n_b = p.nk[nb];
+      const bool singleton = n_o == 1.0;
+      double a, b;
+      if (COS) {
+        const double nrm = sqrt(ss);
+        b = cos_foreign(n_b, cb / nrm);
+        a = singleton ? 0.0 : cos_own(n_o, co / nrm);
+      } else {
+        b = sq_foreign(ss, p.stats[p.k + nb], n_b, cb);
+        a = singleton ? 0.0 : sq_own(ss, p.stats[p.k + own], n_o, co);
+      }
+      p.s[row] = singleton ? 0.0 : assemble_score(a, b);
+      if (p.a) p.a[row] = a;
+      if (p.b) p.b[row] = b;
+    }
+  }
+}
+
 }  // namespace
+
+void exact_ab(fsil_context* c, const ScoreParams& p) {
+  const int grid = c->num_sms * 8;
+  const int2* rows = c->exact_rows.as<int2>();
+  const unsigned long long* cnt = c->exact_count.as<unsigned long long>();
+  if (c->metric == FSIL_COSINE) exact_ab_kernel<true><<<grid, 256, 0, c->stream>>>(p, rows, cnt);
+  else exact_ab_kernel<false><<<grid, 256, 0, c->stream>>>(p, rows, cnt);
+  FSIL_LAUNCHED(c);
+}
 
 void flag_all(fsil_context* c, const ScoreParams& p, int tile_rows) {
   flag_all_kernel<<<static_cast<unsigned>((p.n + 255) / 256), 256, 0, c->stream>>>(
@@ -162,8 +222,9 @@ void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int til
         p.tile_sum, p.tile_flag, p.s, ntiles, tile_rows, p.n, c->group_sum.as<double>());
     FSIL_LAUNCHED(c);
   }
-  total_kernel<<<1, 1024, 0, c->stream>>>(c->group_sum.as<double>(), ngroups, p.flag_count,
-                                          c->result.as<double>());
+  total_kernel<<<1, 1024, 0, c->stream>>>(
+      c->group_sum.as<double>(), ngroups, p.flag_count,
+      c->tc_exact_used ? c->exact_count.as<unsigned long long>() : nullptr, c->result.as<double>());
   FSIL_LAUNCHED(c);
 }
 

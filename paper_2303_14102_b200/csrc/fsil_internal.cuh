@@ -123,6 +123,10 @@ struct fsil_context {
   fsil::DevBuf tile_sum, tile_flag, flag_rows, flag_count;
   fsil::DevBuf result;         // double[4]: sum_s, flagged, ... (shard partial)
   fsil::DevBuf group_sum;
+  fsil::DevBuf xmax;           // float: max |x| of this shard (tensor-core operand scaling)
+  fsil::DevBuf tc_b;           // fp16 cluster-mean pieces + column bias (tcgen05 path)
+  fsil::DevBuf exact_rows, exact_count;  // rows needing the exact own/neighbour recompute
+  bool tc_exact_used = false;
   // host staging for fsil_silhouette (pageable -> pinned)
   fsil::DevBuf hX, hL;         // device copies of host inputs
   fsil::DevBuf o_s, o_nb, o_own, o_a, o_b;

@@ -1,15 +1,499 @@
-// score_tc.cu -- K3: tcgen05 scoring (placeholder until the tensor-core kernel lands).
+// score_tc.cu -- K3: per-point scoring on the 5th-generation tensor cores.
+//
+// Replaces score_range + mean_dist_to_cluster + make_point_score
+// (squared_euclidean.cpp:65-108, cosine.cpp:71-117, report.cpp:16-30) when
+// X . mu^T is a real contraction.  One persistent CTA per SM, warp-specialised:
+//
+//   warp 0      TMA producer: fp32 X boxes (128 rows x 32 cols, 128B swizzle) into a
+//               staging ring; fp16 cluster-mean pieces B_hi/B_lo into the operand ring
+//   warp 1      TMEM owner + single-thread tcgen05.mma issuer (kind::f16, fp32 accum)
+//   warps 2..5  epilogue (one TMEM lane = one row): clamped cluster means, top-2 with a
+//               rigorous error bound, a_i/b_i/s_i from the tensor-core dots in fp64
+//   warps 6..9  converters: x (fp32) -> x*2^-ex split into fp16 hi + lo in the UMMA
+//               K-major SWIZZLE_128B layout, plus ||x||^2 (fp32 and fp64) per row
+//
+// Split precision ("fp16x3"): x~ = hx + lx, mu~ = hm + lm (exact to ~2^-22 after a
+// global power-of-two scaling); dot = hx.hm + hx.lm + lx.hm, three MMAs per K step.
+// Every row carries a certified bound on its dots; rows whose neighbour is not
+// certain go to the fp64 argmin refinement (K4), rows whose a_i/b_i bound exceeds
+// 2e-6 in s_i go to the exact own/neighbour recompute -- both in finalize.cu.
+#include <algorithm>
+#include <cmath>
+#include <cuda_fp16.h>
+
 #include "score_common.cuh"
+#include "sm100.cuh"
 
 namespace fsil {
+namespace {
 
-bool tc_supported(const fsil_context*) { return false; }
-int64_t tc_tiles(const fsil_context* c, int* tile_rows) {
-  *tile_rows = 128;
-  return (c->n + 127) / 128;
+using namespace sm100;
+
+constexpr int BM = 128;               // rows per tile = TMEM lanes
+constexpr int BK = 64;                // fp16 K elements per chunk (one 128-byte swizzle row)
+constexpr int kStgBytes = 2 * BM * 128;  // two fp32 boxes of 32 columns
+constexpr int kABytes = BM * 128;        // one fp16 A piece (hi or lo)
+constexpr int kThreads = 320;            // 10 warps
+constexpr float kTau = 2e-6f;            // certified |ds_i| budget before exact a/b
+
+struct TcParams {
+  ScoreParams p;
+  int ncb, nkc;           // cluster blocks, K chunks
+  float sx;               // 2^-ex: x -> x~
+  float smul;             // 2^(ex+em): dot = acc * smul
+  double smul64;
+  const float* colbias;   // [ncb*BN]: sqeuclid p_k, cosine 0, padding +inf
+  float cdot;             // relative dot bound coefficient
+  float floor_coef;       // absolute-floor coefficient (times ||x||)
+  float mu_max;           // max ||mu_k||
+  float p_max;
+  int2* exact_rows;       // rows needing the exact own/neighbour recompute
+  unsigned long long* exact_count;
+};
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
-void score_tc(fsil_context*, const ScoreParams&) {
-  fail(FSIL_ERR_INVALID_ARGUMENT, "tcgen05 scoring path not built");
+
+template <int BN, bool COS>
+__global__ void __launch_bounds__(kThreads, 1)
+    score_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
+                    const __grid_constant__ CUtensorMap tmap_bl, TcParams tp, int64_t ntiles) {
+  constexpr int kBBytes = BN * 128;
+  constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : 256;
+  constexpr uint32_t kIdesc = idesc_f16_f32(BM, BN);
+  const ScoreParams& p = tp.p;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stg = base;                                  // [2][kStgBytes]
+  uint8_t* a_hi = stg + 2 * kStgBytes;                  // [2][kABytes]
+  uint8_t* a_lo = a_hi + 2 * kABytes;                   // [2][kABytes]
+  uint8_t* b_hi = a_lo + 2 * kABytes;                   // [2][kBBytes]
+  uint8_t* b_lo = b_hi + 2 * kBBytes;                   // [2][kBBytes]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b_lo + 2 * kBBytes);
+  uint64_t* stg_full = bars + 0;    // [2]
+  uint64_t* stg_empty = bars + 2;   // [2]
+  uint64_t* op_full = bars + 4;     // [2]
+  uint64_t* op_empty = bars + 6;    // [2]
+  uint64_t* acc_full = bars + 8;    // [2]
+  uint64_t* acc_empty = bars + 10;  // [2]
+  uint64_t* meta_full = bars + 12;  // [2]
+  uint64_t* meta_empty = bars + 14; // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  float* meta_xi = reinterpret_cast<float*>(bars + 18);          // [2][BM]
+  double* meta_xi64 = reinterpret_cast<double*>(meta_xi + 2 * BM);  // [2][BM]
+  double* red = meta_xi64 + 2 * BM;                               // [4]
+  int* red_flag = reinterpret_cast<int*>(red + 4);                // [1]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ncb = tp.ncb, nkc = tp.nkc;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(stg_full + i, 1);
+      mbar_init(stg_empty + i, 4);
+      mbar_init(op_full + i, 1 + 4);
+      mbar_init(op_empty + i, 1);
+      mbar_init(acc_full + i, 1);
+      mbar_init(acc_empty + i, 4);
+      mbar_init(meta_full + i, 4);
+      mbar_init(meta_empty + i, 4);
+    }
+    fence_barrier_init();
+    prefetch_tmap(&tmap_x);
+    prefetch_tmap(&tmap_bh);
+    prefetch_tmap(&tmap_bl);
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t n1 = 0, n2 = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int row0 = static_cast<int>(t * BM);
+        for (int cb = 0; cb < ncb; ++cb) {
+          for (int kc = 0; kc < nkc; ++kc, ++n1, ++n2) {
+            const int s1 = n1 & 1, s2 = n2 & 1;
+            const uint32_t ph1 = (n1 >> 1) & 1, ph2 = (n2 >> 1) & 1;
+            const int nbox = (kc * BK + 32 < p.d) ? 2 : 1;
+            mbar_wait(stg_empty + s1, ph1 ^ 1);
+            mbar_arrive_expect_tx(stg_full + s1, nbox * BM * 128);
+            for (int b = 0; b < nbox; ++b)
+              tma_load_2d(stg + s1 * kStgBytes + b * BM * 128, &tmap_x, stg_full + s1, kc * BK + b * 32, row0);
+            mbar_wait(op_empty + s2, ph2 ^ 1);
+            mbar_arrive_expect_tx(op_full + s2, 2 * kBBytes);
+            tma_load_2d(b_hi + s2 * kBBytes, &tmap_bh, op_full + s2, kc * BK, cb * BN);
+            tma_load_2d(b_lo + s2 * kBBytes, &tmap_bl, op_full + s2, kc * BK, cb * BN);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      uint32_t n2 = 0, na = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int cb = 0; cb < ncb; ++cb, ++na) {
+          const int ab = na & 1;
+          const uint32_t pha = (na >> 1) & 1;
+          mbar_wait(acc_empty + ab, pha ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + ab * BN;
+          for (int kc = 0; kc < nkc; ++kc, ++n2) {
+            const int s2 = n2 & 1;
+            mbar_wait(op_full + s2, (n2 >> 1) & 1);
+            tc_fence_after();
+            const int rem = p.d - kc * BK;
+            const int nks = rem >= BK ? 4 : (rem + 15) / 16;
+            const uint32_t ah = smem_u32(a_hi + s2 * kABytes), al = smem_u32(a_lo + s2 * kABytes);
+            const uint32_t bh = smem_u32(b_hi + s2 * kBBytes), bl = smem_u32(b_lo + s2 * kBBytes);
+            for (int ks = 0; ks < nks; ++ks) {
+              const uint32_t off = ks * 32;
+              const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
+              mma_f16(d_tmem, desc_k_sw128(ah + off), desc_k_sw128(bh + off), kIdesc, acc0);
+              mma_f16(d_tmem, desc_k_sw128(ah + off), desc_k_sw128(bl + off), kIdesc, 1u);
+              mma_f16(d_tmem, desc_k_sw128(al + off), desc_k_sw128(bh + off), kIdesc, 1u);
+            }
+            mma_commit(op_empty + s2);  // stage free once these MMAs retire
+          }
+          mma_commit(acc_full + ab);    // accumulator ready for the epilogue
+        }
+      }
+    }
+  } else if (warp >= 6) {
+    // ------------------------------------------------------------ converters
+    const int r = threadIdx.x - 6 * 32;  // row in tile, 0..127
+    const int sw = r & 7;
+    uint32_t n1 = 0, n2 = 0, nt = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
+      float xi32 = 0.f;
+      double xi64 = 0.0;
+      for (int cb = 0; cb < ncb; ++cb) {
+        for (int kc = 0; kc < nkc; ++kc, ++n1, ++n2) {
+          const int s1 = n1 & 1, s2 = n2 & 1;
+          mbar_wait(stg_full + s1, (n1 >> 1) & 1);
+          mbar_wait(op_empty + s2, ((n2 >> 1) & 1) ^ 1);
+          const uint8_t* srow = stg + s1 * kStgBytes + r * 128;
+          uint8_t* hrow = a_hi + s2 * kABytes + r * 128;
+          uint8_t* lrow = a_lo + s2 * kABytes + r * 128;
+          const bool two = kc * BK + 32 < p.d;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {  // 8 fp16 A chunks of 16 bytes
+            float4 f0 = make_float4(0.f, 0.f, 0.f, 0.f), f1 = f0;
+            if (j < 4 || two) {
+              const uint8_t* box = srow + (j >> 2) * (BM * 128);
+              f0 = *reinterpret_cast<const float4*>(box + ((((2 * j) & 7) ^ sw) << 4));
+              f1 = *reinterpret_cast<const float4*>(box + ((((2 * j + 1) & 7) ^ sw) << 4));
+            }
+            const float v[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+            if (cb == 0) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                xi32 = fmaf(v[e], v[e], xi32);
+                xi64 = fma(static_cast<double>(v[e]), static_cast<double>(v[e]), xi64);
+              }
+            }
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float x0 = v[2 * e] * tp.sx, x1 = v[2 * e + 1] * tp.sx;
+              const __half2 h = __floats2half2_rn(x0, x1);
+              const float2 hf = __half22float2(h);
+              const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+              hw[e] = *reinterpret_cast<const uint32_t*>(&h);
+              lw[e] = *reinterpret_cast<const uint32_t*>(&l);
+            }
+            const int pos = (j ^ sw) << 4;
+            *reinterpret_cast<uint4*>(hrow + pos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(lrow + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(op_full + s2);
+            mbar_arrive(stg_empty + s1);
+          }
+        }
+        if (cb == 0) {
+          const int tb = nt & 1;
+          mbar_wait(meta_empty + tb, ((nt >> 1) & 1) ^ 1);
+          meta_xi[tb * BM + r] = xi32;
+          meta_xi64[tb * BM + r] = xi64;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(meta_full + tb);
+        }
+      }
+    }
+  } else if (warp >= 2) {
+    // ------------------------------------------------------------ epilogue
+    const int quad = warp & 3;        // TMEM lane quadrant of this warp
+    const int r = quad * 32 + lane;   // row in tile
+    const int ew = warp - 2;          // epilogue warp 0..3
+    uint32_t na = 0, nt = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
+      const int64_t row = t * BM + r;
+      const bool valid = row < p.n;
+      const int own = valid ? p.dense[row] : -1;
+      const int tb = nt & 1;
+      mbar_wait(meta_full + tb, (nt >> 1) & 1);
+      const float xi = meta_xi[tb * BM + r];
+      const double xi64 = meta_xi64[tb * BM + r];
+      const float xn = sqrtf(xi);
+      const float rowc = COS ? 1.0f : xi;                         // row term of m
+      const float rowm = COS ? -(tp.smul / xn) : -2.0f * tp.smul;  // acc multiplier
+      float b1 = INFINITY, b2 = INFINITY, dotb = 0.f, doto = 0.f;
+      int arg = -1;
+      for (int cb = 0; cb < ncb; ++cb, ++na) {
+        const int ab = na & 1;
+        mbar_wait(acc_full + ab, (na >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int q = 0; q < BN / 32; ++q) {
+          float v[32];
+          tmem_ld32(tmem_base + ab * BN + q * 32 + (static_cast<uint32_t>(quad * 32) << 16), v);
+          const int k0 = cb * BN + q * 32;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int k = k0 + j;
+            // clamped mean (sqE.cpp:81, cos.cpp:87); padding columns carry +inf bias
+            float m;
+            if (COS) m = fminf(fmaxf(fmaf(v[j], rowm, rowc), 0.f), 2.f) + __ldg(tp.colbias + k);
+            else m = fmaxf(fmaf(v[j], rowm, rowc + __ldg(tp.colbias + k)), 0.f);
+            if (k == own) {
+              doto = v[j];
+              m = INFINITY;
+            }
+            if (m < b1) {
+              b2 = b1;
+              b1 = m;
+              arg = k;
+              dotb = v[j];
+            } else {
+              b2 = fminf(b2, m);
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty + ab);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(meta_empty + tb);
+
+      // ---- certification and a_i, b_i, s_i from the tensor-core dots
+      double s = 0.0;
+      bool any = false;
+      if (valid) {
+        const float eps_dot = tp.cdot * xn * tp.mu_max + tp.floor_coef * xn;
+        const float eps_m = COS ? (eps_dot / xn + 4.0f * 5.9604645e-8f)
+                                : (2.0f * eps_dot + (p.d + 8) * 5.9604645e-8f * (xi + tp.p_max + 2.0f * xn * tp.mu_max));
+        int nb = arg;
+        bool full = !((b2 - b1) > 2.0f * eps_m) || nb < 0;
+        if (nb < 0) nb = own == 0 ? 1 : 0;
+        const double n_o = p.nk[own], n_b = p.nk[nb];
+        const bool singleton = n_o == 1.0;
+        const double dn = static_cast<double>(dotb) * tp.smul64, dob = static_cast<double>(doto) * tp.smul64;
+        const double ed = static_cast<double>(eps_dot) * 1.0000001;
+        double a, b, da, db;
+        if (COS) {
+          const double nrm = sqrt(xi64);
+          b = cos_foreign(n_b, n_b * dn / nrm);
+          a = singleton ? 0.0 : cos_own(n_o, n_o * dob / nrm);
+          db = ed / nrm;
+          da = n_o / (n_o - 1.0) * ed / nrm;
+        } else {
+          const double* psi = p.stats + p.k;
+          b = sq_foreign(xi64, psi[nb], n_b, n_b * dn);
+          a = singleton ? 0.0 : sq_own(xi64, psi[own], n_o, n_o * dob);
+          db = 2.0 * ed;
+          da = 2.0 * n_o / (n_o - 1.0) * ed;
+        }
+        s = singleton ? 0.0 : assemble_score(a, b);
+        const double mx = fmax(a, b);
+        const bool inexact = !singleton && !(mx > 2.0 * (da + db) && (da + db) / mx <= kTau);
+        p.s[row] = s;
+        if (p.nb) p.nb[row] = nb;
+        if (p.own) p.own[row] = own;
+        if (p.a) p.a[row] = a;
+        if (p.b) p.b[row] = b;
+        if (full) {
+          const unsigned long long idx = atomicAdd(p.flag_count, 1ull);
+          p.flag_rows[idx] = static_cast<int32_t>(row);
+          any = true;
+        } else if (inexact) {
+          const unsigned long long idx = atomicAdd(tp.exact_count, 1ull);
+          tp.exact_rows[idx] = make_int2(static_cast<int>(row), nb);
+          any = true;
+        }
+      }
+      // fixed-order tile sum over the 4 epilogue warps (named barrier 1, 128 threads)
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      const unsigned anyw = __ballot_sync(0xffffffffu, any);
+      if (lane == 0) {
+        red[quad] = s;
+        if (ew == 0) *red_flag = 0;
+      }
+      named_bar(1, 128);
+      if (lane == 0 && anyw) atomicOr(red_flag, 1);
+      named_bar(1, 128);
+      if (ew == 0 && lane == 0) {
+        p.tile_sum[t] = ((red[0] + red[1]) + red[2]) + red[3];
+        p.tile_flag[t] = *red_flag;
+      }
+      named_bar(1, 128);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+// ---------------------------------------------------------------- prep --------
+// B pieces: mu~ = mu * 2^-em split into fp16 hi + lo, [Kp][Dp] zero padded; column
+// bias for the ranking (sqeuclid p_k, cosine 0, padding +inf).
+__global__ void prep_b_kernel(const double* __restrict__ stats, int k, int d, int kp, int dp, bool cos,
+                              float smu, __half* bh, __half* bl, float* colbias) {
+  const int c = blockIdx.x;
+  const double n = c < k ? fmax(stats[c], 1.0) : 1.0;
+  const double* sums = stats + (cos ? k : 2 * k) + static_cast<int64_t>(c) * d;
+  for (int l = threadIdx.x; l < dp; l += blockDim.x) {
+    float h = 0.f, lo = 0.f;
+    if (c < k && l < d) {
+      const double mu = sums[l] / n * static_cast<double>(smu);
+      const __half hh = __double2half(mu);
+      h = __half2float(hh);
+      lo = static_cast<float>(mu - static_cast<double>(h));
+    }
+    bh[static_cast<int64_t>(c) * dp + l] = __float2half_rn(h);
+    bl[static_cast<int64_t>(c) * dp + l] = __float2half_rn(lo);
+  }
+  if (threadIdx.x == 0)
+    colbias[c] = c < k ? (cos ? 0.0f : static_cast<float>(stats[k + c] / n)) : INFINITY;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    FSIL_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
+    if (!ptr || q != cudaDriverEntryPointSuccess) fail(FSIL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* ptr, uint64_t inner, uint64_t outer,
+                        uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {row_bytes};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(FSIL_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+
+int pick_bn(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : 128; }
+
+size_t tc_smem(int bn) {
+  return 1024 + 2 * kStgBytes + 4 * kABytes + 4 * static_cast<size_t>(bn) * 128 + 16 * 8 + 16 + 2 * BM * 4 +
+         2 * BM * 8 + 64;
+}
+
+template <int BN, bool COS>
+void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
+               const TcParams& tp, int64_t ntiles) {
+  auto kern = score_tc_kernel<BN, COS>;
+  const size_t smem = tc_smem(BN);
+  FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int grid = static_cast<int>(std::min<int64_t>(ntiles, c->num_sms));
+  kern<<<grid, kThreads, smem, c->stream>>>(mx, mh, ml, tp, ntiles);
+  FSIL_LAUNCHED(c);
+}
+
+}  // namespace
+
+bool tc_supported(const fsil_context* c) {
+  return c->d % 4 == 0 && c->n < (int64_t(1) << 31) && c->k >= 2 && tc_smem(pick_bn(c->k)) <= c->smem_optin;
+}
+
+int64_t tc_tiles(const fsil_context* c, int* tile_rows) {
+  *tile_rows = BM;
+  return (c->n + BM - 1) / BM;
+}
+
+void score_tc(fsil_context* c, const ScoreParams& p) {
+  const bool cos = c->metric == FSIL_COSINE;
+  const int bn = pick_bn(c->k);
+  const int ncb = (c->k + bn - 1) / bn;
+  const int kp = ncb * bn;
+  const int nkc = (c->d + BK - 1) / BK;
+  const int dp = nkc * BK;
+  // global power-of-two scalings: max|x~| and max|mu~| in [2^14, 2^15)
+  float h_bound[4] = {0, 0, 0, 0}, h_xmax = 0.f;
+  FSIL_CUDA(cudaMemcpyAsync(h_bound, c->bound.p, sizeof(h_bound), cudaMemcpyDeviceToHost, c->stream));
+  FSIL_CUDA(cudaMemcpyAsync(&h_xmax, c->xmax.p, sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  FSIL_CUDA(cudaStreamSynchronize(c->stream));
+  const int ex = h_xmax > 0.f ? std::ilogb(h_xmax) - 14 : 0;
+  const int em = h_bound[2] > 0.f ? std::ilogb(h_bound[2]) - 14 : 0;
+  c->tc_b.ensure(2ull * kp * dp * sizeof(__half) + kp * sizeof(float));
+  __half* bh = c->tc_b.as<__half>();
+  __half* bl = bh + static_cast<size_t>(kp) * dp;
+  float* colbias = reinterpret_cast<float*>(bl + static_cast<size_t>(kp) * dp);
+  prep_b_kernel<<<kp, 128, 0, c->stream>>>(p.stats, c->k, c->d, kp, dp, cos, std::ldexp(1.0f, -em), bh, bl,
+                                           colbias);
+  FSIL_LAUNCHED(c);
+  const CUtensorMap mx = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, c->X, c->d, c->n, c->d * 4ull, 32, BM);
+  const CUtensorMap mh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, bh, dp, kp, dp * 2ull, BK, bn);
+  const CUtensorMap ml = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, bl, dp, kp, dp * 2ull, BK, bn);
+  TcParams tp{};
+  tp.p = p;
+  tp.ncb = ncb;
+  tp.nkc = nkc;
+  tp.sx = std::ldexp(1.0f, -ex);
+  tp.smul = std::ldexp(1.0f, ex + em);
+  tp.smul64 = std::ldexp(1.0, ex + em);
+  tp.colbias = colbias;
+  // |dot error| <= cdot*||x||*max||mu|| + floor: split residuals 3*2^-22 relative, fp32
+  // accumulation over 3*ceil(D/16)+2 MMA steps at 2^-24, and the fp16 subnormal floor
+  // 2^-25 per element in scaled units (times sqrt(D) via Cauchy-Schwarz).
+  const float u = 5.9604645e-8f;
+  tp.cdot = 1.05f * (3.0f * 4.0f * u + (3.0f * ((c->d + 15) / 16) + 2.0f) * u);
+  tp.floor_coef = 1.05f * 0.5f * u * std::sqrt(static_cast<float>(c->d)) *
+                  (std::ldexp(1.0f, em) + std::ldexp(1.0f, ex) * h_bound[0] / std::max(h_xmax, 1e-30f));
+  tp.mu_max = h_bound[0];
+  tp.p_max = h_bound[1];
+  c->exact_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int2));
+  c->exact_count.ensure(sizeof(unsigned long long));
+  FSIL_CUDA(cudaMemsetAsync(c->exact_count.p, 0, sizeof(unsigned long long), c->stream));
+  tp.exact_rows = c->exact_rows.as<int2>();
+  tp.exact_count = c->exact_count.as<unsigned long long>();
+  const int64_t ntiles = (c->n + BM - 1) / BM;
+  if (cos) {
+    if (bn == 32) launch_tc<32, true>(c, mx, mh, ml, tp, ntiles);
+    else if (bn == 64) launch_tc<64, true>(c, mx, mh, ml, tp, ntiles);
+    else launch_tc<128, true>(c, mx, mh, ml, tp, ntiles);
+  } else {
+    if (bn == 32) launch_tc<32, false>(c, mx, mh, ml, tp, ntiles);
+    else if (bn == 64) launch_tc<64, false>(c, mx, mh, ml, tp, ntiles);
+    else launch_tc<128, false>(c, mx, mh, ml, tp, ntiles);
+  }
+  c->tc_exact_used = true;
 }
 
 }  // namespace fsil
