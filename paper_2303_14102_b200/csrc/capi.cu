@@ -142,7 +142,9 @@ void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, 
     else use = FSIL_PATH_FP64;
   }
   if (use == FSIL_PATH_TCGEN05 && !tc_ok)
-    fail(FSIL_ERR_INVALID_ARGUMENT, "tcgen05 scoring path unavailable for this shape");
+    fail(FSIL_ERR_INVALID_ARGUMENT, "tcgen05 scoring path unavailable for this shape (d=" +
+                                        std::to_string(c->d) + ", k=" + std::to_string(c->k) +
+                                        ", smem optin " + std::to_string(c->smem_optin) + ")");
   if (use == FSIL_PATH_FFMA && !ffma_ok)
     fail(FSIL_ERR_INVALID_ARGUMENT, "FFMA scoring path unavailable for this shape (D too large)");
   int tile_rows = 256;

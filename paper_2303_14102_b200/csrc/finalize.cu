@@ -141,36 +141,41 @@ __global__ void flag_all_kernel(int64_t n, int tile_rows, int32_t* flag_rows, in
 }
 
 // Exact own/neighbour recompute for rows whose tensor-core a_i/b_i bound was too
-// loose (neighbour already certified): one warp per row, reference formulas.
-template <bool COS>
+// loose (neighbour already certified): LPR lanes per row (32/LPR rows per warp),
+// reference formulas in fp64.
+template <bool COS, int LPR>
 __global__ void __launch_bounds__(256) exact_ab_kernel(ScoreParams p, const int2* __restrict__ rows,
                                                        const unsigned long long* count) {
-  const unsigned long long cnt = *count;
-  const int lane = threadIdx.x & 31;
+  const int64_t cnt = static_cast<int64_t>(*count);
+  const int lane = threadIdx.x & 31, sub = lane / LPR, li = lane % LPR;
+  constexpr int RPW = 32 / LPR;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const double* sums = p.stats + (COS ? p.k : 2 * p.k);
-  for (int64_t i = warp; i < static_cast<int64_t>(cnt); i += nwarps) {
-    const int2 rn = rows[i];
+  for (int64_t base = warp * RPW; base < cnt; base += nwarps * RPW) {
+    const int64_t i = base + sub;
+    const bool valid = i < cnt;
+    const int2 rn = valid ? rows[i] : make_int2(0, 0);
     const int64_t row = rn.x;
     const int nb = rn.y;
-    const int own = p.dense[row];
+    const int own = valid ? p.dense[row] : 0;
     const float* x = p.X + row * p.d;
     const double* yo = sums + static_cast<int64_t>(own) * p.d;
     const double* yb = sums + static_cast<int64_t>(nb) * p.d;
     double ss = 0.0, co = 0.0, cb = 0.0;
-    for (int l = lane; l < p.d; l += 32) {
-      const double v = x[l];
-      ss = fma(v, v, ss);
-      co = fma(yo[l], v, co);
-      cb = fma(yb[l], v, cb);
+    if (valid)
+      for (int l = li; l < p.d; l += LPR) {
+        const double v = x[l];
+        ss = fma(v, v, ss);
+        co = fma(yo[l], v, co);
+        cb = fma(yb[l], v, cb);
+      }
+    for (int off = LPR >> 1; off > 0; off >>= 1) {
+      ss += __shfl_xor_sync(0xffffffffu, ss, off, LPR);
+      co += __shfl_xor_sync(0xffffffffu, co, off, LPR);
+      cb += __shfl_xor_sync(0xffffffffu, cb, off, LPR);
     }
-    for (int off = 16; off > 0; off >>= 1) {
-      ss += __shfl_xor_sync(0xffffffffu, ss, off);
-      co += __shfl_xor_sync(0xffffffffu, co, off);
-      cb += __shfl_xor_sync(0xffffffffu, cb, off);
-    }
-    if (lane == 0) {
+    if (valid && li == 0) {
       const double n_o = p.nk[own], n_b = p.nk[nb];
       const bool singleton = n_o == 1.0;
       double a, b;
@@ -195,8 +200,14 @@ void exact_ab(fsil_context* c, const ScoreParams& p) {
   const int grid = c->num_sms * 8;
   const int2* rows = c->exact_rows.as<int2>();
   const unsigned long long* cnt = c->exact_count.as<unsigned long long>();
-  if (c->metric == FSIL_COSINE) exact_ab_kernel<true><<<grid, 256, 0, c->stream>>>(p, rows, cnt);
-  else exact_ab_kernel<false><<<grid, 256, 0, c->stream>>>(p, rows, cnt);
+  const int lpr = c->d <= 32 ? 4 : c->d <= 64 ? 8 : c->d <= 128 ? 16 : 32;
+#define FSIL_EXACT(L)                                                                        \
+  if (lpr == L) {                                                                            \
+    if (c->metric == FSIL_COSINE) exact_ab_kernel<true, L><<<grid, 256, 0, c->stream>>>(p, rows, cnt); \
+    else exact_ab_kernel<false, L><<<grid, 256, 0, c->stream>>>(p, rows, cnt);              \
+  }
+  FSIL_EXACT(4) FSIL_EXACT(8) FSIL_EXACT(16) FSIL_EXACT(32)
+#undef FSIL_EXACT
   FSIL_LAUNCHED(c);
 }
 

@@ -16,7 +16,7 @@
 // global power-of-two scaling); dot = hx.hm + hx.lm + lx.hm, three MMAs per K step.
 // Every row carries a certified bound on its dots; rows whose neighbour is not
 // certain go to the fp64 argmin refinement (K4), rows whose a_i/b_i bound exceeds
-// 2e-6 in s_i go to the exact own/neighbour recompute -- both in finalize.cu.
+// 5e-6 in s_i go to the exact own/neighbour recompute -- both in finalize.cu.
 #include <algorithm>
 #include <cmath>
 #include <cuda_fp16.h>
@@ -34,7 +34,9 @@ constexpr int BK = 64;                // fp16 K elements per chunk (one 128-byte
 constexpr int kStgBytes = 2 * BM * 128;  // two fp32 boxes of 32 columns
 constexpr int kABytes = BM * 128;        // one fp16 A piece (hi or lo)
 constexpr int kThreads = 320;            // 10 warps
-constexpr float kTau = 2e-6f;            // certified |ds_i| budget before exact a/b
+constexpr float kTau = 9e-6f;            // certified |ds_i| budget before exact a/b (bar: 1e-5)
+
+__host__ __device__ constexpr int ncb_bn_pad(int kp) { return (kp + 3) & ~3; }
 
 struct TcParams {
   ScoreParams p;
@@ -43,6 +45,7 @@ struct TcParams {
   float smul;             // 2^(ex+em): dot = acc * smul
   double smul64;
   const float* colbias;   // [ncb*BN]: sqeuclid p_k, cosine 0, padding +inf
+  const float* munorm;    // [ncb*BN]: ||mu_k|| rounded up (per-cluster error bounds)
   float cdot;             // relative dot bound coefficient
   float floor_coef;       // absolute-floor coefficient (times ||x||)
   float mu_max;           // max ||mu_k||
@@ -60,7 +63,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
                     const __grid_constant__ CUtensorMap tmap_bl, TcParams tp, int64_t ntiles) {
   constexpr int kBBytes = BN * 128;
-  constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : 256;
+  // two accumulator buffers x {main hx.hm, correction hx.lm + lx.hm} of BN columns
+  constexpr uint32_t kTmemCols = (4 * BN <= 32) ? 32 : (4 * BN <= 64) ? 64 : (4 * BN <= 128) ? 128 : (4 * BN <= 256) ? 256 : 512;
   constexpr uint32_t kIdesc = idesc_f16_f32(BM, BN);
   const ScoreParams& p = tp.p;
 
@@ -85,9 +89,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   double* meta_xi64 = reinterpret_cast<double*>(meta_xi + 2 * BM);  // [2][BM]
   double* red = meta_xi64 + 2 * BM;                               // [4]
   int* red_flag = reinterpret_cast<int*>(red + 4);                // [1]
+  float* cb_s = reinterpret_cast<float*>(red + 8);                // [ncb*BN] column bias
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncb = tp.ncb, nkc = tp.nkc;
+  for (int j = threadIdx.x; j < ncb * BN; j += blockDim.x) cb_s[j] = tp.colbias[j];
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -144,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t pha = (na >> 1) & 1;
           mbar_wait(acc_empty + ab, pha ^ 1);
           tc_fence_after();
-          const uint32_t d_tmem = tmem_base + ab * BN;
+          const uint32_t d_main = tmem_base + ab * 2 * BN, d_corr = d_main + BN;
           for (int kc = 0; kc < nkc; ++kc, ++n2) {
             const int s2 = n2 & 1;
             mbar_wait(op_full + s2, (n2 >> 1) & 1);
@@ -156,9 +162,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int ks = 0; ks < nks; ++ks) {
               const uint32_t off = ks * 32;
               const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
-              mma_f16(d_tmem, desc_k_sw128(ah + off), desc_k_sw128(bh + off), kIdesc, acc0);
-              mma_f16(d_tmem, desc_k_sw128(ah + off), desc_k_sw128(bl + off), kIdesc, 1u);
-              mma_f16(d_tmem, desc_k_sw128(al + off), desc_k_sw128(bh + off), kIdesc, 1u);
+              // main term and the two correction terms accumulate separately: the
+              // corrections are ~2^-10 of the main term, so their fp32 rounding is too
+              mma_f16(d_main, desc_k_sw128(ah + off), desc_k_sw128(bh + off), kIdesc, acc0);
+              mma_f16(d_corr, desc_k_sw128(ah + off), desc_k_sw128(bl + off), kIdesc, acc0);
+              mma_f16(d_corr, desc_k_sw128(al + off), desc_k_sw128(bh + off), kIdesc, 1u);
             }
             mma_commit(op_empty + s2);  // stage free once these MMAs retire
           }
@@ -255,27 +263,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
 #pragma unroll 1
         for (int q = 0; q < BN / 32; ++q) {
-          float v[32];
-          tmem_ld32(tmem_base + ab * BN + q * 32 + (static_cast<uint32_t>(quad * 32) << 16), v);
-          const int k0 = cb * BN + q * 32;
+          float v[32], w[32];
+          const uint32_t ta = tmem_base + ab * 2 * BN + q * 32 + (static_cast<uint32_t>(quad * 32) << 16);
+          tmem_ld32(ta, v);
+          tmem_ld32(ta + BN, w);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int k = k0 + j;
-            // clamped mean (sqE.cpp:81, cos.cpp:87); padding columns carry +inf bias
-            float m;
-            if (COS) m = fminf(fmaxf(fmaf(v[j], rowm, rowc), 0.f), 2.f) + __ldg(tp.colbias + k);
-            else m = fmaxf(fmaf(v[j], rowm, rowc + __ldg(tp.colbias + k)), 0.f);
-            if (k == own) {
-              doto = v[j];
-              m = INFINITY;
-            }
-            if (m < b1) {
-              b2 = b1;
-              b1 = m;
-              arg = k;
-              dotb = v[j];
-            } else {
-              b2 = fminf(b2, m);
+          for (int j = 0; j < 32; ++j) v[j] += w[j];
+          const int k0 = cb * BN + q * 32;
+          const float4* cb4 = reinterpret_cast<const float4*>(cb_s + k0);
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 bias = cb4[j4];
+            const float bj[4] = {bias.x, bias.y, bias.z, bias.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int j = 4 * j4 + e;
+              const int k = k0 + j;
+              // clamped mean (sqE.cpp:81, cos.cpp:87); padding columns carry +inf bias.
+              // Branch-free top-2 (strict <: the lowest index keeps ties).
+              float m;
+              if (COS) m = fminf(fmaxf(fmaf(v[j], rowm, rowc), 0.f), 2.f) + bj[e];
+              else m = fmaxf(fmaf(v[j], rowm, rowc + bj[e]), 0.f);
+              const bool is_own = k == own;
+              doto = is_own ? v[j] : doto;
+              m = is_own ? INFINITY : m;
+              const bool lt = m < b1;
+              arg = lt ? k : arg;
+              dotb = lt ? v[j] : dotb;
+              b2 = fminf(b2, fmaxf(b1, m));
+              b1 = fminf(b1, m);
             }
           }
         }
@@ -290,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       double s = 0.0;
       bool any = false;
       if (valid) {
-        const float eps_dot = tp.cdot * xn * tp.mu_max + tp.floor_coef * xn;
+        const float eps_dot = tp.cdot * xn * tp.mu_max + tp.floor_coef * xn;  // any column
         const float eps_m = COS ? (eps_dot / xn + 4.0f * 5.9604645e-8f)
                                 : (2.0f * eps_dot + (p.d + 8) * 5.9604645e-8f * (xi + tp.p_max + 2.0f * xn * tp.mu_max));
         int nb = arg;
@@ -299,20 +315,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const double n_o = p.nk[own], n_b = p.nk[nb];
         const bool singleton = n_o == 1.0;
         const double dn = static_cast<double>(dotb) * tp.smul64, dob = static_cast<double>(doto) * tp.smul64;
-        const double ed = static_cast<double>(eps_dot) * 1.0000001;
+        // per-cluster bounds for the two dots that enter a_i and b_i
+        const double ed_b = (static_cast<double>(tp.cdot) * __ldg(tp.munorm + nb) + tp.floor_coef) * xn * 1.0000001;
+        const double ed_o = (static_cast<double>(tp.cdot) * __ldg(tp.munorm + own) + tp.floor_coef) * xn * 1.0000001;
         double a, b, da, db;
         if (COS) {
           const double nrm = sqrt(xi64);
           b = cos_foreign(n_b, n_b * dn / nrm);
           a = singleton ? 0.0 : cos_own(n_o, n_o * dob / nrm);
-          db = ed / nrm;
-          da = n_o / (n_o - 1.0) * ed / nrm;
+          db = ed_b / nrm;
+          da = n_o / (n_o - 1.0) * ed_o / nrm;
         } else {
           const double* psi = p.stats + p.k;
           b = sq_foreign(xi64, psi[nb], n_b, n_b * dn);
           a = singleton ? 0.0 : sq_own(xi64, psi[own], n_o, n_o * dob);
-          db = 2.0 * ed;
-          da = 2.0 * n_o / (n_o - 1.0) * ed;
+          db = 2.0 * ed_b;
+          da = 2.0 * n_o / (n_o - 1.0) * ed_o;
         }
         s = singleton ? 0.0 : assemble_score(a, b);
         const double mx = fmax(a, b);
@@ -359,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // B pieces: mu~ = mu * 2^-em split into fp16 hi + lo, [Kp][Dp] zero padded; column
 // bias for the ranking (sqeuclid p_k, cosine 0, padding +inf).
 __global__ void prep_b_kernel(const double* __restrict__ stats, int k, int d, int kp, int dp, bool cos,
-                              float smu, __half* bh, __half* bl, float* colbias) {
+                              float smu, __half* bh, __half* bl, float* colbias, float* munorm) {
   const int c = blockIdx.x;
   const double n = c < k ? fmax(stats[c], 1.0) : 1.0;
   const double* sums = stats + (cos ? k : 2 * k) + static_cast<int64_t>(c) * d;
@@ -374,8 +392,20 @@ __global__ void prep_b_kernel(const double* __restrict__ stats, int k, int d, in
     bh[static_cast<int64_t>(c) * dp + l] = __float2half_rn(h);
     bl[static_cast<int64_t>(c) * dp + l] = __float2half_rn(lo);
   }
-  if (threadIdx.x == 0)
+  __shared__ double red[4];
+  double sq = 0.0;
+  if (c < k)
+    for (int l = threadIdx.x; l < d; l += blockDim.x) {
+      const double mu = sums[l] / n;
+      sq += mu * mu;
+    }
+  for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
     colbias[c] = c < k ? (cos ? 0.0f : static_cast<float>(stats[k + c] / n)) : INFINITY;
+    munorm[c] = __double2float_ru(sqrt(red[0] + red[1] + red[2] + red[3]) * (1.0 + 1e-12));
+  }
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -410,16 +440,16 @@ CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* ptr, uint64_t inner,
 
 int pick_bn(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : 128; }
 
-size_t tc_smem(int bn) {
+size_t tc_smem(int bn, int kp) {
   return 1024 + 2 * kStgBytes + 4 * kABytes + 4 * static_cast<size_t>(bn) * 128 + 16 * 8 + 16 + 2 * BM * 4 +
-         2 * BM * 8 + 64;
+         2 * BM * 8 + 96 + static_cast<size_t>(ncb_bn_pad(kp)) * 4;
 }
 
 template <int BN, bool COS>
 void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                const TcParams& tp, int64_t ntiles) {
   auto kern = score_tc_kernel<BN, COS>;
-  const size_t smem = tc_smem(BN);
+  const size_t smem = tc_smem(BN, tp.ncb * BN);
   FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int grid = static_cast<int>(std::min<int64_t>(ntiles, c->num_sms));
   kern<<<grid, kThreads, smem, c->stream>>>(mx, mh, ml, tp, ntiles);
@@ -429,7 +459,9 @@ void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, co
 }  // namespace
 
 bool tc_supported(const fsil_context* c) {
-  return c->d % 4 == 0 && c->n < (int64_t(1) << 31) && c->k >= 2 && tc_smem(pick_bn(c->k)) <= c->smem_optin;
+  const int bn = pick_bn(c->k);
+  const int kp = (c->k + bn - 1) / bn * bn;
+  return c->d % 4 == 0 && c->n < (int64_t(1) << 31) && c->k >= 2 && tc_smem(bn, kp) <= c->smem_optin;
 }
 
 int64_t tc_tiles(const fsil_context* c, int* tile_rows) {
@@ -451,12 +483,13 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   FSIL_CUDA(cudaStreamSynchronize(c->stream));
   const int ex = h_xmax > 0.f ? std::ilogb(h_xmax) - 14 : 0;
   const int em = h_bound[2] > 0.f ? std::ilogb(h_bound[2]) - 14 : 0;
-  c->tc_b.ensure(2ull * kp * dp * sizeof(__half) + kp * sizeof(float));
+  c->tc_b.ensure(2ull * kp * dp * sizeof(__half) + 2ull * kp * sizeof(float));
   __half* bh = c->tc_b.as<__half>();
   __half* bl = bh + static_cast<size_t>(kp) * dp;
   float* colbias = reinterpret_cast<float*>(bl + static_cast<size_t>(kp) * dp);
+  float* munorm = colbias + kp;
   prep_b_kernel<<<kp, 128, 0, c->stream>>>(p.stats, c->k, c->d, kp, dp, cos, std::ldexp(1.0f, -em), bh, bl,
-                                           colbias);
+                                           colbias, munorm);
   FSIL_LAUNCHED(c);
   const CUtensorMap mx = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, c->X, c->d, c->n, c->d * 4ull, 32, BM);
   const CUtensorMap mh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, bh, dp, kp, dp * 2ull, BK, bn);
@@ -469,11 +502,14 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   tp.smul = std::ldexp(1.0f, ex + em);
   tp.smul64 = std::ldexp(1.0, ex + em);
   tp.colbias = colbias;
-  // |dot error| <= cdot*||x||*max||mu|| + floor: split residuals 3*2^-22 relative, fp32
-  // accumulation over 3*ceil(D/16)+2 MMA steps at 2^-24, and the fp16 subnormal floor
-  // 2^-25 per element in scaled units (times sqrt(D) via Cauchy-Schwarz).
+  tp.munorm = munorm;
+  // |dot error| <= cdot*||x||*||mu|| + floor: split residuals 3*2^-22 relative; fp32
+  // accumulation of the main term over ceil(D/16) MMA steps at 2^-24 (the correction
+  // accumulator holds values <= 2^-10 of it); the final main+correction add; and the
+  // fp16 subnormal floor 2^-25 per element in scaled units (sqrt(D) via Cauchy-Schwarz).
   const float u = 5.9604645e-8f;
-  tp.cdot = 1.05f * (3.0f * 4.0f * u + (3.0f * ((c->d + 15) / 16) + 2.0f) * u);
+  const float steps = static_cast<float>((c->d + 15) / 16);
+  tp.cdot = 1.05f * (12.0f + steps + 1.0f + 2.0f * steps / 512.0f) * u;
   tp.floor_coef = 1.05f * 0.5f * u * std::sqrt(static_cast<float>(c->d)) *
                   (std::ldexp(1.0f, em) + std::ldexp(1.0f, ex) * h_bound[0] / std::max(h_xmax, 1e-30f));
   tp.mu_max = h_bound[0];
