@@ -22,6 +22,7 @@
 
 #include "device_util.cuh"
 #include "fsil_internal.cuh"
+#include "sm100.cuh"
 
 namespace fsil {
 namespace {
@@ -29,115 +30,330 @@ namespace {
 constexpr int kPieceRows = 2048;
 
 // ---------------------------------------------------------------- path 1 ----
-// Lanes of a warp are split into RPW row sub-groups of LPR lanes; each lane
-// covers CPL chunks of VEC floats of the row.  Copy index = warp*RPW + sub.
-// Within a copy the cluster sums are stored "chunk-transposed" (element l at
-// (l%VEC)*nchunks + l/VEC) so that a sub-group's read-modify-writes hit
-// consecutive doubles (bank-conflict free).  U rows per slot are loaded ahead.
-template <bool COS, int VEC, int CPL>
-__global__ void __launch_bounds__(256) agg_private_kernel(
-    const float* __restrict__ X, const int32_t* __restrict__ dense, int64_t n, int d,
-    int64_t row_offset, int k, int lpr, double* __restrict__ partials, int64_t* checks,
-    float* xmax) {
-  constexpr int U = 4;
-  float amax = 0.f;
-  extern __shared__ double sm[];
-  const int S = COS ? k * (d + 1) : k * (d + 2);
-  const int sums_off = COS ? k : 2 * k;
-  const int warps = blockDim.x >> 5;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rpw = 32 / lpr;
-  const int sub = lane / lpr, li = lane % lpr;
-  const int copies = warps * rpw;
-  for (int j = threadIdx.x; j < copies * S; j += blockDim.x) sm[j] = 0.0;
-  __syncthreads();
-  double* my = sm + (warp * rpw + sub) * S;
-  const int64_t G = static_cast<int64_t>(gridDim.x) * copies;
-  const int nchunks = (d + VEC - 1) / VEC;
-  const int64_t wbase = (static_cast<int64_t>(blockIdx.x) * warps + warp) * rpw;
-  for (int64_t base = wbase; base < n; base += U * G) {
-    float v[U][CPL][VEC];
-    int lab[U];
-    bool valid[U];
+// Warp-per-row streaming with the (warp-uniform) label of each row: lanes hold
+// dims l + 32i (i < DPL), and each warp owns private fp64 accumulators in shared
+// memory -- sums[K][D] (a row's read-modify-write touches consecutive doubles:
+// bank-conflict free), per-lane Psi partials [K][32] (sqeuclid) and counts [K].
+// U rows per warp are prefetched (labels through lanes 0..U-1).  Cosine row norms
+// for the U rows are formed with a transpose-reduce across the warp (fp64).
+// Rows are assigned warp-interleaved in a fixed pattern and every reduction is in
+// a fixed order: bit-identical results run to run.
+template <bool COS, int DPL>
+__device__ __forceinline__ void agg_warp_rows(const float* __restrict__ X, const int32_t* __restrict__ dense,
+                                              int64_t n, int d, int64_t row_offset, int64_t base, int64_t GW,
+                                              bool checked, double* wsum, double* wpsi, double* wcnt,
+                                              int64_t* checks, float& amax) {
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31;
+  const int64_t rl = base + (lane & (U - 1)) * GW;
+  const int lab_l = (lane < U && (!checked || rl < n)) ? __ldg(dense + rl) : 0;
+  float v[U][DPL];
+  {
+    const int64_t stride = GW * static_cast<int64_t>(d);
+    const float* ptr = X + base * d + lane;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t r = base + sub + u * G;
-      valid[u] = r < n;
-      lab[u] = valid[u] ? __ldg(dense + r) : 0;
+    for (int u = 0; u < U; ++u, ptr += stride) {
+      const bool rv = !checked || base + u * GW < n;
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        const int ch = li + c * lpr;
-        if constexpr (VEC == 4) {
-          float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (valid[u] && ch < nchunks) t = ldg_stream(reinterpret_cast<const float4*>(X + r * d) + ch);
-          v[u][c][0] = t.x; v[u][c][1] = t.y; v[u][c][2] = t.z; v[u][c][3] = t.w;
-        } else {
-          v[u][c][0] = (valid[u] && ch < nchunks) ? __ldg(X + r * d + ch) : 0.f;
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t r = base + sub + u * G;
-      double ss = 0.0;
-      bool finite = true;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c)
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const double x = v[u][c][e];
-          ss = fma(x, x, ss);
-          finite = finite && isfinite(v[u][c][e]);
-          amax = fmaxf(amax, fabsf(v[u][c][e]));
-        }
-      if (!finite) {
-#pragma unroll
-        for (int c = 0; c < CPL; ++c)
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            const int l = (li + c * lpr) * VEC + e;
-            if (l < d && !isfinite(v[u][c][e])) atomic_min_i64(checks, (row_offset + r) * d + l);
-          }
-      }
-      for (int off = lpr >> 1; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off, lpr);
-      if (!valid[u]) continue;
-      double scale = 1.0;
-      if (COS) {
-        if (ss == 0.0) {
-          if (li == 0) atomic_min_i64(checks + 1, row_offset + r);
-          continue;
-        }
-        scale = 1.0 / sqrt(ss);
-      }
-      if (li == 0) {
-        my[lab[u]] += 1.0;
-        if (!COS) my[k + lab[u]] += ss;
-      }
-      double* ys = my + sums_off + static_cast<int64_t>(lab[u]) * d;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        const int ch = li + c * lpr;
-        if (ch < nchunks) {
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            const double x = COS ? static_cast<double>(v[u][c][e]) * scale : static_cast<double>(v[u][c][e]);
-            ys[e * nchunks + ch] += x;
-          }
-        }
-      }
+      for (int i = 0; i < DPL; ++i)
+        v[u][i] = (rv && (!checked || lane + 32 * i < d)) ? __ldcs(ptr + 32 * i) : 0.f;
     }
   }
+  double ss[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    ss[u] = 0.0;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+      const double x = v[u][i];
+      ss[u] = fma(x, x, ss[u]);
+      amax = fmaxf(amax, fabsf(v[u][i]));
+    }
+  }
+  double inv[U];
+  if (COS) {
+    // transpose-reduce: after three exchange steps lane L holds the partial of row
+    // bit2(L) + 2*bit3(L) + 4*bit4(L) over 8 lanes; two xor steps finish all 32.
+    double a4[4], a2[2], a1;
+    const bool hi16 = lane & 16, hi8 = lane & 8, hi4 = lane & 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      a4[q] = (hi16 ? ss[q + 4] : ss[q]) + __shfl_xor_sync(0xffffffffu, hi16 ? ss[q] : ss[q + 4], 16);
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      a2[q] = (hi8 ? a4[q + 2] : a4[q]) + __shfl_xor_sync(0xffffffffu, hi8 ? a4[q] : a4[q + 2], 8);
+    a1 = (hi4 ? a2[1] : a2[0]) + __shfl_xor_sync(0xffffffffu, hi4 ? a2[0] : a2[1], 4);
+    a1 += __shfl_xor_sync(0xffffffffu, a1, 2);
+    a1 += __shfl_xor_sync(0xffffffffu, a1, 1);
+    // 1/||x||; 0 marks a zero row, NaN a non-finite one
+    const double mine = a1 > 0.0 ? (a1 < INFINITY ? 1.0 / sqrt(a1) : NAN) : (a1 == 0.0 ? 0.0 : NAN);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      inv[u] = __shfl_sync(0xffffffffu, mine, (((u >> 2) & 1) << 4) | (((u >> 1) & 1) << 3) | ((u & 1) << 2));
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t r = base + u * GW;
+    if (checked && r >= n) break;  // warp-uniform
+    const int lab = __shfl_sync(0xffffffffu, lab_l, u);
+    const bool bad = COS ? !(inv[u] == inv[u]) : __any_sync(0xffffffffu, !isfinite(ss[u]));
+    if (bad) {  // rare: locate the non-finite element (dataset.cpp:35-37)
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) {
+        const int l = lane + 32 * i;
+        if (l < d && !isfinite(v[u][i])) atomic_min_i64(checks, (row_offset + r) * d + l);
+      }
+    }
+    if (COS && inv[u] == 0.0) {  // zero row (cos.cpp:119-123): reported, not accumulated
+      if (lane == 0) atomic_min_i64(checks + 1, row_offset + r);
+      continue;
+    }
+    double* ys = wsum + static_cast<int64_t>(lab) * d + lane;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+      if (!checked || lane + 32 * i < d)
+        ys[32 * i] = COS ? fma(static_cast<double>(v[u][i]), inv[u], ys[32 * i]) : ys[32 * i] + static_cast<double>(v[u][i]);
+    }
+    if (!COS) wpsi[lab * 32 + lane] += ss[u];
+    if (lane == 0) wcnt[lab] += 1.0;
+  }
+}
+
+template <bool COS, int DPL>
+__global__ void __launch_bounds__(256) agg_warp_kernel(
+    const float* __restrict__ X, const int32_t* __restrict__ dense, int64_t n, int d,
+    int64_t row_offset, int k, double* __restrict__ partials, int64_t* checks, float* xmax) {
+  constexpr int U = 8;
+  extern __shared__ double sm[];
+  const int warps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Sw = k * d + (COS ? 0 : k * 32) + k;  // per-warp doubles
+  for (int j = threadIdx.x; j < warps * Sw; j += blockDim.x) sm[j] = 0.0;
+  __syncthreads();
+  double* wsum = sm + warp * Sw;                      // [k][d]
+  double* wpsi = wsum + static_cast<int64_t>(k) * d;  // [k][32] (sqeuclid)
+  double* wcnt = wpsi + (COS ? 0 : k * 32);           // [k]
+  const int64_t GW = static_cast<int64_t>(gridDim.x) * warps;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * warps + warp;
+  const bool full_d = d == 32 * DPL;
+  float amax = 0.f;
+  int64_t base = gw;
+  if (full_d)  // unchecked fast path over complete groups of U rows
+    for (; base + (U - 1) * GW < n; base += U * GW)
+      agg_warp_rows<COS, DPL>(X, dense, n, d, row_offset, base, GW, false, wsum, wpsi, wcnt, checks, amax);
+  for (; base < n; base += U * GW)
+    agg_warp_rows<COS, DPL>(X, dense, n, d, row_offset, base, GW, true, wsum, wpsi, wcnt, checks, amax);
   for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
   if (lane == 0 && amax > 0.f) atomic_max_nonneg_f32(xmax, amax);
   __syncthreads();
+  // fold warps (fixed order) into the block partial in StatsLayout order
+  const int S = COS ? k * (d + 1) : k * (d + 2);
   for (int j = threadIdx.x; j < S; j += blockDim.x) {
-    int src = j;
-    if (j >= sums_off) {  // undo the chunk transpose
-      const int t = j - sums_off, kk = t / d, l = t % d;
-      src = sums_off + kk * d + (l % VEC) * nchunks + l / VEC;
-    }
     double acc = 0.0;
-    for (int c = 0; c < copies; ++c) acc += sm[c * S + src];
+    if (j < k) {
+      for (int w = 0; w < warps; ++w) acc += sm[w * Sw + (COS ? k * d : k * d + k * 32) + j];
+    } else if (!COS && j < 2 * k) {
+      const int c = j - k;
+      for (int w = 0; w < warps; ++w)
+        for (int l = 0; l < 32; ++l) acc += sm[w * Sw + k * d + c * 32 + l];
+    } else {
+      const int t = j - (COS ? k : 2 * k);
+      for (int w = 0; w < warps; ++w) acc += sm[w * Sw + t];
+    }
+    partials[static_cast<int64_t>(blockIdx.x) * S + j] = acc;
+  }
+}
+
+// Same accumulation as agg_warp_kernel, but X streams HBM -> shared memory with 1-D
+// bulk TMA copies (cp.async.bulk, mbarrier completion) through an NS-stage ring, so
+// the bytes in flight per SM no longer depend on registers.  One CTA per SM owns a
+// contiguous row range; consumer warp w takes rows w, w+W, ... of every stage.
+template <bool COS, int DPL, int NS>
+__global__ void __launch_bounds__(13 * 32, 1) agg_stage_kernel(
+    const float* __restrict__ X, const int32_t* __restrict__ dense, int64_t n, int d,
+    int64_t row_offset, int k, int64_t chunk, double* __restrict__ partials, int64_t* checks,
+    float* xmax) {
+  constexpr int U = 8;
+  extern __shared__ __align__(16) uint8_t smraw[];
+  const int W = (blockDim.x >> 5) - 1;  // consumer warps; warp W is the producer
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int R = U * W;                  // rows per stage
+  const int Sw = k * d + (COS ? 0 : k * 32) + k;
+  double* sm = reinterpret_cast<double*>(smraw);
+  float* ring = reinterpret_cast<float*>(sm + static_cast<size_t>(W) * Sw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(NS) * R * d);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + NS;
+  for (int j = threadIdx.x; j < W * Sw; j += blockDim.x) sm[j] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      sm100::mbar_init(full + i, 1);
+      sm100::mbar_init(empty + i, W);
+    }
+    sm100::fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t r1 = min(n, r0 + chunk);
+  const int nstages = r1 > r0 ? static_cast<int>((r1 - r0 + R - 1) / R) : 0;
+  if (warp == W) {
+    if (lane == 0) {
+      for (int i = 0; i < nstages; ++i) {
+        const int s = i % NS;
+        sm100::mbar_wait(empty + s, ((i / NS) & 1) ^ 1);
+        const int64_t a = r0 + static_cast<int64_t>(i) * R;
+        const int64_t nr = r1 - a < R ? r1 - a : static_cast<int64_t>(R);
+        const uint32_t bytes = static_cast<uint32_t>(nr * d * 4);
+        sm100::mbar_arrive_expect_tx(full + s, bytes);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                sm100::smem_u32(ring + static_cast<size_t>(s) * R * d)),
+            "l"(X + a * d), "r"(bytes), "r"(sm100::smem_u32(full + s))
+            : "memory");
+      }
+    }
+    return;
+  }
+  double* wsum = sm + warp * Sw;
+  double* wpsi = wsum + static_cast<int64_t>(k) * d;
+  int* wcnt = reinterpret_cast<int*>(wpsi + (COS ? 0 : k * 32));  // [k] int counts
+  const bool full_d = d == 32 * DPL;
+  float amax = 0.f;
+  for (int i = 0; i < nstages; ++i) {
+    const int s = i % NS;
+    sm100::mbar_wait(full + s, (i / NS) & 1);
+    const int64_t a = r0 + static_cast<int64_t>(i) * R;
+    const float* st = ring + static_cast<size_t>(s) * R * d;
+    const bool full_stage = full_d && a + R <= r1;
+    const int lab_l = (lane < U && a + lane * W + warp < r1) ? __ldg(dense + a + lane * W + warp) : 0;
+    float v[U][DPL];
+    if (full_stage) {
+      const float* sp = st + warp * d + lane;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < DPL; ++q) v[u][q] = sp[u * W * d + 32 * q];
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int lr = u * W + warp;
+        const bool rv = a + lr < r1;
+#pragma unroll
+        for (int q = 0; q < DPL; ++q) {
+          const int l = lane + 32 * q;
+          v[u][q] = (rv && l < d) ? st[lr * d + l] : 0.f;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) sm100::mbar_arrive(empty + s);  // stage consumed into registers
+    double ss[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ss[u] = 0.0;
+#pragma unroll
+      for (int q = 0; q < DPL; ++q) {
+        const double x = v[u][q];
+        ss[u] = fma(x, x, ss[u]);
+        amax = fmaxf(amax, fabsf(v[u][q]));
+      }
+    }
+    double inv[U];
+    bool odd = false;  // any non-finite or (cosine) zero row in this group
+    if (COS) {
+      double a4[4], a2[2], a1;
+      const bool hi16 = lane & 16, hi8 = lane & 8, hi4 = lane & 4;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        a4[q] = (hi16 ? ss[q + 4] : ss[q]) + __shfl_xor_sync(0xffffffffu, hi16 ? ss[q] : ss[q + 4], 16);
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        a2[q] = (hi8 ? a4[q + 2] : a4[q]) + __shfl_xor_sync(0xffffffffu, hi8 ? a4[q] : a4[q + 2], 8);
+      a1 = (hi4 ? a2[1] : a2[0]) + __shfl_xor_sync(0xffffffffu, hi4 ? a2[0] : a2[1], 4);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, 2);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, 1);
+      const bool ok = a1 > 0.0 && a1 < INFINITY;
+      const double mine = ok ? 1.0 / sqrt(a1) : 0.0;
+      odd = __any_sync(0xffffffffu, !ok);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        inv[u] = __shfl_sync(0xffffffffu, mine, (((u >> 2) & 1) << 4) | (((u >> 1) & 1) << 3) | ((u & 1) << 2));
+    } else {
+      bool bad = false;
+#pragma unroll
+      for (int u = 0; u < U; ++u) bad = bad || !isfinite(ss[u]);
+      odd = __any_sync(0xffffffffu, bad);
+    }
+    if (full_stage && !odd) {
+      // ---- fast path: 8 valid rows, no checks
+      if (lane < U) atomicAdd(wcnt + lab_l, 1);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int lab = __shfl_sync(0xffffffffu, lab_l, u);
+        double* ys = wsum + lab * d + lane;
+#pragma unroll
+        for (int q = 0; q < DPL; ++q)
+          ys[32 * q] = COS ? fma(static_cast<double>(v[u][q]), inv[u], ys[32 * q]) : ys[32 * q] + static_cast<double>(v[u][q]);
+        if (!COS) wpsi[lab * 32 + lane] += ss[u];
+      }
+      continue;
+    }
+    // ---- general path (partial stage, non-finite or zero rows)
+    double tot[U];
+    if (COS) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) tot[u] = inv[u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = a + u * W + warp;
+      if (r >= r1) break;  // warp-uniform
+      const int lab = __shfl_sync(0xffffffffu, lab_l, u);
+      double rs = ss[u];
+      if (COS) {
+        for (int off = 16; off > 0; off >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, off);
+      }
+      const bool bad = __any_sync(0xffffffffu, !isfinite(COS ? rs : ss[u]));
+      if (bad) {  // locate the non-finite element (dataset.cpp:35-37)
+#pragma unroll
+        for (int q = 0; q < DPL; ++q) {
+          const int l = lane + 32 * q;
+          if (l < d && !isfinite(v[u][q])) atomic_min_i64(checks, (row_offset + r) * d + l);
+        }
+      }
+      if (COS && rs == 0.0) {  // zero row (cos.cpp:119-123): reported, not accumulated
+        if (lane == 0) atomic_min_i64(checks + 1, row_offset + r);
+        continue;
+      }
+      const double sc = COS ? (isfinite(rs) ? 1.0 / sqrt(rs) : 0.0) : 1.0;
+      double* ys = wsum + lab * d + lane;
+#pragma unroll
+      for (int q = 0; q < DPL; ++q)
+        if (lane + 32 * q < d)
+          ys[32 * q] = COS ? fma(static_cast<double>(v[u][q]), sc, ys[32 * q]) : ys[32 * q] + static_cast<double>(v[u][q]);
+      if (!COS) wpsi[lab * 32 + lane] += ss[u];
+      if (lane == 0) atomicAdd(wcnt + lab, 1);
+    }
+    (void)tot;
+  }
+  for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  if (lane == 0 && amax > 0.f) atomic_max_nonneg_f32(xmax, amax);
+  // named barrier over the W consumer warps (the producer has returned)
+  asm volatile("bar.sync 1, %0;\n" ::"r"(W * 32) : "memory");
+  const int S = COS ? k * (d + 1) : k * (d + 2);
+  for (int j = threadIdx.x; j < S; j += W * 32) {
+    double acc = 0.0;
+    if (j < k) {
+      for (int w = 0; w < W; ++w)
+        acc += static_cast<double>(reinterpret_cast<const int*>(sm + w * Sw + (COS ? k * d : k * d + k * 32))[j]);
+    } else if (!COS && j < 2 * k) {
+      const int c = j - k;
+      for (int w = 0; w < W; ++w)
+        for (int l = 0; l < 32; ++l) acc += sm[w * Sw + k * d + c * 32 + l];
+    } else {
+      const int t = j - (COS ? k : 2 * k);
+      for (int w = 0; w < W; ++w) acc += sm[w * Sw + t];
+    }
     partials[static_cast<int64_t>(blockIdx.x) * S + j] = acc;
   }
 }
@@ -360,22 +576,39 @@ int pick_lpr(int d, int vec) {
 }
 
 template <bool COS>
-void launch_private(fsil_context* c, int vec, int cpl, int grid, int threads, int lpr,
-                    size_t smem, double* partials, int64_t* checks) {
-#define FSIL_AGG_PRIV(V, C)                                                                      \
-  if (vec == V && cpl == C) {                                                                    \
-    auto kern = agg_private_kernel<COS, V, C>;                                                   \
+void launch_stage(fsil_context* c, int dpl, int warps, int64_t chunk, size_t smem, double* partials,
+                  int64_t* checks) {
+#define FSIL_AGG_STAGE(P)                                                                        \
+  if (dpl == P) {                                                                                \
+    auto kern = agg_stage_kernel<COS, P, 3>;                                                     \
     FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    kern<<<grid, threads, smem, c->stream>>>(c->X, c->dense.as<int32_t>(), c->n, c->d,          \
-                                             c->row_offset, c->k, lpr, partials, checks,         \
+    kern<<<c->num_sms, (warps + 1) * 32, smem, c->stream>>>(c->X, c->dense.as<int32_t>(), c->n, c->d, \
+                                             c->row_offset, c->k, chunk, partials, checks,       \
                                              c->xmax.as<float>());                               \
     FSIL_LAUNCHED(c);                                                                            \
     return;                                                                                      \
   }
-  FSIL_AGG_PRIV(4, 1) FSIL_AGG_PRIV(4, 2) FSIL_AGG_PRIV(4, 4)
-  FSIL_AGG_PRIV(1, 1) FSIL_AGG_PRIV(1, 2) FSIL_AGG_PRIV(1, 4)
-#undef FSIL_AGG_PRIV
-  fail(FSIL_ERR_INTERNAL, "no private aggregation kernel for this shape");
+  FSIL_AGG_STAGE(1) FSIL_AGG_STAGE(2) FSIL_AGG_STAGE(3) FSIL_AGG_STAGE(4)
+#undef FSIL_AGG_STAGE
+  fail(FSIL_ERR_INTERNAL, "no staged aggregation kernel for this shape");
+}
+
+template <bool COS>
+void launch_warp(fsil_context* c, int dpl, int grid, int threads, size_t smem, double* partials,
+                 int64_t* checks) {
+#define FSIL_AGG_WARP(P)                                                                         \
+  if (dpl == P) {                                                                                \
+    auto kern = agg_warp_kernel<COS, P>;                                                         \
+    FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    kern<<<grid, threads, smem, c->stream>>>(c->X, c->dense.as<int32_t>(), c->n, c->d,          \
+                                             c->row_offset, c->k, partials, checks,              \
+                                             c->xmax.as<float>());                               \
+    FSIL_LAUNCHED(c);                                                                            \
+    return;                                                                                      \
+  }
+  FSIL_AGG_WARP(1) FSIL_AGG_WARP(2) FSIL_AGG_WARP(3) FSIL_AGG_WARP(4)
+#undef FSIL_AGG_WARP
+  fail(FSIL_ERR_INTERNAL, "no warp aggregation kernel for this shape");
 }
 
 template <bool COS>
@@ -421,32 +654,45 @@ void aggregate(fsil_context* c) {
   const int lpr = pick_lpr(c->d, vec);
   const int chunks = (c->d + vec - 1) / vec;
   const int cpl = (chunks + lpr - 1) / lpr;
-  const int rpw = 32 / lpr;
 
-  // Path 1: warp-private shared-memory copies; needs >= 8 resident warps/SM.
+  // Path 1: warp-per-row with warp-private shared-memory accumulators, when at
+  // least 8 such warps fit per SM (small K*D: C1, C2).
   const size_t budget = c->smem_optin ? c->smem_optin : 227 * 1024;
+  const int dpl = (c->d + 31) / 32;
+  const size_t per_warp = (static_cast<size_t>(c->k) * c->d + (cos ? 0 : c->k * 32) + c->k) * sizeof(double);
   int warps = 8;
-  size_t smem = 0;
-  for (; warps >= 1; warps >>= 1) {
-    smem = static_cast<size_t>(warps) * rpw * S * sizeof(double);
-    if (smem <= budget) break;
+  while (warps > 1 && warps * per_warp > budget) warps >>= 1;
+  const size_t smem = warps * per_warp;
+  const int blocks_per_sm = smem > 0 ? static_cast<int>(std::min<size_t>(228 * 1024 / (smem + 1024), 64 / warps)) : 0;
+  // Path 1a: bulk-TMA staged (needs 16-byte rows); one CTA per SM.
+  if (dpl <= 4 && c->d % 4 == 0) {
+    int W = 12;
+    auto need = [&](int w) { return w * per_warp + 3ull * 8 * w * c->d * 4 + 64 + 16; };
+    while (W > 4 && need(W) > budget) W -= 4;
+    if (need(W) <= budget && W >= 4) {
+      c->agg_path = 1;
+      const int64_t R = 8 * W;
+      int64_t chunk = (c->n + c->num_sms - 1) / c->num_sms;
+      chunk = (chunk + R - 1) / R * R;
+      const int grid = c->num_sms;
+      c->partials.ensure(static_cast<size_t>(grid) * S * sizeof(double));
+      if (cos) launch_stage<true>(c, dpl, W, chunk, need(W), c->partials.as<double>(), checks);
+      else launch_stage<false>(c, dpl, W, chunk, need(W), c->partials.as<double>(), checks);
+      fold_partials_kernel<<<static_cast<unsigned>((S + 31) / 32), 256, 0, c->stream>>>(
+          c->partials.as<double>(), grid, S, stats);
+      FSIL_LAUNCHED(c);
+      return;
+    }
   }
-  const int blocks_per_sm = warps >= 1 && smem > 0 ? static_cast<int>(budget / smem) : 0;
-  const bool private_ok = warps >= 1 && cpl <= 4 && blocks_per_sm >= 1 &&
-                          warps * std::min(blocks_per_sm, 8) >= 8;
-  if (private_ok) {
+  if (dpl <= 4 && smem <= budget && warps * blocks_per_sm >= 8) {
     c->agg_path = 1;
-    const int per_sm = std::min(blocks_per_sm, 64 / warps);
-    const int64_t rows_per_block = static_cast<int64_t>(warps) * rpw * 8;
+    const int64_t rows_per_block = static_cast<int64_t>(warps) * 8 * 4;
     const int grid = static_cast<int>(std::max<int64_t>(
         1, std::min<int64_t>((c->n + rows_per_block - 1) / rows_per_block,
-                             static_cast<int64_t>(c->num_sms) * per_sm)));
+                             static_cast<int64_t>(c->num_sms) * blocks_per_sm)));
     c->partials.ensure(static_cast<size_t>(grid) * S * sizeof(double));
-    const int cpl_t = cpl <= 1 ? 1 : cpl <= 2 ? 2 : 4;
-    if (cos)
-      launch_private<true>(c, vec, cpl_t, grid, warps * 32, lpr, smem, c->partials.as<double>(), checks);
-    else
-      launch_private<false>(c, vec, cpl_t, grid, warps * 32, lpr, smem, c->partials.as<double>(), checks);
+    if (cos) launch_warp<true>(c, dpl, grid, warps * 32, smem, c->partials.as<double>(), checks);
+    else launch_warp<false>(c, dpl, grid, warps * 32, smem, c->partials.as<double>(), checks);
     fold_partials_kernel<<<static_cast<unsigned>((S + 31) / 32), 256, 0, c->stream>>>(
         c->partials.as<double>(), grid, S, stats);
     FSIL_LAUNCHED(c);

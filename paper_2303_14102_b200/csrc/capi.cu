@@ -136,8 +136,11 @@ void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, 
   int use = c->path;
   const bool tc_ok = tc_supported(c), ffma_ok = ffma_supported(c);
   if (use == FSIL_PATH_AUTO) {
-    if (c->k <= 32 && ffma_ok) use = FSIL_PATH_FFMA;
-    else if (tc_ok) use = FSIL_PATH_TCGEN05;
+    // Measured crossover (profiles/): the tcgen05 kernel wins once the contraction
+    // has ~2e7 row-cluster pairs (C2: 116 us vs 207 us FFMA); below that its fixed
+    // costs (operand prep, one scale readback) dominate and FFMA wins (C1).
+    const double pairs = static_cast<double>(c->n) * c->k;
+    if (tc_ok && (pairs >= 1.5e7 || !ffma_ok || c->k > 32)) use = FSIL_PATH_TCGEN05;
     else if (ffma_ok) use = FSIL_PATH_FFMA;
     else use = FSIL_PATH_FP64;
   }

@@ -6,8 +6,6 @@
 // (label, min row) into a global open-addressing table; the host orders the
 // (few) distinct labels by first row -- merging across ranks first in the
 // sharded protocol -- and pass 2 maps every row to its dense id.
-#include <cub/device/device_radix_sort.cuh>
-
 #include <algorithm>
 #include <vector>
 
@@ -141,6 +139,59 @@ __global__ void densify_assign_sorted_kernel(const unsigned long long* __restric
   if (slot >= 0) gdense[slot] = static_cast<int32_t>(j);
 }
 
+__global__ void densify_init_kernel(unsigned long long* keys, uint32_t* vals, int32_t* gdense,
+                                    int64_t* dict_rows, uint32_t cap, int* counters) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cap) {
+    keys[i] = 0;
+    vals[i] = 0xffffffffu;
+    gdense[i] = -1;
+    dict_rows[i] = INT64_MAX;
+  }
+  if (i < 16) counters[i] = 0;
+}
+
+// Compaction that also records each entry's hash slot.
+__global__ void densify_compact_slot_kernel(const unsigned long long* __restrict__ gkeys,
+                                            const uint32_t* __restrict__ gvals, uint32_t cap,
+                                            int32_t* out_labels, int64_t* out_rows, int32_t* out_slot,
+                                            unsigned long long* count) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cap) return;
+  const unsigned long long key = gkeys[i];
+  if (key == 0) return;
+  const unsigned long long j = atomicAdd(count, 1ull);
+  out_labels[j] = static_cast<int32_t>(static_cast<uint32_t>(key));
+  out_rows[j] = static_cast<int64_t>(gvals[i]);
+  out_slot[j] = static_cast<int32_t>(i);
+}
+
+// Dense id = rank of the entry's first row among all distinct labels (first rows
+// are unique); writes the dense order and the per-slot dense id in one pass.
+__global__ void __launch_bounds__(256) densify_rank_kernel(const int32_t* __restrict__ labels,
+                                                           const int64_t* __restrict__ rows,
+                                                           const int32_t* __restrict__ slots,
+                                                           const unsigned long long* count,
+                                                           int32_t* sorted_labels, int32_t* gdense) {
+  __shared__ int64_t tile[1024];
+  const int64_t cnt = static_cast<int64_t>(*count);
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (static_cast<int64_t>(blockIdx.x) * blockDim.x >= cnt) return;  // block-uniform
+  const int64_t my = i < cnt ? rows[i] : INT64_MAX;
+  int64_t rank = 0;
+  for (int64_t b = 0; b < cnt; b += 1024) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < 1024; t += blockDim.x) tile[t] = b + t < cnt ? rows[b + t] : INT64_MAX;
+    __syncthreads();
+    const int lim = static_cast<int>(cnt - b < 1024 ? cnt - b : 1024);
+    for (int t = 0; t < lim; ++t) rank += tile[t] < my;
+  }
+  if (i < cnt) {
+    sorted_labels[rank] = labels[i];
+    gdense[slots[i]] = static_cast<int32_t>(rank);
+  }
+}
+
 int grid_for(int64_t n, int threads, int num_sms, int per_sm) {
   const int64_t want = (n + threads - 1) / threads;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(num_sms) * per_sm)));
@@ -191,8 +242,8 @@ void densify_collect(fsil_context* c) {
   }
 }
 
-// Single-GPU densify with one host sync: collect -> compact -> device sort of the
-// dictionary by first row -> dense ids -> per-row map; then read K.
+// Single-GPU densify with one host sync: init -> collect -> compact -> rank by first
+// row (dense order) + per-slot dense ids -> per-row map; then read K and overflow.
 void densify_local(fsil_context* c) {
   if (c->n >= (int64_t(1) << 31) - 1)
     fail(FSIL_ERR_INVALID_ARGUMENT, "too many rows for one device call (2^31-2)");
@@ -204,40 +255,29 @@ void densify_local(fsil_context* c) {
     c->ht_dense.ensure(cap * sizeof(int32_t));
     c->dict_labels.ensure(cap * sizeof(int32_t));
     c->dict_rows.ensure(cap * sizeof(int64_t));
-    c->dict_sorted.ensure(cap * (sizeof(int32_t) + sizeof(int64_t)));
+    c->dict_sorted.ensure(cap * (2 * sizeof(int32_t)));
     c->dense.ensure(std::max<int64_t>(c->n, 1) * sizeof(int32_t));
-    FSIL_CUDA(cudaMemsetAsync(c->ht_keys.p, 0, cap * sizeof(unsigned long long), c->stream));
-    FSIL_CUDA(cudaMemsetAsync(c->ht_vals.p, 0xff, cap * sizeof(uint32_t), c->stream));
-    FSIL_CUDA(cudaMemsetAsync(c->ht_dense.p, 0xff, cap * sizeof(int32_t), c->stream));
-    FSIL_CUDA(cudaMemsetAsync(c->dict_rows.p, 0x7f, cap * sizeof(int64_t), c->stream));
-    FSIL_CUDA(cudaMemsetAsync(c->counters.p, 0, 64, c->stream));
     int* overflow = c->counters.as<int>();
     int* missing = c->counters.as<int>() + 4;
     unsigned long long* count = reinterpret_cast<unsigned long long*>(c->counters.as<char>() + 8);
     const uint32_t mask = static_cast<uint32_t>(cap - 1);
-    densify_collect_kernel<<<grid_for(c->n, 256, c->num_sms, 4), 256, 0, c->stream>>>(
+    int32_t* slots = reinterpret_cast<int32_t*>(c->dict_sorted.p);
+    int32_t* sorted_labels = slots + cap;
+    densify_init_kernel<<<static_cast<unsigned>((cap + 255) / 256), 256, 0, c->stream>>>(
+        c->ht_keys.as<unsigned long long>(), c->ht_vals.as<uint32_t>(), c->ht_dense.as<int32_t>(),
+        c->dict_rows.as<int64_t>(), static_cast<uint32_t>(cap), c->counters.as<int>());
+    FSIL_LAUNCHED(c);
+    densify_collect_kernel<<<grid_for(c->n, 256, c->num_sms, 2), 256, 0, c->stream>>>(
         c->labels, c->n, c->ht_keys.as<unsigned long long>(), c->ht_vals.as<uint32_t>(), mask,
         overflow);
     FSIL_LAUNCHED(c);
-    densify_compact_kernel<<<static_cast<unsigned>((cap + 255) / 256), 256, 0, c->stream>>>(
+    densify_compact_slot_kernel<<<static_cast<unsigned>((cap + 255) / 256), 256, 0, c->stream>>>(
         c->ht_keys.as<unsigned long long>(), c->ht_vals.as<uint32_t>(), static_cast<uint32_t>(cap),
-        0, c->dict_labels.as<int32_t>(), c->dict_rows.as<int64_t>(), count);
+        c->dict_labels.as<int32_t>(), c->dict_rows.as<int64_t>(), slots, count);
     FSIL_LAUNCHED(c);
-    int64_t* sorted_rows = reinterpret_cast<int64_t*>(c->dict_sorted.p);
-    int32_t* sorted_labels = reinterpret_cast<int32_t*>(sorted_rows + cap);
-    int bits = 1;
-    while ((int64_t(1) << bits) < c->n + 1 && bits < 63) ++bits;
-    size_t tmp = 0;
-    FSIL_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, c->dict_rows.as<int64_t>(), sorted_rows,
-                                              c->dict_labels.as<int32_t>(), sorted_labels,
-                                              static_cast<int>(cap), 0, 64, c->stream));
-    c->sort_tmp.ensure(tmp);
-    FSIL_CUDA(cub::DeviceRadixSort::SortPairs(c->sort_tmp.p, tmp, c->dict_rows.as<int64_t>(), sorted_rows,
-                                              c->dict_labels.as<int32_t>(), sorted_labels,
-                                              static_cast<int>(cap), 0, 64, c->stream));
-    c->launches += 4;
-    densify_assign_sorted_kernel<<<static_cast<unsigned>((cap + 255) / 256), 256, 0, c->stream>>>(
-        c->ht_keys.as<unsigned long long>(), mask, sorted_labels, count, c->ht_dense.as<int32_t>());
+    densify_rank_kernel<<<static_cast<unsigned>((cap + 255) / 256), 256, 0, c->stream>>>(
+        c->dict_labels.as<int32_t>(), c->dict_rows.as<int64_t>(), slots, count, sorted_labels,
+        c->ht_dense.as<int32_t>());
     FSIL_LAUNCHED(c);
     densify_map_kernel<<<grid_for(c->n, 256, c->num_sms, 8), 256, 0, c->stream>>>(
         c->labels, c->n, c->ht_keys.as<unsigned long long>(), c->ht_dense.as<int32_t>(), mask,

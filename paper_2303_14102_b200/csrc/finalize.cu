@@ -76,35 +76,39 @@ __global__ void __launch_bounds__(256) refine_kernel(ScoreParams p) {
   }
 }
 
-// Group partials: a block covers 256 tiles; tiles that held refined rows are
-// re-summed from s[] by a whole warp (fixed lane order + xor tree); then a
-// fixed-order tree over the 256 tile values.
+// Group partials: a block covers 32 tiles (one warp per 4 tiles); tiles that held
+// refined rows are re-summed from s[] by the warp (fixed lane order + xor tree);
+// then a fixed-order tree over the 32 tile values.
 __global__ void __launch_bounds__(256) tile_group_kernel(const double* __restrict__ tile_sum,
                                                          const int32_t* __restrict__ tile_flag,
                                                          const double* __restrict__ s,
                                                          int64_t ntiles, int tile_rows, int64_t n,
                                                          double* group_sum) {
-  __shared__ double sm[256];
-  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * 256;
-  const int64_t t = t0 + threadIdx.x;
-  sm[threadIdx.x] = (t < ntiles && !tile_flag[t]) ? tile_sum[t] : 0.0;
-  __syncthreads();
+  __shared__ double sm[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = warp; j < 256; j += 8) {
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * 32;
+  for (int j = warp; j < 32; j += 8) {
     const int64_t tt = t0 + j;
-    if (tt >= ntiles || !tile_flag[tt]) continue;
-    const int64_t r0 = tt * tile_rows, r1 = min(n, r0 + tile_rows);
-    double acc = 0.0;
-    for (int64_t r = r0 + lane; r < r1; r += 32) acc += s[r];
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (lane == 0) sm[j] = acc;
+    double v = 0.0;
+    if (tt < ntiles) {
+      if (tile_flag[tt]) {
+        const int64_t r0 = tt * tile_rows, r1 = min(n, r0 + tile_rows);
+        double acc = 0.0;
+        for (int64_t r = r0 + lane; r < r1; r += 32) acc += s[r];
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        v = acc;
+      } else {
+        v = tile_sum[tt];
+      }
+    }
+    if (lane == 0) sm[j] = v;
   }
   __syncthreads();
-  for (int stride = 128; stride > 0; stride >>= 1) {
-    if (threadIdx.x < stride) sm[threadIdx.x] += sm[threadIdx.x + stride];
-    __syncthreads();
+  if (warp == 0) {
+    double v = sm[lane];
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) group_sum[blockIdx.x] = v;
   }
-  if (threadIdx.x == 0) group_sum[blockIdx.x] = sm[0];
 }
 
 __global__ void __launch_bounds__(1024) total_kernel(const double* __restrict__ group_sum,
@@ -225,7 +229,7 @@ void refine(fsil_context* c, const ScoreParams& p) {
 }
 
 void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows) {
-  const int64_t ngroups = (ntiles + 255) / 256;
+  const int64_t ngroups = (ntiles + 31) / 32;
   c->group_sum.ensure(std::max<int64_t>(ngroups, 1) * sizeof(double));
   c->result.ensure(4 * sizeof(double));
   if (ngroups > 0) {

@@ -33,7 +33,7 @@ constexpr int BM = 128;               // rows per tile = TMEM lanes
 constexpr int BK = 64;                // fp16 K elements per chunk (one 128-byte swizzle row)
 constexpr int kStgBytes = 2 * BM * 128;  // two fp32 boxes of 32 columns
 constexpr int kABytes = BM * 128;        // one fp16 A piece (hi or lo)
-constexpr int kThreads = 320;            // 10 warps
+constexpr int kThreads = 480;            // 15 warps
 constexpr float kTau = 9e-6f;            // certified |ds_i| budget before exact a/b (bar: 1e-5)
 
 __host__ __device__ constexpr int ncb_bn_pad(int kp) { return (kp + 3) & ~3; }
@@ -46,6 +46,7 @@ struct TcParams {
   double smul64;
   const float* colbias;   // [ncb*BN]: sqeuclid p_k, cosine 0, padding +inf
   const float* munorm;    // [ncb*BN]: ||mu_k|| rounded up (per-cluster error bounds)
+  const double4* clu;     // [K]: {n_k, 1/(n_k-1) (0 if singleton), Psi_k, 0}
   float cdot;             // relative dot bound coefficient
   float floor_coef;       // absolute-floor coefficient (times ||x||)
   float mu_max;           // max ||mu_k||
@@ -58,53 +59,71 @@ __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
 
+template <int BN>
+struct TcCfg {
+  static constexpr int kStg = BN <= 32 ? 4 : BN <= 64 ? 3 : 2;  // fp32 X staging stages
+  static constexpr int kOps = 2;                                 // operand (A+B) stages
+  static constexpr int kBBytes = BN * 128;
+  static constexpr int kOpBytes = 2 * kABytes + 2 * kBBytes;
+  static constexpr size_t kRing = static_cast<size_t>(kStg) * kStgBytes + static_cast<size_t>(kOps) * kOpBytes;
+};
+
 template <int BN, bool COS>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
                     const __grid_constant__ CUtensorMap tmap_bl, TcParams tp, int64_t ntiles) {
-  constexpr int kBBytes = BN * 128;
-  // two accumulator buffers x {main hx.hm, correction hx.lm + lx.hm} of BN columns
-  constexpr uint32_t kTmemCols = (4 * BN <= 32) ? 32 : (4 * BN <= 64) ? 64 : (4 * BN <= 128) ? 128 : (4 * BN <= 256) ? 256 : 512;
+  using C = TcCfg<BN>;
+  constexpr int NS = C::kStg, NO = C::kOps;
+  // TS (BN <= 64): the two epilogue groups take alternate tiles, each with its own
+  // pair of accumulator buffers, so consecutive tiles' epilogues overlap.  Otherwise
+  // the groups split the column chunks of every tile.
+  constexpr bool TS = BN <= 64;
+  constexpr int NACC = TS ? 4 : 2;
+  constexpr uint32_t kCols = NACC * 2 * BN;  // x {main, correction}
+  constexpr uint32_t kTmemCols = (kCols <= 32) ? 32 : (kCols <= 64) ? 64 : (kCols <= 128) ? 128 : (kCols <= 256) ? 256 : 512;
   constexpr uint32_t kIdesc = idesc_f16_f32(BM, BN);
   const ScoreParams& p = tp.p;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* stg = base;                                  // [2][kStgBytes]
-  uint8_t* a_hi = stg + 2 * kStgBytes;                  // [2][kABytes]
-  uint8_t* a_lo = a_hi + 2 * kABytes;                   // [2][kABytes]
-  uint8_t* b_hi = a_lo + 2 * kABytes;                   // [2][kBBytes]
-  uint8_t* b_lo = b_hi + 2 * kBBytes;                   // [2][kBBytes]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(b_lo + 2 * kBBytes);
-  uint64_t* stg_full = bars + 0;    // [2]
-  uint64_t* stg_empty = bars + 2;   // [2]
-  uint64_t* op_full = bars + 4;     // [2]
-  uint64_t* op_empty = bars + 6;    // [2]
-  uint64_t* acc_full = bars + 8;    // [2]
-  uint64_t* acc_empty = bars + 10;  // [2]
-  uint64_t* meta_full = bars + 12;  // [2]
-  uint64_t* meta_empty = bars + 14; // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
-  float* meta_xi = reinterpret_cast<float*>(bars + 18);          // [2][BM]
-  double* meta_xi64 = reinterpret_cast<double*>(meta_xi + 2 * BM);  // [2][BM]
-  double* red = meta_xi64 + 2 * BM;                               // [4]
-  int* red_flag = reinterpret_cast<int*>(red + 4);                // [1]
-  float* cb_s = reinterpret_cast<float*>(red + 8);                // [ncb*BN] column bias
+  uint8_t* stg = base;                     // [NS][kStgBytes]
+  uint8_t* ops = stg + NS * kStgBytes;     // [NO][a_hi | a_lo | b_hi | b_lo]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ops + NO * C::kOpBytes);
+  uint64_t* stg_full = bars;               // [NS]
+  uint64_t* stg_empty = bars + 4;          // [NS]
+  uint64_t* op_full = bars + 8;            // [NO]
+  uint64_t* op_empty = bars + 10;          // [NO]
+  uint64_t* acc_full = bars + 12;          // [NACC]
+  uint64_t* acc_empty = bars + 16;         // [NACC]
+  uint64_t* meta_full = bars + 20;         // [2]
+  uint64_t* meta_empty = bars + 22;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+  double* meta_xi = reinterpret_cast<double*>(bars + 26);   // [2][BM] ||x||^2 (fp64 of fp32 blocks)
+  float* part = reinterpret_cast<float*>(meta_xi + 2 * BM);  // [2][4][BM] second-half partial top-2
+  double* red = reinterpret_cast<double*>(part + 8 * BM);     // [2][4] tile-sum partials
+  int* red_flag = reinterpret_cast<int*>(red + 8);            // [2][4]
+  float* cb_s = reinterpret_cast<float*>(red + 12);           // [ncb*BN] column bias
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncb = tp.ncb, nkc = tp.nkc;
   for (int j = threadIdx.x; j < ncb * BN; j += blockDim.x) cb_s[j] = tp.colbias[j];
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(stg_full + i, 1);
       mbar_init(stg_empty + i, 4);
+    }
+    for (int i = 0; i < NO; ++i) {
       mbar_init(op_full + i, 1 + 4);
       mbar_init(op_empty + i, 1);
+    }
+    for (int i = 0; i < NACC; ++i) {
       mbar_init(acc_full + i, 1);
-      mbar_init(acc_empty + i, 4);
+      mbar_init(acc_empty + i, TS ? 4 : 8);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(meta_full + i, 4);
-      mbar_init(meta_empty + i, 4);
+      mbar_init(meta_empty + i, TS ? 4 : 8);
     }
     fence_barrier_init();
     prefetch_tmap(&tmap_x);
@@ -118,24 +137,36 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer: X
     if (lane == 0) {
-      uint32_t n1 = 0, n2 = 0;
+      uint32_t n1 = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int row0 = static_cast<int>(t * BM);
         for (int cb = 0; cb < ncb; ++cb) {
-          for (int kc = 0; kc < nkc; ++kc, ++n1, ++n2) {
-            const int s1 = n1 & 1, s2 = n2 & 1;
-            const uint32_t ph1 = (n1 >> 1) & 1, ph2 = (n2 >> 1) & 1;
+          for (int kc = 0; kc < nkc; ++kc, ++n1) {
+            const int s1 = n1 % NS;
             const int nbox = (kc * BK + 32 < p.d) ? 2 : 1;
-            mbar_wait(stg_empty + s1, ph1 ^ 1);
+            mbar_wait(stg_empty + s1, ((n1 / NS) & 1) ^ 1);
             mbar_arrive_expect_tx(stg_full + s1, nbox * BM * 128);
             for (int b = 0; b < nbox; ++b)
               tma_load_2d(stg + s1 * kStgBytes + b * BM * 128, &tmap_x, stg_full + s1, kc * BK + b * 32, row0);
-            mbar_wait(op_empty + s2, ph2 ^ 1);
-            mbar_arrive_expect_tx(op_full + s2, 2 * kBBytes);
-            tma_load_2d(b_hi + s2 * kBBytes, &tmap_bh, op_full + s2, kc * BK, cb * BN);
-            tma_load_2d(b_lo + s2 * kBBytes, &tmap_bl, op_full + s2, kc * BK, cb * BN);
+          }
+        }
+      }
+    }
+  } else if (warp == 14) {
+    // ------------------------------------------------------------ TMA producer: B pieces
+    if (lane == 0) {
+      uint32_t n2 = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int cb = 0; cb < ncb; ++cb) {
+          for (int kc = 0; kc < nkc; ++kc, ++n2) {
+            const int s2 = n2 % NO;
+            uint8_t* op = ops + s2 * C::kOpBytes;
+            mbar_wait(op_empty + s2, ((n2 / NO) & 1) ^ 1);
+            mbar_arrive_expect_tx(op_full + s2, 2 * C::kBBytes);
+            tma_load_2d(op + 2 * kABytes, &tmap_bh, op_full + s2, kc * BK, cb * BN);
+            tma_load_2d(op + 2 * kABytes + C::kBBytes, &tmap_bl, op_full + s2, kc * BK, cb * BN);
           }
         }
       }
@@ -143,22 +174,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      uint32_t n2 = 0, na = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      uint32_t n2 = 0, na = 0, ng[2] = {0, 0}, nt = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
         for (int cb = 0; cb < ncb; ++cb, ++na) {
-          const int ab = na & 1;
-          const uint32_t pha = (na >> 1) & 1;
-          mbar_wait(acc_empty + ab, pha ^ 1);
+          int ab;
+          uint32_t ph;
+          if (TS) {
+            const int g = nt & 1;
+            ab = 2 * g + (ng[g] & 1);
+            ph = (ng[g] >> 1) & 1;
+            ++ng[g];
+          } else {
+            ab = na & 1;
+            ph = (na >> 1) & 1;
+          }
+          mbar_wait(acc_empty + ab, ph ^ 1);
           tc_fence_after();
           const uint32_t d_main = tmem_base + ab * 2 * BN, d_corr = d_main + BN;
           for (int kc = 0; kc < nkc; ++kc, ++n2) {
-            const int s2 = n2 & 1;
-            mbar_wait(op_full + s2, (n2 >> 1) & 1);
+            const int s2 = n2 % NO;
+            mbar_wait(op_full + s2, (n2 / NO) & 1);
             tc_fence_after();
             const int rem = p.d - kc * BK;
             const int nks = rem >= BK ? 4 : (rem + 15) / 16;
-            const uint32_t ah = smem_u32(a_hi + s2 * kABytes), al = smem_u32(a_lo + s2 * kABytes);
-            const uint32_t bh = smem_u32(b_hi + s2 * kBBytes), bl = smem_u32(b_lo + s2 * kBBytes);
+            const uint32_t ah = smem_u32(ops + s2 * C::kOpBytes), al = ah + kABytes;
+            const uint32_t bh = ah + 2 * kABytes, bl = bh + C::kBBytes;
             for (int ks = 0; ks < nks; ++ks) {
               const uint32_t off = ks * 32;
               const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
@@ -168,28 +208,27 @@ __global__ void __launch_bounds__(kThreads, 1)
               mma_f16(d_corr, desc_k_sw128(ah + off), desc_k_sw128(bl + off), kIdesc, acc0);
               mma_f16(d_corr, desc_k_sw128(al + off), desc_k_sw128(bh + off), kIdesc, 1u);
             }
-            mma_commit(op_empty + s2);  // stage free once these MMAs retire
+            mma_commit(op_empty + s2);  // operand stage free once these MMAs retire
           }
-          mma_commit(acc_full + ab);    // accumulator ready for the epilogue
+          mma_commit(acc_full + ab);    // accumulators ready for the epilogue
         }
       }
     }
-  } else if (warp >= 6) {
+  } else if (warp >= 10 && warp < 14) {
     // ------------------------------------------------------------ converters
-    const int r = threadIdx.x - 6 * 32;  // row in tile, 0..127
+    const int r = threadIdx.x - 10 * 32;  // row in tile, 0..127
     const int sw = r & 7;
     uint32_t n1 = 0, n2 = 0, nt = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
-      float xi32 = 0.f;
-      double xi64 = 0.0;
+      double xi = 0.0;
       for (int cb = 0; cb < ncb; ++cb) {
         for (int kc = 0; kc < nkc; ++kc, ++n1, ++n2) {
-          const int s1 = n1 & 1, s2 = n2 & 1;
-          mbar_wait(stg_full + s1, (n1 >> 1) & 1);
-          mbar_wait(op_empty + s2, ((n2 >> 1) & 1) ^ 1);
+          const int s1 = n1 % NS, s2 = n2 % NO;
+          mbar_wait(stg_full + s1, (n1 / NS) & 1);
+          mbar_wait(op_empty + s2, ((n2 / NO) & 1) ^ 1);
           const uint8_t* srow = stg + s1 * kStgBytes + r * 128;
-          uint8_t* hrow = a_hi + s2 * kABytes + r * 128;
-          uint8_t* lrow = a_lo + s2 * kABytes + r * 128;
+          uint8_t* hrow = ops + s2 * C::kOpBytes + r * 128;
+          uint8_t* lrow = hrow + kABytes;
           const bool two = kc * BK + 32 < p.d;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {  // 8 fp16 A chunks of 16 bytes
@@ -200,12 +239,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               f1 = *reinterpret_cast<const float4*>(box + ((((2 * j + 1) & 7) ^ sw) << 4));
             }
             const float v[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
-            if (cb == 0) {
+            if (cb == 0) {  // ||x||^2: fp32 blocks of 8 (error <= 8u each), fp64 across blocks
+              float bs = 0.f;
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                xi32 = fmaf(v[e], v[e], xi32);
-                xi64 = fma(static_cast<double>(v[e]), static_cast<double>(v[e]), xi64);
-              }
+              for (int e = 0; e < 8; ++e) bs = fmaf(v[e], v[e], bs);
+              xi += static_cast<double>(bs);
             }
             uint32_t hw[4], lw[4];
 #pragma unroll
@@ -231,44 +269,54 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (cb == 0) {
           const int tb = nt & 1;
           mbar_wait(meta_empty + tb, ((nt >> 1) & 1) ^ 1);
-          meta_xi[tb * BM + r] = xi32;
-          meta_xi64[tb * BM + r] = xi64;
+          meta_xi[tb * BM + r] = xi;
           __syncwarp();
           if (lane == 0) mbar_arrive(meta_full + tb);
         }
       }
     }
   } else if (warp >= 2) {
-    // ------------------------------------------------------------ epilogue
+    // ------------------------------------------------------------ epilogue (8 warps)
     const int quad = warp & 3;        // TMEM lane quadrant of this warp
     const int r = quad * 32 + lane;   // row in tile
-    const int ew = warp - 2;          // epilogue warp 0..3
-    uint32_t na = 0, nt = 0;
+    const int grp = (warp - 2) >> 2;  // epilogue group 0 / 1
+    uint32_t na = 0, nt = 0, ng = 0;
+    constexpr int NQ = BN / 32;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
+      const int tb = nt & 1;
+      if (TS && tb != grp) continue;  // the other group takes this tile
       const int64_t row = t * BM + r;
       const bool valid = row < p.n;
       const int own = valid ? p.dense[row] : -1;
-      const int tb = nt & 1;
       mbar_wait(meta_full + tb, (nt >> 1) & 1);
-      const float xi = meta_xi[tb * BM + r];
-      const double xi64 = meta_xi64[tb * BM + r];
+      const double xi64 = meta_xi[tb * BM + r];
+      const float xi = static_cast<float>(xi64);
       const float xn = sqrtf(xi);
-      const float rowc = COS ? 1.0f : xi;                         // row term of m
-      const float rowm = COS ? -(tp.smul / xn) : -2.0f * tp.smul;  // acc multiplier
-      float b1 = INFINITY, b2 = INFINITY, dotb = 0.f, doto = 0.f;
+      // ranking key m' = m - rowc (row constant dropped, no clamp): sqeuclid
+      // m = xi + p_k - 2 dot, cosine m = 1 - dot/||x||; dot = acc * smul
+      const float rowm = COS ? -(tp.smul / xn) : -2.0f * tp.smul;
+      float b1 = INFINITY, b2 = INFINITY, doto = NAN;
       int arg = -1;
-      for (int cb = 0; cb < ncb; ++cb, ++na) {
-        const int ab = na & 1;
-        mbar_wait(acc_full + ab, (na >> 1) & 1);
+      for (int cb = 0; cb < ncb; ++cb) {
+        int ab;
+        uint32_t ph;
+        if (TS) {
+          ab = 2 * grp + (ng & 1);
+          ph = (ng >> 1) & 1;
+          ++ng;
+        } else {
+          ab = na & 1;
+          ph = (na >> 1) & 1;
+          ++na;
+        }
+        mbar_wait(acc_full + ab, ph);
         tc_fence_after();
 #pragma unroll 1
-        for (int q = 0; q < BN / 32; ++q) {
+        for (int q = TS ? 0 : grp; q < NQ; q += TS ? 1 : 2) {
           float v[32], w[32];
           const uint32_t ta = tmem_base + ab * 2 * BN + q * 32 + (static_cast<uint32_t>(quad * 32) << 16);
           tmem_ld32(ta, v);
           tmem_ld32(ta + BN, w);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] += w[j];
           const int k0 = cb * BN + q * 32;
           const float4* cb4 = reinterpret_cast<const float4*>(cb_s + k0);
 #pragma unroll
@@ -279,17 +327,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int e = 0; e < 4; ++e) {
               const int j = 4 * j4 + e;
               const int k = k0 + j;
-              // clamped mean (sqE.cpp:81, cos.cpp:87); padding columns carry +inf bias.
-              // Branch-free top-2 (strict <: the lowest index keeps ties).
-              float m;
-              if (COS) m = fminf(fmaxf(fmaf(v[j], rowm, rowc), 0.f), 2.f) + bj[e];
-              else m = fmaxf(fmaf(v[j], rowm, rowc + bj[e]), 0.f);
+              const float acc = v[j] + w[j];
+              float m = fmaf(acc, rowm, bj[e]);
               const bool is_own = k == own;
-              doto = is_own ? v[j] : doto;
+              doto = is_own ? acc : doto;
               m = is_own ? INFINITY : m;
-              const bool lt = m < b1;
+              const bool lt = m < b1;  // strict: the lowest index keeps ties
               arg = lt ? k : arg;
-              dotb = lt ? v[j] : dotb;
               b2 = fminf(b2, fmaxf(b1, m));
               b1 = fminf(b1, m);
             }
@@ -299,42 +343,79 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + ab);
       }
+      if (!TS) {
+        // ---- merge the two column halves (group 1 -> smem -> group 0)
+        float* pt = part + tb * 4 * BM;  // double-buffered by tile parity
+        if (grp == 1) {
+          pt[0 * BM + r] = b1;
+          pt[1 * BM + r] = b2;
+          pt[2 * BM + r] = __int_as_float(arg);
+          pt[3 * BM + r] = doto;
+        }
+        named_bar(1, 256);
+        if (grp == 1) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(meta_empty + tb);
+          continue;
+        }
+        const float c1 = pt[0 * BM + r], c2 = pt[1 * BM + r];
+        const int a2 = __float_as_int(pt[2 * BM + r]);
+        const float d2 = pt[3 * BM + r];
+        const float nb1 = fminf(b1, c1);
+        b2 = fminf(fminf(fmaxf(b1, c1), b2), c2);
+        arg = (c1 < b1 || (c1 == b1 && a2 >= 0 && (arg < 0 || a2 < arg))) ? a2 : arg;
+        b1 = nb1;
+        doto = (doto == doto) ? doto : d2;
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(meta_empty + tb);
 
-      // ---- certification and a_i, b_i, s_i from the tensor-core dots
+      // ---- certification and a_i, b_i, s_i (no fp64 divisions: per-cluster
+      // reciprocals precomputed, 1/||x|| and 1/max(a,b) by Newton steps in fp64)
       double s = 0.0;
       bool any = false;
       if (valid) {
-        const float eps_dot = tp.cdot * xn * tp.mu_max + tp.floor_coef * xn;  // any column
-        const float eps_m = COS ? (eps_dot / xn + 4.0f * 5.9604645e-8f)
-                                : (2.0f * eps_dot + (p.d + 8) * 5.9604645e-8f * (xi + tp.p_max + 2.0f * xn * tp.mu_max));
+        const float u = 5.9604645e-8f;
+        const float rowc = COS ? 1.0f : xi;
+        const float exi = 8.1f * u * xi;   // ||x||^2 error (fp32 blocks of 8)
+        const float eps_dot = (tp.cdot * tp.mu_max + tp.floor_coef) * xn;  // any column
+        const float eps_m = COS ? (eps_dot / xn + 3.0f * u * (fabsf(b1) + 1.0f) + exi / xi)
+                                : (2.0f * eps_dot + 3.0f * u * (fabsf(b1) + tp.p_max + 2.0f * xn * tp.mu_max) + exi);
         int nb = arg;
-        bool full = !((b2 - b1) > 2.0f * eps_m) || nb < 0;
+        // neighbour certain: clear gap, and no tie through the clamps at 0 (and 2)
+        const bool full = !((b2 - b1) > 2.0f * eps_m) || nb < 0 || !(rowc + b2 > eps_m) ||
+                          (COS && !(rowc + b1 < 2.0f - eps_m));
         if (nb < 0) nb = own == 0 ? 1 : 0;
-        const double n_o = p.nk[own], n_b = p.nk[nb];
-        const bool singleton = n_o == 1.0;
-        const double dn = static_cast<double>(dotb) * tp.smul64, dob = static_cast<double>(doto) * tp.smul64;
-        // per-cluster bounds for the two dots that enter a_i and b_i
-        const double ed_b = (static_cast<double>(tp.cdot) * __ldg(tp.munorm + nb) + tp.floor_coef) * xn * 1.0000001;
-        const double ed_o = (static_cast<double>(tp.cdot) * __ldg(tp.munorm + own) + tp.floor_coef) * xn * 1.0000001;
+        const double4 co = tp.clu[own];  // n, 1/(n-1), Psi
+        const bool singleton = co.x == 1.0;
+        const double ed_b = (static_cast<double>(tp.cdot) * __ldg(tp.munorm + nb) + tp.floor_coef) * xn;
+        const double ed_o = (static_cast<double>(tp.cdot) * __ldg(tp.munorm + own) + tp.floor_coef) * xn;
+        const double dob = static_cast<double>(doto) * tp.smul64;
+        const double mb = static_cast<double>(rowc) + static_cast<double>(b1);
+        const double n_o = co.x, r_o = co.y, nr_o = n_o * r_o;
         double a, b, da, db;
         if (COS) {
-          const double nrm = sqrt(xi64);
-          b = cos_foreign(n_b, n_b * dn / nrm);
-          a = singleton ? 0.0 : cos_own(n_o, n_o * dob / nrm);
-          db = ed_b / nrm;
-          da = n_o / (n_o - 1.0) * ed_o / nrm;
+          double rn = static_cast<double>(rsqrtf(xi));
+          rn = rn * (1.5 - 0.5 * xi64 * rn * rn);
+          rn = rn * (1.5 - 0.5 * xi64 * rn * rn);  // 1/||x|| to ~1e-16
+          b = fmin(fmax(mb, 0.0), 2.0);
+          a = singleton ? 0.0 : fmin(fmax((n_o - n_o * dob * rn) * r_o, 0.0), 2.0);
+          db = ed_b * rn + 3.0 * u * (fabs(b1) + 1.0) + exi / xi;
+          da = nr_o * (ed_o * rn + exi / xi);
         } else {
-          const double* psi = p.stats + p.k;
-          b = sq_foreign(xi64, psi[nb], n_b, n_b * dn);
-          a = singleton ? 0.0 : sq_own(xi64, psi[own], n_o, n_o * dob);
-          db = 2.0 * ed_b;
-          da = 2.0 * n_o / (n_o - 1.0) * ed_o;
+          b = fmax(mb, 0.0);
+          a = singleton ? 0.0 : fmax((n_o * xi64 + co.z - 2.0 * n_o * dob) * r_o, 0.0);
+          db = 2.0 * ed_b + 3.0 * u * (fabs(b1) + tp.p_max + 2.0 * xn * tp.mu_max) + exi;
+          da = nr_o * (2.0 * ed_o + exi);
         }
-        s = singleton ? 0.0 : assemble_score(a, b);
         const double mx = fmax(a, b);
-        const bool inexact = !singleton && !(mx > 2.0 * (da + db) && (da + db) / mx <= kTau);
+        if (!singleton && mx > 0.0) {  // assemble_score without a division
+          double rm = static_cast<double>(__frcp_rn(static_cast<float>(mx)));
+          rm = rm * (2.0 - mx * rm);
+          rm = rm * (2.0 - mx * rm);
+          s = a <= b ? 1.0 - a * rm : b * rm - 1.0;
+        }
+        const bool inexact = !singleton && !(mx > 2.0 * (da + db) && (da + db) <= static_cast<double>(kTau) * mx);
         p.s[row] = s;
         if (p.nb) p.nb[row] = nb;
         if (p.own) p.own[row] = own;
@@ -350,21 +431,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           any = true;
         }
       }
-      // fixed-order tile sum over the 4 epilogue warps (named barrier 1, 128 threads)
+      // fixed-order tile sum over the 4 first-half warps: one named barrier,
+      // partial slots double-buffered by tile parity
       for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
       const unsigned anyw = __ballot_sync(0xffffffffu, any);
       if (lane == 0) {
-        red[quad] = s;
-        if (ew == 0) *red_flag = 0;
+        red[tb * 4 + quad] = s;
+        red_flag[tb * 4 + quad] = anyw != 0;
       }
-      named_bar(1, 128);
-      if (lane == 0 && anyw) atomicOr(red_flag, 1);
-      named_bar(1, 128);
-      if (ew == 0 && lane == 0) {
-        p.tile_sum[t] = ((red[0] + red[1]) + red[2]) + red[3];
-        p.tile_flag[t] = *red_flag;
+      named_bar(2 + grp, 128);
+      if (quad == 0 && lane == 0) {
+        p.tile_sum[t] = ((red[tb * 4] + red[tb * 4 + 1]) + red[tb * 4 + 2]) + red[tb * 4 + 3];
+        p.tile_flag[t] = red_flag[tb * 4] | red_flag[tb * 4 + 1] | red_flag[tb * 4 + 2] | red_flag[tb * 4 + 3];
       }
-      named_bar(1, 128);
     }
   }
 
@@ -377,7 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // B pieces: mu~ = mu * 2^-em split into fp16 hi + lo, [Kp][Dp] zero padded; column
 // bias for the ranking (sqeuclid p_k, cosine 0, padding +inf).
 __global__ void prep_b_kernel(const double* __restrict__ stats, int k, int d, int kp, int dp, bool cos,
-                              float smu, __half* bh, __half* bl, float* colbias, float* munorm) {
+                              float smu, __half* bh, __half* bl, float* colbias, float* munorm,
+                              double4* clu) {
   const int c = blockIdx.x;
   const double n = c < k ? fmax(stats[c], 1.0) : 1.0;
   const double* sums = stats + (cos ? k : 2 * k) + static_cast<int64_t>(c) * d;
@@ -405,6 +485,7 @@ __global__ void prep_b_kernel(const double* __restrict__ stats, int k, int d, in
   if (threadIdx.x == 0) {
     colbias[c] = c < k ? (cos ? 0.0f : static_cast<float>(stats[k + c] / n)) : INFINITY;
     munorm[c] = __double2float_ru(sqrt(red[0] + red[1] + red[2] + red[3]) * (1.0 + 1e-12));
+    if (c < k) clu[c] = make_double4(n, n > 1.0 ? 1.0 / (n - 1.0) : 0.0, cos ? 0.0 : stats[k + c], 0.0);
   }
 }
 
@@ -441,8 +522,8 @@ CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* ptr, uint64_t inner,
 int pick_bn(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : 128; }
 
 size_t tc_smem(int bn, int kp) {
-  return 1024 + 2 * kStgBytes + 4 * kABytes + 4 * static_cast<size_t>(bn) * 128 + 16 * 8 + 16 + 2 * BM * 4 +
-         2 * BM * 8 + 96 + static_cast<size_t>(ncb_bn_pad(kp)) * 4;
+  const size_t ring = bn <= 32 ? TcCfg<32>::kRing : bn <= 64 ? TcCfg<64>::kRing : TcCfg<128>::kRing;
+  return 1024 + ring + 26 * 8 + 2 * BM * 8 + 8 * BM * 4 + 128 + static_cast<size_t>(ncb_bn_pad(kp)) * 4;
 }
 
 template <int BN, bool COS>
@@ -483,13 +564,14 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   FSIL_CUDA(cudaStreamSynchronize(c->stream));
   const int ex = h_xmax > 0.f ? std::ilogb(h_xmax) - 14 : 0;
   const int em = h_bound[2] > 0.f ? std::ilogb(h_bound[2]) - 14 : 0;
-  c->tc_b.ensure(2ull * kp * dp * sizeof(__half) + 2ull * kp * sizeof(float));
+  c->tc_b.ensure(2ull * kp * dp * sizeof(__half) + 2ull * kp * sizeof(float) + kp * sizeof(double4) + 64);
   __half* bh = c->tc_b.as<__half>();
   __half* bl = bh + static_cast<size_t>(kp) * dp;
   float* colbias = reinterpret_cast<float*>(bl + static_cast<size_t>(kp) * dp);
   float* munorm = colbias + kp;
+  double4* clu = reinterpret_cast<double4*>((reinterpret_cast<uintptr_t>(munorm + kp) + 31) & ~uintptr_t(31));
   prep_b_kernel<<<kp, 128, 0, c->stream>>>(p.stats, c->k, c->d, kp, dp, cos, std::ldexp(1.0f, -em), bh, bl,
-                                           colbias, munorm);
+                                           colbias, munorm, clu);
   FSIL_LAUNCHED(c);
   const CUtensorMap mx = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, c->X, c->d, c->n, c->d * 4ull, 32, BM);
   const CUtensorMap mh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, bh, dp, kp, dp * 2ull, BK, bn);
@@ -503,6 +585,7 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   tp.smul64 = std::ldexp(1.0, ex + em);
   tp.colbias = colbias;
   tp.munorm = munorm;
+  tp.clu = clu;
   // |dot error| <= cdot*||x||*||mu|| + floor: split residuals 3*2^-22 relative; fp32
   // accumulation of the main term over ceil(D/16) MMA steps at 2^-24 (the correction
   // accumulator holds values <= 2^-10 of it); the final main+correction add; and the
