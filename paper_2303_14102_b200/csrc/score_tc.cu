@@ -19,6 +19,8 @@
 // 5e-6 in s_i go to the exact own/neighbour recompute -- both in finalize.cu.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cuda_fp16.h>
 
 #include "score_common.cuh"
@@ -33,24 +35,34 @@ constexpr int BM = 128;               // rows per tile = TMEM lanes
 constexpr int BK = 64;                // fp16 K elements per chunk (one 128-byte swizzle row)
 constexpr int kStgBytes = 2 * BM * 128;  // two fp32 boxes of 32 columns
 constexpr int kABytes = BM * 128;        // one fp16 A piece (hi or lo)
-constexpr int kThreads = 480;            // 15 warps
+constexpr int kThreads = 640;            // 20 warps (5 warpgroups)
 constexpr float kTau = 9e-6f;            // certified |ds_i| budget before exact a/b (bar: 1e-5)
 
 __host__ __device__ constexpr int ncb_bn_pad(int kp) { return (kp + 3) & ~3; }
 
+// Operand scalings and error-bound constants, computed on the device by prep_b from
+// the derived bounds (no host round trip between aggregation and scoring).
+struct TcScale {
+  double smul64;          // 2^(ex+em): dot = acc * smul
+  float sx;               // 2^-ex: x -> x~
+  float smul;
+  float floor_coef;       // absolute-floor coefficient (times ||x||)
+  float mu_max;           // max ||mu_k||
+  float p_max;            // max p_k (sqeuclid)
+  float pad;
+};
+
 struct TcParams {
   ScoreParams p;
   int ncb, nkc;           // cluster blocks, K chunks
-  float sx;               // 2^-ex: x -> x~
-  float smul;             // 2^(ex+em): dot = acc * smul
-  double smul64;
   const float* colbias;   // [ncb*BN]: sqeuclid p_k, cosine 0, padding +inf
-  const float* munorm;    // [ncb*BN]: ||mu_k|| rounded up (per-cluster error bounds)
-  const double4* clu;     // [K]: {n_k, 1/(n_k-1) (0 if singleton), Psi_k, 0}
+  const double4* clu;     // [K]: {n_k, 1/(n_k-1) (0 if singleton), Psi_k, ||mu_k|| rounded up}
+  const __half* munorm;   // [ncb*BN]: ||mu_k|| / mu_max rounded up (neighbour error bounds)
+  int nstg;               // X staging stages
+  const TcScale* scale;
   float cdot;             // relative dot bound coefficient
-  float floor_coef;       // absolute-floor coefficient (times ||x||)
-  float mu_max;           // max ||mu_k||
-  float p_max;
+  unsigned long long* dbg;  // optional per-role wait-cycle counters (FSIL_TC_PROFILE)
+  int split;              // separate correction accumulator (large D)
   int2* exact_rows;       // rows needing the exact own/neighbour recompute
   unsigned long long* exact_count;
 };
@@ -61,68 +73,108 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 
 template <int BN>
 struct TcCfg {
-  static constexpr int kStg = BN <= 32 ? 4 : BN <= 64 ? 3 : 2;  // fp32 X staging stages
-  static constexpr int kOps = 2;                                 // operand (A+B) stages
+  static constexpr int kBStg = BN <= 32 ? 4 : BN <= 64 ? 3 : 2;  // B (hi+lo) operand stages
   static constexpr int kBBytes = BN * 128;
-  static constexpr int kOpBytes = 2 * kABytes + 2 * kBBytes;
-  static constexpr size_t kRing = static_cast<size_t>(kStg) * kStgBytes + static_cast<size_t>(kOps) * kOpBytes;
+  static constexpr size_t kBRing = static_cast<size_t>(kBStg) * 2 * kBBytes;
 };
+
+// Optional wait profiling (FSIL_TC_PROFILE): cycles each role spends blocked, per
+// barrier (slots 0..8), added straight to global counters so the normal build keeps
+// no per-thread state for it.
+#define TW(slot, bar, par)                                                          \
+  do {                                                                              \
+    if (tp.dbg) {                                                                   \
+      const long long t0__ = clock64();                                             \
+      mbar_wait(bar, par);                                                          \
+      if (lane == 0) atomicAdd(tp.dbg + (slot), static_cast<unsigned long long>(clock64() - t0__)); \
+    } else {                                                                        \
+      mbar_wait(bar, par);                                                          \
+    }                                                                               \
+  } while (0)
+
+// Warp roles (warpgroup aligned, so each group can set its own register budget):
+//   warpgroup 0: warp 0 X producer (TMA), warp 1 TMEM owner + MMA issuer, warp 2 B
+//                producer (TMA), warp 3 idle -- 40 registers
+//   warpgroups 1-2 (warps 4..11): epilogue, two groups of four -- 120 registers
+//   warpgroups 3-4 (warps 12..19): converters -- 96 registers
+constexpr int kEpiWarp0 = 4, kConvWarp0 = 12;
 
 template <int BN, bool COS>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
                     const __grid_constant__ CUtensorMap tmap_bl, TcParams tp, int64_t ntiles) {
   using C = TcCfg<BN>;
-  constexpr int NS = C::kStg, NO = C::kOps;
-  // TS (BN <= 64): the two epilogue groups take alternate tiles, each with its own
-  // pair of accumulator buffers, so consecutive tiles' epilogues overlap.  Otherwise
-  // the groups split the column chunks of every tile.
-  constexpr bool TS = BN <= 64;
-  constexpr int NACC = TS ? 4 : 2;
-  constexpr uint32_t kCols = NACC * 2 * BN;  // x {main, correction}
-  constexpr uint32_t kTmemCols = (kCols <= 32) ? 32 : (kCols <= 64) ? 64 : (kCols <= 128) ? 128 : (kCols <= 256) ? 256 : 512;
+  constexpr int NB = C::kBStg;
+  // X stages: a TMA-filled fp32 box pair that the converters overwrite in place with
+  // the fp16 A pieces (hi over box 0, lo over box 1), freed by the MMA commit
+  const int NS = tp.nstg;
+  // TS: the two epilogue groups take alternate tiles, each with its own pair of
+  // accumulator buffers, so consecutive tiles' epilogues overlap -- for tiles of at
+  // most two cluster blocks (with more, the MMA stream would serialise on one
+  // group's buffers).  Otherwise the groups split the column chunks of every tile,
+  // cycling through `nacc` buffers (4 when they fit the 512 TMEM columns).
+  const uint32_t astride = tp.split ? 2 * BN : BN;  // TMEM columns per accumulator buffer
+  const bool TS = tp.ncb <= 2 && 4 * astride <= 512;
+  const uint32_t nacc = 4 * astride <= 512 ? 4 : 2;
+  // A-resident: a tile's converted A chunks stay in their stages for every cluster
+  // block (X read and converted once per tile); otherwise re-staged per block
+  const bool ares = tp.ncb > 1 && 2 * tp.nkc <= NS;
+  const int xpasses = ares ? 1 : tp.ncb;
+  constexpr uint32_t kTmemCols = BN <= 32 ? 256 : 512;
   constexpr uint32_t kIdesc = idesc_f16_f32(BM, BN);
   const ScoreParams& p = tp.p;
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* stg = base;                     // [NS][kStgBytes]
-  uint8_t* ops = stg + NS * kStgBytes;     // [NO][a_hi | a_lo | b_hi | b_lo]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ops + NO * C::kOpBytes);
-  uint64_t* stg_full = bars;               // [NS]
-  uint64_t* stg_empty = bars + 4;          // [NS]
-  uint64_t* op_full = bars + 8;            // [NO]
-  uint64_t* op_empty = bars + 10;          // [NO]
-  uint64_t* acc_full = bars + 12;          // [NACC]
-  uint64_t* acc_empty = bars + 16;         // [NACC]
-  uint64_t* meta_full = bars + 20;         // [2]
-  uint64_t* meta_empty = bars + 22;        // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
-  double* meta_xi = reinterpret_cast<double*>(bars + 26);   // [2][BM] ||x||^2 (fp64 of fp32 blocks)
-  float* part = reinterpret_cast<float*>(meta_xi + 2 * BM);  // [2][4][BM] second-half partial top-2
+  // 1024-byte alignment by a pointer offset (keeps the shared address space visible to
+  // the compiler: LDS/STS rather than generic accesses)
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* stg = base;                      // [NS][kStgBytes]
+  uint8_t* bring = stg + NS * kStgBytes;    // [NB][b_hi | b_lo]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + NB * 2 * C::kBBytes);
+  uint64_t* stg_full = bars;               // [NS <= 8] X landed (TMA)
+  uint64_t* stg_empty = bars + 8;          // [NS] stage free (MMA commit)
+  uint64_t* a_full = bars + 16;            // [NS] A pieces written (converters)
+  uint64_t* b_full = bars + 24;            // [NB]
+  uint64_t* b_empty = bars + 28;           // [NB]
+  uint64_t* acc_full = bars + 32;          // [4]
+  uint64_t* acc_empty = bars + 36;         // [4]
+  uint64_t* meta_full = bars + 40;         // [2]
+  uint64_t* meta_empty = bars + 42;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 44);
+  double* meta_xi = reinterpret_cast<double*>(bars + 46);   // [2][2][BM] ||x||^2 halves
+  double4* meta_clu = reinterpret_cast<double4*>(meta_xi + 4 * BM);  // [2][BM] clu[own] per row
+  float* part = reinterpret_cast<float*>(meta_clu + 2 * BM);  // [2][4][BM] second-half partial top-2
   double* red = reinterpret_cast<double*>(part + 8 * BM);     // [2][4] tile-sum partials
   int* red_flag = reinterpret_cast<int*>(red + 8);            // [2][4]
-  float* cb_s = reinterpret_cast<float*>(red + 12);           // [ncb*BN] column bias
+  int* meta_own = reinterpret_cast<int*>(red + 12);           // [2][BM] own cluster per row
+  float* cb_s = reinterpret_cast<float*>(meta_own + 2 * BM);  // [ncb*BN] column bias
+  __half* mn_s = reinterpret_cast<__half*>(cb_s + ncb_bn_pad(tp.ncb * BN));  // [ncb*BN] ||mu_k||/mu_max, rounded up
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncb = tp.ncb, nkc = tp.nkc;
-  for (int j = threadIdx.x; j < ncb * BN; j += blockDim.x) cb_s[j] = tp.colbias[j];
+  const long long t_start = tp.dbg ? clock64() : 0;
+  for (int j = threadIdx.x; j < ncb * BN; j += blockDim.x) {
+    cb_s[j] = tp.colbias[j];
+    mn_s[j] = tp.munorm[j];
+  }
+  const TcScale sc = *tp.scale;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(stg_full + i, 1);
-      mbar_init(stg_empty + i, 4);
+      mbar_init(stg_empty + i, 1);
+      mbar_init(a_full + i, 8);
     }
-    for (int i = 0; i < NO; ++i) {
-      mbar_init(op_full + i, 1 + 4);
-      mbar_init(op_empty + i, 1);
+    for (int i = 0; i < NB; ++i) {
+      mbar_init(b_full + i, 1);
+      mbar_init(b_empty + i, 1);
     }
-    for (int i = 0; i < NACC; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(acc_full + i, 1);
       mbar_init(acc_empty + i, TS ? 4 : 8);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(meta_full + i, 4);
+      mbar_init(meta_full + i, 8);
       mbar_init(meta_empty + i, TS ? 4 : 8);
     }
     fence_barrier_init();
@@ -136,122 +188,141 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer: X
-    if (lane == 0) {
+  if (warp < kEpiWarp0) {
+    setmaxnreg_dec<40>();
+    if (warp == 0 && lane == 0) {
+      // ---------------------------------------------------------- TMA producer: X
       uint32_t n1 = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int row0 = static_cast<int>(t * BM);
-        for (int cb = 0; cb < ncb; ++cb) {
+        for (int xp = 0; xp < xpasses; ++xp) {
           for (int kc = 0; kc < nkc; ++kc, ++n1) {
             const int s1 = n1 % NS;
             const int nbox = (kc * BK + 32 < p.d) ? 2 : 1;
-            mbar_wait(stg_empty + s1, ((n1 / NS) & 1) ^ 1);
+            TW(0, stg_empty + s1, ((n1 / NS) & 1) ^ 1);
             mbar_arrive_expect_tx(stg_full + s1, nbox * BM * 128);
             for (int b = 0; b < nbox; ++b)
               tma_load_2d(stg + s1 * kStgBytes + b * BM * 128, &tmap_x, stg_full + s1, kc * BK + b * 32, row0);
           }
         }
       }
-    }
-  } else if (warp == 14) {
-    // ------------------------------------------------------------ TMA producer: B pieces
-    if (lane == 0) {
+    } else if (warp == 2 && lane == 0) {
+      // ---------------------------------------------------------- TMA producer: B pieces
       uint32_t n2 = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int cb = 0; cb < ncb; ++cb) {
           for (int kc = 0; kc < nkc; ++kc, ++n2) {
-            const int s2 = n2 % NO;
-            uint8_t* op = ops + s2 * C::kOpBytes;
-            mbar_wait(op_empty + s2, ((n2 / NO) & 1) ^ 1);
-            mbar_arrive_expect_tx(op_full + s2, 2 * C::kBBytes);
-            tma_load_2d(op + 2 * kABytes, &tmap_bh, op_full + s2, kc * BK, cb * BN);
-            tma_load_2d(op + 2 * kABytes + C::kBBytes, &tmap_bl, op_full + s2, kc * BK, cb * BN);
+            const int sb = n2 % NB;
+            uint8_t* bs = bring + sb * 2 * C::kBBytes;
+            TW(1, b_empty + sb, ((n2 / NB) & 1) ^ 1);
+            mbar_arrive_expect_tx(b_full + sb, 2 * C::kBBytes);
+            tma_load_2d(bs, &tmap_bh, b_full + sb, kc * BK, cb * BN);
+            tma_load_2d(bs + C::kBBytes, &tmap_bl, b_full + sb, kc * BK, cb * BN);
           }
         }
       }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      uint32_t n2 = 0, na = 0, ng[2] = {0, 0}, nt = 0;
+    } else if (warp == 1 && lane == 0) {
+      // ---------------------------------------------------------- MMA issuer
+      uint32_t n2 = 0, na = 0, ng0 = 0, ng1 = 0, nt = 0, nx = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
         for (int cb = 0; cb < ncb; ++cb, ++na) {
           int ab;
           uint32_t ph;
           if (TS) {
             const int g = nt & 1;
-            ab = 2 * g + (ng[g] & 1);
-            ph = (ng[g] >> 1) & 1;
-            ++ng[g];
+            const uint32_t cnt = g ? ng1 : ng0;  // per-group buffer-pair counters
+            ab = 2 * g + (cnt & 1);
+            ph = (cnt >> 1) & 1;
+            ng0 += g ? 0u : 1u;
+            ng1 += g ? 1u : 0u;
           } else {
-            ab = na & 1;
-            ph = (na >> 1) & 1;
+            ab = na % nacc;
+            ph = (na / nacc) & 1;
           }
-          mbar_wait(acc_empty + ab, ph ^ 1);
+          TW(2, acc_empty + ab, ph ^ 1);
           tc_fence_after();
-          const uint32_t d_main = tmem_base + ab * 2 * BN, d_corr = d_main + BN;
+          const uint32_t d_main = tmem_base + ab * astride, d_corr = tp.split ? d_main + BN : d_main;
           for (int kc = 0; kc < nkc; ++kc, ++n2) {
-            const int s2 = n2 % NO;
-            mbar_wait(op_full + s2, (n2 / NO) & 1);
+            const uint32_t ia = ares ? nx + kc : nx + cb * nkc + kc;  // A item
+            const int s1 = ia % NS, sb = n2 % NB;
+            if (!ares || cb == 0) TW(3, a_full + s1, (ia / NS) & 1);
+            TW(3, b_full + sb, (n2 / NB) & 1);
             tc_fence_after();
             const int rem = p.d - kc * BK;
             const int nks = rem >= BK ? 4 : (rem + 15) / 16;
-            const uint32_t ah = smem_u32(ops + s2 * C::kOpBytes), al = ah + kABytes;
-            const uint32_t bh = ah + 2 * kABytes, bl = bh + C::kBBytes;
+            const uint32_t ah = smem_u32(stg + s1 * kStgBytes), al = ah + kABytes;
+            const uint32_t bh = smem_u32(bring + sb * 2 * C::kBBytes), bl = bh + C::kBBytes;
             for (int ks = 0; ks < nks; ++ks) {
               const uint32_t off = ks * 32;
               const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
-              // main term and the two correction terms accumulate separately: the
-              // corrections are ~2^-10 of the main term, so their fp32 rounding is too
+              // split: the two correction terms (~2^-10 of the main term) accumulate
+              // separately so their fp32 rounding is ~2^-10 smaller; for small D a
+              // single accumulator is certified tightly enough and is cheaper
               mma_f16(d_main, desc_k_sw128(ah + off), desc_k_sw128(bh + off), kIdesc, acc0);
-              mma_f16(d_corr, desc_k_sw128(ah + off), desc_k_sw128(bl + off), kIdesc, acc0);
+              mma_f16(d_corr, desc_k_sw128(ah + off), desc_k_sw128(bl + off), kIdesc, tp.split ? acc0 : 1u);
               mma_f16(d_corr, desc_k_sw128(al + off), desc_k_sw128(bh + off), kIdesc, 1u);
             }
-            mma_commit(op_empty + s2);  // operand stage free once these MMAs retire
+            mma_commit(b_empty + sb);                               // B stage free when these retire
+            if (!ares || cb == ncb - 1) mma_commit(stg_empty + s1);  // A stage: after its last use
           }
-          mma_commit(acc_full + ab);    // accumulators ready for the epilogue
+          mma_commit(acc_full + ab);  // accumulators ready for the epilogue
         }
+        nx += ares ? nkc : ncb * nkc;
       }
     }
-  } else if (warp >= 10 && warp < 14) {
-    // ------------------------------------------------------------ converters
-    const int r = threadIdx.x - 10 * 32;  // row in tile, 0..127
+  } else if (warp >= kConvWarp0) {
+    // ------------------------------------------------------------ converters (8 warps:
+    // two threads per row; thread half hq reads fp32 box hq of the stage, then -- after
+    // the whole group has read -- writes A chunks 4hq..4hq+3 of hi (over box 0) and lo
+    // (over box 1))
+    const int tl = threadIdx.x - kConvWarp0 * 32;
+    const int r = tl & (BM - 1), hq = tl >> 7;  // row in tile, box / chunk half
     const int sw = r & 7;
-    uint32_t n1 = 0, n2 = 0, nt = 0;
+    const float2 sx2 = make_float2(sc.sx, sc.sx), neg1 = make_float2(-1.f, -1.f);
+    uint32_t n1 = 0, nt = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
       double xi = 0.0;
-      for (int cb = 0; cb < ncb; ++cb) {
-        for (int kc = 0; kc < nkc; ++kc, ++n1, ++n2) {
-          const int s1 = n1 % NS, s2 = n2 % NO;
-          mbar_wait(stg_full + s1, (n1 / NS) & 1);
-          mbar_wait(op_empty + s2, ((n2 / NO) & 1) ^ 1);
-          const uint8_t* srow = stg + s1 * kStgBytes + r * 128;
-          uint8_t* hrow = ops + s2 * C::kOpBytes + r * 128;
-          uint8_t* lrow = hrow + kABytes;
-          const bool two = kc * BK + 32 < p.d;
+      // the epilogue's per-row inputs, fetched here off its critical path
+      const int64_t row = t * BM + r;
+      const int own = (hq == 0 && row < p.n) ? __ldg(p.dense + row) : -1;
+      for (int xp = 0; xp < xpasses; ++xp) {
+        for (int kc = 0; kc < nkc; ++kc, ++n1) {
+          const int s1 = n1 % NS;
+          TW(4, stg_full + s1, (n1 / NS) & 1);
+          uint8_t* sbase = stg + s1 * kStgBytes;
+          float4 f[8];
+          if (hq == 0 || kc * BK + 32 < p.d) {
+            const uint8_t* srow = sbase + hq * (BM * 128) + r * 128;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {  // 8 fp16 A chunks of 16 bytes
-            float4 f0 = make_float4(0.f, 0.f, 0.f, 0.f), f1 = f0;
-            if (j < 4 || two) {
-              const uint8_t* box = srow + (j >> 2) * (BM * 128);
-              f0 = *reinterpret_cast<const float4*>(box + ((((2 * j) & 7) ^ sw) << 4));
-              f1 = *reinterpret_cast<const float4*>(box + ((((2 * j + 1) & 7) ^ sw) << 4));
-            }
-            const float v[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
-            if (cb == 0) {  // ||x||^2: fp32 blocks of 8 (error <= 8u each), fp64 across blocks
-              float bs = 0.f;
+            for (int u = 0; u < 8; ++u) f[u] = *reinterpret_cast<const float4*>(srow + ((u ^ sw) << 4));
+          } else {
 #pragma unroll
-              for (int e = 0; e < 8; ++e) bs = fmaf(v[e], v[e], bs);
-              xi += static_cast<double>(bs);
+            for (int u = 0; u < 8; ++u) f[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          named_bar(5, 256);  // every read of the stage precedes the in-place writes
+          uint8_t* hrow = sbase + r * 128;
+          uint8_t* lrow = hrow + BM * 128;
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {  // A chunk j = 8 fp16 = fp32 units 2jj, 2jj+1
+            const int j = 4 * hq + jj;
+            const float v[8] = {f[2 * jj].x,     f[2 * jj].y,     f[2 * jj].z,     f[2 * jj].w,
+                                f[2 * jj + 1].x, f[2 * jj + 1].y, f[2 * jj + 1].z, f[2 * jj + 1].w};
+            if (xp == 0) {  // ||x||^2: fp32 blocks of 8 (error <= 8u each), fp64 across blocks
+              float2 bs = make_float2(0.f, 0.f);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 ve = make_float2(v[2 * e], v[2 * e + 1]);
+                bs = __ffma2_rn(ve, ve, bs);
+              }
+              xi += static_cast<double>(bs.x + bs.y);
             }
             uint32_t hw[4], lw[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float x0 = v[2 * e] * tp.sx, x1 = v[2 * e + 1] * tp.sx;
-              const __half2 h = __floats2half2_rn(x0, x1);
-              const float2 hf = __half22float2(h);
-              const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+            for (int e = 0; e < 4; ++e) {  // packed f32x2: scale (exact), hi, residual, lo
+              const float2 xx = __fmul2_rn(make_float2(v[2 * e], v[2 * e + 1]), sx2);
+              const __half2 h = __float22half2_rn(xx);
+              const float2 res = __ffma2_rn(__half22float2(h), neg1, xx);  // exact
+              const __half2 l = __float22half2_rn(res);
               hw[e] = *reinterpret_cast<const uint32_t*>(&h);
               lw[e] = *reinterpret_cast<const uint32_t*>(&l);
             }
@@ -261,25 +332,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(op_full + s2);
-            mbar_arrive(stg_empty + s1);
-          }
+          if (lane == 0) mbar_arrive(a_full + s1);
         }
-        if (cb == 0) {
+        if (xp == 0) {
           const int tb = nt & 1;
-          mbar_wait(meta_empty + tb, ((nt >> 1) & 1) ^ 1);
-          meta_xi[tb * BM + r] = xi;
+          const double4 co = own >= 0 ? tp.clu[own] : make_double4(1.0, 0.0, 0.0, 0.0);
+          TW(6, meta_empty + tb, ((nt >> 1) & 1) ^ 1);
+          meta_xi[(tb * 2 + hq) * BM + r] = xi;
+          if (hq == 0) {
+            meta_own[tb * BM + r] = own;
+            meta_clu[tb * BM + r] = co;
+          }
           __syncwarp();
           if (lane == 0) mbar_arrive(meta_full + tb);
         }
       }
     }
-  } else if (warp >= 2) {
+  } else {
     // ------------------------------------------------------------ epilogue (8 warps)
-    const int quad = warp & 3;        // TMEM lane quadrant of this warp
-    const int r = quad * 32 + lane;   // row in tile
-    const int grp = (warp - 2) >> 2;  // epilogue group 0 / 1
+    setmaxnreg_inc<120>();  // CTA pool: 4x40 + 8x120 + 8x96 <= 20x96 per lane
+    const int quad = warp & 3;                // TMEM lane quadrant of this warp
+    const int r = quad * 32 + lane;           // row in tile
+    const int grp = (warp - kEpiWarp0) >> 2;  // epilogue group 0 / 1
     uint32_t na = 0, nt = 0, ng = 0;
     constexpr int NQ = BN / 32;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
@@ -287,14 +361,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (TS && tb != grp) continue;  // the other group takes this tile
       const int64_t row = t * BM + r;
       const bool valid = row < p.n;
-      const int own = valid ? p.dense[row] : -1;
-      mbar_wait(meta_full + tb, (nt >> 1) & 1);
-      const double xi64 = meta_xi[tb * BM + r];
+      TW(7, meta_full + tb, (nt >> 1) & 1);
+      const int own = meta_own[tb * BM + r];
+      const double4 co = meta_clu[tb * BM + r];  // n, 1/(n-1), Psi, ||mu||
+      const double xi64 = meta_xi[(tb * 2) * BM + r] + meta_xi[(tb * 2 + 1) * BM + r];
       const float xi = static_cast<float>(xi64);
       const float xn = sqrtf(xi);
       // ranking key m' = m - rowc (row constant dropped, no clamp): sqeuclid
       // m = xi + p_k - 2 dot, cosine m = 1 - dot/||x||; dot = acc * smul
-      const float rowm = COS ? -(tp.smul / xn) : -2.0f * tp.smul;
+      const float rowm = COS ? -(sc.smul / xn) : -2.0f * sc.smul;
       float b1 = INFINITY, b2 = INFINITY, doto = NAN;
       int arg = -1;
       for (int cb = 0; cb < ncb; ++cb) {
@@ -305,19 +380,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           ph = (ng >> 1) & 1;
           ++ng;
         } else {
-          ab = na & 1;
-          ph = (na >> 1) & 1;
+          ab = na % nacc;
+          ph = (na / nacc) & 1;
           ++na;
         }
-        mbar_wait(acc_full + ab, ph);
+        TW(8, acc_full + ab, ph);
+        const long long ts0 = tp.dbg ? clock64() : 0;
         tc_fence_after();
-#pragma unroll 1
-        for (int q = TS ? 0 : grp; q < NQ; q += TS ? 1 : 2) {
-          float v[32], w[32];
-          const uint32_t ta = tmem_base + ab * 2 * BN + q * 32 + (static_cast<uint32_t>(quad * 32) << 16);
-          tmem_ld32(ta, v);
-          tmem_ld32(ta + BN, w);
-          const int k0 = cb * BN + q * 32;
+        // one 32-column chunk: ranking keys, own-column capture, running top-2
+        auto scan32 = [&](const uint32_t(&v)[32], int k0) {
+          const int ownrel = own - k0;
+          int argc = -1;  // chunk-local index of a new best
           const float4* cb4 = reinterpret_cast<const float4*>(cb_s + k0);
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
@@ -326,23 +399,50 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int j = 4 * j4 + e;
-              const int k = k0 + j;
-              const float acc = v[j] + w[j];
+              const float acc = __uint_as_float(v[j]);
               float m = fmaf(acc, rowm, bj[e]);
-              const bool is_own = k == own;
+              const bool is_own = j == ownrel;
               doto = is_own ? acc : doto;
               m = is_own ? INFINITY : m;
               const bool lt = m < b1;  // strict: the lowest index keeps ties
-              arg = lt ? k : arg;
+              argc = lt ? j : argc;
               b2 = fminf(b2, fmaxf(b1, m));
               b1 = fminf(b1, m);
             }
+          }
+          if (argc >= 0) arg = k0 + argc;
+        };
+        const int q0 = TS ? 0 : grp, qs = TS ? 1 : 2;
+        const uint32_t tb0 = tmem_base + ab * astride + (static_cast<uint32_t>(quad * 32) << 16);
+        if (tp.split) {
+#pragma unroll 1
+          for (int q = q0; q < NQ; q += qs) {
+            uint32_t v[32], w[32];
+            tmem_ld32_issue(tb0 + q * 32, v);
+            tmem_ld32_issue(tb0 + q * 32 + BN, w);
+            tmem_ld_wait2(v, w);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
+            scan32(v, cb * BN + q * 32);
+          }
+        } else {
+#pragma unroll 1
+          for (int q = q0; q < NQ; q += 2 * qs) {  // two chunks per TMEM wait
+            uint32_t v[32], w[32];
+            const bool two = q + qs < NQ;
+            tmem_ld32_issue(tb0 + q * 32, v);
+            if (two) tmem_ld32_issue(tb0 + (q + qs) * 32, w);
+            tmem_ld_wait2(v, w);
+            scan32(v, cb * BN + q * 32);
+            if (two) scan32(w, cb * BN + (q + qs) * 32);
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + ab);
+        if (tp.dbg && warp == kEpiWarp0 && lane == 0) atomicAdd(tp.dbg + 12, static_cast<unsigned long long>(clock64() - ts0));
       }
+      const long long tf0 = tp.dbg ? clock64() : 0;
       if (!TS) {
         // ---- merge the two column halves (group 1 -> smem -> group 0)
         float* pt = part + tb * 4 * BM;  // double-buffered by tile parity
@@ -378,19 +478,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float u = 5.9604645e-8f;
         const float rowc = COS ? 1.0f : xi;
         const float exi = 8.1f * u * xi;   // ||x||^2 error (fp32 blocks of 8)
-        const float eps_dot = (tp.cdot * tp.mu_max + tp.floor_coef) * xn;  // any column
+        const float eps_dot = (tp.cdot * sc.mu_max + sc.floor_coef) * xn;  // any column
         const float eps_m = COS ? (eps_dot / xn + 3.0f * u * (fabsf(b1) + 1.0f) + exi / xi)
-                                : (2.0f * eps_dot + 3.0f * u * (fabsf(b1) + tp.p_max + 2.0f * xn * tp.mu_max) + exi);
+                                : (2.0f * eps_dot + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
         int nb = arg;
         // neighbour certain: clear gap, and no tie through the clamps at 0 (and 2)
         const bool full = !((b2 - b1) > 2.0f * eps_m) || nb < 0 || !(rowc + b2 > eps_m) ||
                           (COS && !(rowc + b1 < 2.0f - eps_m));
         if (nb < 0) nb = own == 0 ? 1 : 0;
-        const double4 co = tp.clu[own];  // n, 1/(n-1), Psi
         const bool singleton = co.x == 1.0;
-        const double ed_b = (static_cast<double>(tp.cdot) * __ldg(tp.munorm + nb) + tp.floor_coef) * xn;
-        const double ed_o = (static_cast<double>(tp.cdot) * __ldg(tp.munorm + own) + tp.floor_coef) * xn;
-        const double dob = static_cast<double>(doto) * tp.smul64;
+        const double ed_b =  // per-cluster dot error bounds (tight when cluster norms differ)
+            (static_cast<double>(tp.cdot) * (__half2float(mn_s[nb]) * sc.mu_max) + sc.floor_coef) * xn;
+        const double ed_o = (static_cast<double>(tp.cdot) * co.w + sc.floor_coef) * xn;
+        const double dob = static_cast<double>(doto) * sc.smul64;
         const double mb = static_cast<double>(rowc) + static_cast<double>(b1);
         const double n_o = co.x, r_o = co.y, nr_o = n_o * r_o;
         double a, b, da, db;
@@ -405,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           b = fmax(mb, 0.0);
           a = singleton ? 0.0 : fmax((n_o * xi64 + co.z - 2.0 * n_o * dob) * r_o, 0.0);
-          db = 2.0 * ed_b + 3.0 * u * (fabs(b1) + tp.p_max + 2.0 * xn * tp.mu_max) + exi;
+          db = 2.0 * ed_b + 3.0 * u * (fabs(b1) + sc.p_max + 2.0 * xn * sc.mu_max) + exi;
           da = nr_o * (2.0 * ed_o + exi);
         }
         const double mx = fmax(a, b);
@@ -440,6 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         red_flag[tb * 4 + quad] = anyw != 0;
       }
       named_bar(2 + grp, 128);
+      if (tp.dbg && warp == kEpiWarp0 && lane == 0) atomicAdd(tp.dbg + 13, static_cast<unsigned long long>(clock64() - tf0));
       if (quad == 0 && lane == 0) {
         p.tile_sum[t] = ((red[tb * 4] + red[tb * 4 + 1]) + red[tb * 4 + 2]) + red[tb * 4 + 3];
         p.tile_flag[t] = red_flag[tb * 4] | red_flag[tb * 4 + 1] | red_flag[tb * 4 + 2] | red_flag[tb * 4 + 3];
@@ -447,18 +548,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  if (tp.dbg && lane == 0) {
+    if (warp == 0) atomicAdd(tp.dbg + 9, static_cast<unsigned long long>(clock64() - t_start));
+    if (warp == kEpiWarp0) atomicAdd(tp.dbg + 10, static_cast<unsigned long long>(clock64() - t_start));
+    if (warp == kConvWarp0) atomicAdd(tp.dbg + 11, static_cast<unsigned long long>(clock64() - t_start));
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
 }
 
 // ---------------------------------------------------------------- prep --------
+// Global power-of-two scalings chosen so max|x~| and max|mu~| lie in [2^14, 2^15):
+// ex from max|x| of the shard, em from max|mu_kl| (derive's bound[2]).
+__device__ __forceinline__ int scale_exp(float m) { return m > 0.f ? ilogbf(m) - 14 : 0; }
+
 // B pieces: mu~ = mu * 2^-em split into fp16 hi + lo, [Kp][Dp] zero padded; column
-// bias for the ranking (sqeuclid p_k, cosine 0, padding +inf).
-__global__ void prep_b_kernel(const double* __restrict__ stats, int k, int d, int kp, int dp, bool cos,
-                              float smu, __half* bh, __half* bl, float* colbias, float* munorm,
-                              double4* clu) {
+// bias for the ranking (sqeuclid p_k, cosine 0, padding +inf); per-cluster constants;
+// block 0 also writes the TcScale record the scoring kernel reads.
+__global__ void prep_b_kernel(const double* __restrict__ stats, const float* __restrict__ bound,
+                              const float* __restrict__ xmax, int k, int d, int kp, int dp, bool cos,
+                              __half* bh, __half* bl, float* colbias, __half* munorm, double4* clu,
+                              TcScale* scale) {
   const int c = blockIdx.x;
+  const int em = scale_exp(bound[2]);
+  const float smu = ldexpf(1.0f, -em);
+  if (c == 0 && threadIdx.x == 0) {
+    const float xm = *xmax;
+    const int ex = scale_exp(xm);
+    TcScale t;
+    t.sx = ldexpf(1.0f, -ex);
+    t.smul = ldexpf(1.0f, ex + em);
+    t.smul64 = ldexp(1.0, ex + em);
+    // fp16 subnormal floor: 2^-25 per element in scaled units, sqrt(D) via Cauchy-Schwarz
+    t.floor_coef = 1.05f * 0.5f * 5.9604645e-8f * sqrtf(static_cast<float>(d)) *
+                   (ldexpf(1.0f, em) + ldexpf(1.0f, ex) * bound[0] / fmaxf(xm, 1e-30f));
+    t.mu_max = bound[0];
+    t.p_max = bound[1];
+    t.pad = 0.f;
+    *scale = t;
+  }
   const double n = c < k ? fmax(stats[c], 1.0) : 1.0;
   const double* sums = stats + (cos ? k : 2 * k) + static_cast<int64_t>(c) * d;
   for (int l = threadIdx.x; l < dp; l += blockDim.x) {
@@ -484,8 +613,10 @@ __global__ void prep_b_kernel(const double* __restrict__ stats, int k, int d, in
   __syncthreads();
   if (threadIdx.x == 0) {
     colbias[c] = c < k ? (cos ? 0.0f : static_cast<float>(stats[k + c] / n)) : INFINITY;
-    munorm[c] = __double2float_ru(sqrt(red[0] + red[1] + red[2] + red[3]) * (1.0 + 1e-12));
-    if (c < k) clu[c] = make_double4(n, n > 1.0 ? 1.0 / (n - 1.0) : 0.0, cos ? 0.0 : stats[k + c], 0.0);
+    const double nrm = sqrt(red[0] + red[1] + red[2] + red[3]) * (1.0 + 1e-12);
+    // bound[0] = max ||mu_k|| rounded up, so the ratio is <= 1; every rounding upward
+    munorm[c] = __float2half_ru(__double2float_ru(__ddiv_ru(nrm, fmax(static_cast<double>(bound[0]), 1e-300))));
+    if (c < k) clu[c] = make_double4(n, n > 1.0 ? 1.0 / (n - 1.0) : 0.0, cos ? 0.0 : stats[k + c], nrm);
   }
 }
 
@@ -521,16 +652,26 @@ CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* ptr, uint64_t inner,
 
 int pick_bn(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : 128; }
 
-size_t tc_smem(int bn, int kp) {
-  const size_t ring = bn <= 32 ? TcCfg<32>::kRing : bn <= 64 ? TcCfg<64>::kRing : TcCfg<128>::kRing;
-  return 1024 + ring + 26 * 8 + 2 * BM * 8 + 8 * BM * 4 + 128 + static_cast<size_t>(ncb_bn_pad(kp)) * 4;
+// Shared memory with `nstg` X staging stages: operand ring, staging ring, barriers,
+// meta_xi, merge partials, tile-sum slots, column bias (fp32) and norms (fp16).
+size_t tc_smem(int bn, int kp, int nstg) {
+  const size_t bring = bn <= 32 ? TcCfg<32>::kBRing : bn <= 64 ? TcCfg<64>::kBRing : TcCfg<128>::kBRing;
+  return 1024 + bring + static_cast<size_t>(nstg) * kStgBytes + 46 * 8 + 4 * BM * 8 + 2 * BM * 32 + 8 * BM * 4 +
+         128 + 2 * BM * 4 +
+         static_cast<size_t>(ncb_bn_pad(kp)) * 4 + static_cast<size_t>(kp) * 2 + 16;
+}
+constexpr int kMaxStg = 8;
+int tc_stages(int bn, int kp, size_t optin) {
+  int ns = kMaxStg;
+  while (ns > 2 && tc_smem(bn, kp, ns) > optin) --ns;
+  return ns;
 }
 
 template <int BN, bool COS>
 void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                const TcParams& tp, int64_t ntiles) {
   auto kern = score_tc_kernel<BN, COS>;
-  const size_t smem = tc_smem(BN, tp.ncb * BN);
+  const size_t smem = tc_smem(BN, tp.ncb * BN, tp.nstg);
   FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int grid = static_cast<int>(std::min<int64_t>(ntiles, c->num_sms));
   kern<<<grid, kThreads, smem, c->stream>>>(mx, mh, ml, tp, ntiles);
@@ -542,7 +683,7 @@ void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, co
 bool tc_supported(const fsil_context* c) {
   const int bn = pick_bn(c->k);
   const int kp = (c->k + bn - 1) / bn * bn;
-  return c->d % 4 == 0 && c->n < (int64_t(1) << 31) && c->k >= 2 && tc_smem(bn, kp) <= c->smem_optin;
+  return c->d % 4 == 0 && c->n < (int64_t(1) << 31) && c->k >= 2 && tc_smem(bn, kp, 2) <= c->smem_optin;
 }
 
 int64_t tc_tiles(const fsil_context* c, int* tile_rows) {
@@ -557,21 +698,16 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   const int kp = ncb * bn;
   const int nkc = (c->d + BK - 1) / BK;
   const int dp = nkc * BK;
-  // global power-of-two scalings: max|x~| and max|mu~| in [2^14, 2^15)
-  float h_bound[4] = {0, 0, 0, 0}, h_xmax = 0.f;
-  FSIL_CUDA(cudaMemcpyAsync(h_bound, c->bound.p, sizeof(h_bound), cudaMemcpyDeviceToHost, c->stream));
-  FSIL_CUDA(cudaMemcpyAsync(&h_xmax, c->xmax.p, sizeof(float), cudaMemcpyDeviceToHost, c->stream));
-  FSIL_CUDA(cudaStreamSynchronize(c->stream));
-  const int ex = h_xmax > 0.f ? std::ilogb(h_xmax) - 14 : 0;
-  const int em = h_bound[2] > 0.f ? std::ilogb(h_bound[2]) - 14 : 0;
-  c->tc_b.ensure(2ull * kp * dp * sizeof(__half) + 2ull * kp * sizeof(float) + kp * sizeof(double4) + 64);
+  c->tc_b.ensure(2ull * kp * dp * sizeof(__half) + kp * (sizeof(float) + sizeof(__half)) +
+                 (kp + 1) * sizeof(double4) + 64);
   __half* bh = c->tc_b.as<__half>();
   __half* bl = bh + static_cast<size_t>(kp) * dp;
   float* colbias = reinterpret_cast<float*>(bl + static_cast<size_t>(kp) * dp);
-  float* munorm = colbias + kp;
+  __half* munorm = reinterpret_cast<__half*>(colbias + kp);
   double4* clu = reinterpret_cast<double4*>((reinterpret_cast<uintptr_t>(munorm + kp) + 31) & ~uintptr_t(31));
-  prep_b_kernel<<<kp, 128, 0, c->stream>>>(p.stats, c->k, c->d, kp, dp, cos, std::ldexp(1.0f, -em), bh, bl,
-                                           colbias, munorm, clu);
+  TcScale* scale = reinterpret_cast<TcScale*>(clu + kp);
+  prep_b_kernel<<<kp, 128, 0, c->stream>>>(p.stats, c->bound.as<float>(), c->xmax.as<float>(), c->k, c->d, kp,
+                                           dp, cos, bh, bl, colbias, munorm, clu, scale);
   FSIL_LAUNCHED(c);
   const CUtensorMap mx = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, c->X, c->d, c->n, c->d * 4ull, 32, BM);
   const CUtensorMap mh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, bh, dp, kp, dp * 2ull, BK, bn);
@@ -580,29 +716,34 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   tp.p = p;
   tp.ncb = ncb;
   tp.nkc = nkc;
-  tp.sx = std::ldexp(1.0f, -ex);
-  tp.smul = std::ldexp(1.0f, ex + em);
-  tp.smul64 = std::ldexp(1.0, ex + em);
   tp.colbias = colbias;
-  tp.munorm = munorm;
   tp.clu = clu;
+  tp.munorm = munorm;
+  tp.scale = scale;
+  tp.nstg = tc_stages(bn, kp, c->smem_optin);
   // |dot error| <= cdot*||x||*||mu|| + floor: split residuals 3*2^-22 relative; fp32
   // accumulation of the main term over ceil(D/16) MMA steps at 2^-24 (the correction
   // accumulator holds values <= 2^-10 of it); the final main+correction add; and the
   // fp16 subnormal floor 2^-25 per element in scaled units (sqrt(D) via Cauchy-Schwarz).
   const float u = 5.9604645e-8f;
   const float steps = static_cast<float>((c->d + 15) / 16);
-  tp.cdot = 1.05f * (12.0f + steps + 1.0f + 2.0f * steps / 512.0f) * u;
-  tp.floor_coef = 1.05f * 0.5f * u * std::sqrt(static_cast<float>(c->d)) *
-                  (std::ldexp(1.0f, em) + std::ldexp(1.0f, ex) * h_bound[0] / std::max(h_xmax, 1e-30f));
-  tp.mu_max = h_bound[0];
-  tp.p_max = h_bound[1];
+  tp.split = c->d > 128 ? 1 : 0;
+  if (const char* e = std::getenv("FSIL_TC_SPLIT")) tp.split = std::atoi(e) ? 1 : 0;  // experiments
+  tp.cdot = tp.split ? 1.05f * (12.0f + steps + 1.0f + 2.0f * steps / 512.0f) * u
+                     : 1.05f * (12.0f + 3.0f * steps + 1.0f) * u;  // all 3 terms, one accumulator
   c->exact_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int2));
   c->exact_count.ensure(sizeof(unsigned long long));
   FSIL_CUDA(cudaMemsetAsync(c->exact_count.p, 0, sizeof(unsigned long long), c->stream));
   tp.exact_rows = c->exact_rows.as<int2>();
   tp.exact_count = c->exact_count.as<unsigned long long>();
   const int64_t ntiles = (c->n + BM - 1) / BM;
+  static const bool prof = std::getenv("FSIL_TC_PROFILE") != nullptr;
+  unsigned long long* dbg = nullptr;
+  if (prof) {
+    FSIL_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
+    FSIL_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), c->stream));
+  }
+  tp.dbg = dbg;
   if (cos) {
     if (bn == 32) launch_tc<32, true>(c, mx, mh, ml, tp, ntiles);
     else if (bn == 64) launch_tc<64, true>(c, mx, mh, ml, tp, ntiles);
@@ -613,6 +754,20 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     else launch_tc<128, false>(c, mx, mh, ml, tp, ntiles);
   }
   c->tc_exact_used = true;
+  if (dbg) {
+    unsigned long long h[16];
+    FSIL_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    FSIL_CUDA(cudaStreamSynchronize(c->stream));
+    const char* names[14] = {"X-prod stg_empty", "B-prod op_empty", "MMA acc_empty", "MMA op_full",
+                             "conv stg_full", "conv op_empty", "conv meta_empty", "epi meta_full",
+                             "epi acc_full", "T prod", "T epi(w2)", "T conv(w10)", "w2 scan", "w2 finalize"};
+    const double ctas = static_cast<double>(std::min<int64_t>(ntiles, c->num_sms));
+    std::fprintf(stderr, "[fsil tc profile] bn=%d nstg=%d split=%d per-CTA Mcycles (waits summed over the role's warps):",
+                 bn, tp.nstg, tp.split);
+    for (int i = 0; i < 14; ++i) std::fprintf(stderr, " %s=%.3f", names[i], h[i] / ctas / 1e6);
+    std::fprintf(stderr, "\n");
+    cudaFree(dbg);
+  }
 }
 
 }  // namespace fsil

@@ -39,7 +39,12 @@ def test_library_is_sm100a_native():
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", so], capture_output=True,
                           text=True).stdout
     assert "FFMA2" in sass, "packed FFMA2 missing from the FFMA scoring kernel"
-    assert "score_ffma_kernel" in sass and "agg_private_kernel" in sass
+    for kern in ("score_ffma_kernel", "score_tc_kernel", "agg_stage_kernel", "agg_warp_kernel",
+                 "agg_piece_kernel", "densify_collect_kernel", "refine_kernel"):
+        assert kern in sass, kern
+    # tcgen05 MMA (UTCHMMA), TMA tensor loads (UTMALDG) and bulk copies (UBLKCP)
+    for op in ("UTCHMMA", "UTMALDG", "UBLKCP"):
+        assert op in sass, op
 
 
 def test_host_entries_match_oracle():
