@@ -59,8 +59,11 @@ class OracleShardOps:
         return self.part
 
     def finish(self):
-        if int(self.checks[0]) != np.iinfo(np.int64).max:
-            raise ValueError("non-finite")
+        # same decoding of the MIN-reduced validation word as fsil_shard_finish (capi.cu)
+        bad = int(self.checks[0])
+        if bad != np.iinfo(np.int64).max:
+            d = self.X.shape[1]
+            raise ValueError(f"non-finite feature value at point {bad // d}, dimension {bad % d}")
         return float(self.part[0]) / self.n_global
 
 
@@ -72,8 +75,11 @@ def _worker(rank, world, port, metric, X, L, ret):
     b, e = ranges[rank]
     ops = OracleShardOps(metric, X[b:e], L[b:e], b)
     ops.n_global = n
-    mean = run_sharded(ops, torch.device("cpu"))
-    ret[rank] = (mean, ops.raw.tolist())
+    try:
+        mean = run_sharded(ops, torch.device("cpu"))
+        ret[rank] = (mean, ops.raw.tolist())
+    except ValueError as e:
+        ret[rank] = ("error", str(e))
     dist.destroy_process_group()
 
 
@@ -106,3 +112,19 @@ def test_merge_dictionaries_single_rank():
         assert raw.tolist() == [4, 2, 9]
     finally:
         dist.destroy_process_group()
+
+
+def test_sharded_validation_error_is_global():
+    """A non-finite value on any shard fails every rank with the same message, naming
+    the lowest global (row, dimension) -- the reference's first-offender order
+    (dataset.cpp:35-37) -- via the MIN all-reduce of the validation word."""
+    rng = np.random.default_rng(7)
+    n, d, world = 900, 5, 3
+    X = rng.normal(size=(n, d)).astype(np.float32)
+    L = rng.integers(0, 4, n)
+    X[700, 2] = np.nan   # shard 2
+    X[450, 4] = np.inf   # shard 1: the first offender in dataset order
+    out = _run(world, "sqeuclid", X, L, 29587)
+    for tag, msg in out:
+        assert tag == "error"
+        assert msg == "non-finite feature value at point 450, dimension 4"
