@@ -575,6 +575,17 @@ int pick_lpr(int d, int vec) {
   return lpr;
 }
 
+// stats <- 0, validation word <- none, max|x| <- 0 (one launch instead of three copies)
+__global__ void agg_init_kernel(double* stats, int64_t S, int64_t* checks, float* xmax) {
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int64_t i = i0; i < S; i += static_cast<int64_t>(gridDim.x) * blockDim.x) stats[i] = 0.0;
+  if (i0 == 0) {
+    checks[0] = kNone;
+    checks[1] = kNone;
+    *xmax = 0.f;
+  }
+}
+
 template <bool COS>
 void launch_stage(fsil_context* c, int dpl, int warps, int64_t chunk, size_t smem, double* partials,
                   int64_t* checks) {
@@ -641,11 +652,10 @@ void aggregate(fsil_context* c) {
   c->checks.ensure(2 * sizeof(int64_t));
   double* stats = c->stats_buf.as<double>();
   int64_t* checks = c->checks.as<int64_t>();
-  const int64_t none[2] = {kNone, kNone};
-  FSIL_CUDA(cudaMemcpyAsync(checks, none, sizeof(none), cudaMemcpyHostToDevice, c->stream));
-  FSIL_CUDA(cudaMemsetAsync(stats, 0, S * sizeof(double), c->stream));
   c->xmax.ensure(sizeof(float));
-  FSIL_CUDA(cudaMemsetAsync(c->xmax.p, 0, sizeof(float), c->stream));
+  agg_init_kernel<<<static_cast<unsigned>(std::min<int64_t>((S + 255) / 256 + 1, 1024)), 256, 0, c->stream>>>(
+      stats, S, checks, c->xmax.as<float>());
+  FSIL_LAUNCHED(c);
   if (c->n == 0) {
     c->agg_path = 0;
     return;

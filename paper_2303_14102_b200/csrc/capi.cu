@@ -174,17 +174,30 @@ void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, 
   finalize_sum(c, p, ntiles, tile_rows);
 }
 
+__global__ void pack_summary_kernel(const int64_t* __restrict__ checks, const double* __restrict__ result,
+                                    const int* __restrict__ missing, HostSummary* out) {
+  if (threadIdx.x == 0) {
+    out->checks[0] = checks[0];
+    out->checks[1] = checks[1];
+    out->missing = *missing;
+    out->result[0] = result[0];
+    out->result[1] = result[1];
+    out->result[2] = result[2];
+  }
+}
+
 // Reads the (all-reduced) validation word and sum; raises in the reference's order.
 double finish(fsil_context* c, double* flagged_out) {
   if (c->phase < 4) fail(FSIL_ERR_INVALID_ARGUMENT, "score must come before finish");
-  int64_t checks[2] = {kNone, kNone};
-  double res[3] = {0, 0, 0};
-  int missing = 0;
-  FSIL_CUDA(cudaMemcpyAsync(checks, c->checks.p, sizeof(checks), cudaMemcpyDeviceToHost, c->stream));
-  FSIL_CUDA(cudaMemcpyAsync(res, c->result.p, sizeof(res), cudaMemcpyDeviceToHost, c->stream));
-  FSIL_CUDA(cudaMemcpyAsync(&missing, c->counters.as<int>() + 4, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  pack_summary_kernel<<<1, 32, 0, c->stream>>>(c->checks.as<int64_t>(), c->result.as<double>(),
+                                               c->counters.as<int>() + 4, c->dsum);
+  FSIL_LAUNCHED(c);
   record(c, 6);
   FSIL_CUDA(cudaStreamSynchronize(c->stream));
+  const volatile HostSummary* hs = c->hsum;
+  const int64_t checks[2] = {hs->checks[0], hs->checks[1]};
+  const double res[3] = {hs->result[0], hs->result[1], hs->result[2]};
+  const int missing = static_cast<int>(hs->missing);
   FSIL_CUDA(cudaGetLastError());
   c->phase = 0;
   if (checks[0] != kNone) {
@@ -315,6 +328,12 @@ fsil_status fsil_create(fsil_context** out, int device) {
     FSIL_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
     for (auto& e : c->ev) FSIL_CUDA(cudaEventCreate(&e));
+    void* hs = nullptr;
+    FSIL_CUDA(cudaHostAlloc(&hs, sizeof(fsil::HostSummary), cudaHostAllocMapped));
+    c->hsum = static_cast<fsil::HostSummary*>(hs);
+    void* ds = nullptr;
+    FSIL_CUDA(cudaHostGetDevicePointer(&ds, hs, 0));
+    c->dsum = static_cast<fsil::HostSummary*>(ds);
   });
   if (st != FSIL_OK) {
     g_create_error = c->last_error;  // reachable through fsil_last_error(NULL)
@@ -340,6 +359,7 @@ void fsil_destroy(fsil_context* c) {
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (c->hsum) cudaFreeHost(c->hsum);
   delete c;
 }
 

@@ -47,26 +47,43 @@ __global__ void __launch_bounds__(256) densify_collect_kernel(const int32_t* __r
     svals[i] = 0xffffffffu;
   }
   __syncthreads();
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const unsigned long long key = label_key(labels[i]);
-    const uint32_t row = static_cast<uint32_t>(i);
-    uint32_t h = hash32(static_cast<uint32_t>(key)) & (kSmemSlots - 1);
-    bool done = false;
-    for (int probe = 0; probe < 16; ++probe) {  // bounded: overflow goes global
-      unsigned long long cur = skeys[h];
-      if (cur == 0) {
-        const unsigned long long prev = atomicCAS(skeys + h, 0ull, key);
-        cur = prev == 0 ? key : prev;
-      }
-      if (cur == key) {
-        if (row < svals[h]) atomicMin(svals + h, row);
-        done = true;
-        break;
-      }
-      h = (h + 1) & (kSmemSlots - 1);
+  // Four rows per thread per step (independent loads in flight); within a warp only the
+  // lowest lane of each run of equal labels (= the lowest row) touches the table.
+  const int lane = threadIdx.x & 31;
+  constexpr int U = 4;
+  const int64_t bstride = static_cast<int64_t>(gridDim.x) * blockDim.x * U;
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * U; base < n; base += bstride) {
+    int32_t lab[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * blockDim.x + threadIdx.x;
+      lab[u] = i < n ? __ldg(labels + i) : 0;
     }
-    if (!done && !global_insert(gkeys, gvals, cap_mask, key, row)) atomicExch(overflow, 1);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * blockDim.x + threadIdx.x;
+      const bool valid = i < n;
+      const unsigned long long key = valid ? label_key(lab[u]) : 0ull;
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      if (!valid || (__ffs(peers) - 1) != lane) continue;
+      const uint32_t row = static_cast<uint32_t>(i);
+      uint32_t h = hash32(static_cast<uint32_t>(key)) & (kSmemSlots - 1);
+      bool done = false;
+      for (int probe = 0; probe < 16; ++probe) {  // bounded: overflow goes global
+        unsigned long long cur = skeys[h];
+        if (cur == 0) {
+          const unsigned long long prev = atomicCAS(skeys + h, 0ull, key);
+          cur = prev == 0 ? key : prev;
+        }
+        if (cur == key) {
+          if (row < svals[h]) atomicMin(svals + h, row);
+          done = true;
+          break;
+        }
+        h = (h + 1) & (kSmemSlots - 1);
+      }
+      if (!done && !global_insert(gkeys, gvals, cap_mask, key, row)) atomicExch(overflow, 1);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kSmemSlots; i += blockDim.x) {
@@ -120,7 +137,12 @@ __global__ void __launch_bounds__(256) densify_map_kernel(const int32_t* __restr
                                                           const unsigned long long* __restrict__ gkeys,
                                                           const int32_t* __restrict__ gdense,
                                                           uint32_t cap_mask, int32_t* dense,
-                                                          int* missing) {
+                                                          int* missing, const int* counters,
+                                                          HostSummary* hsum) {
+  if (hsum && blockIdx.x == 0 && threadIdx.x == 0) {  // K and overflow for the host (final here)
+    hsum->overflow = counters[0];
+    hsum->count = static_cast<int64_t>(*reinterpret_cast<const unsigned long long*>(counters + 2));
+  }
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int64_t slot = find_slot(gkeys, cap_mask, label_key(labels[i]));
@@ -281,21 +303,18 @@ void densify_local(fsil_context* c) {
     FSIL_LAUNCHED(c);
     densify_map_kernel<<<grid_for(c->n, 256, c->num_sms, 8), 256, 0, c->stream>>>(
         c->labels, c->n, c->ht_keys.as<unsigned long long>(), c->ht_dense.as<int32_t>(), mask,
-        c->dense.as<int32_t>(), missing);
+        c->dense.as<int32_t>(), missing, c->counters.as<int>(), c->dsum);
     FSIL_LAUNCHED(c);
-    struct {
-      int overflow, pad;
-      unsigned long long count;
-    } h{};
-    FSIL_CUDA(cudaMemcpyAsync(&h, c->counters.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-    FSIL_CUDA(cudaStreamSynchronize(c->stream));
-    if (h.overflow) {
+    FSIL_CUDA(cudaStreamSynchronize(c->stream));  // the one host sync: K decides the kernels
+    const volatile HostSummary* hs = c->hsum;
+    const int64_t over = hs->overflow, cnt = hs->count;
+    if (over) {
       cap *= 4;
       continue;
     }
-    c->ht_cap = static_cast<int64_t>(h.count) * 2 > cap ? cap * 2 : cap;
-    c->n_distinct = static_cast<int64_t>(h.count);
-    c->k = static_cast<int32_t>(h.count);
+    c->ht_cap = cnt * 2 > cap ? cap * 2 : cap;
+    c->n_distinct = cnt;
+    c->k = static_cast<int32_t>(cnt);
     c->dict_sorted_labels = sorted_labels;
     return;
   }
@@ -320,7 +339,7 @@ void densify_assign_and_map(fsil_context* c, const int32_t* raw_in_dense_order, 
   if (c->n > 0) {
     densify_map_kernel<<<grid_for(c->n, 256, c->num_sms, 8), 256, 0, c->stream>>>(
         c->labels, c->n, c->ht_keys.as<unsigned long long>(), c->ht_dense.as<int32_t>(),
-        static_cast<uint32_t>(cap - 1), c->dense.as<int32_t>(), missing);
+        static_cast<uint32_t>(cap - 1), c->dense.as<int32_t>(), missing, nullptr, nullptr);
     FSIL_LAUNCHED(c);
   }
   // `missing` is checked by the caller at the end of the call (no extra sync here).

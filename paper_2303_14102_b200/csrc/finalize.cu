@@ -15,36 +15,67 @@
 namespace fsil {
 namespace {
 
+// One warp per flagged row.  x is staged once in shared memory (fp64); the warp walks
+// the clusters 32 at a time: every lane accumulates partial dots over its dimensions
+// (l = lane + 32 i, coalesced reads of each Y_k) for all 32 clusters, then a butterfly
+// transpose-reduce leaves lane j holding the full dot of cluster kc + j (31 shuffles
+// per 32 clusters instead of 5 per cluster).  Each lane keeps its ascending-k running
+// argmin (strict <); the warp merge breaks ties towards the lowest k.
 template <bool COS>
 __global__ void __launch_bounds__(256) refine_kernel(ScoreParams p) {
+  extern __shared__ double xs_all[];  // [warps per block][d]
   const unsigned long long count = *p.flag_count;
   const int lane = threadIdx.x & 31;
+  double* xs = xs_all + static_cast<int64_t>(threadIdx.x >> 5) * p.d;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const double* sums = p.stats + (COS ? p.k : 2 * p.k);
+  const int d = p.d, K = p.k;
   for (int64_t i = warp; i < static_cast<int64_t>(count); i += nwarps) {
     const int64_t row = p.flag_rows[i];
-    const float* x = p.X + row * p.d;
+    const float* x = p.X + row * d;
     const int own = p.dense[row];
     double ss = 0.0;
-    for (int l = lane; l < p.d; l += 32) {
+    __syncwarp();
+    for (int l = lane; l < d; l += 32) {
       const double v = x[l];
+      xs[l] = v;
       ss = fma(v, v, ss);
     }
     for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    __syncwarp();
     const double nrm = sqrt(ss);
     double best = INFINITY;
     int arg = -1;
-    for (int k = lane; k < p.k; k += 32) {  // ascending within the lane
-      if (k == own) continue;
-      const double* yk = sums + static_cast<int64_t>(k) * p.d;
-      double cross = 0.0;
-      for (int l = 0; l < p.d; ++l) cross = fma(yk[l], static_cast<double>(x[l]), cross);
-      const double m = COS ? cos_foreign(p.nk[k], cross / nrm)
-                           : sq_foreign(ss, p.stats[p.k + k], p.nk[k], cross);
-      if (m < best) {
-        best = m;
-        arg = k;
+    for (int kc = 0; kc < K; kc += 32) {
+      double acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+      for (int l = lane; l < d; l += 32) {
+        const double xv = xs[l];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int k = kc + j < K ? kc + j : K - 1;  // clamped; result unused
+          acc[j] = fma(__ldg(sums + static_cast<int64_t>(k) * d + l), xv, acc[j]);
+        }
+      }
+#pragma unroll
+      for (int sft = 16; sft >= 1; sft >>= 1) {  // transpose-reduce: acc[0] of lane j = cluster kc+j
+        const bool up = (lane & sft) != 0;
+#pragma unroll
+        for (int j = 0; j < sft; ++j) {
+          const double send = up ? acc[j] : acc[j + sft];
+          const double keep = up ? acc[j + sft] : acc[j];
+          acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+        }
+      }
+      const int k = kc + lane;
+      if (k < K && k != own) {
+        const double m = COS ? cos_foreign(p.nk[k], acc[0] / nrm) : sq_foreign(ss, p.stats[p.k + k], p.nk[k], acc[0]);
+        if (m < best) {
+          best = m;
+          arg = k;
+        }
       }
     }
     // warp argmin with ties broken towards the lowest k
@@ -57,9 +88,9 @@ __global__ void __launch_bounds__(256) refine_kernel(ScoreParams p) {
       }
     }
     // own-cluster mean, dims split over lanes
-    const double* yo = sums + static_cast<int64_t>(own) * p.d;
+    const double* yo = sums + static_cast<int64_t>(own) * d;
     double co = 0.0;
-    for (int l = lane; l < p.d; l += 32) co = fma(yo[l], static_cast<double>(x[l]), co);
+    for (int l = lane; l < d; l += 32) co = fma(yo[l], xs[l], co);
     for (int off = 16; off > 0; off >>= 1) co += __shfl_xor_sync(0xffffffffu, co, off);
     if (lane == 0) {
       const double n_o = p.nk[own];
@@ -222,9 +253,19 @@ void flag_all(fsil_context* c, const ScoreParams& p, int tile_rows) {
 }
 
 void refine(fsil_context* c, const ScoreParams& p) {
-  const int grid = c->num_sms * 4;
-  if (c->metric == FSIL_COSINE) refine_kernel<true><<<grid, 256, 0, c->stream>>>(p);
-  else refine_kernel<false><<<grid, 256, 0, c->stream>>>(p);
+  // warps per block limited by the staged rows (fp64 x per warp)
+  const size_t row_bytes = static_cast<size_t>(c->d) * sizeof(double);
+  const int wpb = static_cast<int>(std::min<size_t>(8, c->smem_optin / row_bytes));
+  if (wpb < 1) fail(FSIL_ERR_INVALID_ARGUMENT, "refinement: D too large for shared memory");
+  const size_t smem = wpb * row_bytes;
+  const int grid = c->num_sms * 32 / wpb;
+  if (c->metric == FSIL_COSINE) {
+    FSIL_CUDA(cudaFuncSetAttribute(refine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    refine_kernel<true><<<grid, 32 * wpb, smem, c->stream>>>(p);
+  } else {
+    FSIL_CUDA(cudaFuncSetAttribute(refine_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    refine_kernel<false><<<grid, 32 * wpb, smem, c->stream>>>(p);
+  }
   FSIL_LAUNCHED(c);
 }
 

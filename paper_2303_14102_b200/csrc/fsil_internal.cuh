@@ -82,6 +82,17 @@ struct Derived {
 //   [1] first zero-norm row (cosine only; INT64_MAX if none)
 constexpr int64_t kNone = INT64_MAX;
 
+// Per-call words the host reads back, written by kernels straight into mapped pinned
+// memory (one stream sync, no pageable copies).
+struct HostSummary {
+  int64_t overflow;   // densify: hash table overflowed (retry with a larger table)
+  int64_t count;      // densify: distinct labels (K)
+  int64_t checks[2];  // validation word (after the caller's MIN all-reduce in shard mode)
+  int64_t missing;    // a row's label absent from the dictionary
+  int64_t pad;
+  double result[4];   // sum of s_i, flagged rows, exact rows
+};
+
 }  // namespace fsil
 
 // ---- context (C ABI handle) ----------------------------------------------------------------
@@ -131,6 +142,8 @@ struct fsil_context {
   fsil::DevBuf hX, hL;         // device copies of host inputs
   fsil::DevBuf o_s, o_nb, o_own, o_a, o_b;
   int64_t ht_cap = 0;
+  fsil::HostSummary* hsum = nullptr;  // mapped pinned (host view)
+  fsil::HostSummary* dsum = nullptr;  // device view of the same memory
   cudaEvent_t ev[8] = {};
 };
 
