@@ -84,8 +84,10 @@ void fsil_destroy(fsil_context* ctx);
 const char* fsil_last_error(const fsil_context* ctx);
 int fsil_abi_version(void);
 
-/* Stream used by every kernel of this context (cudaStream_t; NULL = a
- * context-owned stream). */
+/* Stream used by every kernel of this context (cudaStream_t).  NULL selects a
+ * context-owned non-blocking stream (the default); to order with work on the
+ * legacy default stream -- e.g. a framework's stream 0 and collectives issued
+ * on it -- pass cudaStreamLegacy ((void*)0x1), not NULL. */
 fsil_status fsil_set_stream(fsil_context* ctx, void* stream);
 fsil_status fsil_set_path(fsil_context* ctx, int path);
 /* Per-phase CUDA-event timing on the context stream (adds no syncs beyond the call's own). */

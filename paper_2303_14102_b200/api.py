@@ -59,6 +59,9 @@ EXPORTS = {
 }
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the (synchronising) legacy default stream
+
+
 class ValidationError(ValueError):
     """fastsil::ValidationError (types.hpp:41-44): a dataset/argument invariant."""
 
@@ -181,6 +184,12 @@ class Context:
 
     # -- configuration --------------------------------------------------------
     def set_stream(self, stream_handle: Optional[int]):
+        """Run on `stream_handle` (a cudaStream_t as int, e.g. torch's
+        `current_stream().cuda_stream`).  0 -- torch's default stream -- means the
+        legacy default stream (cudaStreamLegacy), so the kernels order with torch
+        and NCCL work on it; None returns to a context-owned stream."""
+        if stream_handle == 0:
+            stream_handle = CUDA_STREAM_LEGACY
         self._check(lib().fsil_set_stream(self._h, stream_handle))
 
     def set_path(self, path: int):
