@@ -141,7 +141,10 @@ struct fsil_context {
   // host staging for fsil_silhouette (pageable -> pinned)
   fsil::DevBuf hX, hL;         // device copies of host inputs
   fsil::DevBuf o_s, o_nb, o_own, o_a, o_b;
-  int64_t ht_cap = 0;
+  int64_t ht_cap = 0;        // hash-table slots wanted for the next call
+  int64_t ht_alloc_cap = 0;  // slots of the current (zero-initialised) table
+  uint32_t ht_epoch = 0;     // epoch of the last densify (table entries are epoch-tagged)
+  int64_t k_last = 0;        // K of the previous call (picks the ordering path)
   fsil::HostSummary* hsum = nullptr;  // mapped pinned (host view)
   fsil::HostSummary* dsum = nullptr;  // device view of the same memory
   cudaEvent_t ev[8] = {};
