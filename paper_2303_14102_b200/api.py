@@ -22,7 +22,7 @@ from typing import Optional
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libfsil.so")
+LIB_PATH = os.environ.get("FSIL_LIB_PATH") or os.path.join(_PKG, "libfsil.so")  # override: A/B builds
 DATAGEN_PATH = os.path.join(_PKG, "libfsil_datagen.so")
 
 SQEUCLID, COSINE, EUCLID = 0, 1, 2

@@ -470,8 +470,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(meta_empty + tb);
 
-      // ---- certification and a_i, b_i, s_i (no fp64 divisions: per-cluster
-      // reciprocals precomputed, 1/||x|| and 1/max(a,b) by Newton steps in fp64)
+      // ---- certification and a_i, b_i, s_i.  Cosine in fp32: the inputs (tensor-core
+      // dots) carry fp32-level certified errors already, the fp32 evaluation adds its
+      // own rounding terms to the bounds, and s_i's final rounding (~3u) stays well
+      // inside the 1e-5 bar on top of kTau.  Squared Euclidean in fp64 (cancellation).
       double s = 0.0;
       bool any = false;
       if (valid) {
@@ -487,40 +489,58 @@ __global__ void __launch_bounds__(kThreads, 1)
                           (COS && !(rowc + b1 < 2.0f - eps_m));
         if (nb < 0) nb = own == 0 ? 1 : 0;
         const bool singleton = co.x == 1.0;
-        const double ed_b =  // per-cluster dot error bounds (tight when cluster norms differ)
-            (static_cast<double>(tp.cdot) * (__half2float(mn_s[nb]) * sc.mu_max) + sc.floor_coef) * xn;
-        const double ed_o = (static_cast<double>(tp.cdot) * co.w + sc.floor_coef) * xn;
-        const double dob = static_cast<double>(doto) * sc.smul64;
-        const double mb = static_cast<double>(rowc) + static_cast<double>(b1);
-        const double n_o = co.x, r_o = co.y, nr_o = n_o * r_o;
-        double a, b, da, db;
+        // per-cluster dot error bounds per unit ||x|| (tight when cluster norms differ)
+        const float eb1 = tp.cdot * (__half2float(mn_s[nb]) * sc.mu_max) + sc.floor_coef;
+        const float eo1 = tp.cdot * static_cast<float>(co.w) + sc.floor_coef;
+        float a32, b32;
+        bool inexact;
         if (COS) {
-          double rn = static_cast<double>(rsqrtf(xi));
-          rn = rn * (1.5 - 0.5 * xi64 * rn * rn);
-          rn = rn * (1.5 - 0.5 * xi64 * rn * rn);  // 1/||x|| to ~1e-16
-          b = fmin(fmax(mb, 0.0), 2.0);
-          a = singleton ? 0.0 : fmin(fmax((n_o - n_o * dob * rn) * r_o, 0.0), 2.0);
-          db = ed_b * rn + 3.0 * u * (fabs(b1) + 1.0) + exi / xi;
-          da = nr_o * (ed_o * rn + exi / xi);
+          // cosine: everything O(1) -- fp32 evaluation, its roundings in the bounds
+          const float dob = doto * sc.smul;  // exact (power-of-two scale)
+          const float n_o = static_cast<float>(co.x), r_o = static_cast<float>(co.y), nr_o = n_o * r_o;
+          const float rnf = rsqrtf(xi);  // 1/||x||: rsqrt (<= 2 ulp) of the rounded xi
+          const float t = n_o * dob * rnf;
+          const float b = fminf(fmaxf(1.0f + b1, 0.0f), 2.0f);
+          const float a = singleton ? 0.0f : fminf(fmaxf((n_o - t) * r_o, 0.0f), 2.0f);
+          const float db = 1.01f * (eb1 + 3.0f * u * (fabsf(b1) + 1.0f) + 8.1f * u + u * b);
+          // dots; ||x||^2 and rsqrt (8.1u/2 + 2.5u); the four fp32 roundings of a
+          const float da = 1.01f * (nr_o * (eo1 + 8.1f * u) + 3.0f * u * nr_o * fabsf(dob * rnf) +
+                                    5.0f * u * (n_o + fabsf(t)) * r_o);
+          const float mx = fmaxf(a, b);
+          if (!singleton && mx > 0.0f) s = a <= b ? 1.0f - __fdividef(a, b) : __fdividef(b, a) - 1.0f;
+          inexact = !singleton && !(mx > 2.0f * (da + db) && (da + db) <= kTau * mx);
+          a32 = a;
+          b32 = b;
         } else {
-          b = fmax(mb, 0.0);
-          a = singleton ? 0.0 : fmax((n_o * xi64 + co.z - 2.0 * n_o * dob) * r_o, 0.0);
-          db = 2.0 * ed_b + 3.0 * u * (fabs(b1) + sc.p_max + 2.0 * xn * sc.mu_max) + exi;
-          da = nr_o * (2.0 * ed_o + exi);
+          // sqeuclid: n xi + Psi - 2 n dot cancels heavily when ||x|| >> the cluster
+          // spread -- fp64 (no divisions: per-cluster reciprocals, Newton 1/max(a,b))
+          const double ed_b = static_cast<double>(eb1) * xn, ed_o = static_cast<double>(eo1) * xn;
+          const double dob = static_cast<double>(doto) * sc.smul64;
+          const double n_o = co.x, r_o = co.y, nr_o = n_o * r_o;
+          const double b = fmax(static_cast<double>(rowc) + static_cast<double>(b1), 0.0);
+          const double a = singleton ? 0.0 : fmax((n_o * xi64 + co.z - 2.0 * n_o * dob) * r_o, 0.0);
+          const double db = 2.0 * ed_b + 3.0 * u * (fabs(b1) + sc.p_max + 2.0 * xn * sc.mu_max) + exi;
+          const double da = nr_o * (2.0 * ed_o + exi);
+          const double mx = fmax(a, b);
+          if (!singleton && mx > 0.0) {  // assemble_score without a division
+            double rm = static_cast<double>(__frcp_rn(static_cast<float>(mx)));
+            rm = rm * (2.0 - mx * rm);
+            rm = rm * (2.0 - mx * rm);
+            s = a <= b ? 1.0 - a * rm : b * rm - 1.0;
+          }
+          inexact = !singleton && !(mx > 2.0 * (da + db) && (da + db) <= static_cast<double>(kTau) * mx);
+          a32 = 0.f;
+          b32 = 0.f;
+          if (p.a) p.a[row] = a;
+          if (p.b) p.b[row] = b;
         }
-        const double mx = fmax(a, b);
-        if (!singleton && mx > 0.0) {  // assemble_score without a division
-          double rm = static_cast<double>(__frcp_rn(static_cast<float>(mx)));
-          rm = rm * (2.0 - mx * rm);
-          rm = rm * (2.0 - mx * rm);
-          s = a <= b ? 1.0 - a * rm : b * rm - 1.0;
-        }
-        const bool inexact = !singleton && !(mx > 2.0 * (da + db) && (da + db) <= static_cast<double>(kTau) * mx);
         p.s[row] = s;
         if (p.nb) p.nb[row] = nb;
         if (p.own) p.own[row] = own;
-        if (p.a) p.a[row] = a;
-        if (p.b) p.b[row] = b;
+        if (COS) {
+          if (p.a) p.a[row] = a32;
+          if (p.b) p.b[row] = b32;
+        }
         if (full) {
           const unsigned long long idx = atomicAdd(p.flag_count, 1ull);
           p.flag_rows[idx] = static_cast<int32_t>(row);
