@@ -285,16 +285,47 @@ __global__ void __launch_bounds__(13 * 32, 1) agg_stage_kernel(
       odd = __any_sync(0xffffffffu, bad);
     }
     if (full_stage && !odd) {
-      // ---- fast path: 8 valid rows, no checks
+      // ---- fast path: 8 valid rows, no checks.  Groups of four rows with distinct
+      // labels (warp-uniform test) issue all their shared-memory loads before any
+      // store, so the read-modify-writes overlap instead of serialising on a possible
+      // alias; a group with a repeated label goes row by row.
       if (lane < U) atomicAdd(wcnt + lab_l, 1);
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int lab = __shfl_sync(0xffffffffu, lab_l, u);
-        double* ys = wsum + lab * d + lane;
+      for (int g = 0; g < U; g += 4) {
+        int lab[4];
 #pragma unroll
-        for (int q = 0; q < DPL; ++q)
-          ys[32 * q] = COS ? fma(static_cast<double>(v[u][q]), inv[u], ys[32 * q]) : ys[32 * q] + static_cast<double>(v[u][q]);
-        if (!COS) wpsi[lab * 32 + lane] += ss[u];
+        for (int u = 0; u < 4; ++u) lab[u] = __shfl_sync(0xffffffffu, lab_l, g + u);
+        const bool distinct = lab[0] != lab[1] && lab[0] != lab[2] && lab[0] != lab[3] && lab[1] != lab[2] &&
+                              lab[1] != lab[3] && lab[2] != lab[3];
+        if (distinct) {
+          double base[4][DPL], pb[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double* ys = wsum + lab[u] * d + lane;
+#pragma unroll
+            for (int q = 0; q < DPL; ++q) base[u][q] = ys[32 * q];
+            if (!COS) pb[u] = wpsi[lab[u] * 32 + lane];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            double* ys = wsum + lab[u] * d + lane;
+#pragma unroll
+            for (int q = 0; q < DPL; ++q)
+              ys[32 * q] = COS ? fma(static_cast<double>(v[g + u][q]), inv[g + u], base[u][q])
+                               : base[u][q] + static_cast<double>(v[g + u][q]);
+            if (!COS) wpsi[lab[u] * 32 + lane] = pb[u] + ss[g + u];
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            double* ys = wsum + lab[u] * d + lane;
+#pragma unroll
+            for (int q = 0; q < DPL; ++q)
+              ys[32 * q] = COS ? fma(static_cast<double>(v[g + u][q]), inv[g + u], ys[32 * q])
+                               : ys[32 * q] + static_cast<double>(v[g + u][q]);
+            if (!COS) wpsi[lab[u] * 32 + lane] += ss[g + u];
+          }
+        }
       }
       continue;
     }

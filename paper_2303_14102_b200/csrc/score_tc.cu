@@ -484,8 +484,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float eps_m = COS ? (eps_dot / xn + 3.0f * u * (fabsf(b1) + 1.0f) + exi / xi)
                                 : (2.0f * eps_dot + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
         int nb = arg;
+        // the winner's key error uses its own cluster norm (the runner-up's column is
+        // not tracked: any-column bound eps_m)
+        const float mu_arg = arg >= 0 ? __half2float(mn_s[arg]) * sc.mu_max : sc.mu_max;
+        const float eps_dot_arg = (tp.cdot * mu_arg + sc.floor_coef) * xn;
+        const float eps_m_arg = COS ? (eps_dot_arg / xn + 3.0f * u * (fabsf(b1) + 1.0f) + exi / xi)
+                                    : (2.0f * eps_dot_arg + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
         // neighbour certain: clear gap, and no tie through the clamps at 0 (and 2)
-        const bool full = !((b2 - b1) > 2.0f * eps_m) || nb < 0 || !(rowc + b2 > eps_m) ||
+        const bool full = !((b2 - b1) > eps_m + eps_m_arg) || nb < 0 || !(rowc + b2 > eps_m) ||
                           (COS && !(rowc + b1 < 2.0f - eps_m));
         if (nb < 0) nb = own == 0 ? 1 : 0;
         const bool singleton = co.x == 1.0;
