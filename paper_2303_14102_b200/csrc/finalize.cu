@@ -107,6 +107,143 @@ __global__ void __launch_bounds__(256) refine_kernel(ScoreParams p) {
   }
 }
 
+// Tiled fp64 refinement for many flagged rows against many clusters (C4, C5): a block
+// takes 32 flagged rows and walks the clusters 64 at a time, D in chunks of 32, with
+// the row and cluster-mean tiles staged in shared memory (each mean tile is read once
+// per 32 rows instead of once per row).  Thread (ty, tx) owns rows 2ty, 2ty+1 and
+// clusters tx + 16 j of each tile: ascending per thread, strict < -- then the 16
+// threads of a row merge with ties to the lowest k (the reference's rule).
+constexpr int kRT = 32, kCT = 64, kDC = 32;
+template <bool COS>
+__global__ void __launch_bounds__(256) refine_tiled_kernel(ScoreParams p) {
+  __shared__ double xs[kRT][kDC + 1];
+  __shared__ double ys[kCT][kDC + 1];
+  __shared__ double s_ss[kRT], s_co[kRT], s_best[kRT][17];
+  __shared__ int s_arg[kRT][17], s_own[kRT];
+  __shared__ int64_t s_row[kRT];
+  const int64_t count = static_cast<int64_t>(*p.flag_count);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4, lane = tid & 31, warp = tid >> 5;
+  const double* sums = p.stats + (COS ? p.k : 2 * p.k);
+  const int d = p.d, K = p.k;
+  for (int64_t t0 = static_cast<int64_t>(blockIdx.x) * kRT; t0 < count; t0 += static_cast<int64_t>(gridDim.x) * kRT) {
+    __syncthreads();
+    if (tid < kRT) {
+      const int64_t i = t0 + tid;
+      const int64_t row = i < count ? p.flag_rows[i] : -1;
+      s_row[tid] = row;
+      s_own[tid] = row >= 0 ? p.dense[row] : -1;
+      s_co[tid] = 0.0;
+    }
+    __syncthreads();
+    for (int r = warp; r < kRT; r += 8) {  // ||x||^2 and the own-cluster dot per row
+      const int64_t row = s_row[r];
+      double ss = 0.0, co = 0.0;
+      if (row >= 0) {
+        const float* x = p.X + row * d;
+        const double* yo = sums + static_cast<int64_t>(s_own[r]) * d;
+        for (int l = lane; l < d; l += 32) {
+          const double v = x[l];
+          ss = fma(v, v, ss);
+          co = fma(yo[l], v, co);
+        }
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        ss += __shfl_xor_sync(0xffffffffu, ss, off);
+        co += __shfl_xor_sync(0xffffffffu, co, off);
+      }
+      if (lane == 0) {
+        s_ss[r] = ss;
+        s_co[r] = co;
+      }
+    }
+    __syncthreads();
+    const int r0 = 2 * ty, r1 = 2 * ty + 1;
+    const double ss0 = s_ss[r0], ss1 = s_ss[r1];
+    const double nrm0 = sqrt(ss0), nrm1 = sqrt(ss1);
+    const int own0 = s_own[r0], own1 = s_own[r1];
+    double best0 = INFINITY, best1 = INFINITY;
+    int arg0 = -1, arg1 = -1;
+    for (int c0 = 0; c0 < K; c0 += kCT) {
+      double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+      for (int l0 = 0; l0 < d; l0 += kDC) {
+        __syncthreads();
+        for (int e = tid; e < kRT * kDC; e += 256) {  // rows (fp32 -> fp64), zero padded
+          const int r = e / kDC, l = e % kDC;
+          const int64_t row = s_row[r];
+          xs[r][l] = (row >= 0 && l0 + l < d) ? static_cast<double>(p.X[row * d + l0 + l]) : 0.0;
+        }
+        for (int e = tid; e < kCT * kDC; e += 256) {  // cluster sums, coalesced along D
+          const int c = e / kDC, l = e % kDC;
+          ys[c][l] = (c0 + c < K && l0 + l < d) ? sums[static_cast<int64_t>(c0 + c) * d + l0 + l] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int l = 0; l < kDC; ++l) {
+          const double xa = xs[r0][l], xb = xs[r1][l];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const double y = ys[tx + 16 * j][l];
+            acc[0][j] = fma(y, xa, acc[0][j]);
+            acc[1][j] = fma(y, xb, acc[1][j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = c0 + tx + 16 * j;
+        if (k >= K) continue;
+        const double nk = p.nk[k];
+        if (k != own0) {
+          const double m = COS ? cos_foreign(nk, acc[0][j] / nrm0) : sq_foreign(ss0, p.stats[K + k], nk, acc[0][j]);
+          if (m < best0) {
+            best0 = m;
+            arg0 = k;
+          }
+        }
+        if (k != own1) {
+          const double m = COS ? cos_foreign(nk, acc[1][j] / nrm1) : sq_foreign(ss1, p.stats[K + k], nk, acc[1][j]);
+          if (m < best1) {
+            best1 = m;
+            arg1 = k;
+          }
+        }
+      }
+    }
+    s_best[r0][tx] = best0;
+    s_arg[r0][tx] = arg0;
+    s_best[r1][tx] = best1;
+    s_arg[r1][tx] = arg1;
+    __syncthreads();
+    if (tid < kRT) {
+      const int r = tid;
+      const int64_t row = s_row[r];
+      if (row >= 0) {
+        double best = INFINITY;
+        int arg = -1;
+        for (int j = 0; j < 16; ++j) {  // lowest k among equal minima
+          const double b = s_best[r][j];
+          const int a = s_arg[r][j];
+          if (a >= 0 && (arg < 0 || b < best || (b == best && a < arg))) {
+            best = b;
+            arg = a;
+          }
+        }
+        const int own = s_own[r];
+        const double n_o = p.nk[own];
+        const bool singleton = n_o == 1.0;
+        double a = 0.0;
+        if (!singleton)
+          a = COS ? cos_own(n_o, s_co[r] / sqrt(s_ss[r])) : sq_own(s_ss[r], p.stats[K + own], n_o, s_co[r]);
+        p.s[row] = singleton ? 0.0 : assemble_score(a, best);
+        if (p.nb) p.nb[row] = arg;
+        if (p.own) p.own[row] = own;
+        if (p.a) p.a[row] = a;
+        if (p.b) p.b[row] = best;
+      }
+    }
+  }
+}
+
 // Group partials: a block covers 32 tiles (one warp per 4 tiles); tiles that held
 // refined rows are re-summed from s[] by the warp (fixed lane order + xor tree);
 // then a fixed-order tree over the 32 tile values.
@@ -252,7 +389,17 @@ void flag_all(fsil_context* c, const ScoreParams& p, int tile_rows) {
   FSIL_LAUNCHED(c);
 }
 
+// Flagged-row count is only known on the device: the tiled kernel is chosen when the
+// cluster-mean table is large (each row would otherwise re-read all of it from L2);
+// its grid covers every flagged row of the worst case the table size allows.
 void refine(fsil_context* c, const ScoreParams& p) {
+  if (static_cast<int64_t>(c->k) * c->d >= 64 * 1024) {
+    const int grid = c->num_sms * 4;
+    if (c->metric == FSIL_COSINE) refine_tiled_kernel<true><<<grid, 256, 0, c->stream>>>(p);
+    else refine_tiled_kernel<false><<<grid, 256, 0, c->stream>>>(p);
+    FSIL_LAUNCHED(c);
+    return;
+  }
   // warps per block limited by the staged rows (fp64 x per warp)
   const size_t row_bytes = static_cast<size_t>(c->d) * sizeof(double);
   const int wpb = static_cast<int>(std::min<size_t>(8, c->smem_optin / row_bytes));
