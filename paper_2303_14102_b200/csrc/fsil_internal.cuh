@@ -137,6 +137,7 @@ struct fsil_context {
   fsil::DevBuf xmax;           // float: max |x| of this shard (tensor-core operand scaling)
   fsil::DevBuf tc_b;           // fp16 cluster-mean pieces + column bias (tcgen05 path)
   fsil::DevBuf exact_rows, exact_count;  // rows needing the exact own/neighbour recompute
+  fsil::DevBuf a_scratch;                // tcgen05 streaming mode: per-CTA converted A chunks
   bool tc_exact_used = false;
   // host staging for fsil_silhouette (pageable -> pinned)
   fsil::DevBuf hX, hL;         // device copies of host inputs

@@ -65,6 +65,7 @@ struct TcParams {
   int split;              // separate correction accumulator (large D)
   int2* exact_rows;       // rows needing the exact own/neighbour recompute
   unsigned long long* exact_count;
+  uint8_t* ascratch;      // streaming mode: [grid][nkc][kStgBytes] converted A chunks (or null)
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -120,6 +121,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   // block (X read and converted once per tile); otherwise re-staged per block
   const bool ares = tp.ncb > 1 && 2 * tp.nkc <= NS;
   const int xpasses = ares ? 1 : tp.ncb;
+  // A-scratch (streaming, several cluster blocks): the first pass over a tile's K
+  // chunks converts X and also bulk-stores each converted stage to this CTA's global
+  // (L2-resident) scratch; the later passes bulk-load the converted chunks instead of
+  // re-staging and re-converting X
+  // (nkc >= NS: a slot is rewritten only after the MMA consumed its previous load)
+  // (several cluster blocks per tile only occur at BN = 128: compiled out otherwise)
+  uint8_t* const scr = (BN == 128 && !ares && tp.ncb > 1 && tp.nkc >= NS) ? tp.ascratch : nullptr;
+  uint8_t* const myscr = scr ? scr + static_cast<size_t>(blockIdx.x) * tp.nkc * kStgBytes : nullptr;
   constexpr uint32_t kTmemCols = BN <= 32 ? 256 : 512;
   constexpr uint32_t kIdesc = idesc_f16_f32(BM, BN);
   const ScoreParams& p = tp.p;
@@ -141,6 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* meta_full = bars + 40;         // [2]
   uint64_t* meta_empty = bars + 42;        // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 44);
+  uint64_t* scr_ready = bars + 45;         // [1] a tile's converted chunks are in scratch
   double* meta_xi = reinterpret_cast<double*>(bars + 46);   // [2][2][BM] ||x||^2 halves
   double4* meta_clu = reinterpret_cast<double4*>(meta_xi + 4 * BM);  // [2][BM] clu[own] per row
   float* part = reinterpret_cast<float*>(meta_clu + 2 * BM);  // [2][4][BM] second-half partial top-2
@@ -163,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < NS; ++i) {
       mbar_init(stg_full + i, 1);
       mbar_init(stg_empty + i, 1);
-      mbar_init(a_full + i, 8);
+      mbar_init(a_full + i, myscr ? 1 : 8);
     }
     for (int i = 0; i < NB; ++i) {
       mbar_init(b_full + i, 1);
@@ -173,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(acc_full + i, 1);
       mbar_init(acc_empty + i, TS ? 4 : 8);
     }
+    mbar_init(scr_ready, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(meta_full + i, 8);
       mbar_init(meta_empty + i, TS ? 4 : 8);
@@ -192,14 +203,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     setmaxnreg_dec<40>();
     if (warp == 0 && lane == 0) {
       // ---------------------------------------------------------- TMA producer: X
-      uint32_t n1 = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      uint32_t n1 = 0, ntl = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++ntl) {
         const int row0 = static_cast<int>(t * BM);
         for (int xp = 0; xp < xpasses; ++xp) {
+          if (myscr && xp == 1) {  // first pass converted and stored: wait, then reuse
+            TW(0, scr_ready, ntl & 1);
+            fence_proxy_async_global();
+          }
           for (int kc = 0; kc < nkc; ++kc, ++n1) {
             const int s1 = n1 % NS;
             const int nbox = (kc * BK + 32 < p.d) ? 2 : 1;
             TW(0, stg_empty + s1, ((n1 / NS) & 1) ^ 1);
+            if (myscr && xp > 0) {
+              mbar_arrive_expect_tx(a_full + s1, kStgBytes);
+              bulk_load(stg + s1 * kStgBytes, myscr + static_cast<size_t>(kc) * kStgBytes, kStgBytes, a_full + s1);
+              continue;
+            }
             mbar_arrive_expect_tx(stg_full + s1, nbox * BM * 128);
             for (int b = 0; b < nbox; ++b)
               tma_load_2d(stg + s1 * kStgBytes + b * BM * 128, &tmap_x, stg_full + s1, kc * BK + b * 32, row0);
@@ -286,6 +306,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t row = t * BM + r;
       const int own = (hq == 0 && row < p.n) ? __ldg(p.dense + row) : -1;
       for (int xp = 0; xp < xpasses; ++xp) {
+        if (myscr && xp > 0) {  // later passes load the stored conversions (producer)
+          n1 += nkc;
+          continue;
+        }
         for (int kc = 0; kc < nkc; ++kc, ++n1) {
           const int s1 = n1 % NS;
           TW(4, stg_full + s1, (n1 / NS) & 1);
@@ -331,8 +355,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             *reinterpret_cast<uint4*>(lrow + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
           }
           fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(a_full + s1);
+          if (myscr) {
+            // one thread: the converted stage -> scratch (source read before the MMA
+            // may release the stage), then the single a_full arrival
+            named_bar(5, 256);
+            if (tl == 0) {
+              bulk_store(myscr + static_cast<size_t>(kc) * kStgBytes, sbase, kStgBytes);
+              bulk_wait_read();
+              mbar_arrive(a_full + s1);
+            }
+          } else {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(a_full + s1);
+          }
+        }
+        if (myscr && tl == 0) {  // this tile's chunks are all in global memory
+          bulk_wait_all();
+          mbar_arrive(scr_ready);
         }
         if (xp == 0) {
           const int tb = nt & 1;
@@ -747,6 +786,15 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   tp.munorm = munorm;
   tp.scale = scale;
   tp.nstg = tc_stages(bn, kp, c->smem_optin);
+  {
+    const int64_t ntiles_ = (c->n + BM - 1) / BM;
+    const bool ares_ = ncb > 1 && 2 * nkc <= tp.nstg;
+    if (!ares_ && ncb > 1 && nkc >= tp.nstg) {  // streaming: per-CTA converted-A scratch
+      const int64_t grid_ = std::min<int64_t>(ntiles_, c->num_sms);
+      c->a_scratch.ensure(static_cast<size_t>(grid_) * nkc * kStgBytes);
+      tp.ascratch = c->a_scratch.as<uint8_t>();
+    }
+  }
   // |dot error| <= cdot*||x||*||mu|| + floor: split residuals 3*2^-22 relative; fp32
   // accumulation of the main term over ceil(D/16) MMA steps at 2^-24 (the correction
   // accumulator holds values <= 2^-10 of it); the final main+correction add; and the
