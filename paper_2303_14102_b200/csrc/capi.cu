@@ -23,7 +23,7 @@ bool ffma_supported(const fsil_context* c);
 void flag_all(fsil_context* c, const ScoreParams& p, int tile_rows);
 void exact_ab(fsil_context* c, const ScoreParams& p);
 void refine(fsil_context* c, const ScoreParams& p);
-void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows);
+void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows, bool local);
 bool tc_supported(const fsil_context* c);
 int64_t tc_tiles(const fsil_context* c, int* tile_rows);
 void score_tc(fsil_context* c, const ScoreParams& p);
@@ -71,6 +71,7 @@ void setup(fsil_context* c, int metric, const float* dX, const int32_t* dlabels,
 void begin(fsil_context* c, int metric, const float* dX, const int32_t* dlabels, int64_t n_local,
            int32_t d, int64_t row_offset, int64_t n_global) {
   setup(c, metric, dX, dlabels, n_local, d, row_offset, n_global);
+  c->local_call = false;
   densify_collect(c);
   c->phase = 1;
 }
@@ -171,7 +172,9 @@ void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, 
   if (c->tc_exact_used) exact_ab(c, p);
   refine(c, p);
   record(c, 5);
-  finalize_sum(c, p, ntiles, tile_rows);
+  // single GPU: the final kernel also fills the mapped host summary (no pack launch)
+  finalize_sum(c, p, ntiles, tile_rows, c->local_call);
+  c->summary_packed = c->local_call;
 }
 
 __global__ void pack_summary_kernel(const int64_t* __restrict__ checks, const double* __restrict__ result,
@@ -189,9 +192,12 @@ __global__ void pack_summary_kernel(const int64_t* __restrict__ checks, const do
 // Reads the (all-reduced) validation word and sum; raises in the reference's order.
 double finish(fsil_context* c, double* flagged_out) {
   if (c->phase < 4) fail(FSIL_ERR_INVALID_ARGUMENT, "score must come before finish");
-  pack_summary_kernel<<<1, 32, 0, c->stream>>>(c->checks.as<int64_t>(), c->result.as<double>(),
-                                               c->counters.as<int>() + 4, c->dsum);
-  FSIL_LAUNCHED(c);
+  if (!c->summary_packed) {  // shard mode (words all-reduced since) or an early-out call
+    pack_summary_kernel<<<1, 32, 0, c->stream>>>(c->checks.as<int64_t>(), c->result.as<double>(),
+                                                 c->counters.as<int>() + 4, c->dsum);
+    FSIL_LAUNCHED(c);
+  }
+  c->summary_packed = false;
   record(c, 6);
   FSIL_CUDA(cudaStreamSynchronize(c->stream));
   const volatile HostSummary* hs = c->hsum;
@@ -261,6 +267,7 @@ double run_device(fsil_context* c, int metric, const float* dX, const int32_t* d
                   int32_t d, double* ds, int32_t* dnb, int32_t* down, double* da, double* db,
                   int32_t* k_out, int32_t* dense_to_raw) {
   setup(c, metric, dX, dlabels, n, d, 0, n);
+  c->local_call = true;
   densify_local(c);  // dictionary ordered on the device; one host sync for K
   record(c, 1);
   c->phase = 2;

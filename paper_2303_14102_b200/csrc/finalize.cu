@@ -246,13 +246,28 @@ __global__ void __launch_bounds__(256) refine_tiled_kernel(ScoreParams p) {
 
 // Group partials: a block covers 32 tiles (one warp per 4 tiles); tiles that held
 // refined rows are re-summed from s[] by the warp (fixed lane order + xor tree);
-// then a fixed-order tree over the 32 tile values.
+// then a fixed-order tree over the 32 tile values.  The last block to finish (atomic
+// ticket) sums the group partials in a fixed order into result[] and, on a single
+// GPU, writes the call's summary straight into mapped host memory.
+struct TotalArgs {
+  double* group_sum;
+  double* result;                        // [0] sum s_i, [1] flagged rows, [2] exact rows
+  const unsigned long long* flag_count;
+  const unsigned long long* exact_count;  // null if unused
+  unsigned int* ticket;                   // zero on entry; reset by the last block
+  HostSummary* hsum;                      // single GPU: summary target (null in shard mode)
+  const int64_t* checks;
+  const int* missing;
+};
+
 __global__ void __launch_bounds__(256) tile_group_kernel(const double* __restrict__ tile_sum,
                                                          const int32_t* __restrict__ tile_flag,
                                                          const double* __restrict__ s,
                                                          int64_t ntiles, int tile_rows, int64_t n,
-                                                         double* group_sum) {
+                                                         TotalArgs ta) {
   __shared__ double sm[32];
+  __shared__ double red[256];
+  __shared__ bool last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * 32;
   for (int j = warp; j < 32; j += 8) {
@@ -275,28 +290,39 @@ __global__ void __launch_bounds__(256) tile_group_kernel(const double* __restric
   if (warp == 0) {
     double v = sm[lane];
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if (lane == 0) group_sum[blockIdx.x] = v;
+    if (lane == 0) {
+      ta.group_sum[blockIdx.x] = v;
+      __threadfence();
+      last = atomicAdd(ta.ticket, 1u) == gridDim.x - 1;
+    }
   }
-}
-
-__global__ void __launch_bounds__(1024) total_kernel(const double* __restrict__ group_sum,
-                                                     int64_t ngroups,
-                                                     const unsigned long long* flag_count,
-                                                     const unsigned long long* exact_count,
-                                                     double* result) {
-  __shared__ double sm[1024];
-  double acc = 0.0;
-  for (int64_t g = threadIdx.x; g < ngroups; g += 1024) acc += group_sum[g];
-  sm[threadIdx.x] = acc;
   __syncthreads();
-  for (int stride = 512; stride > 0; stride >>= 1) {
-    if (threadIdx.x < stride) sm[threadIdx.x] += sm[threadIdx.x + stride];
+  if (!last) return;
+  __threadfence();
+  // fixed order: thread i sums groups i, i + 256, ...; then a fixed tree
+  double acc = 0.0;
+  for (int64_t g = threadIdx.x; g < gridDim.x; g += 256) acc += ta.group_sum[g];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int stride = 128; stride > 0; stride >>= 1) {
+    if (threadIdx.x < stride) red[threadIdx.x] += red[threadIdx.x + stride];
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    result[0] = sm[0];
-    result[1] = static_cast<double>(*flag_count);
-    result[2] = exact_count ? static_cast<double>(*exact_count) : 0.0;
+    const double flagged = static_cast<double>(*ta.flag_count);
+    const double exact = ta.exact_count ? static_cast<double>(*ta.exact_count) : 0.0;
+    ta.result[0] = red[0];
+    ta.result[1] = flagged;
+    ta.result[2] = exact;
+    if (ta.hsum) {
+      ta.hsum->checks[0] = ta.checks[0];
+      ta.hsum->checks[1] = ta.checks[1];
+      ta.hsum->missing = *ta.missing;
+      ta.hsum->result[0] = red[0];
+      ta.hsum->result[1] = flagged;
+      ta.hsum->result[2] = exact;
+    }
+    *ta.ticket = 0u;
   }
 }
 
@@ -416,18 +442,21 @@ void refine(fsil_context* c, const ScoreParams& p) {
   FSIL_LAUNCHED(c);
 }
 
-void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows) {
-  const int64_t ngroups = (ntiles + 31) / 32;
-  c->group_sum.ensure(std::max<int64_t>(ngroups, 1) * sizeof(double));
+void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows, bool local) {
+  const int64_t ngroups = std::max<int64_t>((ntiles + 31) / 32, 1);
+  c->group_sum.ensure(ngroups * sizeof(double));
   c->result.ensure(4 * sizeof(double));
-  if (ngroups > 0) {
-    tile_group_kernel<<<static_cast<unsigned>(ngroups), 256, 0, c->stream>>>(
-        p.tile_sum, p.tile_flag, p.s, ntiles, tile_rows, p.n, c->group_sum.as<double>());
-    FSIL_LAUNCHED(c);
-  }
-  total_kernel<<<1, 1024, 0, c->stream>>>(
-      c->group_sum.as<double>(), ngroups, p.flag_count,
-      c->tc_exact_used ? c->exact_count.as<unsigned long long>() : nullptr, c->result.as<double>());
+  TotalArgs ta;
+  ta.group_sum = c->group_sum.as<double>();
+  ta.result = c->result.as<double>();
+  ta.flag_count = p.flag_count;
+  ta.exact_count = c->tc_exact_used ? c->exact_count.as<unsigned long long>() : nullptr;
+  ta.ticket = reinterpret_cast<unsigned int*>(c->counters.as<int>() + 8);
+  ta.hsum = local ? c->dsum : nullptr;
+  ta.checks = c->checks.as<int64_t>();
+  ta.missing = c->counters.as<int>() + 4;
+  tile_group_kernel<<<static_cast<unsigned>(ngroups), 256, 0, c->stream>>>(p.tile_sum, p.tile_flag, p.s, ntiles,
+                                                                         tile_rows, p.n, ta);
   FSIL_LAUNCHED(c);
 }
 

@@ -146,6 +146,8 @@ struct fsil_context {
   int64_t ht_alloc_cap = 0;  // slots of the current (zero-initialised) table
   uint32_t ht_epoch = 0;     // epoch of the last densify (table entries are epoch-tagged)
   int64_t k_last = 0;        // K of the previous call (picks the ordering path)
+  bool local_call = false;   // single-GPU call (fsil_silhouette[_device]), not the shard protocol
+  bool summary_packed = false;  // this call's HostSummary already written on the device
   fsil::HostSummary* hsum = nullptr;  // mapped pinned (host view)
   fsil::HostSummary* dsum = nullptr;  // device view of the same memory
   cudaEvent_t ev[8] = {};
