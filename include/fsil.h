@@ -7,6 +7,7 @@
  *   ------------------------------------------------------   ---------------------------------
  *   compute_silhouette(const Dataset&, Metric, Engine, int)   fsil_silhouette (host buffers)
  *     engine.hpp:124-125, engine.cpp:76-92                    fsil_silhouette_device (HBM-resident)
+ *   Dataset's fp64 Matrix (dataset.hpp:16-21)                  fsil_silhouette[_device]_f64
  *   validate_and_densify(Matrix, const vector<int>&)          fused into both entries (raw int labels)
  *     dataset.hpp:46, dataset.cpp:26-68
  *   Policy::partial + merge  (aggregate_cluster_stats)        fsil_shard_begin / _dictionary /
@@ -117,6 +118,22 @@ fsil_status fsil_silhouette_device(fsil_context* ctx, int metric, const float* d
                                    double* mean, int32_t* k_out, int32_t* dense_to_raw);
 
 /*
+ * fp64 front end: the same calls on fp64 features -- the reference's
+ * own Matrix (Eigen::MatrixXd, D x N column-major == N x D row-major, dataset.hpp:16-21).
+ * Aggregation, the fp64 refinement and the exact a/b recompute read the fp64 values;
+ * the fast scoring pass reads their fp32 rounding, with that rounding (u relative)
+ * added to its certified error bounds.  Scoring runs on the tensor cores (or in fp64
+ * where the shape has no tensor-core tiling); FSIL_PATH_FFMA is unavailable here.
+ */
+fsil_status fsil_silhouette_f64(fsil_context* ctx, int metric, const double* X, const int32_t* labels,
+                                int64_t n, int32_t d, double* s, int32_t* neighbour, int32_t* own,
+                                double* a, double* b, double* mean, int32_t* k_out, int32_t* dense_to_raw);
+fsil_status fsil_silhouette_device_f64(fsil_context* ctx, int metric, const double* dX,
+                                       const int32_t* dlabels, int64_t n, int32_t d, double* ds,
+                                       int32_t* dneighbour, int32_t* down, double* da, double* db,
+                                       double* mean, int32_t* k_out, int32_t* dense_to_raw);
+
+/*
  * Sharded (multi-GPU, one process per GPU) protocol.  Rank r owns the
  * contiguous global rows [row_offset, row_offset + n_local) (plan_shards
  * semantics).  The caller performs the three exchanges between phases with
@@ -137,6 +154,10 @@ fsil_status fsil_silhouette_device(fsil_context* ctx, int metric, const float* d
 fsil_status fsil_shard_begin(fsil_context* ctx, int metric, const float* dX,
                              const int32_t* dlabels, int64_t n_local, int32_t d,
                              int64_t row_offset, int64_t n_global, int64_t* n_distinct);
+/* fsil_shard_begin on fp64 features (the fp64 front end above). */
+fsil_status fsil_shard_begin_f64(fsil_context* ctx, int metric, const double* dX,
+                                 const int32_t* dlabels, int64_t n_local, int32_t d,
+                                 int64_t row_offset, int64_t n_global, int64_t* n_distinct);
 fsil_status fsil_shard_get_dictionary(fsil_context* ctx, int32_t* raw_labels, int64_t* first_rows);
 fsil_status fsil_shard_set_dictionary(fsil_context* ctx, const int32_t* raw_in_dense_order,
                                       int32_t k);

@@ -1,6 +1,6 @@
 // fsil/silhouette.hpp -- C++ host interface of the B200 Silhouette library, mirroring the
 // reference fastsil library's public entry point so a caller switches by changing the
-// namespace and handing over fp32 features:
+// namespace and handing over fp32 or fp64 features:
 //
 //   reference (/root/reference/proj/include/fastsil)          here (header-only, over fsil.h)
 //   ---------------------------------------------------------  ---------------------------------
@@ -15,8 +15,8 @@
 //                                         engine.hpp:124-125    compute_silhouette(X, labels, ...)
 //
 // The reference's Dataset (an Eigen D x N fp64 matrix + densified labels) is replaced by
-// the raw inputs of validate_and_densify (dataset.hpp:46-48): an N x D row-major fp32
-// matrix -- byte-compatible with a column-major D x N one -- and raw int labels.  The
+// the raw inputs of validate_and_densify (dataset.hpp:46-48): an N x D row-major fp32 or
+// fp64 matrix -- byte-compatible with a column-major D x N one -- and raw int labels.  The
 // same validation runs on the device, in the reference's order, and fails with the
 // same exception types.  Engine::Naive (the O(N^2 D) oracle, naive.cpp) is not part of
 // the GPU product and is rejected with std::invalid_argument.
@@ -28,6 +28,7 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -159,13 +160,30 @@ class Context {
   fsil_context* ctx_ = nullptr;
 };
 
+namespace detail {
+inline fsil_status call_host(fsil_context* c, int m, const float* X, const int32_t* L, int64_t n, int32_t d,
+                             double* s, int32_t* nb, int32_t* own, double* a, double* b, double* mean,
+                             int32_t* k, int32_t* raw) {
+  return fsil_silhouette(c, m, X, L, n, d, s, nb, own, a, b, mean, k, raw);
+}
+inline fsil_status call_host(fsil_context* c, int m, const double* X, const int32_t* L, int64_t n, int32_t d,
+                             double* s, int32_t* nb, int32_t* own, double* a, double* b, double* mean,
+                             int32_t* k, int32_t* raw) {
+  return fsil_silhouette_f64(c, m, X, L, n, d, s, nb, own, a, b, mean, k, raw);
+}
+}  // namespace detail
+
 /// compute_silhouette(validate_and_densify(X, labels), metric, engine, shards)
-/// (engine.hpp:124-125; dataset.hpp:48).  X: n x d row-major fp32 (host memory),
-/// labels: n raw ints.  `shards` is accepted for signature compatibility: the rows are
-/// scored by this context's GPU (the multi-GPU path is the sharded protocol in fsil.h).
-inline SilhouetteReport compute_silhouette(Context& ctx, const float* X, const int32_t* labels, int64_t n,
+/// (engine.hpp:124-125; dataset.hpp:48).  X: n x d row-major features in host memory,
+/// fp32 or fp64 -- fp64 is the reference's own Matrix (Eigen::MatrixXd, D x N
+/// column-major: pass .data()), aggregated and refined exactly in fp64; labels: n raw
+/// ints.  `shards` is accepted for signature compatibility: the rows are scored by this
+/// context's GPU (the multi-GPU path is the sharded protocol in fsil.h).
+template <typename T>
+inline SilhouetteReport compute_silhouette(Context& ctx, const T* X, const int32_t* labels, int64_t n,
                                            int32_t d, Metric metric, Engine engine = Engine::Fast,
                                            int shards = 0) {
+  static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>, "features are fp32 or fp64");
   (void)shards;
   if (engine == Engine::Naive)
     throw std::invalid_argument("the naive O(N^2 D) engine is a CPU oracle; the GPU library runs Engine::Fast");
@@ -174,8 +192,8 @@ inline SilhouetteReport compute_silhouette(Context& ctx, const float* X, const i
   std::vector<int32_t> nb(static_cast<size_t>(n)), own(static_cast<size_t>(n)), raw(static_cast<size_t>(n));
   double mean = 0.0;
   int32_t k = 0;
-  ctx.check(fsil_silhouette(ctx.handle(), detail::metric_code(metric), X, labels, n, d, s.data(), nb.data(),
-                            own.data(), a.data(), b.data(), &mean, &k, raw.data()));
+  ctx.check(detail::call_host(ctx.handle(), detail::metric_code(metric), X, labels, n, d, s.data(), nb.data(),
+                              own.data(), a.data(), b.data(), &mean, &k, raw.data()));
   SilhouetteReport r;
   r.scores.resize(static_cast<size_t>(n));
   for (int64_t i = 0; i < n; ++i) {
@@ -196,8 +214,9 @@ inline SilhouetteReport compute_silhouette(Context& ctx, const float* X, const i
   return r;
 }
 
-/// Convenience overload on a per-thread default context for device 0.
-inline SilhouetteReport compute_silhouette(const std::vector<float>& X, const std::vector<int32_t>& labels,
+/// Convenience overload on a per-thread default context for device 0 (fp32 or fp64).
+template <typename T>
+inline SilhouetteReport compute_silhouette(const std::vector<T>& X, const std::vector<int32_t>& labels,
                                            int32_t d, Metric metric, Engine engine = Engine::Fast,
                                            int shards = 0) {
   if (d <= 0 || X.size() != labels.size() * static_cast<size_t>(d))

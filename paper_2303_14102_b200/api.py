@@ -48,7 +48,12 @@ EXPORTS = {
                                        _P, _P, _P]),
     "fsil_silhouette_device": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _I64, _I32, _P, _P, _P,
                                               _P, _P, _P, _P, _P]),
+    "fsil_silhouette_f64": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _I64, _I32, _P, _P, _P, _P, _P,
+                                           _P, _P, _P]),
+    "fsil_silhouette_device_f64": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _I64, _I32, _P, _P, _P,
+                                                  _P, _P, _P, _P, _P]),
     "fsil_shard_begin": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _I64, _I32, _I64, _I64, _P]),
+    "fsil_shard_begin_f64": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _I64, _I32, _I64, _I64, _P]),
     "fsil_shard_get_dictionary": (ctypes.c_int, [_P, _P, _P]),
     "fsil_shard_set_dictionary": (ctypes.c_int, [_P, _P, _I32]),
     "fsil_shard_aggregate": (ctypes.c_int, [_P, _P, _P, _P]),
@@ -205,9 +210,12 @@ class Context:
 
     # -- whole dataset ----------------------------------------------------------
     def silhouette(self, X, labels, metric="sqeuclid", want_ab=True) -> SilhouetteReport:
-        """fsil_silhouette over host arrays (copies in and out of HBM)."""
+        """fsil_silhouette over host arrays (copies in and out of HBM).  float64 features
+        take the fp64 front end (fsil_silhouette_f64: exact aggregation and refinement
+        on the caller's values, the reference's own Matrix type); anything else is fp32."""
         m = metric_code(metric)
-        X = np.ascontiguousarray(X, dtype=np.float32)
+        f64 = getattr(X, "dtype", None) == np.float64
+        X = np.ascontiguousarray(X, dtype=np.float64 if f64 else np.float32)
         if X.ndim != 2:
             X = X.reshape(X.shape[0], -1)
         n, d = X.shape
@@ -223,37 +231,38 @@ class Context:
         k = ctypes.c_int32(0)
         d2r = np.empty(max(n, 1), np.int32)
         t0 = time.perf_counter()
-        self._check(lib().fsil_silhouette(self._h, m, _ptr(X), _ptr(labels), n, d, _ptr(s), _ptr(nb),
-                                          _ptr(own), _ptr(a), _ptr(b), ctypes.byref(mean),
-                                          ctypes.byref(k), _ptr(d2r)))
+        entry = lib().fsil_silhouette_f64 if f64 else lib().fsil_silhouette
+        self._check(entry(self._h, m, _ptr(X), _ptr(labels), n, d, _ptr(s), _ptr(nb), _ptr(own), _ptr(a),
+                          _ptr(b), ctypes.byref(mean), ctypes.byref(k), _ptr(d2r)))
         wall = (time.perf_counter() - t0) * 1e3
         return SilhouetteReport(s, nb, own, a, b, mean.value, _METRIC_TAGS[m], "fast", 1, wall,
                                 d2r[: k.value].tolist())
 
     def silhouette_device(self, X, labels, metric="sqeuclid", s=None, neighbour=None, own=None,
                           a=None, b=None, dense_to_raw=None):
-        """fsil_silhouette_device: X [n,d] fp32 and labels [n] int32 are CUDA tensors
-        (or raw device pointers with explicit shape via silhouette_device_ptr)."""
+        """fsil_silhouette_device: X [n,d] fp32 (or fp64: the fp64 front end) and labels
+        [n] int32 are CUDA tensors (or raw device pointers via silhouette_device_ptr)."""
         n, d = X.shape
+        f64 = str(getattr(X, "dtype", "")) == "torch.float64"
         return self.silhouette_device_ptr(X.data_ptr(), labels.data_ptr(), n, d, metric, s,
-                                          neighbour, own, a, b, dense_to_raw)
+                                          neighbour, own, a, b, dense_to_raw, f64=f64)
 
     def silhouette_device_ptr(self, x_ptr, l_ptr, n, d, metric="sqeuclid", s=None, neighbour=None,
-                              own=None, a=None, b=None, dense_to_raw=None):
+                              own=None, a=None, b=None, dense_to_raw=None, f64=False):
         m = metric_code(metric)
         mean = ctypes.c_double(0.0)
         k = ctypes.c_int32(0)
-        self._check(lib().fsil_silhouette_device(self._h, m, x_ptr, l_ptr, n, d, _ptr(s),
-                                                 _ptr(neighbour), _ptr(own), _ptr(a), _ptr(b),
-                                                 ctypes.byref(mean), ctypes.byref(k),
-                                                 _ptr(dense_to_raw)))
+        entry = lib().fsil_silhouette_device_f64 if f64 else lib().fsil_silhouette_device
+        self._check(entry(self._h, m, x_ptr, l_ptr, n, d, _ptr(s), _ptr(neighbour), _ptr(own), _ptr(a),
+                          _ptr(b), ctypes.byref(mean), ctypes.byref(k), _ptr(dense_to_raw)))
         return mean.value, k.value
 
     # -- sharded protocol (see include/fsil.h) ------------------------------------
-    def shard_begin(self, metric, x_ptr, l_ptr, n_local, d, row_offset, n_global) -> int:
+    def shard_begin(self, metric, x_ptr, l_ptr, n_local, d, row_offset, n_global, f64=False) -> int:
         nd = ctypes.c_int64(0)
-        self._check(lib().fsil_shard_begin(self._h, metric_code(metric), x_ptr, l_ptr, n_local, d,
-                                           row_offset, n_global, ctypes.byref(nd)))
+        entry = lib().fsil_shard_begin_f64 if f64 else lib().fsil_shard_begin
+        self._check(entry(self._h, metric_code(metric), x_ptr, l_ptr, n_local, d, row_offset, n_global,
+                          ctypes.byref(nd)))
         return nd.value
 
     def shard_get_dictionary(self, n_distinct):

@@ -38,8 +38,9 @@ constexpr int kPieceRows = 2048;
 // for the U rows are formed with a transpose-reduce across the warp (fp64).
 // Rows are assigned warp-interleaved in a fixed pattern and every reduction is in
 // a fixed order: bit-identical results run to run.
-template <bool COS, int DPL>
-__device__ __forceinline__ void agg_warp_rows(const float* __restrict__ X, const int32_t* __restrict__ dense,
+// T: the input element type (float, or double for the fp64 front end).
+template <bool COS, int DPL, typename T>
+__device__ __forceinline__ void agg_warp_rows(const T* __restrict__ X, const int32_t* __restrict__ dense,
                                               int64_t n, int d, int64_t row_offset, int64_t base, int64_t GW,
                                               bool checked, double* wsum, double* wpsi, double* wcnt,
                                               int64_t* checks, float& amax) {
@@ -47,16 +48,16 @@ __device__ __forceinline__ void agg_warp_rows(const float* __restrict__ X, const
   const int lane = threadIdx.x & 31;
   const int64_t rl = base + (lane & (U - 1)) * GW;
   const int lab_l = (lane < U && (!checked || rl < n)) ? __ldg(dense + rl) : 0;
-  float v[U][DPL];
+  T v[U][DPL];
   {
     const int64_t stride = GW * static_cast<int64_t>(d);
-    const float* ptr = X + base * d + lane;
+    const T* ptr = X + base * d + lane;
 #pragma unroll
     for (int u = 0; u < U; ++u, ptr += stride) {
       const bool rv = !checked || base + u * GW < n;
 #pragma unroll
       for (int i = 0; i < DPL; ++i)
-        v[u][i] = (rv && (!checked || lane + 32 * i < d)) ? __ldcs(ptr + 32 * i) : 0.f;
+        v[u][i] = (rv && (!checked || lane + 32 * i < d)) ? __ldcs(ptr + 32 * i) : T(0);
     }
   }
   double ss[U];
@@ -67,7 +68,7 @@ __device__ __forceinline__ void agg_warp_rows(const float* __restrict__ X, const
     for (int i = 0; i < DPL; ++i) {
       const double x = v[u][i];
       ss[u] = fma(x, x, ss[u]);
-      amax = fmaxf(amax, fabsf(v[u][i]));
+      amax = fmaxf(amax, fabsf(static_cast<float>(v[u][i])));
     }
   }
   double inv[U];
@@ -119,9 +120,9 @@ __device__ __forceinline__ void agg_warp_rows(const float* __restrict__ X, const
   }
 }
 
-template <bool COS, int DPL>
+template <bool COS, int DPL, typename T>
 __global__ void __launch_bounds__(256) agg_warp_kernel(
-    const float* __restrict__ X, const int32_t* __restrict__ dense, int64_t n, int d,
+    const T* __restrict__ X, const int32_t* __restrict__ dense, int64_t n, int d,
     int64_t row_offset, int k, double* __restrict__ partials, int64_t* checks, float* xmax) {
   constexpr int U = 8;
   extern __shared__ double sm[];
@@ -140,9 +141,9 @@ __global__ void __launch_bounds__(256) agg_warp_kernel(
   int64_t base = gw;
   if (full_d)  // unchecked fast path over complete groups of U rows
     for (; base + (U - 1) * GW < n; base += U * GW)
-      agg_warp_rows<COS, DPL>(X, dense, n, d, row_offset, base, GW, false, wsum, wpsi, wcnt, checks, amax);
+      agg_warp_rows<COS, DPL, T>(X, dense, n, d, row_offset, base, GW, false, wsum, wpsi, wcnt, checks, amax);
   for (; base < n; base += U * GW)
-    agg_warp_rows<COS, DPL>(X, dense, n, d, row_offset, base, GW, true, wsum, wpsi, wcnt, checks, amax);
+    agg_warp_rows<COS, DPL, T>(X, dense, n, d, row_offset, base, GW, true, wsum, wpsi, wcnt, checks, amax);
   for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
   if (lane == 0 && amax > 0.f) atomic_max_nonneg_f32(xmax, amax);
   __syncthreads();
@@ -434,9 +435,9 @@ __global__ void pieces_per_cluster_kernel(const int64_t* seg_begin, const int64_
 // the sorted row ids.  Lanes: RPW row sub-groups of LPR lanes; CPL chunks of
 // VEC floats per lane.  Piece partial layout: [count][psi][sums d] (psi only
 // for sqeuclid).
-template <bool COS, int VEC, int CPL>
+template <bool COS, int VEC, int CPL, typename T>
 __global__ void __launch_bounds__(256) agg_piece_kernel(
-    const float* __restrict__ X, const int32_t* __restrict__ rows, int64_t n, int d,
+    const T* __restrict__ X, const int32_t* __restrict__ rows, int64_t n, int d,
     int64_t row_offset, int k, int lpr, const int64_t* __restrict__ seg_begin,
     const int64_t* __restrict__ seg_end, const int64_t* __restrict__ piece_start,
     double* __restrict__ piece_out, int64_t* checks, float* xmax) {
@@ -468,16 +469,16 @@ __global__ void __launch_bounds__(256) agg_piece_kernel(
     const int64_t pos = base + sub;  // warp-uniform trip count
     const bool valid = pos < b1;
     const int64_t r = valid ? rows[pos] : 0;
-    float v[CPL][VEC];
+    T v[CPL][VEC];
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
       const int ch = li + q * lpr;
-      if constexpr (VEC == 4) {
+      if constexpr (VEC == 4) {  // float input only
         float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
         if (valid && ch < nchunks) t = ldg_stream(reinterpret_cast<const float4*>(X + r * d) + ch);
         v[q][0] = t.x; v[q][1] = t.y; v[q][2] = t.z; v[q][3] = t.w;
       } else {
-        v[q][0] = (valid && ch < nchunks) ? __ldg(X + r * d + ch) : 0.f;
+        v[q][0] = (valid && ch < nchunks) ? __ldg(X + r * d + ch) : T(0);
       }
     }
     double ss = 0.0;
@@ -489,7 +490,7 @@ __global__ void __launch_bounds__(256) agg_piece_kernel(
         const double x = v[q][e];
         ss += x * x;
         finite = finite && isfinite(v[q][e]);
-        amax = fmaxf(amax, fabsf(v[q][e]));
+        amax = fmaxf(amax, fabsf(static_cast<float>(v[q][e])));
       }
     if (!finite) {
 #pragma unroll
@@ -635,14 +636,14 @@ void launch_stage(fsil_context* c, int dpl, int warps, int64_t chunk, size_t sme
   fail(FSIL_ERR_INTERNAL, "no staged aggregation kernel for this shape");
 }
 
-template <bool COS>
-void launch_warp(fsil_context* c, int dpl, int grid, int threads, size_t smem, double* partials,
+template <bool COS, typename T>
+void launch_warp(fsil_context* c, const T* X, int dpl, int grid, int threads, size_t smem, double* partials,
                  int64_t* checks) {
 #define FSIL_AGG_WARP(P)                                                                         \
   if (dpl == P) {                                                                                \
-    auto kern = agg_warp_kernel<COS, P>;                                                         \
+    auto kern = agg_warp_kernel<COS, P, T>;                                                      \
     FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    kern<<<grid, threads, smem, c->stream>>>(c->X, c->dense.as<int32_t>(), c->n, c->d,          \
+    kern<<<grid, threads, smem, c->stream>>>(X, c->dense.as<int32_t>(), c->n, c->d,             \
                                              c->row_offset, c->k, partials, checks,              \
                                              c->xmax.as<float>());                               \
     FSIL_LAUNCHED(c);                                                                            \
@@ -653,20 +654,22 @@ void launch_warp(fsil_context* c, int dpl, int grid, int threads, size_t smem, d
   fail(FSIL_ERR_INTERNAL, "no warp aggregation kernel for this shape");
 }
 
-template <bool COS>
-void launch_pieces(fsil_context* c, int vec, int cpl, int64_t max_pieces, int lpr,
+template <bool COS, typename T>
+void launch_pieces(fsil_context* c, const T* X, int vec, int cpl, int64_t max_pieces, int lpr,
                    const int32_t* rows, int64_t* seg_begin, int64_t* seg_end,
                    int64_t* piece_start, double* piece_out, int64_t* checks) {
   const unsigned grid = static_cast<unsigned>((max_pieces * 32 + 255) / 256);
 #define FSIL_AGG_PIECE(V, C)                                                                     \
   if (vec == V && cpl == C) {                                                                    \
-    agg_piece_kernel<COS, V, C><<<grid, 256, 0, c->stream>>>(                                    \
-        c->X, rows, c->n, c->d, c->row_offset, c->k, lpr, seg_begin, seg_end, piece_start,       \
+    agg_piece_kernel<COS, V, C, T><<<grid, 256, 0, c->stream>>>(                                 \
+        X, rows, c->n, c->d, c->row_offset, c->k, lpr, seg_begin, seg_end, piece_start,          \
         piece_out, checks, c->xmax.as<float>());                                                 \
     FSIL_LAUNCHED(c);                                                                            \
     return;                                                                                      \
   }
-  FSIL_AGG_PIECE(4, 1) FSIL_AGG_PIECE(4, 2) FSIL_AGG_PIECE(4, 4) FSIL_AGG_PIECE(4, 8)
+  if constexpr (sizeof(T) == 4) {
+    FSIL_AGG_PIECE(4, 1) FSIL_AGG_PIECE(4, 2) FSIL_AGG_PIECE(4, 4) FSIL_AGG_PIECE(4, 8)
+  }
   FSIL_AGG_PIECE(1, 1) FSIL_AGG_PIECE(1, 2) FSIL_AGG_PIECE(1, 4) FSIL_AGG_PIECE(1, 8)
   FSIL_AGG_PIECE(1, 16) FSIL_AGG_PIECE(1, 32)
 #undef FSIL_AGG_PIECE
@@ -691,7 +694,9 @@ void aggregate(fsil_context* c) {
     c->agg_path = 0;
     return;
   }
-  const int vec = (c->d % 4 == 0) ? 4 : 1;
+  // fp64 front end: the exact fp64 features (c->X64) feed the aggregation
+  const bool x64 = c->X64 != nullptr;
+  const int vec = (c->d % 4 == 0 && !x64) ? 4 : 1;
   const int lpr = pick_lpr(c->d, vec);
   const int chunks = (c->d + vec - 1) / vec;
   const int cpl = (chunks + lpr - 1) / lpr;
@@ -706,7 +711,7 @@ void aggregate(fsil_context* c) {
   const size_t smem = warps * per_warp;
   const int blocks_per_sm = smem > 0 ? static_cast<int>(std::min<size_t>(228 * 1024 / (smem + 1024), 64 / warps)) : 0;
   // Path 1a: bulk-TMA staged (needs 16-byte rows); one CTA per SM.
-  if (dpl <= 4 && c->d % 4 == 0) {
+  if (dpl <= 4 && c->d % 4 == 0 && !x64) {
     int W = 12;
     auto need = [&](int w) { return w * per_warp + 3ull * 8 * w * c->d * 4 + 64 + 16; };
     while (W > 4 && need(W) > budget) W -= 4;
@@ -732,8 +737,13 @@ void aggregate(fsil_context* c) {
         1, std::min<int64_t>((c->n + rows_per_block - 1) / rows_per_block,
                              static_cast<int64_t>(c->num_sms) * blocks_per_sm)));
     c->partials.ensure(static_cast<size_t>(grid) * S * sizeof(double));
-    if (cos) launch_warp<true>(c, dpl, grid, warps * 32, smem, c->partials.as<double>(), checks);
-    else launch_warp<false>(c, dpl, grid, warps * 32, smem, c->partials.as<double>(), checks);
+    if (x64) {
+      if (cos) launch_warp<true>(c, c->X64, dpl, grid, warps * 32, smem, c->partials.as<double>(), checks);
+      else launch_warp<false>(c, c->X64, dpl, grid, warps * 32, smem, c->partials.as<double>(), checks);
+    } else {
+      if (cos) launch_warp<true>(c, c->X, dpl, grid, warps * 32, smem, c->partials.as<double>(), checks);
+      else launch_warp<false>(c, c->X, dpl, grid, warps * 32, smem, c->partials.as<double>(), checks);
+    }
     fold_partials_kernel<<<static_cast<unsigned>((S + 31) / 32), 256, 0, c->stream>>>(
         c->partials.as<double>(), grid, S, stats);
     FSIL_LAUNCHED(c);
@@ -784,12 +794,15 @@ void aggregate(fsil_context* c) {
   const int S1 = cos ? c->d + 1 : c->d + 2;
   c->partials.ensure(static_cast<size_t>(max_pieces) * S1 * sizeof(double));
   const int cpl_t = cpl <= 1 ? 1 : cpl <= 2 ? 2 : cpl <= 4 ? 4 : cpl <= 8 ? 8 : cpl <= 16 ? 16 : 32;
-  if (cos)
-    launch_pieces<true>(c, vec, cpl_t, max_pieces, lpr, c->sort_vals.as<int32_t>(), seg_begin,
-                        seg_end, piece_start, c->partials.as<double>(), checks);
-  else
-    launch_pieces<false>(c, vec, cpl_t, max_pieces, lpr, c->sort_vals.as<int32_t>(), seg_begin,
-                         seg_end, piece_start, c->partials.as<double>(), checks);
+  const int32_t* srows = c->sort_vals.as<int32_t>();
+  double* pout = c->partials.as<double>();
+  if (x64) {
+    if (cos) launch_pieces<true>(c, c->X64, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);
+    else launch_pieces<false>(c, c->X64, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);
+  } else {
+    if (cos) launch_pieces<true>(c, c->X, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);
+    else launch_pieces<false>(c, c->X, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);
+  }
   const int64_t nthreads = static_cast<int64_t>(c->k) * S1;
   fold_pieces_kernel<<<static_cast<unsigned>((nthreads + 255) / 256), 256, 0, c->stream>>>(
       c->partials.as<double>(), piece_start, c->k, c->d, cos, stats);

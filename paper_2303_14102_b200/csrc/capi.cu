@@ -46,7 +46,15 @@ void check_shape(int64_t n_global, int64_t d) {
   if (d < 1) fail(FSIL_ERR_VALIDATION, "dataset needs at least 1 feature dimension");
 }
 
-void setup(fsil_context* c, int metric, const float* dX, const int32_t* dlabels, int64_t n_local,
+// fp64 front end: the fast scoring pass reads a rounded fp32 copy
+__global__ void to_f32_kernel(const double* __restrict__ in, float* __restrict__ out, int64_t count) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<float>(in[i]);
+}
+
+// dX: fp32 (x64 = false) or fp64 (x64 = true) features, n_local x d row-major.
+void setup(fsil_context* c, int metric, const void* dX, bool x64, const int32_t* dlabels, int64_t n_local,
            int32_t d, int64_t row_offset, int64_t n_global) {
   check_metric(metric);
   check_shape(n_global, d);
@@ -55,7 +63,20 @@ void setup(fsil_context* c, int metric, const float* dX, const int32_t* dlabels,
   if (n_local > 0 && (!dX || !dlabels)) fail(FSIL_ERR_INVALID_ARGUMENT, "null input pointer");
   FSIL_CUDA(cudaSetDevice(c->device));
   c->metric = metric;
-  c->X = dX;
+  if (x64) {
+    c->X64 = static_cast<const double*>(dX);
+    const int64_t count = n_local * static_cast<int64_t>(d);
+    c->x32.ensure(std::max<int64_t>(count, 1) * sizeof(float));
+    if (count > 0) {
+      to_f32_kernel<<<static_cast<unsigned>(std::min<int64_t>((count + 255) / 256, int64_t(c->num_sms) * 16)), 256, 0,
+                      c->stream>>>(c->X64, c->x32.as<float>(), count);
+      FSIL_LAUNCHED(c);
+    }
+    c->X = c->x32.as<float>();
+  } else {
+    c->X64 = nullptr;
+    c->X = static_cast<const float*>(dX);
+  }
   c->labels = dlabels;
   c->n = n_local;
   c->n_global = n_global;
@@ -63,14 +84,14 @@ void setup(fsil_context* c, int metric, const float* dX, const int32_t* dlabels,
   c->d = d;
   c->dp = (static_cast<int64_t>(d) + 3) / 4 * 4;
   c->k = 0;
-  c->launches = 0;
   c->stats = fsil_stats{};
   record(c, 0);
 }
 
-void begin(fsil_context* c, int metric, const float* dX, const int32_t* dlabels, int64_t n_local,
+void begin(fsil_context* c, int metric, const void* dX, bool x64, const int32_t* dlabels, int64_t n_local,
            int32_t d, int64_t row_offset, int64_t n_global) {
-  setup(c, metric, dX, dlabels, n_local, d, row_offset, n_global);
+  c->launches = 0;
+  setup(c, metric, dX, x64, dlabels, n_local, d, row_offset, n_global);
   c->local_call = false;
   densify_collect(c);
   c->phase = 1;
@@ -101,6 +122,7 @@ ScoreParams make_params(fsil_context* c, double* s, int32_t* nb, int32_t* own, d
                         double* b) {
   ScoreParams p{};
   p.X = c->X;
+  p.X64 = c->X64;
   p.dense = c->dense.as<int32_t>();
   p.n = c->n;
   p.d = c->d;
@@ -135,7 +157,9 @@ void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, 
   derive(c);
   ScoreParams p = make_params(c, s, nb, own, a, b);
   int use = c->path;
-  const bool tc_ok = tc_supported(c), ffma_ok = ffma_supported(c);
+  // the FFMA kernel's own fp64 a/b recompute reads the fp32 features: not exact on
+  // the fp64 front end, which therefore scores on the tensor cores or in fp64
+  const bool tc_ok = tc_supported(c), ffma_ok = !c->X64 && ffma_supported(c);
   if (use == FSIL_PATH_AUTO) {
     // Measured crossover (profiles/): the tcgen05 kernel wins once the contraction
     // has ~2e7 row-cluster pairs (C2: 116 us vs 207 us FFMA); below that its fixed
@@ -150,7 +174,8 @@ void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, 
                                         std::to_string(c->d) + ", k=" + std::to_string(c->k) +
                                         ", smem optin " + std::to_string(c->smem_optin) + ")");
   if (use == FSIL_PATH_FFMA && !ffma_ok)
-    fail(FSIL_ERR_INVALID_ARGUMENT, "FFMA scoring path unavailable for this shape (D too large)");
+    fail(FSIL_ERR_INVALID_ARGUMENT, c->X64 ? "FFMA scoring path unavailable for fp64 features"
+                                           : "FFMA scoring path unavailable for this shape (D too large)");
   int tile_rows = 256;
   const int64_t ntiles = use == FSIL_PATH_TCGEN05 ? tc_tiles(c, &tile_rows) : ffma_tiles(c->n);
   c->tile_sum.ensure(std::max<int64_t>(ntiles, 1) * sizeof(double));
@@ -263,10 +288,11 @@ std::vector<std::pair<int64_t, int32_t>> fetch_dictionary(fsil_context* c) {
   return out;
 }
 
-double run_device(fsil_context* c, int metric, const float* dX, const int32_t* dlabels, int64_t n,
+double run_device(fsil_context* c, int metric, const void* dX, bool x64, const int32_t* dlabels, int64_t n,
                   int32_t d, double* ds, int32_t* dnb, int32_t* down, double* da, double* db,
                   int32_t* k_out, int32_t* dense_to_raw) {
-  setup(c, metric, dX, dlabels, n, d, 0, n);
+  c->launches = 0;
+  setup(c, metric, dX, x64, dlabels, n, d, 0, n);
   c->local_call = true;
   densify_local(c);  // dictionary ordered on the device; one host sync for K
   record(c, 1);
@@ -416,22 +442,35 @@ fsil_status fsil_silhouette_device(fsil_context* c, int metric, const float* dX,
                                    double* mean, int32_t* k_out, int32_t* dense_to_raw) {
   if (!c) return FSIL_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
-    const double m = run_device(c, metric, dX, dlabels, n, d, ds, dnb, down, da, db, k_out, dense_to_raw);
+    const double m = run_device(c, metric, dX, false, dlabels, n, d, ds, dnb, down, da, db, k_out, dense_to_raw);
+    if (mean) *mean = m;
+  });
+}
+fsil_status fsil_silhouette_device_f64(fsil_context* c, int metric, const double* dX, const int32_t* dlabels,
+                                       int64_t n, int32_t d, double* ds, int32_t* dnb, int32_t* down, double* da,
+                                       double* db, double* mean, int32_t* k_out, int32_t* dense_to_raw) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    const double m = run_device(c, metric, dX, true, dlabels, n, d, ds, dnb, down, da, db, k_out, dense_to_raw);
     if (mean) *mean = m;
   });
 }
 
-fsil_status fsil_silhouette(fsil_context* c, int metric, const float* X, const int32_t* labels,
-                            int64_t n, int32_t d, double* s, int32_t* neighbour, int32_t* own,
-                            double* a, double* b, double* mean, int32_t* k_out,
-                            int32_t* dense_to_raw) {
+}  // extern "C"
+
+namespace {
+// Host buffers: copy X (fp32 or fp64) and labels to HBM, run, copy results back.
+template <typename T>
+fsil_status host_call(fsil_context* c, int metric, const T* X, const int32_t* labels, int64_t n, int32_t d,
+                      double* s, int32_t* neighbour, int32_t* own, double* a, double* b, double* mean,
+                      int32_t* k_out, int32_t* dense_to_raw) {
   if (!c) return FSIL_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
     check_metric(metric);
     check_shape(n, d);
     if (!X || !labels) fail(FSIL_ERR_INVALID_ARGUMENT, "null input pointer");
     FSIL_CUDA(cudaSetDevice(c->device));
-    const size_t xb = static_cast<size_t>(n) * d * sizeof(float);
+    const size_t xb = static_cast<size_t>(n) * d * sizeof(T);
     c->hX.ensure(xb);
     c->hL.ensure(n * sizeof(int32_t));
     FSIL_CUDA(cudaMemcpyAsync(c->hX.p, X, xb, cudaMemcpyHostToDevice, c->stream));
@@ -444,8 +483,8 @@ fsil_status fsil_silhouette(fsil_context* c, int metric, const float* X, const i
     if (own) { c->o_own.ensure(n * sizeof(int32_t)); down = c->o_own.as<int32_t>(); }
     if (a) { c->o_a.ensure(n * sizeof(double)); da = c->o_a.as<double>(); }
     if (b) { c->o_b.ensure(n * sizeof(double)); db = c->o_b.as<double>(); }
-    const double m = run_device(c, metric, c->hX.as<float>(), c->hL.as<int32_t>(), n, d, ds, dnb,
-                                down, da, db, k_out, dense_to_raw);
+    const double m = run_device(c, metric, c->hX.p, sizeof(T) == 8, c->hL.as<int32_t>(), n, d, ds, dnb, down, da,
+                                db, k_out, dense_to_raw);
     if (s) FSIL_CUDA(cudaMemcpyAsync(s, ds, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     if (neighbour) FSIL_CUDA(cudaMemcpyAsync(neighbour, dnb, n * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
     if (own) FSIL_CUDA(cudaMemcpyAsync(own, down, n * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
@@ -455,13 +494,35 @@ fsil_status fsil_silhouette(fsil_context* c, int metric, const float* X, const i
     if (mean) *mean = m;
   });
 }
+}  // namespace
 
+extern "C" {
+
+fsil_status fsil_silhouette(fsil_context* c, int metric, const float* X, const int32_t* labels, int64_t n,
+                            int32_t d, double* s, int32_t* neighbour, int32_t* own, double* a, double* b,
+                            double* mean, int32_t* k_out, int32_t* dense_to_raw) {
+  return host_call(c, metric, X, labels, n, d, s, neighbour, own, a, b, mean, k_out, dense_to_raw);
+}
+fsil_status fsil_silhouette_f64(fsil_context* c, int metric, const double* X, const int32_t* labels, int64_t n,
+                                int32_t d, double* s, int32_t* neighbour, int32_t* own, double* a, double* b,
+                                double* mean, int32_t* k_out, int32_t* dense_to_raw) {
+  return host_call(c, metric, X, labels, n, d, s, neighbour, own, a, b, mean, k_out, dense_to_raw);
+}
 fsil_status fsil_shard_begin(fsil_context* c, int metric, const float* dX, const int32_t* dlabels,
                              int64_t n_local, int32_t d, int64_t row_offset, int64_t n_global,
                              int64_t* n_distinct) {
   if (!c) return FSIL_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
-    begin(c, metric, dX, dlabels, n_local, d, row_offset, n_global);
+    begin(c, metric, dX, false, dlabels, n_local, d, row_offset, n_global);
+    if (n_distinct) *n_distinct = c->n_distinct;
+  });
+}
+fsil_status fsil_shard_begin_f64(fsil_context* c, int metric, const double* dX, const int32_t* dlabels,
+                                 int64_t n_local, int32_t d, int64_t row_offset, int64_t n_global,
+                                 int64_t* n_distinct) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    begin(c, metric, dX, true, dlabels, n_local, d, row_offset, n_global);
     if (n_distinct) *n_distinct = c->n_distinct;
   });
 }

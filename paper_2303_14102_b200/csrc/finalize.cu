@@ -33,12 +33,12 @@ __global__ void __launch_bounds__(256) refine_kernel(ScoreParams p) {
   const int d = p.d, K = p.k;
   for (int64_t i = warp; i < static_cast<int64_t>(count); i += nwarps) {
     const int64_t row = p.flag_rows[i];
-    const float* x = p.X + row * d;
+    const int64_t xo = row * d;
     const int own = p.dense[row];
     double ss = 0.0;
     __syncwarp();
     for (int l = lane; l < d; l += 32) {
-      const double v = x[l];
+      const double v = xval(p, xo + l);
       xs[l] = v;
       ss = fma(v, v, ss);
     }
@@ -139,10 +139,10 @@ __global__ void __launch_bounds__(256) refine_tiled_kernel(ScoreParams p) {
       const int64_t row = s_row[r];
       double ss = 0.0, co = 0.0;
       if (row >= 0) {
-        const float* x = p.X + row * d;
+        const int64_t xo = row * d;
         const double* yo = sums + static_cast<int64_t>(s_own[r]) * d;
         for (int l = lane; l < d; l += 32) {
-          const double v = x[l];
+          const double v = xval(p, xo + l);
           ss = fma(v, v, ss);
           co = fma(yo[l], v, co);
         }
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(256) refine_tiled_kernel(ScoreParams p) {
         for (int e = tid; e < kRT * kDC; e += 256) {  // rows (fp32 -> fp64), zero padded
           const int r = e / kDC, l = e % kDC;
           const int64_t row = s_row[r];
-          xs[r][l] = (row >= 0 && l0 + l < d) ? static_cast<double>(p.X[row * d + l0 + l]) : 0.0;
+          xs[r][l] = (row >= 0 && l0 + l < d) ? xval(p, row * d + l0 + l) : 0.0;
         }
         for (int e = tid; e < kCT * kDC; e += 256) {  // cluster sums, coalesced along D
           const int c = e / kDC, l = e % kDC;
@@ -357,13 +357,13 @@ __global__ void __launch_bounds__(256) exact_ab_kernel(ScoreParams p, const int2
     const int64_t row = rn.x;
     const int nb = rn.y;
     const int own = valid ? p.dense[row] : 0;
-    const float* x = p.X + row * p.d;
+    const int64_t xo = row * p.d;
     const double* yo = sums + static_cast<int64_t>(own) * p.d;
     const double* yb = sums + static_cast<int64_t>(nb) * p.d;
     double ss = 0.0, co = 0.0, cb = 0.0;
     if (valid)
       for (int l = li; l < p.d; l += LPR) {
-        const double v = x[l];
+        const double v = xval(p, xo + l);
         ss = fma(v, v, ss);
         co = fma(yo[l], v, co);
         cb = fma(yb[l], v, cb);

@@ -110,7 +110,8 @@ struct fsil_context {
 
   // shard/call state
   int metric = FSIL_SQEUCLID;
-  const float* X = nullptr;
+  const float* X = nullptr;       // fp32 features the scoring kernels read
+  const double* X64 = nullptr;    // fp64 front end: the caller's features (aggregation, exact parts)
   const int32_t* labels = nullptr;
   int64_t n = 0, n_global = 0, row_offset = 0;
   int32_t d = 0, k = 0;
@@ -138,6 +139,7 @@ struct fsil_context {
   fsil::DevBuf tc_b;           // fp16 cluster-mean pieces + column bias (tcgen05 path)
   fsil::DevBuf exact_rows, exact_count;  // rows needing the exact own/neighbour recompute
   fsil::DevBuf a_scratch;                // tcgen05 streaming mode: per-CTA converted A chunks
+  fsil::DevBuf x32;                      // fp64 front end: rounded fp32 copy for the fast pass
   bool tc_exact_used = false;
   // host staging for fsil_silhouette (pageable -> pinned)
   fsil::DevBuf hX, hL;         // device copies of host inputs

@@ -13,7 +13,8 @@
 namespace fsil {
 
 struct ScoreParams {
-  const float* X;
+  const float* X;         // fp32 features (the fast scoring pass)
+  const double* X64;      // fp64 front end: the caller's exact features (null for fp32 input)
   const int32_t* dense;
   int64_t n;
   int d, dp, k;
@@ -34,6 +35,12 @@ struct ScoreParams {
   int32_t* flag_rows;     // [n]
   unsigned long long* flag_count;
 };
+
+// Feature element idx (row * d + l) as the exact-path kernels see it: the caller's
+// fp64 value on the fp64 front end, else the fp32 input widened.
+__device__ __forceinline__ double xval(const ScoreParams& p, int64_t idx) {
+  return p.X64 ? p.X64[idx] : static_cast<double>(p.X[idx]);
+}
 
 // fp32 bound constant gamma_m = m u / (1 - m u), u = 2^-24.
 __device__ __forceinline__ float gamma_f32(int m) {

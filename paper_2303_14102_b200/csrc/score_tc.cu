@@ -66,6 +66,7 @@ struct TcParams {
   int2* exact_rows;       // rows needing the exact own/neighbour recompute
   unsigned long long* exact_count;
   uint8_t* ascratch;      // streaming mode: [grid][nkc][kStgBytes] converted A chunks (or null)
+  float exic;             // ||x||^2 relative error / u: 8.1 (fp32 blocks of 8), +2.1 on fp64 input
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -518,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (valid) {
         const float u = 5.9604645e-8f;
         const float rowc = COS ? 1.0f : xi;
-        const float exi = 8.1f * u * xi;   // ||x||^2 error (fp32 blocks of 8)
+        const float exi = tp.exic * u * xi;  // ||x||^2 error (fp32 blocks of 8; fp64 input rounding)
         const float eps_dot = (tp.cdot * sc.mu_max + sc.floor_coef) * xn;  // any column
         const float eps_m = COS ? (eps_dot / xn + 3.0f * u * (fabsf(b1) + 1.0f) + exi / xi)
                                 : (2.0f * eps_dot + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
@@ -547,9 +548,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float t = n_o * dob * rnf;
           const float b = fminf(fmaxf(1.0f + b1, 0.0f), 2.0f);
           const float a = singleton ? 0.0f : fminf(fmaxf((n_o - t) * r_o, 0.0f), 2.0f);
-          const float db = 1.01f * (eb1 + 3.0f * u * (fabsf(b1) + 1.0f) + 8.1f * u + u * b);
+          const float db = 1.01f * (eb1 + 3.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u + u * b);
           // dots; ||x||^2 and rsqrt (8.1u/2 + 2.5u); the four fp32 roundings of a
-          const float da = 1.01f * (nr_o * (eo1 + 8.1f * u) + 3.0f * u * nr_o * fabsf(dob * rnf) +
+          const float da = 1.01f * (nr_o * (eo1 + tp.exic * u) + 3.0f * u * nr_o * fabsf(dob * rnf) +
                                     5.0f * u * (n_o + fabsf(t)) * r_o);
           const float mx = fmaxf(a, b);
           if (!singleton && mx > 0.0f) s = a <= b ? 1.0f - __fdividef(a, b) : __fdividef(b, a) - 1.0f;
@@ -805,6 +806,13 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   if (const char* e = std::getenv("FSIL_TC_SPLIT")) tp.split = std::atoi(e) ? 1 : 0;  // experiments
   tp.cdot = tp.split ? 1.05f * (12.0f + steps + 1.0f + 2.0f * steps / 512.0f) * u
                      : 1.05f * (12.0f + 3.0f * steps + 1.0f) * u;  // all 3 terms, one accumulator
+  // fp64 front end: the fast pass reads the fp32 rounding of the caller's features
+  // (|x32 - x| <= u|x|): +u on the dots, +2.1u on ||x||^2
+  tp.exic = 8.1f;
+  if (c->X64) {
+    tp.cdot += 1.01f * u;
+    tp.exic += 2.1f;
+  }
   c->exact_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int2));
   c->exact_count.ensure(sizeof(unsigned long long));
   FSIL_CUDA(cudaMemsetAsync(c->exact_count.p, 0, sizeof(unsigned long long), c->stream));

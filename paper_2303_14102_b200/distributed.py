@@ -103,7 +103,7 @@ class CudaShardOps:
     def begin(self):
         n, d = self.X.shape
         nd = self.ctx.shard_begin(self.metric, self.X.data_ptr(), self.L.data_ptr(), n, d,
-                                  self.row_offset, self.n_global)
+                                  self.row_offset, self.n_global, f64=self.X.dtype == torch.float64)
         return self.ctx.shard_get_dictionary(nd)
 
     def set_dictionary(self, raw):

@@ -62,6 +62,10 @@ int main(int argc, char** argv) {
     }
     CHECK(r.scores[0].own_cluster == 0 && r.scores[0].neighbour_cluster == 1 && r.scores[2].own_cluster == 1);
     CHECK(r.cluster_names.size() == 2 && r.cluster_names[0] == "7" && r.cluster_names[1] == "3");
+    // the same known answer through the fp64 front end (the reference's Matrix type)
+    const std::vector<double> sq64 = {0, 0, 0, 1, 4, 0, 4, 1};
+    r = fsil::compute_silhouette(ctx, sq64.data(), lab.data(), 4, 2, fsil::Metric::SquaredEuclidean);
+    CHECK(near(r.mean, 31.0 / 33.0, 1e-12) && near(r.scores[3].b, 16.5, 1e-12));
     // orthogonal cosine clusters -> mean 1
     const std::vector<float> co = {1, 0, 2, 0, 0, 1, 0, 3};
     r = fsil::compute_silhouette(ctx, co.data(), lab.data(), 4, 2, fsil::Metric::Cosine);

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "fsil.h")).read()
-    return sorted(set(re.findall(r"\b(fsil_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(fsil_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():

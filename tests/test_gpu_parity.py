@@ -299,7 +299,7 @@ def _shard_loopback(X, L, metric, nshards, path=0):
         for c, x, l, (b, e) in zip(ctxs, Xd, Ld, ranges):
             c.set_path(path)
             c.set_stream(torch.cuda.current_stream(dev).cuda_stream)  # ordered with the exchanges
-            nd = c.shard_begin(metric, x.data_ptr(), l.data_ptr(), e - b, d, b, n)
+            nd = c.shard_begin(metric, x.data_ptr(), l.data_ptr(), e - b, d, b, n, f64=x.dtype == torch.float64)
             labs, rows = c.shard_get_dictionary(nd)
             for lab, row in zip(labs.tolist(), rows.tolist()):
                 first[lab] = min(row, first.get(lab, row))
@@ -365,3 +365,52 @@ def test_shard_protocol_validation_is_global():
     means, errors, *_ = _shard_loopback(X, L, "sqeuclid", 3)
     assert not means and len(errors) == 3
     assert all(e == "non-finite feature value at point 1200, dimension 7" for e in errors)
+
+
+@pytest.mark.parametrize("metric", ["sqeuclid", "cosine"])
+@pytest.mark.parametrize("offset", [0.0, 1000.0])
+def test_fp64_front_end_matches_fp64_oracle(ctx, metric, offset):
+    """fsil_silhouette_f64 on features fp32 cannot represent (and, with the offset, whose
+    fp32 rounding is far coarser than the cluster spread): aggregation and refinement
+    read the fp64 values, so the result is the fp64 reference's -- not the fp32 data's."""
+    rng = np.random.default_rng(11 if offset else 12)
+    n, d, k = 20_000, 64, 12
+    centres = rng.normal(size=(k, d)) * 2.0
+    L = rng.integers(0, k, n)
+    X = (offset + centres[L] + rng.normal(size=(n, d)) * 0.7).astype(np.float64)
+    L = L * 3 + 5
+    ref = oracle.silhouette(X, L, metric)
+    for path in ("auto", "tcgen05", "fp64"):
+        ctx.set_path(PATHS[path])
+        got = ctx.silhouette(X, L, metric)
+        tag = f"fp64 {metric} offset={offset} path={path}"
+        mism = np.flatnonzero(got.neighbour != ref.neighbour)
+        if mism.size:
+            assert reference_noise_ties(X, ref, metric, mism, got.neighbour[mism]).all(), tag
+        assert np.abs(got.s - ref.s).max() <= S_TOL, tag
+        assert abs(got.mean - ref.mean) <= MEAN_TOL, tag
+    ctx.set_path(0)
+
+
+def test_fp64_front_end_rejects_ffma(ctx):
+    from paper_2303_14102_b200 import FsilError
+    X = np.random.default_rng(1).normal(size=(500, 16))
+    L = np.arange(500) % 4
+    ctx.set_path(PATHS["ffma"])
+    try:
+        with pytest.raises((ValueError, FsilError)):
+            ctx.silhouette(X, L, "sqeuclid")
+    finally:
+        ctx.set_path(0)
+
+
+def test_fp64_front_end_sharded():
+    rng = np.random.default_rng(5)
+    n, d = 9000, 32
+    X = (rng.normal(size=(n, d)) * 3 + 50.0).astype(np.float64)
+    L = rng.integers(0, 7, n) * 2 + 1
+    ref = oracle.silhouette(X, L, "sqeuclid")
+    means, errors, s, nb, raw = _shard_loopback(X, L, "sqeuclid", 3, 0)
+    assert not errors and raw.tolist() == ref.dense_to_raw.tolist()
+    assert all(abs(m - ref.mean) <= MEAN_TOL for m in means)
+    assert np.abs(s - ref.s).max() <= S_TOL
