@@ -134,6 +134,17 @@ fsil_status fsil_silhouette_device_f64(fsil_context* ctx, int metric, const doub
                                        double* mean, int32_t* k_out, int32_t* dense_to_raw);
 
 /*
+ * The Theta(N^2 D) engine (naive_silhouette, naive.cpp:30-71) on the GPU:
+ * every pairwise distance in fp64, for cross-checks (the reference's `compare`) and for
+ * FSIL_EUCLID, which has no linear-time decomposition.  Same validation, outputs and
+ * errors as fsil_silhouette_f64; meant for small N (K x 128 + 64 x D doubles of shared
+ * memory per block).
+ */
+fsil_status fsil_silhouette_naive(fsil_context* ctx, int metric, const double* X, const int32_t* labels,
+                                  int64_t n, int32_t d, double* s, int32_t* neighbour, int32_t* own,
+                                  double* a, double* b, double* mean, int32_t* k_out, int32_t* dense_to_raw);
+
+/*
  * Sharded (multi-GPU, one process per GPU) protocol.  Rank r owns the
  * contiguous global rows [row_offset, row_offset + n_local) (plan_shards
  * semantics).  The caller performs the three exchanges between phases with

@@ -18,8 +18,8 @@
 // the raw inputs of validate_and_densify (dataset.hpp:46-48): an N x D row-major fp32 or
 // fp64 matrix -- byte-compatible with a column-major D x N one -- and raw int labels.  The
 // same validation runs on the device, in the reference's order, and fails with the
-// same exception types.  Engine::Naive (the O(N^2 D) oracle, naive.cpp) is not part of
-// the GPU product and is rejected with std::invalid_argument.
+// same exception types.  Engine::Naive runs the Theta(N^2 D) engine (naive.cpp) on the
+// GPU in fp64 -- the only engine for Metric::Euclidean.
 #pragma once
 
 #include <chrono>
@@ -185,15 +185,26 @@ inline SilhouetteReport compute_silhouette(Context& ctx, const T* X, const int32
                                            int shards = 0) {
   static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>, "features are fp32 or fp64");
   (void)shards;
-  if (engine == Engine::Naive)
-    throw std::invalid_argument("the naive O(N^2 D) engine is a CPU oracle; the GPU library runs Engine::Fast");
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<double> s(static_cast<size_t>(n)), a(static_cast<size_t>(n)), b(static_cast<size_t>(n));
   std::vector<int32_t> nb(static_cast<size_t>(n)), own(static_cast<size_t>(n)), raw(static_cast<size_t>(n));
   double mean = 0.0;
   int32_t k = 0;
-  ctx.check(detail::call_host(ctx.handle(), detail::metric_code(metric), X, labels, n, d, s.data(), nb.data(),
-                              own.data(), a.data(), b.data(), &mean, &k, raw.data()));
+  if (engine == Engine::Naive) {  // the Theta(N^2 D) engine (fp64 features; fsil_silhouette_naive)
+    std::vector<double> x64;
+    const double* xp = nullptr;
+    if constexpr (std::is_same_v<T, double>) {
+      xp = X;
+    } else {
+      x64.assign(X, X + static_cast<size_t>(n) * static_cast<size_t>(d));
+      xp = x64.data();
+    }
+    ctx.check(fsil_silhouette_naive(ctx.handle(), detail::metric_code(metric), xp, labels, n, d, s.data(), nb.data(),
+                                    own.data(), a.data(), b.data(), &mean, &k, raw.data()));
+  } else {
+    ctx.check(detail::call_host(ctx.handle(), detail::metric_code(metric), X, labels, n, d, s.data(), nb.data(),
+                                own.data(), a.data(), b.data(), &mean, &k, raw.data()));
+  }
   SilhouetteReport r;
   r.scores.resize(static_cast<size_t>(n));
   for (int64_t i = 0; i < n; ++i) {

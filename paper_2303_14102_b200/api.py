@@ -52,6 +52,8 @@ EXPORTS = {
                                            _P, _P, _P]),
     "fsil_silhouette_device_f64": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _I64, _I32, _P, _P, _P,
                                                   _P, _P, _P, _P, _P]),
+    "fsil_silhouette_naive": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _I64, _I32, _P, _P, _P, _P,
+                                             _P, _P, _P, _P]),
     "fsil_shard_begin": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _I64, _I32, _I64, _I64, _P]),
     "fsil_shard_begin_f64": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _I64, _I32, _I64, _I64, _P]),
     "fsil_shard_get_dictionary": (ctypes.c_int, [_P, _P, _P]),
@@ -209,12 +211,17 @@ class Context:
         return {f: getattr(s, f) for f, _ in fsil_stats._fields_}
 
     # -- whole dataset ----------------------------------------------------------
-    def silhouette(self, X, labels, metric="sqeuclid", want_ab=True) -> SilhouetteReport:
+    def silhouette_naive(self, X, labels, metric="sqeuclid") -> SilhouetteReport:
+        """fsil_silhouette_naive: the Theta(N^2 D) engine (naive.cpp:30-71) on the GPU, every
+        pairwise distance in fp64; the only engine for metric "euclid"."""
+        return self.silhouette(X, labels, metric, want_ab=True, _naive=True)
+
+    def silhouette(self, X, labels, metric="sqeuclid", want_ab=True, _naive=False) -> SilhouetteReport:
         """fsil_silhouette over host arrays (copies in and out of HBM).  float64 features
         take the fp64 front end (fsil_silhouette_f64: exact aggregation and refinement
         on the caller's values, the reference's own Matrix type); anything else is fp32."""
         m = metric_code(metric)
-        f64 = getattr(X, "dtype", None) == np.float64
+        f64 = _naive or getattr(X, "dtype", None) == np.float64
         X = np.ascontiguousarray(X, dtype=np.float64 if f64 else np.float32)
         if X.ndim != 2:
             X = X.reshape(X.shape[0], -1)
@@ -231,12 +238,13 @@ class Context:
         k = ctypes.c_int32(0)
         d2r = np.empty(max(n, 1), np.int32)
         t0 = time.perf_counter()
-        entry = lib().fsil_silhouette_f64 if f64 else lib().fsil_silhouette
+        entry = (lib().fsil_silhouette_naive if _naive else
+                 lib().fsil_silhouette_f64 if f64 else lib().fsil_silhouette)
         self._check(entry(self._h, m, _ptr(X), _ptr(labels), n, d, _ptr(s), _ptr(nb), _ptr(own), _ptr(a),
                           _ptr(b), ctypes.byref(mean), ctypes.byref(k), _ptr(d2r)))
         wall = (time.perf_counter() - t0) * 1e3
-        return SilhouetteReport(s, nb, own, a, b, mean.value, _METRIC_TAGS[m], "fast", 1, wall,
-                                d2r[: k.value].tolist())
+        return SilhouetteReport(s, nb, own, a, b, mean.value, _METRIC_TAGS[m], "naive" if _naive else "fast",
+                                1, wall, d2r[: k.value].tolist())
 
     def silhouette_device(self, X, labels, metric="sqeuclid", s=None, neighbour=None, own=None,
                           a=None, b=None, dense_to_raw=None):
@@ -309,10 +317,10 @@ def compute_silhouette(X, labels, metric="sqeuclid", engine="fast", shards: int 
     (engine.cpp:76-92) on one B200.  `shards` is accepted for signature parity (the
     reference's CPU thread count); the device decomposition is fixed by the kernels.
     Multi-GPU row sharding lives in paper_2303_14102_b200.distributed."""
-    if engine != "fast":
-        raise ValidationError("the B200 engine implements the fast (linear-time) path; the naive "
-                              "O(N^2 D) engine is the CPU oracle")
-    rep = default_context(device).silhouette(X, labels, metric)
+    if engine not in ("fast", "naive"):
+        raise ValidationError(f"unknown engine '{engine}' (use fast or naive)")
+    ctx = default_context(device)
+    rep = ctx.silhouette_naive(X, labels, metric) if engine == "naive" else ctx.silhouette(X, labels, metric)
     rep.shards = shards if shards > 0 else 1
     return rep
 
@@ -338,3 +346,27 @@ def assemble_score(a: float, b: float) -> float:
     if st != OK:
         raise ValueError(f"assemble_score: negative mean distance (a={a}, b={b})")
     return s.value
+
+
+def compare(X, labels, metric="sqeuclid", rtol=1e-9, atol=1e-12, inject_fault=0.0, device: int = 0) -> dict:
+    """The reference's `compare` (tools/main.cpp:62-108) on the GPU: the fast engine against
+    the naive Theta(N^2 D) engine; every a_i, b_i, s_i must satisfy |fast - naive| <= atol +
+    rtol |naive|.  `inject_fault` perturbs the fast s_i (the reference's test hook).  The
+    reference's defaults (1e-9, 1e-12) are fp64-vs-fp64; this fast engine certifies
+    |ds_i| <= 1e-5 absolute, so GPU compares use atol = 1e-5 and
+    rtol ~ 1e-4 (a_i, b_i are certified to ~1e-5 relative)."""
+    ctx = default_context(device)
+    fast = ctx.silhouette(X, labels, metric)
+    naive = ctx.silhouette_naive(X, labels, metric)
+    fs = fast.s + inject_fault
+    max_abs, max_rel, within = 0.0, 0.0, True
+    for got, ref in ((fast.a, naive.a), (fast.b, naive.b), (fs, naive.s)):
+        dev = np.abs(got - ref)
+        max_abs = max(max_abs, float(dev.max(initial=0.0)))
+        nz = ref != 0
+        if nz.any():
+            max_rel = max(max_rel, float((dev[nz] / np.abs(ref[nz])).max()))
+        within = within and bool(np.all(dev <= atol + rtol * np.abs(ref)))
+    return {"fast_mean": fast.mean, "naive_mean": naive.mean, "max_abs_deviation": max_abs,
+            "max_rel_deviation": max_rel, "within": within, "rtol": rtol, "atol": atol,
+            "fast_wall_ms": fast.wall_time_ms, "naive_wall_ms": naive.wall_time_ms}

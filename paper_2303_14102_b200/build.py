@@ -26,7 +26,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas",
          f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 
 LIBS = {
-    "libfsil.so": ["densify.cu", "aggregate.cu", "score_ffma.cu", "score_tc.cu", "finalize.cu",
+    "libfsil.so": ["densify.cu", "aggregate.cu", "score_ffma.cu", "score_tc.cu", "naive.cu", "finalize.cu",
                    "capi.cu"],
     "libfsil_datagen.so": ["datagen.cu"],
 }

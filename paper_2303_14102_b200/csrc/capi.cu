@@ -19,6 +19,8 @@ namespace fsil {
 
 void score_ffma(fsil_context* c, const ScoreParams& p);
 int64_t ffma_tiles(int64_t n);
+void score_naive(fsil_context* c, const ScoreParams& p);
+int64_t naive_tiles(int64_t n, int* tile_rows);
 bool ffma_supported(const fsil_context* c);
 void flag_all(fsil_context* c, const ScoreParams& p, int tile_rows);
 void exact_ab(fsil_context* c, const ScoreParams& p);
@@ -150,8 +152,29 @@ void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, 
   c->result.ensure(4 * sizeof(double));
   FSIL_CUDA(cudaMemsetAsync(c->result.p, 0, 4 * sizeof(double), c->stream));
   c->phase = 4;
-  if (c->k < 2 || c->metric == FSIL_EUCLID || c->n == 0) {  // reported by finish
+  if (c->k < 2 || (c->metric == FSIL_EUCLID && !c->naive_call) || c->n == 0) {  // reported by finish
     record(c, 3); record(c, 4); record(c, 5);
+    return;
+  }
+  if (c->naive_call) {  // the Theta(N^2 D) engine: every pair in fp64, nothing to refine
+    ScoreParams p = make_params(c, s, nb, own, a, b);
+    int tile_rows = 128;
+    const int64_t ntiles = naive_tiles(c->n, &tile_rows);
+    c->tile_sum.ensure(std::max<int64_t>(ntiles, 1) * sizeof(double));
+    c->tile_flag.ensure(std::max<int64_t>(ntiles, 1) * sizeof(int32_t));
+    c->flag_count.ensure(sizeof(unsigned long long));
+    FSIL_CUDA(cudaMemsetAsync(c->flag_count.p, 0, sizeof(unsigned long long), c->stream));
+    p.tile_sum = c->tile_sum.as<double>();
+    p.tile_flag = c->tile_flag.as<int32_t>();
+    p.flag_count = c->flag_count.as<unsigned long long>();
+    record(c, 3);
+    c->tc_exact_used = false;
+    score_naive(c, p);
+    c->score_path = 0;
+    record(c, 4);
+    record(c, 5);
+    finalize_sum(c, p, ntiles, tile_rows, c->local_call);
+    c->summary_packed = c->local_call;
     return;
   }
   derive(c);
@@ -239,7 +262,7 @@ double finish(fsil_context* c, double* flagged_out) {
   if (c->k < 2)
     fail(FSIL_ERR_VALIDATION, "silhouette undefined for a single cluster: need K >= 2, got K = " +
                                   std::to_string(c->k));
-  if (c->metric == FSIL_EUCLID)
+  if (c->metric == FSIL_EUCLID && !c->naive_call)
     fail(FSIL_ERR_VALIDATION,
          "no fast engine for plain euclidean distance (no aggregable decomposition); use the naive "
          "engine");
@@ -463,8 +486,13 @@ namespace {
 template <typename T>
 fsil_status host_call(fsil_context* c, int metric, const T* X, const int32_t* labels, int64_t n, int32_t d,
                       double* s, int32_t* neighbour, int32_t* own, double* a, double* b, double* mean,
-                      int32_t* k_out, int32_t* dense_to_raw) {
+                      int32_t* k_out, int32_t* dense_to_raw, bool naive = false) {
   if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  struct NaiveScope {  // the engine flag lasts for this call only
+    fsil_context* c;
+    ~NaiveScope() { c->naive_call = false; }
+  } scope{c};
+  c->naive_call = naive;
   return guarded(c, [&] {
     check_metric(metric);
     check_shape(n, d);
@@ -507,6 +535,11 @@ fsil_status fsil_silhouette_f64(fsil_context* c, int metric, const double* X, co
                                 int32_t d, double* s, int32_t* neighbour, int32_t* own, double* a, double* b,
                                 double* mean, int32_t* k_out, int32_t* dense_to_raw) {
   return host_call(c, metric, X, labels, n, d, s, neighbour, own, a, b, mean, k_out, dense_to_raw);
+}
+fsil_status fsil_silhouette_naive(fsil_context* c, int metric, const double* X, const int32_t* labels, int64_t n,
+                                  int32_t d, double* s, int32_t* neighbour, int32_t* own, double* a, double* b,
+                                  double* mean, int32_t* k_out, int32_t* dense_to_raw) {
+  return host_call(c, metric, X, labels, n, d, s, neighbour, own, a, b, mean, k_out, dense_to_raw, true);
 }
 fsil_status fsil_shard_begin(fsil_context* c, int metric, const float* dX, const int32_t* dlabels,
                              int64_t n_local, int32_t d, int64_t row_offset, int64_t n_global,

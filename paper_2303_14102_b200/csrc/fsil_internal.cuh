@@ -150,6 +150,7 @@ struct fsil_context {
   int64_t k_last = 0;        // K of the previous call (picks the ordering path)
   bool local_call = false;   // single-GPU call (fsil_silhouette[_device]), not the shard protocol
   bool summary_packed = false;  // this call's HostSummary already written on the device
+  bool naive_call = false;      // fsil_silhouette_naive: the Theta(N^2 D) engine
   fsil::HostSummary* hsum = nullptr;  // mapped pinned (host view)
   fsil::HostSummary* dsum = nullptr;  // device view of the same memory
   cudaEvent_t ev[8] = {};

@@ -86,13 +86,13 @@ int main(int argc, char** argv) {
       threw = true;
     }
     CHECK(threw);
-    threw = false;
-    try {
-      fsil::compute_silhouette(ctx, sq.data(), lab.data(), 4, 2, fsil::Metric::SquaredEuclidean, fsil::Engine::Naive);
-    } catch (const std::invalid_argument&) {
-      threw = true;
-    }
-    CHECK(threw);
+    // the naive engine: the same known answer, and plain Euclidean (naive only):
+    // a = 1, b = (4 + sqrt(17)) / 2 for every point of the square
+    r = fsil::compute_silhouette(ctx, sq.data(), lab.data(), 4, 2, fsil::Metric::SquaredEuclidean, fsil::Engine::Naive);
+    CHECK(near(r.mean, 31.0 / 33.0, 1e-12) && r.engine == fsil::Engine::Naive);
+    r = fsil::compute_silhouette(ctx, sq.data(), lab.data(), 4, 2, fsil::Metric::Euclidean, fsil::Engine::Naive);
+    const double be = (4.0 + std::sqrt(17.0)) / 2.0;
+    CHECK(near(r.scores[0].a, 1.0, 1e-12) && near(r.scores[0].b, be, 1e-12) && near(r.mean, 1.0 - 1.0 / be, 1e-12));
     std::printf("golden: mean %.17g, K %zu, path %d\n", 31.0 / 33.0, r.cluster_names.size(), ctx.stats().path);
   }
   if (failures) std::fprintf(stderr, "%d check(s) failed\n", failures);

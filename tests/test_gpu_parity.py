@@ -414,3 +414,35 @@ def test_fp64_front_end_sharded():
     assert not errors and raw.tolist() == ref.dense_to_raw.tolist()
     assert all(abs(m - ref.mean) <= MEAN_TOL for m in means)
     assert np.abs(s - ref.s).max() <= S_TOL
+
+
+@pytest.mark.parametrize("metric", ["sqeuclid", "cosine", "euclid"])
+def test_naive_engine_matches_naive_oracle(ctx, metric):
+    """fsil_silhouette_naive (every pairwise distance in fp64, naive.cpp:30-71) against the
+    oracle's own naive engine -- including plain Euclidean, which only this engine serves."""
+    rng = np.random.default_rng(21)
+    n, d = 3000, 16
+    X = rng.normal(size=(n, d)) + rng.normal(size=(6, d))[rng.integers(0, 6, n)] * 3
+    L = rng.integers(0, 6, n) * 7 + 2
+    L[17] = 999  # a singleton
+    ref = oracle.silhouette(X, L, metric, engine="naive")
+    got = ctx.silhouette_naive(X, L, metric)
+    assert got.engine == "naive"
+    assert np.array_equal(got.neighbour, ref.neighbour)
+    assert np.abs(got.s - ref.s).max() <= 1e-12
+    assert np.allclose(got.a, ref.a, rtol=1e-12, atol=1e-12) and np.allclose(got.b, ref.b, rtol=1e-12, atol=1e-12)
+    assert abs(got.mean - ref.mean) <= 1e-13
+
+
+def test_compare_fast_against_naive():
+    """The reference's compare contract (tools/main.cpp:62-108) on the GPU engines."""
+    from paper_2303_14102_b200.api import compare
+    rng = np.random.default_rng(22)
+    X = rng.normal(size=(4000, 32)) + rng.normal(size=(5, 32))[rng.integers(0, 5, 4000)] * 2
+    L = rng.integers(0, 5, 4000)
+    # the fast engine's contract: |ds_i| <= 1e-5 (absolute), a_i/b_i to ~1e-5 relative
+    for metric in ("cosine", "sqeuclid"):
+        ok = compare(X, L, metric, rtol=1e-4, atol=S_TOL)
+        assert ok["within"] and abs(ok["fast_mean"] - ok["naive_mean"]) <= MEAN_TOL, (metric, ok)
+    bad = compare(X, L, "cosine", rtol=1e-4, atol=S_TOL, inject_fault=1e-3)
+    assert not bad["within"] and bad["max_abs_deviation"] >= 1e-3 * 0.99
