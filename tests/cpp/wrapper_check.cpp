@@ -10,6 +10,9 @@
 #include <string>
 #include <vector>
 
+#include <sstream>
+
+#include "fsil/report_io.hpp"
 #include "fsil/silhouette.hpp"
 
 static int failures = 0;
@@ -39,6 +42,19 @@ int main(int argc, char** argv) {
   }
   CHECK(threw);
   CHECK(fsil::parse_metric("sqeuclid") == fsil::Metric::SquaredEuclidean);
+  // report emission (report_io.cpp): 17 significant digits, csv + summary, jsonl
+  {
+    fsil::SilhouetteReport rep;
+    rep.scores.push_back({1.0, 16.5, 1.0 - 1.0 / 16.5, 0, 1});
+    rep.mean = 0.1;
+    std::ostringstream csv, js;
+    fsil::write_report(rep, csv, fsil::ReportFormat::Csv);
+    fsil::write_report(rep, js, fsil::ReportFormat::Jsonl);
+    CHECK(csv.str() == "index,own_cluster,neighbour_cluster,a,b,s\n0,0,1,1,16.5,0.93939393939393945\n"
+                       "# summary: mean=0.10000000000000001 metric=squared_euclidean engine=fast shards=1 "
+                       "wall_time_ms=0\n");
+    CHECK(js.str().rfind("{\"index\":0,\"own\":0,\"neighbour\":1,\"a\":1,\"b\":16.5,\"s\":0.93939393939393945}\n", 0) == 0);
+  }
   CHECK(fsil::metric_name(fsil::Metric::Cosine) == "cosine");
 
   if (mode == "no-device") {

@@ -446,3 +446,30 @@ def test_compare_fast_against_naive():
         assert ok["within"] and abs(ok["fast_mean"] - ok["naive_mean"]) <= MEAN_TOL, (metric, ok)
     bad = compare(X, L, "cosine", rtol=1e-4, atol=S_TOL, inject_fault=1e-3)
     assert not bad["within"] and bad["max_abs_deviation"] >= 1e-3 * 0.99
+
+
+def test_cli_score_and_compare(tmp_path):
+    """The reference tool's score / compare over the GPU engines: CSV in, report out,
+    exit codes 0 (ok) and 3 (tolerance exceeded) -- tools/main.cpp:19-108."""
+    import json
+    import subprocess
+    import sys
+    from paper_2303_14102_b200.io import CsvDataset, write_points_csv
+    rng = np.random.default_rng(31)
+    X = rng.normal(size=(1500, 8)) + rng.normal(size=(4, 8))[rng.integers(0, 4, 1500)] * 3
+    L = rng.integers(0, 4, 1500).astype(np.int32)
+    csv = tmp_path / "pts.csv"
+    write_points_csv(CsvDataset(X, L, ["w", "x", "y", "z"]), csv)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    run = lambda *a: subprocess.run([sys.executable, "-m", "paper_2303_14102_b200", *a], cwd=root,
+                                    capture_output=True, text=True, timeout=300)
+    out = tmp_path / "rep.jsonl"
+    r = run("score", "--input", str(csv), "--metric", "cosine", "--output", str(out))
+    assert r.returncode == 0, r.stderr
+    lines = [json.loads(x) for x in out.read_text().splitlines()]
+    ref = oracle.silhouette(X, L, "cosine")
+    assert len(lines) == 1501 and abs(lines[-1]["mean"] - ref.mean) <= MEAN_TOL
+    assert max(abs(p["s"] - ref.s[p["index"]]) for p in lines[:-1]) <= S_TOL
+    assert run("score", "--input", str(csv), "--engine", "naive", "--format", "csv").returncode == 0
+    assert run("compare", "--input", str(csv)).returncode == 0
+    assert run("compare", "--input", str(csv), "--inject-fault", "1e-3").returncode == 3
