@@ -551,18 +551,35 @@ __global__ void __launch_bounds__(256) agg_piece_kernel(
   }
 }
 
-__global__ void fold_pieces_kernel(const double* __restrict__ piece_out,
-                                   const int64_t* __restrict__ piece_start, int k, int d, bool cos,
-                                   double* __restrict__ stats) {
+// Piece partials -> stats.  A block folds one cluster's 32-column slice: warp w sums the
+// pieces p = w, w + 8, ... (lanes = columns: coalesced, independent loads), then the 8
+// warp partials in a fixed order -- deterministic, and a large cluster's pieces are
+// folded 8 x 32 wide instead of by one thread each.
+__global__ void __launch_bounds__(256) fold_pieces_kernel(const double* __restrict__ piece_out,
+                                                          const int64_t* __restrict__ piece_start, int k, int d,
+                                                          bool cos, double* __restrict__ stats) {
+  __shared__ double part[8][33];
   const int S1 = cos ? d + 1 : d + 2;
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= static_cast<int64_t>(k) * S1) return;
-  const int c = static_cast<int>(t / S1), j = static_cast<int>(t % S1);
+  const int nchunk = (S1 + 31) / 32;
+  const int c = static_cast<int>(blockIdx.x / nchunk);
+  const int j = static_cast<int>(blockIdx.x % nchunk) * 32 + (threadIdx.x & 31);
+  const int w = threadIdx.x >> 5;
   double acc = 0.0;
-  for (int64_t p = piece_start[c]; p < piece_start[c + 1]; ++p) acc += piece_out[p * S1 + j];
-  if (j == 0) stats[c] = acc;
-  else if (!cos && j == 1) stats[k + c] = acc;
-  else stats[(cos ? k : 2 * k) + static_cast<int64_t>(c) * d + (j - (cos ? 1 : 2))] = acc;
+  if (j < S1) {
+    const int64_t p1 = piece_start[c + 1];
+#pragma unroll 4
+    for (int64_t p = piece_start[c] + w; p < p1; p += 8) acc += piece_out[p * S1 + j];
+  }
+  part[w][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (w == 0 && j < S1) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += part[q][threadIdx.x];
+    if (j == 0) stats[c] = t;
+    else if (!cos && j == 1) stats[k + c] = t;
+    else stats[(cos ? k : 2 * k) + static_cast<int64_t>(c) * d + (j - (cos ? 1 : 2))] = t;
+  }
 }
 
 // ---------------------------------------------------------------- derive ----
@@ -803,8 +820,7 @@ void aggregate(fsil_context* c) {
     if (cos) launch_pieces<true>(c, c->X, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);
     else launch_pieces<false>(c, c->X, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);
   }
-  const int64_t nthreads = static_cast<int64_t>(c->k) * S1;
-  fold_pieces_kernel<<<static_cast<unsigned>((nthreads + 255) / 256), 256, 0, c->stream>>>(
+  fold_pieces_kernel<<<static_cast<unsigned>(static_cast<int64_t>(c->k) * ((S1 + 31) / 32)), 256, 0, c->stream>>>(
       c->partials.as<double>(), piece_start, c->k, c->d, cos, stats);
   FSIL_LAUNCHED(c);
 }
