@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="override N (parity/debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU protocol (NCCL exchanges) even on one rank (path check)")
     return ap.parse_args()
 
 
@@ -184,7 +186,8 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    sharded = world > 1 or a.sharded
+    if sharded:
         dist.init_process_group("nccl", device_id=dev)
     from paper_2303_14102_b200 import Context, PATH_AUTO, PATH_FFMA, PATH_TCGEN05
     from paper_2303_14102_b200.api import PATH_FP64
@@ -203,7 +206,7 @@ def main():
     n_global = N * world
 
     def step():
-        if world == 1:
+        if not sharded:
             return ctx.silhouette_device(X, L, metric, s=s, neighbour=nb)[0]
         return compute_silhouette_sharded(ctx, metric, X, L, rank * N, n_global, s=s, neighbour=nb)
 
@@ -225,7 +228,7 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    if world > 1:
+    if sharded:
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -234,11 +237,11 @@ def main():
         mean = step()
     ev1.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
+    if sharded:
         dist.barrier()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1) / a.steps
-    if world > 1:
+    if sharded:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -318,7 +321,7 @@ def main():
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(launches_per_step) * a.steps, "clocks": clk}
         print(json.dumps(out))
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
     return 0
 

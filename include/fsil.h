@@ -178,6 +178,23 @@ fsil_status fsil_shard_score(fsil_context* ctx, double* ds, int32_t* dneighbour,
                              double* da, double* db, double** d_partial);
 fsil_status fsil_shard_finish(fsil_context* ctx, double* mean);
 
+/*
+ * The same protocol with the dictionary exchange on the device (no host round trip):
+ *   fsil_shard_begin_device        -> device buffer of `capacity` (label, first global row)
+ *                                     int64 pairs (unused: row -1), identical capacity on
+ *                                     every rank; xtype 0 = fp32 features, 1 = fp64
+ *   [exchange: all-gather the buffers of all ranks, rank order]
+ *   fsil_shard_set_dictionary_device <- the gathered nranks x capacity pairs: merged on the
+ *                                     device (first appearance), one host sync for K
+ * then fsil_shard_aggregate / _score / _finish as above.
+ */
+fsil_status fsil_shard_begin_device(fsil_context* ctx, int metric, const void* dX, int xtype,
+                                    const int32_t* dlabels, int64_t n_local, int32_t d,
+                                    int64_t row_offset, int64_t n_global, int64_t** d_entries,
+                                    int64_t* capacity);
+fsil_status fsil_shard_set_dictionary_device(fsil_context* ctx, const int64_t* d_gathered,
+                                             int32_t nranks, int64_t capacity);
+
 /* plan_shards (engine.cpp:8-25): writes w' = min(w, n) (begin, end) pairs. */
 fsil_status fsil_plan_shards(int64_t n, int32_t requested, int64_t* ranges, int32_t* num_shards);
 /* assemble_score (report.cpp:7-14). */

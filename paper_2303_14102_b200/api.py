@@ -56,6 +56,9 @@ EXPORTS = {
                                              _P, _P, _P, _P]),
     "fsil_shard_begin": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _I64, _I32, _I64, _I64, _P]),
     "fsil_shard_begin_f64": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _I64, _I32, _I64, _I64, _P]),
+    "fsil_shard_begin_device": (ctypes.c_int, [_P, ctypes.c_int, _P, ctypes.c_int, _P, _I64, _I32, _I64, _I64,
+                                               _P, _P]),
+    "fsil_shard_set_dictionary_device": (ctypes.c_int, [_P, _P, _I32, _I64]),
     "fsil_shard_get_dictionary": (ctypes.c_int, [_P, _P, _P]),
     "fsil_shard_set_dictionary": (ctypes.c_int, [_P, _P, _I32]),
     "fsil_shard_aggregate": (ctypes.c_int, [_P, _P, _P, _P]),
@@ -272,6 +275,17 @@ class Context:
         self._check(entry(self._h, metric_code(metric), x_ptr, l_ptr, n_local, d, row_offset, n_global,
                           ctypes.byref(nd)))
         return nd.value
+
+    def shard_begin_device(self, metric, x_ptr, l_ptr, n_local, d, row_offset, n_global, f64=False):
+        """Device dictionary exchange, pass 1: (entries device pointer, capacity)."""
+        ptr, cap = ctypes.c_void_p(), ctypes.c_int64(0)
+        self._check(lib().fsil_shard_begin_device(self._h, metric_code(metric), x_ptr, 1 if f64 else 0, l_ptr,
+                                                  n_local, d, row_offset, n_global, ctypes.byref(ptr),
+                                                  ctypes.byref(cap)))
+        return ptr.value, cap.value
+
+    def shard_set_dictionary_device(self, gathered_ptr, nranks, capacity):
+        self._check(lib().fsil_shard_set_dictionary_device(self._h, gathered_ptr, nranks, capacity))
 
     def shard_get_dictionary(self, n_distinct):
         labs = np.empty(max(n_distinct, 1), np.int32)

@@ -560,6 +560,37 @@ fsil_status fsil_shard_begin_f64(fsil_context* c, int metric, const double* dX, 
   });
 }
 
+fsil_status fsil_shard_begin_device(fsil_context* c, int metric, const void* dX, int xtype, const int32_t* dlabels,
+                                    int64_t n_local, int32_t d, int64_t row_offset, int64_t n_global,
+                                    int64_t** d_entries, int64_t* capacity) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    if (xtype != 0 && xtype != 1) fail(FSIL_ERR_INVALID_ARGUMENT, "xtype: 0 (fp32) or 1 (fp64)");
+    c->launches = 0;
+    setup(c, metric, dX, xtype == 1, dlabels, n_local, d, row_offset, n_global);
+    c->local_call = false;
+    // the same capacity on every rank: from the previous call's global K (identical everywhere)
+    int64_t cap_x = 8192;
+    while (cap_x < 2 * c->k_global_last + 2) cap_x *= 2;
+    int64_t* buf = densify_exchange_begin(c, cap_x);
+    c->phase = 1;
+    if (d_entries) *d_entries = buf;
+    if (capacity) *capacity = cap_x;
+  });
+}
+fsil_status fsil_shard_set_dictionary_device(fsil_context* c, const int64_t* d_gathered, int32_t nranks,
+                                             int64_t capacity) {
+  if (!c) return FSIL_ERR_INVALID_ARGUMENT;
+  return guarded(c, [&] {
+    if (c->phase < 1) fail(FSIL_ERR_INVALID_ARGUMENT, "fsil_shard_begin_device must come first");
+    if (!d_gathered || nranks < 1 || capacity < 2) fail(FSIL_ERR_INVALID_ARGUMENT, "bad exchange buffer");
+    densify_exchange_set(c, d_gathered, nranks, capacity);
+    c->k_global_last = c->k;
+    record(c, 1);
+    c->phase = 2;
+  });
+}
+
 fsil_status fsil_shard_get_dictionary(fsil_context* c, int32_t* raw_labels, int64_t* first_rows) {
   if (!c) return FSIL_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {

@@ -238,6 +238,46 @@ __global__ void densify_assign_kernel(const unsigned long long* __restrict__ key
   if (slot >= 0) slot_dense[slot] = j;
 }
 
+// Device-side dictionary exchange (sharded protocol without host round trips).
+// Local entries -> a fixed-capacity buffer of (label, first global row) int64 pairs,
+// unused entries row = -1; the last entry carries row = -2 if this rank's labels did
+// not fit (every rank then fails the merge the same way).
+__global__ void densify_xcompact_kernel(const unsigned long long* __restrict__ keys,
+                                        const unsigned long long* __restrict__ vals, uint32_t cap, uint32_t epoch,
+                                        int64_t row_offset, int64_t* xbuf, int64_t cap_x, unsigned long long* count,
+                                        const int* overflow) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0 && *overflow) {  // local table overflow: poison the exchange
+    xbuf[2 * (cap_x - 1)] = 0;
+    xbuf[2 * (cap_x - 1) + 1] = -2;
+  }
+  if (i >= cap) return;
+  const unsigned long long key = keys[i];
+  if (static_cast<uint32_t>(key >> 32) != epoch) return;
+  const unsigned long long j = atomicAdd(count, 1ull);
+  if (static_cast<int64_t>(j) >= cap_x - 1) {  // the last slot is the header
+    xbuf[2 * (cap_x - 1)] = 0;
+    xbuf[2 * (cap_x - 1) + 1] = -2;
+    return;
+  }
+  xbuf[2 * j] = static_cast<int32_t>(static_cast<uint32_t>(key));
+  xbuf[2 * j + 1] = row_offset + static_cast<int64_t>(value_row(vals[i]));
+}
+
+// Every rank's gathered entries -> one table (label -> min first global row).
+__global__ void densify_xinsert_kernel(const int64_t* __restrict__ gathered, int64_t total,
+                                       unsigned long long* keys, unsigned long long* vals, uint32_t mask,
+                                       uint32_t epoch, int* overflow) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const int64_t row = gathered[2 * e + 1];
+  if (row == -2) atomicExch(overflow, 1);
+  if (row < 0) return;
+  if (row >= 0xffffffffll || !global_insert(keys, vals, mask, epoch, static_cast<int32_t>(gathered[2 * e]),
+                                             static_cast<uint32_t>(row)))
+    atomicExch(overflow, 1);
+}
+
 int grid_for(int64_t n, int threads, int num_sms, int per_sm) {
   const int64_t want = (n + threads - 1) / threads;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(num_sms) * per_sm)));
@@ -386,6 +426,82 @@ void densify_assign_and_map(fsil_context* c, const int32_t* raw_in_dense_order, 
     FSIL_LAUNCHED(c);
   }
   // `missing` is checked by the caller at the end of the call (no extra sync here).
+}
+
+}  // namespace fsil
+
+namespace fsil {
+
+// Sharded protocol, device exchange, pass 1: local dictionary into the exchange buffer
+// (no host sync).  Returns the buffer (cap_x entries of two int64).
+int64_t* densify_exchange_begin(fsil_context* c, int64_t cap_x) {
+  if (c->n >= (int64_t(1) << 32) - 1)
+    fail(FSIL_ERR_INVALID_ARGUMENT, "shard too large: a rank holds at most 2^32-2 rows");
+  const int64_t cap = std::max<int64_t>(c->ht_cap, 8192);
+  const uint32_t epoch = prepare_table(c, cap);
+  launch_collect(c, cap, epoch);
+  c->xbuf.ensure(static_cast<size_t>(cap_x) * 2 * sizeof(int64_t));
+  FSIL_CUDA(cudaMemsetAsync(c->xbuf.p, 0xff, static_cast<size_t>(cap_x) * 2 * sizeof(int64_t), c->stream));
+  unsigned long long* count = reinterpret_cast<unsigned long long*>(c->counters.as<char>() + 8);
+  densify_xcompact_kernel<<<static_cast<unsigned>((cap + 255) / 256), 256, 0, c->stream>>>(
+      c->ht_keys.as<unsigned long long>(), c->ht_vals.as<unsigned long long>(), static_cast<uint32_t>(cap), epoch,
+      c->row_offset, c->xbuf.as<int64_t>(), cap_x, count, c->counters.as<int>());
+  FSIL_LAUNCHED(c);
+  return c->xbuf.as<int64_t>();
+}
+
+// Pass 2: merge the gathered buffers of `nranks` ranks into the global dictionary
+// (first-appearance order), dense ids for this rank's rows; one host sync for K.
+void densify_exchange_set(fsil_context* c, const int64_t* gathered, int nranks, int64_t cap_x) {
+  int64_t cap = 8192;
+  while (cap < 2 * static_cast<int64_t>(nranks) * cap_x && cap < (int64_t(1) << 26)) cap *= 2;
+  const uint32_t epoch = prepare_table(c, cap);  // the exchange reuses the context table
+  int* counters = c->counters.as<int>();
+  const uint32_t mask = static_cast<uint32_t>(cap - 1);
+  c->dict_sorted.ensure(cap * (2 * sizeof(int32_t)));
+  c->dense.ensure(std::max<int64_t>(c->n, 1) * sizeof(int32_t));
+  int32_t* sorted_labels = reinterpret_cast<int32_t*>(c->dict_sorted.p) + cap;
+  const int64_t total = static_cast<int64_t>(nranks) * cap_x;
+  densify_xinsert_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, c->stream>>>(
+      gathered, total, c->ht_keys.as<unsigned long long>(), c->ht_vals.as<unsigned long long>(), mask, epoch,
+      counters);
+  FSIL_LAUNCHED(c);
+  densify_finish_kernel<<<1, 1024, 0, c->stream>>>(c->ht_keys.as<unsigned long long>(),
+                                                   c->ht_vals.as<unsigned long long>(), static_cast<uint32_t>(cap),
+                                                   epoch, sorted_labels, c->ht_dense.as<int32_t>(), counters, c->dsum);
+  FSIL_LAUNCHED(c);
+  FSIL_CUDA(cudaStreamSynchronize(c->stream));
+  const volatile HostSummary* hs = c->hsum;
+  if (hs->overflow)
+    fail(FSIL_ERR_INVALID_ARGUMENT, "device dictionary exchange: more distinct labels than its capacity (" +
+                                        std::to_string(cap_x - 1) + " per rank); use the host exchange");
+  const int64_t cnt = hs->count;
+  if (hs->pad) {  // more labels than the one-block ordering holds: multi-block
+    c->dict_labels.ensure(cap * sizeof(int32_t));
+    c->dict_rows.ensure(cap * sizeof(int64_t));
+    int32_t* slots = reinterpret_cast<int32_t*>(c->dict_sorted.p);
+    unsigned long long* count = reinterpret_cast<unsigned long long*>(c->counters.as<char>() + 8);
+    FSIL_CUDA(cudaMemsetAsync(count, 0, sizeof(unsigned long long), c->stream));
+    densify_compact_kernel<<<static_cast<unsigned>((cap + 255) / 256), 256, 0, c->stream>>>(
+        c->ht_keys.as<unsigned long long>(), c->ht_vals.as<unsigned long long>(), static_cast<uint32_t>(cap), epoch, 0,
+        c->dict_labels.as<int32_t>(), c->dict_rows.as<int64_t>(), slots, count);
+    FSIL_LAUNCHED(c);
+    densify_rank_kernel<<<static_cast<unsigned>((cap + 255) / 256), 256, 0, c->stream>>>(
+        c->dict_labels.as<int32_t>(), c->dict_rows.as<int64_t>(), slots, count, sorted_labels,
+        c->ht_dense.as<int32_t>());
+    FSIL_LAUNCHED(c);
+  }
+  FSIL_CUDA(cudaMemsetAsync(counters + 4, 0, sizeof(int), c->stream));  // missing
+  if (c->n > 0) {
+    densify_map_kernel<<<grid_for(c->n, 256, c->num_sms, 8), 256, 0, c->stream>>>(
+        c->labels, c->n, c->ht_keys.as<unsigned long long>(), c->ht_dense.as<int32_t>(), mask, epoch,
+        c->dense.as<int32_t>(), counters + 4);
+    FSIL_LAUNCHED(c);
+  }
+  c->ht_cap = std::max<int64_t>(c->ht_cap, 8192);
+  c->n_distinct = cnt;
+  c->k = static_cast<int32_t>(cnt);
+  c->dict_sorted_labels = sorted_labels;
 }
 
 }  // namespace fsil

@@ -140,6 +140,7 @@ struct fsil_context {
   fsil::DevBuf exact_rows, exact_count;  // rows needing the exact own/neighbour recompute
   fsil::DevBuf a_scratch;                // tcgen05 streaming mode: per-CTA converted A chunks
   fsil::DevBuf x32;                      // fp64 front end: rounded fp32 copy for the fast pass
+  fsil::DevBuf xbuf;                     // sharded protocol: device dictionary exchange entries
   bool tc_exact_used = false;
   // host staging for fsil_silhouette (pageable -> pinned)
   fsil::DevBuf hX, hL;         // device copies of host inputs
@@ -148,6 +149,7 @@ struct fsil_context {
   int64_t ht_alloc_cap = 0;  // slots of the current (zero-initialised) table
   uint32_t ht_epoch = 0;     // epoch of the last densify (table entries are epoch-tagged)
   int64_t k_last = 0;        // K of the previous call (picks the ordering path)
+  int64_t k_global_last = 0; // sharded: the previous call's global K (sizes the device exchange)
   bool local_call = false;   // single-GPU call (fsil_silhouette[_device]), not the shard protocol
   bool summary_packed = false;  // this call's HostSummary already written on the device
   bool naive_call = false;      // fsil_silhouette_naive: the Theta(N^2 D) engine
@@ -162,6 +164,8 @@ namespace fsil {
 void densify_collect(fsil_context* c);     // fills ctx->n_distinct (syncs)
 void densify_local(fsil_context* c);       // single GPU: dense ids + K, one sync
 void densify_assign_and_map(fsil_context* c, const int32_t* raw_in_dense_order, int32_t k);
+int64_t* densify_exchange_begin(fsil_context* c, int64_t cap_x);
+void densify_exchange_set(fsil_context* c, const int64_t* gathered, int nranks, int64_t cap_x);
 void aggregate(fsil_context* c);           // stats_buf + checks
 void derive(fsil_context* c);              // mu32, p32, nk, bound
 void score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, double* b);

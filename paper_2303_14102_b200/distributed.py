@@ -62,15 +62,22 @@ def merge_dictionaries(labels: np.ndarray, first_rows: np.ndarray, device, group
 
 
 def run_sharded(ops: ShardOps, device, group=None) -> float:
-    """The three-exchange protocol; returns the global mean silhouette S."""
-    labels, rows = ops.begin()
-    raw = merge_dictionaries(labels, rows, device, group)
-    ops.set_dictionary(raw)
+    """The three-exchange protocol; returns the global mean silhouette S.  Ops with a
+    device dictionary exchange (CudaShardOps) gather and merge the dictionaries on the
+    GPUs; others go through the host merge."""
+    if hasattr(ops, "exchange_dictionary"):
+        ops.exchange_dictionary(group)
+    else:
+        labels, rows = ops.begin()
+        raw = merge_dictionaries(labels, rows, device, group)
+        ops.set_dictionary(raw)
     stats, checks = ops.aggregate()
     dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(checks, op=dist.ReduceOp.MIN, group=group)
+    # the validation word is only read by finish: its MIN overlaps the scoring kernels
+    pending = dist.all_reduce(checks, op=dist.ReduceOp.MIN, group=group, async_op=True)
     partial = ops.score()
     dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
+    pending.wait()
     return ops.finish()
 
 
@@ -99,6 +106,18 @@ class CudaShardOps:
         self.device = X.device
         # kernels run on torch's current stream, so NCCL orders after them
         ctx.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def exchange_dictionary(self, group=None):
+        """Device exchange: local (label, first row) pairs -> all-gather (NCCL) -> merged
+        on every GPU (fsil_shard_begin_device / fsil_shard_set_dictionary_device)."""
+        n, d = self.X.shape
+        ptr, cap = self.ctx.shard_begin_device(self.metric, self.X.data_ptr(), self.L.data_ptr(), n, d,
+                                               self.row_offset, self.n_global, f64=self.X.dtype == torch.float64)
+        local = device_view(ptr, 2 * cap, torch.int64, self.device)
+        world = dist.get_world_size(group)
+        gathered = torch.empty(world * 2 * cap, dtype=torch.int64, device=self.device)
+        dist.all_gather_into_tensor(gathered, local, group=group)
+        self.ctx.shard_set_dictionary_device(gathered.data_ptr(), world, cap)
 
     def begin(self):
         n, d = self.X.shape

@@ -278,7 +278,7 @@ def test_full_size_sampled_rows(ctx, name):
     assert np.abs(sv - s_h[rows]).max() <= S_TOL
 
 
-def _shard_loopback(X, L, metric, nshards, path=0):
+def _shard_loopback(X, L, metric, nshards, path=0, device_exchange=False):
     """The multi-GPU protocol (fsil_shard_*) with `nshards` contexts on one device and
     the three exchanges done in-process (device sums / minima), one shard after the
     other -- the device entry points and the exchange layouts under test, not NCCL."""
@@ -295,17 +295,30 @@ def _shard_loopback(X, L, metric, nshards, path=0):
     sd = [torch.empty(e - b, dtype=torch.float64, device=dev) for b, e in ranges]
     nbd = [torch.empty(e - b, dtype=torch.int32, device=dev) for b, e in ranges]
     try:
-        first = {}
-        for c, x, l, (b, e) in zip(ctxs, Xd, Ld, ranges):
-            c.set_path(path)
-            c.set_stream(torch.cuda.current_stream(dev).cuda_stream)  # ordered with the exchanges
-            nd = c.shard_begin(metric, x.data_ptr(), l.data_ptr(), e - b, d, b, n, f64=x.dtype == torch.float64)
-            labs, rows = c.shard_get_dictionary(nd)
-            for lab, row in zip(labs.tolist(), rows.tolist()):
-                first[lab] = min(row, first.get(lab, row))
-        raw = np.array([lab for lab, _ in sorted(first.items(), key=lambda kv: kv[1])], np.int32)
-        for c in ctxs:
-            c.shard_set_dictionary(raw)
+        if device_exchange:  # buffers gathered in rank order, merged on the device
+            bufs = []
+            for c, x, l, (b, e) in zip(ctxs, Xd, Ld, ranges):
+                c.set_path(path)
+                c.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+                ptr, cap = c.shard_begin_device(metric, x.data_ptr(), l.data_ptr(), e - b, d, b, n,
+                                                f64=x.dtype == torch.float64)
+                bufs.append(device_view(ptr, 2 * cap, torch.int64, dev).clone())
+            gathered = torch.cat(bufs)
+            for c in ctxs:
+                c.shard_set_dictionary_device(gathered.data_ptr(), len(ctxs), cap)
+            raw = np.array(ctxs[0].dictionary_labels() if hasattr(ctxs[0], "dictionary_labels") else [], np.int32)
+        else:
+            first = {}
+            for c, x, l, (b, e) in zip(ctxs, Xd, Ld, ranges):
+                c.set_path(path)
+                c.set_stream(torch.cuda.current_stream(dev).cuda_stream)  # ordered with the exchanges
+                nd = c.shard_begin(metric, x.data_ptr(), l.data_ptr(), e - b, d, b, n, f64=x.dtype == torch.float64)
+                labs, rows = c.shard_get_dictionary(nd)
+                for lab, row in zip(labs.tolist(), rows.tolist()):
+                    first[lab] = min(row, first.get(lab, row))
+            raw = np.array([lab for lab, _ in sorted(first.items(), key=lambda kv: kv[1])], np.int32)
+            for c in ctxs:
+                c.shard_set_dictionary(raw)
         stats, checks = [], []
         for c in ctxs:
             ps, ln, pc = c.shard_aggregate()
@@ -473,3 +486,22 @@ def test_cli_score_and_compare(tmp_path):
     assert run("score", "--input", str(csv), "--engine", "naive", "--format", "csv").returncode == 0
     assert run("compare", "--input", str(csv)).returncode == 0
     assert run("compare", "--input", str(csv), "--inject-fault", "1e-3").returncode == 3
+
+
+@pytest.mark.parametrize("nshards,metric,path", [(2, "sqeuclid", 0), (3, "cosine", 2), (4, "cosine", 0)])
+def test_shard_protocol_device_exchange(nshards, metric, path):
+    """The dictionary exchanged and merged on the device (what bench.py --gpus N uses):
+    same global first-appearance order and results as one process."""
+    rng = np.random.default_rng(nshards * 13 + path)
+    n, d = 20_000, 64
+    X = (rng.normal(size=(n, d)) + 3 * rng.normal(size=(12, d))[rng.integers(0, 12, n)]).astype(np.float32)
+    L = rng.integers(0, 12, n) * 5 - 17
+    L[n - 3:] = 999  # a cluster only the last shard holds
+    L[:2] = 4242     # and one that the first shard holds first
+    ref = oracle.silhouette(X, L, metric)
+    means, errors, s, nb, _ = _shard_loopback(X, L, metric, nshards, path, device_exchange=True)
+    assert not errors
+    for m in means:
+        assert abs(m - ref.mean) <= MEAN_TOL
+    assert np.abs(s - ref.s).max() <= S_TOL
+    assert np.array_equal(nb, ref.neighbour)
