@@ -409,7 +409,7 @@ void fsil_destroy(fsil_context* c) {
                           &c->sort_tmp, &c->sort_keys, &c->sort_vals, &c->iota, &c->seg_start,
                           &c->piece_start, &c->mu32, &c->p32, &c->nk, &c->bound, &c->s_tmp,
                           &c->tile_sum, &c->tile_flag, &c->flag_rows, &c->flag_count, &c->result,
-                          &c->group_sum, &c->xmax, &c->tc_b, &c->exact_rows, &c->exact_count, &c->a_scratch, &c->hX, &c->hL, &c->o_s, &c->o_nb, &c->o_own, &c->o_a,
+                          &c->group_sum, &c->xmax, &c->tc_b, &c->exact_rows, &c->exact_count, &c->a_scratch, &c->x32, &c->xbuf, &c->xt_keys, &c->xt_vals, &c->xt_dense, &c->hX, &c->hL, &c->o_s, &c->o_nb, &c->o_own, &c->o_a,
                           &c->o_b};
   for (auto* b : bufs) b->release();
   for (auto& e : c->ev)

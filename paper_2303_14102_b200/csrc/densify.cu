@@ -455,20 +455,33 @@ int64_t* densify_exchange_begin(fsil_context* c, int64_t cap_x) {
 void densify_exchange_set(fsil_context* c, const int64_t* gathered, int nranks, int64_t cap_x) {
   int64_t cap = 8192;
   while (cap < 2 * static_cast<int64_t>(nranks) * cap_x && cap < (int64_t(1) << 26)) cap *= 2;
-  const uint32_t epoch = prepare_table(c, cap);  // the exchange reuses the context table
+  // the global dictionary gets its own epoch-tagged table (the local one keeps its size:
+  // neither is re-zeroed from call to call)
+  if (cap != c->xt_cap || c->xt_epoch == 0xffffffffu) {
+    c->xt_keys.ensure(cap * sizeof(unsigned long long));
+    c->xt_vals.ensure(cap * sizeof(unsigned long long));
+    c->xt_dense.ensure(cap * sizeof(int32_t));
+    FSIL_CUDA(cudaMemsetAsync(c->xt_keys.p, 0, cap * sizeof(unsigned long long), c->stream));
+    FSIL_CUDA(cudaMemsetAsync(c->xt_vals.p, 0, cap * sizeof(unsigned long long), c->stream));
+    c->xt_cap = cap;
+    c->xt_epoch = 0;
+  }
+  const uint32_t epoch = ++c->xt_epoch;
+  unsigned long long* keys = c->xt_keys.as<unsigned long long>();
+  unsigned long long* vals = c->xt_vals.as<unsigned long long>();
+  int32_t* slot_dense = c->xt_dense.as<int32_t>();
   int* counters = c->counters.as<int>();
+  FSIL_CUDA(cudaMemsetAsync(counters, 0, 64, c->stream));
   const uint32_t mask = static_cast<uint32_t>(cap - 1);
   c->dict_sorted.ensure(cap * (2 * sizeof(int32_t)));
   c->dense.ensure(std::max<int64_t>(c->n, 1) * sizeof(int32_t));
   int32_t* sorted_labels = reinterpret_cast<int32_t*>(c->dict_sorted.p) + cap;
   const int64_t total = static_cast<int64_t>(nranks) * cap_x;
   densify_xinsert_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, c->stream>>>(
-      gathered, total, c->ht_keys.as<unsigned long long>(), c->ht_vals.as<unsigned long long>(), mask, epoch,
-      counters);
+      gathered, total, keys, vals, mask, epoch, counters);
   FSIL_LAUNCHED(c);
-  densify_finish_kernel<<<1, 1024, 0, c->stream>>>(c->ht_keys.as<unsigned long long>(),
-                                                   c->ht_vals.as<unsigned long long>(), static_cast<uint32_t>(cap),
-                                                   epoch, sorted_labels, c->ht_dense.as<int32_t>(), counters, c->dsum);
+  densify_finish_kernel<<<1, 1024, 0, c->stream>>>(keys, vals, static_cast<uint32_t>(cap), epoch, sorted_labels,
+                                                   slot_dense, counters, c->dsum);
   FSIL_LAUNCHED(c);
   FSIL_CUDA(cudaStreamSynchronize(c->stream));
   const volatile HostSummary* hs = c->hsum;
@@ -483,19 +496,17 @@ void densify_exchange_set(fsil_context* c, const int64_t* gathered, int nranks, 
     unsigned long long* count = reinterpret_cast<unsigned long long*>(c->counters.as<char>() + 8);
     FSIL_CUDA(cudaMemsetAsync(count, 0, sizeof(unsigned long long), c->stream));
     densify_compact_kernel<<<static_cast<unsigned>((cap + 255) / 256), 256, 0, c->stream>>>(
-        c->ht_keys.as<unsigned long long>(), c->ht_vals.as<unsigned long long>(), static_cast<uint32_t>(cap), epoch, 0,
-        c->dict_labels.as<int32_t>(), c->dict_rows.as<int64_t>(), slots, count);
+        keys, vals, static_cast<uint32_t>(cap), epoch, 0, c->dict_labels.as<int32_t>(), c->dict_rows.as<int64_t>(),
+        slots, count);
     FSIL_LAUNCHED(c);
     densify_rank_kernel<<<static_cast<unsigned>((cap + 255) / 256), 256, 0, c->stream>>>(
-        c->dict_labels.as<int32_t>(), c->dict_rows.as<int64_t>(), slots, count, sorted_labels,
-        c->ht_dense.as<int32_t>());
+        c->dict_labels.as<int32_t>(), c->dict_rows.as<int64_t>(), slots, count, sorted_labels, slot_dense);
     FSIL_LAUNCHED(c);
   }
   FSIL_CUDA(cudaMemsetAsync(counters + 4, 0, sizeof(int), c->stream));  // missing
   if (c->n > 0) {
     densify_map_kernel<<<grid_for(c->n, 256, c->num_sms, 8), 256, 0, c->stream>>>(
-        c->labels, c->n, c->ht_keys.as<unsigned long long>(), c->ht_dense.as<int32_t>(), mask, epoch,
-        c->dense.as<int32_t>(), counters + 4);
+        c->labels, c->n, keys, slot_dense, mask, epoch, c->dense.as<int32_t>(), counters + 4);
     FSIL_LAUNCHED(c);
   }
   c->ht_cap = std::max<int64_t>(c->ht_cap, 8192);

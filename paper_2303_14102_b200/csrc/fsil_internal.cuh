@@ -141,6 +141,9 @@ struct fsil_context {
   fsil::DevBuf a_scratch;                // tcgen05 streaming mode: per-CTA converted A chunks
   fsil::DevBuf x32;                      // fp64 front end: rounded fp32 copy for the fast pass
   fsil::DevBuf xbuf;                     // sharded protocol: device dictionary exchange entries
+  fsil::DevBuf xt_keys, xt_vals, xt_dense;  // ... and the global-dictionary table (own epochs)
+  int64_t xt_cap = 0;
+  uint32_t xt_epoch = 0;
   bool tc_exact_used = false;
   // host staging for fsil_silhouette (pageable -> pinned)
   fsil::DevBuf hX, hL;         // device copies of host inputs
