@@ -47,7 +47,9 @@ typedef enum {
   FSIL_ERR_INVALID_ARGUMENT = 3, /* std::invalid_argument (API misuse)                     */
   FSIL_ERR_CUDA = 4,             /* CUDA runtime / device failure                          */
   FSIL_ERR_NCCL = 5,             /* collective failure (reported by the caller's exchange) */
-  FSIL_ERR_INTERNAL = 6
+  FSIL_ERR_INTERNAL = 6,
+  FSIL_AGAIN = 7                 /* not an error: fsil_shard_finish after a device dictionary
+                                    exchange whose speculated K missed; repeat the protocol */
 } fsil_status;
 
 /* Metric (types.hpp:20-24).  FSIL_EUCLID exists only to reproduce the
@@ -185,8 +187,16 @@ fsil_status fsil_shard_finish(fsil_context* ctx, double* mean);
  *                                     every rank; xtype 0 = fp32 features, 1 = fp64
  *   [exchange: all-gather the buffers of all ranks, rank order]
  *   fsil_shard_set_dictionary_device <- the gathered nranks x capacity pairs: merged on the
- *                                     device (first appearance), one host sync for K
+ *                                     device (first appearance)
  * then fsil_shard_aggregate / _score / _finish as above.
+ *
+ * K speculation.  The kernels after the dictionary are sized by K.  Rather than wait for
+ * the merged count, set_dictionary_device launches them for the previous call's global K
+ * (identical on every rank), so the protocol's only host sync is in fsil_shard_finish.
+ * finish checks the count; if it differs, every rank returns FSIL_AGAIN and the caller
+ * repeats the protocol from fsil_shard_begin_device (the repeat waits for the count).  The
+ * single-GPU entries speculate the same way and repeat internally.  FSIL_SPECULATE=0 in the
+ * environment at fsil_create turns it off.
  */
 fsil_status fsil_shard_begin_device(fsil_context* ctx, int metric, const void* dX, int xtype,
                                     const int32_t* dlabels, int64_t n_local, int32_t d,

@@ -30,7 +30,7 @@ PATH_AUTO, PATH_FFMA, PATH_TCGEN05, PATH_FP64 = 0, 1, 2, 3
 _METRIC_TAGS = {SQEUCLID: "squared_euclidean", COSINE: "cosine", EUCLID: "euclidean_oracle"}
 
 # FSIL status codes (include/fsil.h)
-OK, ERR_IO, ERR_VALIDATION, ERR_INVALID_ARGUMENT, ERR_CUDA, ERR_NCCL, ERR_INTERNAL = range(7)
+OK, ERR_IO, ERR_VALIDATION, ERR_INVALID_ARGUMENT, ERR_CUDA, ERR_NCCL, ERR_INTERNAL, AGAIN = range(8)
 
 # fsil.h entry points: name -> (restype, argtypes)
 _P = ctypes.c_void_p
@@ -88,6 +88,11 @@ class FsilError(RuntimeError):
         self.status = status
 
 
+class ShardAgain(FsilError):
+    """FSIL_AGAIN from fsil_shard_finish: the speculated global K missed (every rank sees
+    it); the protocol is repeated from fsil_shard_begin_device."""
+
+
 class fsil_stats(ctypes.Structure):
     _fields_ = [("n", _I64), ("d", _I32), ("k", _I32), ("path", _I32), ("agg_path", _I32),
                 ("flagged_rows", _I64), ("exact_rows", _I64), ("kernel_launches", _I64), ("ms_densify", ctypes.c_float),
@@ -121,6 +126,8 @@ def _raise(status: int, msg: str):
         raise IoError(msg)
     if status == ERR_INVALID_ARGUMENT:
         raise ValueError(msg)
+    if status == AGAIN:
+        raise ShardAgain(status, msg)
     raise FsilError(status, msg)
 
 

@@ -6,6 +6,7 @@
 //   K0 densify (densify.cu) -> K1 aggregate (aggregate.cu) -> derive ->
 //   K2 score_ffma | K3 score_tc -> K4 refine -> K5 tile-group sum (finalize.cu)
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -86,6 +87,8 @@ void setup(fsil_context* c, int metric, const void* dX, bool x64, const int32_t*
   c->d = d;
   c->dp = (static_cast<int64_t>(d) + 3) / 4 * 4;
   c->k = 0;
+  c->k_spec = false;
+  c->spec_missed = false;
   c->stats = fsil_stats{};
   record(c, 0);
 }
@@ -135,6 +138,7 @@ ScoreParams make_params(fsil_context* c, double* s, int32_t* nb, int32_t* own, d
   p.stats = c->stats_buf.as<double>();
   p.nk = c->nk.as<double>();
   p.bound = c->bound.as<float>();
+  p.abort = c->counters.as<int>() + kAbortWord;
   if (!s) {
     c->s_tmp.ensure(std::max<int64_t>(c->n, 1) * sizeof(double));
     s = c->s_tmp.as<double>();
@@ -249,6 +253,19 @@ double finish(fsil_context* c, double* flagged_out) {
   record(c, 6);
   FSIL_CUDA(cudaStreamSynchronize(c->stream));
   const volatile HostSummary* hs = c->hsum;
+  if (c->k_spec) {  // the dictionary's count, written by the densify kernels, against the speculated K
+    c->k_spec = false;
+    const bool over = hs->overflow != 0;
+    if (over && !c->local_call)
+      fail(FSIL_ERR_INVALID_ARGUMENT, "device dictionary exchange: more distinct labels than its capacity (" +
+                                          std::to_string(c->spec_cap_x - 1) + " per rank); use the host exchange");
+    if (over || hs->count != c->k || (hs->pad && !c->spec_big)) {
+      c->spec_missed = true;  // redo the call with the host waiting for the count
+      c->spec_block_once = true;
+      if (!over) (c->local_call ? c->k_last : c->k_global_last) = hs->count;
+      return 0.0;
+    }
+  }
   const int64_t checks[2] = {hs->checks[0], hs->checks[1]};
   const double res[3] = {hs->result[0], hs->result[1], hs->result[2]};
   const int missing = static_cast<int>(hs->missing);
@@ -315,19 +332,31 @@ double run_device(fsil_context* c, int metric, const void* dX, bool x64, const i
                   int32_t d, double* ds, int32_t* dnb, int32_t* down, double* da, double* db,
                   int32_t* k_out, int32_t* dense_to_raw) {
   c->launches = 0;
-  setup(c, metric, dX, x64, dlabels, n, d, 0, n);
-  c->local_call = true;
-  densify_local(c);  // dictionary ordered on the device; one host sync for K
-  record(c, 1);
-  c->phase = 2;
-  do_aggregate(c);
-  do_score(c, ds, dnb, down, da, db);
-  if (dense_to_raw && c->k > 0)
-    FSIL_CUDA(cudaMemcpyAsync(dense_to_raw, c->dict_sorted_labels, c->k * sizeof(int32_t),
-                              cudaMemcpyDeviceToHost, c->stream));
-  const double mean = finish(c, nullptr);
-  if (k_out) *k_out = c->k;
-  return mean;
+  for (;;) {
+    setup(c, metric, dX, x64, dlabels, n, d, 0, n);
+    c->local_call = true;
+    densify_local(c);  // dictionary ordered on the device (K speculated from the last call)
+    record(c, 1);
+    c->phase = 2;
+    do_aggregate(c);
+    do_score(c, ds, dnb, down, da, db);
+    if (dense_to_raw && c->k > 0) {  // staged: the caller's buffer holds the true K only
+      if (c->k > c->d2r_cap) {
+        if (c->d2r_host) FSIL_CUDA(cudaFreeHost(c->d2r_host));
+        c->d2r_host = nullptr;
+        c->d2r_cap = 0;
+        FSIL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->d2r_host), c->k * sizeof(int32_t), cudaHostAllocDefault));
+        c->d2r_cap = c->k;
+      }
+      FSIL_CUDA(cudaMemcpyAsync(c->d2r_host, c->dict_sorted_labels, c->k * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                c->stream));
+    }
+    const double mean = finish(c, nullptr);  // the call's one host sync
+    if (c->spec_missed) continue;            // K changed since the last call: once more, unspeculated
+    if (dense_to_raw && c->k > 0) std::memcpy(dense_to_raw, c->d2r_host, c->k * sizeof(int32_t));
+    if (k_out) *k_out = c->k;
+    return mean;
+  }
 }
 
 template <typename F>
@@ -381,6 +410,8 @@ fsil_status fsil_create(fsil_context** out, int device) {
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
     c->smem_optin = prop.sharedMemPerBlockOptin;
+    if (const char* e = std::getenv("FSIL_SPECULATE")) c->speculate = std::string(e) != "0";
+    if (const char* e = std::getenv("FSIL_DEBUG_SYNC")) c->debug_sync = std::string(e) == "1";
     FSIL_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
     for (auto& e : c->ev) FSIL_CUDA(cudaEventCreate(&e));
@@ -416,6 +447,7 @@ void fsil_destroy(fsil_context* c) {
     if (e) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   if (c->hsum) cudaFreeHost(c->hsum);
+  if (c->d2r_host) cudaFreeHost(c->d2r_host);
   delete c;
 }
 
@@ -634,6 +666,9 @@ fsil_status fsil_shard_finish(fsil_context* c, double* mean) {
   if (!c) return FSIL_ERR_INVALID_ARGUMENT;
   return guarded(c, [&] {
     const double m = finish(c, nullptr);
+    if (c->spec_missed)
+      fail(FSIL_AGAIN, "the global number of clusters changed since the previous call: repeat the protocol "
+                       "from fsil_shard_begin_device");
     if (mean) *mean = m;
   });
 }

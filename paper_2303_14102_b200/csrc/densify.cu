@@ -137,7 +137,8 @@ __global__ void __launch_bounds__(256) densify_collect_kernel(const int32_t* __r
 __global__ void __launch_bounds__(1024) densify_finish_kernel(const unsigned long long* __restrict__ keys,
                                                               const unsigned long long* __restrict__ vals,
                                                               uint32_t cap, uint32_t epoch, int32_t* sorted_labels,
-                                                              int32_t* slot_dense, int* counters, HostSummary* hsum) {
+                                                              int32_t* slot_dense, int* counters, HostSummary* hsum,
+                                                              int32_t k_spec = 0, bool spec_big = false) {
   __shared__ int32_t s_lab[kSmallK];
   __shared__ uint32_t s_row[kSmallK];
   __shared__ uint32_t s_slot[kSmallK];
@@ -167,6 +168,8 @@ __global__ void __launch_bounds__(1024) densify_finish_kernel(const unsigned lon
   }
   if (threadIdx.x == 0) {
     counters[1] = cnt > kSmallK ? 1 : 0;  // needs the multi-block ordering
+    // speculated K (k_spec > 0): raise the miss flag the scoring kernels check at entry
+    if (k_spec > 0 && (cnt != k_spec || counters[0] != 0 || (cnt > kSmallK && !spec_big))) counters[kAbortWord] = 1;
     *reinterpret_cast<unsigned long long*>(counters + 2) = static_cast<unsigned long long>(cnt);
     if (hsum) {
       hsum->overflow = counters[0];
@@ -180,12 +183,19 @@ __global__ void __launch_bounds__(1024) densify_finish_kernel(const unsigned lon
 __global__ void __launch_bounds__(256) densify_map_kernel(const int32_t* __restrict__ labels, int64_t n,
                                                           const unsigned long long* __restrict__ gkeys,
                                                           const int32_t* __restrict__ slot_dense, uint32_t mask,
-                                                          uint32_t epoch, int32_t* dense, int* missing) {
+                                                          uint32_t epoch, int32_t k_lim, int32_t* dense,
+                                                          int* missing) {
+  // k_lim: the K the following kernels are launched for (the speculated K, or INT_MAX when
+  // the host waits for the count).  An id outside [0, k_lim) -- only possible when the
+  // speculation misses -- is stored as 0 and flagged, so every later kernel stays in bounds.
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int64_t slot = find_slot(gkeys, mask, epoch, __ldg(labels + i));
-    const int32_t dj = slot >= 0 ? slot_dense[slot] : -1;
-    if (dj < 0) atomicExch(missing, 1);
+    int32_t dj = slot >= 0 ? slot_dense[slot] : -1;
+    if (dj < 0 || dj >= k_lim) {
+      atomicExch(missing, 1);
+      dj = 0;
+    }
     dense[i] = dj;
   }
 }
@@ -350,6 +360,11 @@ void densify_local(fsil_context* c) {
     fail(FSIL_ERR_INVALID_ARGUMENT, "too many rows for one device call (2^31-2)");
   int64_t cap = std::max<int64_t>(c->ht_cap, 8192);
   bool big = c->k_last > kSmallK;  // the previous call's K predicts the ordering path
+  // Speculation: launch everything after the dictionary for the previous call's K instead
+  // of waiting for this call's count; finish() checks the count (one host sync per call)
+  // and the call is redone without speculation when it differs.
+  const bool spec = c->speculate && !c->spec_block_once && c->k_last >= 2;
+  c->spec_block_once = false;
   for (;;) {
     const uint32_t epoch = prepare_table(c, cap);
     c->dict_sorted.ensure(cap * (2 * sizeof(int32_t)));
@@ -361,7 +376,7 @@ void densify_local(fsil_context* c) {
     densify_finish_kernel<<<1, 1024, 0, c->stream>>>(c->ht_keys.as<unsigned long long>(),
                                                      c->ht_vals.as<unsigned long long>(), static_cast<uint32_t>(cap),
                                                      epoch, sorted_labels, c->ht_dense.as<int32_t>(), counters,
-                                                     c->dsum);
+                                                     c->dsum, spec ? static_cast<int32_t>(c->k_last) : 0, big);
     FSIL_LAUNCHED(c);
     if (big) {
       c->dict_labels.ensure(cap * sizeof(int32_t));
@@ -381,10 +396,18 @@ void densify_local(fsil_context* c) {
     if (c->n > 0) {
       densify_map_kernel<<<grid_for(c->n, 256, c->num_sms, 8), 256, 0, c->stream>>>(
           c->labels, c->n, c->ht_keys.as<unsigned long long>(), c->ht_dense.as<int32_t>(), mask, epoch,
-          c->dense.as<int32_t>(), counters + 4);
+          spec ? static_cast<int32_t>(c->k_last) : INT32_MAX, c->dense.as<int32_t>(), counters + 4);
       FSIL_LAUNCHED(c);
     }
-    FSIL_CUDA(cudaStreamSynchronize(c->stream));  // the one host sync: K decides the kernels
+    if (spec) {
+      c->k_spec = true;
+      c->spec_big = big;
+      c->n_distinct = c->k_last;
+      c->k = static_cast<int32_t>(c->k_last);
+      c->dict_sorted_labels = sorted_labels;
+      return;
+    }
+    FSIL_CUDA(cudaStreamSynchronize(c->stream));  // K decides the kernels
     const volatile HostSummary* hs = c->hsum;
     const int64_t over = hs->overflow, cnt = hs->count;
     const bool needs_big = hs->pad != 0;
@@ -422,7 +445,7 @@ void densify_assign_and_map(fsil_context* c, const int32_t* raw_in_dense_order, 
   if (c->n > 0) {
     densify_map_kernel<<<grid_for(c->n, 256, c->num_sms, 8), 256, 0, c->stream>>>(
         c->labels, c->n, c->ht_keys.as<unsigned long long>(), c->ht_dense.as<int32_t>(),
-        static_cast<uint32_t>(cap - 1), epoch, c->dense.as<int32_t>(), c->counters.as<int>() + 4);
+        static_cast<uint32_t>(cap - 1), epoch, k, c->dense.as<int32_t>(), c->counters.as<int>() + 4);
     FSIL_LAUNCHED(c);
   }
   // `missing` is checked by the caller at the end of the call (no extra sync here).
@@ -480,16 +503,29 @@ void densify_exchange_set(fsil_context* c, const int64_t* gathered, int nranks, 
   densify_xinsert_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, c->stream>>>(
       gathered, total, keys, vals, mask, epoch, counters);
   FSIL_LAUNCHED(c);
+  // Speculation (as in densify_local): every rank holds the same previous global K, so all
+  // speculate alike and all see the same miss at finish (FSIL_AGAIN: repeat the protocol).
+  const bool spec = c->speculate && !c->spec_block_once && c->k_global_last >= 2;
+  c->spec_block_once = false;
+  int64_t cnt = c->k_global_last;
+  bool big = c->k_global_last > kSmallK;
   densify_finish_kernel<<<1, 1024, 0, c->stream>>>(keys, vals, static_cast<uint32_t>(cap), epoch, sorted_labels,
-                                                   slot_dense, counters, c->dsum);
+                                                   slot_dense, counters, c->dsum,
+                                                   spec ? static_cast<int32_t>(c->k_global_last) : 0, big);
   FSIL_LAUNCHED(c);
-  FSIL_CUDA(cudaStreamSynchronize(c->stream));
-  const volatile HostSummary* hs = c->hsum;
-  if (hs->overflow)
-    fail(FSIL_ERR_INVALID_ARGUMENT, "device dictionary exchange: more distinct labels than its capacity (" +
-                                        std::to_string(cap_x - 1) + " per rank); use the host exchange");
-  const int64_t cnt = hs->count;
-  if (hs->pad) {  // more labels than the one-block ordering holds: multi-block
+  if (!spec) {
+    FSIL_CUDA(cudaStreamSynchronize(c->stream));
+    const volatile HostSummary* hs = c->hsum;
+    if (hs->overflow)
+      fail(FSIL_ERR_INVALID_ARGUMENT, "device dictionary exchange: more distinct labels than its capacity (" +
+                                          std::to_string(cap_x - 1) + " per rank); use the host exchange");
+    cnt = hs->count;
+    big = hs->pad != 0;
+  }
+  c->k_spec = spec;
+  c->spec_big = big;
+  c->spec_cap_x = cap_x;
+  if (big) {  // more labels than the one-block ordering holds: multi-block
     c->dict_labels.ensure(cap * sizeof(int32_t));
     c->dict_rows.ensure(cap * sizeof(int64_t));
     int32_t* slots = reinterpret_cast<int32_t*>(c->dict_sorted.p);
@@ -506,7 +542,8 @@ void densify_exchange_set(fsil_context* c, const int64_t* gathered, int nranks, 
   FSIL_CUDA(cudaMemsetAsync(counters + 4, 0, sizeof(int), c->stream));  // missing
   if (c->n > 0) {
     densify_map_kernel<<<grid_for(c->n, 256, c->num_sms, 8), 256, 0, c->stream>>>(
-        c->labels, c->n, keys, slot_dense, mask, epoch, c->dense.as<int32_t>(), counters + 4);
+        c->labels, c->n, keys, slot_dense, mask, epoch, spec ? static_cast<int32_t>(c->k_global_last) : INT32_MAX,
+        c->dense.as<int32_t>(), counters + 4);
     FSIL_LAUNCHED(c);
   }
   c->ht_cap = std::max<int64_t>(c->ht_cap, 8192);

@@ -23,6 +23,7 @@ namespace {
 // argmin (strict <); the warp merge breaks ties towards the lowest k.
 template <bool COS>
 __global__ void __launch_bounds__(256) refine_kernel(ScoreParams p) {
+  if (*p.abort) return;
   extern __shared__ double xs_all[];  // [warps per block][d]
   const unsigned long long count = *p.flag_count;
   const int lane = threadIdx.x & 31;
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(256) refine_kernel(ScoreParams p) {
 constexpr int kRT = 32, kCT = 64, kDC = 32;
 template <bool COS>
 __global__ void __launch_bounds__(256) refine_tiled_kernel(ScoreParams p) {
+  if (*p.abort) return;
   __shared__ double xs[kRT][kDC + 1];
   __shared__ double ys[kCT][kDC + 1];
   __shared__ double s_ss[kRT], s_co[kRT], s_best[kRT][17];
@@ -344,6 +346,7 @@ __global__ void flag_all_kernel(int64_t n, int tile_rows, int32_t* flag_rows, in
 template <bool COS, int LPR>
 __global__ void __launch_bounds__(256) exact_ab_kernel(ScoreParams p, const int2* __restrict__ rows,
                                                        const unsigned long long* count) {
+  if (*p.abort) return;
   const int64_t cnt = static_cast<int64_t>(*count);
   const int lane = threadIdx.x & 31, sub = lane / LPR, li = lane % LPR;
   constexpr int RPW = 32 / LPR;

@@ -31,9 +31,18 @@ struct Error : std::runtime_error {
     if (e__ != cudaSuccess)                                                                \
       ::fsil::fail(FSIL_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e__)); \
     ++(ctx)->launches;                                                                     \
+    if ((ctx)->debug_sync) {  /* FSIL_DEBUG_SYNC=1: name the kernel that faults */           \
+      e__ = cudaStreamSynchronize((ctx)->stream);                                            \
+      if (e__ != cudaSuccess)                                                                \
+        ::fsil::fail(FSIL_ERR_CUDA, std::string("kernel at " __FILE__ ":") +                 \
+                                        std::to_string(__LINE__) + ": " + cudaGetErrorString(e__)); \
+    }                                                                                        \
   } while (0)
 
-constexpr int kNumSMs = 148;  // B200; the context re-reads the real count
+constexpr int kNumSMs = 148;
+// int index in the context's 64-byte counters block (zeroed by every dictionary pass) of
+// the K-speculation miss flag the densify kernels raise for the scoring kernels
+constexpr int kAbortWord = 10;  // B200; the context re-reads the real count
 
 // ---- grow-only device scratch -----------------------------------------------------------
 struct DevBuf {
@@ -143,6 +152,17 @@ struct fsil_context {
   fsil::DevBuf xbuf;                     // sharded protocol: device dictionary exchange entries
   fsil::DevBuf xt_keys, xt_vals, xt_dense;  // ... and the global-dictionary table (own epochs)
   int64_t xt_cap = 0;
+  // K speculation (densify_local / densify_exchange_set): kernels launched for the previous
+  // call's K, checked by finish() against this call's count.
+  bool speculate = true;   // FSIL_SPECULATE=0 disables
+  bool debug_sync = false;  // FSIL_DEBUG_SYNC=1: synchronise and check after every launch
+  bool k_spec = false;     // this call speculated
+  bool spec_big = false;   // ... with the multi-block ordering launched
+  bool spec_missed = false;
+  bool spec_block_once = false;  // the retry after a miss waits for the count
+  int32_t* d2r_host = nullptr;    // pinned staging of dense_to_raw (copied out once K is confirmed)
+  int64_t d2r_cap = 0;
+  int64_t spec_cap_x = 0;
   uint32_t xt_epoch = 0;
   bool tc_exact_used = false;
   // host staging for fsil_silhouette (pageable -> pinned)

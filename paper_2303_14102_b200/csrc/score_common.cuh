@@ -34,6 +34,8 @@ struct ScoreParams {
   int32_t* tile_flag;     // [ntiles]
   int32_t* flag_rows;     // [n]
   unsigned long long* flag_count;
+  const int* abort;       // set on the device when this call's K speculation missed: the
+                          // scoring kernels return at entry (their inputs are not a dataset's)
 };
 
 // Feature element idx (row * d + l) as the exact-path kernels see it: the caller's

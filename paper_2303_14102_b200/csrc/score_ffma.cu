@@ -65,6 +65,7 @@ __device__ __forceinline__ void load_tile(const ScoreParams& p, float* xs, int64
 
 template <int KB, bool COS, int VEC, bool MULTI>
 __global__ void __launch_bounds__(kThreads) score_ffma_kernel(ScoreParams p, int64_t ntiles) {
+  if (*p.abort) return;  // K speculation missed: the call is repeated
   extern __shared__ __align__(16) float smem[];
   // single-group case: Yt2[dp/2][KB] pairs {Y[k][l], Y[k][l+1]} (fp64) so that the
   // per-lane own/neighbour gathers of the fp64 epilogue all hit one smem row

@@ -105,6 +105,7 @@ template <int BN, bool COS>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
                     const __grid_constant__ CUtensorMap tmap_bl, TcParams tp, int64_t ntiles) {
+  if (*tp.p.abort) return;  // K speculation missed: the call is repeated
   using C = TcCfg<BN>;
   constexpr int NB = C::kBStg;
   // X stages: a TMA-filled fp32 box pair that the converters overwrite in place with
@@ -635,7 +636,8 @@ __device__ __forceinline__ int scale_exp(float m) { return m > 0.f ? ilogbf(m) -
 __global__ void prep_b_kernel(const double* __restrict__ stats, const float* __restrict__ bound,
                               const float* __restrict__ xmax, int k, int d, int kp, int dp, bool cos,
                               __half* bh, __half* bl, float* colbias, __half* munorm, double4* clu,
-                              TcScale* scale) {
+                              TcScale* scale, const int* abort) {
+  if (*abort) return;
   const int c = blockIdx.x;
   const int em = scale_exp(bound[2]);
   const float smu = ldexpf(1.0f, -em);
@@ -773,7 +775,7 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   double4* clu = reinterpret_cast<double4*>((reinterpret_cast<uintptr_t>(munorm + kp) + 31) & ~uintptr_t(31));
   TcScale* scale = reinterpret_cast<TcScale*>(clu + kp);
   prep_b_kernel<<<kp, 128, 0, c->stream>>>(p.stats, c->bound.as<float>(), c->xmax.as<float>(), c->k, c->d, kp,
-                                           dp, cos, bh, bl, colbias, munorm, clu, scale);
+                                           dp, cos, bh, bl, colbias, munorm, clu, scale, p.abort);
   FSIL_LAUNCHED(c);
   const CUtensorMap mx = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, c->X, c->d, c->n, c->d * 4ull, 32, BM);
   const CUtensorMap mh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, bh, dp, kp, dp * 2ull, BK, bn);

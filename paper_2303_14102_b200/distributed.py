@@ -65,20 +65,26 @@ def run_sharded(ops: ShardOps, device, group=None) -> float:
     """The three-exchange protocol; returns the global mean silhouette S.  Ops with a
     device dictionary exchange (CudaShardOps) gather and merge the dictionaries on the
     GPUs; others go through the host merge."""
-    if hasattr(ops, "exchange_dictionary"):
-        ops.exchange_dictionary(group)
-    else:
-        labels, rows = ops.begin()
-        raw = merge_dictionaries(labels, rows, device, group)
-        ops.set_dictionary(raw)
-    stats, checks = ops.aggregate()
-    dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
-    # the validation word is only read by finish: its MIN overlaps the scoring kernels
-    pending = dist.all_reduce(checks, op=dist.ReduceOp.MIN, group=group, async_op=True)
-    partial = ops.score()
-    dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
-    pending.wait()
-    return ops.finish()
+    from .api import ShardAgain
+    for _ in range(3):
+        if hasattr(ops, "exchange_dictionary"):
+            ops.exchange_dictionary(group)
+        else:
+            labels, rows = ops.begin()
+            raw = merge_dictionaries(labels, rows, device, group)
+            ops.set_dictionary(raw)
+        stats, checks = ops.aggregate()
+        dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
+        # the validation word is only read by finish: its MIN overlaps the scoring kernels
+        pending = dist.all_reduce(checks, op=dist.ReduceOp.MIN, group=group, async_op=True)
+        partial = ops.score()
+        dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
+        pending.wait()
+        try:
+            return ops.finish()
+        except ShardAgain:  # K speculation missed on every rank alike: once more, unspeculated
+            continue
+    raise RuntimeError("sharded protocol: K speculation missed repeatedly")
 
 
 class _DeviceArray:

@@ -278,23 +278,31 @@ def test_full_size_sampled_rows(ctx, name):
     assert np.abs(sv - s_h[rows]).max() <= S_TOL
 
 
-def _shard_loopback(X, L, metric, nshards, path=0, device_exchange=False):
+def _shard_loopback(X, L, metric, nshards, path=0, device_exchange=False, ctxs=None, attempts=None):
     """The multi-GPU protocol (fsil_shard_*) with `nshards` contexts on one device and
     the three exchanges done in-process (device sums / minima), one shard after the
-    other -- the device entry points and the exchange layouts under test, not NCCL."""
+    other -- the device entry points and the exchange layouts under test, not NCCL.
+    `ctxs` reuses contexts across calls (K speculation); a finish that returns FSIL_AGAIN
+    on every shard repeats the protocol, as run_sharded does; `attempts` collects how many
+    rounds each call took."""
     import torch
     from paper_2303_14102_b200 import Context, ValidationError, plan_shards
+    from paper_2303_14102_b200.api import ShardAgain
     from paper_2303_14102_b200.distributed import device_view
 
     n, d = X.shape
     ranges = plan_shards(n, nshards)
-    ctxs = [Context(0) for _ in ranges]
+    own = ctxs is None
+    if own:
+        ctxs = [Context(0) for _ in ranges]
+    assert len(ctxs) == len(ranges)
     dev = torch.device("cuda", 0)
     Xd = [torch.from_numpy(X[b:e]).to(dev) for b, e in ranges]
     Ld = [torch.from_numpy(np.asarray(L[b:e], np.int32)).to(dev) for b, e in ranges]
     sd = [torch.empty(e - b, dtype=torch.float64, device=dev) for b, e in ranges]
     nbd = [torch.empty(e - b, dtype=torch.int32, device=dev) for b, e in ranges]
-    try:
+
+    def one_round():
         if device_exchange:  # buffers gathered in rank order, merged on the device
             bufs = []
             for c, x, l, (b, e) in zip(ctxs, Xd, Ld, ranges):
@@ -306,7 +314,7 @@ def _shard_loopback(X, L, metric, nshards, path=0, device_exchange=False):
             gathered = torch.cat(bufs)
             for c in ctxs:
                 c.shard_set_dictionary_device(gathered.data_ptr(), len(ctxs), cap)
-            raw = np.array(ctxs[0].dictionary_labels() if hasattr(ctxs[0], "dictionary_labels") else [], np.int32)
+            raw = np.array([], np.int32)
         else:
             first = {}
             for c, x, l, (b, e) in zip(ctxs, Xd, Ld, ranges):
@@ -336,18 +344,33 @@ def _shard_loopback(X, L, metric, nshards, path=0, device_exchange=False):
         for pp in parts:
             pp.copy_(ptot)
         torch.cuda.synchronize()
-        means, errors = [], []
+        means, errors, again = [], [], 0
         for c in ctxs:
             try:
                 means.append(c.shard_finish())
             except ValidationError as e:
                 errors.append(str(e))
+            except ShardAgain:
+                again += 1
+        assert again in (0, len(ctxs)), "FSIL_AGAIN must be seen by every shard alike"
+        return (means, errors, raw) if again == 0 else None
+
+    try:
+        for k in range(1, 4):
+            r = one_round()
+            if r is not None:
+                break
+        assert r is not None, "K speculation missed repeatedly"
+        if attempts is not None:
+            attempts.append(k)
+        means, errors, raw = r
         s = torch.cat(sd).cpu().numpy()
         nb = torch.cat(nbd).cpu().numpy()
         return means, errors, s, nb, raw
     finally:
-        for c in ctxs:
-            c.close()
+        if own:
+            for c in ctxs:
+                c.close()
 
 
 @pytest.mark.parametrize("nshards,metric,path", [(2, "sqeuclid", 0), (3, "cosine", 0), (2, "cosine", 2),
@@ -505,3 +528,51 @@ def test_shard_protocol_device_exchange(nshards, metric, path):
         assert abs(m - ref.mean) <= MEAN_TOL
     assert np.abs(s - ref.s).max() <= S_TOL
     assert np.array_equal(nb, ref.neighbour)
+
+
+def test_k_speculation_sequence():
+    """One context, K changing from call to call: each call's kernels are launched for the
+    previous call's K and checked at the end (a miss repeats the call unspeculated).  Hits,
+    misses up and down, the multi-block ordering in both directions and K = 1 all give the
+    oracle's answer."""
+    from paper_2303_14102_b200 import Context, ValidationError
+    c = Context(0)
+    try:
+        rng = np.random.default_rng(21)
+        for n, d, k in [(4000, 16, 6), (4000, 16, 6), (5000, 24, 9), (3000, 8, 3), (3000, 8, 3),
+                        (6000, 12, 3000), (6000, 12, 3000), (2000, 12, 40), (2000, 8, 2)]:
+            X = (rng.normal(size=(n, d)) + rng.normal(size=(1, d)) * 2).astype(np.float32)
+            L = rng.permutation(np.arange(n) % k) * 3 + 1
+            for metric in ("sqeuclid", "cosine"):
+                check(c, X, L, metric, label=f"spec k={k}")
+        X = rng.normal(size=(500, 4)).astype(np.float32)
+        with pytest.raises(ValidationError, match="single cluster"):
+            c.silhouette(X, np.full(500, 7), "sqeuclid")
+        check(c, X, np.arange(500) % 5, "sqeuclid", label="after K=1")
+    finally:
+        c.close()
+
+
+def test_shard_k_speculation_again():
+    """Sharded device exchange with contexts reused: the first call waits for the count,
+    a call with a new K misses on every shard alike (FSIL_AGAIN) and is repeated, a call
+    with the same K is served by the speculation."""
+    from paper_2303_14102_b200 import Context
+    ctxs = [Context(0) for _ in range(3)]
+    try:
+        rng = np.random.default_rng(5)
+        n, d = 9000, 32
+        attempts = []
+        for k in (7, 11, 11, 4):
+            X = (rng.normal(size=(n, d)) + 2 * rng.normal(size=(k, d))[rng.integers(0, k, n)]).astype(np.float32)
+            L = rng.permutation(np.arange(n) % k) * 5 - 2
+            ref = oracle.silhouette(X, L, "cosine")
+            means, errors, s, nb, _ = _shard_loopback(X, L, "cosine", 3, 0, device_exchange=True, ctxs=ctxs,
+                                                      attempts=attempts)
+            assert not errors
+            assert all(abs(m - ref.mean) <= MEAN_TOL for m in means)
+            assert np.abs(s - ref.s).max() <= S_TOL and np.array_equal(nb, ref.neighbour)
+        assert attempts == [1, 2, 1, 2], attempts
+    finally:
+        for c in ctxs:
+            c.close()
