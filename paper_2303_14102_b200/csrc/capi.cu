@@ -256,13 +256,11 @@ double finish(fsil_context* c, double* flagged_out) {
   if (c->k_spec) {  // the dictionary's count, written by the densify kernels, against the speculated K
     c->k_spec = false;
     const bool over = hs->overflow != 0;
-    if (over && !c->local_call)
-      fail(FSIL_ERR_INVALID_ARGUMENT, "device dictionary exchange: more distinct labels than its capacity (" +
-                                          std::to_string(c->spec_cap_x - 1) + " per rank); use the host exchange");
     if (over || hs->count != c->k || (hs->pad && !c->spec_big)) {
       c->spec_missed = true;  // redo the call with the host waiting for the count
       c->spec_block_once = true;
       if (!over) (c->local_call ? c->k_last : c->k_global_last) = hs->count;
+      else if (!c->local_call) exchange_grow(c, c->spec_cap_x);  // a rank's dictionary outgrew the exchange
       return 0.0;
     }
   }
@@ -602,7 +600,7 @@ fsil_status fsil_shard_begin_device(fsil_context* c, int metric, const void* dX,
     setup(c, metric, dX, xtype == 1, dlabels, n_local, d, row_offset, n_global);
     c->local_call = false;
     // the same capacity on every rank: from the previous call's global K (identical everywhere)
-    int64_t cap_x = 8192;
+    int64_t cap_x = 64;
     while (cap_x < 2 * c->k_global_last + 2) cap_x *= 2;
     int64_t* buf = densify_exchange_begin(c, cap_x);
     c->phase = 1;

@@ -473,11 +473,18 @@ int64_t* densify_exchange_begin(fsil_context* c, int64_t cap_x) {
   return c->xbuf.as<int64_t>();
 }
 
+// After an exchange overflow: the repeat gets a larger exchange buffer and local table.
+void exchange_grow(fsil_context* c, int64_t cap_x) {
+  c->k_global_last = std::max<int64_t>(c->k_global_last, cap_x) * 4;
+  c->ht_cap = std::max<int64_t>(c->ht_cap, 8192) * 4;
+  c->spec_block_once = true;
+}
+
 // Pass 2: merge the gathered buffers of `nranks` ranks into the global dictionary
 // (first-appearance order), dense ids for this rank's rows; one host sync for K.
 void densify_exchange_set(fsil_context* c, const int64_t* gathered, int nranks, int64_t cap_x) {
-  int64_t cap = 8192;
-  while (cap < 2 * static_cast<int64_t>(nranks) * cap_x && cap < (int64_t(1) << 26)) cap *= 2;
+  int64_t cap = 1024;
+  while (cap < 2 * static_cast<int64_t>(nranks) * cap_x && cap < (int64_t(1) << 28)) cap *= 2;
   // the global dictionary gets its own epoch-tagged table (the local one keeps its size:
   // neither is re-zeroed from call to call)
   if (cap != c->xt_cap || c->xt_epoch == 0xffffffffu) {
@@ -516,9 +523,11 @@ void densify_exchange_set(fsil_context* c, const int64_t* gathered, int nranks, 
   if (!spec) {
     FSIL_CUDA(cudaStreamSynchronize(c->stream));
     const volatile HostSummary* hs = c->hsum;
-    if (hs->overflow)
-      fail(FSIL_ERR_INVALID_ARGUMENT, "device dictionary exchange: more distinct labels than its capacity (" +
-                                          std::to_string(cap_x - 1) + " per rank); use the host exchange");
+    if (hs->overflow) {  // some rank's dictionary outgrew the exchange: every rank sees it
+      exchange_grow(c, cap_x);
+      fail(FSIL_AGAIN, "device dictionary exchange: more distinct labels than its capacity (" +
+                           std::to_string(cap_x - 1) + " per rank); repeat with a larger one");
+    }
     cnt = hs->count;
     big = hs->pad != 0;
   }

@@ -189,6 +189,7 @@ void densify_local(fsil_context* c);       // single GPU: dense ids + K, one syn
 void densify_assign_and_map(fsil_context* c, const int32_t* raw_in_dense_order, int32_t k);
 int64_t* densify_exchange_begin(fsil_context* c, int64_t cap_x);
 void densify_exchange_set(fsil_context* c, const int64_t* gathered, int nranks, int64_t cap_x);
+void exchange_grow(fsil_context* c, int64_t cap_x);
 void aggregate(fsil_context* c);           // stats_buf + checks
 void derive(fsil_context* c);              // mu32, p32, nk, bound
 void score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, double* b);

@@ -66,25 +66,31 @@ def run_sharded(ops: ShardOps, device, group=None) -> float:
     device dictionary exchange (CudaShardOps) gather and merge the dictionaries on the
     GPUs; others go through the host merge."""
     from .api import ShardAgain
-    for _ in range(3):
-        if hasattr(ops, "exchange_dictionary"):
-            ops.exchange_dictionary(group)
-        else:
-            labels, rows = ops.begin()
-            raw = merge_dictionaries(labels, rows, device, group)
-            ops.set_dictionary(raw)
-        stats, checks = ops.aggregate()
-        dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
-        # the validation word is only read by finish: its MIN overlaps the scoring kernels
-        pending = dist.all_reduce(checks, op=dist.ReduceOp.MIN, group=group, async_op=True)
-        partial = ops.score()
-        dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
-        pending.wait()
+    for _ in range(8):
         try:
-            return ops.finish()
-        except ShardAgain:  # K speculation missed on every rank alike: once more, unspeculated
+            return _sharded_round(ops, device, group)
+        except ShardAgain:
+            # every rank alike: the speculated K missed (raised by finish) or a dictionary
+            # outgrew the device exchange (raised by the dictionary step): repeat
             continue
-    raise RuntimeError("sharded protocol: K speculation missed repeatedly")
+    raise RuntimeError("sharded protocol: repeated FSIL_AGAIN")
+
+
+def _sharded_round(ops: ShardOps, device, group=None) -> float:
+    if hasattr(ops, "exchange_dictionary"):
+        ops.exchange_dictionary(group)
+    else:
+        labels, rows = ops.begin()
+        raw = merge_dictionaries(labels, rows, device, group)
+        ops.set_dictionary(raw)
+    stats, checks = ops.aggregate()
+    dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
+    # the validation word is only read by finish: its MIN overlaps the scoring kernels
+    pending = dist.all_reduce(checks, op=dist.ReduceOp.MIN, group=group, async_op=True)
+    partial = ops.score()
+    dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)
+    pending.wait()
+    return ops.finish()
 
 
 class _DeviceArray:
@@ -95,9 +101,33 @@ class _DeviceArray:
                                          "version": 3, "strides": None}
 
 
+_VIEWS = {}
+
+
 def device_view(ptr: int, n: int, dtype: torch.dtype, device) -> torch.Tensor:
-    typestr = {torch.float64: "<f8", torch.int64: "<i8"}[dtype]
-    return torch.as_tensor(_DeviceArray(ptr, n, typestr), device=device)
+    """A non-owning tensor over n elements at ptr.  Cached by (ptr, n, dtype): libfsil's
+    buffers are stable from call to call, and building the view is host time on every
+    step of the protocol."""
+    key = (ptr, n, dtype, str(device))
+    v = _VIEWS.get(key)
+    if v is None:
+        if len(_VIEWS) >= 256:
+            _VIEWS.clear()
+        typestr = {torch.float64: "<f8", torch.int64: "<i8"}[dtype]
+        v = _VIEWS[key] = torch.as_tensor(_DeviceArray(ptr, n, typestr), device=device)
+    return v
+
+
+_GATHER = {}
+
+
+def _gather_buffer(n: int, device) -> torch.Tensor:
+    key = (n, str(device))
+    buf = _GATHER.get(key)
+    if buf is None:
+        _GATHER.clear()
+        buf = _GATHER[key] = torch.empty(n, dtype=torch.int64, device=device)
+    return buf
 
 
 class CudaShardOps:
@@ -121,7 +151,7 @@ class CudaShardOps:
                                                self.row_offset, self.n_global, f64=self.X.dtype == torch.float64)
         local = device_view(ptr, 2 * cap, torch.int64, self.device)
         world = dist.get_world_size(group)
-        gathered = torch.empty(world * 2 * cap, dtype=torch.int64, device=self.device)
+        gathered = _gather_buffer(world * 2 * cap, self.device)
         dist.all_gather_into_tensor(gathered, local, group=group)
         self.ctx.shard_set_dictionary_device(gathered.data_ptr(), world, cap)
 

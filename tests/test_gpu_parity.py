@@ -312,8 +312,15 @@ def _shard_loopback(X, L, metric, nshards, path=0, device_exchange=False, ctxs=N
                                                 f64=x.dtype == torch.float64)
                 bufs.append(device_view(ptr, 2 * cap, torch.int64, dev).clone())
             gathered = torch.cat(bufs)
+            again = 0
             for c in ctxs:
-                c.shard_set_dictionary_device(gathered.data_ptr(), len(ctxs), cap)
+                try:
+                    c.shard_set_dictionary_device(gathered.data_ptr(), len(ctxs), cap)
+                except ShardAgain:  # a dictionary outgrew the exchange buffer
+                    again += 1
+            assert again in (0, len(ctxs)), "FSIL_AGAIN must be seen by every shard alike"
+            if again:
+                return None
             raw = np.array([], np.int32)
         else:
             first = {}
@@ -356,7 +363,7 @@ def _shard_loopback(X, L, metric, nshards, path=0, device_exchange=False, ctxs=N
         return (means, errors, raw) if again == 0 else None
 
     try:
-        for k in range(1, 4):
+        for k in range(1, 9):
             r = one_round()
             if r is not None:
                 break
@@ -573,6 +580,32 @@ def test_shard_k_speculation_again():
             assert all(abs(m - ref.mean) <= MEAN_TOL for m in means)
             assert np.abs(s - ref.s).max() <= S_TOL and np.array_equal(nb, ref.neighbour)
         assert attempts == [1, 2, 1, 2], attempts
+    finally:
+        for c in ctxs:
+            c.close()
+
+
+def test_shard_exchange_overflow_again():
+    """More distinct labels per rank than the device exchange holds (its first capacity
+    is 63 entries): every shard returns FSIL_AGAIN, the repeat uses a larger buffer;
+    also when the overflow is only seen at finish (speculated call), and across the
+    multi-block ordering (K > 2048)."""
+    from paper_2303_14102_b200 import Context
+    ctxs = [Context(0) for _ in range(3)]
+    try:
+        rng = np.random.default_rng(9)
+        n, d = 12_000, 16
+        attempts = []
+        for k in (500, 500, 3000, 3000):
+            X = (rng.normal(size=(n, d)) + 2 * rng.normal(size=(k, d))[rng.integers(0, k, n)]).astype(np.float32)
+            L = rng.permutation(np.arange(n) % k) * 3 + 11
+            ref = oracle.silhouette(X, L, "sqeuclid")
+            means, errors, s, nb, _ = _shard_loopback(X, L, "sqeuclid", 3, 0, device_exchange=True, ctxs=ctxs,
+                                                      attempts=attempts)
+            assert not errors
+            assert all(abs(m - ref.mean) <= MEAN_TOL for m in means)
+            assert np.abs(s - ref.s).max() <= S_TOL and np.array_equal(nb, ref.neighbour)
+        assert attempts == [2, 1, 2, 1], attempts
     finally:
         for c in ctxs:
             c.close()
