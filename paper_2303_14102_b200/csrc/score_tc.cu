@@ -24,6 +24,7 @@
 #include <cuda_fp16.h>
 
 #include "score_common.cuh"
+
 #include "sm100.cuh"
 
 namespace fsil {
@@ -302,6 +303,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int sw = r & 7;
     const float2 sx2 = make_float2(sc.sx, sc.sx), neg1 = make_float2(-1.f, -1.f);
     uint32_t n1 = 0, nt = 0;
+    int s1 = 0;        // n1 % NS, kept incrementally (NS is a runtime value)
+    uint32_t ph1 = 0;  // (n1 / NS) & 1
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
       double xi = 0.0;
       // the epilogue's per-row inputs, fetched here off its critical path
@@ -310,11 +313,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int xp = 0; xp < xpasses; ++xp) {
         if (myscr && xp > 0) {  // later passes load the stored conversions (producer)
           n1 += nkc;
+          s1 = static_cast<int>(n1 % NS);
+          ph1 = (n1 / NS) & 1;
           continue;
         }
         for (int kc = 0; kc < nkc; ++kc, ++n1) {
-          const int s1 = n1 % NS;
-          TW(4, stg_full + s1, (n1 / NS) & 1);
+          TW(4, stg_full + s1, ph1);
           uint8_t* sbase = stg + s1 * kStgBytes;
           float4 f[8];
           if (hq == 0 || kc * BK + 32 < p.d) {
@@ -370,6 +374,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(a_full + s1);
           }
+          if (++s1 == NS) {
+            s1 = 0;
+            ph1 ^= 1;
+          }
         }
         if (myscr && tl == 0) {  // this tile's chunks are all in global memory
           bulk_wait_all();
@@ -407,10 +415,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const double4 co = meta_clu[tb * BM + r];  // n, 1/(n-1), Psi, ||mu||
       const double xi64 = meta_xi[(tb * 2) * BM + r] + meta_xi[(tb * 2 + 1) * BM + r];
       const float xi = static_cast<float>(xi64);
-      const float xn = sqrtf(xi);
+      const float xn = COS ? 0.0f : sqrtf(xi);
+      const float rnf = COS ? rsqrtf(xi) : 0.0f;  // 1/||x|| (MUFU.RSQ, <= 2.2u) for cosine
       // ranking key m' = m - rowc (row constant dropped, no clamp): sqeuclid
       // m = xi + p_k - 2 dot, cosine m = 1 - dot/||x||; dot = acc * smul
-      const float rowm = COS ? -(sc.smul / xn) : -2.0f * sc.smul;
+      const float rowm = COS ? -(sc.smul * rnf) : -2.0f * sc.smul;
       float b1 = INFINITY, b2 = INFINITY, doto = NAN;
       int arg = -1;
       for (int cb = 0; cb < ncb; ++cb) {
@@ -521,16 +530,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float u = 5.9604645e-8f;
         const float rowc = COS ? 1.0f : xi;
         const float exi = tp.exic * u * xi;  // ||x||^2 error (fp32 blocks of 8; fp64 input rounding)
-        const float eps_dot = (tp.cdot * sc.mu_max + sc.floor_coef) * xn;  // any column
-        const float eps_m = COS ? (eps_dot / xn + 3.0f * u * (fabsf(b1) + 1.0f) + exi / xi)
-                                : (2.0f * eps_dot + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
+        // key error: the dot bound (per unit ||x|| for cosine); the key's own roundings
+        // (cosine: rsqrt 2.2u + product 0.5u + fma 0.5u on |m| <= 1, within 4u(|b1|+1));
+        // the ||x||^2 error
+        const float eps_dot1 = tp.cdot * sc.mu_max + sc.floor_coef;  // any column, per unit ||x||
+        const float eps_m = COS ? (eps_dot1 + 4.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u)
+                                : (2.0f * eps_dot1 * xn + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
         int nb = arg;
         // the winner's key error uses its own cluster norm (the runner-up's column is
         // not tracked: any-column bound eps_m)
         const float mu_arg = arg >= 0 ? __half2float(mn_s[arg]) * sc.mu_max : sc.mu_max;
-        const float eps_dot_arg = (tp.cdot * mu_arg + sc.floor_coef) * xn;
-        const float eps_m_arg = COS ? (eps_dot_arg / xn + 3.0f * u * (fabsf(b1) + 1.0f) + exi / xi)
-                                    : (2.0f * eps_dot_arg + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
+        const float eps_dot1_arg = tp.cdot * mu_arg + sc.floor_coef;
+        const float eps_m_arg = COS ? (eps_dot1_arg + 4.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u)
+                                    : (2.0f * eps_dot1_arg * xn + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
         // neighbour certain: clear gap, and no tie through the clamps at 0 (and 2)
         const bool full = !((b2 - b1) > eps_m + eps_m_arg) || nb < 0 || !(rowc + b2 > eps_m) ||
                           (COS && !(rowc + b1 < 2.0f - eps_m));
@@ -545,11 +557,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           // cosine: everything O(1) -- fp32 evaluation, its roundings in the bounds
           const float dob = doto * sc.smul;  // exact (power-of-two scale)
           const float n_o = static_cast<float>(co.x), r_o = static_cast<float>(co.y), nr_o = n_o * r_o;
-          const float rnf = rsqrtf(xi);  // 1/||x||: rsqrt (<= 2 ulp) of the rounded xi
-          const float t = n_o * dob * rnf;
+          const float t = n_o * dob * rnf;  // rnf: rsqrt (<= 2.2u) of the rounded xi
           const float b = fminf(fmaxf(1.0f + b1, 0.0f), 2.0f);
           const float a = singleton ? 0.0f : fminf(fmaxf((n_o - t) * r_o, 0.0f), 2.0f);
-          const float db = 1.01f * (eb1 + 3.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u + u * b);
+          const float db = 1.01f * (eb1 + 4.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u + u * b);
           // dots; ||x||^2 and rsqrt (8.1u/2 + 2.5u); the four fp32 roundings of a
           const float da = 1.01f * (nr_o * (eo1 + tp.exic * u) + 3.0f * u * nr_o * fabsf(dob * rnf) +
                                     5.0f * u * (n_o + fabsf(t)) * r_o);
