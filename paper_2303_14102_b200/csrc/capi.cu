@@ -27,6 +27,7 @@ void flag_all(fsil_context* c, const ScoreParams& p, int tile_rows);
 void exact_ab(fsil_context* c, const ScoreParams& p);
 void refine(fsil_context* c, const ScoreParams& p);
 void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows, bool local);
+bool post_fused(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows, bool local);
 bool tc_supported(const fsil_context* c);
 int64_t tc_tiles(const fsil_context* c, int* tile_rows);
 void score_tc(fsil_context* c, const ScoreParams& p);
@@ -221,11 +222,15 @@ void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, 
   else flag_all(c, p, tile_rows);
   c->score_path = use;
   record(c, 4);
-  if (c->tc_exact_used) exact_ab(c, p);
-  refine(c, p);
-  record(c, 5);
   // single GPU: the final kernel also fills the mapped host summary (no pack launch)
-  finalize_sum(c, p, ntiles, tile_rows, c->local_call);
+  if (c->fuse_post && post_fused(c, p, ntiles, tile_rows, c->local_call)) {
+    record(c, 5);  // (refine phase = the fused post-scoring kernel; finalize phase empty)
+  } else {
+    if (c->tc_exact_used) exact_ab(c, p);
+    refine(c, p);
+    record(c, 5);
+    finalize_sum(c, p, ntiles, tile_rows, c->local_call);
+  }
   c->summary_packed = c->local_call;
 }
 
@@ -410,6 +415,7 @@ fsil_status fsil_create(fsil_context** out, int device) {
     c->smem_optin = prop.sharedMemPerBlockOptin;
     if (const char* e = std::getenv("FSIL_SPECULATE")) c->speculate = std::string(e) != "0";
     if (const char* e = std::getenv("FSIL_DEBUG_SYNC")) c->debug_sync = std::string(e) == "1";
+    if (const char* e = std::getenv("FSIL_FUSE_POST")) c->fuse_post = std::string(e) != "0";
     FSIL_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
     for (auto& e : c->ev) FSIL_CUDA(cudaEventCreate(&e));

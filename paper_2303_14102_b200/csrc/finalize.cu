@@ -22,15 +22,11 @@ namespace {
 // per 32 clusters instead of 5 per cluster).  Each lane keeps its ascending-k running
 // argmin (strict <); the warp merge breaks ties towards the lowest k.
 template <bool COS>
-__global__ void __launch_bounds__(256) refine_kernel(ScoreParams p) {
-  if (*p.abort) return;
-  extern __shared__ double xs_all[];  // [warps per block][d]
+__device__ __forceinline__ void refine_rows(const ScoreParams& p, double* xs, int64_t warp, int64_t nwarps,
+                                            int lane, const double* staged = nullptr) {
   const unsigned long long count = *p.flag_count;
-  const int lane = threadIdx.x & 31;
-  double* xs = xs_all + static_cast<int64_t>(threadIdx.x >> 5) * p.d;
-  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const double* sums = p.stats + (COS ? p.k : 2 * p.k);
+  // cluster sums: staged in shared memory by the caller (small tables), else global
+  const double* sums = staged ? staged : p.stats + (COS ? p.k : 2 * p.k);
   const int d = p.d, K = p.k;
   for (int64_t i = warp; i < static_cast<int64_t>(count); i += nwarps) {
     const int64_t row = p.flag_rows[i];
@@ -57,7 +53,8 @@ __global__ void __launch_bounds__(256) refine_kernel(ScoreParams p) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int k = kc + j < K ? kc + j : K - 1;  // clamped; result unused
-          acc[j] = fma(__ldg(sums + static_cast<int64_t>(k) * d + l), xv, acc[j]);
+          acc[j] = fma(staged ? sums[static_cast<int64_t>(k) * d + l] : __ldg(sums + static_cast<int64_t>(k) * d + l), xv,
+                       acc[j]);
         }
       }
 #pragma unroll
@@ -106,6 +103,15 @@ __global__ void __launch_bounds__(256) refine_kernel(ScoreParams p) {
       if (p.b) p.b[row] = best;
     }
   }
+}
+
+template <bool COS>
+__global__ void __launch_bounds__(256) refine_kernel(ScoreParams p) {
+  if (*p.abort) return;
+  extern __shared__ double xs_all[];  // [warps per block][d]
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  refine_rows<COS>(p, xs_all + static_cast<int64_t>(threadIdx.x >> 5) * p.d, warp, nwarps, threadIdx.x & 31);
 }
 
 // Tiled fp64 refinement for many flagged rows against many clusters (C4, C5): a block
@@ -262,48 +268,55 @@ struct TotalArgs {
   const int* missing;
 };
 
-__global__ void __launch_bounds__(256) tile_group_kernel(const double* __restrict__ tile_sum,
-                                                         const int32_t* __restrict__ tile_flag,
-                                                         const double* __restrict__ s,
-                                                         int64_t ntiles, int tile_rows, int64_t n,
-                                                         TotalArgs ta) {
+// One group of 32 tiles by a 256-thread block; true in the block that completed the
+// last of `ngroups` groups (it then sums them: tile_total).
+__device__ __forceinline__ bool tile_group_one(const double* __restrict__ tile_sum,
+                                               const int32_t* __restrict__ tile_flag, const double* s,
+                                               int64_t ntiles, int tile_rows, int64_t n, const TotalArgs& ta,
+                                               int64_t g, int64_t ngroups) {
   __shared__ double sm[32];
-  __shared__ double red[256];
+  __shared__ int fl[32];
   __shared__ bool last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * 32;
-  for (int j = warp; j < 32; j += 8) {
+  const int64_t t0 = g * 32;
+  if (warp == 0) {  // every tile's flag and partial in one round trip
+    const int64_t tt = t0 + lane;
+    const bool in = tt < ntiles;
+    fl[lane] = in ? tile_flag[tt] : 0;
+    sm[lane] = in ? tile_sum[tt] : 0.0;
+  }
+  __syncthreads();
+  for (int j = warp; j < 32; j += 8) {  // tiles that held refined rows: re-sum from s[]
+    if (!fl[j]) continue;
     const int64_t tt = t0 + j;
-    double v = 0.0;
-    if (tt < ntiles) {
-      if (tile_flag[tt]) {
-        const int64_t r0 = tt * tile_rows, r1 = min(n, r0 + tile_rows);
-        double acc = 0.0;
-        for (int64_t r = r0 + lane; r < r1; r += 32) acc += s[r];
-        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        v = acc;
-      } else {
-        v = tile_sum[tt];
-      }
-    }
-    if (lane == 0) sm[j] = v;
+    const int64_t r0 = tt * tile_rows, r1 = min(n, r0 + tile_rows);
+    double acc = 0.0;
+    for (int64_t r = r0 + lane; r < r1; r += 32) acc += __ldcg(s + r);  // written by this grid
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) sm[j] = acc;
   }
   __syncthreads();
   if (warp == 0) {
     double v = sm[lane];
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
     if (lane == 0) {
-      ta.group_sum[blockIdx.x] = v;
+      ta.group_sum[g] = v;
       __threadfence();
-      last = atomicAdd(ta.ticket, 1u) == gridDim.x - 1;
+      last = atomicAdd(ta.ticket, 1u) == static_cast<unsigned>(ngroups - 1);
     }
   }
   __syncthreads();
-  if (!last) return;
+  const bool l = last;
+  __syncthreads();  // `last` is rewritten by the block's next group
+  return l;
+}
+
+__device__ __forceinline__ void tile_total(const TotalArgs& ta, int64_t ngroups) {
+  __shared__ double red[256];
   __threadfence();
   // fixed order: thread i sums groups i, i + 256, ...; then a fixed tree
   double acc = 0.0;
-  for (int64_t g = threadIdx.x; g < gridDim.x; g += 256) acc += ta.group_sum[g];
+  for (int64_t g = threadIdx.x; g < ngroups; g += 256) acc += __ldcg(ta.group_sum + g);
   red[threadIdx.x] = acc;
   __syncthreads();
   for (int stride = 128; stride > 0; stride >>= 1) {
@@ -328,6 +341,15 @@ __global__ void __launch_bounds__(256) tile_group_kernel(const double* __restric
   }
 }
 
+__global__ void __launch_bounds__(256) tile_group_kernel(const double* __restrict__ tile_sum,
+                                                         const int32_t* __restrict__ tile_flag,
+                                                         const double* __restrict__ s,
+                                                         int64_t ntiles, int tile_rows, int64_t n,
+                                                         TotalArgs ta) {
+  if (tile_group_one(tile_sum, tile_flag, s, ntiles, tile_rows, n, ta, blockIdx.x, gridDim.x))
+    tile_total(ta, gridDim.x);
+}
+
 // FSIL_PATH_FP64: every row goes through the fp64 re-evaluation.
 __global__ void flag_all_kernel(int64_t n, int tile_rows, int32_t* flag_rows, int32_t* tile_flag,
                                 double* tile_sum, unsigned long long* flag_count) {
@@ -344,14 +366,12 @@ __global__ void flag_all_kernel(int64_t n, int tile_rows, int32_t* flag_rows, in
 // loose (neighbour already certified): LPR lanes per row (32/LPR rows per warp),
 // reference formulas in fp64.
 template <bool COS, int LPR>
-__global__ void __launch_bounds__(256) exact_ab_kernel(ScoreParams p, const int2* __restrict__ rows,
-                                                       const unsigned long long* count) {
-  if (*p.abort) return;
+__device__ __forceinline__ void exact_rows_body(const ScoreParams& p, const int2* __restrict__ rows,
+                                                const unsigned long long* count, int64_t warp, int64_t nwarps,
+                                                int lane) {
   const int64_t cnt = static_cast<int64_t>(*count);
-  const int lane = threadIdx.x & 31, sub = lane / LPR, li = lane % LPR;
+  const int sub = lane / LPR, li = lane % LPR;
   constexpr int RPW = 32 / LPR;
-  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const double* sums = p.stats + (COS ? p.k : 2 * p.k);
   for (int64_t base = warp * RPW; base < cnt; base += nwarps * RPW) {
     const int64_t i = base + sub;
@@ -393,6 +413,64 @@ __global__ void __launch_bounds__(256) exact_ab_kernel(ScoreParams p, const int2
       if (p.b) p.b[row] = b;
     }
   }
+}
+
+template <bool COS, int LPR>
+__global__ void __launch_bounds__(256) exact_ab_kernel(ScoreParams p, const int2* __restrict__ rows,
+                                                       const unsigned long long* count) {
+  if (*p.abort) return;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  exact_rows_body<COS, LPR>(p, rows, count, warp, nwarps, threadIdx.x & 31);
+}
+
+// Grid-wide barrier for a co-resident (cooperatively launched) grid: arrival count
+// plus a generation word; the last arriver resets the count and bumps the generation.
+__device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = gen;
+    const unsigned int g0 = *vgen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0u;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*vgen == g0) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// The whole post-scoring phase in one cooperative launch (small cluster tables):
+// exact a/b rows and flagged rows (disjoint sets), grid barrier, then the tile groups
+// and -- in the block that finishes the last group -- the fixed-order total.
+template <bool COS, int LPR>
+__global__ void __launch_bounds__(256) post_kernel(ScoreParams p, const int2* __restrict__ exact_rows,
+                                                   const unsigned long long* exact_count, int64_t ntiles,
+                                                   int tile_rows, TotalArgs ta, unsigned int* bar, bool stage) {
+  extern __shared__ double xs_all[];  // [8 warps][d], then (stage) the cluster sums [K][d]
+  const bool abort = *p.abort != 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  double* staged = nullptr;
+  if (stage) {  // the table in shared memory: its loads overlap the first rows' own
+    staged = xs_all + 8 * p.d;
+    const double* sums = p.stats + (COS ? p.k : 2 * p.k);
+    for (int64_t e = threadIdx.x; e < static_cast<int64_t>(p.k) * p.d; e += blockDim.x) staged[e] = __ldg(sums + e);
+    __syncthreads();
+  }
+  if (!abort) {
+    if (exact_count) exact_rows_body<COS, LPR>(p, exact_rows, exact_count, warp, nwarps, lane);
+    refine_rows<COS>(p, xs_all + static_cast<int64_t>(threadIdx.x >> 5) * p.d, warp, nwarps, lane, staged);
+  }
+  grid_barrier(bar, bar + 1);
+  const int64_t ngroups = (ntiles + 31) / 32 > 0 ? (ntiles + 31) / 32 : 1;
+  for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x)
+    if (tile_group_one(p.tile_sum, p.tile_flag, p.s, ntiles, tile_rows, p.n, ta, g, ngroups)) tile_total(ta, ngroups);
 }
 
 }  // namespace
@@ -445,8 +523,8 @@ void refine(fsil_context* c, const ScoreParams& p) {
   FSIL_LAUNCHED(c);
 }
 
-void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows, bool local) {
-  const int64_t ngroups = std::max<int64_t>((ntiles + 31) / 32, 1);
+namespace {
+TotalArgs total_args(fsil_context* c, const ScoreParams& p, int64_t ngroups, bool local) {
   c->group_sum.ensure(ngroups * sizeof(double));
   c->result.ensure(4 * sizeof(double));
   TotalArgs ta;
@@ -458,6 +536,48 @@ void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int til
   ta.hsum = local ? c->dsum : nullptr;
   ta.checks = c->checks.as<int64_t>();
   ta.missing = c->counters.as<int>() + 4;
+  return ta;
+}
+}  // namespace
+
+// exact_ab + refine + finalize_sum as one cooperative launch when the per-row refine
+// applies (cluster table below the tiled kernel's threshold); false: not applicable.
+bool post_fused(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows, bool local) {
+  if (static_cast<int64_t>(c->k) * c->d >= 64 * 1024) return false;
+  size_t smem = 8 * static_cast<size_t>(c->d) * sizeof(double);
+  if (smem > c->smem_optin) return false;
+  const size_t table = static_cast<size_t>(c->k) * c->d * sizeof(double);
+  bool stage = smem + table <= 64 * 1024;  // small tables: staged per block
+  if (stage) smem += table;
+  const int64_t ngroups = std::max<int64_t>((ntiles + 31) / 32, 1);
+  TotalArgs ta = total_args(c, p, ngroups, local);
+  const int2* rows = c->exact_rows.as<int2>();
+  const unsigned long long* cnt = c->tc_exact_used ? c->exact_count.as<unsigned long long>() : nullptr;
+  unsigned int* bar = reinterpret_cast<unsigned int*>(c->counters.as<int>() + 12);
+  const int lpr = c->d <= 32 ? 4 : c->d <= 64 ? 8 : c->d <= 128 ? 16 : 32;
+  void* kern = nullptr;
+#define FSIL_POST(L)                                                                                 \
+  if (lpr == L) kern = c->metric == FSIL_COSINE ? reinterpret_cast<void*>(post_kernel<true, L>)     \
+                                                : reinterpret_cast<void*>(post_kernel<false, L>);
+  FSIL_POST(4) FSIL_POST(8) FSIL_POST(16) FSIL_POST(32)
+#undef FSIL_POST
+  FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  FSIL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+  if (per_sm < 1) return false;
+  const int grid = std::min(per_sm, 2) * c->num_sms;  // co-resident: the grid barrier needs it
+  ScoreParams pp = p;
+  int64_t nt = ntiles;
+  int tr = tile_rows;
+  void* args[] = {&pp, &rows, &cnt, &nt, &tr, &ta, &bar, &stage};
+  FSIL_CUDA(cudaLaunchCooperativeKernel(kern, grid, 256, args, smem, c->stream));
+  FSIL_LAUNCHED(c);
+  return true;
+}
+
+void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows, bool local) {
+  const int64_t ngroups = std::max<int64_t>((ntiles + 31) / 32, 1);
+  TotalArgs ta = total_args(c, p, ngroups, local);
   tile_group_kernel<<<static_cast<unsigned>(ngroups), 256, 0, c->stream>>>(p.tile_sum, p.tile_flag, p.s, ntiles,
                                                                          tile_rows, p.n, ta);
   FSIL_LAUNCHED(c);

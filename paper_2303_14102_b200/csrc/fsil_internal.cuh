@@ -156,6 +156,7 @@ struct fsil_context {
   // call's K, checked by finish() against this call's count.
   bool speculate = true;   // FSIL_SPECULATE=0 disables
   bool debug_sync = false;  // FSIL_DEBUG_SYNC=1: synchronise and check after every launch
+  bool fuse_post = true;    // FSIL_FUSE_POST=0: separate exact / refine / tile-group launches
   bool k_spec = false;     // this call speculated
   bool spec_big = false;   // ... with the multi-block ordering launched
   bool spec_missed = false;
