@@ -60,11 +60,13 @@ __device__ bool global_insert(unsigned long long* keys, unsigned long long* vals
   return false;
 }
 
+// `coherent`: through L2 (a table written earlier in the same kernel)
+template <bool coherent = false>
 __device__ int64_t find_slot(const unsigned long long* keys, uint32_t mask, uint32_t epoch, int32_t lab) {
   const unsigned long long key = ekey(epoch, lab);
   uint32_t h = hash32(static_cast<uint32_t>(lab)) & mask;
   for (uint32_t probe = 0; probe <= mask; ++probe) {
-    const unsigned long long cur = keys[h];
+    const unsigned long long cur = coherent ? __ldcg(keys + h) : keys[h];
     if (cur == key) return h;
     if (static_cast<uint32_t>(cur >> 32) != epoch) return -1;
     h = (h + 1) & mask;
@@ -74,10 +76,9 @@ __device__ int64_t find_slot(const unsigned long long* keys, uint32_t mask, uint
 
 // Per-block shared-memory dedup of a contiguous row range; only the lowest lane of
 // each run of equal labels in a warp touches the table.
-__global__ void __launch_bounds__(256) densify_collect_kernel(const int32_t* __restrict__ labels, int64_t n,
-                                                              int64_t chunk, unsigned long long* gkeys,
-                                                              unsigned long long* gvals, uint32_t mask,
-                                                              uint32_t epoch, int* overflow) {
+__device__ __forceinline__ void collect_body(const int32_t* __restrict__ labels, int64_t n, int64_t chunk,
+                                             unsigned long long* gkeys, unsigned long long* gvals, uint32_t mask,
+                                             uint32_t epoch, int* overflow) {
   __shared__ unsigned long long skeys[kSmemSlots];
   __shared__ uint32_t svals[kSmemSlots];
   for (int i = threadIdx.x; i < kSmemSlots; i += blockDim.x) {
@@ -131,28 +132,43 @@ __global__ void __launch_bounds__(256) densify_collect_kernel(const int32_t* __r
   }
 }
 
+__global__ void __launch_bounds__(256) densify_collect_kernel(const int32_t* __restrict__ labels, int64_t n,
+                                                              int64_t chunk, unsigned long long* gkeys,
+                                                              unsigned long long* gvals, uint32_t mask,
+                                                              uint32_t epoch, int* overflow) {
+  collect_body(labels, n, chunk, gkeys, gvals, mask, epoch, overflow);
+}
+
 // Single block: compact the current-epoch slots, rank by first row, write the dense
 // order (sorted_labels) and the per-slot dense id.  More than kSmallK labels: flag
 // counters[1] and leave the ordering to the multi-block kernels.
-__global__ void __launch_bounds__(1024) densify_finish_kernel(const unsigned long long* __restrict__ keys,
-                                                              const unsigned long long* __restrict__ vals,
-                                                              uint32_t cap, uint32_t epoch, int32_t* sorted_labels,
-                                                              int32_t* slot_dense, int* counters, HostSummary* hsum,
-                                                              int32_t k_spec = 0, bool spec_big = false) {
+__device__ __forceinline__ void finish_body(const unsigned long long* keys, const unsigned long long* vals,
+                                            uint32_t cap, uint32_t epoch, int32_t* sorted_labels, int32_t* slot_dense,
+                                            int* counters, HostSummary* hsum, int32_t k_spec, bool spec_big) {
   __shared__ int32_t s_lab[kSmallK];
   __shared__ uint32_t s_row[kSmallK];
   __shared__ uint32_t s_slot[kSmallK];
   __shared__ int s_count;
   if (threadIdx.x == 0) s_count = 0;
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) {
-    const unsigned long long key = keys[i];
-    if (static_cast<uint32_t>(key >> 32) != epoch) continue;
-    const int j = atomicAdd(&s_count, 1);
-    if (j < kSmallK) {
-      s_lab[j] = static_cast<int32_t>(static_cast<uint32_t>(key));
-      s_row[j] = value_row(vals[i]);
-      s_slot[j] = i;
+  constexpr int B = 8;  // slots in flight per thread
+  for (uint32_t i0 = 0; i0 < cap; i0 += B * blockDim.x) {
+    unsigned long long kk[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const uint32_t i = i0 + u * blockDim.x + threadIdx.x;
+      kk[u] = i < cap ? __ldcg(keys + i) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const uint32_t i = i0 + u * blockDim.x + threadIdx.x;
+      if (i >= cap || static_cast<uint32_t>(kk[u] >> 32) != epoch) continue;
+      const int j = atomicAdd(&s_count, 1);
+      if (j < kSmallK) {
+        s_lab[j] = static_cast<int32_t>(static_cast<uint32_t>(kk[u]));
+        s_row[j] = value_row(__ldcg(vals + i));
+        s_slot[j] = i;
+      }
     }
   }
   __syncthreads();
@@ -169,29 +185,37 @@ __global__ void __launch_bounds__(1024) densify_finish_kernel(const unsigned lon
   if (threadIdx.x == 0) {
     counters[1] = cnt > kSmallK ? 1 : 0;  // needs the multi-block ordering
     // speculated K (k_spec > 0): raise the miss flag the scoring kernels check at entry
-    if (k_spec > 0 && (cnt != k_spec || counters[0] != 0 || (cnt > kSmallK && !spec_big))) counters[kAbortWord] = 1;
+    const int over = __ldcg(counters);  // raised by any block (atomics)
+    if (k_spec > 0 && (cnt != k_spec || over != 0 || (cnt > kSmallK && !spec_big))) counters[kAbortWord] = 1;
     *reinterpret_cast<unsigned long long*>(counters + 2) = static_cast<unsigned long long>(cnt);
     if (hsum) {
-      hsum->overflow = counters[0];
+      hsum->overflow = over;
       hsum->count = cnt;
       hsum->pad = counters[1];
     }
   }
 }
 
+__global__ void __launch_bounds__(1024) densify_finish_kernel(const unsigned long long* __restrict__ keys,
+                                                              const unsigned long long* __restrict__ vals,
+                                                              uint32_t cap, uint32_t epoch, int32_t* sorted_labels,
+                                                              int32_t* slot_dense, int* counters, HostSummary* hsum,
+                                                              int32_t k_spec = 0, bool spec_big = false) {
+  finish_body(keys, vals, cap, epoch, sorted_labels, slot_dense, counters, hsum, k_spec, spec_big);
+}
+
 // Row -> dense id through the global table (per-slot dense ids; L1/L2 resident).
-__global__ void __launch_bounds__(256) densify_map_kernel(const int32_t* __restrict__ labels, int64_t n,
-                                                          const unsigned long long* __restrict__ gkeys,
-                                                          const int32_t* __restrict__ slot_dense, uint32_t mask,
-                                                          uint32_t epoch, int32_t k_lim, int32_t* dense,
-                                                          int* missing) {
+template <bool coherent = false>
+__device__ __forceinline__ void map_body(const int32_t* __restrict__ labels, int64_t n,
+                                         const unsigned long long* gkeys, const int32_t* slot_dense, uint32_t mask,
+                                         uint32_t epoch, int32_t k_lim, int32_t* dense, int* missing) {
   // k_lim: the K the following kernels are launched for (the speculated K, or INT_MAX when
   // the host waits for the count).  An id outside [0, k_lim) -- only possible when the
   // speculation misses -- is stored as 0 and flagged, so every later kernel stays in bounds.
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int64_t slot = find_slot(gkeys, mask, epoch, __ldg(labels + i));
-    int32_t dj = slot >= 0 ? slot_dense[slot] : -1;
+    const int64_t slot = find_slot<coherent>(gkeys, mask, epoch, __ldg(labels + i));
+    int32_t dj = slot >= 0 ? (coherent ? __ldcg(slot_dense + slot) : slot_dense[slot]) : -1;
     if (dj < 0 || dj >= k_lim) {
       atomicExch(missing, 1);
       dj = 0;
@@ -199,6 +223,15 @@ __global__ void __launch_bounds__(256) densify_map_kernel(const int32_t* __restr
     dense[i] = dj;
   }
 }
+
+__global__ void __launch_bounds__(256) densify_map_kernel(const int32_t* __restrict__ labels, int64_t n,
+                                                          const unsigned long long* __restrict__ gkeys,
+                                                          const int32_t* __restrict__ slot_dense, uint32_t mask,
+                                                          uint32_t epoch, int32_t k_lim, int32_t* dense,
+                                                          int* missing) {
+  map_body(labels, n, gkeys, slot_dense, mask, epoch, k_lim, dense, missing);
+}
+
 
 __global__ void densify_compact_kernel(const unsigned long long* __restrict__ keys,
                                        const unsigned long long* __restrict__ vals, uint32_t cap, uint32_t epoch,

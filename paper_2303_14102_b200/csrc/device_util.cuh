@@ -64,4 +64,24 @@ __device__ __forceinline__ double assemble_score(double a, double b) {
   return a <= b ? 1.0 - a / b : b / a - 1.0;
 }
 
+// Grid-wide barrier for a co-resident (cooperatively launched) grid: arrival count
+// plus a generation word; the last arriver resets the count and bumps the generation.
+__device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = gen;
+    const unsigned int g0 = *vgen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0u;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*vgen == g0) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 }  // namespace fsil

@@ -424,26 +424,6 @@ __global__ void __launch_bounds__(256) exact_ab_kernel(ScoreParams p, const int2
   exact_rows_body<COS, LPR>(p, rows, count, warp, nwarps, threadIdx.x & 31);
 }
 
-// Grid-wide barrier for a co-resident (cooperatively launched) grid: arrival count
-// plus a generation word; the last arriver resets the count and bumps the generation.
-__device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned int* vgen = gen;
-    const unsigned int g0 = *vgen;
-    __threadfence();
-    if (atomicAdd(count, 1u) == gridDim.x - 1) {
-      *count = 0u;
-      __threadfence();
-      atomicAdd(gen, 1u);
-    } else {
-      while (*vgen == g0) __nanosleep(64);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 // The whole post-scoring phase in one cooperative launch (small cluster tables):
 // exact a/b rows and flagged rows (disjoint sets), grid barrier, then the tile groups
 // and -- in the block that finishes the last group -- the fixed-order total.
