@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(256) agg_warp_kernel(
 // the bytes in flight per SM no longer depend on registers.  One CTA per SM owns a
 // contiguous row range; consumer warp w takes rows w, w+W, ... of every stage.
 template <bool COS, int DPL, int NS>
-__global__ void __launch_bounds__(13 * 32, 1) agg_stage_kernel(
+__global__ void __launch_bounds__(16 * 32, 1) agg_stage_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ dense, int64_t n, int d,
     int64_t row_offset, int k, int64_t chunk, double* __restrict__ partials, int64_t* checks,
     float* xmax) {
@@ -181,7 +181,8 @@ __global__ void __launch_bounds__(13 * 32, 1) agg_stage_kernel(
   const int R = U * W;                  // rows per stage
   const int Sw = k * d + (COS ? 0 : k * 32) + k;
   double* sm = reinterpret_cast<double*>(smraw);
-  float* ring = reinterpret_cast<float*>(sm + static_cast<size_t>(W) * Sw);
+  // bulk-copy destinations need 16-byte alignment (W * Sw may be odd)
+  float* ring = reinterpret_cast<float*>(sm + ((static_cast<size_t>(W) * Sw + 1) & ~size_t(1)));
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(NS) * R * d);
   uint64_t* full = bars;
   uint64_t* empty = bars + NS;
@@ -637,10 +638,10 @@ __global__ void agg_init_kernel(double* stats, int64_t S, int64_t* checks, float
 
 template <bool COS>
 void launch_stage(fsil_context* c, int dpl, int warps, int64_t chunk, size_t smem, double* partials,
-                  int64_t* checks) {
+                  int64_t* checks, int ns) {
 #define FSIL_AGG_STAGE(P)                                                                        \
   if (dpl == P) {                                                                                \
-    auto kern = agg_stage_kernel<COS, P, 3>;                                                     \
+    auto kern = ns == 2 ? agg_stage_kernel<COS, P, 2> : agg_stage_kernel<COS, P, 3>;             \
     FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     kern<<<c->num_sms, (warps + 1) * 32, smem, c->stream>>>(c->X, c->dense.as<int32_t>(), c->n, c->d, \
                                              c->row_offset, c->k, chunk, partials, checks,       \
@@ -729,9 +730,14 @@ void aggregate(fsil_context* c) {
   const int blocks_per_sm = smem > 0 ? static_cast<int>(std::min<size_t>(228 * 1024 / (smem + 1024), 64 / warps)) : 0;
   // Path 1a: bulk-TMA staged (needs 16-byte rows); one CTA per SM.
   if (dpl <= 4 && c->d % 4 == 0 && !x64) {
-    int W = 12;
-    auto need = [&](int w) { return w * per_warp + 3ull * 8 * w * c->d * 4 + 64 + 16; };
-    while (W > 4 && need(W) > budget) W -= 4;
+    // Consumer throughput bounds this kernel (measured at C2: T ~ 40 us + 632 us / W),
+    // while the ring depth does not (NS = 2..6 alike): two stages, and as many
+    // consumer warps (<= 15, one producer: 512 threads) as the private copies allow.
+    // C2: W = 15 -> 89 us (W = 12, NS = 3: 95 us).
+    int W = 15;
+    const int NSs = 2;
+    auto need = [&](int w) { return w * per_warp + 8 + static_cast<size_t>(NSs) * 8 * w * c->d * 4 + 64 + 16; };
+    while (W > 4 && need(W) > budget) --W;
     if (need(W) <= budget && W >= 4) {
       c->agg_path = 1;
       const int64_t R = 8 * W;
@@ -739,8 +745,8 @@ void aggregate(fsil_context* c) {
       chunk = (chunk + R - 1) / R * R;
       const int grid = c->num_sms;
       c->partials.ensure(static_cast<size_t>(grid) * S * sizeof(double));
-      if (cos) launch_stage<true>(c, dpl, W, chunk, need(W), c->partials.as<double>(), checks);
-      else launch_stage<false>(c, dpl, W, chunk, need(W), c->partials.as<double>(), checks);
+      if (cos) launch_stage<true>(c, dpl, W, chunk, need(W), c->partials.as<double>(), checks, NSs);
+      else launch_stage<false>(c, dpl, W, chunk, need(W), c->partials.as<double>(), checks, NSs);
       fold_partials_kernel<<<static_cast<unsigned>((S + 31) / 32), 256, 0, c->stream>>>(
           c->partials.as<double>(), grid, S, stats);
       FSIL_LAUNCHED(c);
