@@ -19,6 +19,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "device_util.cuh"
 #include "fsil_internal.cuh"
@@ -391,6 +392,201 @@ __global__ void __launch_bounds__(16 * 32, 1) agg_stage_kernel(
   }
 }
 
+// Two-phase batched aggregation (D in {16, 32, 64, 128}, K*(D+2) small).  Every
+// warp streams its own batches of 32 contiguous rows (one bulk copy each, double
+// buffered per warp, no producer warp and no CTA-wide barrier) and
+//   phase A  one lane per row: the row's fp64 ||x||^2 (rotated 16-byte chunks, so the
+//            eight lanes of a shared-memory wavefront hit distinct banks), max|x|, the
+//            finite / zero-norm checks, the count, and the row's scale (cosine
+//            1/||x||; squared Euclidean the Psi contribution ||x||^2);
+//   phase B  one lane per pair of dimensions: eight rows' contributions formed in
+//            registers first, then eight read-modify-writes of the warp-private fp64
+//            accumulators [K][D (+Psi, pad)].
+// Compared with agg_stage (lanes own dimensions throughout) the per-row norm needs no
+// cross-lane transpose-reduce or broadcast, and the label arrives by one shuffle.
+// Rows go to warps in a fixed pattern and every sum has a fixed order: bit-identical
+// results run to run.  Replaces the same reference code as agg_stage
+// (squared_euclidean.cpp:37-54, cosine.cpp:39-61, cos.cpp:119-123, dataset.cpp:35-37).
+template <int D, bool COS, int BR>
+struct BatchCfg {
+  static constexpr int NCH = D / 4;           // 16-byte chunks per row
+  static constexpr int LPR = 32 / BR;         // phase-A lanes per row
+  static constexpr int DX = COS ? D : D + 2;  // accumulated doubles per cluster: sums (+ Psi, pad)
+  static constexpr int NP = DX / 2;           // double pairs per cluster
+  static constexpr int PPL = (NP + 31) / 32;  // pairs per lane
+  static constexpr int SLOT = BR * D;         // floats per batch slot
+};
+
+// batch rows: 16 (two phase-A lanes per row, more warps fit) unless D is small
+__host__ __device__ inline int batch_rows(int d) { return d >= 64 ? 16 : 32; }
+
+__host__ __device__ inline size_t batch_warp_bytes(int k, int d, bool cos) {
+  const size_t dx = cos ? d : d + 2;
+  const size_t br = batch_rows(d);
+  return static_cast<size_t>(k) * dx * 8 + ((static_cast<size_t>(k) * 4 + 15) & ~size_t(15)) + br * 8 +
+         2 * br * d * 4 + 16;
+}
+
+template <bool COS, int D, int BR>
+__global__ void __launch_bounds__(16 * 32, 1) agg_batch_kernel(
+    const float* __restrict__ X, const int32_t* __restrict__ dense, int64_t n, int64_t row_offset, int k,
+    double* __restrict__ partials, int64_t* checks, float* xmax) {
+  using C = BatchCfg<D, COS, BR>;
+  extern __shared__ __align__(16) uint8_t smraw[];
+  const int W = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int accw = k * C::DX;                          // doubles per warp accumulator
+  const int cntw = ((k * 4 + 15) & ~15) / 4;           // ints per warp count array (16B multiple)
+  double* acc = reinterpret_cast<double*>(smraw);      // [W][K][DX]
+  int* cnt = reinterpret_cast<int*>(acc + static_cast<size_t>(W) * accw);  // [W][cntw]
+  double* wv_all = reinterpret_cast<double*>(cnt + static_cast<size_t>(W) * cntw);  // [W][BR]
+  float* slots = reinterpret_cast<float*>(wv_all + W * BR);                 // [W][2][SLOT]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slots + static_cast<size_t>(W) * 2 * C::SLOT);  // [W][2]
+  for (int j = threadIdx.x; j < W * accw; j += blockDim.x) acc[j] = 0.0;
+  for (int j = threadIdx.x; j < W * cntw; j += blockDim.x) cnt[j] = 0;
+  if (threadIdx.x < 2 * W) sm100::mbar_init(bars + threadIdx.x, 1);
+  sm100::fence_barrier_init();
+  __syncthreads();
+
+  double* wacc = acc + static_cast<size_t>(warp) * accw;
+  int* wcnt = cnt + warp * cntw;
+  double* wv = wv_all + warp * BR;
+  float* wslot = slots + static_cast<size_t>(warp) * 2 * C::SLOT;
+  uint64_t* wbar = bars + 2 * warp;
+  const int64_t nb = (n + BR - 1) / BR;
+  const int64_t G = static_cast<int64_t>(gridDim.x) * W;
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * W + warp;
+  auto issue = [&](int64_t b, int s) {
+    if (lane == 0) {
+      const int64_t r0 = b * BR;
+      const int64_t rows = n - r0 < BR ? n - r0 : BR;
+      const uint32_t bytes = static_cast<uint32_t>(rows * D * 4);
+      sm100::mbar_arrive_expect_tx(wbar + s, bytes);
+      sm100::bulk_load(wslot + s * C::SLOT, X + r0 * D, bytes, wbar + s);
+    }
+  };
+  if (g < nb) issue(g, 0);
+  if (g + G < nb) issue(g + G, 1);
+
+  const int rl = lane % BR, half = lane / BR;  // phase A: row, part of the row
+  float amax = 0.f;
+  int j = 0;
+  for (int64_t b = g; b < nb; b += G, ++j) {
+    const int s = j & 1;
+    const int64_t r0 = b * BR;
+    const int rows = static_cast<int>(n - r0 < BR ? n - r0 : BR);
+    const bool rv = rl < rows;
+    const int lab = rv ? __ldg(dense + r0 + rl) : 0;  // lanes rl and rl + BR hold the same row
+    sm100::mbar_wait(wbar + s, (j >> 1) & 1);
+    const float* sl = wslot + s * C::SLOT;
+
+    // ---- phase A: LPR lanes per row
+    double ss;
+    {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      if (rv) {
+        const float4* rp = reinterpret_cast<const float4*>(sl + rl * D);
+#pragma unroll
+        for (int i = 0; i < C::NCH / C::LPR; ++i) {
+          const float4 f = rp[(i * C::LPR + half + rl) & (C::NCH - 1)];
+          s0 = fma(static_cast<double>(f.x), static_cast<double>(f.x), s0);
+          s1 = fma(static_cast<double>(f.y), static_cast<double>(f.y), s1);
+          s2 = fma(static_cast<double>(f.z), static_cast<double>(f.z), s2);
+          s3 = fma(static_cast<double>(f.w), static_cast<double>(f.w), s3);
+          amax = fmaxf(amax, fmaxf(fabsf(f.x), fabsf(f.y)));
+          amax = fmaxf(amax, fmaxf(fabsf(f.z), fabsf(f.w)));
+        }
+      }
+      ss = (s0 + s1) + (s2 + s3);
+      if (C::LPR == 2) ss += __shfl_xor_sync(0xffffffffu, ss, 16);
+    }
+    if (rv && half == 0) {
+      const int64_t row = row_offset + r0 + rl;
+      if (!isfinite(ss)) {  // rare: the first non-finite element of the row (dataset.cpp:35-37)
+        for (int l = 0; l < D; ++l)
+          if (!isfinite(sl[rl * D + l])) {
+            atomic_min_i64(checks, row * D + l);
+            break;
+          }
+      } else if (COS && ss == 0.0) {  // zero row (cos.cpp:119-123): reported
+        atomic_min_i64(checks + 1, row);
+      }
+      wv[rl] = COS ? (ss > 0.0 && ss < INFINITY ? 1.0 / sqrt(ss) : 0.0) : ss;
+      atomicAdd(wcnt + lab, 1);
+    }
+    __syncwarp();
+
+    // ---- phase B: lane = pairs of dimensions (the Psi pair after the sums); eight
+    // rows' contributions in registers, then their read-modify-writes in row order
+    auto rows8 = [&](int rb, bool checked) {
+      double2 p[8][C::PPL];
+      int L[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = (rb + u) & (BR - 1);
+        L[u] = __shfl_sync(0xffffffffu, lab, r);
+        const double v = wv[r];
+        const float* xr = sl + r * D;
+#pragma unroll
+        for (int q = 0; q < C::PPL; ++q) {
+          const int pi = lane + 32 * q;
+          if (pi < D / 2) {
+            const float2 x = *reinterpret_cast<const float2*>(xr + 2 * pi);
+            p[u][q] = COS ? make_double2(static_cast<double>(x.x) * v, static_cast<double>(x.y) * v)
+                          : make_double2(static_cast<double>(x.x), static_cast<double>(x.y));
+          } else {
+            p[u][q] = make_double2(COS ? 0.0 : v, 0.0);  // squared Euclidean: (Psi, pad)
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (checked && rb + u >= rows) break;  // warp-uniform
+#pragma unroll
+        for (int q = 0; q < C::PPL; ++q) {
+          const int pi = lane + 32 * q;
+          if (pi < C::NP) {
+            double2* a = reinterpret_cast<double2*>(wacc + L[u] * C::DX + 2 * pi);
+            double2 t = *a;
+            t.x += p[u][q].x;
+            t.y += p[u][q].y;
+            *a = t;
+          }
+        }
+      }
+    };
+    if (rows == BR) {
+#pragma unroll 1
+      for (int rb = 0; rb < BR; rb += 8) rows8(rb, false);
+    } else {
+#pragma unroll 1
+      for (int rb = 0; rb < rows; rb += 8) rows8(rb, true);
+    }
+    __syncwarp();  // every lane has read slot s
+    if (b + 2 * G < nb) issue(b + 2 * G, s);
+  }
+  for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  if (lane == 0 && amax > 0.f) atomic_max_nonneg_f32(xmax, amax);
+  __syncthreads();
+  // fold the warps (fixed order) into this block's partial, StatsLayout order
+  const int S = COS ? k * (D + 1) : k * (D + 2);
+  for (int jj = threadIdx.x; jj < S; jj += blockDim.x) {
+    double a = 0.0;
+    if (jj < k) {
+      for (int w = 0; w < W; ++w) a += static_cast<double>(cnt[w * cntw + jj]);
+    } else if (!COS && jj < 2 * k) {
+      const int c = jj - k;
+      for (int w = 0; w < W; ++w) a += acc[static_cast<size_t>(w) * accw + c * C::DX + D];
+    } else {
+      const int t = jj - (COS ? k : 2 * k);
+      const int c = t / D, l = t - c * D;
+      for (int w = 0; w < W; ++w) a += acc[static_cast<size_t>(w) * accw + c * C::DX + l];
+    }
+    partials[static_cast<int64_t>(blockIdx.x) * S + jj] = a;
+  }
+}
+
+
 // Sum of block partials per element: 8 fixed strided chains + fixed tree.
 __global__ void __launch_bounds__(256) fold_partials_kernel(const double* __restrict__ partials,
                                                             int nblocks, int64_t S,
@@ -654,6 +850,23 @@ void launch_stage(fsil_context* c, int dpl, int warps, int64_t chunk, size_t sme
   fail(FSIL_ERR_INTERNAL, "no staged aggregation kernel for this shape");
 }
 
+template <bool COS>
+void launch_batch(fsil_context* c, int warps, size_t smem, double* partials, int64_t* checks) {
+#define FSIL_AGG_BATCH(DD)                                                                       \
+  if (c->d == DD) {                                                                              \
+    auto kern = agg_batch_kernel<COS, DD, DD >= 64 ? 16 : 32>;                                                       \
+    FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    kern<<<c->num_sms, warps * 32, smem, c->stream>>>(c->X, c->dense.as<int32_t>(), c->n,         \
+                                                      c->row_offset, c->k, partials, checks,    \
+                                                      c->xmax.as<float>());                     \
+    FSIL_LAUNCHED(c);                                                                            \
+    return;                                                                                      \
+  }
+  FSIL_AGG_BATCH(16) FSIL_AGG_BATCH(32) FSIL_AGG_BATCH(64) FSIL_AGG_BATCH(128)
+#undef FSIL_AGG_BATCH
+  fail(FSIL_ERR_INTERNAL, "no batched aggregation kernel for this shape");
+}
+
 template <bool COS, typename T>
 void launch_warp(fsil_context* c, const T* X, int dpl, int grid, int threads, size_t smem, double* partials,
                  int64_t* checks) {
@@ -728,6 +941,28 @@ void aggregate(fsil_context* c) {
   while (warps > 1 && warps * per_warp > budget) warps >>= 1;
   const size_t smem = warps * per_warp;
   const int blocks_per_sm = smem > 0 ? static_cast<int>(std::min<size_t>(228 * 1024 / (smem + 1024), 64 / warps)) : 0;
+  // Path 1b: two-phase batches (D a power of two in 16..128); one CTA per SM with as
+  // many warps (<= 16) as the per-warp accumulators and batch slots allow.
+  static const bool batch_on = [] {
+    const char* e = std::getenv("FSIL_AGG_BATCH");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (batch_on && !x64 && (c->d == 16 || c->d == 32 || c->d == 64 || c->d == 128)) {
+    const size_t pw = batch_warp_bytes(c->k, c->d, cos);
+    int W = 16;
+    while (W > 4 && W * pw > budget) --W;
+    if (W * pw <= budget) {
+      c->agg_path = 3;
+      const int grid = c->num_sms;
+      c->partials.ensure(static_cast<size_t>(grid) * S * sizeof(double));
+      if (cos) launch_batch<true>(c, W, W * pw, c->partials.as<double>(), checks);
+      else launch_batch<false>(c, W, W * pw, c->partials.as<double>(), checks);
+      fold_partials_kernel<<<static_cast<unsigned>((S + 31) / 32), 256, 0, c->stream>>>(
+          c->partials.as<double>(), grid, S, stats);
+      FSIL_LAUNCHED(c);
+      return;
+    }
+  }
   // Path 1a: bulk-TMA staged (needs 16-byte rows); one CTA per SM.
   if (dpl <= 4 && c->d % 4 == 0 && !x64) {
     // Consumer throughput bounds this kernel (measured at C2: T ~ 40 us + 632 us / W),
