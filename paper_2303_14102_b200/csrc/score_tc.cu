@@ -86,10 +86,10 @@ struct TcCfg {
 // no per-thread state for it.
 #define TW(slot, bar, par)                                                          \
   do {                                                                              \
-    if (tp.dbg) {                                                                   \
+    if (PROF && dbgp) {                                                             \
       const long long t0__ = clock64();                                             \
       mbar_wait(bar, par);                                                          \
-      if (lane == 0) atomicAdd(tp.dbg + (slot), static_cast<unsigned long long>(clock64() - t0__)); \
+      if (lane == 0) atomicAdd(dbgp + (slot), static_cast<unsigned long long>(clock64() - t0__)); \
     } else {                                                                        \
       mbar_wait(bar, par);                                                          \
     }                                                                               \
@@ -101,8 +101,16 @@ struct TcCfg {
 //   warpgroups 1-2 (warps 4..11): epilogue, two groups of four -- 120 registers
 //   warpgroups 3-4 (warps 12..19): converters -- 96 registers
 constexpr int kEpiWarp0 = 4, kConvWarp0 = 12;
+#ifndef FSIL_EPI_REGS
+#define FSIL_EPI_REGS 136
+#endif
+#ifndef FSIL_CONV_REGS
+#define FSIL_CONV_REGS 80
+#endif
+// CTA register pool per lane: 4 x 40 + 8 x epilogue + 8 x converters <= 20 x 96
+static_assert(4 * 40 + 8 * FSIL_EPI_REGS + 8 * FSIL_CONV_REGS <= 20 * 96, "register split exceeds the pool");
 
-template <int BN, bool COS>
+template <int BN, bool COS, bool PROF>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
                     const __grid_constant__ CUtensorMap tmap_bl, TcParams tp, int64_t ntiles) {
@@ -165,7 +173,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ncb = tp.ncb, nkc = tp.nkc;
-  const long long t_start = tp.dbg ? clock64() : 0;
+  unsigned long long* const dbgp = PROF ? tp.dbg : nullptr;  // compiled out unless profiling
+  const long long t_start = dbgp ? clock64() : 0;
   for (int j = threadIdx.x; j < ncb * BN; j += blockDim.x) {
     cb_s[j] = tp.colbias[j];
     mn_s[j] = tp.munorm[j];
@@ -294,6 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= kConvWarp0) {
+    if (FSIL_CONV_REGS != 96) setmaxnreg_dec<FSIL_CONV_REGS>();
     // ------------------------------------------------------------ converters (8 warps:
     // two threads per row; thread half hq reads fp32 box hq of the stage, then -- after
     // the whole group has read -- writes A chunks 4hq..4hq+3 of hi (over box 0) and lo
@@ -320,12 +330,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kc = 0; kc < nkc; ++kc, ++n1) {
           TW(4, stg_full + s1, ph1);
           uint8_t* sbase = stg + s1 * kStgBytes;
+          // (box 1 of the last chunk may be absent: those lanes read stale bytes, then zero
+          // them on a warp-uniform branch rather than zero-initialising every chunk)
           float4 f[8];
-          if (hq == 0 || kc * BK + 32 < p.d) {
-            const uint8_t* srow = sbase + hq * (BM * 128) + r * 128;
+          const uint8_t* srow = sbase + hq * (BM * 128) + r * 128;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) f[u] = *reinterpret_cast<const float4*>(srow + ((u ^ sw) << 4));
-          } else {
+          for (int u = 0; u < 8; ++u) f[u] = *reinterpret_cast<const float4*>(srow + ((u ^ sw) << 4));
+          if (hq == 1 && kc * BK + 32 >= p.d) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) f[u] = make_float4(0.f, 0.f, 0.f, 0.f);
           }
@@ -399,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue (8 warps)
-    setmaxnreg_inc<120>();  // CTA pool: 4x40 + 8x120 + 8x96 <= 20x96 per lane
+    setmaxnreg_inc<FSIL_EPI_REGS>();  // CTA pool: see the static_assert above
     const int quad = warp & 3;                // TMEM lane quadrant of this warp
     const int r = quad * 32 + lane;           // row in tile
     const int grp = (warp - kEpiWarp0) >> 2;  // epilogue group 0 / 1
@@ -435,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++na;
         }
         TW(8, acc_full + ab, ph);
-        const long long ts0 = tp.dbg ? clock64() : 0;
+        const long long ts0 = dbgp ? clock64() : 0;
         tc_fence_after();
         // one 32-column chunk: ranking keys, own-column capture, running top-2
         auto scan32 = [&](const uint32_t(&v)[32], int k0) {
@@ -490,9 +501,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + ab);
-        if (tp.dbg && warp == kEpiWarp0 && lane == 0) atomicAdd(tp.dbg + 12, static_cast<unsigned long long>(clock64() - ts0));
+        if (dbgp && warp == kEpiWarp0 && lane == 0) atomicAdd(dbgp + 12, static_cast<unsigned long long>(clock64() - ts0));
       }
-      const long long tf0 = tp.dbg ? clock64() : 0;
+      const long long tf0 = dbgp ? clock64() : 0;
       if (!TS) {
         // ---- merge the two column halves (group 1 -> smem -> group 0)
         float* pt = part + tb * 4 * BM;  // double-buffered by tile parity
@@ -618,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         red_flag[tb * 4 + quad] = anyw != 0;
       }
       named_bar(2 + grp, 128);
-      if (tp.dbg && warp == kEpiWarp0 && lane == 0) atomicAdd(tp.dbg + 13, static_cast<unsigned long long>(clock64() - tf0));
+      if (dbgp && warp == kEpiWarp0 && lane == 0) atomicAdd(dbgp + 13, static_cast<unsigned long long>(clock64() - tf0));
       if (quad == 0 && lane == 0) {
         p.tile_sum[t] = ((red[tb * 4] + red[tb * 4 + 1]) + red[tb * 4 + 2]) + red[tb * 4 + 3];
         p.tile_flag[t] = red_flag[tb * 4] | red_flag[tb * 4 + 1] | red_flag[tb * 4 + 2] | red_flag[tb * 4 + 3];
@@ -626,10 +637,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
-  if (tp.dbg && lane == 0) {
-    if (warp == 0) atomicAdd(tp.dbg + 9, static_cast<unsigned long long>(clock64() - t_start));
-    if (warp == kEpiWarp0) atomicAdd(tp.dbg + 10, static_cast<unsigned long long>(clock64() - t_start));
-    if (warp == kConvWarp0) atomicAdd(tp.dbg + 11, static_cast<unsigned long long>(clock64() - t_start));
+  if (dbgp && lane == 0) {
+    if (warp == 0) atomicAdd(dbgp + 9, static_cast<unsigned long long>(clock64() - t_start));
+    if (warp == kEpiWarp0) atomicAdd(dbgp + 10, static_cast<unsigned long long>(clock64() - t_start));
+    if (warp == kConvWarp0) atomicAdd(dbgp + 11, static_cast<unsigned long long>(clock64() - t_start));
   }
   tc_fence_before();
   __syncthreads();
@@ -749,7 +760,7 @@ int tc_stages(int bn, int kp, size_t optin) {
 template <int BN, bool COS>
 void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                const TcParams& tp, int64_t ntiles) {
-  auto kern = score_tc_kernel<BN, COS>;
+  auto kern = tp.dbg ? score_tc_kernel<BN, COS, true> : score_tc_kernel<BN, COS, false>;
   const size_t smem = tc_smem(BN, tp.ncb * BN, tp.nstg);
   FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int grid = static_cast<int>(std::min<int64_t>(ntiles, c->num_sms));
