@@ -430,7 +430,7 @@ __host__ __device__ inline size_t batch_warp_bytes(int k, int d, bool cos) {
 template <bool COS, int D, int BR>
 __global__ void __launch_bounds__(16 * 32, 1) agg_batch_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ dense, int64_t n, int64_t row_offset, int k,
-    double* __restrict__ partials, int64_t* checks, float* xmax) {
+    double* __restrict__ partials, int64_t* checks, float* xmax, double* __restrict__ xi_out) {
   using C = BatchCfg<D, COS, BR>;
   extern __shared__ __align__(16) uint8_t smraw[];
   const int W = blockDim.x >> 5;
@@ -512,6 +512,7 @@ __global__ void __launch_bounds__(16 * 32, 1) agg_batch_kernel(
         atomic_min_i64(checks + 1, row);
       }
       wv[rl] = COS ? (ss > 0.0 && ss < INFINITY ? 1.0 / sqrt(ss) : 0.0) : ss;
+      xi_out[r0 + rl] = ss;  // ||x||^2 for the scoring pass (fp64, from the exact squares)
       atomicAdd(wcnt + lab, 1);
     }
     __syncwarp();
@@ -858,7 +859,7 @@ void launch_batch(fsil_context* c, int warps, size_t smem, double* partials, int
     FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     kern<<<c->num_sms, warps * 32, smem, c->stream>>>(c->X, c->dense.as<int32_t>(), c->n,         \
                                                       c->row_offset, c->k, partials, checks,    \
-                                                      c->xmax.as<float>());                     \
+                                                      c->xmax.as<float>(), c->xi_rows.as<double>()); \
     FSIL_LAUNCHED(c);                                                                            \
     return;                                                                                      \
   }
@@ -918,6 +919,7 @@ void aggregate(fsil_context* c) {
   double* stats = c->stats_buf.as<double>();
   int64_t* checks = c->checks.as<int64_t>();
   c->xmax.ensure(sizeof(float));
+  c->xi_valid = false;
   agg_init_kernel<<<static_cast<unsigned>(std::min<int64_t>((S + 255) / 256 + 1, 1024)), 256, 0, c->stream>>>(
       stats, S, checks, c->xmax.as<float>());
   FSIL_LAUNCHED(c);
@@ -953,6 +955,8 @@ void aggregate(fsil_context* c) {
     while (W > 4 && W * pw > budget) --W;
     if (W * pw <= budget) {
       c->agg_path = 3;
+      c->xi_rows.ensure(static_cast<size_t>(c->n) * sizeof(double));
+      c->xi_valid = true;
       const int grid = c->num_sms;
       c->partials.ensure(static_cast<size_t>(grid) * S * sizeof(double));
       if (cos) launch_batch<true>(c, W, W * pw, c->partials.as<double>(), checks);

@@ -149,6 +149,8 @@ struct fsil_context {
   fsil::DevBuf exact_rows, exact_count;  // rows needing the exact own/neighbour recompute
   fsil::DevBuf a_scratch;                // tcgen05 streaming mode: per-CTA converted A chunks
   fsil::DevBuf x32;                      // fp64 front end: rounded fp32 copy for the fast pass
+  fsil::DevBuf xi_rows;                  // fp64 ||x||^2 per row, written by the batched aggregation
+  bool xi_valid = false;                 // xi_rows holds this call's rows (scoring reads them)
   fsil::DevBuf xbuf;                     // sharded protocol: device dictionary exchange entries
   fsil::DevBuf xt_keys, xt_vals, xt_dense;  // ... and the global-dictionary table (own epochs)
   int64_t xt_cap = 0;

@@ -60,6 +60,8 @@ struct TcParams {
   const double4* clu;     // [K]: {n_k, 1/(n_k-1) (0 if singleton), Psi_k, ||mu_k|| rounded up}
   const __half* munorm;   // [ncb*BN]: ||mu_k|| / mu_max rounded up (neighbour error bounds)
   int nstg;               // X staging stages
+  int nsa;                // decoupled mode: A operand slots (0: A converted in place in the X stages)
+  int dual;               // two MMA-issuing warps (alternate tiles; TS mode only)
   const TcScale* scale;
   float cdot;             // relative dot bound coefficient
   unsigned long long* dbg;  // optional per-role wait-cycle counters (FSIL_TC_PROFILE)
@@ -68,7 +70,22 @@ struct TcParams {
   unsigned long long* exact_count;
   uint8_t* ascratch;      // streaming mode: [grid][nkc][kStgBytes] converted A chunks (or null)
   float exic;             // ||x||^2 relative error / u: 8.1 (fp32 blocks of 8), +2.1 on fp64 input
+  const double* xi_rows;  // per-row fp64 ||x||^2 from the aggregation pass (or null: converters form it)
+  long long* trace;       // FSIL_TRACE builds: per-tile role timestamps of CTA 0 (or null)
 };
+
+// Timeline tracing (compile with -DFSIL_TRACE, run with FSIL_TC_TRACE=1): CTA 0 records
+// clock64() at fixed points of each role for its first 64 tiles.
+#ifdef FSIL_TRACE
+#define TRACE(i, k)                                                                                  \
+  do {                                                                                               \
+    if (blockIdx.x == 0 && tp.trace && (threadIdx.x & 31) == 0 && (i) < 64) tp.trace[(i) * 9 + (k)] = clock64(); \
+  } while (0)
+#else
+#define TRACE(i, k) \
+  do {              \
+  } while (0)
+#endif
 
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
@@ -105,12 +122,17 @@ constexpr int kEpiWarp0 = 4, kConvWarp0 = 12;
 #define FSIL_EPI_REGS 136
 #endif
 #ifndef FSIL_CONV_REGS
-#define FSIL_CONV_REGS 80
+#define FSIL_CONV_REGS 72
+#endif
+#ifndef FSIL_WG0_REGS
+#define FSIL_WG0_REGS 64
 #endif
 // CTA register pool per lane: 4 x 40 + 8 x epilogue + 8 x converters <= 20 x 96
-static_assert(4 * 40 + 8 * FSIL_EPI_REGS + 8 * FSIL_CONV_REGS <= 20 * 96, "register split exceeds the pool");
+static_assert(4 * FSIL_WG0_REGS + 8 * FSIL_EPI_REGS + 8 * FSIL_CONV_REGS <= 20 * 96, "register split exceeds the pool");
 
-template <int BN, bool COS, bool PROF>
+// KC: columns of each 32-column chunk the epilogue scans (BN = 32 with K <= 24 skips
+// the padding columns; otherwise 32)
+template <int BN, bool COS, bool PROF, int KC>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
                     const __grid_constant__ CUtensorMap tmap_bl, TcParams tp, int64_t ntiles) {
@@ -120,6 +142,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   // X stages: a TMA-filled fp32 box pair that the converters overwrite in place with
   // the fp16 A pieces (hi over box 0, lo over box 1), freed by the MMA commit
   const int NS = tp.nstg;
+  // Decoupled (NSA > 0; one cluster block, ||x||^2 from the aggregation pass): the
+  // converters read a stage into registers and free it at once, then write the A
+  // pieces into one of NSA separate operand slots that the MMA commit frees -- the X
+  // stages only cover TMA latency instead of being held through conversion and MMA.
+  const int NSA = tp.nsa;
   // TS: the two epilogue groups take alternate tiles, each with its own pair of
   // accumulator buffers, so consecutive tiles' epilogues overlap -- for tiles of at
   // most two cluster blocks (with more, the MMA stream would serialise on one
@@ -149,11 +176,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   // the compiler: LDS/STS rather than generic accesses)
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* stg = base;                      // [NS][kStgBytes]
-  uint8_t* bring = stg + NS * kStgBytes;    // [NB][b_hi | b_lo]
+  uint8_t* aslot = stg + NS * kStgBytes;    // [NSA][kStgBytes] decoupled A operand slots
+  uint8_t* bring = aslot + NSA * kStgBytes; // [NB][b_hi | b_lo]
   uint64_t* bars = reinterpret_cast<uint64_t*>(bring + NB * 2 * C::kBBytes);
   uint64_t* stg_full = bars;               // [NS <= 8] X landed (TMA)
   uint64_t* stg_empty = bars + 8;          // [NS] stage free (MMA commit)
-  uint64_t* a_full = bars + 16;            // [NS] A pieces written (converters)
+  uint64_t* a_full = bars + 16;            // [NS] A pieces written (converters) -- [NSA] decoupled
+  uint64_t* a_empty = stg_empty + NS;      // decoupled: [NSA] A slot free (MMA commit); NS + NSA <= 8
   uint64_t* b_full = bars + 24;            // [NB]
   uint64_t* b_empty = bars + 28;           // [NB]
   uint64_t* acc_full = bars + 32;          // [4]
@@ -184,9 +213,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(stg_full + i, 1);
-      mbar_init(stg_empty + i, 1);
+      mbar_init(stg_empty + i, NSA ? 8 : 1);
       mbar_init(a_full + i, myscr ? 1 : 8);
     }
+    for (int i = 0; i < NSA; ++i) mbar_init(a_empty + i, 1);
     for (int i = 0; i < NB; ++i) {
       mbar_init(b_full + i, 1);
       mbar_init(b_empty + i, 1);
@@ -212,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp < kEpiWarp0) {
-    setmaxnreg_dec<40>();
+    if (FSIL_WG0_REGS != 96) setmaxnreg_dec<FSIL_WG0_REGS>();
     if (warp == 0 && lane == 0) {
       // ---------------------------------------------------------- TMA producer: X
       uint32_t n1 = 0, ntl = 0;
@@ -235,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive_expect_tx(stg_full + s1, nbox * BM * 128);
             for (int b = 0; b < nbox; ++b)
               tma_load_2d(stg + s1 * kStgBytes + b * BM * 128, &tmap_x, stg_full + s1, kc * BK + b * 32, row0);
+            TRACE(ntl, 0);
           }
         }
       }
@@ -250,13 +281,45 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive_expect_tx(b_full + sb, 2 * C::kBBytes);
             tma_load_2d(bs, &tmap_bh, b_full + sb, kc * BK, cb * BN);
             tma_load_2d(bs + C::kBBytes, &tmap_bl, b_full + sb, kc * BK, cb * BN);
+            TRACE((t - blockIdx.x) / gridDim.x, 8);
           }
         }
       }
-    } else if (warp == 1 && lane == 0) {
-      // ---------------------------------------------------------- MMA issuer
-      uint32_t n2 = 0, na = 0, ng0 = 0, ng1 = 0, nt = 0, nx = 0;
+    } else if ((warp == 1 || (warp == 3 && TS && tp.dual)) && lane == 0) {
+      // ---------------------------------------------------------- MMA issuer(s)
+      // With alternating epilogue groups (TS) warps 1 and 3 issue the MMAs of even and
+      // odd tiles respectively: each tile's operand slots, B stages and accumulator pair
+      // are used by exactly one issuer, so the two streams need no ordering between them,
+      // and the issue work (uniform-datapath descriptor arithmetic, waits) is halved per
+      // issuing warp.  Both walk every tile to keep the ring counters in step.
+      const uint32_t iid = warp == 3 ? 1u : 0u;
+      const bool dual = TS && tp.dual;
+      // ring positions (slot, phase) advance incrementally: no runtime division
+      const int NA = NSA ? NSA : NS;
+      uint8_t* const abuf = NSA ? aslot : stg;
+      uint64_t* const a_free = NSA ? a_empty : stg_empty;
+      int a_s = 0, b_s = 0;
+      uint32_t a_ph = 0, b_ph = 0;
+      auto adv = [](int& sl, uint32_t& ph, int n, int k) {
+        sl += k;
+        while (sl >= n) {
+          sl -= n;
+          ph ^= 1u;
+        }
+      };
+      uint32_t na = 0, ng0 = 0, ng1 = 0, nt = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
+        const bool mine = !dual || (nt & 1u) == iid;
+        if (!mine) {  // the other issuer's tile: advance the counters only
+          if (nt & 1) ng1 += ncb;
+          else ng0 += ncb;
+          na += ncb;
+          adv(b_s, b_ph, NB, ncb * nkc);
+          adv(a_s, a_ph, NA, ares ? nkc : ncb * nkc);
+          continue;
+        }
+        int s_end = a_s;
+        uint32_t ph_end = a_ph;
         for (int cb = 0; cb < ncb; ++cb, ++na) {
           int ab;
           uint32_t ph;
@@ -274,32 +337,54 @@ __global__ void __launch_bounds__(kThreads, 1)
           TW(2, acc_empty + ab, ph ^ 1);
           tc_fence_after();
           const uint32_t d_main = tmem_base + ab * astride, d_corr = tp.split ? d_main + BN : d_main;
-          for (int kc = 0; kc < nkc; ++kc, ++n2) {
-            const uint32_t ia = ares ? nx + kc : nx + cb * nkc + kc;  // A item
-            const int s1 = ia % NS, sb = n2 % NB;
-            if (!ares || cb == 0) TW(3, a_full + s1, (ia / NS) & 1);
-            TW(3, b_full + sb, (n2 / NB) & 1);
+          // A items of this block: the tile's chunks (A-resident: the same items for every
+          // block), otherwise the next ncb*nkc items
+          int sa = a_s;
+          uint32_t pa = a_ph;
+          if (!ares) adv(sa, pa, NA, cb * nkc);
+          for (int kc = 0; kc < nkc; ++kc) {
+            if (!ares || cb == 0) TW(3, a_full + sa, pa);
+            TW(3, b_full + b_s, b_ph);
+            TRACE(nt, 3);
             tc_fence_after();
             const int rem = p.d - kc * BK;
-            const int nks = rem >= BK ? 4 : (rem + 15) / 16;
-            const uint32_t ah = smem_u32(stg + s1 * kStgBytes), al = ah + kABytes;
-            const uint32_t bh = smem_u32(bring + sb * 2 * C::kBBytes), bl = bh + C::kBBytes;
-            for (int ks = 0; ks < nks; ++ks) {
-              const uint32_t off = ks * 32;
-              const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
-              // split: the two correction terms (~2^-10 of the main term) accumulate
-              // separately so their fp32 rounding is ~2^-10 smaller; for small D a
-              // single accumulator is certified tightly enough and is cheaper
-              mma_f16(d_main, desc_k_sw128(ah + off), desc_k_sw128(bh + off), kIdesc, acc0);
-              mma_f16(d_corr, desc_k_sw128(ah + off), desc_k_sw128(bl + off), kIdesc, tp.split ? acc0 : 1u);
-              mma_f16(d_corr, desc_k_sw128(al + off), desc_k_sw128(bh + off), kIdesc, 1u);
+            // descriptors of the chunk's operand pieces; a 16-element K step is +32 B, i.e.
+            // +2 in the descriptor's address field
+            const uint64_t dah = desc_k_sw128(smem_u32(abuf + sa * kStgBytes)), dal = dah + (kABytes >> 4);
+            const uint64_t dbh = desc_k_sw128(smem_u32(bring + b_s * 2 * C::kBBytes)), dbl = dbh + (C::kBBytes >> 4);
+            const uint32_t acc_in = kc > 0 ? 1u : 0u;
+            // split: the two correction terms (~2^-10 of the main term) accumulate
+            // separately so their fp32 rounding is ~2^-10 smaller; for small D a
+            // single accumulator is certified tightly enough and is cheaper
+            if (rem >= BK) {
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks) {
+                const uint32_t acc0 = ks > 0 ? 1u : acc_in;
+                mma_f16(d_main, dah + 2 * ks, dbh + 2 * ks, kIdesc, acc0);
+                mma_f16(d_corr, dah + 2 * ks, dbl + 2 * ks, kIdesc, tp.split ? acc0 : 1u);
+                mma_f16(d_corr, dal + 2 * ks, dbh + 2 * ks, kIdesc, 1u);
+              }
+            } else {
+              const int nks = (rem + 15) / 16;
+              for (int ks = 0; ks < nks; ++ks) {
+                const uint32_t acc0 = ks > 0 ? 1u : acc_in;
+                mma_f16(d_main, dah + 2 * ks, dbh + 2 * ks, kIdesc, acc0);
+                mma_f16(d_corr, dah + 2 * ks, dbl + 2 * ks, kIdesc, tp.split ? acc0 : 1u);
+                mma_f16(d_corr, dal + 2 * ks, dbh + 2 * ks, kIdesc, 1u);
+              }
             }
-            mma_commit(b_empty + sb);                               // B stage free when these retire
-            if (!ares || cb == ncb - 1) mma_commit(stg_empty + s1);  // A stage: after its last use
+            mma_commit(b_empty + b_s);                                 // B stage free when these retire
+            if (!ares || cb == ncb - 1) mma_commit(a_free + sa);       // A stage / slot: after its last use
+            adv(sa, pa, NA, 1);
+            adv(b_s, b_ph, NB, 1);
           }
+          s_end = sa;
+          ph_end = pa;
           mma_commit(acc_full + ab);  // accumulators ready for the epilogue
+          TRACE(nt, 4);
         }
-        nx += ares ? nkc : ncb * nkc;
+        a_s = s_end;  // the tile's last A item + 1 (A-resident: the tile's nkc items)
+        a_ph = ph_end;
       }
     }
   } else if (warp >= kConvWarp0) {
@@ -315,11 +400,110 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t n1 = 0, nt = 0;
     int s1 = 0;        // n1 % NS, kept incrementally (NS is a runtime value)
     uint32_t ph1 = 0;  // (n1 / NS) & 1
+    // ext: ||x||^2 comes from the aggregation pass and the epilogue fetches its per-row
+    // inputs itself -- the converters only convert (no norm, no meta hand-off)
+    const bool ext = tp.xi_rows != nullptr;
+    if (NSA) {
+      // decoupled: stage -> registers -> free the stage -> convert into an A slot
+      const uint32_t rd = hq * (BM * 128) + r * 128, wr = r * 128;
+      const bool tail_box = hq == 1;
+      int sa = 0;
+      uint32_t pha = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kc = 0; kc < nkc; ++kc) {
+          mbar_wait(stg_full + s1, ph1);
+          if (warp == kConvWarp0) TRACE((t - blockIdx.x) / gridDim.x, 1);
+          const uint8_t* sbase = stg + s1 * kStgBytes;
+          float4 f[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) f[u] = *reinterpret_cast<const float4*>(sbase + rd + ((u ^ sw) << 4));
+          __syncwarp();
+          if (lane == 0) mbar_arrive(stg_empty + s1);  // the stage is in registers: TMA may refill it
+          if (++s1 == NS) {
+            s1 = 0;
+            ph1 ^= 1;
+          }
+          if (tail_box && kc * BK + 32 >= p.d) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) f[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          mbar_wait(a_empty + sa, pha ^ 1);
+          uint8_t* abase = aslot + sa * kStgBytes;
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const float v[8] = {f[2 * jj].x,     f[2 * jj].y,     f[2 * jj].z,     f[2 * jj].w,
+                                f[2 * jj + 1].x, f[2 * jj + 1].y, f[2 * jj + 1].z, f[2 * jj + 1].w};
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 xx = __fmul2_rn(make_float2(v[2 * e], v[2 * e + 1]), sx2);
+              const __half2 h = __float22half2_rn(xx);
+              const float2 res = __ffma2_rn(__half22float2(h), neg1, xx);  // exact
+              const __half2 l = __float22half2_rn(res);
+              hw[e] = *reinterpret_cast<const uint32_t*>(&h);
+              lw[e] = *reinterpret_cast<const uint32_t*>(&l);
+            }
+            const uint32_t pos = wr + (((4 * hq + jj) ^ sw) << 4);
+            *reinterpret_cast<uint4*>(abase + pos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(abase + BM * 128 + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(a_full + sa);
+          if (warp == kConvWarp0) TRACE((t - blockIdx.x) / gridDim.x, 2);
+          if (++sa == NSA) {
+            sa = 0;
+            pha ^= 1;
+          }
+        }
+      }
+    } else if (ext && !myscr && xpasses == 1) {
+      // lean loop (every stage converted exactly once, nothing else): the per-thread
+      // swizzled offsets are loop invariant
+      const uint32_t rd = hq * (BM * 128) + r * 128, wr = r * 128;
+      const bool tail_box = hq == 1;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kc = 0; kc < nkc; ++kc) {
+          mbar_wait(stg_full + s1, ph1);
+          uint8_t* sbase = stg + s1 * kStgBytes;
+          float4 f[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) f[u] = *reinterpret_cast<const float4*>(sbase + rd + ((u ^ sw) << 4));
+          if (tail_box && kc * BK + 32 >= p.d) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) f[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          named_bar(5, 256);  // every read of the stage precedes the in-place writes
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const float v[8] = {f[2 * jj].x,     f[2 * jj].y,     f[2 * jj].z,     f[2 * jj].w,
+                                f[2 * jj + 1].x, f[2 * jj + 1].y, f[2 * jj + 1].z, f[2 * jj + 1].w};
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 xx = __fmul2_rn(make_float2(v[2 * e], v[2 * e + 1]), sx2);
+              const __half2 h = __float22half2_rn(xx);
+              const float2 res = __ffma2_rn(__half22float2(h), neg1, xx);  // exact
+              const __half2 l = __float22half2_rn(res);
+              hw[e] = *reinterpret_cast<const uint32_t*>(&h);
+              lw[e] = *reinterpret_cast<const uint32_t*>(&l);
+            }
+            const uint32_t pos = wr + (((4 * hq + jj) ^ sw) << 4);
+            *reinterpret_cast<uint4*>(sbase + pos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(sbase + BM * 128 + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(a_full + s1);
+          if (++s1 == NS) {
+            s1 = 0;
+            ph1 ^= 1;
+          }
+        }
+      }
+    } else
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
       double xi = 0.0;
-      // the epilogue's per-row inputs, fetched here off its critical path
-      const int64_t row = t * BM + r;
-      const int own = (hq == 0 && row < p.n) ? __ldg(p.dense + row) : -1;
       for (int xp = 0; xp < xpasses; ++xp) {
         if (myscr && xp > 0) {  // later passes load the stored conversions (producer)
           n1 += nkc;
@@ -348,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int j = 4 * hq + jj;
             const float v[8] = {f[2 * jj].x,     f[2 * jj].y,     f[2 * jj].z,     f[2 * jj].w,
                                 f[2 * jj + 1].x, f[2 * jj + 1].y, f[2 * jj + 1].z, f[2 * jj + 1].w};
-            if (xp == 0) {  // ||x||^2: fp32 blocks of 8 (error <= 8u each), fp64 across blocks
+            if (xp == 0 && !ext) {  // ||x||^2: fp32 blocks of 8 (error <= 8u each), fp64 across blocks
               float2 bs = make_float2(0.f, 0.f);
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
@@ -394,15 +578,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           bulk_wait_all();
           mbar_arrive(scr_ready);
         }
-        if (xp == 0) {
+        if (xp == 0 && !ext) {  // ||x||^2 halves to the epilogue
           const int tb = nt & 1;
-          const double4 co = own >= 0 ? tp.clu[own] : make_double4(1.0, 0.0, 0.0, 0.0);
           TW(6, meta_empty + tb, ((nt >> 1) & 1) ^ 1);
           meta_xi[(tb * 2 + hq) * BM + r] = xi;
-          if (hq == 0) {
-            meta_own[tb * BM + r] = own;
-            meta_clu[tb * BM + r] = co;
-          }
           __syncwarp();
           if (lane == 0) mbar_arrive(meta_full + tb);
         }
@@ -416,15 +595,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int grp = (warp - kEpiWarp0) >> 2;  // epilogue group 0 / 1
     uint32_t na = 0, nt = 0, ng = 0;
     constexpr int NQ = BN / 32;
+    // Per-row inputs (own cluster; ||x||^2 when the aggregation pass provides it) are
+    // fetched from global memory one tile ahead of their use, so their DRAM latency
+    // overlaps the current tile instead of serialising with it; clu[own] (L2) is issued
+    // at the start of the tile and first used after the scan.
+    const int64_t tstep = (TS ? 2 : 1) * static_cast<int64_t>(gridDim.x);
+    int own_n = -1;
+    double xi_n = 0.0;
+    auto fetch = [&](int64_t tt) {
+      const int64_t rr = tt * BM + r;
+      const bool ok = tt < ntiles && rr < p.n;
+      own_n = ok ? __ldg(p.dense + rr) : -1;
+      xi_n = ok && tp.xi_rows ? __ldg(tp.xi_rows + rr) : 0.0;
+    };
+    fetch(blockIdx.x + (TS ? grp : 0) * static_cast<int64_t>(gridDim.x));
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
       const int tb = nt & 1;
       if (TS && tb != grp) continue;  // the other group takes this tile
       const int64_t row = t * BM + r;
       const bool valid = row < p.n;
-      TW(7, meta_full + tb, (nt >> 1) & 1);
-      const int own = meta_own[tb * BM + r];
-      const double4 co = meta_clu[tb * BM + r];  // n, 1/(n-1), Psi, ||mu||
-      const double xi64 = meta_xi[(tb * 2) * BM + r] + meta_xi[(tb * 2 + 1) * BM + r];
+      const int own = own_n;
+      double xi64 = xi_n;
+      const double4 co = own >= 0 ? tp.clu[own] : make_double4(1.0, 0.0, 0.0, 0.0);  // n, 1/(n-1), Psi, ||mu||
+      fetch(t + tstep);
+      if (!tp.xi_rows) {
+        TW(7, meta_full + tb, (nt >> 1) & 1);
+        xi64 = meta_xi[(tb * 2) * BM + r] + meta_xi[(tb * 2 + 1) * BM + r];
+      }
       const float xi = static_cast<float>(xi64);
       const float xn = COS ? 0.0f : sqrtf(xi);
       const float rnf = COS ? rsqrtf(xi) : 0.0f;  // 1/||x|| (MUFU.RSQ, <= 2.2u) for cosine
@@ -446,6 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++na;
         }
         TW(8, acc_full + ab, ph);
+        if (quad == 0) TRACE(nt, 5);
         const long long ts0 = dbgp ? clock64() : 0;
         tc_fence_after();
         // one 32-column chunk: ranking keys, own-column capture, running top-2
@@ -454,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           int argc = -1;  // chunk-local index of a new best
           const float4* cb4 = reinterpret_cast<const float4*>(cb_s + k0);
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
+          for (int j4 = 0; j4 < KC / 4; ++j4) {
             const float4 bias = cb4[j4];
             const float bj[4] = {bias.x, bias.y, bias.z, bias.w};
 #pragma unroll
@@ -501,6 +699,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + ab);
+        if (quad == 0) TRACE(nt, 6);
         if (dbgp && warp == kEpiWarp0 && lane == 0) atomicAdd(dbgp + 12, static_cast<unsigned long long>(clock64() - ts0));
       }
       const long long tf0 = dbgp ? clock64() : 0;
@@ -516,7 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar(1, 256);
         if (grp == 1) {
           __syncwarp();
-          if (lane == 0) mbar_arrive(meta_empty + tb);
+          if (lane == 0 && !tp.xi_rows) mbar_arrive(meta_empty + tb);
           continue;
         }
         const float c1 = pt[0 * BM + r], c2 = pt[1 * BM + r];
@@ -529,7 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         doto = (doto == doto) ? doto : d2;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(meta_empty + tb);
+      if (lane == 0 && !tp.xi_rows) mbar_arrive(meta_empty + tb);
 
       // ---- certification and a_i, b_i, s_i.  Cosine in fp32: the inputs (tensor-core
       // dots) carry fp32-level certified errors already, the fp32 evaluation adds its
@@ -633,6 +832,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (quad == 0 && lane == 0) {
         p.tile_sum[t] = ((red[tb * 4] + red[tb * 4 + 1]) + red[tb * 4 + 2]) + red[tb * 4 + 3];
         p.tile_flag[t] = red_flag[tb * 4] | red_flag[tb * 4 + 1] | red_flag[tb * 4 + 2] | red_flag[tb * 4 + 3];
+        TRACE(nt, 7);
       }
     }
   }
@@ -757,11 +957,11 @@ int tc_stages(int bn, int kp, size_t optin) {
   return ns;
 }
 
-template <int BN, bool COS>
+template <int BN, bool COS, int KC = 32>
 void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                const TcParams& tp, int64_t ntiles) {
-  auto kern = tp.dbg ? score_tc_kernel<BN, COS, true> : score_tc_kernel<BN, COS, false>;
-  const size_t smem = tc_smem(BN, tp.ncb * BN, tp.nstg);
+  auto kern = tp.dbg ? score_tc_kernel<BN, COS, true, KC> : score_tc_kernel<BN, COS, false, KC>;
+  const size_t smem = tc_smem(BN, tp.ncb * BN, tp.nstg + tp.nsa);
   FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int grid = static_cast<int>(std::min<int64_t>(ntiles, c->num_sms));
   kern<<<grid, kThreads, smem, c->stream>>>(mx, mh, ml, tp, ntiles);
@@ -811,6 +1011,25 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   tp.munorm = munorm;
   tp.scale = scale;
   tp.nstg = tc_stages(bn, kp, c->smem_optin);
+  if (const char* e = std::getenv("FSIL_TC_NSTG")) tp.nstg = std::max(2, std::min(tp.nstg, std::atoi(e)));  // experiments
+  // decoupled A slots: one cluster block, per-row ||x||^2 from the aggregation pass, and
+  // room for >= 2 X stages besides the two slots
+  tp.nsa = 0;
+  {
+    static const int dual_env = [] {
+      const char* e = std::getenv("FSIL_TC_DUAL");
+      return e ? std::atoi(e) : 1;
+    }();
+    tp.dual = dual_env;
+    static const int dec_env = [] {
+      const char* e = std::getenv("FSIL_TC_DECOUPLE");
+      return e ? std::atoi(e) : 1;
+    }();
+    if (dec_env && ncb == 1 && c->xi_valid && !c->X64 && tp.nstg >= 4) {
+      tp.nsa = 2;
+      tp.nstg -= 2;
+    }
+  }
   {
     const int64_t ntiles_ = (c->n + BM - 1) / BM;
     const bool ares_ = ncb > 1 && 2 * nkc <= tp.nstg;
@@ -837,6 +1056,10 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     tp.cdot += 1.01f * u;
     tp.exic += 2.1f;
   }
+  // ||x||^2 from the batched aggregation: fp64 over exact squares, so only its fp32
+  // rounding (0.5u) remains in the bounds
+  tp.xi_rows = c->xi_valid && !c->X64 ? c->xi_rows.as<double>() : nullptr;
+  if (tp.xi_rows) tp.exic = 1.0f;
   c->exact_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int2));
   c->exact_count.ensure(sizeof(unsigned long long));
   FSIL_CUDA(cudaMemsetAsync(c->exact_count.p, 0, sizeof(unsigned long long), c->stream));
@@ -850,16 +1073,43 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     FSIL_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), c->stream));
   }
   tp.dbg = dbg;
+  static const bool trace = std::getenv("FSIL_TC_TRACE") != nullptr;
+  long long* trc = nullptr;
+  if (trace) {
+    FSIL_CUDA(cudaMalloc(&trc, 64 * 9 * sizeof(long long)));
+    FSIL_CUDA(cudaMemsetAsync(trc, 0, 64 * 9 * sizeof(long long), c->stream));
+  }
+  tp.trace = trc;
+  // K <= 24 at BN = 32: the epilogue scans only the first 16 / 24 columns
+  const int kc_scan = bn == 32 && c->k <= 16 ? 16 : bn == 32 && c->k <= 24 ? 24 : 32;
   if (cos) {
-    if (bn == 32) launch_tc<32, true>(c, mx, mh, ml, tp, ntiles);
+    if (bn == 32 && kc_scan == 16) launch_tc<32, true, 16>(c, mx, mh, ml, tp, ntiles);
+    else if (bn == 32 && kc_scan == 24) launch_tc<32, true, 24>(c, mx, mh, ml, tp, ntiles);
+    else if (bn == 32) launch_tc<32, true>(c, mx, mh, ml, tp, ntiles);
     else if (bn == 64) launch_tc<64, true>(c, mx, mh, ml, tp, ntiles);
     else launch_tc<128, true>(c, mx, mh, ml, tp, ntiles);
   } else {
-    if (bn == 32) launch_tc<32, false>(c, mx, mh, ml, tp, ntiles);
+    if (bn == 32 && kc_scan == 16) launch_tc<32, false, 16>(c, mx, mh, ml, tp, ntiles);
+    else if (bn == 32 && kc_scan == 24) launch_tc<32, false, 24>(c, mx, mh, ml, tp, ntiles);
+    else if (bn == 32) launch_tc<32, false>(c, mx, mh, ml, tp, ntiles);
     else if (bn == 64) launch_tc<64, false>(c, mx, mh, ml, tp, ntiles);
     else launch_tc<128, false>(c, mx, mh, ml, tp, ntiles);
   }
   c->tc_exact_used = true;
+  if (trc) {
+    long long h[64 * 9];
+    FSIL_CUDA(cudaMemcpyAsync(h, trc, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    FSIL_CUDA(cudaStreamSynchronize(c->stream));
+    const long long t0 = h[0];
+    std::fprintf(stderr, "[fsil tc trace] CTA 0, us from tile 0's X issue: tile | X-issue conv-in conv-out mma-go mma-commit epi-in epi-empty epi-done B-issue\n");
+    for (int i = 0; i < 64; ++i) {
+      if (!h[i * 9] && i) break;
+      std::fprintf(stderr, "%3d", i);
+      for (int k = 0; k < 9; ++k) std::fprintf(stderr, " %8.2f", h[i * 9 + k] ? (h[i * 9 + k] - t0) / 1965.0 : -1.0);
+      std::fprintf(stderr, "\n");
+    }
+    cudaFree(trc);
+  }
   if (dbg) {
     unsigned long long h[16];
     FSIL_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
