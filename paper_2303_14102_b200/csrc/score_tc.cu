@@ -285,7 +285,57 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-    } else if ((warp == 1 || (warp == 3 && TS && tp.dual)) && lane == 0) {
+    } else if (warp == 1 && lane == 0 && !(TS && NSA)) {
+      // ---------------------------------------------------------- MMA issuer (column-split
+      // epilogue or in-place A stages: C3/C4/C5).  A/B-measured: this form is 3-5% faster
+      // there than the ring-counter issuer below, which wins with decoupled A slots (C2).
+      uint32_t n2 = 0, na = 0, ng0 = 0, ng1 = 0, nt = 0, nx = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
+        for (int cb = 0; cb < ncb; ++cb, ++na) {
+          int ab;
+          uint32_t ph;
+          if (TS) {
+            const int g = nt & 1;
+            const uint32_t cnt = g ? ng1 : ng0;  // per-group buffer-pair counters
+            ab = 2 * g + (cnt & 1);
+            ph = (cnt >> 1) & 1;
+            ng0 += g ? 0u : 1u;
+            ng1 += g ? 1u : 0u;
+          } else {
+            ab = na % nacc;
+            ph = (na / nacc) & 1;
+          }
+          TW(2, acc_empty + ab, ph ^ 1);
+          tc_fence_after();
+          const uint32_t d_main = tmem_base + ab * astride, d_corr = tp.split ? d_main + BN : d_main;
+          for (int kc = 0; kc < nkc; ++kc, ++n2) {
+            const uint32_t ia = ares ? nx + kc : nx + cb * nkc + kc;  // A item
+            const int s1 = static_cast<int>(ia % NS), sb = n2 % NB;
+            if (!ares || cb == 0) TW(3, a_full + s1, (ia / NS) & 1);
+            TW(3, b_full + sb, (n2 / NB) & 1);
+            tc_fence_after();
+            const int rem = p.d - kc * BK;
+            const int nks = rem >= BK ? 4 : (rem + 15) / 16;
+            const uint32_t ah = smem_u32(stg + s1 * kStgBytes), al = ah + kABytes;
+            const uint32_t bh = smem_u32(bring + sb * 2 * C::kBBytes), bl = bh + C::kBBytes;
+            for (int ks = 0; ks < nks; ++ks) {
+              const uint32_t off = ks * 32;
+              const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
+              // split: the two correction terms (~2^-10 of the main term) accumulate
+              // separately so their fp32 rounding is ~2^-10 smaller; for small D a
+              // single accumulator is certified tightly enough and is cheaper
+              mma_f16(d_main, desc_k_sw128(ah + off), desc_k_sw128(bh + off), kIdesc, acc0);
+              mma_f16(d_corr, desc_k_sw128(ah + off), desc_k_sw128(bl + off), kIdesc, tp.split ? acc0 : 1u);
+              mma_f16(d_corr, desc_k_sw128(al + off), desc_k_sw128(bh + off), kIdesc, 1u);
+            }
+            mma_commit(b_empty + sb);                               // B stage free when these retire
+            if (!ares || cb == ncb - 1) mma_commit(stg_empty + s1);  // A stage: after its last use
+          }
+          mma_commit(acc_full + ab);  // accumulators ready for the epilogue
+        }
+        nx += ares ? nkc : ncb * nkc;
+      }
+    } else if ((warp == 1 || (warp == 3 && tp.dual)) && lane == 0 && TS && NSA) {
       // ---------------------------------------------------------- MMA issuer(s)
       // With alternating epilogue groups (TS) warps 1 and 3 issue the MMAs of even and
       // odd tiles respectively: each tile's operand slots, B stages and accumulator pair
@@ -504,6 +554,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
       double xi = 0.0;
+      // the epilogue's per-row inputs, fetched here off its critical path
+      const int64_t row = t * BM + r;
+      const int own = (hq == 0 && row < p.n) ? __ldg(p.dense + row) : -1;
       for (int xp = 0; xp < xpasses; ++xp) {
         if (myscr && xp > 0) {  // later passes load the stored conversions (producer)
           n1 += nkc;
@@ -578,10 +631,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           bulk_wait_all();
           mbar_arrive(scr_ready);
         }
-        if (xp == 0 && !ext) {  // ||x||^2 halves to the epilogue
+        if (xp == 0) {  // ||x||^2 halves, own cluster and its constants to the epilogue
           const int tb = nt & 1;
+          const double4 co = own >= 0 ? tp.clu[own] : make_double4(1.0, 0.0, 0.0, 0.0);
           TW(6, meta_empty + tb, ((nt >> 1) & 1) ^ 1);
           meta_xi[(tb * 2 + hq) * BM + r] = xi;
+          if (hq == 0) {
+            meta_own[tb * BM + r] = own;
+            meta_clu[tb * BM + r] = co;
+          }
           __syncwarp();
           if (lane == 0) mbar_arrive(meta_full + tb);
         }
@@ -608,18 +666,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       own_n = ok ? __ldg(p.dense + rr) : -1;
       xi_n = ok && tp.xi_rows ? __ldg(tp.xi_rows + rr) : 0.0;
     };
-    fetch(blockIdx.x + (TS ? grp : 0) * static_cast<int64_t>(gridDim.x));
+    if (tp.xi_rows) fetch(blockIdx.x + (TS ? grp : 0) * static_cast<int64_t>(gridDim.x));
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
       const int tb = nt & 1;
       if (TS && tb != grp) continue;  // the other group takes this tile
       const int64_t row = t * BM + r;
       const bool valid = row < p.n;
-      const int own = own_n;
-      double xi64 = xi_n;
-      const double4 co = own >= 0 ? tp.clu[own] : make_double4(1.0, 0.0, 0.0, 0.0);  // n, 1/(n-1), Psi, ||mu||
-      fetch(t + tstep);
-      if (!tp.xi_rows) {
+      int own;
+      double xi64;
+      double4 co;  // n, 1/(n-1), Psi, ||mu||
+      if (tp.xi_rows) {  // the lean converters hand nothing over: prefetched inputs
+        own = own_n;
+        xi64 = xi_n;
+        co = own >= 0 ? tp.clu[own] : make_double4(1.0, 0.0, 0.0, 0.0);
+        fetch(t + tstep);
+      } else {  // the converters' hand-off through shared memory
         TW(7, meta_full + tb, (nt >> 1) & 1);
+        own = meta_own[tb * BM + r];
+        co = meta_clu[tb * BM + r];
         xi64 = meta_xi[(tb * 2) * BM + r] + meta_xi[(tb * 2 + 1) * BM + r];
       }
       const float xi = static_cast<float>(xi64);
