@@ -314,7 +314,7 @@ def main():
                           "global_batch": n_global, "seq_len": D, "parallelism": f"dp{world}",
                           "l2": f"inputs larger than L2 ({N * D * 4 / 1e6:.0f} MB X per GPU)",
                           "path": ["", "ffma", "tcgen05", "fp64"][st["path"]],
-                          "agg_path": ["", "warp-private smem", "label-sorted"][st["agg_path"]]},
+                          "agg_path": ["", "warp-private smem", "label-sorted", "two-phase batches (warp-private smem)"][st["agg_path"]]},
                "dist_evals_per_s": value * K, "mean_silhouette": mean,
                "refined_rows": st["flagged_rows"],
                "phases_ms": {k_: float(np.median(v)) for k_, v in phase.items()},

@@ -75,7 +75,7 @@ typedef struct {
   int32_t d;
   int32_t k;               /* dense clusters */
   int32_t path;            /* fsil_path actually used */
-  int32_t agg_path;        /* 1 = warp-private shared-memory, 2 = label-sorted segments */
+  int32_t agg_path;        /* 1 = warp-private shared-memory, 2 = label-sorted segments, 3 = two-phase batches */
   int64_t flagged_rows;    /* rows re-evaluated by the fp64 argmin refinement kernel */
   int64_t exact_rows;      /* rows whose a_i, b_i were recomputed exactly (tcgen05 path) */
   int64_t kernel_launches; /* kernels launched by the last call */
