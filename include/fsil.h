@@ -80,6 +80,7 @@ typedef struct {
   int64_t exact_rows;      /* rows whose a_i, b_i were recomputed exactly (tcgen05 path) */
   int64_t kernel_launches; /* kernels launched by the last call */
   float ms_densify, ms_aggregate, ms_score, ms_refine, ms_finalize; /* device time, 0 unless timing on */
+  float ms_score_kernel;   /* the scoring kernel alone (ms_score minus its operand preparation) */
 } fsil_stats;
 
 fsil_status fsil_create(fsil_context** ctx, int device);

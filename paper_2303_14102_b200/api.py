@@ -97,7 +97,8 @@ class fsil_stats(ctypes.Structure):
     _fields_ = [("n", _I64), ("d", _I32), ("k", _I32), ("path", _I32), ("agg_path", _I32),
                 ("flagged_rows", _I64), ("exact_rows", _I64), ("kernel_launches", _I64), ("ms_densify", ctypes.c_float),
                 ("ms_aggregate", ctypes.c_float), ("ms_score", ctypes.c_float),
-                ("ms_refine", ctypes.c_float), ("ms_finalize", ctypes.c_float)]
+                ("ms_refine", ctypes.c_float), ("ms_finalize", ctypes.c_float),
+                ("ms_score_kernel", ctypes.c_float)]
 
 
 _lib = None

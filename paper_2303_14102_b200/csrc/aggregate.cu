@@ -597,7 +597,13 @@ __global__ void __launch_bounds__(256) fold_partials_kernel(const double* __rest
   const int64_t j = static_cast<int64_t>(blockIdx.x) * 32 + tx;
   double acc = 0.0;
   if (j < S)
-    for (int b = ty; b < nblocks; b += 8) acc += partials[b * S + j];
+    for (int b0 = ty; b0 < nblocks; b0 += 64) {  // 8 loads in flight, then the same ordered adds
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = b0 + 8 * u < nblocks ? partials[static_cast<int64_t>(b0 + 8 * u) * S + j] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
   sm[ty][tx] = acc;
   __syncthreads();
   if (ty == 0 && j < S) {
@@ -785,6 +791,11 @@ __global__ void __launch_bounds__(256) fold_pieces_kernel(const double* __restri
 __global__ void derive_kernel(const double* __restrict__ stats, int k, int d, int dp, bool cos,
                               float* mu32, float* p32, double* nk, float* bound) {
   const int c = blockIdx.x;
+  if (c >= k) {  // padding clusters up to the 32-multiple: zero operand rows (no memsets)
+    for (int l = threadIdx.x; l < dp; l += blockDim.x) mu32[static_cast<int64_t>(c) * dp + l] = 0.f;
+    if (threadIdx.x == 0) p32[c] = 0.f;
+    return;
+  }
   const double cnt = stats[c];
   const double n = cnt > 0.0 ? cnt : 1.0;
   const double* sums = stats + (cos ? k : 2 * k) + static_cast<int64_t>(c) * d;
@@ -807,6 +818,7 @@ __global__ void derive_kernel(const double* __restrict__ stats, int k, int d, in
     for (int w = 0; w < (blockDim.x + 31) / 32; ++w) tot += red[w];
     nk[c] = cnt;
     atomic_max_nonneg_f32(bound + 0, __double2float_ru(sqrt(tot) * (1.0 + 1e-12)));
+    if (cos) p32[c] = 0.f;
     if (!cos) {
       const double p = stats[k + c] / n;
       p32[c] = static_cast<float>(p);
@@ -823,13 +835,19 @@ int pick_lpr(int d, int vec) {
 }
 
 // stats <- 0, validation word <- none, max|x| <- 0 (one launch instead of three copies)
-__global__ void agg_init_kernel(double* stats, int64_t S, int64_t* checks, float* xmax) {
+__global__ void agg_init_kernel(double* stats, int64_t S, int64_t* checks, float* xmax, float* bound,
+                                double* result, unsigned long long* flag_count, unsigned long long* exact_count) {
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   for (int64_t i = i0; i < S; i += static_cast<int64_t>(gridDim.x) * blockDim.x) stats[i] = 0.0;
   if (i0 == 0) {
     checks[0] = kNone;
     checks[1] = kNone;
     *xmax = 0.f;
+    for (int i = 0; i < 4; ++i) bound[i] = 0.f;  // derive's atomic maxima
+    // the scoring phase's counters and partial result (no separate memsets per call)
+    for (int i = 0; i < 4; ++i) result[i] = 0.0;
+    *flag_count = 0ull;
+    *exact_count = 0ull;
   }
 }
 
@@ -920,8 +938,13 @@ void aggregate(fsil_context* c) {
   int64_t* checks = c->checks.as<int64_t>();
   c->xmax.ensure(sizeof(float));
   c->xi_valid = false;
+  c->bound.ensure(4 * sizeof(float));
+  c->result.ensure(4 * sizeof(double));
+  c->flag_count.ensure(sizeof(unsigned long long));
+  c->exact_count.ensure(sizeof(unsigned long long));
   agg_init_kernel<<<static_cast<unsigned>(std::min<int64_t>((S + 255) / 256 + 1, 1024)), 256, 0, c->stream>>>(
-      stats, S, checks, c->xmax.as<float>());
+      stats, S, checks, c->xmax.as<float>(), c->bound.as<float>(), c->result.as<double>(),
+      c->flag_count.as<unsigned long long>(), c->exact_count.as<unsigned long long>());
   FSIL_LAUNCHED(c);
   if (c->n == 0) {
     c->agg_path = 0;
@@ -1077,10 +1100,8 @@ void derive(fsil_context* c) {
   c->p32.ensure(kpad * sizeof(float));
   c->nk.ensure(kpad * sizeof(double));
   c->bound.ensure(4 * sizeof(float));
-  FSIL_CUDA(cudaMemsetAsync(c->mu32.p, 0, kpad * c->dp * sizeof(float), c->stream));
-  FSIL_CUDA(cudaMemsetAsync(c->p32.p, 0, kpad * sizeof(float), c->stream));
-  FSIL_CUDA(cudaMemsetAsync(c->bound.p, 0, 4 * sizeof(float), c->stream));
-  derive_kernel<<<c->k, 128, 0, c->stream>>>(c->stats_buf.as<double>(), c->k, c->d,
+  // (bound was zeroed by agg_init; padding rows are zeroed by their own blocks)
+  derive_kernel<<<static_cast<unsigned>(kpad), 128, 0, c->stream>>>(c->stats_buf.as<double>(), c->k, c->d,
                                              static_cast<int>(c->dp), cos, c->mu32.as<float>(),
                                              c->p32.as<float>(), c->nk.as<double>(),
                                              c->bound.as<float>());

@@ -35,6 +35,7 @@ void score_tc(fsil_context* c, const ScoreParams& p);
 namespace {
 
 void record(fsil_context* c, int i) {
+  if (i == 3) c->ev7_recorded = false;  // the scoring phase starts: its kernel mark is re-taken
   if (c->timing) FSIL_CUDA(cudaEventRecord(c->ev[i], c->stream));
 }
 
@@ -154,8 +155,7 @@ ScoreParams make_params(fsil_context* c, double* s, int32_t* nb, int32_t* own, d
 
 void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, double* b) {
   if (c->phase < 3) fail(FSIL_ERR_INVALID_ARGUMENT, "aggregate must come before score");
-  c->result.ensure(4 * sizeof(double));
-  FSIL_CUDA(cudaMemsetAsync(c->result.p, 0, 4 * sizeof(double), c->stream));
+  c->result.ensure(4 * sizeof(double));  // zeroed with the counters by agg_init
   c->phase = 4;
   if (c->k < 2 || (c->metric == FSIL_EUCLID && !c->naive_call) || c->n == 0) {  // reported by finish
     record(c, 3); record(c, 4); record(c, 5);
@@ -209,8 +209,7 @@ void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, 
   c->tile_sum.ensure(std::max<int64_t>(ntiles, 1) * sizeof(double));
   c->tile_flag.ensure(std::max<int64_t>(ntiles, 1) * sizeof(int32_t));
   c->flag_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int32_t));
-  c->flag_count.ensure(sizeof(unsigned long long));
-  FSIL_CUDA(cudaMemsetAsync(c->flag_count.p, 0, sizeof(unsigned long long), c->stream));
+  c->flag_count.ensure(sizeof(unsigned long long));  // zeroed by agg_init
   p.tile_sum = c->tile_sum.as<double>();
   p.tile_flag = c->tile_flag.as<int32_t>();
   p.flag_rows = c->flag_rows.as<int32_t>();
@@ -303,6 +302,9 @@ double finish(fsil_context* c, double* flagged_out) {
                     &c->stats.ms_refine, &c->stats.ms_finalize};
     const int from[5] = {0, 1, 3, 4, 5}, to[5] = {1, 2, 4, 5, 6};
     for (int i = 0; i < 5; ++i) FSIL_CUDA(cudaEventElapsedTime(ms[i], c->ev[from[i]], c->ev[to[i]]));
+    // ev[7]: recorded by the scoring launcher right before the scoring kernel itself
+    c->stats.ms_score_kernel = c->stats.ms_score;
+    if (c->ev7_recorded) FSIL_CUDA(cudaEventElapsedTime(&c->stats.ms_score_kernel, c->ev[7], c->ev[4]));
   }
   if (flagged_out) *flagged_out = res[1];
   return res[0] / static_cast<double>(c->n_global);

@@ -437,6 +437,14 @@ __global__ void __launch_bounds__(256) post_kernel(ScoreParams p, const int2* __
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   double* staged = nullptr;
+  // blocks whose warps have no flagged or exact row skip the table (C2: ~70 flagged rows,
+  // i.e. a handful of blocks do any per-row work)
+  if (stage) {
+    const int64_t w0 = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5);
+    const int64_t nflag = static_cast<int64_t>(*p.flag_count);
+    const int64_t nexact = exact_count ? static_cast<int64_t>(*exact_count) : 0;
+    stage = w0 < nflag || w0 * (32 / LPR) < nexact;
+  }
   if (stage) {  // the table in shared memory: its loads overlap the first rows' own
     staged = xs_all + 8 * p.d;
     const double* sums = p.stats + (COS ? p.k : 2 * p.k);
@@ -545,7 +553,7 @@ bool post_fused(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_
   int per_sm = 0;
   FSIL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
   if (per_sm < 1) return false;
-  const int grid = std::min(per_sm, 2) * c->num_sms;  // co-resident: the grid barrier needs it
+  const int grid = c->num_sms;  // co-resident (the grid barrier needs it); one block per SM keeps the barrier short
   ScoreParams pp = p;
   int64_t nt = ntiles;
   int tr = tile_rows;

@@ -182,6 +182,7 @@ struct fsil_context {
   fsil::HostSummary* hsum = nullptr;  // mapped pinned (host view)
   fsil::HostSummary* dsum = nullptr;  // device view of the same memory
   cudaEvent_t ev[8] = {};
+  bool ev7_recorded = false;  // ev[7] marks the scoring kernel's own launch (timing runs)
 };
 
 namespace fsil {

@@ -1026,6 +1026,10 @@ void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, co
                const TcParams& tp, int64_t ntiles) {
   auto kern = tp.dbg ? score_tc_kernel<BN, COS, true, KC> : score_tc_kernel<BN, COS, false, KC>;
   const size_t smem = tc_smem(BN, tp.ncb * BN, tp.nstg + tp.nsa);
+  if (c->timing) {  // the kernel alone, for the roofline (ms_score_kernel)
+    FSIL_CUDA(cudaEventRecord(c->ev[7], c->stream));
+    c->ev7_recorded = true;
+  }
   FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int grid = static_cast<int>(std::min<int64_t>(ntiles, c->num_sms));
   kern<<<grid, kThreads, smem, c->stream>>>(mx, mh, ml, tp, ntiles);
@@ -1126,7 +1130,7 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   if (tp.xi_rows) tp.exic = 1.0f;
   c->exact_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int2));
   c->exact_count.ensure(sizeof(unsigned long long));
-  FSIL_CUDA(cudaMemsetAsync(c->exact_count.p, 0, sizeof(unsigned long long), c->stream));
+  // (exact_count was zeroed by agg_init)
   tp.exact_rows = c->exact_rows.as<int2>();
   tp.exact_count = c->exact_count.as<unsigned long long>();
   const int64_t ntiles = (c->n + BM - 1) / BM;
