@@ -202,6 +202,45 @@ def test_validation_errors_match_reference(ctx):
           np.arange(100) % 3, "sqeuclid")
 
 
+# The two-phase batched aggregation (agg path 3) takes D in {16, 32, 64, 128} with small
+# K*D: batches of 32 (D < 64) or 16 rows, partial last batches, fewer rows than one batch,
+# Psi as an extra accumulated pair (squared Euclidean), and -- on the cosine tcgen05 path --
+# the per-row ||x||^2 it hands to the scoring kernel.
+@pytest.mark.parametrize("n,d,k", [(1003, 32, 12), (517, 128, 9), (10, 64, 3), (33, 16, 2), (4099, 64, 31),
+                                   (20000, 32, 5)])
+@pytest.mark.parametrize("metric", ["sqeuclid", "cosine"])
+def test_batched_aggregation_shapes(ctx, n, d, k, metric):
+    rng = np.random.default_rng(n + 11 * d + k)
+    X = (rng.normal(size=(n, d)) + rng.normal(size=(1, d)) * 2).astype(np.float32)
+    L = rng.integers(0, k, n) * 3 + 5
+    got, _ = check(ctx, X, L, metric)
+    assert ctx.stats()["agg_path"] == 3, "expected the batched aggregation path"
+    if n >= 4000:  # also through the tensor-core scoring kernel (decoupled mode, external ||x||^2)
+        check(ctx, X, L, metric, "tcgen05")
+
+
+def test_batched_aggregation_validation(ctx):
+    """Validation inside the batched path (D = 64): the first non-finite element in
+    row-major order wins (dataset.cpp:35-37); a zero row fails cosine (cos.cpp:119-123)."""
+    from paper_2303_14102_b200 import ValidationError
+    rng = np.random.default_rng(3)
+    X = rng.normal(size=(300, 64)).astype(np.float32)
+    L = np.arange(300) % 4
+    Xb = X.copy()
+    Xb[211, 40] = np.inf
+    Xb[37, 5] = np.nan
+    Xb[37, 63] = np.nan
+    with pytest.raises(ValidationError, match="non-finite feature value at point 37, dimension 5"):
+        ctx.silhouette(Xb, L, "sqeuclid")
+    Xz = X.copy()
+    Xz[150] = 0.0
+    Xz[290] = 0.0
+    with pytest.raises(ValidationError, match=r"cosine distance undefined for zero vector \(point 150\)"):
+        ctx.silhouette(Xz, L, "cosine")
+    got, _ = check(ctx, X, L, "cosine")  # still usable
+    assert ctx.stats()["agg_path"] == 3
+
+
 def test_determinism(ctx):
     rng = np.random.default_rng(9)
     X = rng.normal(size=(50000, 24)).astype(np.float32)
