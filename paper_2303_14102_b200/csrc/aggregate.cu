@@ -447,6 +447,7 @@ __global__ void __launch_bounds__(16 * 32, 1) agg_batch_kernel(
   if (threadIdx.x < 2 * W) sm100::mbar_init(bars + threadIdx.x, 1);
   sm100::fence_barrier_init();
   __syncthreads();
+  griddep_wait();  // (PDL) the set-up above overlaps the predecessor's tail
 
   double* wacc = acc + static_cast<size_t>(warp) * accw;
   int* wcnt = cnt + warp * cntw;
@@ -592,6 +593,7 @@ __global__ void __launch_bounds__(16 * 32, 1) agg_batch_kernel(
 __global__ void __launch_bounds__(256) fold_partials_kernel(const double* __restrict__ partials,
                                                             int nblocks, int64_t S,
                                                             double* __restrict__ stats) {
+  griddep_wait();
   __shared__ double sm[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t j = static_cast<int64_t>(blockIdx.x) * 32 + tx;
@@ -790,6 +792,7 @@ __global__ void __launch_bounds__(256) fold_pieces_kernel(const double* __restri
 // Per-cluster constants of the scoring pass (fp32 operand copies + bounds).
 __global__ void derive_kernel(const double* __restrict__ stats, int k, int d, int dp, bool cos,
                               float* mu32, float* p32, double* nk, float* bound) {
+  griddep_wait();
   const int c = blockIdx.x;
   if (c >= k) {  // padding clusters up to the 32-multiple: zero operand rows (no memsets)
     for (int l = threadIdx.x; l < dp; l += blockDim.x) mu32[static_cast<int64_t>(c) * dp + l] = 0.f;
@@ -837,6 +840,7 @@ int pick_lpr(int d, int vec) {
 // stats <- 0, validation word <- none, max|x| <- 0 (one launch instead of three copies)
 __global__ void agg_init_kernel(double* stats, int64_t S, int64_t* checks, float* xmax, float* bound,
                                 double* result, unsigned long long* flag_count, unsigned long long* exact_count) {
+  griddep_wait();
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   for (int64_t i = i0; i < S; i += static_cast<int64_t>(gridDim.x) * blockDim.x) stats[i] = 0.0;
   if (i0 == 0) {
@@ -875,10 +879,8 @@ void launch_batch(fsil_context* c, int warps, size_t smem, double* partials, int
   if (c->d == DD) {                                                                              \
     auto kern = agg_batch_kernel<COS, DD, DD >= 64 ? 16 : 32>;                                                       \
     FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    kern<<<c->num_sms, warps * 32, smem, c->stream>>>(c->X, c->dense.as<int32_t>(), c->n,         \
-                                                      c->row_offset, c->k, partials, checks,    \
-                                                      c->xmax.as<float>(), c->xi_rows.as<double>()); \
-    FSIL_LAUNCHED(c);                                                                            \
+    launch_pdl(c, kern, c->num_sms, warps * 32, smem, c->X, c->dense.as<int32_t>(), c->n,         \
+               c->row_offset, c->k, partials, checks, c->xmax.as<float>(), c->xi_rows.as<double>()); \
     return;                                                                                      \
   }
   FSIL_AGG_BATCH(16) FSIL_AGG_BATCH(32) FSIL_AGG_BATCH(64) FSIL_AGG_BATCH(128)
@@ -942,10 +944,9 @@ void aggregate(fsil_context* c) {
   c->result.ensure(4 * sizeof(double));
   c->flag_count.ensure(sizeof(unsigned long long));
   c->exact_count.ensure(sizeof(unsigned long long));
-  agg_init_kernel<<<static_cast<unsigned>(std::min<int64_t>((S + 255) / 256 + 1, 1024)), 256, 0, c->stream>>>(
-      stats, S, checks, c->xmax.as<float>(), c->bound.as<float>(), c->result.as<double>(),
-      c->flag_count.as<unsigned long long>(), c->exact_count.as<unsigned long long>());
-  FSIL_LAUNCHED(c);
+  launch_pdl(c, agg_init_kernel, static_cast<unsigned>(std::min<int64_t>((S + 255) / 256 + 1, 1024)), 256, 0, stats,
+             S, checks, c->xmax.as<float>(), c->bound.as<float>(), c->result.as<double>(),
+             c->flag_count.as<unsigned long long>(), c->exact_count.as<unsigned long long>());
   if (c->n == 0) {
     c->agg_path = 0;
     return;
@@ -984,9 +985,8 @@ void aggregate(fsil_context* c) {
       c->partials.ensure(static_cast<size_t>(grid) * S * sizeof(double));
       if (cos) launch_batch<true>(c, W, W * pw, c->partials.as<double>(), checks);
       else launch_batch<false>(c, W, W * pw, c->partials.as<double>(), checks);
-      fold_partials_kernel<<<static_cast<unsigned>((S + 31) / 32), 256, 0, c->stream>>>(
-          c->partials.as<double>(), grid, S, stats);
-      FSIL_LAUNCHED(c);
+      launch_pdl(c, fold_partials_kernel, static_cast<unsigned>((S + 31) / 32), 256, 0, c->partials.as<double>(), grid,
+                 S, stats);
       return;
     }
   }
@@ -1101,11 +1101,9 @@ void derive(fsil_context* c) {
   c->nk.ensure(kpad * sizeof(double));
   c->bound.ensure(4 * sizeof(float));
   // (bound was zeroed by agg_init; padding rows are zeroed by their own blocks)
-  derive_kernel<<<static_cast<unsigned>(kpad), 128, 0, c->stream>>>(c->stats_buf.as<double>(), c->k, c->d,
-                                             static_cast<int>(c->dp), cos, c->mu32.as<float>(),
-                                             c->p32.as<float>(), c->nk.as<double>(),
-                                             c->bound.as<float>());
-  FSIL_LAUNCHED(c);
+  launch_pdl(c, derive_kernel, static_cast<unsigned>(kpad), 128, 0, c->stats_buf.as<double>(), c->k, c->d,
+             static_cast<int>(c->dp), cos, c->mu32.as<float>(), c->p32.as<float>(), c->nk.as<double>(),
+             c->bound.as<float>());
 }
 
 }  // namespace fsil

@@ -416,6 +416,7 @@ fsil_status fsil_create(fsil_context** out, int device) {
     c->num_sms = prop.multiProcessorCount;
     c->smem_optin = prop.sharedMemPerBlockOptin;
     if (const char* e = std::getenv("FSIL_SPECULATE")) c->speculate = std::string(e) != "0";
+    if (const char* e = std::getenv("FSIL_PDL")) c->pdl = std::string(e) != "0";
     if (const char* e = std::getenv("FSIL_DEBUG_SYNC")) c->debug_sync = std::string(e) == "1";
     if (const char* e = std::getenv("FSIL_FUSE_POST")) c->fuse_post = std::string(e) != "0";
     FSIL_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));

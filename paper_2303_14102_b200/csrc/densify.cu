@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(256) densify_collect_kernel(const int32_t* __r
                                                               int64_t chunk, unsigned long long* gkeys,
                                                               unsigned long long* gvals, uint32_t mask,
                                                               uint32_t epoch, int* overflow) {
+  griddep_wait();
   collect_body(labels, n, chunk, gkeys, gvals, mask, epoch, overflow);
 }
 
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(1024) densify_finish_kernel(const unsigned lon
                                                               uint32_t cap, uint32_t epoch, int32_t* sorted_labels,
                                                               int32_t* slot_dense, int* counters, HostSummary* hsum,
                                                               int32_t k_spec = 0, bool spec_big = false) {
+  griddep_wait();
   finish_body(keys, vals, cap, epoch, sorted_labels, slot_dense, counters, hsum, k_spec, spec_big);
 }
 
@@ -229,6 +231,7 @@ __global__ void __launch_bounds__(256) densify_map_kernel(const int32_t* __restr
                                                           const int32_t* __restrict__ slot_dense, uint32_t mask,
                                                           uint32_t epoch, int32_t k_lim, int32_t* dense,
                                                           int* missing) {
+  griddep_wait();
   map_body(labels, n, gkeys, slot_dense, mask, epoch, k_lim, dense, missing);
 }
 
@@ -346,10 +349,8 @@ void launch_collect(fsil_context* c, int64_t cap, uint32_t epoch) {
   if (c->n == 0) return;
   const int grid = grid_for(c->n, 1024, c->num_sms, 2);
   const int64_t chunk = (c->n + grid - 1) / grid;
-  densify_collect_kernel<<<grid, 256, 0, c->stream>>>(c->labels, c->n, chunk, c->ht_keys.as<unsigned long long>(),
-                                                      c->ht_vals.as<unsigned long long>(),
-                                                      static_cast<uint32_t>(cap - 1), epoch, c->counters.as<int>());
-  FSIL_LAUNCHED(c);
+  launch_pdl(c, densify_collect_kernel, grid, 256, 0, c->labels, c->n, chunk, c->ht_keys.as<unsigned long long>(),
+             c->ht_vals.as<unsigned long long>(), static_cast<uint32_t>(cap - 1), epoch, c->counters.as<int>());
 }
 
 }  // namespace
@@ -406,11 +407,9 @@ void densify_local(fsil_context* c) {
     int* counters = c->counters.as<int>();
     const uint32_t mask = static_cast<uint32_t>(cap - 1);
     launch_collect(c, cap, epoch);
-    densify_finish_kernel<<<1, 1024, 0, c->stream>>>(c->ht_keys.as<unsigned long long>(),
-                                                     c->ht_vals.as<unsigned long long>(), static_cast<uint32_t>(cap),
-                                                     epoch, sorted_labels, c->ht_dense.as<int32_t>(), counters,
-                                                     c->dsum, spec ? static_cast<int32_t>(c->k_last) : 0, big);
-    FSIL_LAUNCHED(c);
+    launch_pdl(c, densify_finish_kernel, 1, 1024, 0, c->ht_keys.as<unsigned long long>(),
+               c->ht_vals.as<unsigned long long>(), static_cast<uint32_t>(cap), epoch, sorted_labels,
+               c->ht_dense.as<int32_t>(), counters, c->dsum, spec ? static_cast<int32_t>(c->k_last) : 0, big);
     if (big) {
       c->dict_labels.ensure(cap * sizeof(int32_t));
       c->dict_rows.ensure(cap * sizeof(int64_t));
@@ -427,10 +426,9 @@ void densify_local(fsil_context* c) {
       FSIL_LAUNCHED(c);
     }
     if (c->n > 0) {
-      densify_map_kernel<<<grid_for(c->n, 256, c->num_sms, 8), 256, 0, c->stream>>>(
-          c->labels, c->n, c->ht_keys.as<unsigned long long>(), c->ht_dense.as<int32_t>(), mask, epoch,
-          spec ? static_cast<int32_t>(c->k_last) : INT32_MAX, c->dense.as<int32_t>(), counters + 4);
-      FSIL_LAUNCHED(c);
+      launch_pdl(c, densify_map_kernel, grid_for(c->n, 256, c->num_sms, 8), 256, 0, c->labels, c->n,
+                 c->ht_keys.as<unsigned long long>(), c->ht_dense.as<int32_t>(), mask, epoch,
+                 spec ? static_cast<int32_t>(c->k_last) : INT32_MAX, c->dense.as<int32_t>(), counters + 4);
     }
     if (spec) {
       c->k_spec = true;

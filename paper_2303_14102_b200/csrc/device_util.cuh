@@ -6,6 +6,10 @@
 
 namespace fsil {
 
+// Programmatic dependent launch: wait until the stream predecessor grid has completed
+// and its writes are visible (a no-op when the kernel was launched without PDL).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
   x ^= x >> 16;
   x *= 0x7feb352dU;

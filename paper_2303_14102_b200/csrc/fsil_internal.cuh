@@ -183,9 +183,31 @@ struct fsil_context {
   fsil::HostSummary* dsum = nullptr;  // device view of the same memory
   cudaEvent_t ev[8] = {};
   bool ev7_recorded = false;  // ev[7] marks the scoring kernel's own launch (timing runs)
+  bool pdl = true;             // programmatic dependent launch on the hot chain (FSIL_PDL=0: off)
 };
 
 namespace fsil {
+
+// Launch on the context stream with programmatic dependent launch: the kernel may be
+// scheduled while its stream predecessor drains (hiding the launch gap between the
+// chain's kernels).  Every kernel launched this way calls griddep_wait() before touching
+// memory, so it still observes everything its predecessors wrote.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(fsil_context* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  FSIL_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+  FSIL_LAUNCHED(c);
+}
 
 // kernels.cu entry points (host launchers), all async on ctx->stream
 void densify_collect(fsil_context* c);     // fills ctx->n_distinct (syncs)

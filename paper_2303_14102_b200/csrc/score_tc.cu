@@ -136,6 +136,7 @@ template <int BN, bool COS, bool PROF, int KC>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
                     const __grid_constant__ CUtensorMap tmap_bl, TcParams tp, int64_t ntiles) {
+  griddep_wait();           // (PDL) prep_b's operands and every earlier phase are visible
   if (*tp.p.abort) return;  // K speculation missed: the call is repeated
   using C = TcCfg<BN>;
   constexpr int NB = C::kBStg;
@@ -923,6 +924,7 @@ __global__ void prep_b_kernel(const double* __restrict__ stats, const float* __r
                               const float* __restrict__ xmax, int k, int d, int kp, int dp, bool cos,
                               __half* bh, __half* bl, float* colbias, __half* munorm, double4* clu,
                               TcScale* scale, const int* abort) {
+  griddep_wait();
   if (*abort) return;
   const int c = blockIdx.x;
   const int em = scale_exp(bound[2]);
@@ -1032,8 +1034,7 @@ void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, co
   }
   FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int grid = static_cast<int>(std::min<int64_t>(ntiles, c->num_sms));
-  kern<<<grid, kThreads, smem, c->stream>>>(mx, mh, ml, tp, ntiles);
-  FSIL_LAUNCHED(c);
+  launch_pdl(c, kern, grid, kThreads, smem, mx, mh, ml, tp, ntiles);
 }
 
 }  // namespace
@@ -1064,9 +1065,8 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   __half* munorm = reinterpret_cast<__half*>(colbias + kp);
   double4* clu = reinterpret_cast<double4*>((reinterpret_cast<uintptr_t>(munorm + kp) + 31) & ~uintptr_t(31));
   TcScale* scale = reinterpret_cast<TcScale*>(clu + kp);
-  prep_b_kernel<<<kp, 128, 0, c->stream>>>(p.stats, c->bound.as<float>(), c->xmax.as<float>(), c->k, c->d, kp,
-                                           dp, cos, bh, bl, colbias, munorm, clu, scale, p.abort);
-  FSIL_LAUNCHED(c);
+  launch_pdl(c, prep_b_kernel, kp, 128, 0, p.stats, c->bound.as<float>(), c->xmax.as<float>(), c->k, c->d, kp, dp,
+             cos, bh, bl, colbias, munorm, clu, scale, p.abort);
   const CUtensorMap mx = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, c->X, c->d, c->n, c->d * 4ull, 32, BM);
   const CUtensorMap mh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, bh, dp, kp, dp * 2ull, BK, bn);
   const CUtensorMap ml = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, bl, dp, kp, dp * 2ull, BK, bn);
