@@ -431,6 +431,7 @@ template <bool COS, int LPR>
 __global__ void __launch_bounds__(256) post_kernel(ScoreParams p, const int2* __restrict__ exact_rows,
                                                    const unsigned long long* exact_count, int64_t ntiles,
                                                    int tile_rows, TotalArgs ta, unsigned int* bar, bool stage) {
+  griddep_wait();  // (PDL) the scoring kernel's rows, flags and tile sums are visible
   extern __shared__ double xs_all[];  // [8 warps][d], then (stage) the cluster sums [K][d]
   const bool abort = *p.abort != 0;
   const int lane = threadIdx.x & 31;
@@ -558,7 +559,20 @@ bool post_fused(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_
   int64_t nt = ntiles;
   int tr = tile_rows;
   void* args[] = {&pp, &rows, &cnt, &nt, &tr, &ta, &bar, &stage};
-  FSIL_CUDA(cudaLaunchCooperativeKernel(kern, grid, 256, args, smem, c->stream));
+  // cooperative (co-resident grid for the grid barrier) and, on the hot chain, PDL
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = 256;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  FSIL_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
   FSIL_LAUNCHED(c);
   return true;
 }
