@@ -268,25 +268,27 @@ struct TotalArgs {
   const int* missing;
 };
 
-// One group of 32 tiles by a 256-thread block; true in the block that completed the
-// last of `ngroups` groups (it then sums them: tile_total).
+// One group of kGroupTiles (64) tiles by a 256-thread block -- C2's 7,813 tiles make 123
+// groups, one round over 148 blocks; true in the block that completed the last of
+// `ngroups` groups (it then sums them: tile_total).
+constexpr int kGroupTiles = 64;
 __device__ __forceinline__ bool tile_group_one(const double* __restrict__ tile_sum,
                                                const int32_t* __restrict__ tile_flag, const double* s,
                                                int64_t ntiles, int tile_rows, int64_t n, const TotalArgs& ta,
                                                int64_t g, int64_t ngroups) {
-  __shared__ double sm[32];
-  __shared__ int fl[32];
+  __shared__ double sm[kGroupTiles];
+  __shared__ int fl[kGroupTiles];
   __shared__ bool last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t t0 = g * 32;
-  if (warp == 0) {  // every tile's flag and partial in one round trip
-    const int64_t tt = t0 + lane;
+  const int64_t t0 = g * kGroupTiles;
+  if (threadIdx.x < kGroupTiles) {  // every tile's flag and partial in one round trip
+    const int64_t tt = t0 + threadIdx.x;
     const bool in = tt < ntiles;
-    fl[lane] = in ? tile_flag[tt] : 0;
-    sm[lane] = in ? tile_sum[tt] : 0.0;
+    fl[threadIdx.x] = in ? tile_flag[tt] : 0;
+    sm[threadIdx.x] = in ? tile_sum[tt] : 0.0;
   }
   __syncthreads();
-  for (int j = warp; j < 32; j += 8) {  // tiles that held refined rows: re-sum from s[]
+  for (int j = warp; j < kGroupTiles; j += 8) {  // tiles that held refined rows: re-sum from s[]
     if (!fl[j]) continue;
     const int64_t tt = t0 + j;
     const int64_t r0 = tt * tile_rows, r1 = min(n, r0 + tile_rows);
@@ -297,7 +299,7 @@ __device__ __forceinline__ bool tile_group_one(const double* __restrict__ tile_s
   }
   __syncthreads();
   if (warp == 0) {
-    double v = sm[lane];
+    double v = sm[lane] + sm[lane + 32];  // fixed pairing, then a fixed xor tree
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
     if (lane == 0) {
       ta.group_sum[g] = v;
@@ -457,7 +459,7 @@ __global__ void __launch_bounds__(256) post_kernel(ScoreParams p, const int2* __
     refine_rows<COS>(p, xs_all + static_cast<int64_t>(threadIdx.x >> 5) * p.d, warp, nwarps, lane, staged);
   }
   grid_barrier(bar, bar + 1);
-  const int64_t ngroups = (ntiles + 31) / 32 > 0 ? (ntiles + 31) / 32 : 1;
+  const int64_t ngroups = (ntiles + kGroupTiles - 1) / kGroupTiles > 0 ? (ntiles + kGroupTiles - 1) / kGroupTiles : 1;
   for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x)
     if (tile_group_one(p.tile_sum, p.tile_flag, p.s, ntiles, tile_rows, p.n, ta, g, ngroups)) tile_total(ta, ngroups);
 }
@@ -538,7 +540,7 @@ bool post_fused(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_
   const size_t table = static_cast<size_t>(c->k) * c->d * sizeof(double);
   bool stage = smem + table <= 64 * 1024;  // small tables: staged per block
   if (stage) smem += table;
-  const int64_t ngroups = std::max<int64_t>((ntiles + 31) / 32, 1);
+  const int64_t ngroups = std::max<int64_t>((ntiles + kGroupTiles - 1) / kGroupTiles, 1);
   TotalArgs ta = total_args(c, p, ngroups, local);
   const int2* rows = c->exact_rows.as<int2>();
   const unsigned long long* cnt = c->tc_exact_used ? c->exact_count.as<unsigned long long>() : nullptr;
@@ -578,7 +580,7 @@ bool post_fused(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_
 }
 
 void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows, bool local) {
-  const int64_t ngroups = std::max<int64_t>((ntiles + 31) / 32, 1);
+  const int64_t ngroups = std::max<int64_t>((ntiles + kGroupTiles - 1) / kGroupTiles, 1);
   TotalArgs ta = total_args(c, p, ngroups, local);
   tile_group_kernel<<<static_cast<unsigned>(ngroups), 256, 0, c->stream>>>(p.tile_sum, p.tile_flag, p.s, ntiles,
                                                                          tile_rows, p.n, ta);
