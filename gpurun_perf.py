@@ -17,7 +17,7 @@ for cfg, paths in [('C1', [1, 2]), ('C2', [1, 2]), ('C3', [2]), ('C4', [2]), ('C
         for _ in range(reps): m = ctx.silhouette_device(X, L, metric, s=s, neighbour=nb)
         torch.cuda.synchronize(); dt = (time.time() - t0) / reps
         ctx.set_timing(True); ctx.silhouette_device(X, L, metric, s=s, neighbour=nb); st = ctx.stats(); ctx.set_timing(False)
-        r = dict(ms=dt * 1e3, pts_per_s=n / dt, mean=m[0], **{k: st[k] for k in ('path', 'agg_path', 'flagged_rows', 'exact_rows', 'kernel_launches', 'ms_densify', 'ms_aggregate', 'ms_score', 'ms_refine', 'ms_finalize')})
+        r = dict(ms=dt * 1e3, pts_per_s=n / dt, mean=m[0], **{k: st[k] for k in ('path', 'agg_path', 'flagged_rows', 'exact_rows', 'kernel_launches', 'ms_densify', 'ms_aggregate', 'ms_score', 'ms_refine', 'ms_finalize', 'ms_score_kernel')})
         res[f'{cfg}_p{path}'] = r
         print(cfg, path, json.dumps(r), flush=True)
     del X, L, s, nb
