@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT"
+for rep in 1 2; do
+for lib in ab/libfsil_prev.so paper_2303_14102_b200/libfsil.so; do
+  FSIL_LIB_PATH=$PWD/$lib timeout 300 python tools/gpurun/gpurun_phases.py C2 2>&1 | sed "s|^|$lib |"
+done; done
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
