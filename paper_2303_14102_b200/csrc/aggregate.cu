@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(256) agg_piece_kernel(
     const T* __restrict__ X, const int32_t* __restrict__ rows, int64_t n, int d,
     int64_t row_offset, int k, int lpr, const int64_t* __restrict__ seg_begin,
     const int64_t* __restrict__ seg_end, const int64_t* __restrict__ piece_start,
-    double* __restrict__ piece_out, int64_t* checks, float* xmax) {
+    double* __restrict__ piece_out, int64_t* checks, float* xmax, double* __restrict__ xi_out) {
   const int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t total = piece_start[k];
@@ -708,8 +708,14 @@ __global__ void __launch_bounds__(256) agg_piece_kernel(
         }
     }
     double scale = 1.0;
+    if (!COS && xi_out) {  // the row's exact ||x||^2 for the scoring pass (Psi keeps the partials)
+      double sr = ss;
+      for (int off = lpr >> 1; off > 0; off >>= 1) sr += __shfl_xor_sync(0xffffffffu, sr, off, lpr);
+      if (valid && li == 0) xi_out[r] = sr;
+    }
     if (COS) {
       for (int off = lpr >> 1; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off, lpr);
+      if (valid && li == 0 && xi_out) xi_out[r] = ss;
       if (!valid) continue;
       if (ss == 0.0) {
         if (li == 0) atomic_min_i64(checks + 1, row_offset + r);
@@ -915,7 +921,7 @@ void launch_pieces(fsil_context* c, const T* X, int vec, int cpl, int64_t max_pi
   if (vec == V && cpl == C) {                                                                    \
     agg_piece_kernel<COS, V, C, T><<<grid, 256, 0, c->stream>>>(                                 \
         X, rows, c->n, c->d, c->row_offset, c->k, lpr, seg_begin, seg_end, piece_start,          \
-        piece_out, checks, c->xmax.as<float>());                                                 \
+        piece_out, checks, c->xmax.as<float>(), sizeof(T) == 4 ? c->xi_rows.as<double>() : nullptr); \
     FSIL_LAUNCHED(c);                                                                            \
     return;                                                                                      \
   }
@@ -1037,6 +1043,10 @@ void aggregate(fsil_context* c) {
 
   // Path 2: label-sorted segments.
   if (c->n >= (int64_t(1) << 31)) fail(FSIL_ERR_INVALID_ARGUMENT, "shard too large for the sorted aggregation path (2^31 rows)");
+  if (!x64) {  // exact per-row ||x||^2 (fp64) for the scoring pass
+    c->xi_rows.ensure(static_cast<size_t>(c->n) * sizeof(double));
+    c->xi_valid = true;
+  }
   const int cpl_max = vec == 4 ? 8 : 32;
   if (cpl > cpl_max)
     fail(FSIL_ERR_INVALID_ARGUMENT, "feature dimension too large for this build (D <= 1024)");

@@ -72,6 +72,7 @@ struct TcParams {
   float exic;             // ||x||^2 relative error / u: 8.1 (fp32 blocks of 8), +2.1 on fp64 input
   const double* xi_rows;  // per-row fp64 ||x||^2 from the aggregation pass (or null: converters form it)
   long long* trace;       // FSIL_TRACE builds: per-tile role timestamps of CTA 0 (or null)
+  int lean;               // converters only convert; the epilogue fetches own/clu/||x||^2 itself
 };
 
 // Timeline tracing (compile with -DFSIL_TRACE, run with FSIL_TC_TRACE=1): CTA 0 records
@@ -453,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t ph1 = 0;  // (n1 / NS) & 1
     // ext: ||x||^2 comes from the aggregation pass and the epilogue fetches its per-row
     // inputs itself -- the converters only convert (no norm, no meta hand-off)
-    const bool ext = tp.xi_rows != nullptr;
+    const bool ext = tp.lean != 0;
     if (NSA) {
       // decoupled: stage -> registers -> free the stage -> convert into an A slot
       const uint32_t rd = hq * (BM * 128) + r * 128, wr = r * 128;
@@ -586,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int j = 4 * hq + jj;
             const float v[8] = {f[2 * jj].x,     f[2 * jj].y,     f[2 * jj].z,     f[2 * jj].w,
                                 f[2 * jj + 1].x, f[2 * jj + 1].y, f[2 * jj + 1].z, f[2 * jj + 1].w};
-            if (xp == 0 && !ext) {  // ||x||^2: fp32 blocks of 8 (error <= 8u each), fp64 across blocks
+            if (xp == 0 && !tp.xi_rows) {  // ||x||^2: fp32 blocks of 8 (error <= 8u each), fp64 across blocks
               float2 bs = make_float2(0.f, 0.f);
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
@@ -667,7 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       own_n = ok ? __ldg(p.dense + rr) : -1;
       xi_n = ok && tp.xi_rows ? __ldg(tp.xi_rows + rr) : 0.0;
     };
-    if (tp.xi_rows) fetch(blockIdx.x + (TS ? grp : 0) * static_cast<int64_t>(gridDim.x));
+    if (tp.lean) fetch(blockIdx.x + (TS ? grp : 0) * static_cast<int64_t>(gridDim.x));
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
       const int tb = nt & 1;
       if (TS && tb != grp) continue;  // the other group takes this tile
@@ -676,7 +677,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int own;
       double xi64;
       double4 co;  // n, 1/(n-1), Psi, ||mu||
-      if (tp.xi_rows) {  // the lean converters hand nothing over: prefetched inputs
+      // ||x||^2 from the aggregation pass (exact fp64) when it wrote one, issued early
+      const double xi_g = (!tp.lean && tp.xi_rows && valid) ? __ldg(tp.xi_rows + row) : 0.0;
+      if (tp.lean) {  // the lean converters hand nothing over: prefetched inputs
         own = own_n;
         xi64 = xi_n;
         co = own >= 0 ? tp.clu[own] : make_double4(1.0, 0.0, 0.0, 0.0);
@@ -685,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         TW(7, meta_full + tb, (nt >> 1) & 1);
         own = meta_own[tb * BM + r];
         co = meta_clu[tb * BM + r];
-        xi64 = meta_xi[(tb * 2) * BM + r] + meta_xi[(tb * 2 + 1) * BM + r];
+        xi64 = tp.xi_rows ? xi_g : meta_xi[(tb * 2) * BM + r] + meta_xi[(tb * 2 + 1) * BM + r];
       }
       const float xi = static_cast<float>(xi64);
       const float xn = COS ? 0.0f : sqrtf(xi);
@@ -780,7 +783,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar(1, 256);
         if (grp == 1) {
           __syncwarp();
-          if (lane == 0 && !tp.xi_rows) mbar_arrive(meta_empty + tb);
+          if (lane == 0 && !tp.lean) mbar_arrive(meta_empty + tb);
           continue;
         }
         const float c1 = pt[0 * BM + r], c2 = pt[1 * BM + r];
@@ -793,7 +796,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         doto = (doto == doto) ? doto : d2;
       }
       __syncwarp();
-      if (lane == 0 && !tp.xi_rows) mbar_arrive(meta_empty + tb);
+      if (lane == 0 && !tp.lean) mbar_arrive(meta_empty + tb);
 
       // ---- certification and a_i, b_i, s_i.  Cosine in fp32: the inputs (tensor-core
       // dots) carry fp32-level certified errors already, the fp32 evaluation adds its
@@ -1093,7 +1096,7 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
       const char* e = std::getenv("FSIL_TC_DECOUPLE");
       return e ? std::atoi(e) : 1;
     }();
-    if (dec_env && ncb == 1 && c->xi_valid && !c->X64 && tp.nstg >= 4) {
+    if (dec_env && ncb == 1 && c->xi_valid && c->agg_path == 3 && !c->X64 && tp.nstg >= 4) {
       tp.nsa = 2;
       tp.nstg -= 2;
     }
@@ -1128,6 +1131,9 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   // rounding (0.5u) remains in the bounds
   tp.xi_rows = c->xi_valid && !c->X64 ? c->xi_rows.as<double>() : nullptr;
   if (tp.xi_rows) tp.exic = 1.0f;
+  // lean converters: only where the batched aggregation wrote ||x||^2 (C1/C2-like shapes);
+  // the label-sorted path's ||x||^2 goes to the epilogue through the usual hand-off
+  tp.lean = tp.xi_rows && c->agg_path == 3 ? 1 : 0;
   c->exact_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int2));
   c->exact_count.ensure(sizeof(unsigned long long));
   // (exact_count was zeroed by agg_init)
