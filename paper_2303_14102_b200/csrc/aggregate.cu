@@ -708,14 +708,9 @@ __global__ void __launch_bounds__(256) agg_piece_kernel(
         }
     }
     double scale = 1.0;
-    if (!COS && xi_out) {  // the row's exact ||x||^2 for the scoring pass (Psi keeps the partials)
-      double sr = ss;
-      for (int off = lpr >> 1; off > 0; off >>= 1) sr += __shfl_xor_sync(0xffffffffu, sr, off, lpr);
-      if (valid && li == 0) xi_out[r] = sr;
-    }
     if (COS) {
       for (int off = lpr >> 1; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off, lpr);
-      if (valid && li == 0 && xi_out) xi_out[r] = ss;
+      if (valid && li == 0 && xi_out) xi_out[r] = ss;  // exact ||x||^2 for the scoring pass (cosine)
       if (!valid) continue;
       if (ss == 0.0) {
         if (li == 0) atomic_min_i64(checks + 1, row_offset + r);
@@ -921,7 +916,7 @@ void launch_pieces(fsil_context* c, const T* X, int vec, int cpl, int64_t max_pi
   if (vec == V && cpl == C) {                                                                    \
     agg_piece_kernel<COS, V, C, T><<<grid, 256, 0, c->stream>>>(                                 \
         X, rows, c->n, c->d, c->row_offset, c->k, lpr, seg_begin, seg_end, piece_start,          \
-        piece_out, checks, c->xmax.as<float>(), sizeof(T) == 4 ? c->xi_rows.as<double>() : nullptr); \
+        piece_out, checks, c->xmax.as<float>(), c->xi_valid ? c->xi_rows.as<double>() : nullptr); \
     FSIL_LAUNCHED(c);                                                                            \
     return;                                                                                      \
   }
@@ -1043,7 +1038,11 @@ void aggregate(fsil_context* c) {
 
   // Path 2: label-sorted segments.
   if (c->n >= (int64_t(1) << 31)) fail(FSIL_ERR_INVALID_ARGUMENT, "shard too large for the sorted aggregation path (2^31 rows)");
-  if (!x64) {  // exact per-row ||x||^2 (fp64) for the scoring pass
+  // exact per-row ||x||^2 (fp64) for the scoring pass -- cosine only: there the sorted
+  // pieces reduce each row's norm anyway, while for squared Euclidean the extra per-row
+  // reduction and scattered 8-byte writes cost more than they save (measured: C3
+  // aggregation 1.58 -> 3.74 ms, C4 5.7 -> 9.2 ms)
+  if (!x64 && cos) {
     c->xi_rows.ensure(static_cast<size_t>(c->n) * sizeof(double));
     c->xi_valid = true;
   }
