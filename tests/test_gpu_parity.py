@@ -250,6 +250,26 @@ def test_determinism(ctx):
     assert np.array_equal(r1.s, r2.s) and r1.mean == r2.mean and np.array_equal(r1.neighbour, r2.neighbour)
 
 
+def test_determinism_batched_tcgen05_and_timing(ctx):
+    """The C2-shaped path (batched aggregation, decoupled tcgen05 scoring, PDL chain):
+    bit-identical across calls, and the per-phase timers (bench.py's roofline input)
+    report the scoring kernel alone inside the scoring phase."""
+    rng = np.random.default_rng(21)
+    X = (rng.normal(size=(60000, 64)) + rng.normal(size=(1, 64))).astype(np.float32)
+    L = rng.integers(0, 20, 60000)
+    ctx.set_path(PATHS["tcgen05"])
+    r1 = ctx.silhouette(X, L, "cosine")
+    ctx.set_timing(True)
+    r2 = ctx.silhouette(X, L, "cosine")
+    st = ctx.stats()
+    ctx.set_timing(False)
+    ctx.set_path(0)
+    assert np.array_equal(r1.s, r2.s) and r1.mean == r2.mean and np.array_equal(r1.neighbour, r2.neighbour)
+    assert st["agg_path"] == 3 and st["path"] == PATHS["tcgen05"]
+    assert 0.0 < st["ms_score_kernel"] <= st["ms_score"]
+    assert all(st[k] > 0.0 for k in ("ms_densify", "ms_aggregate", "ms_refine"))
+
+
 def _config(ctx, name, n=None):
     from paper_2303_14102_b200 import datagen
     X, L, metric = datagen.generate_host(name, n=n)
