@@ -133,7 +133,9 @@ static_assert(4 * FSIL_WG0_REGS + 8 * FSIL_EPI_REGS + 8 * FSIL_CONV_REGS <= 20 *
 
 // KC: columns of each 32-column chunk the epilogue scans (BN = 32 with K <= 24 skips
 // the padding columns; otherwise 32)
-template <int BN, bool COS, bool PROF, int KC>
+// EG: epilogue groups.  3 only in decoupled mode at BN = 32 (C2): warps 4..15 are three
+// groups of four taking tiles round-robin, warps 16..19 the converters (one row each).
+template <int BN, bool COS, bool PROF, int KC, int EG = 2>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
                     const __grid_constant__ CUtensorMap tmap_bl, TcParams tp, int64_t ntiles) {
@@ -149,6 +151,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // pieces into one of NSA separate operand slots that the MMA commit frees -- the X
   // stages only cover TMA latency instead of being held through conversion and MMA.
   const int NSA = tp.nsa;
+  constexpr int kConv0 = kEpiWarp0 + 4 * EG;  // first converter warp
+  constexpr int kConvWarps = 20 - kConv0;     // 8 (EG = 2) or 4 (EG = 3)
   // TS: the two epilogue groups take alternate tiles, each with its own pair of
   // accumulator buffers, so consecutive tiles' epilogues overlap -- for tiles of at
   // most two cluster blocks (with more, the MMA stream would serialise on one
@@ -187,18 +191,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* a_empty = stg_empty + NS;      // decoupled: [NSA] A slot free (MMA commit); NS + NSA <= 8
   uint64_t* b_full = bars + 24;            // [NB]
   uint64_t* b_empty = bars + 28;           // [NB]
-  uint64_t* acc_full = bars + 32;          // [4]
-  uint64_t* acc_empty = bars + 36;         // [4]
-  uint64_t* meta_full = bars + 40;         // [2]
-  uint64_t* meta_empty = bars + 42;        // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 44);
-  uint64_t* scr_ready = bars + 45;         // [1] a tile's converted chunks are in scratch
-  double* meta_xi = reinterpret_cast<double*>(bars + 46);   // [2][2][BM] ||x||^2 halves
+  uint64_t* acc_full = bars + 32;          // [6]
+  uint64_t* acc_empty = bars + 38;         // [6]
+  uint64_t* meta_full = bars + 44;         // [2]
+  uint64_t* meta_empty = bars + 46;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 48);
+  uint64_t* scr_ready = bars + 49;         // [1] a tile's converted chunks are in scratch
+  double* meta_xi = reinterpret_cast<double*>(bars + 50);   // [2][2][BM] ||x||^2 halves
   double4* meta_clu = reinterpret_cast<double4*>(meta_xi + 4 * BM);  // [2][BM] clu[own] per row
   float* part = reinterpret_cast<float*>(meta_clu + 2 * BM);  // [2][4][BM] second-half partial top-2
-  double* red = reinterpret_cast<double*>(part + 8 * BM);     // [2][4] tile-sum partials
-  int* red_flag = reinterpret_cast<int*>(red + 8);            // [2][4]
-  int* meta_own = reinterpret_cast<int*>(red + 12);           // [2][BM] own cluster per row
+  double* red = reinterpret_cast<double*>(part + 8 * BM);     // [3][4] tile-sum partials
+  int* red_flag = reinterpret_cast<int*>(red + 12);           // [3][4]
+  int* meta_own = reinterpret_cast<int*>(red + 18);           // [2][BM] own cluster per row
   float* cb_s = reinterpret_cast<float*>(meta_own + 2 * BM);  // [ncb*BN] column bias
   __half* mn_s = reinterpret_cast<__half*>(cb_s + ncb_bn_pad(tp.ncb * BN));  // [ncb*BN] ||mu_k||/mu_max, rounded up
 
@@ -215,15 +219,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(stg_full + i, 1);
-      mbar_init(stg_empty + i, NSA ? 8 : 1);
-      mbar_init(a_full + i, myscr ? 1 : 8);
+      mbar_init(stg_empty + i, NSA ? kConvWarps : 1);
+      mbar_init(a_full + i, myscr ? 1 : kConvWarps);
     }
     for (int i = 0; i < NSA; ++i) mbar_init(a_empty + i, 1);
     for (int i = 0; i < NB; ++i) {
       mbar_init(b_full + i, 1);
       mbar_init(b_empty + i, 1);
     }
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 2 * EG; ++i) {
       mbar_init(acc_full + i, 1);
       mbar_init(acc_empty + i, TS ? 4 : 8);
     }
@@ -359,12 +363,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           ph ^= 1u;
         }
       };
-      uint32_t na = 0, ng0 = 0, ng1 = 0, nt = 0;
+      uint32_t na = 0, nt = 0, ngc[EG] = {};
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
         const bool mine = !dual || (nt & 1u) == iid;
         if (!mine) {  // the other issuer's tile: advance the counters only
-          if (nt & 1) ng1 += ncb;
-          else ng0 += ncb;
+          ngc[nt % EG] += ncb;
           na += ncb;
           adv(b_s, b_ph, NB, ncb * nkc);
           adv(a_s, a_ph, NA, ares ? nkc : ncb * nkc);
@@ -376,12 +379,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           int ab;
           uint32_t ph;
           if (TS) {
-            const int g = nt & 1;
-            const uint32_t cnt = g ? ng1 : ng0;  // per-group buffer-pair counters
+            const int g = static_cast<int>(nt % EG);
+            const uint32_t cnt = ngc[g];  // per-group buffer-pair counters
             ab = 2 * g + (cnt & 1);
             ph = (cnt >> 1) & 1;
-            ng0 += g ? 0u : 1u;
-            ng1 += g ? 1u : 0u;
+            ++ngc[g];
           } else {
             ab = na % nacc;
             ph = (na / nacc) & 1;
@@ -439,13 +441,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         a_ph = ph_end;
       }
     }
-  } else if (warp >= kConvWarp0) {
-    if (FSIL_CONV_REGS != 96) setmaxnreg_dec<FSIL_CONV_REGS>();
+  } else if (warp >= kConv0) {
+    constexpr int kConvRegs = EG == 3 ? 56 : FSIL_CONV_REGS;
+    static_assert(4 * FSIL_WG0_REGS + 12 * 120 + 4 * 56 <= 20 * 96, "EG = 3 register split exceeds the pool");
+    if (kConvRegs != 96) setmaxnreg_dec<kConvRegs>();
     // ------------------------------------------------------------ converters (8 warps:
     // two threads per row; thread half hq reads fp32 box hq of the stage, then -- after
     // the whole group has read -- writes A chunks 4hq..4hq+3 of hi (over box 0) and lo
     // (over box 1))
-    const int tl = threadIdx.x - kConvWarp0 * 32;
+    const int tl = threadIdx.x - kConv0 * 32;
     const int r = tl & (BM - 1), hq = tl >> 7;  // row in tile, box / chunk half
     const int sw = r & 7;
     const float2 sx2 = make_float2(sc.sx, sc.sx), neg1 = make_float2(-1.f, -1.f);
@@ -455,7 +459,64 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ext: ||x||^2 comes from the aggregation pass and the epilogue fetches its per-row
     // inputs itself -- the converters only convert (no norm, no meta hand-off)
     const bool ext = tp.lean != 0;
-    if (NSA) {
+    if (EG == 3) {
+      // decoupled, four converter warps (one thread per row, both 32-column boxes in
+      // turn, two 16-byte units at a time -- 56 registers): wait for the stage and a free
+      // A slot, convert, then free the stage and publish the slot
+      const uint32_t wr = r * 128;
+      int sa = 0;
+      uint32_t pha = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kc = 0; kc < nkc; ++kc) {
+          mbar_wait(stg_full + s1, ph1);
+          mbar_wait(a_empty + sa, pha ^ 1);
+          const uint8_t* sbase = stg + s1 * kStgBytes;
+          uint8_t* abase = aslot + sa * kStgBytes;
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            const bool absent = h == 1 && kc * BK + 32 >= p.d;  // box 1 of the last chunk
+            const uint8_t* srow = sbase + h * (BM * 128) + r * 128;
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              float4 f0 = *reinterpret_cast<const float4*>(srow + (((2 * jj) ^ sw) << 4));
+              float4 f1 = *reinterpret_cast<const float4*>(srow + (((2 * jj + 1) ^ sw) << 4));
+              if (absent) {
+                f0 = make_float4(0.f, 0.f, 0.f, 0.f);
+                f1 = f0;
+              }
+              const float v[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+              uint32_t hw[4], lw[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 xx = __fmul2_rn(make_float2(v[2 * e], v[2 * e + 1]), sx2);
+                const __half2 hh = __float22half2_rn(xx);
+                const float2 res = __ffma2_rn(__half22float2(hh), neg1, xx);  // exact
+                const __half2 l = __float22half2_rn(res);
+                hw[e] = *reinterpret_cast<const uint32_t*>(&hh);
+                lw[e] = *reinterpret_cast<const uint32_t*>(&l);
+              }
+              const uint32_t pos = wr + (((4 * h + jj) ^ sw) << 4);
+              *reinterpret_cast<uint4*>(abase + pos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+              *reinterpret_cast<uint4*>(abase + BM * 128 + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(stg_empty + s1);  // the stage has been read
+            mbar_arrive(a_full + sa);
+          }
+          if (++s1 == NS) {
+            s1 = 0;
+            ph1 ^= 1;
+          }
+          if (++sa == NSA) {
+            sa = 0;
+            pha ^= 1;
+          }
+        }
+      }
+    } else if (NSA) {
       // decoupled: stage -> registers -> free the stage -> convert into an A slot
       const uint32_t rd = hq * (BM * 128) + r * 128, wr = r * 128;
       const bool tail_box = hq == 1;
@@ -464,7 +525,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         for (int kc = 0; kc < nkc; ++kc) {
           mbar_wait(stg_full + s1, ph1);
-          if (warp == kConvWarp0) TRACE((t - blockIdx.x) / gridDim.x, 1);
+          if (warp == kConv0) TRACE((t - blockIdx.x) / gridDim.x, 1);
           const uint8_t* sbase = stg + s1 * kStgBytes;
           float4 f[8];
 #pragma unroll
@@ -502,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) mbar_arrive(a_full + sa);
-          if (warp == kConvWarp0) TRACE((t - blockIdx.x) / gridDim.x, 2);
+          if (warp == kConv0) TRACE((t - blockIdx.x) / gridDim.x, 2);
           if (++sa == NSA) {
             sa = 0;
             pha ^= 1;
@@ -649,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue (8 warps)
-    setmaxnreg_inc<FSIL_EPI_REGS>();  // CTA pool: see the static_assert above
+    setmaxnreg_inc<EG == 3 ? 120 : FSIL_EPI_REGS>();  // CTA pool: see the static_asserts
     const int quad = warp & 3;                // TMEM lane quadrant of this warp
     const int r = quad * 32 + lane;           // row in tile
     const int grp = (warp - kEpiWarp0) >> 2;  // epilogue group 0 / 1
@@ -659,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // fetched from global memory one tile ahead of their use, so their DRAM latency
     // overlaps the current tile instead of serialising with it; clu[own] (L2) is issued
     // at the start of the tile and first used after the scan.
-    const int64_t tstep = (TS ? 2 : 1) * static_cast<int64_t>(gridDim.x);
+    const int64_t tstep = (TS ? EG : 1) * static_cast<int64_t>(gridDim.x);
     int own_n = -1;
     double xi_n = 0.0;
     auto fetch = [&](int64_t tt) {
@@ -671,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tp.lean) fetch(blockIdx.x + (TS ? grp : 0) * static_cast<int64_t>(gridDim.x));
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
       const int tb = nt & 1;
-      if (TS && tb != grp) continue;  // the other group takes this tile
+      if (TS && static_cast<int>(nt % EG) != grp) continue;  // another group takes this tile
       const int64_t row = t * BM + r;
       const bool valid = row < p.n;
       int own;
@@ -891,15 +952,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       // partial slots double-buffered by tile parity
       for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
       const unsigned anyw = __ballot_sync(0xffffffffu, any);
+      const int rs = TS ? grp : tb;  // tile-sum slot: per group (alternating tiles) or per parity
       if (lane == 0) {
-        red[tb * 4 + quad] = s;
-        red_flag[tb * 4 + quad] = anyw != 0;
+        red[rs * 4 + quad] = s;
+        red_flag[rs * 4 + quad] = anyw != 0;
       }
       named_bar(2 + grp, 128);
       if (dbgp && warp == kEpiWarp0 && lane == 0) atomicAdd(dbgp + 13, static_cast<unsigned long long>(clock64() - tf0));
       if (quad == 0 && lane == 0) {
-        p.tile_sum[t] = ((red[tb * 4] + red[tb * 4 + 1]) + red[tb * 4 + 2]) + red[tb * 4 + 3];
-        p.tile_flag[t] = red_flag[tb * 4] | red_flag[tb * 4 + 1] | red_flag[tb * 4 + 2] | red_flag[tb * 4 + 3];
+        p.tile_sum[t] = ((red[rs * 4] + red[rs * 4 + 1]) + red[rs * 4 + 2]) + red[rs * 4 + 3];
+        p.tile_flag[t] = red_flag[rs * 4] | red_flag[rs * 4 + 1] | red_flag[rs * 4 + 2] | red_flag[rs * 4 + 3];
         TRACE(nt, 7);
       }
     }
@@ -908,7 +970,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (dbgp && lane == 0) {
     if (warp == 0) atomicAdd(dbgp + 9, static_cast<unsigned long long>(clock64() - t_start));
     if (warp == kEpiWarp0) atomicAdd(dbgp + 10, static_cast<unsigned long long>(clock64() - t_start));
-    if (warp == kConvWarp0) atomicAdd(dbgp + 11, static_cast<unsigned long long>(clock64() - t_start));
+    if (warp == kConv0) atomicAdd(dbgp + 11, static_cast<unsigned long long>(clock64() - t_start));
   }
   tc_fence_before();
   __syncthreads();
@@ -1015,7 +1077,7 @@ int pick_bn(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : 128; }
 // meta_xi, merge partials, tile-sum slots, column bias (fp32) and norms (fp16).
 size_t tc_smem(int bn, int kp, int nstg) {
   const size_t bring = bn <= 32 ? TcCfg<32>::kBRing : bn <= 64 ? TcCfg<64>::kBRing : TcCfg<128>::kBRing;
-  return 1024 + bring + static_cast<size_t>(nstg) * kStgBytes + 46 * 8 + 4 * BM * 8 + 2 * BM * 32 + 8 * BM * 4 +
+  return 1024 + bring + static_cast<size_t>(nstg) * kStgBytes + 50 * 8 + 4 * BM * 8 + 2 * BM * 32 + 8 * BM * 4 + 48 +
          128 + 2 * BM * 4 +
          static_cast<size_t>(ncb_bn_pad(kp)) * 4 + static_cast<size_t>(kp) * 2 + 16;
 }
@@ -1026,10 +1088,10 @@ int tc_stages(int bn, int kp, size_t optin) {
   return ns;
 }
 
-template <int BN, bool COS, int KC = 32>
+template <int BN, bool COS, int KC = 32, int EG = 2>
 void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                const TcParams& tp, int64_t ntiles) {
-  auto kern = tp.dbg ? score_tc_kernel<BN, COS, true, KC> : score_tc_kernel<BN, COS, false, KC>;
+  auto kern = tp.dbg ? score_tc_kernel<BN, COS, true, KC, EG> : score_tc_kernel<BN, COS, false, KC, EG>;
   const size_t smem = tc_smem(BN, tp.ncb * BN, tp.nstg + tp.nsa);
   if (c->timing) {  // the kernel alone, for the roofline (ms_score_kernel)
     FSIL_CUDA(cudaEventRecord(c->ev[7], c->stream));
@@ -1156,14 +1218,26 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   tp.trace = trc;
   // K <= 24 at BN = 32: the epilogue scans only the first 16 / 24 columns
   const int kc_scan = bn == 32 && c->k <= 16 ? 16 : bn == 32 && c->k <= 24 ? 24 : 32;
+  // three epilogue groups (decoupled mode at BN = 32, where the epilogue paces the kernel)
+  static const bool eg3_env = [] {
+    const char* e = std::getenv("FSIL_TC_EG3");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool eg3 = eg3_env && bn == 32 && tp.nsa > 0;
   if (cos) {
-    if (bn == 32 && kc_scan == 16) launch_tc<32, true, 16>(c, mx, mh, ml, tp, ntiles);
+    if (eg3 && kc_scan == 16) launch_tc<32, true, 16, 3>(c, mx, mh, ml, tp, ntiles);
+    else if (eg3 && kc_scan == 24) launch_tc<32, true, 24, 3>(c, mx, mh, ml, tp, ntiles);
+    else if (eg3) launch_tc<32, true, 32, 3>(c, mx, mh, ml, tp, ntiles);
+    else if (bn == 32 && kc_scan == 16) launch_tc<32, true, 16>(c, mx, mh, ml, tp, ntiles);
     else if (bn == 32 && kc_scan == 24) launch_tc<32, true, 24>(c, mx, mh, ml, tp, ntiles);
     else if (bn == 32) launch_tc<32, true>(c, mx, mh, ml, tp, ntiles);
     else if (bn == 64) launch_tc<64, true>(c, mx, mh, ml, tp, ntiles);
     else launch_tc<128, true>(c, mx, mh, ml, tp, ntiles);
   } else {
-    if (bn == 32 && kc_scan == 16) launch_tc<32, false, 16>(c, mx, mh, ml, tp, ntiles);
+    if (eg3 && kc_scan == 16) launch_tc<32, false, 16, 3>(c, mx, mh, ml, tp, ntiles);
+    else if (eg3 && kc_scan == 24) launch_tc<32, false, 24, 3>(c, mx, mh, ml, tp, ntiles);
+    else if (eg3) launch_tc<32, false, 32, 3>(c, mx, mh, ml, tp, ntiles);
+    else if (bn == 32 && kc_scan == 16) launch_tc<32, false, 16>(c, mx, mh, ml, tp, ntiles);
     else if (bn == 32 && kc_scan == 24) launch_tc<32, false, 24>(c, mx, mh, ml, tp, ntiles);
     else if (bn == 32) launch_tc<32, false>(c, mx, mh, ml, tp, ntiles);
     else if (bn == 64) launch_tc<64, false>(c, mx, mh, ml, tp, ntiles);
