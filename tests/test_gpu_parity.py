@@ -215,8 +215,9 @@ def test_batched_aggregation_shapes(ctx, n, d, k, metric):
     L = rng.integers(0, k, n) * 3 + 5
     got, _ = check(ctx, X, L, metric)
     assert ctx.stats()["agg_path"] == 3, "expected the batched aggregation path"
-    if n >= 4000:  # also through the tensor-core scoring kernel (decoupled mode, external ||x||^2)
-        check(ctx, X, L, metric, "tcgen05")
+    # also through the tensor-core scoring kernel: decoupled mode with external ||x||^2 and
+    # three epilogue groups at BN = 32 (D = 16: the second box absent; D = 128: two chunks)
+    check(ctx, X, L, metric, "tcgen05")
 
 
 def test_batched_aggregation_validation(ctx):
