@@ -475,16 +475,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* abase = aslot + sa * kStgBytes;
 #pragma unroll 1
           for (int h = 0; h < 2; ++h) {
-            const bool absent = h == 1 && kc * BK + 32 >= p.d;  // box 1 of the last chunk
+            // box 1 of a last chunk with D - 64 kc <= 32 was not loaded, and the MMA's K
+            // steps (nks) stop before it: its A pieces are neither written nor read
+            if (h == 1 && kc * BK + 32 >= p.d) break;
             const uint8_t* srow = sbase + h * (BM * 128) + r * 128;
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
-              float4 f0 = *reinterpret_cast<const float4*>(srow + (((2 * jj) ^ sw) << 4));
-              float4 f1 = *reinterpret_cast<const float4*>(srow + (((2 * jj + 1) ^ sw) << 4));
-              if (absent) {
-                f0 = make_float4(0.f, 0.f, 0.f, 0.f);
-                f1 = f0;
-              }
+              const float4 f0 = *reinterpret_cast<const float4*>(srow + (((2 * jj) ^ sw) << 4));
+              const float4 f1 = *reinterpret_cast<const float4*>(srow + (((2 * jj + 1) ^ sw) << 4));
               const float v[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
               uint32_t hw[4], lw[4];
 #pragma unroll
