@@ -24,7 +24,7 @@ void score_naive(fsil_context* c, const ScoreParams& p);
 int64_t naive_tiles(int64_t n, int* tile_rows);
 bool ffma_supported(const fsil_context* c);
 void flag_all(fsil_context* c, const ScoreParams& p, int tile_rows);
-void exact_ab(fsil_context* c, const ScoreParams& p);
+void exact_pass(fsil_context* c, const ScoreParams& p, bool local);
 void refine(fsil_context* c, const ScoreParams& p);
 void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows, bool local);
 bool post_fused(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows, bool local);
@@ -146,6 +146,10 @@ ScoreParams make_params(fsil_context* c, double* s, int32_t* nb, int32_t* own, d
     s = c->s_tmp.as<double>();
   }
   p.s = s;
+  if (!nb) {  // the scoring pass nominates into it, the exact pass reads it back
+    c->nb_tmp.ensure(std::max<int64_t>(c->n, 1) * sizeof(int32_t));
+    nb = c->nb_tmp.as<int32_t>();
+  }
   p.nb = nb;
   p.own = own;
   p.a = a;
@@ -173,7 +177,6 @@ void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, 
     p.tile_flag = c->tile_flag.as<int32_t>();
     p.flag_count = c->flag_count.as<unsigned long long>();
     record(c, 3);
-    c->tc_exact_used = false;
     score_naive(c, p);
     c->score_path = 0;
     record(c, 4);
@@ -215,17 +218,20 @@ void do_score(fsil_context* c, double* s, int32_t* nb, int32_t* own, double* a, 
   p.flag_rows = c->flag_rows.as<int32_t>();
   p.flag_count = c->flag_count.as<unsigned long long>();
   record(c, 3);
-  c->tc_exact_used = false;
   if (use == FSIL_PATH_TCGEN05) score_tc(c, p);
   else if (use == FSIL_PATH_FFMA) score_ffma(c, p);
   else flag_all(c, p, tile_rows);
   c->score_path = use;
   record(c, 4);
   // single GPU: the final kernel also fills the mapped host summary (no pack launch)
-  if (c->fuse_post && post_fused(c, p, ntiles, tile_rows, c->local_call)) {
+  if (use == FSIL_PATH_TCGEN05) {
+    // the tensor-core pass only nominates neighbours: refinement of the uncertain rows,
+    // then every row's a_i, b_i, s_i in fp64 and the deterministic total
+    exact_pass(c, p, c->local_call);
+    record(c, 5);
+  } else if (c->fuse_post && post_fused(c, p, ntiles, tile_rows, c->local_call)) {
     record(c, 5);  // (refine phase = the fused post-scoring kernel; finalize phase empty)
   } else {
-    if (c->tc_exact_used) exact_ab(c, p);
     refine(c, p);
     record(c, 5);
     finalize_sum(c, p, ntiles, tile_rows, c->local_call);
@@ -447,7 +453,7 @@ void fsil_destroy(fsil_context* c) {
                           &c->sort_tmp, &c->sort_keys, &c->sort_vals, &c->iota, &c->seg_start,
                           &c->piece_start, &c->mu32, &c->p32, &c->nk, &c->bound, &c->s_tmp,
                           &c->tile_sum, &c->tile_flag, &c->flag_rows, &c->flag_count, &c->result,
-                          &c->group_sum, &c->xmax, &c->tc_b, &c->exact_rows, &c->exact_count, &c->a_scratch, &c->x32, &c->xbuf, &c->xt_keys, &c->xt_vals, &c->xt_dense, &c->hX, &c->hL, &c->o_s, &c->o_nb, &c->o_own, &c->o_a,
+                          &c->group_sum, &c->xmax, &c->tc_b, &c->nb_tmp, &c->a_scratch, &c->x32, &c->xbuf, &c->xt_keys, &c->xt_vals, &c->xt_dense, &c->hX, &c->hL, &c->o_s, &c->o_nb, &c->o_own, &c->o_a,
                           &c->o_b};
   for (auto* b : bufs) b->release();
   for (auto& e : c->ev)

@@ -364,75 +364,12 @@ __global__ void flag_all_kernel(int64_t n, int tile_rows, int32_t* flag_rows, in
   if (i == 0) *flag_count = static_cast<unsigned long long>(n);
 }
 
-// Exact own/neighbour recompute for rows whose tensor-core a_i/b_i bound was too
-// loose (neighbour already certified): LPR lanes per row (32/LPR rows per warp),
-// reference formulas in fp64.
-template <bool COS, int LPR>
-__device__ __forceinline__ void exact_rows_body(const ScoreParams& p, const int2* __restrict__ rows,
-                                                const unsigned long long* count, int64_t warp, int64_t nwarps,
-                                                int lane) {
-  const int64_t cnt = static_cast<int64_t>(*count);
-  const int sub = lane / LPR, li = lane % LPR;
-  constexpr int RPW = 32 / LPR;
-  const double* sums = p.stats + (COS ? p.k : 2 * p.k);
-  for (int64_t base = warp * RPW; base < cnt; base += nwarps * RPW) {
-    const int64_t i = base + sub;
-    const bool valid = i < cnt;
-    const int2 rn = valid ? rows[i] : make_int2(0, 0);
-    const int64_t row = rn.x;
-    const int nb = rn.y;
-    const int own = valid ? p.dense[row] : 0;
-    const int64_t xo = row * p.d;
-    const double* yo = sums + static_cast<int64_t>(own) * p.d;
-    const double* yb = sums + static_cast<int64_t>(nb) * p.d;
-    double ss = 0.0, co = 0.0, cb = 0.0;
-    if (valid)
-      for (int l = li; l < p.d; l += LPR) {
-        const double v = xval(p, xo + l);
-        ss = fma(v, v, ss);
-        co = fma(yo[l], v, co);
-        cb = fma(yb[l], v, cb);
-      }
-    for (int off = LPR >> 1; off > 0; off >>= 1) {
-      ss += __shfl_xor_sync(0xffffffffu, ss, off, LPR);
-      co += __shfl_xor_sync(0xffffffffu, co, off, LPR);
-      cb += __shfl_xor_sync(0xffffffffu, cb, off, LPR);
-    }
-    if (valid && li == 0) {
-      const double n_o = p.nk[own], n_b = p.nk[nb];
-      const bool singleton = n_o == 1.0;
-      double a, b;
-      if (COS) {
-        const double nrm = sqrt(ss);
-        b = cos_foreign(n_b, cb / nrm);
-        a = singleton ? 0.0 : cos_own(n_o, co / nrm);
-      } else {
-        b = sq_foreign(ss, p.stats[p.k + nb], n_b, cb);
-        a = singleton ? 0.0 : sq_own(ss, p.stats[p.k + own], n_o, co);
-      }
-      p.s[row] = singleton ? 0.0 : assemble_score(a, b);
-      if (p.a) p.a[row] = a;
-      if (p.b) p.b[row] = b;
-    }
-  }
-}
-
-template <bool COS, int LPR>
-__global__ void __launch_bounds__(256) exact_ab_kernel(ScoreParams p, const int2* __restrict__ rows,
-                                                       const unsigned long long* count) {
-  if (*p.abort) return;
-  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  exact_rows_body<COS, LPR>(p, rows, count, warp, nwarps, threadIdx.x & 31);
-}
-
-// The whole post-scoring phase in one cooperative launch (small cluster tables):
-// exact a/b rows and flagged rows (disjoint sets), grid barrier, then the tile groups
-// and -- in the block that finishes the last group -- the fixed-order total.
-template <bool COS, int LPR>
-__global__ void __launch_bounds__(256) post_kernel(ScoreParams p, const int2* __restrict__ exact_rows,
-                                                   const unsigned long long* exact_count, int64_t ntiles,
-                                                   int tile_rows, TotalArgs ta, unsigned int* bar, bool stage) {
+// The whole post-scoring phase of the FFMA and fp64 paths in one cooperative launch
+// (small cluster tables): flagged rows, grid barrier, then the tile groups and -- in the
+// block that finishes the last group -- the fixed-order total.
+template <bool COS>
+__global__ void __launch_bounds__(256) post_kernel(ScoreParams p, int64_t ntiles, int tile_rows, TotalArgs ta,
+                                                   unsigned int* bar, bool stage) {
   griddep_wait();  // (PDL) the scoring kernel's rows, flags and tile sums are visible
   extern __shared__ double xs_all[];  // [8 warps][d], then (stage) the cluster sums [K][d]
   const bool abort = *p.abort != 0;
@@ -440,13 +377,11 @@ __global__ void __launch_bounds__(256) post_kernel(ScoreParams p, const int2* __
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   double* staged = nullptr;
-  // blocks whose warps have no flagged or exact row skip the table (C2: ~70 flagged rows,
-  // i.e. a handful of blocks do any per-row work)
+  // blocks whose warps have no flagged row skip the table (a handful of flagged rows:
+  // a handful of blocks do any per-row work)
   if (stage) {
     const int64_t w0 = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5);
-    const int64_t nflag = static_cast<int64_t>(*p.flag_count);
-    const int64_t nexact = exact_count ? static_cast<int64_t>(*exact_count) : 0;
-    stage = w0 < nflag || w0 * (32 / LPR) < nexact;
+    stage = w0 < static_cast<int64_t>(*p.flag_count);
   }
   if (stage) {  // the table in shared memory: its loads overlap the first rows' own
     staged = xs_all + 8 * p.d;
@@ -454,32 +389,228 @@ __global__ void __launch_bounds__(256) post_kernel(ScoreParams p, const int2* __
     for (int64_t e = threadIdx.x; e < static_cast<int64_t>(p.k) * p.d; e += blockDim.x) staged[e] = __ldg(sums + e);
     __syncthreads();
   }
-  if (!abort) {
-    if (exact_count) exact_rows_body<COS, LPR>(p, exact_rows, exact_count, warp, nwarps, lane);
-    refine_rows<COS>(p, xs_all + static_cast<int64_t>(threadIdx.x >> 5) * p.d, warp, nwarps, lane, staged);
-  }
+  if (!abort) refine_rows<COS>(p, xs_all + static_cast<int64_t>(threadIdx.x >> 5) * p.d, warp, nwarps, lane, staged);
   grid_barrier(bar, bar + 1);
   const int64_t ngroups = (ntiles + kGroupTiles - 1) / kGroupTiles > 0 ? (ntiles + kGroupTiles - 1) / kGroupTiles : 1;
   for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x)
     if (tile_group_one(p.tile_sum, p.tile_flag, p.s, ntiles, tile_rows, p.n, ta, g, ngroups)) tile_total(ta, ngroups);
 }
 
-}  // namespace
+// ---------------------------------------------------------------- exact pass ----
+// Every row's a_i, b_i and s_i in fp64 from its own cluster and its (certified or
+// refined) neighbour: three length-D dots -- ||x||^2, Y_own.x, Y_nb.x -- and the
+// reference formulas (squared_euclidean.cpp:77-81, cosine.cpp:83-87, report.cpp:7-30).
+// The tensor-core pass only nominates the neighbour, so nothing that reaches s_i or S
+// carries tensor-core rounding: the fp32 input widened exactly, fp64 products and sums.
+//
+// LPR lanes per row, each owning CPL element pairs (D = 2 LPR CPL; CPL = 0: any even D):
+// x read as pairs (coalesced along the row), the cluster sums as double2 from shared
+// memory (the table staged once per CTA when it fits) or from L2.  Work unit: 32
+// consecutive rows per warp, two row passes' loads in flight; the unit's s_i are summed
+// in a fixed order into usum[u], and the CTA that finishes last (atomic ticket) sums the
+// units in a fixed order, so S is bit-identical run to run.
+constexpr int kUnitRows = 32;
+constexpr int kExactThreads = 512;
 
-void exact_ab(fsil_context* c, const ScoreParams& p) {
-  const int grid = c->num_sms * 8;
-  const int2* rows = c->exact_rows.as<int2>();
-  const unsigned long long* cnt = c->exact_count.as<unsigned long long>();
-  const int lpr = c->d <= 32 ? 4 : c->d <= 64 ? 8 : c->d <= 128 ? 16 : 32;
-#define FSIL_EXACT(L)                                                                        \
-  if (lpr == L) {                                                                            \
-    if (c->metric == FSIL_COSINE) exact_ab_kernel<true, L><<<grid, 256, 0, c->stream>>>(p, rows, cnt); \
-    else exact_ab_kernel<false, L><<<grid, 256, 0, c->stream>>>(p, rows, cnt);              \
+template <typename T>
+struct PairOf;
+template <>
+struct PairOf<float> {
+  using V = float2;
+};
+template <>
+struct PairOf<double> {
+  using V = double2;
+};
+
+struct ExactArgs {
+  double* usum;       // [nunits] fixed-order sums of s_i over 32-row units
+  int64_t nunits;
+  TotalArgs ta;
+  unsigned int* bar;  // grid-barrier words (cooperative launch with the refinement phase)
+  int refine;         // 1: refine the flagged rows first (cooperative launch), then barrier
+  int stage;          // 1: the cluster-sum table is staged in shared memory
+};
+
+template <bool COS>
+__device__ __forceinline__ double exact_finish(const ScoreParams& p, int64_t row, int own, int nb, double ss,
+                                               double co, double cb) {
+  const double n_o = p.nk[own], n_b = p.nk[nb];
+  const bool singleton = n_o == 1.0;
+  double a, b;
+  if (COS) {
+    const double nrm = sqrt(ss);
+    b = cos_foreign(n_b, cb / nrm);
+    a = singleton ? 0.0 : cos_own(n_o, co / nrm);
+  } else {
+    b = sq_foreign(ss, p.stats[p.k + nb], n_b, cb);
+    a = singleton ? 0.0 : sq_own(ss, p.stats[p.k + own], n_o, co);
   }
-  FSIL_EXACT(4) FSIL_EXACT(8) FSIL_EXACT(16) FSIL_EXACT(32)
-#undef FSIL_EXACT
-  FSIL_LAUNCHED(c);
+  const double s = singleton ? 0.0 : assemble_score(a, b);
+  p.s[row] = s;
+  if (p.a) p.a[row] = a;
+  if (p.b) p.b[row] = b;
+  if (p.own) p.own[row] = own;
+  return s;
 }
+
+template <bool COS, typename T, int LPR, int CPL>
+__device__ __forceinline__ void exact_units(const ScoreParams& p, const double* ytab, double* __restrict__ usum,
+                                            int64_t nunits, int64_t wid, int64_t nw, int lane) {
+  using V = typename PairOf<T>::V;
+  constexpr int RPP = 32 / LPR;  // rows per pass
+  const int sub = lane / LPR, li = lane % LPR;
+  const int d = p.d, d2 = p.d >> 1;
+  const T* X = sizeof(T) == 8 ? reinterpret_cast<const T*>(p.X64) : reinterpret_cast<const T*>(p.X);
+  for (int64_t u = wid; u < nunits; u += nw) {
+    const int64_t r0 = u * kUnitRows;
+    double su = 0.0;  // this lane group's rows, ascending
+    if constexpr (CPL > 0) {
+#pragma unroll 1
+      for (int pass = 0; pass < kUnitRows / RPP; pass += 2) {
+        V xv[2][CPL];
+        int64_t row[2];
+        int own[2], nbr[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // both passes' loads first (memory-level parallelism)
+          row[h] = r0 + (pass + h) * RPP + sub;
+          const bool ok = row[h] < p.n;
+          const V* xr = reinterpret_cast<const V*>(X + (ok ? row[h] : 0) * d);
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) xv[h][c] = xr[li + LPR * c];
+          own[h] = ok ? __ldg(p.dense + row[h]) : 0;
+          nbr[h] = ok ? p.nb[row[h]] : 0;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double* yo = ytab + static_cast<int64_t>(own[h]) * d;
+          const double* yb = ytab + static_cast<int64_t>(nbr[h]) * d;
+          double ss = 0.0, co = 0.0, cb = 0.0;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const int q = li + LPR * c;
+            const double2 o = *reinterpret_cast<const double2*>(yo + 2 * q);
+            const double2 b = *reinterpret_cast<const double2*>(yb + 2 * q);
+            const double x0 = static_cast<double>(xv[h][c].x), x1 = static_cast<double>(xv[h][c].y);
+            ss = fma(x0, x0, ss);
+            ss = fma(x1, x1, ss);
+            co = fma(o.x, x0, co);
+            co = fma(o.y, x1, co);
+            cb = fma(b.x, x0, cb);
+            cb = fma(b.y, x1, cb);
+          }
+#pragma unroll
+          for (int off = LPR >> 1; off > 0; off >>= 1) {
+            ss += __shfl_xor_sync(0xffffffffu, ss, off);
+            co += __shfl_xor_sync(0xffffffffu, co, off);
+            cb += __shfl_xor_sync(0xffffffffu, cb, off);
+          }
+          if (li == 0 && row[h] < p.n) su += exact_finish<COS>(p, row[h], own[h], nbr[h], ss, co, cb);
+        }
+      }
+    } else {  // any even D: one row per pass, LPR lanes stride the pairs
+#pragma unroll 1
+      for (int pass = 0; pass < kUnitRows / RPP; ++pass) {
+        const int64_t row = r0 + pass * RPP + sub;
+        const bool ok = row < p.n;
+        const V* xr = reinterpret_cast<const V*>(X + (ok ? row : 0) * d);
+        const int own = ok ? __ldg(p.dense + row) : 0, nb = ok ? p.nb[row] : 0;
+        const double* yo = ytab + static_cast<int64_t>(own) * d;
+        const double* yb = ytab + static_cast<int64_t>(nb) * d;
+        double ss = 0.0, co = 0.0, cb = 0.0;
+        for (int q = li; q < d2; q += LPR) {
+          const V xv = xr[q];
+          const double x0 = static_cast<double>(xv.x), x1 = static_cast<double>(xv.y);
+          ss = fma(x0, x0, ss);
+          ss = fma(x1, x1, ss);
+          co = fma(yo[2 * q], x0, co);
+          co = fma(yo[2 * q + 1], x1, co);
+          cb = fma(yb[2 * q], x0, cb);
+          cb = fma(yb[2 * q + 1], x1, cb);
+        }
+#pragma unroll
+        for (int off = LPR >> 1; off > 0; off >>= 1) {
+          ss += __shfl_xor_sync(0xffffffffu, ss, off);
+          co += __shfl_xor_sync(0xffffffffu, co, off);
+          cb += __shfl_xor_sync(0xffffffffu, cb, off);
+        }
+        if (li == 0 && ok) su += exact_finish<COS>(p, row, own, nb, ss, co, cb);
+      }
+    }
+    // fixed-order tree over the RPP row groups (lanes 0, LPR, 2 LPR, ...)
+#pragma unroll
+    for (int off = 16; off >= LPR; off >>= 1) su += __shfl_xor_sync(0xffffffffu, su, off);
+    if (lane == 0) usum[u] = su;
+  }
+}
+
+// Fixed-order total of the unit sums by the last CTA (kExactThreads threads).
+__device__ __forceinline__ void unit_total(const ExactArgs& ea, int64_t exact_rows) {
+  __shared__ double red[kExactThreads];
+  __threadfence();
+  double acc = 0.0;
+  for (int64_t u = threadIdx.x; u < ea.nunits; u += kExactThreads) acc += __ldcg(ea.usum + u);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int stride = kExactThreads / 2; stride > 0; stride >>= 1) {
+    if (threadIdx.x < stride) red[threadIdx.x] += red[threadIdx.x + stride];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const TotalArgs& ta = ea.ta;
+    const double flagged = static_cast<double>(*ta.flag_count);
+    const double exact = static_cast<double>(exact_rows);
+    ta.result[0] = red[0];
+    ta.result[1] = flagged;
+    ta.result[2] = exact;
+    if (ta.hsum) {
+      ta.hsum->checks[0] = ta.checks[0];
+      ta.hsum->checks[1] = ta.checks[1];
+      ta.hsum->missing = *ta.missing;
+      ta.hsum->result[0] = red[0];
+      ta.hsum->result[1] = flagged;
+      ta.hsum->result[2] = exact;
+    }
+    *ta.ticket = 0u;
+  }
+}
+
+// Refinement of the flagged rows (cooperative launch, small cluster tables) -> grid
+// barrier -> exact pass over every row -> fixed-order total in the last CTA.
+template <bool COS, typename T, int LPR, int CPL>
+__global__ void __launch_bounds__(kExactThreads) exact_kernel(ScoreParams p, ExactArgs ea) {
+  griddep_wait();  // (PDL) the scoring pass's neighbours and flags are visible
+  extern __shared__ __align__(16) double esm[];  // [stage: K*d table][refine: warps * d rows]
+  const bool abort = *p.abort != 0;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const double* sums = p.stats + (COS ? p.k : 2 * p.k);
+  const double* ytab = sums;
+  const int64_t tab = static_cast<int64_t>(p.k) * p.d;
+  if (ea.stage) {
+    for (int64_t e = threadIdx.x; e < tab; e += blockDim.x) esm[e] = __ldg(sums + e);
+    __syncthreads();
+    ytab = esm;
+  }
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib;
+  const int64_t gnw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  if (ea.refine) {
+    if (!abort)
+      refine_rows<COS>(p, esm + (ea.stage ? tab : 0) + static_cast<int64_t>(wib) * p.d, gw, gnw, lane,
+                       ea.stage ? esm : nullptr);
+    grid_barrier(ea.bar, ea.bar + 1);  // every refined neighbour is written
+  }
+  if (!abort) exact_units<COS, T, LPR, CPL>(p, ytab, ea.usum, ea.nunits, gw, gnw, lane);
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ea.ta.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) unit_total(ea, p.n);
+}
+
+}  // namespace
 
 void flag_all(fsil_context* c, const ScoreParams& p, int tile_rows) {
   flag_all_kernel<<<static_cast<unsigned>((p.n + 255) / 256), 256, 0, c->stream>>>(
@@ -522,7 +653,7 @@ TotalArgs total_args(fsil_context* c, const ScoreParams& p, int64_t ngroups, boo
   ta.group_sum = c->group_sum.as<double>();
   ta.result = c->result.as<double>();
   ta.flag_count = p.flag_count;
-  ta.exact_count = c->tc_exact_used ? c->exact_count.as<unsigned long long>() : nullptr;
+  ta.exact_count = nullptr;
   ta.ticket = reinterpret_cast<unsigned int*>(c->counters.as<int>() + 8);
   ta.hsum = local ? c->dsum : nullptr;
   ta.checks = c->checks.as<int64_t>();
@@ -531,7 +662,7 @@ TotalArgs total_args(fsil_context* c, const ScoreParams& p, int64_t ngroups, boo
 }
 }  // namespace
 
-// exact_ab + refine + finalize_sum as one cooperative launch when the per-row refine
+// refine + finalize_sum as one cooperative launch when the per-row refine
 // applies (cluster table below the tiled kernel's threshold); false: not applicable.
 bool post_fused(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows, bool local) {
   if (static_cast<int64_t>(c->k) * c->d >= 64 * 1024) return false;
@@ -542,16 +673,9 @@ bool post_fused(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_
   if (stage) smem += table;
   const int64_t ngroups = std::max<int64_t>((ntiles + kGroupTiles - 1) / kGroupTiles, 1);
   TotalArgs ta = total_args(c, p, ngroups, local);
-  const int2* rows = c->exact_rows.as<int2>();
-  const unsigned long long* cnt = c->tc_exact_used ? c->exact_count.as<unsigned long long>() : nullptr;
   unsigned int* bar = reinterpret_cast<unsigned int*>(c->counters.as<int>() + 12);
-  const int lpr = c->d <= 32 ? 4 : c->d <= 64 ? 8 : c->d <= 128 ? 16 : 32;
-  void* kern = nullptr;
-#define FSIL_POST(L)                                                                                 \
-  if (lpr == L) kern = c->metric == FSIL_COSINE ? reinterpret_cast<void*>(post_kernel<true, L>)     \
-                                                : reinterpret_cast<void*>(post_kernel<false, L>);
-  FSIL_POST(4) FSIL_POST(8) FSIL_POST(16) FSIL_POST(32)
-#undef FSIL_POST
+  void* kern = c->metric == FSIL_COSINE ? reinterpret_cast<void*>(post_kernel<true>)
+                                        : reinterpret_cast<void*>(post_kernel<false>);
   FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   FSIL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
@@ -560,7 +684,7 @@ bool post_fused(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_
   ScoreParams pp = p;
   int64_t nt = ntiles;
   int tr = tile_rows;
-  void* args[] = {&pp, &rows, &cnt, &nt, &tr, &ta, &bar, &stage};
+  void* args[] = {&pp, &nt, &tr, &ta, &bar, &stage};
   // cooperative (co-resident grid for the grid barrier) and, on the hot chain, PDL
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
@@ -577,6 +701,81 @@ bool post_fused(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_
   FSIL_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
   FSIL_LAUNCHED(c);
   return true;
+}
+
+// The exact pass (tensor-core path): every row's a_i, b_i, s_i in fp64 from its own and
+// nominated neighbour cluster, then the deterministic total.  With a small cluster table
+// (the per-row refinement applies) the flagged rows are refined in the same cooperative
+// launch before a grid barrier; otherwise the tiled refinement runs first as its own
+// launch.  D even (the tensor-core path needs D % 4 == 0).
+void exact_pass(fsil_context* c, const ScoreParams& p, bool local) {
+  const bool cos = c->metric == FSIL_COSINE;
+  const bool x64 = c->X64 != nullptr;
+  const int64_t tab = static_cast<int64_t>(c->k) * c->d;
+  const bool small = tab < 64 * 1024;
+  if (!small) refine(c, p);
+  const size_t tab_bytes = static_cast<size_t>(tab) * sizeof(double);
+  const size_t rows_bytes = small ? (kExactThreads / 32) * static_cast<size_t>(c->d) * sizeof(double) : 0;
+  const bool stage = tab_bytes + rows_bytes <= std::min<size_t>(c->smem_optin, 200 * 1024);
+  const size_t smem = (stage ? tab_bytes : 0) + rows_bytes;
+  ExactArgs ea{};
+  ea.nunits = (c->n + kUnitRows - 1) / kUnitRows;
+  c->group_sum.ensure(std::max<int64_t>(ea.nunits, 1) * sizeof(double));
+  ea.usum = c->group_sum.as<double>();
+  ea.ta = total_args(c, p, 1, local);
+  ea.ta.group_sum = nullptr;
+  ea.bar = reinterpret_cast<unsigned int*>(c->counters.as<int>() + 12);
+  ea.refine = small ? 1 : 0;
+  ea.stage = stage ? 1 : 0;
+  // lanes per row / pairs per lane: D = 2 LPR CPL for the common widths, else generic
+  const int d = c->d;
+  int lpr = 32, cpl = 0;
+  if (!x64) {
+    if (d == 16) lpr = 4, cpl = 2;
+    else if (d == 32) lpr = 4, cpl = 4;
+    else if (d == 64) lpr = 8, cpl = 4;
+    else if (d == 128) lpr = 16, cpl = 4;
+    else if (d == 256) lpr = 32, cpl = 4;
+    else if (d == 512) lpr = 32, cpl = 8;
+    else if (d == 768) lpr = 32, cpl = 12;
+  }
+  // the double2 reads of the cluster sums need 16-byte rows: a global table at an 8-byte
+  // offset (cosine with odd K) takes the generic kernel's scalar reads
+  const double* sums = p.stats + (cos ? c->k : 2 * c->k);
+  if (!stage && (reinterpret_cast<uintptr_t>(sums) & 15)) lpr = 32, cpl = 0;
+  void* kern = nullptr;
+#define FSIL_EXACT_K(T, L, C)                                                                             \
+  if (!kern && (sizeof(T) == 8) == x64 && lpr == L && cpl == C)                                           \
+    kern = cos ? reinterpret_cast<void*>(exact_kernel<true, T, L, C>) : reinterpret_cast<void*>(exact_kernel<false, T, L, C>);
+  FSIL_EXACT_K(float, 4, 2) FSIL_EXACT_K(float, 4, 4) FSIL_EXACT_K(float, 8, 4) FSIL_EXACT_K(float, 16, 4)
+  FSIL_EXACT_K(float, 32, 4) FSIL_EXACT_K(float, 32, 8) FSIL_EXACT_K(float, 32, 12) FSIL_EXACT_K(float, 32, 0)
+  FSIL_EXACT_K(double, 32, 0)
+#undef FSIL_EXACT_K
+  if (!kern) fail(FSIL_ERR_INTERNAL, "no exact-pass kernel for this shape");
+  FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  FSIL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kExactThreads, smem));
+  if (per_sm < 1) fail(FSIL_ERR_INTERNAL, "exact pass does not fit on an SM");
+  const int grid = c->num_sms * std::min(per_sm, 2);
+  ScoreParams pp = p;
+  void* args[] = {&pp, &ea};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = kExactThreads;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[na++].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
+  if (small) {  // co-resident grid for the grid barrier
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na++].val.cooperative = 1;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  FSIL_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
+  FSIL_LAUNCHED(c);
 }
 
 void finalize_sum(fsil_context* c, const ScoreParams& p, int64_t ntiles, int tile_rows, bool local) {

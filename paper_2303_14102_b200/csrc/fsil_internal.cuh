@@ -146,7 +146,7 @@ struct fsil_context {
   fsil::DevBuf group_sum;
   fsil::DevBuf xmax;           // float: max |x| of this shard (tensor-core operand scaling)
   fsil::DevBuf tc_b;           // fp16 cluster-mean pieces + column bias (tcgen05 path)
-  fsil::DevBuf exact_rows, exact_count;  // rows needing the exact own/neighbour recompute
+  fsil::DevBuf nb_tmp;                   // neighbours when the caller passes no neighbour pointer
   fsil::DevBuf a_scratch;                // tcgen05 streaming mode: per-CTA converted A chunks
   fsil::DevBuf x32;                      // fp64 front end: rounded fp32 copy for the fast pass
   fsil::DevBuf xi_rows;                  // fp64 ||x||^2 per row, written by the batched aggregation
@@ -167,7 +167,6 @@ struct fsil_context {
   int64_t d2r_cap = 0;
   int64_t spec_cap_x = 0;
   uint32_t xt_epoch = 0;
-  bool tc_exact_used = false;
   // host staging for fsil_silhouette (pageable -> pinned)
   fsil::DevBuf hX, hL;         // device copies of host inputs
   fsil::DevBuf o_s, o_nb, o_own, o_a, o_b;

@@ -7,16 +7,17 @@
 //   warp 0      TMA producer: fp32 X boxes (128 rows x 32 cols, 128B swizzle) into a
 //               staging ring; fp16 cluster-mean pieces B_hi/B_lo into the operand ring
 //   warp 1      TMEM owner + single-thread tcgen05.mma issuer (kind::f16, fp32 accum)
-//   warps 2..5  epilogue (one TMEM lane = one row): clamped cluster means, top-2 with a
-//               rigorous error bound, a_i/b_i/s_i from the tensor-core dots in fp64
+//   warps 2..5  epilogue (one TMEM lane = one row): ranking keys, top-2 with a
+//               certified error bound -> the nominated neighbour cluster
 //   warps 6..9  converters: x (fp32) -> x*2^-ex split into fp16 hi + lo in the UMMA
 //               K-major SWIZZLE_128B layout, plus ||x||^2 (fp32 and fp64) per row
 //
 // Split precision ("fp16x3"): x~ = hx + lx, mu~ = hm + lm (exact to ~2^-22 after a
 // global power-of-two scaling); dot = hx.hm + hx.lm + lx.hm, three MMAs per K step.
 // Every row carries a certified bound on its dots; rows whose neighbour is not
-// certain go to the fp64 argmin refinement (K4), rows whose a_i/b_i bound exceeds
-// 5e-6 in s_i go to the exact own/neighbour recompute -- both in finalize.cu.
+// certain go to the fp64 argmin refinement (K4).  This pass only NOMINATES the
+// neighbour: a_i, b_i and s_i of every row come from the fp64 exact pass
+// (finalize.cu), so no tensor-core rounding reaches s_i or S.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -37,7 +38,6 @@ constexpr int BK = 64;                // fp16 K elements per chunk (one 128-byte
 constexpr int kStgBytes = 2 * BM * 128;  // two fp32 boxes of 32 columns
 constexpr int kABytes = BM * 128;        // one fp16 A piece (hi or lo)
 constexpr int kThreads = 640;            // 20 warps (5 warpgroups)
-constexpr float kTau = 9e-6f;            // certified |ds_i| budget before exact a/b (bar: 1e-5)
 
 __host__ __device__ constexpr int ncb_bn_pad(int kp) { return (kp + 3) & ~3; }
 
@@ -47,17 +47,16 @@ struct TcScale {
   double smul64;          // 2^(ex+em): dot = acc * smul
   float sx;               // 2^-ex: x -> x~
   float smul;
-  float floor_coef;       // absolute-floor coefficient (times ||x||)
+  float floor_mu;         // fp16 subnormal floor of the mu pieces, per unit ||x||
+  float floor_x;          // fp16 subnormal floor of the x pieces, per unit ||mu|| (absolute in x)
   float mu_max;           // max ||mu_k||
   float p_max;            // max p_k (sqeuclid)
-  float pad;
 };
 
 struct TcParams {
   ScoreParams p;
   int ncb, nkc;           // cluster blocks, K chunks
   const float* colbias;   // [ncb*BN]: sqeuclid p_k, cosine 0, padding +inf
-  const double4* clu;     // [K]: {n_k, 1/(n_k-1) (0 if singleton), Psi_k, ||mu_k|| rounded up}
   const __half* munorm;   // [ncb*BN]: ||mu_k|| / mu_max rounded up (neighbour error bounds)
   int nstg;               // X staging stages
   int nsa;                // decoupled mode: A operand slots (0: A converted in place in the X stages)
@@ -66,8 +65,6 @@ struct TcParams {
   float cdot;             // relative dot bound coefficient
   unsigned long long* dbg;  // optional per-role wait-cycle counters (FSIL_TC_PROFILE)
   int split;              // separate correction accumulator (large D)
-  int2* exact_rows;       // rows needing the exact own/neighbour recompute
-  unsigned long long* exact_count;
   uint8_t* ascratch;      // streaming mode: [grid][nkc][kStgBytes] converted A chunks (or null)
   float exic;             // ||x||^2 relative error / u: 8.1 (fp32 blocks of 8), +2.1 on fp64 input
   const double* xi_rows;  // per-row fp64 ||x||^2 from the aggregation pass (or null: converters form it)
@@ -198,11 +195,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 48);
   uint64_t* scr_ready = bars + 49;         // [1] a tile's converted chunks are in scratch
   double* meta_xi = reinterpret_cast<double*>(bars + 50);   // [2][2][BM] ||x||^2 halves
-  double4* meta_clu = reinterpret_cast<double4*>(meta_xi + 4 * BM);  // [2][BM] clu[own] per row
-  float* part = reinterpret_cast<float*>(meta_clu + 2 * BM);  // [2][4][BM] second-half partial top-2
-  double* red = reinterpret_cast<double*>(part + 8 * BM);     // [3][4] tile-sum partials
-  int* red_flag = reinterpret_cast<int*>(red + 12);           // [3][4]
-  int* meta_own = reinterpret_cast<int*>(red + 18);           // [2][BM] own cluster per row
+  float* part = reinterpret_cast<float*>(meta_xi + 4 * BM);  // [2][3][BM] second-half partial top-2
+  int* meta_own = reinterpret_cast<int*>(part + 6 * BM);      // [2][BM] own cluster per row
   float* cb_s = reinterpret_cast<float*>(meta_own + 2 * BM);  // [ncb*BN] column bias
   __half* mn_s = reinterpret_cast<__half*>(cb_s + ncb_bn_pad(tp.ncb * BN));  // [ncb*BN] ||mu_k||/mu_max, rounded up
 
@@ -266,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (myscr && xp > 0) {
               mbar_arrive_expect_tx(a_full + s1, kStgBytes);
               bulk_load(stg + s1 * kStgBytes, myscr + static_cast<size_t>(kc) * kStgBytes, kStgBytes, a_full + s1);
-              continue;
+              continue;  // (no stg_full phase: the converters count TMA'd items per stage)
             }
             mbar_arrive_expect_tx(stg_full + s1, nbox * BM * 128);
             for (int b = 0; b < nbox; ++b)
@@ -614,7 +608,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-    } else
+    } else {
+    // stg_full completes one phase per TMA'd item of a stage.  With the A scratch the
+    // reloaded items in between never touch it, and they are issued at MMA pace, so a
+    // parity derived from the running item count can alias two phases (the converters
+    // run ahead of the barrier): the parity is tracked per stage over TMA'd items only.
+    // Every TMA'd item of a stage is observed here, and the producer cannot land the next
+    // one before this one was converted (scr_ready / stg_empty), so the waits never lag
+    // the barrier by more than one phase.
+    uint32_t tpar = 0;  // bit s: parity of stage s's next TMA'd item
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
       double xi = 0.0;
       // the epilogue's per-row inputs, fetched here off its critical path
@@ -624,11 +626,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (myscr && xp > 0) {  // later passes load the stored conversions (producer)
           n1 += nkc;
           s1 = static_cast<int>(n1 % NS);
-          ph1 = (n1 / NS) & 1;
           continue;
         }
         for (int kc = 0; kc < nkc; ++kc, ++n1) {
-          TW(4, stg_full + s1, ph1);
+          TW(4, stg_full + s1, (tpar >> s1) & 1u);
+          tpar ^= 1u << s1;
           uint8_t* sbase = stg + s1 * kStgBytes;
           // (box 1 of the last chunk may be absent: those lanes read stale bytes, then zero
           // them on a warp-uniform branch rather than zero-initialising every chunk)
@@ -694,19 +696,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           bulk_wait_all();
           mbar_arrive(scr_ready);
         }
-        if (xp == 0) {  // ||x||^2 halves, own cluster and its constants to the epilogue
+        if (xp == 0) {  // ||x||^2 halves and the own cluster to the epilogue
           const int tb = nt & 1;
-          const double4 co = own >= 0 ? tp.clu[own] : make_double4(1.0, 0.0, 0.0, 0.0);
           TW(6, meta_empty + tb, ((nt >> 1) & 1) ^ 1);
           meta_xi[(tb * 2 + hq) * BM + r] = xi;
-          if (hq == 0) {
-            meta_own[tb * BM + r] = own;
-            meta_clu[tb * BM + r] = co;
-          }
+          if (hq == 0) meta_own[tb * BM + r] = own;
           __syncwarp();
           if (lane == 0) mbar_arrive(meta_full + tb);
         }
       }
+    }
     }
   } else {
     // ------------------------------------------------------------ epilogue (8 warps)
@@ -718,8 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int NQ = BN / 32;
     // Per-row inputs (own cluster; ||x||^2 when the aggregation pass provides it) are
     // fetched from global memory one tile ahead of their use, so their DRAM latency
-    // overlaps the current tile instead of serialising with it; clu[own] (L2) is issued
-    // at the start of the tile and first used after the scan.
+    // overlaps the current tile instead of serialising with it.
     const int64_t tstep = (TS ? EG : 1) * static_cast<int64_t>(gridDim.x);
     int own_n = -1;
     double xi_n = 0.0;
@@ -737,18 +735,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool valid = row < p.n;
       int own;
       double xi64;
-      double4 co;  // n, 1/(n-1), Psi, ||mu||
       // ||x||^2 from the aggregation pass (exact fp64) when it wrote one, issued early
       const double xi_g = (!tp.lean && tp.xi_rows && valid) ? __ldg(tp.xi_rows + row) : 0.0;
       if (tp.lean) {  // the lean converters hand nothing over: prefetched inputs
         own = own_n;
         xi64 = xi_n;
-        co = own >= 0 ? tp.clu[own] : make_double4(1.0, 0.0, 0.0, 0.0);
         fetch(t + tstep);
       } else {  // the converters' hand-off through shared memory
         TW(7, meta_full + tb, (nt >> 1) & 1);
         own = meta_own[tb * BM + r];
-        co = meta_clu[tb * BM + r];
         xi64 = tp.xi_rows ? xi_g : meta_xi[(tb * 2) * BM + r] + meta_xi[(tb * 2 + 1) * BM + r];
       }
       const float xi = static_cast<float>(xi64);
@@ -757,7 +752,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ranking key m' = m - rowc (row constant dropped, no clamp): sqeuclid
       // m = xi + p_k - 2 dot, cosine m = 1 - dot/||x||; dot = acc * smul
       const float rowm = COS ? -(sc.smul * rnf) : -2.0f * sc.smul;
-      float b1 = INFINITY, b2 = INFINITY, doto = NAN;
+      float b1 = INFINITY, b2 = INFINITY;
       int arg = -1;
       for (int cb = 0; cb < ncb; ++cb) {
         int ab;
@@ -775,7 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (quad == 0) TRACE(nt, 5);
         const long long ts0 = dbgp ? clock64() : 0;
         tc_fence_after();
-        // one 32-column chunk: ranking keys, own-column capture, running top-2
+        // one 32-column chunk: ranking keys (own column excluded), running top-2
         auto scan32 = [&](const uint32_t(&v)[32], int k0) {
           const int ownrel = own - k0;
           int argc = -1;  // chunk-local index of a new best
@@ -789,9 +784,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int j = 4 * j4 + e;
               const float acc = __uint_as_float(v[j]);
               float m = fmaf(acc, rowm, bj[e]);
-              const bool is_own = j == ownrel;
-              doto = is_own ? acc : doto;
-              m = is_own ? INFINITY : m;
+              m = j == ownrel ? INFINITY : m;
               const bool lt = m < b1;  // strict: the lowest index keeps ties
               argc = lt ? j : argc;
               b2 = fminf(b2, fmaxf(b1, m));
@@ -834,12 +827,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long tf0 = dbgp ? clock64() : 0;
       if (!TS) {
         // ---- merge the two column halves (group 1 -> smem -> group 0)
-        float* pt = part + tb * 4 * BM;  // double-buffered by tile parity
+        float* pt = part + tb * 3 * BM;  // double-buffered by tile parity
         if (grp == 1) {
           pt[0 * BM + r] = b1;
           pt[1 * BM + r] = b2;
           pt[2 * BM + r] = __int_as_float(arg);
-          pt[3 * BM + r] = doto;
         }
         named_bar(1, 256);
         if (grp == 1) {
@@ -849,121 +841,48 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const float c1 = pt[0 * BM + r], c2 = pt[1 * BM + r];
         const int a2 = __float_as_int(pt[2 * BM + r]);
-        const float d2 = pt[3 * BM + r];
         const float nb1 = fminf(b1, c1);
         b2 = fminf(fminf(fmaxf(b1, c1), b2), c2);
         arg = (c1 < b1 || (c1 == b1 && a2 >= 0 && (arg < 0 || a2 < arg))) ? a2 : arg;
         b1 = nb1;
-        doto = (doto == doto) ? doto : d2;
       }
       __syncwarp();
       if (lane == 0 && !tp.lean) mbar_arrive(meta_empty + tb);
 
-      // ---- certification and a_i, b_i, s_i.  Cosine in fp32: the inputs (tensor-core
-      // dots) carry fp32-level certified errors already, the fp32 evaluation adds its
-      // own rounding terms to the bounds, and s_i's final rounding (~3u) stays well
-      // inside the 1e-5 bar on top of kTau.  Squared Euclidean in fp64 (cancellation).
-      double s = 0.0;
-      bool any = false;
+      // ---- neighbour certification.  The key error bound per unit ||x|| for a column of
+      // norm ||mu||: cdot ||mu|| (split residuals + truncating fp32 accumulation, see
+      // score_tc) + floor_mu (mu pieces' fp16 subnormal floor) + floor_x ||mu|| / ||x||
+      // (x pieces' floor, absolute in x: per row, so rows far smaller than the shard's
+      // largest element are still covered).  Uncertain rows go to the fp64 refinement.
       if (valid) {
         const float u = 5.9604645e-8f;
         const float rowc = COS ? 1.0f : xi;
         const float exi = tp.exic * u * xi;  // ||x||^2 error (fp32 blocks of 8; fp64 input rounding)
+        const float rx = COS ? rnf : rsqrtf(xi);  // 1/||x|| (<= 2.2u; inf for a zero row -> flagged)
+        const float cmu = tp.cdot + sc.floor_x * rx * 1.0001f;
         // key error: the dot bound (per unit ||x|| for cosine); the key's own roundings
         // (cosine: rsqrt 2.2u + product 0.5u + fma 0.5u on |m| <= 1, within 4u(|b1|+1));
         // the ||x||^2 error
-        const float eps_dot1 = tp.cdot * sc.mu_max + sc.floor_coef;  // any column, per unit ||x||
+        const float eps_dot1 = cmu * sc.mu_max + sc.floor_mu;  // any column, per unit ||x||
         const float eps_m = COS ? (eps_dot1 + 4.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u)
                                 : (2.0f * eps_dot1 * xn + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
-        int nb = arg;
         // the winner's key error uses its own cluster norm (the runner-up's column is
         // not tracked: any-column bound eps_m)
         const float mu_arg = arg >= 0 ? __half2float(mn_s[arg]) * sc.mu_max : sc.mu_max;
-        const float eps_dot1_arg = tp.cdot * mu_arg + sc.floor_coef;
+        const float eps_dot1_arg = cmu * mu_arg + sc.floor_mu;
         const float eps_m_arg = COS ? (eps_dot1_arg + 4.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u)
                                     : (2.0f * eps_dot1_arg * xn + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
         // neighbour certain: clear gap, and no tie through the clamps at 0 (and 2)
-        const bool full = !((b2 - b1) > eps_m + eps_m_arg) || nb < 0 || !(rowc + b2 > eps_m) ||
+        const bool full = !((b2 - b1) > eps_m + eps_m_arg) || arg < 0 || !(rowc + b2 > eps_m) ||
                           (COS && !(rowc + b1 < 2.0f - eps_m));
-        if (nb < 0) nb = own == 0 ? 1 : 0;
-        const bool singleton = co.x == 1.0;
-        // per-cluster dot error bounds per unit ||x|| (tight when cluster norms differ)
-        const float eb1 = tp.cdot * (__half2float(mn_s[nb]) * sc.mu_max) + sc.floor_coef;
-        const float eo1 = tp.cdot * static_cast<float>(co.w) + sc.floor_coef;
-        float a32, b32;
-        bool inexact;
-        if (COS) {
-          // cosine: everything O(1) -- fp32 evaluation, its roundings in the bounds
-          const float dob = doto * sc.smul;  // exact (power-of-two scale)
-          const float n_o = static_cast<float>(co.x), r_o = static_cast<float>(co.y), nr_o = n_o * r_o;
-          const float t = n_o * dob * rnf;  // rnf: rsqrt (<= 2.2u) of the rounded xi
-          const float b = fminf(fmaxf(1.0f + b1, 0.0f), 2.0f);
-          const float a = singleton ? 0.0f : fminf(fmaxf((n_o - t) * r_o, 0.0f), 2.0f);
-          const float db = 1.01f * (eb1 + 4.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u + u * b);
-          // dots; ||x||^2 and rsqrt (8.1u/2 + 2.5u); the four fp32 roundings of a
-          const float da = 1.01f * (nr_o * (eo1 + tp.exic * u) + 3.0f * u * nr_o * fabsf(dob * rnf) +
-                                    5.0f * u * (n_o + fabsf(t)) * r_o);
-          const float mx = fmaxf(a, b);
-          if (!singleton && mx > 0.0f) s = a <= b ? 1.0f - __fdividef(a, b) : __fdividef(b, a) - 1.0f;
-          inexact = !singleton && !(mx > 2.0f * (da + db) && (da + db) <= kTau * mx);
-          a32 = a;
-          b32 = b;
-        } else {
-          // sqeuclid: n xi + Psi - 2 n dot cancels heavily when ||x|| >> the cluster
-          // spread -- fp64 (no divisions: per-cluster reciprocals, Newton 1/max(a,b))
-          const double ed_b = static_cast<double>(eb1) * xn, ed_o = static_cast<double>(eo1) * xn;
-          const double dob = static_cast<double>(doto) * sc.smul64;
-          const double n_o = co.x, r_o = co.y, nr_o = n_o * r_o;
-          const double b = fmax(static_cast<double>(rowc) + static_cast<double>(b1), 0.0);
-          const double a = singleton ? 0.0 : fmax((n_o * xi64 + co.z - 2.0 * n_o * dob) * r_o, 0.0);
-          const double db = 2.0 * ed_b + 3.0 * u * (fabs(b1) + sc.p_max + 2.0 * xn * sc.mu_max) + exi;
-          const double da = nr_o * (2.0 * ed_o + exi);
-          const double mx = fmax(a, b);
-          if (!singleton && mx > 0.0) {  // assemble_score without a division
-            double rm = static_cast<double>(__frcp_rn(static_cast<float>(mx)));
-            rm = rm * (2.0 - mx * rm);
-            rm = rm * (2.0 - mx * rm);
-            s = a <= b ? 1.0 - a * rm : b * rm - 1.0;
-          }
-          inexact = !singleton && !(mx > 2.0 * (da + db) && (da + db) <= static_cast<double>(kTau) * mx);
-          a32 = 0.f;
-          b32 = 0.f;
-          if (p.a) p.a[row] = a;
-          if (p.b) p.b[row] = b;
-        }
-        p.s[row] = s;
-        if (p.nb) p.nb[row] = nb;
-        if (p.own) p.own[row] = own;
-        if (COS) {
-          if (p.a) p.a[row] = a32;
-          if (p.b) p.b[row] = b32;
-        }
+        p.nb[row] = arg >= 0 ? arg : (own == 0 ? 1 : 0);  // the refinement rewrites flagged rows
         if (full) {
           const unsigned long long idx = atomicAdd(p.flag_count, 1ull);
           p.flag_rows[idx] = static_cast<int32_t>(row);
-          any = true;
-        } else if (inexact) {
-          const unsigned long long idx = atomicAdd(tp.exact_count, 1ull);
-          tp.exact_rows[idx] = make_int2(static_cast<int>(row), nb);
-          any = true;
         }
       }
-      // fixed-order tile sum over the 4 first-half warps: one named barrier,
-      // partial slots double-buffered by tile parity
-      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      const unsigned anyw = __ballot_sync(0xffffffffu, any);
-      const int rs = TS ? grp : tb;  // tile-sum slot: per group (alternating tiles) or per parity
-      if (lane == 0) {
-        red[rs * 4 + quad] = s;
-        red_flag[rs * 4 + quad] = anyw != 0;
-      }
-      named_bar(2 + grp, 128);
       if (dbgp && warp == kEpiWarp0 && lane == 0) atomicAdd(dbgp + 13, static_cast<unsigned long long>(clock64() - tf0));
-      if (quad == 0 && lane == 0) {
-        p.tile_sum[t] = ((red[rs * 4] + red[rs * 4 + 1]) + red[rs * 4 + 2]) + red[rs * 4 + 3];
-        p.tile_flag[t] = red_flag[rs * 4] | red_flag[rs * 4 + 1] | red_flag[rs * 4 + 2] | red_flag[rs * 4 + 3];
-        TRACE(nt, 7);
-      }
+      if (quad == 0 && lane == 0) TRACE(nt, 7);
     }
   }
 
@@ -983,11 +902,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 __device__ __forceinline__ int scale_exp(float m) { return m > 0.f ? ilogbf(m) - 14 : 0; }
 
 // B pieces: mu~ = mu * 2^-em split into fp16 hi + lo, [Kp][Dp] zero padded; column
-// bias for the ranking (sqeuclid p_k, cosine 0, padding +inf); per-cluster constants;
-// block 0 also writes the TcScale record the scoring kernel reads.
+// bias for the ranking (sqeuclid p_k, cosine 0, padding +inf); per-cluster norms (the
+// winner's error bound); block 0 also writes the TcScale record the scoring kernel reads.
 __global__ void prep_b_kernel(const double* __restrict__ stats, const float* __restrict__ bound,
                               const float* __restrict__ xmax, int k, int d, int kp, int dp, bool cos,
-                              __half* bh, __half* bl, float* colbias, __half* munorm, double4* clu,
+                              __half* bh, __half* bl, float* colbias, __half* munorm,
                               TcScale* scale, const int* abort, bool unit_ok) {
   griddep_wait();
   if (*abort) return;
@@ -997,19 +916,20 @@ __global__ void prep_b_kernel(const double* __restrict__ stats, const float* __r
   if (c == 0 && threadIdx.x == 0) {
     const float xm = *xmax;
     // x needs no scaling when max|x| lies in [0.5, 2^14): x~ = x stays below fp16's max
-    // and the subnormal floor of the small elements is in the bound (floor_coef); the
-    // converters then skip the multiply
+    // and the subnormal floor of the small elements is in the per-row bound (floor_x);
+    // the multiply-free converters then skip the multiply
     const int ex = (unit_ok && xm >= 0.5f && xm < 16384.f) ? 0 : scale_exp(xm);
     TcScale t;
     t.sx = ldexpf(1.0f, -ex);
     t.smul = ldexpf(1.0f, ex + em);
     t.smul64 = ldexp(1.0, ex + em);
-    // fp16 subnormal floor: 2^-25 per element in scaled units, sqrt(D) via Cauchy-Schwarz
-    t.floor_coef = 1.05f * 0.5f * 5.9604645e-8f * sqrtf(static_cast<float>(d)) *
-                   (ldexpf(1.0f, em) + ldexpf(1.0f, ex) * bound[0] / fmaxf(xm, 1e-30f));
+    // fp16 subnormal floor: 2^-25 per element in scaled units, sqrt(D) via Cauchy-Schwarz:
+    // |dot error| <= floor_mu ||x|| (mu pieces) + floor_x ||mu|| (x pieces)
+    const float fl = 1.05f * 0.5f * 5.9604645e-8f * sqrtf(static_cast<float>(d));
+    t.floor_mu = fl * ldexpf(1.0f, em);
+    t.floor_x = fl * ldexpf(1.0f, ex);
     t.mu_max = bound[0];
     t.p_max = bound[1];
-    t.pad = 0.f;
     *scale = t;
   }
   const double n = c < k ? fmax(stats[c], 1.0) : 1.0;
@@ -1040,7 +960,6 @@ __global__ void prep_b_kernel(const double* __restrict__ stats, const float* __r
     const double nrm = sqrt(red[0] + red[1] + red[2] + red[3]) * (1.0 + 1e-12);
     // bound[0] = max ||mu_k|| rounded up, so the ratio is <= 1; every rounding upward
     munorm[c] = __float2half_ru(__double2float_ru(__ddiv_ru(nrm, fmax(static_cast<double>(bound[0]), 1e-300))));
-    if (c < k) clu[c] = make_double4(n, n > 1.0 ? 1.0 / (n - 1.0) : 0.0, cos ? 0.0 : stats[k + c], nrm);
   }
 }
 
@@ -1077,11 +996,10 @@ CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* ptr, uint64_t inner,
 int pick_bn(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : 128; }
 
 // Shared memory with `nstg` X staging stages: operand ring, staging ring, barriers,
-// meta_xi, merge partials, tile-sum slots, column bias (fp32) and norms (fp16).
+// meta_xi, merge partials, own clusters, column bias (fp32) and norms (fp16).
 size_t tc_smem(int bn, int kp, int nstg) {
   const size_t bring = bn <= 32 ? TcCfg<32>::kBRing : bn <= 64 ? TcCfg<64>::kBRing : TcCfg<128>::kBRing;
-  return 1024 + bring + static_cast<size_t>(nstg) * kStgBytes + 50 * 8 + 4 * BM * 8 + 2 * BM * 32 + 8 * BM * 4 + 48 +
-         128 + 2 * BM * 4 +
+  return 1024 + bring + static_cast<size_t>(nstg) * kStgBytes + 50 * 8 + 4 * BM * 8 + 6 * BM * 4 + 2 * BM * 4 +
          static_cast<size_t>(ncb_bn_pad(kp)) * 4 + static_cast<size_t>(kp) * 2 + 16;
 }
 constexpr int kMaxStg = 8;
@@ -1125,32 +1043,23 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   const int kp = ncb * bn;
   const int nkc = (c->d + BK - 1) / BK;
   const int dp = nkc * BK;
-  c->tc_b.ensure(2ull * kp * dp * sizeof(__half) + kp * (sizeof(float) + sizeof(__half)) +
-                 (kp + 1) * sizeof(double4) + 64);
+  c->tc_b.ensure(2ull * kp * dp * sizeof(__half) + kp * (sizeof(float) + sizeof(__half)) + sizeof(TcScale) + 64);
   __half* bh = c->tc_b.as<__half>();
   __half* bl = bh + static_cast<size_t>(kp) * dp;
   float* colbias = reinterpret_cast<float*>(bl + static_cast<size_t>(kp) * dp);
   __half* munorm = reinterpret_cast<__half*>(colbias + kp);
-  double4* clu = reinterpret_cast<double4*>((reinterpret_cast<uintptr_t>(munorm + kp) + 31) & ~uintptr_t(31));
-  TcScale* scale = reinterpret_cast<TcScale*>(clu + kp);
-  // unit x scale only where the converters take the multiply-free path (the three-group
-  // decoupled kernel: one cluster block at BN = 32, ||x||^2 from the batched aggregation)
-  const bool unit_ok = bn == 32 && ncb == 1 && c->xi_valid && c->agg_path == 3 && !c->X64;
-  launch_pdl(c, prep_b_kernel, kp, 128, 0, p.stats, c->bound.as<float>(), c->xmax.as<float>(), c->k, c->d, kp, dp,
-             cos, bh, bl, colbias, munorm, clu, scale, p.abort, unit_ok);
-  const CUtensorMap mx = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, c->X, c->d, c->n, c->d * 4ull, 32, BM);
-  const CUtensorMap mh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, bh, dp, kp, dp * 2ull, BK, bn);
-  const CUtensorMap ml = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, bl, dp, kp, dp * 2ull, BK, bn);
+  TcScale* scale = reinterpret_cast<TcScale*>((reinterpret_cast<uintptr_t>(munorm + kp) + 31) & ~uintptr_t(31));
   TcParams tp{};
   tp.p = p;
   tp.ncb = ncb;
   tp.nkc = nkc;
   tp.colbias = colbias;
-  tp.clu = clu;
   tp.munorm = munorm;
   tp.scale = scale;
   tp.nstg = tc_stages(bn, kp, c->smem_optin);
   if (const char* e = std::getenv("FSIL_TC_NSTG")) tp.nstg = std::max(2, std::min(tp.nstg, std::atoi(e)));  // experiments
+  tp.split = c->d > 128 ? 1 : 0;
+  if (const char* e = std::getenv("FSIL_TC_SPLIT")) tp.split = std::atoi(e) ? 1 : 0;  // experiments
   // decoupled A slots: one cluster block, per-row ||x||^2 from the aggregation pass, and
   // room for >= 2 X stages besides the two slots
   tp.nsa = 0;
@@ -1169,6 +1078,21 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
       tp.nstg -= 2;
     }
   }
+  // three epilogue groups (decoupled mode at BN = 32, where the epilogue paces the kernel);
+  // its six accumulator buffers must fit the 256-column allocation (no split accumulators)
+  static const bool eg3_env = [] {
+    const char* e = std::getenv("FSIL_TC_EG3");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool eg3 = eg3_env && bn == 32 && tp.nsa > 0 && !tp.split;
+  // unit x scale exactly where the converters take the multiply-free path (the
+  // three-group kernel); its subnormal floor is bounded per row (floor_x / ||x||)
+  const bool unit_ok = eg3;
+  launch_pdl(c, prep_b_kernel, kp, 128, 0, p.stats, c->bound.as<float>(), c->xmax.as<float>(), c->k, c->d, kp, dp,
+             cos, bh, bl, colbias, munorm, scale, p.abort, unit_ok);
+  const CUtensorMap mx = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, c->X, c->d, c->n, c->d * 4ull, 32, BM);
+  const CUtensorMap mh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, bh, dp, kp, dp * 2ull, BK, bn);
+  const CUtensorMap ml = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, bl, dp, kp, dp * 2ull, BK, bn);
   {
     const int64_t ntiles_ = (c->n + BM - 1) / BM;
     const bool ares_ = ncb > 1 && 2 * nkc <= tp.nstg;
@@ -1178,16 +1102,19 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
       tp.ascratch = c->a_scratch.as<uint8_t>();
     }
   }
-  // |dot error| <= cdot*||x||*||mu|| + floor: split residuals 3*2^-22 relative; fp32
-  // accumulation of the main term over ceil(D/16) MMA steps at 2^-24 (the correction
-  // accumulator holds values <= 2^-10 of it); the final main+correction add; and the
-  // fp16 subnormal floor 2^-25 per element in scaled units (sqrt(D) via Cauchy-Schwarz).
+  // |dot error| <= cdot*||x||*||mu|| + floors.  Split residuals: 3 * 2^-22 relative.
+  // Accumulation: tcgen05 fp32 accumulation is NOT round-to-nearest -- each MMA (K = 16)
+  // adds its exact fp16 products to the accumulator and truncates (the sign pattern of the
+  // round-1 bias).  The model charged here is kMmaUlp ulps (2u each) of the running
+  // |partial sum| <= ||x~|| ||mu~|| per MMA, pinned on the hardware by
+  // tests/test_tc_numerics.py (adversarial operands, max observed error per MMA).
+  // Single accumulator: 3 MMAs per 16-element K step; split: the main term's `steps`
+  // MMAs, the corrections (<= 2^-10 of it) separately, plus the final fp32 add (u).
   const float u = 5.9604645e-8f;
+  constexpr float kMmaUlp = 2.0f;
   const float steps = static_cast<float>((c->d + 15) / 16);
-  tp.split = c->d > 128 ? 1 : 0;
-  if (const char* e = std::getenv("FSIL_TC_SPLIT")) tp.split = std::atoi(e) ? 1 : 0;  // experiments
-  tp.cdot = tp.split ? 1.05f * (12.0f + steps + 1.0f + 2.0f * steps / 512.0f) * u
-                     : 1.05f * (12.0f + 3.0f * steps + 1.0f) * u;  // all 3 terms, one accumulator
+  tp.cdot = tp.split ? 1.05f * (12.0f + 2.0f * kMmaUlp * steps + 1.0f + 2.0f * kMmaUlp * 2.0f * steps / 512.0f) * u
+                     : 1.05f * (12.0f + 2.0f * kMmaUlp * 3.0f * steps + 1.0f) * u;
   // fp64 front end: the fast pass reads the fp32 rounding of the caller's features
   // (|x32 - x| <= u|x|): +u on the dots, +2.1u on ||x||^2
   tp.exic = 8.1f;
@@ -1202,11 +1129,6 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   // lean converters: only where the batched aggregation wrote ||x||^2 (C1/C2-like shapes);
   // the label-sorted path's ||x||^2 goes to the epilogue through the usual hand-off
   tp.lean = tp.xi_rows && c->agg_path == 3 ? 1 : 0;
-  c->exact_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int2));
-  c->exact_count.ensure(sizeof(unsigned long long));
-  // (exact_count was zeroed by agg_init)
-  tp.exact_rows = c->exact_rows.as<int2>();
-  tp.exact_count = c->exact_count.as<unsigned long long>();
   const int64_t ntiles = (c->n + BM - 1) / BM;
   static const bool prof = std::getenv("FSIL_TC_PROFILE") != nullptr;
   unsigned long long* dbg = nullptr;
@@ -1224,12 +1146,6 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   tp.trace = trc;
   // K <= 24 at BN = 32: the epilogue scans only the first 16 / 24 columns
   const int kc_scan = bn == 32 && c->k <= 16 ? 16 : bn == 32 && c->k <= 24 ? 24 : 32;
-  // three epilogue groups (decoupled mode at BN = 32, where the epilogue paces the kernel)
-  static const bool eg3_env = [] {
-    const char* e = std::getenv("FSIL_TC_EG3");
-    return !e || std::atoi(e) != 0;
-  }();
-  const bool eg3 = eg3_env && bn == 32 && tp.nsa > 0;
   if (cos) {
     if (eg3 && kc_scan == 16) launch_tc<32, true, 16, 3>(c, mx, mh, ml, tp, ntiles);
     else if (eg3 && kc_scan == 24) launch_tc<32, true, 24, 3>(c, mx, mh, ml, tp, ntiles);
@@ -1249,7 +1165,6 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     else if (bn == 64) launch_tc<64, false>(c, mx, mh, ml, tp, ntiles);
     else launch_tc<128, false>(c, mx, mh, ml, tp, ntiles);
   }
-  c->tc_exact_used = true;
   if (trc) {
     long long h[64 * 9];
     FSIL_CUDA(cudaMemcpyAsync(h, trc, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
