@@ -7,6 +7,7 @@ with the repo snapshot to the GPU box).
 Products (git-ignored, not gpurun-ignored):
     paper_2303_14102_b200/libfsil.so         the product: C ABI of include/fsil.h
     paper_2303_14102_b200/libfsil_datagen.so synthetic config generators (bench/test inputs)
+    paper_2303_14102_b200/libfsil_probe.so   tcgen05 accumulation probe (tests only)
 """
 from __future__ import annotations
 
@@ -29,6 +30,8 @@ LIBS = {
     "libfsil.so": ["densify.cu", "aggregate.cu", "score_ffma.cu", "score_tc.cu", "naive.cu", "finalize.cu",
                    "capi.cu"],
     "libfsil_datagen.so": ["datagen.cu"],
+    # test infrastructure: the tcgen05 accumulation probe (tests/test_tc_numerics.py)
+    "libfsil_probe.so": ["tc_probe.cu"],
 }
 
 

@@ -458,59 +458,92 @@ template <bool COS, typename T, int LPR, int CPL>
 __device__ __forceinline__ void exact_units(const ScoreParams& p, const double* ytab, double* __restrict__ usum,
                                             int64_t nunits, int64_t wid, int64_t nw, int lane) {
   using V = typename PairOf<T>::V;
-  constexpr int RPP = 32 / LPR;  // rows per pass
+  constexpr int RPP = 32 / LPR;           // rows per pass
+  constexpr int PPU = kUnitRows / RPP;    // passes per unit (= LPR)
   const int sub = lane / LPR, li = lane % LPR;
   const int d = p.d, d2 = p.d >> 1;
   const T* X = sizeof(T) == 8 ? reinterpret_cast<const T*>(p.X64) : reinterpret_cast<const T*>(p.X);
-  for (int64_t u = wid; u < nunits; u += nw) {
-    const int64_t r0 = u * kUnitRows;
-    double su = 0.0;  // this lane group's rows, ascending
-    if constexpr (CPL > 0) {
-#pragma unroll 1
-      for (int pass = 0; pass < kUnitRows / RPP; pass += 2) {
-        V xv[2][CPL];
-        int64_t row[2];
-        int own[2], nbr[2];
+  if (wid >= nunits) return;
+  if constexpr (CPL > 0) {
+    // The warp's passes (units wid, wid + nw, ...; PPU passes each) form one stream with a
+    // rolling register ring: pass j + DEPTH is loaded while pass j is reduced, so DEPTH
+    // passes' rows are always in flight (the pass is HBM-latency bound otherwise).
+    constexpr int DEPTH = CPL >= 8 ? 2 : 4;
+    static_assert(PPU % DEPTH == 0, "a unit must end on a ring boundary");
+    const int64_t npass = ((nunits - 1 - wid) / nw + 1) * PPU;
+    V buf[DEPTH][CPL];
+    int bown[DEPTH], bnb[DEPTH];
+    // after the unit's PPU passes, lane L holds row L's three dots: the fp64 finish (five
+    // divisions) then runs once per unit with every lane active, and s_i is stored coalesced
+    double rss = 0.0, rco = 0.0, rcb = 0.0;
+    int rown = 0, rnb = 0;
+    const int src_lane = (lane % RPP) * LPR;  // group leader holding row (pass * RPP + lane % RPP)
+    auto row_of = [&](int64_t j) { return (wid + (j / PPU) * nw) * kUnitRows + (j % PPU) * RPP + sub; };
+    auto load = [&](int64_t j, V (&b)[CPL], int& o, int& nb) {
+      const int64_t row = row_of(j);
+      const bool ok = j < npass && row < p.n;
+      const V* xr = reinterpret_cast<const V*>(X + (ok ? row : 0) * d);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {  // both passes' loads first (memory-level parallelism)
-          row[h] = r0 + (pass + h) * RPP + sub;
-          const bool ok = row[h] < p.n;
-          const V* xr = reinterpret_cast<const V*>(X + (ok ? row[h] : 0) * d);
+      for (int c = 0; c < CPL; ++c) b[c] = xr[li + LPR * c];
+      o = ok ? __ldg(p.dense + row) : 0;
+      nb = ok ? p.nb[row] : 0;
+    };
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) xv[h][c] = xr[li + LPR * c];
-          own[h] = ok ? __ldg(p.dense + row[h]) : 0;
-          nbr[h] = ok ? p.nb[row[h]] : 0;
+    for (int h = 0; h < DEPTH; ++h) load(h, buf[h], bown[h], bnb[h]);
+    for (int64_t j0 = 0; j0 < npass; j0 += DEPTH) {
+#pragma unroll
+      for (int h = 0; h < DEPTH; ++h) {
+        const int64_t j = j0 + h;
+        const int own = bown[h], nb = bnb[h];
+        const double* yo = ytab + static_cast<int64_t>(own) * d;
+        const double* yb = ytab + static_cast<int64_t>(nb) * d;
+        double ss = 0.0, co = 0.0, cb = 0.0;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int q = li + LPR * c;
+          const double2 o = *reinterpret_cast<const double2*>(yo + 2 * q);
+          const double2 b = *reinterpret_cast<const double2*>(yb + 2 * q);
+          const double x0 = static_cast<double>(buf[h][c].x), x1 = static_cast<double>(buf[h][c].y);
+          ss = fma(x0, x0, ss);
+          ss = fma(x1, x1, ss);
+          co = fma(o.x, x0, co);
+          co = fma(o.y, x1, co);
+          cb = fma(b.x, x0, cb);
+          cb = fma(b.y, x1, cb);
         }
+        load(j + DEPTH, buf[h], bown[h], bnb[h]);  // refill the slot just consumed
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const double* yo = ytab + static_cast<int64_t>(own[h]) * d;
-          const double* yb = ytab + static_cast<int64_t>(nbr[h]) * d;
-          double ss = 0.0, co = 0.0, cb = 0.0;
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            const int q = li + LPR * c;
-            const double2 o = *reinterpret_cast<const double2*>(yo + 2 * q);
-            const double2 b = *reinterpret_cast<const double2*>(yb + 2 * q);
-            const double x0 = static_cast<double>(xv[h][c].x), x1 = static_cast<double>(xv[h][c].y);
-            ss = fma(x0, x0, ss);
-            ss = fma(x1, x1, ss);
-            co = fma(o.x, x0, co);
-            co = fma(o.y, x1, co);
-            cb = fma(b.x, x0, cb);
-            cb = fma(b.y, x1, cb);
-          }
-#pragma unroll
-          for (int off = LPR >> 1; off > 0; off >>= 1) {
-            ss += __shfl_xor_sync(0xffffffffu, ss, off);
-            co += __shfl_xor_sync(0xffffffffu, co, off);
-            cb += __shfl_xor_sync(0xffffffffu, cb, off);
-          }
-          if (li == 0 && row[h] < p.n) su += exact_finish<COS>(p, row[h], own[h], nbr[h], ss, co, cb);
+        for (int off = LPR >> 1; off > 0; off >>= 1) {
+          ss += __shfl_xor_sync(0xffffffffu, ss, off);
+          co += __shfl_xor_sync(0xffffffffu, co, off);
+          cb += __shfl_xor_sync(0xffffffffu, cb, off);
+        }
+        const double vss = __shfl_sync(0xffffffffu, ss, src_lane), vco = __shfl_sync(0xffffffffu, co, src_lane),
+                     vcb = __shfl_sync(0xffffffffu, cb, src_lane);
+        const int vown = __shfl_sync(0xffffffffu, own, src_lane), vnb = __shfl_sync(0xffffffffu, nb, src_lane);
+        if (lane / RPP == static_cast<int>(j % PPU)) {
+          rss = vss;
+          rco = vco;
+          rcb = vcb;
+          rown = vown;
+          rnb = vnb;
         }
       }
-    } else {  // any even D: one row per pass, LPR lanes stride the pairs
+      if ((j0 + DEPTH) % PPU == 0) {  // a unit ends here: one row per lane, fixed-order tree
+        const int64_t u = wid + ((j0 + DEPTH) / PPU - 1) * nw;
+        const int64_t row = u * kUnitRows + lane;
+        double su = row < p.n ? exact_finish<COS>(p, row, rown, rnb, rss, rco, rcb) : 0.0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) su += __shfl_xor_sync(0xffffffffu, su, off);
+        if (lane == 0) usum[u] = su;
+      }
+    }
+  } else {  // any even D: one row per pass, LPR lanes stride the pairs
+    for (int64_t u = wid; u < nunits; u += nw) {
+      const int64_t r0 = u * kUnitRows;
+      double su = 0.0;
 #pragma unroll 1
-      for (int pass = 0; pass < kUnitRows / RPP; ++pass) {
+      for (int pass = 0; pass < PPU; ++pass) {
         const int64_t row = r0 + pass * RPP + sub;
         const bool ok = row < p.n;
         const V* xr = reinterpret_cast<const V*>(X + (ok ? row : 0) * d);
@@ -536,11 +569,10 @@ __device__ __forceinline__ void exact_units(const ScoreParams& p, const double* 
         }
         if (li == 0 && ok) su += exact_finish<COS>(p, row, own, nb, ss, co, cb);
       }
-    }
-    // fixed-order tree over the RPP row groups (lanes 0, LPR, 2 LPR, ...)
 #pragma unroll
-    for (int off = 16; off >= LPR; off >>= 1) su += __shfl_xor_sync(0xffffffffu, su, off);
-    if (lane == 0) usum[u] = su;
+      for (int off = 16; off >= LPR; off >>= 1) su += __shfl_xor_sync(0xffffffffu, su, off);
+      if (lane == 0) usum[u] = su;
+    }
   }
 }
 
@@ -731,11 +763,12 @@ void exact_pass(fsil_context* c, const ScoreParams& p, bool local) {
   const int d = c->d;
   int lpr = 32, cpl = 0;
   if (!x64) {
+    // (a row's 16-byte pairs: 8 lanes read a table row's 128-byte line conflict-free)
     if (d == 16) lpr = 4, cpl = 2;
     else if (d == 32) lpr = 4, cpl = 4;
     else if (d == 64) lpr = 8, cpl = 4;
-    else if (d == 128) lpr = 16, cpl = 4;
-    else if (d == 256) lpr = 32, cpl = 4;
+    else if (d == 128) lpr = 8, cpl = 8;
+    else if (d == 256) lpr = 16, cpl = 8;
     else if (d == 512) lpr = 32, cpl = 8;
     else if (d == 768) lpr = 32, cpl = 12;
   }
@@ -747,8 +780,8 @@ void exact_pass(fsil_context* c, const ScoreParams& p, bool local) {
 #define FSIL_EXACT_K(T, L, C)                                                                             \
   if (!kern && (sizeof(T) == 8) == x64 && lpr == L && cpl == C)                                           \
     kern = cos ? reinterpret_cast<void*>(exact_kernel<true, T, L, C>) : reinterpret_cast<void*>(exact_kernel<false, T, L, C>);
-  FSIL_EXACT_K(float, 4, 2) FSIL_EXACT_K(float, 4, 4) FSIL_EXACT_K(float, 8, 4) FSIL_EXACT_K(float, 16, 4)
-  FSIL_EXACT_K(float, 32, 4) FSIL_EXACT_K(float, 32, 8) FSIL_EXACT_K(float, 32, 12) FSIL_EXACT_K(float, 32, 0)
+  FSIL_EXACT_K(float, 4, 2) FSIL_EXACT_K(float, 4, 4) FSIL_EXACT_K(float, 8, 4) FSIL_EXACT_K(float, 8, 8)
+  FSIL_EXACT_K(float, 16, 8) FSIL_EXACT_K(float, 32, 8) FSIL_EXACT_K(float, 32, 12) FSIL_EXACT_K(float, 32, 0)
   FSIL_EXACT_K(double, 32, 0)
 #undef FSIL_EXACT_K
   if (!kern) fail(FSIL_ERR_INTERNAL, "no exact-pass kernel for this shape");
