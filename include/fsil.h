@@ -77,10 +77,11 @@ typedef struct {
   int32_t path;            /* fsil_path actually used */
   int32_t agg_path;        /* 1 = warp-private shared-memory, 2 = label-sorted segments, 3 = two-phase batches */
   int64_t flagged_rows;    /* rows re-evaluated by the fp64 argmin refinement kernel */
-  int64_t exact_rows;      /* rows whose a_i, b_i were recomputed exactly (tcgen05 path) */
+  int64_t exact_rows;      /* rows whose a_i, b_i, s_i came from the fp64 exact pass (tcgen05 path: all) */
   int64_t kernel_launches; /* kernels launched by the last call */
   float ms_densify, ms_aggregate, ms_score, ms_refine, ms_finalize; /* device time, 0 unless timing on */
   float ms_score_kernel;   /* the scoring kernel alone (ms_score minus its operand preparation) */
+  int64_t pair_rows;       /* rows whose neighbour was one of two certified candidates, decided in fp64 */
 } fsil_stats;
 
 fsil_status fsil_create(fsil_context** ctx, int device);

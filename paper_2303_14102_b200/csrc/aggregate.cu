@@ -840,7 +840,8 @@ int pick_lpr(int d, int vec) {
 
 // stats <- 0, validation word <- none, max|x| <- 0 (one launch instead of three copies)
 __global__ void agg_init_kernel(double* stats, int64_t S, int64_t* checks, float* xmax, float* bound,
-                                double* result, unsigned long long* flag_count) {
+                                double* result, unsigned long long* flag_count,
+                                unsigned long long* pair_count) {
   griddep_wait();
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   for (int64_t i = i0; i < S; i += static_cast<int64_t>(gridDim.x) * blockDim.x) stats[i] = 0.0;
@@ -852,6 +853,7 @@ __global__ void agg_init_kernel(double* stats, int64_t S, int64_t* checks, float
     // the scoring phase's counters and partial result (no separate memsets per call)
     for (int i = 0; i < 4; ++i) result[i] = 0.0;
     *flag_count = 0ull;
+    *pair_count = 0ull;
   }
 }
 
@@ -943,9 +945,10 @@ void aggregate(fsil_context* c) {
   c->bound.ensure(4 * sizeof(float));
   c->result.ensure(4 * sizeof(double));
   c->flag_count.ensure(sizeof(unsigned long long));
+  c->pair_count.ensure(sizeof(unsigned long long));
   launch_pdl(c, agg_init_kernel, static_cast<unsigned>(std::min<int64_t>((S + 255) / 256 + 1, 1024)), 256, 0, stats,
              S, checks, c->xmax.as<float>(), c->bound.as<float>(), c->result.as<double>(),
-             c->flag_count.as<unsigned long long>());
+             c->flag_count.as<unsigned long long>(), c->pair_count.as<unsigned long long>());
   if (c->n == 0) {
     c->agg_path = 0;
     return;

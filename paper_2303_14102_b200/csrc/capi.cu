@@ -248,6 +248,7 @@ __global__ void pack_summary_kernel(const int64_t* __restrict__ checks, const do
     out->result[0] = result[0];
     out->result[1] = result[1];
     out->result[2] = result[2];
+    out->result[3] = result[3];
   }
 }
 
@@ -275,7 +276,7 @@ double finish(fsil_context* c, double* flagged_out) {
     }
   }
   const int64_t checks[2] = {hs->checks[0], hs->checks[1]};
-  const double res[3] = {hs->result[0], hs->result[1], hs->result[2]};
+  const double res[4] = {hs->result[0], hs->result[1], hs->result[2], hs->result[3]};
   const int missing = static_cast<int>(hs->missing);
   FSIL_CUDA(cudaGetLastError());
   c->phase = 0;
@@ -302,6 +303,7 @@ double finish(fsil_context* c, double* flagged_out) {
   c->stats.agg_path = c->agg_path;
   c->stats.flagged_rows = static_cast<int64_t>(res[1]);
   c->stats.exact_rows = static_cast<int64_t>(res[2]);
+  c->stats.pair_rows = static_cast<int64_t>(res[3]);
   c->stats.kernel_launches = c->launches;
   if (c->timing) {
     float* ms[5] = {&c->stats.ms_densify, &c->stats.ms_aggregate, &c->stats.ms_score,
@@ -453,7 +455,7 @@ void fsil_destroy(fsil_context* c) {
                           &c->sort_tmp, &c->sort_keys, &c->sort_vals, &c->iota, &c->seg_start,
                           &c->piece_start, &c->mu32, &c->p32, &c->nk, &c->bound, &c->s_tmp,
                           &c->tile_sum, &c->tile_flag, &c->flag_rows, &c->flag_count, &c->result,
-                          &c->group_sum, &c->xmax, &c->tc_b, &c->nb_tmp, &c->a_scratch, &c->x32, &c->xbuf, &c->xt_keys, &c->xt_vals, &c->xt_dense, &c->hX, &c->hL, &c->o_s, &c->o_nb, &c->o_own, &c->o_a,
+                          &c->group_sum, &c->xmax, &c->tc_b, &c->nb_tmp, &c->pair_rows, &c->pair_count, &c->a_scratch, &c->x32, &c->xbuf, &c->xt_keys, &c->xt_vals, &c->xt_dense, &c->hX, &c->hL, &c->o_s, &c->o_nb, &c->o_own, &c->o_a,
                           &c->o_b};
   for (auto* b : bufs) b->release();
   for (auto& e : c->ev)

@@ -262,6 +262,7 @@ struct TotalArgs {
   double* result;                        // [0] sum s_i, [1] flagged rows, [2] exact rows
   const unsigned long long* flag_count;
   const unsigned long long* exact_count;  // null if unused
+  const unsigned long long* pair_count;   // tcgen05 top-3 certified pairs (null if unused)
   unsigned int* ticket;                   // zero on entry; reset by the last block
   HostSummary* hsum;                      // single GPU: summary target (null in shard mode)
   const int64_t* checks;
@@ -428,6 +429,7 @@ struct ExactArgs {
   int64_t nunits;
   TotalArgs ta;
   unsigned int* bar;  // grid-barrier words (cooperative launch with the refinement phase)
+  const int2* pairs;  // certified pairs (resolved with the refinement phase)
   int refine;         // 1: refine the flagged rows first (cooperative launch), then barrier
   int stage;          // 1: the cluster-sum table is staged in shared memory
 };
@@ -592,9 +594,11 @@ __device__ __forceinline__ void unit_total(const ExactArgs& ea, int64_t exact_ro
     const TotalArgs& ta = ea.ta;
     const double flagged = static_cast<double>(*ta.flag_count);
     const double exact = static_cast<double>(exact_rows);
+    const double pairs = ta.pair_count ? static_cast<double>(*ta.pair_count) : 0.0;
     ta.result[0] = red[0];
     ta.result[1] = flagged;
     ta.result[2] = exact;
+    ta.result[3] = pairs;
     if (ta.hsum) {
       ta.hsum->checks[0] = ta.checks[0];
       ta.hsum->checks[1] = ta.checks[1];
@@ -602,9 +606,62 @@ __device__ __forceinline__ void unit_total(const ExactArgs& ea, int64_t exact_ro
       ta.hsum->result[0] = red[0];
       ta.hsum->result[1] = flagged;
       ta.hsum->result[2] = exact;
+      ta.hsum->result[3] = pairs;
     }
     *ta.ticket = 0u;
   }
+}
+
+// Certified pairs (tcgen05 top-3): the neighbour is one of two columns {nb[row], c2}.
+// One warp per pair: the two fp64 foreign means with the reference formula, clamp
+// included, then the reference's rule -- strict <, equal means keep the lower index
+// (squared_euclidean.cpp:94-103, cosine.cpp:103-112).
+template <bool COS>
+__device__ __forceinline__ void pair_rows_body(const ScoreParams& p, const int2* __restrict__ pairs,
+                                               const unsigned long long* count, const double* sums, int64_t warp,
+                                               int64_t nwarps, int lane) {
+  const int64_t cnt = static_cast<int64_t>(*count);
+  const int d = p.d;
+  for (int64_t i = warp; i < cnt; i += nwarps) {
+    const int2 pr = pairs[i];
+    const int64_t row = pr.x;
+    const int c1 = p.nb[row], c2 = pr.y;
+    const double* y1 = sums + static_cast<int64_t>(c1) * d;
+    const double* y2 = sums + static_cast<int64_t>(c2) * d;
+    double ss = 0.0, d1 = 0.0, d2 = 0.0;
+    for (int l = lane; l < d; l += 32) {
+      const double v = xval(p, row * d + l);
+      ss = fma(v, v, ss);
+      d1 = fma(y1[l], v, d1);
+      d2 = fma(y2[l], v, d2);
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      ss += __shfl_xor_sync(0xffffffffu, ss, off);
+      d1 += __shfl_xor_sync(0xffffffffu, d1, off);
+      d2 += __shfl_xor_sync(0xffffffffu, d2, off);
+    }
+    if (lane == 0) {
+      double m1, m2;
+      if (COS) {
+        const double nrm = sqrt(ss);
+        m1 = cos_foreign(p.nk[c1], d1 / nrm);
+        m2 = cos_foreign(p.nk[c2], d2 / nrm);
+      } else {
+        m1 = sq_foreign(ss, p.stats[p.k + c1], p.nk[c1], d1);
+        m2 = sq_foreign(ss, p.stats[p.k + c2], p.nk[c2], d2);
+      }
+      p.nb[row] = (m2 < m1 || (m2 == m1 && c2 < c1)) ? c2 : c1;
+    }
+  }
+}
+
+template <bool COS>
+__global__ void __launch_bounds__(256) pair_kernel(ScoreParams p, const int2* __restrict__ pairs,
+                                                   const unsigned long long* count) {
+  if (*p.abort) return;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  pair_rows_body<COS>(p, pairs, count, p.stats + (COS ? p.k : 2 * p.k), warp, nwarps, threadIdx.x & 31);
 }
 
 // Refinement of the flagged rows (cooperative launch, small cluster tables) -> grid
@@ -626,9 +683,11 @@ __global__ void __launch_bounds__(kExactThreads) exact_kernel(ScoreParams p, Exa
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib;
   const int64_t gnw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   if (ea.refine) {
-    if (!abort)
+    if (!abort) {
       refine_rows<COS>(p, esm + (ea.stage ? tab : 0) + static_cast<int64_t>(wib) * p.d, gw, gnw, lane,
                        ea.stage ? esm : nullptr);
+      if (ea.ta.pair_count) pair_rows_body<COS>(p, ea.pairs, ea.ta.pair_count, ytab, gw, gnw, lane);
+    }
     grid_barrier(ea.bar, ea.bar + 1);  // every refined neighbour is written
   }
   if (!abort) exact_units<COS, T, LPR, CPL>(p, ytab, ea.usum, ea.nunits, gw, gnw, lane);
@@ -686,6 +745,7 @@ TotalArgs total_args(fsil_context* c, const ScoreParams& p, int64_t ngroups, boo
   ta.result = c->result.as<double>();
   ta.flag_count = p.flag_count;
   ta.exact_count = nullptr;
+  ta.pair_count = nullptr;
   ta.ticket = reinterpret_cast<unsigned int*>(c->counters.as<int>() + 8);
   ta.hsum = local ? c->dsum : nullptr;
   ta.checks = c->checks.as<int64_t>();
@@ -745,7 +805,14 @@ void exact_pass(fsil_context* c, const ScoreParams& p, bool local) {
   const bool x64 = c->X64 != nullptr;
   const int64_t tab = static_cast<int64_t>(c->k) * c->d;
   const bool small = tab < 64 * 1024;
-  if (!small) refine(c, p);
+  const unsigned long long* pcount = c->pair_count.as<unsigned long long>();
+  if (!small) {  // full refinements (tiled) and certified pairs as their own launches
+    refine(c, p);
+    const unsigned pgrid = static_cast<unsigned>(c->num_sms * 8);
+    if (cos) pair_kernel<true><<<pgrid, 256, 0, c->stream>>>(p, c->pair_rows.as<int2>(), pcount);
+    else pair_kernel<false><<<pgrid, 256, 0, c->stream>>>(p, c->pair_rows.as<int2>(), pcount);
+    FSIL_LAUNCHED(c);
+  }
   const size_t tab_bytes = static_cast<size_t>(tab) * sizeof(double);
   const size_t rows_bytes = small ? (kExactThreads / 32) * static_cast<size_t>(c->d) * sizeof(double) : 0;
   const bool stage = tab_bytes + rows_bytes <= std::min<size_t>(c->smem_optin, 200 * 1024);
@@ -756,6 +823,8 @@ void exact_pass(fsil_context* c, const ScoreParams& p, bool local) {
   ea.usum = c->group_sum.as<double>();
   ea.ta = total_args(c, p, 1, local);
   ea.ta.group_sum = nullptr;
+  ea.ta.pair_count = pcount;  // zeroed by agg_init; written only by the tcgen05 top-3 epilogue
+  ea.pairs = c->pair_rows.as<int2>();
   ea.bar = reinterpret_cast<unsigned int*>(c->counters.as<int>() + 12);
   ea.refine = small ? 1 : 0;
   ea.stage = stage ? 1 : 0;

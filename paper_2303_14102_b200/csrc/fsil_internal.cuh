@@ -99,7 +99,7 @@ struct HostSummary {
   int64_t checks[2];  // validation word (after the caller's MIN all-reduce in shard mode)
   int64_t missing;    // a row's label absent from the dictionary
   int64_t pad;
-  double result[4];   // sum of s_i, flagged rows, exact rows
+  double result[4];   // sum of s_i, flagged rows, exact rows, certified-pair rows
 };
 
 }  // namespace fsil
@@ -147,6 +147,7 @@ struct fsil_context {
   fsil::DevBuf xmax;           // float: max |x| of this shard (tensor-core operand scaling)
   fsil::DevBuf tc_b;           // fp16 cluster-mean pieces + column bias (tcgen05 path)
   fsil::DevBuf nb_tmp;                   // neighbours when the caller passes no neighbour pointer
+  fsil::DevBuf pair_rows, pair_count;    // tcgen05 top-3: rows resolved as a certified pair
   fsil::DevBuf a_scratch;                // tcgen05 streaming mode: per-CTA converted A chunks
   fsil::DevBuf x32;                      // fp64 front end: rounded fp32 copy for the fast pass
   fsil::DevBuf xi_rows;                  // fp64 ||x||^2 per row, written by the batched aggregation

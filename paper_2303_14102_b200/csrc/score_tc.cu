@@ -69,7 +69,9 @@ struct TcParams {
   float exic;             // ||x||^2 relative error / u: 8.1 (fp32 blocks of 8), +2.1 on fp64 input
   const double* xi_rows;  // per-row fp64 ||x||^2 from the aggregation pass (or null: converters form it)
   long long* trace;       // FSIL_TRACE builds: per-tile role timestamps of CTA 0 (or null)
-  int lean;               // converters only convert; the epilogue fetches own/clu/||x||^2 itself
+  int lean;               // converters only convert; the epilogue fetches own/||x||^2 itself
+  int2* pair_rows;        // T3: rows whose neighbour is one of {nb, .y} (certified pair)
+  unsigned long long* pair_count;
 };
 
 // Timeline tracing (compile with -DFSIL_TRACE, run with FSIL_TC_TRACE=1): CTA 0 records
@@ -132,7 +134,10 @@ static_assert(4 * FSIL_WG0_REGS + 8 * FSIL_EPI_REGS + 8 * FSIL_CONV_REGS <= 20 *
 // the padding columns; otherwise 32)
 // EG: epilogue groups.  3 only in decoupled mode at BN = 32 (C2): warps 4..15 are three
 // groups of four taking tiles round-robin, warps 16..19 the converters (one row each).
-template <int BN, bool COS, bool PROF, int KC, int EG = 2>
+// T3: the epilogue also tracks the third-best key and the runner-up's column, so a row
+// whose top-2 is uncertain but whose third-best is clear resolves as a certified pair (two
+// fp64 foreign means) instead of a full K x D refinement (large cluster tables, C5).
+template <int BN, bool COS, bool PROF, int KC, int EG = 2, bool T3 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
                     const __grid_constant__ CUtensorMap tmap_bl, TcParams tp, int64_t ntiles) {
@@ -195,8 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 48);
   uint64_t* scr_ready = bars + 49;         // [1] a tile's converted chunks are in scratch
   double* meta_xi = reinterpret_cast<double*>(bars + 50);   // [2][2][BM] ||x||^2 halves
-  float* part = reinterpret_cast<float*>(meta_xi + 4 * BM);  // [2][3][BM] second-half partial top-2
-  int* meta_own = reinterpret_cast<int*>(part + 6 * BM);      // [2][BM] own cluster per row
+  float* part = reinterpret_cast<float*>(meta_xi + 4 * BM);  // [2][5][BM] second-half partial top-2/3
+  int* meta_own = reinterpret_cast<int*>(part + 10 * BM);     // [2][BM] own cluster per row
   float* cb_s = reinterpret_cast<float*>(meta_own + 2 * BM);  // [ncb*BN] column bias
   __half* mn_s = reinterpret_cast<__half*>(cb_s + ncb_bn_pad(tp.ncb * BN));  // [ncb*BN] ||mu_k||/mu_max, rounded up
 
@@ -752,8 +757,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ranking key m' = m - rowc (row constant dropped, no clamp): sqeuclid
       // m = xi + p_k - 2 dot, cosine m = 1 - dot/||x||; dot = acc * smul
       const float rowm = COS ? -(sc.smul * rnf) : -2.0f * sc.smul;
-      float b1 = INFINITY, b2 = INFINITY;
-      int arg = -1;
+      float b1 = INFINITY, b2 = INFINITY, b3 = INFINITY;
+      int arg = -1, arg2 = -1;
       for (int cb = 0; cb < ncb; ++cb) {
         int ab;
         uint32_t ph;
@@ -786,12 +791,19 @@ __global__ void __launch_bounds__(kThreads, 1)
               float m = fmaf(acc, rowm, bj[e]);
               m = j == ownrel ? INFINITY : m;
               const bool lt = m < b1;  // strict: the lowest index keeps ties
-              argc = lt ? j : argc;
+              if (T3) {
+                const bool lt2 = m < b2;
+                arg2 = lt ? arg : (lt2 ? k0 + j : arg2);
+                arg = lt ? k0 + j : arg;
+                b3 = fminf(b3, fmaxf(b2, m));
+              } else {
+                argc = lt ? j : argc;
+              }
               b2 = fminf(b2, fmaxf(b1, m));
               b1 = fminf(b1, m);
             }
           }
-          if (argc >= 0) arg = k0 + argc;
+          if (!T3 && argc >= 0) arg = k0 + argc;
         };
         const int q0 = TS ? 0 : grp, qs = TS ? 1 : 2;
         const uint32_t tb0 = tmem_base + ab * astride + (static_cast<uint32_t>(quad * 32) << 16);
@@ -827,11 +839,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long tf0 = dbgp ? clock64() : 0;
       if (!TS) {
         // ---- merge the two column halves (group 1 -> smem -> group 0)
-        float* pt = part + tb * 3 * BM;  // double-buffered by tile parity
+        float* pt = part + tb * 5 * BM;  // double-buffered by tile parity
         if (grp == 1) {
           pt[0 * BM + r] = b1;
           pt[1 * BM + r] = b2;
           pt[2 * BM + r] = __int_as_float(arg);
+          if (T3) {
+            pt[3 * BM + r] = b3;
+            pt[4 * BM + r] = __int_as_float(arg2);
+          }
         }
         named_bar(1, 256);
         if (grp == 1) {
@@ -841,10 +857,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const float c1 = pt[0 * BM + r], c2 = pt[1 * BM + r];
         const int a2 = __float_as_int(pt[2 * BM + r]);
-        const float nb1 = fminf(b1, c1);
-        b2 = fminf(fminf(fmaxf(b1, c1), b2), c2);
-        arg = (c1 < b1 || (c1 == b1 && a2 >= 0 && (arg < 0 || a2 < arg))) ? a2 : arg;
-        b1 = nb1;
+        if (T3) {
+          // merge the other half's (c1, a2), (c2, a2b), c3 into (b1, arg), (b2, arg2), b3:
+          // lexicographic (key, column) order, so equal keys keep the lowest column
+          const float c3 = pt[3 * BM + r];
+          const int a2b = __float_as_int(pt[4 * BM + r]);
+          auto before = [](float x, int ix, float y, int iy) { return x < y || (x == y && ix >= 0 && (iy < 0 || ix < iy)); };
+          auto insert = [&](float m, int im) {
+            b3 = fminf(b3, fmaxf(b2, m));
+            if (before(m, im, b1, arg)) {
+              b2 = b1;
+              arg2 = arg;
+              b1 = m;
+              arg = im;
+            } else if (before(m, im, b2, arg2)) {
+              b2 = m;
+              arg2 = im;
+            }
+          };
+          insert(c1, a2);
+          insert(c2, a2b);
+          b3 = fminf(b3, c3);
+        } else {
+          const float nb1 = fminf(b1, c1);
+          b2 = fminf(fminf(fmaxf(b1, c1), b2), c2);
+          arg = (c1 < b1 || (c1 == b1 && a2 >= 0 && (arg < 0 || a2 < arg))) ? a2 : arg;
+          b1 = nb1;
+        }
       }
       __syncwarp();
       if (lane == 0 && !tp.lean) mbar_arrive(meta_empty + tb);
@@ -876,7 +915,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool full = !((b2 - b1) > eps_m + eps_m_arg) || arg < 0 || !(rowc + b2 > eps_m) ||
                           (COS && !(rowc + b1 < 2.0f - eps_m));
         p.nb[row] = arg >= 0 ? arg : (own == 0 ? 1 : 0);  // the refinement rewrites flagged rows
-        if (full) {
+        // T3: the neighbour is one of the top two when every other column is clearly
+        // behind the winner (third-best gap, no clamp tie) -- two fp64 means decide it
+        const bool pair = T3 && full && arg >= 0 && arg2 >= 0 && (b3 - b1) > eps_m + eps_m_arg &&
+                          (rowc + b3 > eps_m) && (!COS || rowc + b1 < 2.0f - eps_m);
+        if (pair) {
+          const unsigned long long idx = atomicAdd(tp.pair_count, 1ull);
+          tp.pair_rows[idx] = make_int2(static_cast<int>(row), arg2);
+        } else if (full) {
           const unsigned long long idx = atomicAdd(p.flag_count, 1ull);
           p.flag_rows[idx] = static_cast<int32_t>(row);
         }
@@ -999,7 +1045,7 @@ int pick_bn(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : 128; }
 // meta_xi, merge partials, own clusters, column bias (fp32) and norms (fp16).
 size_t tc_smem(int bn, int kp, int nstg) {
   const size_t bring = bn <= 32 ? TcCfg<32>::kBRing : bn <= 64 ? TcCfg<64>::kBRing : TcCfg<128>::kBRing;
-  return 1024 + bring + static_cast<size_t>(nstg) * kStgBytes + 50 * 8 + 4 * BM * 8 + 6 * BM * 4 + 2 * BM * 4 +
+  return 1024 + bring + static_cast<size_t>(nstg) * kStgBytes + 50 * 8 + 4 * BM * 8 + 10 * BM * 4 + 2 * BM * 4 +
          static_cast<size_t>(ncb_bn_pad(kp)) * 4 + static_cast<size_t>(kp) * 2 + 16;
 }
 constexpr int kMaxStg = 8;
@@ -1009,10 +1055,10 @@ int tc_stages(int bn, int kp, size_t optin) {
   return ns;
 }
 
-template <int BN, bool COS, int KC = 32, int EG = 2>
+template <int BN, bool COS, int KC = 32, int EG = 2, bool T3 = false>
 void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                const TcParams& tp, int64_t ntiles) {
-  auto kern = tp.dbg ? score_tc_kernel<BN, COS, true, KC, EG> : score_tc_kernel<BN, COS, false, KC, EG>;
+  auto kern = tp.dbg ? score_tc_kernel<BN, COS, true, KC, EG, T3> : score_tc_kernel<BN, COS, false, KC, EG, T3>;
   const size_t smem = tc_smem(BN, tp.ncb * BN, tp.nstg + tp.nsa);
   if (c->timing) {  // the kernel alone, for the roofline (ms_score_kernel)
     FSIL_CUDA(cudaEventRecord(c->ev[7], c->stream));
@@ -1148,6 +1194,16 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     FSIL_CUDA(cudaMemsetAsync(trc, 0, 64 * 9 * sizeof(long long), c->stream));
   }
   tp.trace = trc;
+  // top-3 / certified pairs where a full refinement row is expensive (the tiled refinement's
+  // regime, K*D >= 64K) and the column halves are merged anyway (more than two blocks)
+  static const bool t3_env = [] {
+    const char* e = std::getenv("FSIL_TC_TOP3");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool t3 = t3_env && bn == 128 && ncb > 2 && static_cast<int64_t>(c->k) * c->d >= 64 * 1024;
+  c->pair_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int2));
+  tp.pair_rows = c->pair_rows.as<int2>();
+  tp.pair_count = c->pair_count.as<unsigned long long>();  // zeroed by agg_init
   // K <= 24 at BN = 32: the epilogue scans only the first 16 / 24 columns
   const int kc_scan = bn == 32 && c->k <= 16 ? 16 : bn == 32 && c->k <= 24 ? 24 : 32;
   if (cos) {
@@ -1158,6 +1214,7 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     else if (bn == 32 && kc_scan == 24) launch_tc<32, true, 24>(c, mx, mh, ml, tp, ntiles);
     else if (bn == 32) launch_tc<32, true>(c, mx, mh, ml, tp, ntiles);
     else if (bn == 64) launch_tc<64, true>(c, mx, mh, ml, tp, ntiles);
+    else if (t3) launch_tc<128, true, 32, 2, true>(c, mx, mh, ml, tp, ntiles);
     else launch_tc<128, true>(c, mx, mh, ml, tp, ntiles);
   } else {
     if (eg3 && kc_scan == 16) launch_tc<32, false, 16, 3>(c, mx, mh, ml, tp, ntiles);
@@ -1167,6 +1224,7 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     else if (bn == 32 && kc_scan == 24) launch_tc<32, false, 24>(c, mx, mh, ml, tp, ntiles);
     else if (bn == 32) launch_tc<32, false>(c, mx, mh, ml, tp, ntiles);
     else if (bn == 64) launch_tc<64, false>(c, mx, mh, ml, tp, ntiles);
+    else if (t3) launch_tc<128, false, 32, 2, true>(c, mx, mh, ml, tp, ntiles);
     else launch_tc<128, false>(c, mx, mh, ml, tp, ntiles);
   }
   if (trc) {

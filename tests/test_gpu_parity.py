@@ -234,16 +234,16 @@ def test_tc_cosine_mixed_norms_unit_scale(ctx):
 
 
 @pytest.mark.parametrize("metric", ["sqeuclid", "cosine"])
-@pytest.mark.parametrize("k_pad", [0, 97, 290])
-def test_tc_certificate_adversarial_near_ties(ctx, metric, k_pad):
+@pytest.mark.parametrize("k_pad,d", [(0, 64), (97, 64), (290, 64), (290, 256)])
+def test_tc_certificate_adversarial_near_ties(ctx, metric, k_pad, d):
     """Pins the neighbour certificate: rows placed at controlled distances from the
     bisector of two mirror clusters A (dense id 1) and B (dense id 2), so their top-2 gap
     runs log-uniformly from ~1e-10 to ~1e-1 relative -- across the tensor-core error bound --
     far from the origin (large ||x||, the dot-error regime).  Rows the certificate passes
     must carry exactly the oracle's neighbour; the rest go to the fp64 refinement.
-    k_pad far-away clusters add cluster blocks (BN = 128, several blocks)."""
-    rng = np.random.default_rng(17 + k_pad)
-    d = 64
+    k_pad far-away clusters add cluster blocks (BN = 128, several blocks); at D = 256 the
+    table is large enough for the top-3 epilogue, whose certified pairs must agree too."""
+    rng = np.random.default_rng(17 + k_pad + d)
     base = np.full(d, 30.0) if metric == "sqeuclid" else np.zeros(d)
     e = np.zeros(d)
     e[0] = 1.0
