@@ -2,24 +2,32 @@
 """Benchmark of the B200 linear-time Silhouette hot path (BASELINE.json metric:
 Silhouette points/sec at 1/2/4/8 B200, % of roofline).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--also C4]
+                    [--impl ours|reference]
 
 A step is one whole Silhouette of the workload: densify + cluster aggregation +
-scoring + fp64 refinement + deterministic mean (fsil_silhouette_device, inputs
-resident in HBM).  Default workload: BASELINE.json configs[1] (C2: cosine,
-N=1,000,000, D=64, K=20, fp32).  Multi-GPU (torchrun): each rank holds a
-config-sized shard (weak scaling; global N = N_config x world) and the ranks
-exchange the dictionary, the K x (D+1) statistics and the scalar sum over NCCL.
+tensor-core neighbour nomination + fp64 refinement/exact pass + deterministic
+mean, on HBM-resident inputs.  Default workload: BASELINE.json configs[4] (C5:
+cosine, N=40,000,000, D=768, K=4,096, fp32, 123 GB) -- the largest configuration
+one B200 holds; C4 (the 100M-point config of the scaling target) is measured in
+the same run and reported under "also".
 
-Prints ONE JSON line on rank 0.  The `--impl reference` arm times the CPU
-restatement of the reference path (oracle/, the reference itself cannot be
-compiled here: SURVEY.md 8c) on this host's cores.
+Scaling is STRONG: the global dataset is fixed; with N GPUs each rank generates its
+plan_shards (engine.cpp:8-25) rows of the one global dataset (byte-identical to those
+rows of the whole) and the ranks run the sharded protocol (dictionary all-gather,
+K x (D+2) fp64 all-reduce, scalar all-reduce over NCCL).  `--gpus N` without
+WORLD_SIZE in the environment re-launches itself under torch.distributed.run.
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU restatement of the
+reference path (oracle/, test infrastructure; the reference itself cannot be built
+here) on this host's cores.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,6 +41,7 @@ sys.path.insert(0, ROOT)
 
 CONFIG_ORDER = ["C1", "C2", "C3", "C4", "C5"]
 METRIC = "Silhouette points/sec (N·K dist-evals/s) at 1/2/4/8 B200; % of roofline"
+TENSOR_CONFIGS = {"C4", "C5"}  # FLOP-bound at P_tc; C1-C3 HBM-bound
 
 
 def parse():
@@ -40,15 +49,32 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2", choices=CONFIG_ORDER)
+    ap.add_argument("--config", default="C5", choices=CONFIG_ORDER)
+    ap.add_argument("--also", default=None, help="comma-separated secondary configs (default: C4 with C5)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", default="auto", choices=["auto", "ffma", "tcgen05", "fp64"])
-    ap.add_argument("--n", type=int, default=None, help="override N (parity/debug only)")
+    ap.add_argument("--n", type=int, default=None, help="override N (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU protocol (NCCL exchanges) even on one rank (path check)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.also is None:
+        a.also = "C4" if a.config == "C5" else ""
+    a.also = [c for c in a.also.split(",") if c and c != a.config]
+    return a
+
+
+def maybe_relaunch(a) -> int | None:
+    """--gpus N > 1 outside torchrun: start N ranks (one per GPU) with this same command."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def measured_peaks():
@@ -56,13 +82,28 @@ def measured_peaks():
     if os.path.exists(p):
         with open(p) as f:
             j = json.load(f)
-        return float(j["hbm_gbs"]), float(j["bf16_tflops"]), "measured"
-    return 6650.0, 1590.0, "fallback"
+        return {"hbm": float(j["hbm_gbs"]), "tc_burst": float(j["bf16_tflops"]),
+                "tc_sustained": float(j.get("bf16_tflops_sustained", j["bf16_tflops"])), "src": "measured"}
+    # B200_PROFILING.md fallback
+    return {"hbm": 6650.0, "tc_burst": 1590.0, "tc_sustained": 1590.0, "src": "fallback"}
 
 
 def bytes_per_point(d):
     # read x (4D) + label (4); write s (8) + neighbour (4)
     return 4 * d + 16
+
+
+def plan_shards(n, w):
+    """plan_shards (engine.cpp:8-25): w' = min(w, n) contiguous ranges, the first n mod w'
+    one row longer."""
+    w = max(1, min(w, n))
+    base, extra = divmod(n, w)
+    out, b = [], 0
+    for i in range(w):
+        e = b + base + (1 if i < extra else 0)
+        out.append((b, e))
+        b = e
+    return out
 
 
 class ClockSampler:
@@ -75,7 +116,6 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.rows = []
-        self._stop = threading.Event()
         self._proc = None
 
     def start(self):
@@ -114,214 +154,310 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_baseline(X, L, metric, max_rows, trials=3):
-    """CPU restatement of the reference (oracle/, TEST INFRASTRUCTURE) on this host's
-    cores: the reference's own run_two_phase window, best of 3 (bench.cpp:72-79)."""
-    import oracle
+def cpu_sample_rows(config, d, k):
+    """Rows of the CPU sample: about 3 s of the reference path's fp64 work on this host
+    (per-row cost 2KD + O(D), independent of N -- PAPER.md:238-249)."""
+    cores = os.cpu_count() or 1
+    budget_flops = 3.0e9 * cores  # ~1.3 GFLOP/s/core measured for the scalar port, x ~2.3 s
+    per_row = 2.0 * k * d + 6 * d
+    rows = int(budget_flops / per_row)
+    return int(max(2 * k, min(rows, 5_000_000)))
 
-    n = min(X.shape[0], max_rows)
-    Xs, Ls = np.ascontiguousarray(X[:n]), np.ascontiguousarray(L[:n])
+
+def cpu_sample(config, n_full):
+    """The CPU sample of a workload: the config's own generator at N = M rows (same K, D
+    and value distributions; every cluster present for C3-C5's size rules), or the first
+    M rows when the config's N is small enough to generate whole."""
+    from paper_2303_14102_b200 import datagen
+    cid, metric, N, D, K, seed = datagen.CONFIGS[config]
+    rows = min(n_full, cpu_sample_rows(config, D, K))
+    if n_full <= 5_000_000:
+        X, L, _ = datagen.generate_host(config, n=n_full)
+        X, L = X[:rows], L[:rows]
+        how = f"rows [0,{rows}) of {config}"
+    else:
+        X, L, _ = datagen.generate_host(config, n=rows)
+        how = (f"{config} recipe at N={rows} (D={D}, K={K}); per-row cost 2KD is independent of N, "
+               f"so points/s extrapolates to N={n_full}")
+    return X, L, metric, rows, how
+
+
+def cpu_baseline(config, n_full, trials=3):
+    """CPU restatement of the reference (oracle/, TEST INFRASTRUCTURE) on this host's
+    cores: the reference's own run_two_phase window (engine.hpp:107-113), best of 3
+    (bench.cpp:72-79)."""
+    import oracle
+    X, L, metric, rows, how = cpu_sample(config, n_full)
     cores = os.cpu_count() or 1
     best = None
     for _ in range(trials):
-        r = oracle.silhouette(Xs, Ls, metric, "fast", shards=cores)
+        r = oracle.silhouette(X, L, metric, "fast", shards=cores)
         best = r.wall_ms if best is None else min(best, r.wall_ms)
-    return {"value": n / (best / 1e3), "unit": "points/s", "cores": cores, "kind": "port",
-            "sample": f"rows [0,{n}) of the workload, full aggregation+scoring+mean window "
-                      f"(engine.hpp:107-113), best of {trials}", "ms": best}
+    return {"value": rows / (best / 1e3), "unit": "points/s", "cores": cores, "kind": "port",
+            "sample": how + f"; full aggregation+scoring+mean window, best of {trials}", "ms": best}
 
 
-def sample_rows(cfg, d, k):
-    # bound the CPU sample to ~10-30 s of fp64 work at ~1 GFLOP/s/core x cores
+def reference_arm(a, rank, world):
+    """--impl reference: the CPU restatement of the reference path on this host's cores,
+    rank 0 only, each step a bounded sample of the workload."""
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_2303_14102_b200 import datagen
+    cid, metric, N, D, K, seed = datagen.CONFIGS[a.config]
+    N = a.n or N
+    X, L, metric, rows, how = cpu_sample(a.config, N)
     cores = os.cpu_count() or 1
-    budget_flops = 15e9 * cores
-    per_row = 2.0 * k * d + 6 * d
-    return int(max(2000, min(budget_flops / per_row, 5_000_000)))
+    for _ in range(max(a.warmup, 0)):
+        oracle.silhouette(X, L, metric, "fast", shards=cores)
+    times = [oracle.silhouette(X, L, metric, "fast", shards=cores).wall_ms for _ in range(a.steps)]
+    ms = float(np.mean(times))
+    val = rows / (ms / 1e3)
+    out = {"metric": METRIC, "value": val, "unit": "points/s", "n_gpus": world,
+           "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": f"{a.config} ({metric}, N={N}, D={D}, K={K}); CPU step = {how}",
+                      "global_batch": rows, "seq_len": D,
+                      "parallelism": f"{cores} host threads (std::thread, engine.cpp:34-55)"},
+           "cpu_baseline": {"value": val, "unit": "points/s", "cores": cores, "kind": "port", "sample": how},
+           "e2e": {"value": val, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "gpu_launches": 0}
+    print(json.dumps(out))
+    return 0
+
+
+class Runner:
+    """One config on this rank: resident shard, timed steps, phase timing, e2e."""
+
+    def __init__(self, a, config, rank, world, local, dev):
+        import torch
+        from paper_2303_14102_b200 import Context, PATH_AUTO, PATH_FFMA, PATH_TCGEN05, datagen
+        from paper_2303_14102_b200.api import PATH_FP64
+        self.torch = torch
+        self.a, self.config, self.rank, self.world, self.dev = a, config, rank, world, dev
+        cid, self.metric, N, self.D, self.K, seed = datagen.CONFIGS[config]
+        self.cid = cid
+        self.N = (a.n or N) if config == a.config else N
+        self.b, self.e = plan_shards(self.N, world)[rank] if rank < min(world, self.N) else (self.N, self.N)
+        self.n = self.e - self.b
+        self.sharded = world > 1 or a.sharded
+        self.X, self.L, _ = datagen.generate_device(config, n=self.N, rows=(self.b, self.e), device=local)
+        torch.cuda.synchronize()
+        self.ctx = Context(local)
+        self.ctx.set_path({"auto": PATH_AUTO, "ffma": PATH_FFMA, "tcgen05": PATH_TCGEN05, "fp64": PATH_FP64}[a.path])
+        self.stream = torch.cuda.current_stream(dev)
+        self.ctx.set_stream(self.stream.cuda_stream)
+        self.s = torch.empty(self.n, dtype=torch.float64, device=dev)
+        self.nb = torch.empty(self.n, dtype=torch.int32, device=dev)
+
+    def step(self, X=None, L=None):
+        from paper_2303_14102_b200.distributed import compute_silhouette_sharded
+        X = self.X if X is None else X
+        L = self.L if L is None else L
+        if not self.sharded:
+            return self.ctx.silhouette_device(X, L, self.metric, s=self.s, neighbour=self.nb)[0]
+        return compute_silhouette_sharded(self.ctx, self.metric, X, L, self.b, self.N, s=self.s, neighbour=self.nb)
+
+    def timed(self, steps, fn):
+        """max over ranks of the device time of `steps` calls (CUDA events on the stream)."""
+        import torch.distributed as dist
+        torch = self.torch
+        if self.sharded:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(self.stream)
+        out = None
+        for _ in range(steps):
+            out = fn()
+        ev1.record(self.stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / steps
+        if self.sharded:
+            dist.barrier()
+            t = torch.tensor([ms], dtype=torch.float64, device=self.dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, out
+
+    def run(self, steps, warmup, clocks=None):
+        a = self.a
+        for _ in range(max(warmup, 3)):
+            self.step()
+        self.torch.cuda.synchronize()
+        # per-kernel timing pass (libfsil's CUDA events on its stream) for the roofline
+        self.ctx.set_timing(True)
+        phase = {k: [] for k in ("densify", "aggregate", "score", "score_kernel", "refine", "finalize")}
+        for _ in range(2):
+            self.step()
+            st = self.ctx.stats()
+            for k_ in phase:
+                phase[k_].append(st["ms_" + k_])
+        self.ctx.set_timing(False)
+        self.st = self.ctx.stats()
+        if clocks:
+            clocks.start()
+            time.sleep(0.3)
+        self.ms, self.mean = self.timed(steps, self.step)
+        self.clk = clocks.stop() if clocks else None
+        self.phases = {k_: float(np.median(v)) for k_, v in phase.items()}
+        self.value = self.N / (self.ms / 1e3)
+        return self
+
+    def roofline(self):
+        pk = measured_peaks()
+        score_ms = self.phases["score_kernel"]
+        rf = {"kernel": "tensor-core neighbour pass alone (score_tc; operand prep excluded)",
+              "peak_source": pk["src"], "points_per_launch": self.n, "launch_ms": score_ms}
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", f"ncu_{self.config}_score_summary.json")
+        if os.path.exists(prof):
+            with open(prof) as f:
+                j = json.load(f)
+            if "dram_bytes_per_point" in j:
+                traffic = j["dram_bytes_per_point"] * self.n
+                rf["traffic_source"] = f"{os.path.relpath(prof, ROOT)} (ncu --set full, per point x points)"
+            else:
+                traffic = j.get("dram_bytes_per_launch")
+        if self.config in TENSOR_CONFIGS:
+            # fp32-faithful split-precision rate: 3 fp16 MMAs per product (SURVEY 8(d)),
+            # the sustained bf16 figure for a kernel inside a long step
+            peak = pk["tc_sustained"] / 3.0
+            flops = 2.0 * self.K * self.D * self.n
+            achieved = flops / (score_ms / 1e3) / 1e12
+            rf.update({"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                       "frac": achieved / peak, "traffic": traffic, "algorithmic_flops_per_point": 2 * self.K * self.D,
+                       "peak_note": "P_tc = bf16_tflops_sustained / 3 (split-precision fp16x3)"})
+        else:
+            bpp = bytes_per_point(self.D)
+            achieved = (self.n * bpp) / (score_ms / 1e3) / 1e9
+            rf.update({"bound": "hbm", "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s",
+                       "frac": achieved / pk["hbm"], "traffic": traffic, "algorithmic_bytes_per_point": bpp})
+        return rf
+
+    def e2e(self, steps):
+        """The same metric through the host entry (pinned host X and labels copied in, s and
+        neighbour copied out, every step).  The resident device copy is released first so
+        the largest config's host entry fits (it stages its own device copy)."""
+        import ctypes
+        torch = self.torch
+        n, D = self.n, self.D
+        try:
+            hX = torch.empty((n, D), dtype=torch.float32, pin_memory=True)
+            hL = torch.empty(n, dtype=torch.int32, pin_memory=True)
+            mem = "pinned"
+        except RuntimeError:
+            hX = torch.empty((n, D), dtype=torch.float32)
+            hL = torch.empty(n, dtype=torch.int32)
+            mem = "pageable"
+        hX.copy_(self.X)
+        hL.copy_(self.L)
+        hs = torch.empty(n, dtype=torch.float64, pin_memory=mem == "pinned")
+        hnb = torch.empty(n, dtype=torch.int32, pin_memory=mem == "pinned")
+        torch.cuda.synchronize()
+        del self.X, self.L
+        torch.cuda.empty_cache()
+        if not self.sharded:
+            from paper_2303_14102_b200.api import lib, metric_code
+            mean_c, k_c = ctypes.c_double(), ctypes.c_int32()
+            h = self.ctx._h
+
+            def host_step():
+                rc = lib().fsil_silhouette(h, metric_code(self.metric), hX.data_ptr(), hL.data_ptr(), n, D,
+                                           hs.data_ptr(), hnb.data_ptr(), None, None, None,
+                                           ctypes.byref(mean_c), ctypes.byref(k_c), None)
+                if rc != 0:
+                    raise RuntimeError(lib().fsil_last_error(h).decode())
+                return mean_c.value
+            api = "fsil_silhouette (C ABI, host buffers)"
+        else:
+            dX = torch.empty((n, D), dtype=torch.float32, device=self.dev)
+            dL = torch.empty(n, dtype=torch.int32, device=self.dev)
+
+            def host_step():
+                dX.copy_(hX, non_blocking=True)
+                dL.copy_(hL, non_blocking=True)
+                m = self.step(dX, dL)
+                hs.copy_(self.s, non_blocking=True)
+                hnb.copy_(self.nb, non_blocking=True)
+                return m
+            api = "compute_silhouette_sharded (host shards copied in/out per step)"
+        host_step()
+        e_ms, mean = self.timed(steps, host_step)
+        return {"value": self.N / (e_ms / 1e3), "unit": "points/s", "ms_per_step": e_ms,
+                "h2d_bytes_per_step": (n * D * 4 + n * 4) * self.world,
+                "d2h_bytes_per_step": (n * 12 + 8) * self.world, "api": api, "host_memory": mem,
+                "steps": steps, "mean": mean}
+
+    def close(self):
+        for attr in ("X", "L", "s", "nb"):
+            if hasattr(self, attr):
+                delattr(self, attr)
+        self.ctx.close()
+        self.torch.cuda.empty_cache()
 
 
 def main():
     a = parse()
+    rc = maybe_relaunch(a)
+    if rc is not None:
+        return rc
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    from paper_2303_14102_b200.datagen import CONFIGS
-
-    cid, metric, N, D, K, seed = CONFIGS[a.config]
-    N = a.n or N
-
     if a.impl == "reference":
-        if rank != 0:
-            return 0
-        from paper_2303_14102_b200 import datagen
-        import torch
-        rows = min(N, sample_rows(a.config, D, K))
-        X, L, _ = datagen.generate_host(a.config, n=N if N <= 5_000_000 else rows)
-        X, L = X[:rows], L[:rows]
-        import oracle
-        cores = os.cpu_count() or 1
-        for _ in range(max(a.warmup, 0)):
-            oracle.silhouette(X, L, metric, "fast", shards=cores)
-        times = []
-        for _ in range(a.steps):
-            times.append(oracle.silhouette(X, L, metric, "fast", shards=cores).wall_ms)
-        ms = float(np.mean(times))
-        val = rows / (ms / 1e3)
-        out = {"metric": METRIC, "value": val, "unit": "points/s", "n_gpus": world,
-               "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-               "impl": "reference",
-               "config": {"workload": f"{a.config} ({metric}, N={N}, D={D}, K={K}); CPU step = "
-                                      f"rows [0,{rows})", "global_batch": rows, "seq_len": D,
-                          "parallelism": f"{cores} host threads (std::thread, engine.cpp:34-55)"},
-               "cpu_baseline": {"value": val, "unit": "points/s", "cores": cores, "kind": "port",
-                                "sample": f"rows [0,{rows}) of {a.config}, run_two_phase window"},
-               "e2e": {"value": val, "unit": "points/s", "h2d_bytes_per_step": 0,
-                       "d2h_bytes_per_step": 0},
-               "gpu_launches": 0}
-        print(json.dumps(out))
-        return 0
+        return reference_arm(a, rank, world)
 
     import torch
     import torch.distributed as dist
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    sharded = world > 1 or a.sharded
-    if sharded:
+    if world > 1 or a.sharded:
         dist.init_process_group("nccl", device_id=dev)
-    from paper_2303_14102_b200 import Context, PATH_AUTO, PATH_FFMA, PATH_TCGEN05
-    from paper_2303_14102_b200.api import PATH_FP64
-    from paper_2303_14102_b200 import datagen
-    from paper_2303_14102_b200.distributed import compute_silhouette_sharded
 
-    X, L, _ = datagen.generate_device(a.config, n=N, seed=seed + 7919 * rank)
-    torch.cuda.synchronize()
-    ctx = Context(local)
-    ctx.set_path({"auto": PATH_AUTO, "ffma": PATH_FFMA, "tcgen05": PATH_TCGEN05,
-                  "fp64": PATH_FP64}[a.path])
-    stream = torch.cuda.current_stream(dev)
-    ctx.set_stream(stream.cuda_stream)
-    s = torch.empty(N, dtype=torch.float64, device=dev)
-    nb = torch.empty(N, dtype=torch.int32, device=dev)
-    n_global = N * world
+    main_r = Runner(a, a.config, rank, world, local, dev)
+    main_r.run(a.steps, a.warmup, ClockSampler(local))
+    roof = main_r.roofline()
+    st = main_r.st
+    e2e = None if a.no_e2e else main_r.e2e(max(2, min(a.steps, 5)))
+    main_r.close()
 
-    def step():
-        if not sharded:
-            return ctx.silhouette_device(X, L, metric, s=s, neighbour=nb)[0]
-        return compute_silhouette_sharded(ctx, metric, X, L, rank * N, n_global, s=s, neighbour=nb)
-
-    for _ in range(max(a.warmup, 3)):
-        mean = step()
-    torch.cuda.synchronize()
-
-    # per-kernel timing pass (CUDA events inside libfsil on the same stream) for the roofline
-    ctx.set_timing(True)
-    phase = {"densify": [], "aggregate": [], "score": [], "score_kernel": [], "refine": [], "finalize": []}
-    for _ in range(3):
-        step()
-        st = ctx.stats()
-        for k_ in phase:
-            phase[k_].append(st["ms_" + k_])
-    ctx.set_timing(False)
-    launches_per_step = ctx.stats()["kernel_launches"]
-
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    if sharded:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(a.steps):
-        mean = step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    if sharded:
-        dist.barrier()
-    clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1) / a.steps
-    if sharded:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    value = n_global / (ms / 1e3)
-    st = ctx.stats()
-
-    # roofline of the dominant kernel (the scoring pass)
-    hbm, tflops, peak_kind = measured_peaks()
-    score_ms = float(np.median(phase["score_kernel"]))  # the scoring kernel alone (ev on its stream)
-    bpp = bytes_per_point(D)
-    achieved = (N * bpp) / (score_ms / 1e3) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", f"ncu_{a.config}_score_summary.json")
-    if os.path.exists(prof):
-        with open(prof) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": traffic,
-                "kernel": "scoring kernel alone (score_tc / score_ffma; operand prep excluded)", "peak_source": peak_kind,
-                "algorithmic_bytes_per_point": bpp, "points_per_launch": N,
-                "launch_ms": score_ms}
-
-    # end-to-end through the public host entry (pinned host buffers, H2D + D2H in the window)
-    e2e = None
-    if world == 1 and not a.no_e2e:
-        hX = torch.empty((N, D), dtype=torch.float32, pin_memory=True)
-        hL = torch.empty(N, dtype=torch.int32, pin_memory=True)
-        hX.copy_(X)
-        hL.copy_(L)
-        hs = torch.empty(N, dtype=torch.float64, pin_memory=True)
-        hnb = torch.empty(N, dtype=torch.int32, pin_memory=True)
-        import ctypes
-        from paper_2303_14102_b200.api import lib, metric_code
-        mean_c, k_c = ctypes.c_double(), ctypes.c_int32()
-
-        def host_step():
-            rc = lib().fsil_silhouette(ctx._h, metric_code(metric), hX.data_ptr(), hL.data_ptr(), N, D,
-                                       hs.data_ptr(), hnb.data_ptr(), None, None, None,
-                                       ctypes.byref(mean_c), ctypes.byref(k_c), None)
-            if rc != 0:
-                raise RuntimeError(lib().fsil_last_error(ctx._h).decode())
-
-        for _ in range(3):
-            host_step()
-        e_steps = max(3, min(a.steps, 10))
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(e_steps):
-            host_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e_ms = e0.elapsed_time(e1) / e_steps
-        e2e = {"value": N / (e_ms / 1e3), "unit": "points/s", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": N * D * 4 + N * 4, "d2h_bytes_per_step": N * 12 + 8,
-               "api": "fsil_silhouette (C ABI, host buffers)", "mean": mean_c.value}
+    also = {}
+    for cfg in a.also:
+        r = Runner(a, cfg, rank, world, local, dev).run(a.steps, a.warmup)
+        also[cfg] = {"value": r.value, "unit": "points/s", "ms_per_step": r.ms, "global_batch": r.N,
+                     "seq_len": r.D, "k": r.K, "metric": r.metric, "mean_silhouette": r.mean,
+                     "dist_evals_per_s": r.value * r.K, "phases_ms": r.phases, "roofline": r.roofline(),
+                     "refined_rows": r.st["flagged_rows"], "pair_rows": r.st["pair_rows"],
+                     "e2e": None if a.no_e2e else r.e2e(max(2, min(a.steps, 5)))}
+        r.close()
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        rows = min(N, sample_rows(a.config, D, K))
-        cpu = cpu_baseline(X[:rows].cpu().numpy(), L[:rows].cpu().numpy(), metric, rows)
+        cpu = cpu_baseline(a.config, main_r.N)
 
     if rank == 0:
-        out = {"metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
-               "steps": a.steps, "warmup": max(a.warmup, 3), "ms_per_step": ms,
-               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        from paper_2303_14102_b200 import datagen
+        cid = datagen.CONFIGS[a.config][0]
+        out = {"metric": METRIC, "value": main_r.value, "unit": "points/s", "n_gpus": world,
+               "steps": a.steps, "warmup": max(a.warmup, 3), "ms_per_step": main_r.ms,
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                "data": "synthetic",
-               "config": {"workload": f"{a.config}: {metric}, N={N} per GPU, D={D}, K={K}, fp32 "
-                                      f"features, int32 labels (BASELINE.json configs[{cid - 1}])",
-                          "global_batch": n_global, "seq_len": D, "parallelism": f"dp{world}",
-                          "l2": f"inputs larger than L2 ({N * D * 4 / 1e6:.0f} MB X per GPU)",
+               "config": {"workload": f"{a.config}: {main_r.metric}, N={main_r.N} (global, plan_shards rows per "
+                                      f"rank), D={main_r.D}, K={main_r.K}, fp32 features, int32 labels "
+                                      f"(BASELINE.json configs[{cid - 1}])",
+                          "global_batch": main_r.N, "seq_len": main_r.D, "parallelism": f"dp{world} (row shards)",
+                          "l2": f"inputs larger than L2 ({main_r.n * main_r.D * 4 / 1e9:.1f} GB X per GPU)",
                           "path": ["", "ffma", "tcgen05", "fp64"][st["path"]],
-                          "agg_path": ["", "warp-private smem", "label-sorted", "two-phase batches (warp-private smem)"][st["agg_path"]]},
-               "dist_evals_per_s": value * K, "mean_silhouette": mean,
-               "refined_rows": st["flagged_rows"],
-               "phases_ms": {k_: float(np.median(v)) for k_, v in phase.items()},
-               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-               "gpu_launches": int(launches_per_step) * a.steps, "clocks": clk}
+                          "agg_path": ["", "warp-private smem", "label-sorted", "two-phase batches"][st["agg_path"]]},
+               "dist_evals_per_s": main_r.value * main_r.K, "mean_silhouette": main_r.mean,
+               "refined_rows": st["flagged_rows"], "pair_rows": st["pair_rows"],
+               "phases_ms": main_r.phases, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+               "gpu_launches": int(st["kernel_launches"]) * a.steps, "clocks": main_r.clk, "also": also}
         print(json.dumps(out))
-    if sharded:
+    if world > 1 or a.sharded:
         dist.destroy_process_group()
     return 0
 

@@ -107,24 +107,26 @@ __global__ void centres_kernel(uint64_t seed, int k, int d, float scale, bool no
   for (int l = threadIdx.x; l < d; l += blockDim.x) centres[static_cast<int64_t>(c) * d + l] /= red[0];
 }
 
-__global__ void uniform_labels_kernel(uint64_t seed, int64_t n, int k, int32_t* labels) {
+__global__ void uniform_labels_kernel(uint64_t seed, int64_t row0, int64_t n, int k, int32_t* labels) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const uint64_t u = splitmix_at(seed, i);
+  const uint64_t u = splitmix_at(seed, row0 + i);
   labels[i] = static_cast<int32_t>((u >> 32) * static_cast<uint64_t>(k) >> 32);
 }
 
 // One warp per point.  mode: 0 = centre + sigma N (sqeuclid), 1 = normalise(dir +
-// sigma N) * magnitude (cosine; mag_kind 0: U(0.5,5), 1: LogNormal(0, 0.25)).
-__global__ void points_kernel(uint64_t seed_noise, uint64_t seed_mag, int64_t n, int d,
+// sigma N) * magnitude (cosine; mag_kind 0: U(0.5,5), 1: LogNormal(0, 0.25)).  Local row i
+// is global row row0 + i: every value is a function of the global index.
+__global__ void points_kernel(uint64_t seed_noise, uint64_t seed_mag, int64_t row0, int64_t n, int d,
                               const double* centres, const int32_t* labels, float sigma, int mode,
                               int mag_kind, float* X) {
-  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t li = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (i >= n) return;
-  const int lab = labels[i];
+  if (li >= n) return;
+  const int64_t i = row0 + li;
+  const int lab = labels[li];
   const double* c = centres + static_cast<int64_t>(lab) * d;
-  float* x = X + i * d;
+  float* x = X + li * d;
   if (mode == 0) {
     for (int l = lane; l < d; l += 32)
       x[l] = static_cast<float>(c[l] + sigma * normal_f(seed_noise, static_cast<uint64_t>(i) * d + l));
@@ -259,12 +261,15 @@ int fsilgen_blobs_host(int64_t n, int32_t d, int32_t k, double spread, double se
   return 0;
 }
 
-// C2..C5 on the device.  Returns 0 on success; dX [n*d] fp32, dlabels [n].
-int fsilgen_device(int config, int64_t n, int32_t d, int32_t k, uint64_t seed, float* dX,
-                   int32_t* dlabels, void* stream_ptr, char* err, size_t errlen) {
+// C2..C5 on the device, rows [row0, row0 + n) of the n_global-row dataset (any rank's
+// shard of one global dataset: the same bytes as rows row0.. of the whole).  Returns 0 on
+// success; dX [n*d] fp32, dlabels [n].
+int fsilgen_device_rows(int config, int64_t n_global, int64_t row0, int64_t n, int32_t d, int32_t k,
+                        uint64_t seed, float* dX, int32_t* dlabels, void* stream_ptr, char* err, size_t errlen) {
   cudaStream_t st = static_cast<cudaStream_t>(stream_ptr);
   try {
-    if (n < 2 || d < 1 || k < 2) throw std::runtime_error("bad generator shape");
+    if (n_global < 2 || d < 1 || k < 2 || row0 < 0 || n < 1 || row0 + n > n_global)
+      throw std::runtime_error("bad generator shape");
     double* centres = nullptr;
     check(cudaMalloc(&centres, static_cast<size_t>(k) * d * sizeof(double)), "cudaMalloc");
     const uint64_t s_cent = stream_seed(seed, 1), s_noise = stream_seed(seed, 2),
@@ -275,14 +280,14 @@ int fsilgen_device(int config, int64_t n, int32_t d, int32_t k, uint64_t seed, f
     switch (config) {
       case 2: {
         centres_kernel<<<k, 128, 0, st>>>(s_cent, k, d, 1.0f, true, centres);
-        uniform_labels_kernel<<<thr_grid, 256, 0, st>>>(s_lab, n, k, dlabels);
-        points_kernel<<<warps_grid, 256, 0, st>>>(s_noise, s_mag, n, d, centres, dlabels, 0.1f, 1, 0, dX);
+        uniform_labels_kernel<<<thr_grid, 256, 0, st>>>(s_lab, row0, n, k, dlabels);
+        points_kernel<<<warps_grid, 256, 0, st>>>(s_noise, s_mag, row0, n, d, centres, dlabels, 0.1f, 1, 0, dX);
         break;
       }
       case 3: {
         std::vector<double> p(static_cast<size_t>(k));
         for (int32_t j = 0; j < k; ++j) p[j] = std::pow(static_cast<double>(j + 1), -1.1);
-        auto sz = apportion(p, n, 1);
+        auto sz = apportion(p, n_global, 1);
         // force the two smallest clusters to sizes 1 and 2 (singleton path)
         std::vector<size_t> idx(static_cast<size_t>(k));
         std::iota(idx.begin(), idx.end(), 0);
@@ -292,16 +297,16 @@ int fsilgen_device(int config, int64_t n, int32_t d, int32_t k, uint64_t seed, f
         sz[idx[1]] = 2;
         sz[idx.back()] += give;
         auto lab = shuffled_labels(sz, s_shuf);
-        check(cudaMemcpyAsync(dlabels, lab.data(), lab.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st), "H2D");
+        check(cudaMemcpyAsync(dlabels, lab.data() + row0, n * sizeof(int32_t), cudaMemcpyHostToDevice, st), "H2D");
         centres_kernel<<<k, 128, 0, st>>>(s_cent, k, d, 5.0f, false, centres);
-        points_kernel<<<warps_grid, 256, 0, st>>>(s_noise, s_mag, n, d, centres, dlabels, 1.0f, 0, 0, dX);
+        points_kernel<<<warps_grid, 256, 0, st>>>(s_noise, s_mag, row0, n, d, centres, dlabels, 1.0f, 0, 0, dX);
         check(cudaStreamSynchronize(st), "sync");
         break;
       }
       case 4: {
         centres_kernel<<<k, 128, 0, st>>>(s_cent, k, d, 3.0f, false, centres);
-        uniform_labels_kernel<<<thr_grid, 256, 0, st>>>(s_lab, n, k, dlabels);
-        points_kernel<<<warps_grid, 256, 0, st>>>(s_noise, s_mag, n, d, centres, dlabels, 1.0f, 0, 0, dX);
+        uniform_labels_kernel<<<thr_grid, 256, 0, st>>>(s_lab, row0, n, k, dlabels);
+        points_kernel<<<warps_grid, 256, 0, st>>>(s_noise, s_mag, row0, n, d, centres, dlabels, 1.0f, 0, 0, dX);
         nearest_kernel<<<thr_grid, 256, 0, st>>>(dX, n, d, centres, k, dlabels);
         break;
       }
@@ -310,11 +315,11 @@ int fsilgen_device(int config, int64_t n, int32_t d, int32_t k, uint64_t seed, f
         GaussianStream g{SplitMix64{s_size ^ 0x5555}};
         std::vector<double> p(static_cast<size_t>(k));
         for (auto& v : p) v = gamma_variate(0.5, rng, g);
-        auto sz = apportion(p, n, 1);
+        auto sz = apportion(p, n_global, 1);
         auto lab = shuffled_labels(sz, s_shuf);
-        check(cudaMemcpyAsync(dlabels, lab.data(), lab.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st), "H2D");
+        check(cudaMemcpyAsync(dlabels, lab.data() + row0, n * sizeof(int32_t), cudaMemcpyHostToDevice, st), "H2D");
         centres_kernel<<<k, 128, 0, st>>>(s_cent, k, d, 1.0f, true, centres);
-        points_kernel<<<warps_grid, 256, 0, st>>>(s_noise, s_mag, n, d, centres, dlabels, 0.3f, 1, 1, dX);
+        points_kernel<<<warps_grid, 256, 0, st>>>(s_noise, s_mag, row0, n, d, centres, dlabels, 0.3f, 1, 1, dX);
         check(cudaStreamSynchronize(st), "sync");
         break;
       }
@@ -331,6 +336,11 @@ int fsilgen_device(int config, int64_t n, int32_t d, int32_t k, uint64_t seed, f
     }
     return 1;
   }
+}
+
+int fsilgen_device(int config, int64_t n, int32_t d, int32_t k, uint64_t seed, float* dX, int32_t* dlabels,
+                   void* stream_ptr, char* err, size_t errlen) {
+  return fsilgen_device_rows(config, n, 0, n, d, k, seed, dX, dlabels, stream_ptr, err, errlen);
 }
 
 }  // extern "C"

@@ -36,6 +36,9 @@ def _dl():
                                          ctypes.c_double, ctypes.c_double, ctypes.c_uint64, P, P]
         L.fsilgen_device.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                      ctypes.c_uint64, P, P, P, ctypes.c_char_p, ctypes.c_size_t]
+        L.fsilgen_device_rows.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                          ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, P, P, P,
+                                          ctypes.c_char_p, ctypes.c_size_t]
         _lib = L
     return _lib
 
@@ -50,21 +53,24 @@ def blobs(n, d, k, seed, spread=1.0, separation=10.0):
     return X, L
 
 
-def generate_device(config: str, n=None, d=None, k=None, seed=None, device=0):
-    """Generate a config on the GPU -> (X [n,d] float32 cuda tensor, labels [n] int32)."""
+def generate_device(config: str, n=None, d=None, k=None, seed=None, device=0, rows=None):
+    """Generate a config on the GPU -> (X [n,d] float32 cuda tensor, labels [n] int32).
+    rows=(begin, end): only those rows of the n-row dataset (one rank's shard of a global
+    dataset, byte-identical to the same rows of the whole)."""
     import torch
 
     cid, metric, N, D, K, S = CONFIGS[config]
     n, d, k, seed = n or N, d or D, k or K, S if seed is None else seed
     dev = torch.device("cuda", device)
+    b, e = rows if rows is not None else (0, n)
     if cid == 1:
         X, L = blobs(n, d, k, seed)
-        return torch.from_numpy(X).to(dev), torch.from_numpy(L).to(dev), metric
-    X = torch.empty((n, d), dtype=torch.float32, device=dev)
-    L = torch.empty(n, dtype=torch.int32, device=dev)
+        return torch.from_numpy(X[b:e]).to(dev), torch.from_numpy(L[b:e]).to(dev), metric
+    X = torch.empty((e - b, d), dtype=torch.float32, device=dev)
+    L = torch.empty(e - b, dtype=torch.int32, device=dev)
     err = ctypes.create_string_buffer(256)
     stream = torch.cuda.current_stream(dev).cuda_stream
-    rc = _dl().fsilgen_device(cid, n, d, k, seed, X.data_ptr(), L.data_ptr(), stream, err, 256)
+    rc = _dl().fsilgen_device_rows(cid, n, b, e - b, d, k, seed, X.data_ptr(), L.data_ptr(), stream, err, 256)
     if rc != 0:
         raise FsilError(ERR_INTERNAL, err.value.decode())
     return X, L, metric

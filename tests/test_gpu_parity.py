@@ -766,3 +766,25 @@ def test_shard_exchange_overflow_again():
     finally:
         for c in ctxs:
             c.close()
+
+
+@pytest.mark.parametrize("name,n,nshards", [("C2", 200_000, 2), ("C3", 400_000, 4), ("C4", 300_000, 8),
+                                            ("C5", 60_000, 3)])
+def test_strong_scaling_shards_match_single_gpu(ctx, name, n, nshards):
+    """bench.py's strong scaling: each rank generates its plan_shards rows of ONE global
+    dataset (datagen rows=...), byte-identical to those rows of the whole, and the sharded
+    protocol over those shards reproduces the single-GPU result: S within 1e-12 (only the
+    order of the all-reduced fp64 sums differs), neighbours identical, s_i within 1e-12."""
+    import torch
+    from paper_2303_14102_b200 import datagen, plan_shards
+    Xw, Lw, metric = datagen.generate_device(name, n=n)
+    for b, e in plan_shards(n, nshards):
+        Xs, Ls, _ = datagen.generate_device(name, n=n, rows=(b, e))
+        assert torch.equal(Xs, Xw[b:e]) and torch.equal(Ls, Lw[b:e]), (b, e)
+    X, L = Xw.cpu().numpy(), Lw.cpu().numpy()
+    del Xw, Lw
+    single = ctx.silhouette(X, L, metric)
+    means, errors, s, nb, _ = _shard_loopback(X, L, metric, nshards, device_exchange=True)
+    assert not errors and all(abs(m - single.mean) <= 1e-12 for m in means), (means, single.mean)
+    assert np.array_equal(nb, single.neighbour)
+    assert np.abs(s - single.s).max() <= 1e-12
