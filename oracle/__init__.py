@@ -16,7 +16,10 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libfsil_oracle.so")
+_REF_PATH = os.path.join(_HERE, "_ref", "libfsil_ref.so")
+_REF_SRC = "/root/reference/proj"
 _lib = None
+_ref_lib = None
 
 SQEUCLID, COSINE, EUCLID = 0, 1, 2
 FAST, NAIVE = 0, 1
@@ -36,6 +39,47 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB_PATH):
         subprocess.run(["make", "-C", _HERE, "-s"], check=True)
     return _LIB_PATH
+
+
+def build_ref(force: bool = False):
+    """oracle/_ref/libfsil_ref.so: the reference's own sources compiled against the Eigen
+    shim (oracle/Makefile `ref`).  Built only where /root/reference exists (this
+    container); elsewhere the prebuilt library that travelled with the snapshot is used.
+    Returns the path, or None when neither is available."""
+    if os.path.isdir(_REF_SRC) and (force or not os.path.exists(_REF_PATH)):
+        subprocess.run(["make", "-C", _HERE, "-s", "ref"], check=True)
+    return _REF_PATH if os.path.exists(_REF_PATH) else None
+
+
+def _bind_common(L, prefix):
+    P = ctypes.c_void_p
+    i64, i32, sz, cp = ctypes.c_int64, ctypes.c_int, ctypes.c_size_t, ctypes.c_char_p
+    for name in ("silhouette_f32", "silhouette"):
+        getattr(L, f"{prefix}_{name}").argtypes = [i32, i32, P, P, i64, i64, i32, P, P, P, P, P, P, P,
+                                                   P, P, cp, sz]
+    getattr(L, f"{prefix}_plan_shards").argtypes = [i64, i32, P, P, cp, sz]
+    getattr(L, f"{prefix}_assemble_score").argtypes = [ctypes.c_double, ctypes.c_double, P, cp, sz]
+    getattr(L, f"{prefix}_default_shards").restype = i32
+
+
+def ref_lib():
+    """The reference library (oracle/_ref), or None if it is not built."""
+    global _ref_lib
+    if _ref_lib is None:
+        path = build_ref()
+        if path is None:
+            return None
+        L = ctypes.CDLL(path)
+        _bind_common(L, "ref")
+        P = ctypes.c_void_p
+        i64, sz, cp = ctypes.c_int64, ctypes.c_size_t, ctypes.c_char_p
+        L.ref_generate_blobs.argtypes = [i64, i64, i64, ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
+                                         P, P, cp, sz]
+        L.ref_read_csv_text.argtypes = [cp, ctypes.c_char, ctypes.c_int, cp, ctypes.c_int, P, P, P, P, cp, sz,
+                                        cp, sz]
+        L.ref_score_report.argtypes = [ctypes.c_int, P, P, i64, i64, ctypes.c_int, cp, sz, P, cp, sz]
+        _ref_lib = L
+    return _ref_lib
 
 
 def lib():
@@ -85,8 +129,10 @@ class OracleReport:
     wall_ms: float
 
 
-def silhouette(X, labels, metric="sqeuclid", engine="fast", shards=0) -> OracleReport:
-    """compute_silhouette(validate_and_densify(X, labels), ...) (engine.cpp:76-92)."""
+def silhouette(X, labels, metric="sqeuclid", engine="fast", shards=0, reference=False) -> OracleReport:
+    """compute_silhouette(validate_and_densify(X, labels), ...) (engine.cpp:76-92).
+    reference=True runs the reference's own compiled code (oracle/_ref) instead of the
+    restatement; both share this signature."""
     m = METRICS[metric] if isinstance(metric, str) else int(metric)
     e = NAIVE if engine == "naive" else FAST
     X = np.ascontiguousarray(X)
@@ -98,10 +144,12 @@ def silhouette(X, labels, metric="sqeuclid", engine="fast", shards=0) -> OracleR
     k = ctypes.c_int32(0)
     d2r = np.zeros(max(n, 1), np.int32)
     err = ctypes.create_string_buffer(512)
-    fn = lib().orc_silhouette_f32 if X.dtype == np.float32 else lib().orc_silhouette
+    L, pre = (ref_lib(), "ref") if reference else (lib(), "orc")
+    if L is None:
+        raise RuntimeError("oracle/_ref/libfsil_ref.so is not built (needs /root/reference)")
     if X.dtype not in (np.float32, np.float64):
         X = X.astype(np.float64)
-        fn = lib().orc_silhouette
+    fn = getattr(L, f"{pre}_silhouette_f32" if X.dtype == np.float32 else f"{pre}_silhouette")
     rc = fn(m, e, _ptr(X), _ptr(labels), n if labels.shape[0] == n else labels.shape[0], d, shards,
             *[_ptr(o) for o in out], ctypes.byref(mean), ctypes.byref(k), _ptr(d2r),
             ctypes.byref(wall), err, 512)
@@ -175,23 +223,68 @@ def score_rows(X, dense, counts, sums, psi, rows, metric="sqeuclid"):
     return a, b, s, nb
 
 
-def plan_shards(n, w):
+def plan_shards(n, w, reference=False):
     """plan_shards (engine.cpp:8-25) -> list of (begin, end)."""
     ranges = np.zeros(2 * max(1, min(max(w, 1), max(n, 1))), np.int64)
     ns = ctypes.c_int(0)
     err = ctypes.create_string_buffer(512)
-    rc = lib().orc_plan_shards(n, w, _ptr(ranges), ctypes.byref(ns), err, 512)
+    fn = ref_lib().ref_plan_shards if reference else lib().orc_plan_shards
+    rc = fn(n, w, _ptr(ranges), ctypes.byref(ns), err, 512)
     _check(rc, err)
     return [(int(ranges[2 * i]), int(ranges[2 * i + 1])) for i in range(ns.value)]
 
 
-def assemble_score(a, b):
+def assemble_score(a, b, reference=False):
     s = ctypes.c_double(0)
     err = ctypes.create_string_buffer(512)
-    rc = lib().orc_assemble_score(a, b, ctypes.byref(s), err, 512)
+    fn = ref_lib().ref_assemble_score if reference else lib().orc_assemble_score
+    rc = fn(a, b, ctypes.byref(s), err, 512)
     _check(rc, err)
     return s.value
 
 
 def default_shards():
     return lib().orc_default_shards()
+
+
+def ref_generate_blobs(n, d, k, seed, spread=1.0, separation=8.0):
+    """The reference's generate_blobs (blobs.cpp:25-54) -> (X fp64 [n,d], dense labels)."""
+    X = np.zeros((n, d))
+    L = np.zeros(n, np.int32)
+    err = ctypes.create_string_buffer(512)
+    _check(ref_lib().ref_generate_blobs(n, d, k, spread, separation, seed, _ptr(X), _ptr(L), err, 512), err)
+    return X, L
+
+
+def ref_read_csv_text(text, delimiter=",", label_index=-1, label_name="", has_header=None):
+    """The reference's read_csv_text (csv.cpp:54-159) -> (X fp64, dense labels, names)."""
+    L = ref_lib()
+    t = text.encode()
+    n, d = ctypes.c_int64(0), ctypes.c_int64(0)
+    err = ctypes.create_string_buffer(1024)
+    hh = -1 if has_header is None else int(bool(has_header))
+    args = (t, delimiter.encode(), label_index, label_name.encode(), hh)
+    _check(L.ref_read_csv_text(*args, ctypes.byref(n), ctypes.byref(d), None, None, None, 0, err, 1024), err)
+    X = np.zeros((n.value, d.value))
+    lab = np.zeros(n.value, np.int32)
+    names = ctypes.create_string_buffer(1 << 20)
+    _check(L.ref_read_csv_text(*args, ctypes.byref(n), ctypes.byref(d), _ptr(X), _ptr(lab), names, 1 << 20,
+                               err, 1024), err)
+    return X, lab, names.value.decode().split("\n")[:-1]
+
+
+def ref_score_report(X, labels, metric="sqeuclid", fmt="csv"):
+    """compute_silhouette(..., shards=1) then write_report (report_io.cpp:53-68) -> text."""
+    m = METRICS[metric] if isinstance(metric, str) else int(metric)
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    labels = np.ascontiguousarray(labels, dtype=np.int32)
+    n, d = X.shape
+    L = ref_lib()
+    ln = ctypes.c_size_t(0)
+    err = ctypes.create_string_buffer(1024)
+    f = 1 if fmt == "jsonl" else 0
+    _check(L.ref_score_report(m, _ptr(X), _ptr(labels), n, d, f, None, 0, ctypes.byref(ln), err, 1024), err)
+    buf = ctypes.create_string_buffer(ln.value + 1)
+    _check(L.ref_score_report(m, _ptr(X), _ptr(labels), n, d, f, buf, ln.value + 1, ctypes.byref(ln), err, 1024),
+           err)
+    return buf.value.decode()

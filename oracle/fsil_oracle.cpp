@@ -52,18 +52,50 @@ struct Dataset {
   int label(Index i) const { return labels[static_cast<size_t>(i)]; }
 };
 
-// Eigen-free restatements of squaredNorm / dot / norm (types.hpp:3 includes
-// Eigen; its vectorised reduction order is not reproduced -- parity unpinned
-// at the bit level, ~1e-16 relative).
-static double sq_norm(const double* x, Index d) {
-  double acc = 0.0;
-  for (Index l = 0; l < d; ++l) acc += x[l] * x[l];
-  return acc;
+// squaredNorm / dot / norm as the reference's Eigen computes them (types.hpp:3;
+// Eigen 3.4.0, restated -- Eigen is not installed here).  The reference is built
+// without -march (proj/CMakeLists.txt:20), so Eigen reduces with SSE2 Packet2d in
+// redux_impl<LinearVectorizedTraversal, NoUnrolling> (Eigen/src/Core/Redux.h):
+// four interleaved partial sums over 4*floor(n/4) terms -- lane j sums terms
+// j, j+4, j+8, ... -- folded as (s0+s2, s1+s3), plus one more pair when n mod 4 >= 2,
+// then lane 0 + lane 1, then the odd tail term.  sum() of nothing is 0.  Pinned
+// bit for bit against the reference sources compiled by oracle/Makefile `ref`.
+template <typename Term>
+static double eigen_redux_sum(Index n, Term term) {
+  if (n == 0) return 0.0;
+  const Index pairs_end = (n / 2) * 2, quads_end = (n / 4) * 4;
+  if (pairs_end == 0) return term(0);
+  double s0 = term(0), s1 = term(1);
+  if (pairs_end > 2) {
+    double s2 = term(2), s3 = term(3);
+    for (Index i = 4; i < quads_end; i += 4) {
+      s0 += term(i);
+      s1 += term(i + 1);
+      s2 += term(i + 2);
+      s3 += term(i + 3);
+    }
+    s0 += s2;
+    s1 += s3;
+    if (pairs_end > quads_end) {
+      s0 += term(quads_end);
+      s1 += term(quads_end + 1);
+    }
+  }
+  double res = s0 + s1;
+  for (Index i = pairs_end; i < n; ++i) res += term(i);
+  return res;
 }
-static double dot(const double* x, const double* y, Index d) {
-  double acc = 0.0;
-  for (Index l = 0; l < d; ++l) acc += x[l] * y[l];
-  return acc;
+static double sq_norm(const double* x, Index d) {  // cwiseAbs2().sum()
+  return eigen_redux_sum(d, [x](Index l) { return x[l] * x[l]; });
+}
+static double dot(const double* x, const double* y, Index d) {  // binaryExpr(conj_prod).sum()
+  return eigen_redux_sum(d, [x, y](Index l) { return x[l] * y[l]; });
+}
+static double sq_dist(const double* p, const double* q, Index d) {  // (p - q).squaredNorm()
+  return eigen_redux_sum(d, [p, q](Index l) {
+    const double t = p[l] - q[l];
+    return t * t;
+  });
 }
 static double norm(const double* x, Index d) { return std::sqrt(sq_norm(x, d)); }
 
@@ -481,16 +513,10 @@ static Report run_two_phase(const Dataset& ds, const ShardPlan& plan) {
 // ---- naive.cpp:12-71 --------------------------------------------------------
 static double pairwise_distance(const double* p, const double* q, Index d, Metric metric) {
   switch (metric) {
-    case Metric::SquaredEuclidean: {
-      double acc = 0.0;
-      for (Index l = 0; l < d; ++l) acc += (p[l] - q[l]) * (p[l] - q[l]);
-      return acc;
-    }
-    case Metric::Euclidean: {
-      double acc = 0.0;
-      for (Index l = 0; l < d; ++l) acc += (p[l] - q[l]) * (p[l] - q[l]);
-      return std::sqrt(acc);
-    }
+    case Metric::SquaredEuclidean:
+      return sq_dist(p, q, d);
+    case Metric::Euclidean:
+      return std::sqrt(sq_dist(p, q, d));
     case Metric::Cosine: {
       const double np = norm(p, d), nq = norm(q, d);
       if (np == 0.0 || nq == 0.0) throw ValidationError("cosine distance undefined for zero vector");

@@ -7,13 +7,14 @@
  * --impl reference legs may load this library.  The product (libfsil.so) never
  * links or calls it.
  *
- * Parity status: the reference cannot be compiled here (Eigen3, vendor/ and
- * tests/CMakeLists.txt are absent), so this restatement is
- * pinned against the reference's own known answers (SPEC.md goldens and per-op
- * examples), against its in-product naive O(N^2 D) oracle restated below, and
- * against scikit-learn's silhouette_samples (tests/golden/).  Bit-level parity
- * with Eigen's vectorised reduction order is unpinned; every fp64 reordering
- * difference is ~1e-16 relative, far inside the 1e-5 / 1e-6 tolerances.
+ * Parity status: pinned bit for bit to the reference itself.  oracle/Makefile
+ * `ref` compiles the reference's own .cpp files (unmodified, from
+ * /root/reference/proj/src) against a committed Eigen-API shim into
+ * oracle/_ref/libfsil_ref.so; tests/test_oracle.py checks that this
+ * restatement returns identical a, b, s, own, neighbour and mean bits on every
+ * shape it runs (the reductions restate Eigen 3.4.0's SSE2 redux order).  It is
+ * also checked against SPEC.md's goldens, the naive O(N^2 D) engine and
+ * scikit-learn's silhouette_samples (tests/golden/).
  */
 #ifndef FSIL_ORACLE_H
 #define FSIL_ORACLE_H

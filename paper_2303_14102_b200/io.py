@@ -120,6 +120,12 @@ def read_csv_text(text: str, schema: CsvSchema = CsvSchema(), name: str = "<stri
             index[lab] = len(names)
             names.append(lab)
         codes[r] = index[lab]
+    # read_csv_text ends in validate_and_densify (csv.cpp:158, dataset.cpp:29-57): the
+    # dataset-level invariants come back from the reader itself, as in the reference.
+    if n < 2:
+        raise ValidationError(f"dataset needs at least 2 points, got {n}")
+    if len(names) < 2:
+        raise ValidationError(f"silhouette undefined for a single cluster: need K >= 2, got K = {len(names)}")
     return CsvDataset(X, codes, names)
 
 
