@@ -18,9 +18,11 @@ rows of the whole) and the ranks run the sharded protocol (dictionary all-gather
 K x (D+2) fp64 all-reduce, scalar all-reduce over NCCL).  `--gpus N` without
 WORLD_SIZE in the environment re-launches itself under torch.distributed.run.
 
-Prints ONE JSON line on rank 0.  `--impl reference` times the CPU restatement of the
-reference path (oracle/, test infrastructure; the reference itself cannot be built
-here) on this host's cores.
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference's own CPU
+code for the path -- its .cpp files compiled unmodified against the Eigen shim
+(oracle/_ref, built by oracle/Makefile `ref`; kind "reference") -- on this host's cores;
+where that library is absent it falls back to the bit-identical restatement (oracle/,
+kind "port").  Both are test infrastructure, never the measured product.
 """
 from __future__ import annotations
 
@@ -182,35 +184,44 @@ def cpu_sample(config, n_full):
     return X, L, metric, rows, how
 
 
-def cpu_baseline(config, n_full, trials=3):
-    """CPU restatement of the reference (oracle/, TEST INFRASTRUCTURE) on this host's
-    cores: the reference's own run_two_phase window (engine.hpp:107-113), best of 3
-    (bench.cpp:72-79)."""
+def cpu_impl():
+    """(kind, run) for the CPU arm: the reference's own compiled code (oracle/_ref) when
+    present, else the restatement that tests/test_reference_pin.py pins to it bit for bit."""
     import oracle
+    ref = oracle.ref_lib() is not None
+    kind = "reference" if ref else "port"
+    return kind, lambda X, L, metric, cores: oracle.silhouette(X, L, metric, "fast", shards=cores, reference=ref)
+
+
+def cpu_baseline(config, n_full, trials=3):
+    """The reference's CPU path (oracle/_ref, or the restatement; TEST INFRASTRUCTURE) on
+    this host's cores: the reference's own run_two_phase window (engine.hpp:107-113),
+    best of 3 (bench.cpp:72-79)."""
+    kind, run = cpu_impl()
     X, L, metric, rows, how = cpu_sample(config, n_full)
     cores = os.cpu_count() or 1
     best = None
     for _ in range(trials):
-        r = oracle.silhouette(X, L, metric, "fast", shards=cores)
+        r = run(X, L, metric, cores)
         best = r.wall_ms if best is None else min(best, r.wall_ms)
-    return {"value": rows / (best / 1e3), "unit": "points/s", "cores": cores, "kind": "port",
+    return {"value": rows / (best / 1e3), "unit": "points/s", "cores": cores, "kind": kind,
             "sample": how + f"; full aggregation+scoring+mean window, best of {trials}", "ms": best}
 
 
 def reference_arm(a, rank, world):
-    """--impl reference: the CPU restatement of the reference path on this host's cores,
-    rank 0 only, each step a bounded sample of the workload."""
+    """--impl reference: the reference's CPU path (oracle/_ref; else the restatement) on
+    this host's cores, rank 0 only, each step a bounded sample of the workload."""
     if rank != 0:
         return 0
-    import oracle
     from paper_2303_14102_b200 import datagen
+    kind, run = cpu_impl()
     cid, metric, N, D, K, seed = datagen.CONFIGS[a.config]
     N = a.n or N
     X, L, metric, rows, how = cpu_sample(a.config, N)
     cores = os.cpu_count() or 1
     for _ in range(max(a.warmup, 0)):
-        oracle.silhouette(X, L, metric, "fast", shards=cores)
-    times = [oracle.silhouette(X, L, metric, "fast", shards=cores).wall_ms for _ in range(a.steps)]
+        run(X, L, metric, cores)
+    times = [run(X, L, metric, cores).wall_ms for _ in range(a.steps)]
     ms = float(np.mean(times))
     val = rows / (ms / 1e3)
     out = {"metric": METRIC, "value": val, "unit": "points/s", "n_gpus": world,
@@ -220,7 +231,7 @@ def reference_arm(a, rank, world):
            "config": {"workload": f"{a.config} ({metric}, N={N}, D={D}, K={K}); CPU step = {how}",
                       "global_batch": rows, "seq_len": D,
                       "parallelism": f"{cores} host threads (std::thread, engine.cpp:34-55)"},
-           "cpu_baseline": {"value": val, "unit": "points/s", "cores": cores, "kind": "port", "sample": how},
+           "cpu_baseline": {"value": val, "unit": "points/s", "cores": cores, "kind": kind, "sample": how},
            "e2e": {"value": val, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "gpu_launches": 0}
     print(json.dumps(out))

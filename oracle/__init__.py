@@ -94,6 +94,7 @@ def lib():
         L.orc_aggregate_f32.argtypes = [i32, P, P, i64, i64, i32, P, P, P, P, cp, sz]
         L.orc_aggregate_dense_f32.argtypes = [i32, P, P, i64, i64, i32, i32, P, P, P, cp, sz]
         L.orc_score_rows_f32.argtypes = [i32, P, P, i64, i64, i32, P, P, P, P, i64, P, P, P, P, cp, sz]
+        L.orc_score_rows_mt_f32.argtypes = [i32, P, P, i64, i64, i32, P, P, P, P, i64, i32, P, P, P, P, cp, sz]
         L.orc_plan_shards.argtypes = [i64, i32, P, P, cp, sz]
         L.orc_assemble_score.argtypes = [dbl, dbl, P, cp, sz]
         L.orc_default_shards.restype = i32
@@ -202,8 +203,9 @@ def aggregate_dense(X, dense, k, metric="sqeuclid", shards=0):
     return counts, sums, (psi if m == SQEUCLID else None)
 
 
-def score_rows(X, dense, counts, sums, psi, rows, metric="sqeuclid"):
-    """score_range on sampled rows against global stats -> (a, b, s, neighbour)."""
+def score_rows(X, dense, counts, sums, psi, rows, metric="sqeuclid", threads=1, want_ab=True):
+    """score_range on rows (None = all) against global stats -> (a, b, s, neighbour);
+    threads=0 uses every host core.  want_ab=False returns a, b as None (saves 16 B/row)."""
     m = METRICS[metric] if isinstance(metric, str) else int(metric)
     X = np.ascontiguousarray(X, dtype=np.float32)
     n, d = X.shape
@@ -211,14 +213,15 @@ def score_rows(X, dense, counts, sums, psi, rows, metric="sqeuclid"):
     counts = np.ascontiguousarray(counts, dtype=np.int64)
     sums = np.ascontiguousarray(sums, dtype=np.float64)
     psi_a = None if psi is None else np.ascontiguousarray(psi, dtype=np.float64)
-    rows = np.ascontiguousarray(rows, dtype=np.int64)
-    mm = rows.shape[0]
-    a, b, s = np.zeros(mm), np.zeros(mm), np.zeros(mm)
+    rows = None if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
+    mm = n if rows is None else rows.shape[0]
+    a, b = (np.zeros(mm), np.zeros(mm)) if want_ab else (None, None)
+    s = np.zeros(mm)
     nb = np.zeros(mm, np.int32)
     err = ctypes.create_string_buffer(512)
-    rc = lib().orc_score_rows_f32(m, _ptr(X), _ptr(dense), n, d, counts.shape[0], _ptr(counts),
-                                  _ptr(sums), _ptr(psi_a), _ptr(rows), mm, _ptr(a), _ptr(b),
-                                  _ptr(s), _ptr(nb), err, 512)
+    rc = lib().orc_score_rows_mt_f32(m, _ptr(X), _ptr(dense), n, d, counts.shape[0], _ptr(counts),
+                                     _ptr(sums), _ptr(psi_a), _ptr(rows), mm, threads, _ptr(a), _ptr(b),
+                                     _ptr(s), _ptr(nb), err, 512)
     _check(rc, err)
     return a, b, s, nb
 

@@ -759,39 +759,62 @@ int orc_score_rows_f32(int metric, const float* X, const int32_t* dense, int64_t
                        int32_t k, const int64_t* counts, const double* sums, const double* psi,
                        const int64_t* rows, int64_t m, double* a, double* b, double* s,
                        int32_t* neighbour, char* err, size_t errlen) {
+  return orc_score_rows_mt_f32(metric, X, dense, n, d, k, counts, sums, psi, rows, m, 1, a, b, s,
+                               neighbour, err, errlen);
+}
+
+int orc_score_rows_mt_f32(int metric, const float* X, const int32_t* dense, int64_t n, int64_t d,
+                          int32_t k, const int64_t* counts, const double* sums, const double* psi,
+                          const int64_t* rows, int64_t m, int threads, double* a, double* b,
+                          double* s, int32_t* neighbour, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
-    // A compact dataset holding only the sampled rows; stats are the global ones.
-    orc::Dataset ds;
-    ds.n = m;
-    ds.d = d;
-    ds.pts.resize(static_cast<size_t>(m * d));
-    ds.labels.resize(static_cast<size_t>(m));
-    ds.sizes.assign(static_cast<size_t>(k), 0);
-    for (int64_t j = 0; j < m; ++j) {
-      const int64_t r = rows[j];
-      if (r < 0 || r >= n) throw std::invalid_argument("row index out of range");
-      for (int64_t l = 0; l < d; ++l) ds.pts[j * d + l] = static_cast<double>(X[r * d + l]);
-      ds.labels[j] = dense[r];
-    }
-    std::vector<orc::PointScore> out(static_cast<size_t>(m));
-    if (to_metric(metric) == orc::Metric::SquaredEuclidean) {
-      orc::SqStats st = orc::SqStats::zero(k, d);
-      std::copy(counts, counts + k, st.counts.begin());
-      std::copy(psi, psi + k, st.psi.begin());
-      std::copy(sums, sums + k * d, st.y.begin());
-      orc::SqPolicy::score(ds, st, 0, m, out);
+    const bool sq = to_metric(metric) == orc::Metric::SquaredEuclidean;
+    orc::SqStats sst;
+    orc::CosStats cst;
+    if (sq) {
+      sst = orc::SqStats::zero(k, d);
+      std::copy(counts, counts + k, sst.counts.begin());
+      std::copy(psi, psi + k, sst.psi.begin());
+      std::copy(sums, sums + k * d, sst.y.begin());
     } else {
-      orc::CosStats st = orc::CosStats::zero(k, d);
-      std::copy(counts, counts + k, st.counts.begin());
-      std::copy(sums, sums + k * d, st.omega.begin());
-      orc::CosPolicy::score(ds, st, 0, m, out);
+      cst = orc::CosStats::zero(k, d);
+      std::copy(counts, counts + k, cst.counts.begin());
+      std::copy(sums, sums + k * d, cst.omega.begin());
     }
-    for (int64_t j = 0; j < m; ++j) {
-      if (a) a[j] = out[j].a;
-      if (b) b[j] = out[j].b;
-      if (s) s[j] = out[j].s;
-      if (neighbour) neighbour[j] = out[j].neighbour_cluster;
-    }
+    // Chunks of rows, each a compact dataset of those rows (fp32 widened exactly)
+    // against the global stats, scored by the policy's score_range.
+    constexpr int64_t kChunk = 4096;
+    const int64_t nchunks = (m + kChunk - 1) / kChunk;
+    std::atomic<int64_t> next{0};
+    auto body = [&](int) {
+      orc::Dataset ds;
+      ds.d = d;
+      ds.sizes.assign(static_cast<size_t>(k), 0);
+      std::vector<orc::PointScore> out;
+      for (int64_t c; (c = next.fetch_add(1)) < nchunks;) {
+        const int64_t j0 = c * kChunk, cm = std::min(m, j0 + kChunk) - j0;
+        ds.n = cm;
+        ds.pts.resize(static_cast<size_t>(cm * d));
+        ds.labels.resize(static_cast<size_t>(cm));
+        for (int64_t j = 0; j < cm; ++j) {
+          const int64_t r = rows ? rows[j0 + j] : j0 + j;
+          if (r < 0 || r >= n) throw std::invalid_argument("row index out of range");
+          for (int64_t l = 0; l < d; ++l) ds.pts[j * d + l] = static_cast<double>(X[r * d + l]);
+          ds.labels[j] = dense[r];
+        }
+        out.assign(static_cast<size_t>(cm), orc::PointScore{});
+        if (sq) orc::SqPolicy::score(ds, sst, 0, cm, out);
+        else orc::CosPolicy::score(ds, cst, 0, cm, out);
+        for (int64_t j = 0; j < cm; ++j) {
+          if (a) a[j0 + j] = out[j].a;
+          if (b) b[j0 + j] = out[j].b;
+          if (s) s[j0 + j] = out[j].s;
+          if (neighbour) neighbour[j0 + j] = out[j].neighbour_cluster;
+        }
+      }
+    };
+    const int w = threads > 0 ? threads : orc::default_shards();
+    orc::run_workers(static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(w, nchunks))), body);
   });
 }
 

@@ -80,6 +80,12 @@ int orc_score_rows_f32(int metric, const float* X, const int32_t* dense, int64_t
                        const int64_t* rows, int64_t m, double* a, double* b, double* s,
                        int32_t* neighbour, char* err, size_t errlen);
 
+/* Same on `threads` std::threads (0 = all); rows == NULL scores rows [0, m). */
+int orc_score_rows_mt_f32(int metric, const float* X, const int32_t* dense, int64_t n, int64_t d,
+                          int32_t k, const int64_t* counts, const double* sums, const double* psi,
+                          const int64_t* rows, int64_t m, int threads, double* a, double* b,
+                          double* s, int32_t* neighbour, char* err, size_t errlen);
+
 /* aggregate_cluster_stats over labels that are already dense ids in [0, k)
  * (skips the string densify, which is impractical at 1e8 rows); same block
  * plan and fold as orc_aggregate_f32.  Used to pin full-size configs. */

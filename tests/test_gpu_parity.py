@@ -4,6 +4,7 @@ seeded inputs.  Bar (BASELINE.json north_star): identical neighbour cluster
 1e-4 relative (AB_RTOL; not a BASELINE bar).  Runs on a B200 under gpurun
 (`pytest -m gpu`)."""
 import json
+import math
 import os
 
 import numpy as np
@@ -405,34 +406,85 @@ def test_scaled_configs_full_oracle(ctx, name, n):
     check(ctx, X, L, metric, label=name)
 
 
-@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
-def test_full_size_sampled_rows(ctx, name):
-    """BASELINE.json full sizes: the oracle aggregates all N rows (fp64, dense
-    labels), then scores a sample of rows exactly; s_i depends only on (x_i, label_i,
-    global stats).  Size-independent properties checked on every row."""
+def _full_size_gpu(ctx, name, path=0, data=None):
+    """One full-size config on the device through fsil_silhouette_device -> host arrays.
+    data=(Xd, Ld, metric) reuses already generated device inputs."""
     import torch
     from paper_2303_14102_b200 import datagen
-    Xd, Ld, metric = datagen.generate_device(name)
+    Xd, Ld, metric = data if data is not None else datagen.generate_device(name)
     n, d = Xd.shape
     s = torch.empty(n, dtype=torch.float64, device="cuda")
     nb = torch.empty(n, dtype=torch.int32, device="cuda")
     own = torch.empty(n, dtype=torch.int32, device="cuda")
-    d2r = np.empty(n if n < 10_000_000 else 10_000_000, np.int32)
-    mean, k = ctx.silhouette_device(Xd, Ld, metric, s=s, neighbour=nb, own=own, dense_to_raw=d2r)
-    s_h, nb_h, own_h = s.cpu().numpy(), nb.cpu().numpy(), own.cpu().numpy()
+    d2r = np.empty(min(n, 10_000_000), np.int32)
+    ctx.set_path(path)
+    try:
+        mean, k = ctx.silhouette_device(Xd, Ld, metric, s=s, neighbour=nb, own=own, dense_to_raw=d2r)
+        mean2, _ = ctx.silhouette_device(Xd, Ld, metric, s=s, neighbour=nb)
+    finally:
+        ctx.set_path(0)
+    assert mean2 == mean  # bit-identical rerun
+    out = dict(X=Xd, L=Ld, metric=metric, mean=mean, k=k, s=s.cpu().numpy(), nb=nb.cpu().numpy(),
+               own=own.cpu().numpy(), d2r=d2r[:k].copy())
+    s_h, nb_h, own_h = out["s"], out["nb"], out["own"]
     assert np.all(np.abs(s_h) <= 1.0) and abs(s_h.mean() - mean) <= 1e-9
     assert np.all(nb_h != own_h) and nb_h.min() >= 0 and nb_h.max() < k
-    mean2, _ = ctx.silhouette_device(Xd, Ld, metric, s=s, neighbour=nb)
-    assert mean2 == mean  # bit-identical rerun
-    X, L = Xd.cpu().numpy(), Ld.cpu().numpy()
-    del Xd
+    return out
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_size_oracle_all_rows(ctx, name):
+    """BASELINE.json full sizes (C3: 1e7 x 128, K=100; C4: 1e8 x 32, K=1000) against the
+    oracle on EVERY row: the oracle aggregates all N rows (engine.hpp:50-80 block plan
+    and fold) and scores all N rows (score_range, sqE.cpp:84-108) on every host core.
+    Bar: neighbours identical, |ds_i| <= 1e-5, |dS| <= 1e-6 -- and, because every s_i is
+    computed in fp64 by the reference formulas, the achieved agreement is asserted
+    at fp64 noise (|dS| <= 1e-10)."""
+    g = _full_size_gpu(ctx, name)
+    X, L = g["X"].cpu().numpy(), g["L"].cpu().numpy()
+    del g["X"], g["L"]
+    n = X.shape[0]
     dense, raw = oracle.first_appearance(L)
-    assert raw.tolist() == d2r[:k].tolist() and np.array_equal(dense, own_h)
-    counts, sums, psi = oracle.aggregate_dense(X, dense, k, metric)
-    rows = np.random.default_rng(2).choice(n, 2000, replace=False)
-    a, b, sv, nbv = oracle.score_rows(X, dense, counts, sums, psi, rows, metric)
-    assert np.array_equal(nbv, nb_h[rows])
-    assert np.abs(sv - s_h[rows]).max() <= S_TOL
+    del L
+    assert raw.tolist() == g["d2r"].tolist() and np.array_equal(dense, g["own"])
+    counts, sums, psi = oracle.aggregate_dense(X, dense, g["k"], g["metric"])
+    _, _, sv, nbv = oracle.score_rows(X, dense, counts, sums, psi, None, g["metric"], threads=0, want_ab=False)
+    mism = np.flatnonzero(nbv != g["nb"])
+    assert mism.size == 0, f"{name}: {mism.size} neighbour mismatches, rows {mism[:5]}"
+    ds = np.abs(sv - g["s"]).max()
+    dS = abs(math.fsum(sv) / n - g["mean"])
+    print(f"{name} full size: N={n} S_gpu={g['mean']:.15f} S_oracle={math.fsum(sv) / n:.15f} "
+          f"|dS|={dS:.3e} max|ds_i|={ds:.3e}")
+    assert ds <= S_TOL and dS <= MEAN_TOL
+    assert ds <= S_TIGHT and dS <= MEAN_TIGHT
+
+
+def test_full_size_c5_fp64_path_and_oracle_rows(ctx):
+    """C5 at full size (4e7 x 768, K=4096; 2.5e14 flops, beyond a CPU run): the fast path
+    (tcgen05 nomination + fp64 exact pass) against FSIL_PATH_FP64 (every row refined over
+    all K clusters in fp64 with the reference formula and tie rule) on ALL rows, and both
+    against the oracle on 3000 sampled rows scored with the oracle's own global aggregates."""
+    fast = _full_size_gpu(ctx, "C5")
+    full = _full_size_gpu(ctx, "C5", path=PATHS["fp64"], data=(fast["X"], fast["L"], "cosine"))
+    mism = np.flatnonzero(fast["nb"] != full["nb"])
+    assert mism.size == 0, f"C5: {mism.size} neighbour mismatches vs the fp64 path, rows {mism[:5]}"
+    assert np.abs(fast["s"] - full["s"]).max() <= S_TIGHT
+    assert abs(fast["mean"] - full["mean"]) <= MEAN_TIGHT
+    Xd = fast["X"]
+    L = fast["L"].cpu().numpy()
+    n = L.shape[0]
+    dense, raw = oracle.first_appearance(L)
+    assert raw.tolist() == fast["d2r"].tolist() and np.array_equal(dense, fast["own"])
+    del fast["X"], full["X"], fast["L"], full["L"]
+    X = Xd.cpu().numpy()
+    del Xd
+    counts, sums, psi = oracle.aggregate_dense(X, dense, fast["k"], "cosine")
+    rows = np.random.default_rng(5).choice(n, 3000, replace=False)
+    _, _, sv, nbv = oracle.score_rows(X, dense, counts, sums, psi, rows, "cosine", threads=0)
+    assert np.array_equal(nbv, fast["nb"][rows])
+    assert np.abs(sv - fast["s"][rows]).max() <= S_TIGHT
+    print(f"C5 full size: S_fast={fast['mean']:.15f} S_fp64={full['mean']:.15f} "
+          f"|dS|={abs(fast['mean'] - full['mean']):.3e}")
 
 
 def _shard_loopback(X, L, metric, nshards, path=0, device_exchange=False, ctxs=None, attempts=None):
