@@ -27,7 +27,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas",
          f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 
 LIBS = {
-    "libfsil.so": ["densify.cu", "aggregate.cu", "score_ffma.cu", "score_tc.cu", "naive.cu", "finalize.cu",
+    "libfsil.so": ["densify.cu", "aggregate.cu", "score_ffma.cu", "score_tc.cu", "score_tc2.cu", "naive.cu", "finalize.cu",
                    "capi.cu"],
     "libfsil_datagen.so": ["datagen.cu"],
     # test infrastructure: the tcgen05 accumulation probe (tests/test_tc_numerics.py)

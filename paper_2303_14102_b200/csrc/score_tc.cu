@@ -24,55 +24,13 @@
 #include <cstdlib>
 #include <cuda_fp16.h>
 
-#include "score_common.cuh"
-
-#include "sm100.cuh"
+#include "score_tc.cuh"
 
 namespace fsil {
 namespace {
 
 using namespace sm100;
-
-constexpr int BM = 128;               // rows per tile = TMEM lanes
-constexpr int BK = 64;                // fp16 K elements per chunk (one 128-byte swizzle row)
-constexpr int kStgBytes = 2 * BM * 128;  // two fp32 boxes of 32 columns
-constexpr int kABytes = BM * 128;        // one fp16 A piece (hi or lo)
-constexpr int kThreads = 640;            // 20 warps (5 warpgroups)
-
-__host__ __device__ constexpr int ncb_bn_pad(int kp) { return (kp + 3) & ~3; }
-
-// Operand scalings and error-bound constants, computed on the device by prep_b from
-// the derived bounds (no host round trip between aggregation and scoring).
-struct TcScale {
-  double smul64;          // 2^(ex+em): dot = acc * smul
-  float sx;               // 2^-ex: x -> x~
-  float smul;
-  float floor_mu;         // fp16 subnormal floor of the mu pieces, per unit ||x||
-  float floor_x;          // fp16 subnormal floor of the x pieces, per unit ||mu|| (absolute in x)
-  float mu_max;           // max ||mu_k||
-  float p_max;            // max p_k (sqeuclid)
-};
-
-struct TcParams {
-  ScoreParams p;
-  int ncb, nkc;           // cluster blocks, K chunks
-  const float* colbias;   // [ncb*BN]: sqeuclid p_k, cosine 0, padding +inf
-  const __half* munorm;   // [ncb*BN]: ||mu_k|| / mu_max rounded up (neighbour error bounds)
-  int nstg;               // X staging stages
-  int nsa;                // decoupled mode: A operand slots (0: A converted in place in the X stages)
-  int dual;               // two MMA-issuing warps (alternate tiles; TS mode only)
-  const TcScale* scale;
-  float cdot;             // relative dot bound coefficient
-  unsigned long long* dbg;  // optional per-role wait-cycle counters (FSIL_TC_PROFILE)
-  int split;              // separate correction accumulator (large D)
-  uint8_t* ascratch;      // streaming mode: [grid][nkc][kStgBytes] converted A chunks (or null)
-  float exic;             // ||x||^2 relative error / u: 8.1 (fp32 blocks of 8), +2.1 on fp64 input
-  const double* xi_rows;  // per-row fp64 ||x||^2 from the aggregation pass (or null: converters form it)
-  long long* trace;       // FSIL_TRACE builds: per-tile role timestamps of CTA 0 (or null)
-  int lean;               // converters only convert; the epilogue fetches own/||x||^2 itself
-  int2* pair_rows;        // T3: rows whose neighbour is one of {nb, .y} (certified pair)
-  unsigned long long* pair_count;
-};
+using namespace tc;
 
 // Timeline tracing (compile with -DFSIL_TRACE, run with FSIL_TC_TRACE=1): CTA 0 records
 // clock64() at fixed points of each role for its first 64 tiles.
@@ -86,10 +44,6 @@ struct TcParams {
   do {              \
   } while (0)
 #endif
-
-__device__ __forceinline__ void named_bar(int id, int n) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
-}
 
 template <int BN>
 struct TcCfg {
@@ -893,40 +847,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // score_tc) + floor_mu (mu pieces' fp16 subnormal floor) + floor_x ||mu|| / ||x||
       // (x pieces' floor, absolute in x: per row, so rows far smaller than the shard's
       // largest element are still covered).  Uncertain rows go to the fp64 refinement.
-      if (valid) {
-        const float u = 5.9604645e-8f;
-        const float rowc = COS ? 1.0f : xi;
-        const float exi = tp.exic * u * xi;  // ||x||^2 error (fp32 blocks of 8; fp64 input rounding)
-        const float rx = COS ? rnf : rsqrtf(xi);  // 1/||x|| (<= 2.2u; inf for a zero row -> flagged)
-        const float cmu = tp.cdot + sc.floor_x * rx * 1.0001f;
-        // key error: the dot bound (per unit ||x|| for cosine); the key's own roundings
-        // (cosine: rsqrt 2.2u + product 0.5u + fma 0.5u on |m| <= 1, within 4u(|b1|+1));
-        // the ||x||^2 error
-        const float eps_dot1 = cmu * sc.mu_max + sc.floor_mu;  // any column, per unit ||x||
-        const float eps_m = COS ? (eps_dot1 + 4.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u)
-                                : (2.0f * eps_dot1 * xn + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
-        // the winner's key error uses its own cluster norm (the runner-up's column is
-        // not tracked: any-column bound eps_m)
-        const float mu_arg = arg >= 0 ? __half2float(mn_s[arg]) * sc.mu_max : sc.mu_max;
-        const float eps_dot1_arg = cmu * mu_arg + sc.floor_mu;
-        const float eps_m_arg = COS ? (eps_dot1_arg + 4.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u)
-                                    : (2.0f * eps_dot1_arg * xn + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
-        // neighbour certain: clear gap, and no tie through the clamps at 0 (and 2)
-        const bool full = !((b2 - b1) > eps_m + eps_m_arg) || arg < 0 || !(rowc + b2 > eps_m) ||
-                          (COS && !(rowc + b1 < 2.0f - eps_m));
-        p.nb[row] = arg >= 0 ? arg : (own == 0 ? 1 : 0);  // the refinement rewrites flagged rows
-        // T3: the neighbour is one of the top two when every other column is clearly
-        // behind the winner (third-best gap, no clamp tie) -- two fp64 means decide it
-        const bool pair = T3 && full && arg >= 0 && arg2 >= 0 && (b3 - b1) > eps_m + eps_m_arg &&
-                          (rowc + b3 > eps_m) && (!COS || rowc + b1 < 2.0f - eps_m);
-        if (pair) {
-          const unsigned long long idx = atomicAdd(tp.pair_count, 1ull);
-          tp.pair_rows[idx] = make_int2(static_cast<int>(row), arg2);
-        } else if (full) {
-          const unsigned long long idx = atomicAdd(p.flag_count, 1ull);
-          p.flag_rows[idx] = static_cast<int32_t>(row);
-        }
-      }
+      if (valid)
+        certify_row<COS, T3>(tp, sc, row, own, xi, xn, rnf, b1, b2, b3, arg, arg2,
+                             arg >= 0 ? __half2float(mn_s[arg]) : 1.0f);
       if (dbgp && warp == kEpiWarp0 && lane == 0) atomicAdd(dbgp + 13, static_cast<unsigned long long>(clock64() - tf0));
       if (quad == 0 && lane == 0) TRACE(nt, 7);
     }
@@ -941,6 +864,42 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
 }
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    FSIL_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
+    if (!ptr || q != cudaDriverEntryPointSuccess) fail(FSIL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+}  // namespace
+
+namespace tc {
+CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* ptr, uint64_t inner, uint64_t outer,
+                        uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {row_bytes};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(FSIL_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+}  // namespace tc
+
+namespace {
 
 // ---------------------------------------------------------------- prep --------
 // Global power-of-two scalings chosen so max|x~| and max|mu~| lie in [2^14, 2^15):
@@ -1009,36 +968,6 @@ __global__ void prep_b_kernel(const double* __restrict__ stats, const float* __r
   }
 }
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q{};
-    FSIL_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
-    if (!ptr || q != cudaDriverEntryPointSuccess) fail(FSIL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    fn = reinterpret_cast<EncodeTiledFn>(ptr);
-  }
-  return fn;
-}
-
-CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* ptr, uint64_t inner, uint64_t outer,
-                        uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
-  CUtensorMap m;
-  const cuuint64_t dims[2] = {inner, outer};
-  const cuuint64_t strides[1] = {row_bytes};
-  const cuuint32_t box[2] = {box_inner, box_outer};
-  const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) fail(FSIL_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
-  return m;
-}
-
 int pick_bn(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : 128; }
 
 // Shared memory with `nstg` X staging stages: operand ring, staging ring, barriers,
@@ -1085,10 +1014,21 @@ int64_t tc_tiles(const fsil_context* c, int* tile_rows) {
 void score_tc(fsil_context* c, const ScoreParams& p) {
   const bool cos = c->metric == FSIL_COSINE;
   const int bn = pick_bn(c->k);
-  const int ncb = (c->k + bn - 1) / bn;
-  const int kp = ncb * bn;
+  int ncb = (c->k + bn - 1) / bn;
   const int nkc = (c->d + BK - 1) / BK;
   const int dp = nkc * BK;
+  // CTA pairs (score_tc2.cu) for streaming cluster tables: 256-column blocks, so the
+  // B pieces and column tables are padded to a multiple of 256
+  bool pair = false;
+  {
+    TcParams probe{};
+    probe.nkc = nkc;
+    const int nstg_ = tc_stages(bn, ncb * bn, c->smem_optin);
+    const bool streaming = ncb > 1 && !(2 * nkc <= nstg_) && nkc >= nstg_;
+    pair = streaming && pair_supported(c, probe, bn);
+    if (pair) ncb = (c->k + 255) / 256 * 2;
+  }
+  const int kp = ncb * bn;
   c->tc_b.ensure(2ull * kp * dp * sizeof(__half) + kp * (sizeof(float) + sizeof(__half)) + sizeof(TcScale) + 64);
   __half* bh = c->tc_b.as<__half>();
   __half* bl = bh + static_cast<size_t>(kp) * dp;
@@ -1204,6 +1144,16 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   c->pair_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int2));
   tp.pair_rows = c->pair_rows.as<int2>();
   tp.pair_count = c->pair_count.as<unsigned long long>();  // zeroed by agg_init
+  if (pair) {
+    // one fp32 accumulator (512 TMEM columns hold two 256-column buffers): the correction
+    // products share the main accumulator, 3 MMAs per K step in its rounding bound
+    tp.split = 0;
+    tp.cdot = 1.05f * (12.0f + 2.0f * kMmaUlp * 3.0f * steps + 1.0f) * u;
+    if (c->X64) tp.cdot += 1.01f * u;
+    const bool t3p = t3_env && static_cast<int64_t>(c->k) * c->d >= 64 * 1024;
+    launch_tc_pair(c, mx, mh, ml, tp, ntiles, cos, t3p);
+    return;
+  }
   // K <= 24 at BN = 32: the epilogue scans only the first 16 / 24 columns
   const int kc_scan = bn == 32 && c->k <= 16 ? 16 : bn == 32 && c->k <= 24 ? 24 : 32;
   if (cos) {

@@ -1,0 +1,547 @@
+// score_tc2.cu -- K3 on CTA pairs: tcgen05.mma.cta_group::2 for large cluster tables.
+//
+// Same job as score_tc.cu's streaming mode -- nominate each row's neighbour cluster from
+// the split-precision ("fp16x3") dots x . mu_k with a certified bound; replaces the
+// neighbour loop of score_range (squared_euclidean.cpp:96-103, cosine.cpp:105-112) -- but
+// the MMAs are 256 x 256 x 16 over the two CTAs of a cluster (one TPC).  The single-CTA
+// kernel's 128 x 128 x 16 MMA reads 8 KB of shared memory per 64 tensor cycles (all of an
+// SM's shared-memory bandwidth) and, streaming a 4096-column table, pulls 64 KB of
+// operands from L2 per 12 MMAs.  Here each CTA holds its own 128 rows of A and its own 128
+// of the block's 256 B columns: per SM an MMA reads 8 KB per 128 cycles and the L2
+// operand traffic per flop halves.
+//
+// Roles per CTA (640 threads, 20 warps; registers as score_tc.cu):
+//   warp 0      X producer: TMA of this CTA's 128 rows on the first pass over a tile; on
+//               the later cluster blocks, cta_group::2 tensor copies of the converted
+//               chunks back from this CTA's L2-resident scratch, completing on the
+//               LEADER's a_full barrier
+//   warp 1      TMEM: cta_group::2 allocation of 512 columns (two 256-column fp32
+//               accumulators); in the leader CTA, lane 0 issues every MMA of the pair
+//   warp 2      B producer: this CTA's 128 columns (hi, lo) of each 256-column block,
+//               completing on the leader's b_full barrier
+//   warps 4-11  epilogue: two groups of four split each block's eight 32-column chunks;
+//               keys, running top-3, certification (certify_row, score_tc.cuh)
+//   warps 12-19 converters: fp32 -> fp16 hi/lo in place (2 threads per row), store of the
+//               converted chunk to the scratch, one arrival per chunk on the leader
+//
+// Cross-CTA protocol.  Barriers the MMA issuer waits on live in the leader (rank 0):
+// a_full (2 arrivals: one per CTA; reload passes add the bytes of both CTAs' copies),
+// b_full (the leader's expect_tx covers both CTAs' B bytes) and acc_empty (8 epilogue
+// warps of each CTA).  The MMA commits multicast to both CTAs' stg_empty, b_empty and
+// acc_full.  Remote arrivals are release.cluster; the issuer's waits acquire.cluster.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "score_tc.cuh"
+
+namespace fsil {
+namespace tc {
+namespace {
+
+constexpr int kPairN = 256;                // MMA N: cluster columns per block
+constexpr int kHalfN = 128;                // B columns held by each CTA
+constexpr int kBPiece = kHalfN * 128;      // one B piece (hi or lo) per stage per CTA: 16 KB
+constexpr uint32_t kPairCols = 512;        // TMEM columns: two 256-column accumulators
+constexpr int kEpi0 = 4, kConv0 = 12;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_count_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;\n" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same object in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(caddr) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t caddr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;\n" ::"r"(caddr),
+               "r"(bytes)
+               : "memory");
+}
+// wait with cluster-scope acquire: the phase may have been completed by the peer CTA
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+        : "memory");
+  } while (!ok);
+}
+// 2-D tensor copy of the pair (cta_group::2): lands in this CTA's shared memory, the
+// transaction bytes complete on the barrier at cluster address `bar_caddr` (the leader's)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_caddr, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_caddr)
+      : "memory");
+}
+template <uint32_t NCOLS>
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* smem_dst) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(smem_dst)),
+               "n"(NCOLS));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::);
+}
+template <uint32_t NCOLS>
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(NCOLS));
+}
+// D[tmem of both CTAs] (+)= A[256 x 16: 128 rows per CTA] * B[256 x 16: 128 columns per CTA]^T
+__device__ __forceinline__ void mma_f16_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// arrive on the barrier at this offset in every CTA of `mask` once the issued MMAs retire
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+
+// Shared memory (identical offsets in both CTAs: the MMA addresses the peer's operands
+// through the leader's descriptors)
+struct PairSmem {
+  static size_t bytes(int ns, int nb) {
+    return 1024 + static_cast<size_t>(ns) * kStgBytes + static_cast<size_t>(nb) * 2 * kBPiece + 64 * 8 +
+           4 * BM * 8 + 10 * BM * 4 + 2 * BM * 4 + 64;
+  }
+};
+
+template <bool COS, bool T3>
+__global__ void __launch_bounds__(kThreads, 1)
+    score_tc_pair_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
+                         const __grid_constant__ CUtensorMap tmap_bl, const __grid_constant__ CUtensorMap tmap_scr,
+                         TcParams tp, int64_t ntiles, int ns, int nb) {
+  griddep_wait();           // (PDL) prep_b's operands and every earlier phase are visible
+  if (*tp.p.abort) return;  // K speculation missed: the call is repeated (both CTAs return)
+  const ScoreParams& p = tp.p;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int ncb = tp.ncb, nkc = tp.nkc;
+  const int64_t nst = (ntiles + 1) / 2;  // super-tiles of 256 rows
+  const int64_t cid = cluster_id_x(), ncl = cluster_count_x();
+  constexpr uint32_t kIdesc = idesc_f16_f32(256, kPairN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* stg = base;                               // [ns][kStgBytes]: X fp32 -> A hi | lo in place
+  uint8_t* bring = stg + ns * kStgBytes;             // [nb][B hi | B lo] (this CTA's 128 columns)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + nb * 2 * kBPiece);
+  uint64_t* stg_full = bars;         // [ns <= 8] local: X landed (first pass)
+  uint64_t* stg_empty = bars + 8;    // [ns] local: stage free (multicast MMA commit)
+  uint64_t* a_full = bars + 16;      // [ns] leader: converted / reloaded chunk of both CTAs
+  uint64_t* b_full = bars + 24;      // [nb <= 8] leader: B of both CTAs
+  uint64_t* b_empty = bars + 32;     // [nb] local (multicast commit)
+  uint64_t* acc_full = bars + 40;    // [2] local (multicast commit)
+  uint64_t* acc_empty = bars + 42;   // [2] leader: 8 epilogue warps x 2 CTAs
+  uint64_t* meta_full = bars + 44;   // [2] local
+  uint64_t* meta_empty = bars + 46;  // [2] local
+  uint64_t* scr_ready = bars + 48;   // [1] local: a tile's converted chunks are in scratch
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 49);
+  double* meta_xi = reinterpret_cast<double*>(bars + 64);    // [2][2][BM]
+  float* part = reinterpret_cast<float*>(meta_xi + 4 * BM);  // [2][5][BM]
+  int* meta_own = reinterpret_cast<int*>(part + 10 * BM);     // [2][BM]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* const myscr = tp.ascratch + static_cast<size_t>(blockIdx.x) * nkc * kStgBytes;
+  const TcScale sc = *tp.scale;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ns; ++i) {
+      mbar_init(stg_full + i, 1);
+      mbar_init(stg_empty + i, 1);
+      mbar_init(a_full + i, 2);
+    }
+    for (int i = 0; i < nb; ++i) {
+      mbar_init(b_full + i, 1);
+      mbar_init(b_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(acc_full + i, 1);
+      mbar_init(acc_empty + i, 16);
+      mbar_init(meta_full + i, 8);
+      mbar_init(meta_empty + i, 4);
+    }
+    mbar_init(scr_ready, 1);
+    fence_barrier_init();
+    prefetch_tmap(&tmap_x);
+    prefetch_tmap(&tmap_bh);
+    prefetch_tmap(&tmap_bl);
+    prefetch_tmap(&tmap_scr);
+  }
+  if (warp == 1) tmem_alloc_pair<kPairCols>(tmem_slot);
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs' barriers initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < kEpi0) {
+    setmaxnreg_dec<64>();
+    if (warp == 0 && lane == 0) {
+      // ------------------------------------------------------------ X producer
+      uint32_t n1 = 0, ntl = 0;
+      for (int64_t st = cid; st < nst; st += ncl, ++ntl) {
+        const int row0 = static_cast<int>(st * 2 * BM + rank * BM);
+        for (int xp = 0; xp < ncb; ++xp) {
+          if (xp == 1) {  // the first pass converted and stored this tile: reuse it
+            mbar_wait(scr_ready, ntl & 1);
+            fence_proxy_async_global();
+          }
+          for (int kc = 0; kc < nkc; ++kc, ++n1) {
+            const int s1 = static_cast<int>(n1 % ns);
+            mbar_wait_cluster(stg_empty + s1, ((n1 / ns) & 1) ^ 1);  // (multicast commit)
+            if (xp > 0) {
+              const uint32_t af = mapa_u32(smem_u32(a_full + s1), 0);
+              if (leader) mbar_arrive_expect_tx_cluster(af, 2 * kStgBytes);
+              tma_load_2d_pair(stg + s1 * kStgBytes, &tmap_scr, af, 0,
+                               static_cast<int>((static_cast<int64_t>(blockIdx.x) * nkc + kc) * BM));
+              if (!leader) mbar_arrive_cluster(af);
+              continue;
+            }
+            const int nbox = (kc * BK + 32 < p.d) ? 2 : 1;
+            mbar_arrive_expect_tx(stg_full + s1, nbox * BM * 128);
+            for (int b = 0; b < nbox; ++b)
+              tma_load_2d(stg + s1 * kStgBytes + b * BM * 128, &tmap_x, stg_full + s1, kc * BK + b * 32, row0);
+          }
+        }
+      }
+    } else if (warp == 2 && lane == 0) {
+      // ------------------------------------------------------------ B producer
+      uint32_t n2 = 0;
+      for (int64_t st = cid; st < nst; st += ncl) {
+        for (int cb = 0; cb < ncb; ++cb) {
+          for (int kc = 0; kc < nkc; ++kc, ++n2) {
+            const int sb = static_cast<int>(n2 % nb);
+            uint8_t* bs = bring + sb * 2 * kBPiece;
+            mbar_wait_cluster(b_empty + sb, ((n2 / nb) & 1) ^ 1);
+            const uint32_t bf = mapa_u32(smem_u32(b_full + sb), 0);
+            if (leader) mbar_arrive_expect_tx_cluster(bf, 4 * kBPiece);
+            const int col = cb * kPairN + static_cast<int>(rank) * kHalfN;
+            tma_load_2d_pair(bs, &tmap_bh, bf, kc * BK, col);
+            tma_load_2d_pair(bs + kBPiece, &tmap_bl, bf, kc * BK, col);
+          }
+        }
+      }
+    } else if (warp == 1 && lane == 0 && leader) {
+      // ------------------------------------------------------------ MMA issuer (the pair's)
+      uint32_t n2 = 0, ia = 0, na = 0;
+      for (int64_t st = cid; st < nst; st += ncl) {
+        for (int cb = 0; cb < ncb; ++cb, ++na) {
+          const int ab = static_cast<int>(na & 1);
+          mbar_wait_cluster(acc_empty + ab, ((na >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem_base + ab * kPairN;
+          for (int kc = 0; kc < nkc; ++kc, ++n2, ++ia) {
+            const int s1 = static_cast<int>(ia % ns), sb = static_cast<int>(n2 % nb);
+            mbar_wait_cluster(a_full + s1, (ia / ns) & 1);
+            mbar_wait_cluster(b_full + sb, (n2 / nb) & 1);
+            tc_fence_after();
+            const int rem = p.d - kc * BK;
+            const int nks = rem >= BK ? 4 : (rem + 15) / 16;
+            const uint64_t dah = desc_k_sw128(smem_u32(stg + s1 * kStgBytes)), dal = dah + (kABytes >> 4);
+            const uint64_t dbh = desc_k_sw128(smem_u32(bring + sb * 2 * kBPiece)), dbl = dbh + (kBPiece >> 4);
+            for (int ks = 0; ks < nks; ++ks) {
+              const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
+              mma_f16_pair(d, dah + 2 * ks, dbh + 2 * ks, kIdesc, acc0);
+              mma_f16_pair(d, dah + 2 * ks, dbl + 2 * ks, kIdesc, 1u);
+              mma_f16_pair(d, dal + 2 * ks, dbh + 2 * ks, kIdesc, 1u);
+            }
+            mma_commit_pair(b_empty + sb, 0x3);
+            mma_commit_pair(stg_empty + s1, 0x3);
+          }
+          mma_commit_pair(acc_full + ab, 0x3);
+        }
+      }
+    }
+  } else if (warp >= kConv0) {
+    setmaxnreg_dec<72>();
+    // ------------------------------------------------------------ converters
+    const int tl = threadIdx.x - kConv0 * 32;
+    const int r = tl & (BM - 1), hq = tl >> 7;
+    const int sw = r & 7;
+    const float2 sx2 = make_float2(sc.sx, sc.sx), neg1 = make_float2(-1.f, -1.f);
+    uint32_t n1 = 0, nt = 0, tpar = 0;  // tpar bit s: parity of stage s's next X landing
+    int s1 = 0;
+    for (int64_t st = cid; st < nst; st += ncl, ++nt) {
+      const int64_t row = st * 2 * BM + rank * BM + r;
+      const int own = (hq == 0 && row < p.n) ? __ldg(p.dense + row) : -1;
+      double xi = 0.0;
+      for (int kc = 0; kc < nkc; ++kc, ++n1) {
+        mbar_wait(stg_full + s1, (tpar >> s1) & 1u);
+        tpar ^= 1u << s1;
+        uint8_t* sbase = stg + s1 * kStgBytes;
+        float4 f[8];
+        const uint8_t* srow = sbase + hq * (BM * 128) + r * 128;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) f[u] = *reinterpret_cast<const float4*>(srow + ((u ^ sw) << 4));
+        if (hq == 1 && kc * BK + 32 >= p.d) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) f[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        named_bar_sync(5, 256);  // every read of the stage precedes the in-place writes
+        uint8_t* hrow = sbase + r * 128;
+        uint8_t* lrow = hrow + BM * 128;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = 4 * hq + jj;
+          const float v[8] = {f[2 * jj].x,     f[2 * jj].y,     f[2 * jj].z,     f[2 * jj].w,
+                              f[2 * jj + 1].x, f[2 * jj + 1].y, f[2 * jj + 1].z, f[2 * jj + 1].w};
+          if (!tp.xi_rows) {  // ||x||^2: fp32 blocks of 8 (error <= 8u each), fp64 across blocks
+            float2 bs = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 ve = make_float2(v[2 * e], v[2 * e + 1]);
+              bs = __ffma2_rn(ve, ve, bs);
+            }
+            xi += static_cast<double>(bs.x + bs.y);
+          }
+          uint32_t hw[4], lw[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {  // packed f32x2: scale (exact), hi, residual (exact), lo
+            const float2 xx = __fmul2_rn(make_float2(v[2 * e], v[2 * e + 1]), sx2);
+            const __half2 h = __float22half2_rn(xx);
+            const float2 res = __ffma2_rn(__half22float2(h), neg1, xx);
+            const __half2 l = __float22half2_rn(res);
+            hw[e] = *reinterpret_cast<const uint32_t*>(&h);
+            lw[e] = *reinterpret_cast<const uint32_t*>(&l);
+          }
+          const int pos = (j ^ sw) << 4;
+          *reinterpret_cast<uint4*>(hrow + pos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+          *reinterpret_cast<uint4*>(lrow + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(5, 256);
+        if (tl == 0) {
+          // the converted chunk -> scratch (read before the MMA may free the stage), then
+          // this CTA's single arrival on the leader's a_full
+          bulk_store(myscr + static_cast<size_t>(kc) * kStgBytes, sbase, kStgBytes);
+          bulk_wait_read();
+          mbar_arrive_cluster(mapa_u32(smem_u32(a_full + s1), 0));
+        }
+        if (++s1 == ns) s1 = 0;
+      }
+      if (tl == 0) {  // this tile's chunks are all in global memory
+        bulk_wait_all();
+        mbar_arrive(scr_ready);
+      }
+      // the reload passes (ncb - 1 of nkc chunks each) go through the same stages
+      n1 += static_cast<uint32_t>((ncb - 1) * nkc);
+      s1 = static_cast<int>(n1 % ns);
+      // ||x||^2 halves and the own cluster to the epilogue
+      const int tb = nt & 1;
+      mbar_wait(meta_empty + tb, ((nt >> 1) & 1) ^ 1);
+      meta_xi[(tb * 2 + hq) * BM + r] = xi;
+      if (hq == 0) meta_own[tb * BM + r] = own;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(meta_full + tb);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (8 warps)
+    setmaxnreg_inc<136>();
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int grp = (warp - kEpi0) >> 2;
+    uint32_t na = 0, nt = 0;
+    constexpr int NQ = kPairN / 32;
+    for (int64_t st = cid; st < nst; st += ncl, ++nt) {
+      const int tb = nt & 1;
+      const int64_t row = st * 2 * BM + rank * BM + r;
+      const bool valid = row < p.n;
+      const double xi_g = (tp.xi_rows && valid) ? __ldg(tp.xi_rows + row) : 0.0;
+      mbar_wait(meta_full + tb, (nt >> 1) & 1);
+      const int own = meta_own[tb * BM + r];
+      const double xi64 = tp.xi_rows ? xi_g : meta_xi[(tb * 2) * BM + r] + meta_xi[(tb * 2 + 1) * BM + r];
+      const float xi = static_cast<float>(xi64);
+      const float xn = COS ? 0.0f : sqrtf(xi);
+      const float rnf = COS ? rsqrtf(xi) : 0.0f;
+      const float rowm = COS ? -(sc.smul * rnf) : -2.0f * sc.smul;
+      float b1 = INFINITY, b2 = INFINITY, b3 = INFINITY;
+      int arg = -1, arg2 = -1;
+      // one 32-column chunk: ranking keys (own column excluded), running top-2 / top-3
+      auto scan32 = [&](const uint32_t(&v)[32], int k0) {
+        const int ownrel = own - k0;
+        int argc = -1;
+        const float4* cb4 = reinterpret_cast<const float4*>(tp.colbias + k0);
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 bias = __ldg(cb4 + j4);
+          const float bj[4] = {bias.x, bias.y, bias.z, bias.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int j = 4 * j4 + e;
+            float m = fmaf(__uint_as_float(v[j]), rowm, bj[e]);
+            m = j == ownrel ? INFINITY : m;
+            const bool lt = m < b1;  // strict: the lowest index keeps ties
+            if (T3) {
+              const bool lt2 = m < b2;
+              arg2 = lt ? arg : (lt2 ? k0 + j : arg2);
+              arg = lt ? k0 + j : arg;
+              b3 = fminf(b3, fmaxf(b2, m));
+            } else {
+              argc = lt ? j : argc;
+            }
+            b2 = fminf(b2, fmaxf(b1, m));
+            b1 = fminf(b1, m);
+          }
+        }
+        if (!T3 && argc >= 0) arg = k0 + argc;
+      };
+      for (int cb = 0; cb < ncb; ++cb, ++na) {
+        const int ab = static_cast<int>(na & 1);
+        mbar_wait_cluster(acc_full + ab, (na >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tb0 = tmem_base + ab * kPairN + (static_cast<uint32_t>(quad * 32) << 16);
+#pragma unroll 1
+        for (int q = grp; q < NQ; q += 4) {  // this group's chunks q and q + 2, one TMEM wait
+          uint32_t v[32], w[32];
+          tmem_ld32_issue(tb0 + q * 32, v);
+          tmem_ld32_issue(tb0 + (q + 2) * 32, w);
+          tmem_ld_wait2(v, w);
+          scan32(v, cb * kPairN + q * 32);
+          scan32(w, cb * kPairN + (q + 2) * 32);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_u32(smem_u32(acc_empty + ab), 0));
+      }
+      // ---- merge the two column halves (group 1 -> smem -> group 0)
+      float* pt = part + tb * 5 * BM;
+      if (grp == 1) {
+        pt[0 * BM + r] = b1;
+        pt[1 * BM + r] = b2;
+        pt[2 * BM + r] = __int_as_float(arg);
+        pt[3 * BM + r] = b3;
+        pt[4 * BM + r] = __int_as_float(arg2);
+      }
+      named_bar_sync(1, 256);
+      if (grp == 1) continue;
+      const float c1 = pt[0 * BM + r], c2 = pt[1 * BM + r];
+      const int a2 = __float_as_int(pt[2 * BM + r]);
+      if (T3) {
+        const float c3 = pt[3 * BM + r];
+        const int a2b = __float_as_int(pt[4 * BM + r]);
+        auto before = [](float x, int ix, float y, int iy) { return x < y || (x == y && ix >= 0 && (iy < 0 || ix < iy)); };
+        auto insert = [&](float m, int im) {
+          b3 = fminf(b3, fmaxf(b2, m));
+          if (before(m, im, b1, arg)) {
+            b2 = b1;
+            arg2 = arg;
+            b1 = m;
+            arg = im;
+          } else if (before(m, im, b2, arg2)) {
+            b2 = m;
+            arg2 = im;
+          }
+        };
+        insert(c1, a2);
+        insert(c2, a2b);
+        b3 = fminf(b3, c3);
+      } else {
+        const float nb1 = fminf(b1, c1);
+        b2 = fminf(fminf(fmaxf(b1, c1), b2), c2);
+        arg = (c1 < b1 || (c1 == b1 && a2 >= 0 && (arg < 0 || a2 < arg))) ? a2 : arg;
+        b1 = nb1;
+      }
+      // group 0 has read the partials and the meta slot: both may be reused
+      __syncwarp();
+      if (lane == 0) mbar_arrive(meta_empty + tb);
+      if (valid)
+        certify_row<COS, T3>(tp, sc, row, own, xi, xn, rnf, b1, b2, b3, arg, arg2,
+                             arg >= 0 ? __half2float(__ldg(tp.munorm + arg)) : 1.0f);
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs done with the pair's TMEM and barriers
+  if (warp == 1) tmem_dealloc_pair<kPairCols>(tmem_base);
+}
+
+}  // namespace
+
+bool pair_supported(const fsil_context* c, const TcParams& tp, int bn) {
+  static const bool env = [] {
+    const char* e = std::getenv("FSIL_TC_PAIR");
+    return !e || std::atoi(e) != 0;
+  }();
+  // streaming regime only (several 256-column blocks, a tile's chunks too many to keep),
+  // an even grid of one CTA per SM, and the 8 (X) + 8 (B) barrier slots
+  const int ncb2 = (c->k + kPairN - 1) / kPairN;
+  return env && bn == 128 && ncb2 >= 2 && tp.nkc >= 3 && c->num_sms >= 2 && !c->X64 &&
+         PairSmem::bytes(3, 3) <= c->smem_optin;
+}
+
+void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
+                    TcParams tp, int64_t ntiles, bool cos, bool t3) {
+  // stages: X/A and B rings of 32 KB each; as many as fit, at least 3 + 3, at most 8 + 8
+  int ns = 3, nb = 3;
+  while (PairSmem::bytes(ns + 1, nb) <= c->smem_optin && ns < std::min(tp.nkc, 8) && ns <= nb) ++ns;
+  while (PairSmem::bytes(ns, nb + 1) <= c->smem_optin && nb < 8) ++nb;
+  tp.ncb = (c->k + kPairN - 1) / kPairN;
+  const int grid = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(2 * ((ntiles + 1) / 2), c->num_sms & ~1)));
+  c->a_scratch.ensure(static_cast<size_t>(grid) * tp.nkc * kStgBytes);
+  tp.ascratch = c->a_scratch.as<uint8_t>();
+  // the scratch as a 2-D tensor of 256-byte rows: one 32 KB box = one converted chunk
+  const CUtensorMap mscr = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_UINT16, tp.ascratch, 128,
+                                       static_cast<uint64_t>(grid) * tp.nkc * BM, 256, 128, BM,
+                                       CU_TENSOR_MAP_SWIZZLE_NONE);
+  const size_t smem = PairSmem::bytes(ns, nb);
+  auto kern = cos ? (t3 ? score_tc_pair_kernel<true, true> : score_tc_pair_kernel<true, false>)
+                  : (t3 ? score_tc_pair_kernel<false, true> : score_tc_pair_kernel<false, false>);
+  FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  if (c->timing) {  // the kernel alone, for the roofline (ms_score_kernel)
+    FSIL_CUDA(cudaEventRecord(c->ev[7], c->stream));
+    c->ev7_recorded = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  FSIL_CUDA(cudaLaunchKernelEx(&cfg, kern, mx, mh, ml, mscr, tp, ntiles, ns, nb));
+  FSIL_LAUNCHED(c);
+}
+
+}  // namespace tc
+}  // namespace fsil
