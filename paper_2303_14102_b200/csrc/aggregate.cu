@@ -758,6 +758,304 @@ __global__ void __launch_bounds__(256) agg_piece_kernel(
   }
 }
 
+// ---------------------------------------------------------------- path 2 ----
+// Hand-written stable counting sort of the rows by dense label (no library sort):
+//   count   : G warp-chunks of L consecutive rows; each warp histograms its chunk in
+//             shared memory (match_any groups equal labels) -> hist[c][g]
+//   offsets : per label, an exclusive scan over the chunks (a row of chunk g lands
+//             after every row of chunks < g with the same label) + the label's total
+//   starts  : one block scans the K totals -> segment bounds, pieces per cluster and
+//             their exclusive scan (the piece table)
+//   scatter : each warp walks its chunk again in row order; a row's slot is its label's
+//             running counter + its rank among equal labels in the 32-row group
+// Rows of a label keep ascending row order, so every piece sum below is a fixed
+// left-to-right order: bit-identical results run to run.
+__global__ void __launch_bounds__(128) label_count_kernel(const int32_t* __restrict__ dense, int64_t n,
+                                                          int64_t L, int G, int k, int32_t* __restrict__ hist) {
+  extern __shared__ int32_t hsh[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * (blockDim.x >> 5) + w;
+  int32_t* h = hsh + static_cast<size_t>(w) * k;
+  for (int c = lane; c < k; c += 32) h[c] = 0;
+  __syncwarp();
+  if (g >= G) return;
+  const int64_t b0 = static_cast<int64_t>(g) * L, b1 = min(n, b0 + L);
+  constexpr int U = 4;  // 32-row groups whose labels are in flight together
+  for (int64_t base = b0; base < b1; base += 32 * U) {
+    int lab[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * 32 + lane;
+      lab[u] = i < b1 ? __ldg(dense + i) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned peers = __match_any_sync(0xffffffffu, lab[u]);
+      if (lab[u] >= 0 && lane == __ffs(peers) - 1) h[lab[u]] += __popc(peers);
+      __syncwarp();
+    }
+  }
+  for (int c = lane; c < k; c += 32) hist[static_cast<size_t>(c) * G + g] = h[c];
+}
+
+// block c: exclusive scan of hist[c][0..G) in place; totals[c] = the label's row count
+__global__ void __launch_bounds__(256) label_offsets_kernel(int32_t* __restrict__ hist, int G, int64_t* totals) {
+  __shared__ int32_t ws[8];
+  const int c = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int32_t* h = hist + static_cast<size_t>(c) * G;
+  int32_t carry = 0;
+  for (int base = 0; base < G; base += 256) {
+    const int j = base + threadIdx.x;
+    const int32_t v = j < G ? h[j] : 0;
+    int32_t x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    if (lane == 31) ws[w] = x;
+    __syncthreads();
+    int32_t wpre = 0, tot = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      wpre += q < w ? ws[q] : 0;
+      tot += ws[q];
+    }
+    if (j < G) h[j] = carry + wpre + x - v;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) totals[c] = carry;
+}
+
+// one block: segment bounds from the totals, pieces per cluster and the piece table
+__global__ void __launch_bounds__(1024) label_starts_kernel(const int64_t* __restrict__ totals, int k,
+                                                            int64_t* seg_begin, int64_t* seg_end,
+                                                            int64_t* piece_start) {
+  __shared__ int64_t ws[2][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t carry_r = 0, carry_p = 0;
+  for (int base = 0; base < k + 1; base += blockDim.x) {
+    const int c = base + threadIdx.x;
+    const int64_t t = c < k ? totals[c] : 0;
+    const int64_t pc = (t + kPieceRows - 1) / kPieceRows;
+    int64_t xr = t, xp = pc;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t yr = __shfl_up_sync(0xffffffffu, xr, off), yp = __shfl_up_sync(0xffffffffu, xp, off);
+      if (lane >= off) {
+        xr += yr;
+        xp += yp;
+      }
+    }
+    if (lane == 31) {
+      ws[0][w] = xr;
+      ws[1][w] = xp;
+    }
+    __syncthreads();
+    int64_t pr = 0, pp = 0, tr = 0, tp = 0;
+    for (int q = 0; q < nw; ++q) {
+      pr += q < w ? ws[0][q] : 0;
+      pp += q < w ? ws[1][q] : 0;
+      tr += ws[0][q];
+      tp += ws[1][q];
+    }
+    if (c <= k) {
+      const int64_t begin = carry_r + pr + xr - t;
+      if (c < k) {
+        seg_begin[c] = begin;
+        seg_end[c] = begin + t;
+      }
+      piece_start[c] = carry_p + pp + xp - pc;
+    }
+    carry_r += tr;
+    carry_p += tp;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(128) label_scatter_kernel(const int32_t* __restrict__ dense, int64_t n,
+                                                            int64_t L, int G, int k,
+                                                            const int32_t* __restrict__ hist,
+                                                            const int64_t* __restrict__ seg_begin,
+                                                            int32_t* __restrict__ sorted_rows) {
+  extern __shared__ int32_t hsh[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * (blockDim.x >> 5) + w;
+  if (g >= G) return;
+  int32_t* cnt = hsh + static_cast<size_t>(w) * k;  // next free slot of each label
+  for (int c = lane; c < k; c += 32)
+    cnt[c] = static_cast<int32_t>(seg_begin[c]) + hist[static_cast<size_t>(c) * G + g];
+  __syncwarp();
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t b0 = static_cast<int64_t>(g) * L, b1 = min(n, b0 + L);
+  constexpr int U = 4;
+  for (int64_t base = b0; base < b1; base += 32 * U) {
+    int lab[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * 32 + lane;
+      lab[u] = i < b1 ? __ldg(dense + i) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {  // groups in row order: the sort stays stable
+      const bool ok = lab[u] >= 0;
+      const unsigned peers = __match_any_sync(0xffffffffu, lab[u]);
+      if (ok) sorted_rows[cnt[lab[u]] + __popc(peers & lt)] = static_cast<int32_t>(base + u * 32 + lane);
+      __syncwarp();
+      if (ok && lane == __ffs(peers) - 1) cnt[lab[u]] += __popc(peers);
+      __syncwarp();
+    }
+  }
+}
+
+// Pieces with the rows staged by bulk copies (fp32 rows of 16-byte multiples): each
+// warp keeps R slots of rpw = 32 / lpr gathered rows in flight in its own shared-memory
+// ring (one mbarrier per slot; lanes 0..rpw-1 each copy their row of the slot), so the
+// row loads of a piece overlap instead of one row load per sub-group at a time.  The
+// per-row arithmetic and the piece layout are agg_piece_kernel's.
+template <bool COS, int CPL>
+__global__ void __launch_bounds__(256) agg_piece_ring_kernel(
+    const float* __restrict__ X, const int32_t* __restrict__ rows, int64_t n, int d,
+    int64_t row_offset, int k, int lpr, int R, const int64_t* __restrict__ seg_begin,
+    const int64_t* __restrict__ seg_end, const int64_t* __restrict__ piece_start,
+    double* __restrict__ piece_out, int64_t* checks, float* xmax, double* __restrict__ xi_out) {
+  extern __shared__ __align__(128) uint8_t rsh[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t p0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int rpw = 32 / lpr;
+  const int row_bytes = d * 4;
+  const int slot_bytes = rpw * row_bytes;
+  uint8_t* ring = rsh + static_cast<size_t>(w) * R * slot_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rsh + static_cast<size_t>(blockDim.x >> 5) * R * slot_bytes) + w * R;
+  const int64_t total = piece_start[k];
+  if (lane == 0)
+    for (int s = 0; s < R; ++s) sm100::mbar_init(bars + s, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncwarp();
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  uint32_t used = 0;  // slot uses so far (mbarrier phases continue across pieces)
+  for (int64_t p = p0; p < total; p += nwarps) {
+  int lo = 0, hi = k - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (piece_start[mid] <= p) lo = mid;
+    else hi = mid - 1;
+  }
+  const int c = lo;
+  const int64_t b0 = seg_begin[c] + (p - piece_start[c]) * kPieceRows;
+  const int64_t b1 = min(seg_end[c], b0 + kPieceRows);
+  const int iters = static_cast<int>((b1 - b0 + rpw - 1) / rpw);
+  // slot s <- the rows of iteration it (lanes 0..rpw-1 one row each; lane 0 arms the tx)
+  auto fill = [&](int it, int s) {
+    const int64_t pos = b0 + static_cast<int64_t>(it) * rpw + lane;
+    const int nrows = static_cast<int>(min(static_cast<int64_t>(rpw), b1 - (b0 + static_cast<int64_t>(it) * rpw)));
+    if (lane == 0) sm100::mbar_arrive_expect_tx(bars + s, nrows * row_bytes);
+    if (lane < nrows) {
+      const int64_t r = __ldg(rows + pos);
+      sm100::bulk_load(ring + static_cast<size_t>(s) * slot_bytes + lane * row_bytes, X + r * d, row_bytes, bars + s);
+    }
+  };
+  for (int j = 0; j < R && j < iters; ++j) fill(j, static_cast<int>((used + j) % R));
+  const int sub = lane / lpr, li = lane % lpr;
+  const int nchunks = d >> 2;
+  double acc[CPL][4];
+#pragma unroll
+  for (int q = 0; q < CPL; ++q)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[q][e] = 0.0;
+  double psi = 0.0, cnt = 0.0;
+  float amax = 0.f;
+  for (int it = 0; it < iters; ++it) {
+    const uint32_t u = used + it;
+    const int s = static_cast<int>(u % R);
+    sm100::mbar_wait(bars + s, (u / R) & 1);
+    const int64_t pos = b0 + static_cast<int64_t>(it) * rpw + sub;
+    const bool valid = pos < b1;
+    const int64_t r = valid ? __ldg(rows + pos) : 0;
+    const uint8_t* srow = ring + static_cast<size_t>(s) * slot_bytes + sub * row_bytes;
+    float v[CPL][4];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int ch = li + q * lpr;
+      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (valid && ch < nchunks) t = *reinterpret_cast<const float4*>(srow + ch * 16);
+      v[q][0] = t.x; v[q][1] = t.y; v[q][2] = t.z; v[q][3] = t.w;
+    }
+    __syncwarp();  // every lane has read the slot: refill it
+    if (it + R < iters) fill(it + R, s);
+    double ss = 0.0;
+    bool finite = true;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const double x = v[q][e];
+        ss += x * x;
+        finite = finite && isfinite(v[q][e]);
+        amax = fmaxf(amax, fabsf(v[q][e]));
+      }
+    if (!finite) {
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int l = (li + q * lpr) * 4 + e;
+          if (l < d && !isfinite(v[q][e])) atomic_min_i64(checks, (row_offset + r) * d + l);
+        }
+    }
+    double scale = 1.0;
+    if (COS) {
+      for (int off = lpr >> 1; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off, lpr);
+      if (valid && li == 0 && xi_out) xi_out[r] = ss;
+      if (!valid) continue;
+      if (ss == 0.0) {
+        if (li == 0) atomic_min_i64(checks + 1, row_offset + r);
+        continue;
+      }
+      scale = 1.0 / sqrt(ss);
+    } else {
+      if (!valid) continue;
+      psi += ss;
+    }
+    cnt += 1.0;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        acc[q][e] += COS ? static_cast<double>(v[q][e]) * scale : static_cast<double>(v[q][e]);
+  }
+  for (int off = 16; off >= lpr; off >>= 1) {
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[q][e] += __shfl_xor_sync(0xffffffffu, acc[q][e], off);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+  }
+  if (!COS)
+    for (int off = 16; off > 0; off >>= 1) psi += __shfl_xor_sync(0xffffffffu, psi, off);
+  for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  if (lane == 0 && amax > 0.f) atomic_max_nonneg_f32(xmax, amax);
+  const int S1 = COS ? d + 1 : d + 2;
+  double* out = piece_out + p * S1;
+  if (lane == 0) {
+    out[0] = cnt;
+    if (!COS) out[1] = psi;
+  }
+  if (sub == 0) {
+    double* sums = out + (COS ? 1 : 2);
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int l = (li + q * lpr) * 4 + e;
+        if (l < d) sums[l] = acc[q][e];
+      }
+  }
+  used += static_cast<uint32_t>(iters);
+  }
+}
+
 // Piece partials -> stats.  A block folds one cluster's 32-column slice: warp w sums the
 // pieces p = w, w + 8, ... (lanes = columns: coalesced, independent loads), then the 8
 // warp partials in a fixed order -- deterministic, and a large cluster's pieces are
@@ -1051,49 +1349,109 @@ void aggregate(fsil_context* c) {
   if (cpl > cpl_max)
     fail(FSIL_ERR_INVALID_ARGUMENT, "feature dimension too large for this build (D <= 1024)");
   c->agg_path = 2;
-  const int n32 = static_cast<int>(c->n);
-  c->iota.ensure(c->n * sizeof(int32_t));
-  c->sort_keys.ensure(c->n * sizeof(int32_t));
-  c->sort_vals.ensure(c->n * sizeof(int32_t));
-  iota_kernel<<<static_cast<unsigned>((c->n + 255) / 256), 256, 0, c->stream>>>(c->iota.as<int32_t>(), c->n);
-  FSIL_LAUNCHED(c);
-  int bits = 1;
-  while ((int64_t(1) << bits) < c->k) ++bits;
-  size_t tmp_bytes = 0;
-  FSIL_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, c->dense.as<int32_t>(),
-                                            c->sort_keys.as<int32_t>(), c->iota.as<int32_t>(),
-                                            c->sort_vals.as<int32_t>(), n32, 0, bits, c->stream));
-  c->sort_tmp.ensure(tmp_bytes);
-  FSIL_CUDA(cub::DeviceRadixSort::SortPairs(c->sort_tmp.p, tmp_bytes, c->dense.as<int32_t>(),
-                                            c->sort_keys.as<int32_t>(), c->iota.as<int32_t>(),
-                                            c->sort_vals.as<int32_t>(), n32, 0, bits, c->stream));
-  c->launches += 4;
   c->seg_start.ensure((2 * static_cast<size_t>(c->k) + 2) * sizeof(int64_t));
   int64_t* seg_begin = c->seg_start.as<int64_t>();
   int64_t* seg_end = seg_begin + c->k + 1;
-  FSIL_CUDA(cudaMemsetAsync(seg_begin, 0, (2 * static_cast<size_t>(c->k) + 2) * sizeof(int64_t), c->stream));
-  segment_bounds_kernel<<<static_cast<unsigned>((c->n + 255) / 256), 256, 0, c->stream>>>(
-      c->sort_keys.as<int32_t>(), c->n, seg_begin, seg_end);
-  FSIL_LAUNCHED(c);
   c->piece_start.ensure((2 * static_cast<size_t>(c->k) + 4) * sizeof(int64_t));
   int64_t* ppc = c->piece_start.as<int64_t>();
   int64_t* piece_start = ppc + c->k + 2;
-  pieces_per_cluster_kernel<<<(c->k + 1 + 255) / 256, 256, 0, c->stream>>>(seg_begin, seg_end, c->k, ppc);
-  FSIL_LAUNCHED(c);
-  size_t scan_bytes = 0;
-  FSIL_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, ppc, piece_start, c->k + 1, c->stream));
-  if (scan_bytes > c->sort_tmp.bytes) c->sort_tmp.ensure(scan_bytes);
-  FSIL_CUDA(cub::DeviceScan::ExclusiveSum(c->sort_tmp.p, scan_bytes, ppc, piece_start, c->k + 1, c->stream));
-  c->launches += 1;
+  c->sort_vals.ensure(c->n * sizeof(int32_t));
+  // stable counting sort by dense label (hand-written, path 2 above): warps per block so
+  // that the per-warp label counters fit shared memory
+  int sw = 4;
+  while (sw > 1 && static_cast<size_t>(sw) * c->k * sizeof(int32_t) > budget) sw >>= 1;
+  static const bool cub_env = [] {
+    const char* e = std::getenv("FSIL_AGG_CUB");
+    return e && std::atoi(e) != 0;
+  }();
+  if (!cub_env && static_cast<size_t>(sw) * c->k * sizeof(int32_t) <= budget) {
+    // warp-chunks: enough warps to keep the label loads in flight, while the K x G
+    // histogram stays <= 16M entries
+    const int64_t g_cap = std::max<int64_t>(static_cast<int64_t>(c->num_sms) * 16, (int64_t(16) << 20) / c->k);
+    const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((c->n + 1023) / 1024, g_cap)));
+    const int64_t L = (c->n + G - 1) / G;
+    const size_t hist_bytes = static_cast<size_t>(c->k) * G * sizeof(int32_t);
+    c->sort_tmp.ensure(hist_bytes + static_cast<size_t>(c->k) * sizeof(int64_t) + 64);
+    int32_t* hist = c->sort_tmp.as<int32_t>();
+    int64_t* totals = reinterpret_cast<int64_t*>(c->sort_tmp.as<uint8_t>() + ((hist_bytes + 15) / 16) * 16);
+    const unsigned sgrid = static_cast<unsigned>((G + sw - 1) / sw);
+    const size_t ssm = static_cast<size_t>(sw) * c->k * sizeof(int32_t);
+    if (ssm > 48 * 1024) {
+      FSIL_CUDA(cudaFuncSetAttribute(label_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ssm)));
+      FSIL_CUDA(cudaFuncSetAttribute(label_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ssm)));
+    }
+    label_count_kernel<<<sgrid, 32 * sw, ssm, c->stream>>>(c->dense.as<int32_t>(), c->n, L, G, c->k, hist);
+    label_offsets_kernel<<<static_cast<unsigned>(c->k), 256, 0, c->stream>>>(hist, G, totals);
+    label_starts_kernel<<<1, 1024, 0, c->stream>>>(totals, c->k, seg_begin, seg_end, piece_start);
+    label_scatter_kernel<<<sgrid, 32 * sw, ssm, c->stream>>>(c->dense.as<int32_t>(), c->n, L, G, c->k, hist,
+                                                             seg_begin, c->sort_vals.as<int32_t>());
+    c->launches += 4;
+  } else {
+    // very large K: the library radix sort (cub) and scan
+    const int n32 = static_cast<int>(c->n);
+    c->iota.ensure(c->n * sizeof(int32_t));
+    c->sort_keys.ensure(c->n * sizeof(int32_t));
+    iota_kernel<<<static_cast<unsigned>((c->n + 255) / 256), 256, 0, c->stream>>>(c->iota.as<int32_t>(), c->n);
+    FSIL_LAUNCHED(c);
+    int bits = 1;
+    while ((int64_t(1) << bits) < c->k) ++bits;
+    size_t tmp_bytes = 0;
+    FSIL_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, c->dense.as<int32_t>(),
+                                              c->sort_keys.as<int32_t>(), c->iota.as<int32_t>(),
+                                              c->sort_vals.as<int32_t>(), n32, 0, bits, c->stream));
+    c->sort_tmp.ensure(tmp_bytes);
+    FSIL_CUDA(cub::DeviceRadixSort::SortPairs(c->sort_tmp.p, tmp_bytes, c->dense.as<int32_t>(),
+                                              c->sort_keys.as<int32_t>(), c->iota.as<int32_t>(),
+                                              c->sort_vals.as<int32_t>(), n32, 0, bits, c->stream));
+    c->launches += 4;
+    FSIL_CUDA(cudaMemsetAsync(seg_begin, 0, (2 * static_cast<size_t>(c->k) + 2) * sizeof(int64_t), c->stream));
+    segment_bounds_kernel<<<static_cast<unsigned>((c->n + 255) / 256), 256, 0, c->stream>>>(
+        c->sort_keys.as<int32_t>(), c->n, seg_begin, seg_end);
+    FSIL_LAUNCHED(c);
+    pieces_per_cluster_kernel<<<(c->k + 1 + 255) / 256, 256, 0, c->stream>>>(seg_begin, seg_end, c->k, ppc);
+    FSIL_LAUNCHED(c);
+    size_t scan_bytes = 0;
+    FSIL_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, ppc, piece_start, c->k + 1, c->stream));
+    if (scan_bytes > c->sort_tmp.bytes) c->sort_tmp.ensure(scan_bytes);
+    FSIL_CUDA(cub::DeviceScan::ExclusiveSum(c->sort_tmp.p, scan_bytes, ppc, piece_start, c->k + 1, c->stream));
+    c->launches += 1;
+  }
   const int64_t max_pieces = c->n / kPieceRows + c->k + 1;
   const int S1 = cos ? c->d + 1 : c->d + 2;
   c->partials.ensure(static_cast<size_t>(max_pieces) * S1 * sizeof(double));
   const int cpl_t = cpl <= 1 ? 1 : cpl <= 2 ? 2 : cpl <= 4 ? 4 : cpl <= 8 ? 8 : cpl <= 16 ? 16 : 32;
   const int32_t* srows = c->sort_vals.as<int32_t>();
+  static const bool ring_env = [] {
+    const char* e = std::getenv("FSIL_AGG_RING");
+    return !e || std::atoi(e) != 0;
+  }();
   double* pout = c->partials.as<double>();
   if (x64) {
     if (cos) launch_pieces<true>(c, c->X64, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);
     else launch_pieces<false>(c, c->X64, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);
+  } else if (vec == 4 && cpl_t <= 8 && c->d >= 256 && ring_env) {
+    // wide rows (>= 1 KB): bulk-copy ring, R slots per warp (~24 KB of rows in flight per
+    // warp), persistent warps striding over the pieces.  Narrow rows keep the register
+    // ring of agg_piece_kernel (one bulk copy per small row costs more than it hides).
+    const int rpw = 32 / lpr;
+    const int slot = rpw * c->d * 4;
+    const int R = static_cast<int>(std::max(2, std::min(16, 24576 / slot)));
+    const int W = 8;
+    const size_t rsm = static_cast<size_t>(W) * R * slot + static_cast<size_t>(W) * R * 8;
+    const int per_sm = std::max(1, static_cast<int>(std::min<size_t>(2, budget / rsm)));
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
+        1, std::min<int64_t>((max_pieces + W - 1) / W, static_cast<int64_t>(c->num_sms) * per_sm)));
+#define FSIL_AGG_RING(C)                                                                                   \
+  if (cpl_t == C) {                                                                                        \
+    auto kern = cos ? agg_piece_ring_kernel<true, C> : agg_piece_ring_kernel<false, C>;                    \
+    FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsm))); \
+    kern<<<grid, 32 * W, rsm, c->stream>>>(c->X, srows, c->n, c->d, c->row_offset, c->k, lpr, R, seg_begin,  \
+                                           seg_end, piece_start, pout, checks, c->xmax.as<float>(),          \
+                                           c->xi_valid ? c->xi_rows.as<double>() : nullptr);                  \
+    FSIL_LAUNCHED(c);                                                                                      \
+  }
+    FSIL_AGG_RING(1) else FSIL_AGG_RING(2) else FSIL_AGG_RING(4) else FSIL_AGG_RING(8)
+#undef FSIL_AGG_RING
   } else {
     if (cos) launch_pieces<true>(c, c->X, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);
     else launch_pieces<false>(c, c->X, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);

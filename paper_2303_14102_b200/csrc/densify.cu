@@ -25,6 +25,7 @@ namespace fsil {
 namespace {
 
 constexpr int kSmemSlots = 1024;
+constexpr int kMapSmemSlots = 8192;  // map: tables up to this many slots live in shared memory (96 KB)
 constexpr int kSmallK = 2048;    // finish kernel: dictionary held in shared memory
 
 __device__ __forceinline__ unsigned long long ekey(uint32_t epoch, int32_t lab) {
@@ -78,10 +79,12 @@ __device__ int64_t find_slot(const unsigned long long* keys, uint32_t mask, uint
 // each run of equal labels in a warp touches the table.
 __device__ __forceinline__ void collect_body(const int32_t* __restrict__ labels, int64_t n, int64_t chunk,
                                              unsigned long long* gkeys, unsigned long long* gvals, uint32_t mask,
-                                             uint32_t epoch, int* overflow) {
-  __shared__ unsigned long long skeys[kSmemSlots];
-  __shared__ uint32_t svals[kSmemSlots];
-  for (int i = threadIdx.x; i < kSmemSlots; i += blockDim.x) {
+                                             uint32_t epoch, int* overflow, int nslots) {
+  // nslots (a power of two, dynamic shared memory): ~4x the expected label count, so the
+  // bounded probe sequences rarely spill to the global table
+  extern __shared__ __align__(8) unsigned long long skeys[];
+  uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + nslots);
+  for (int i = threadIdx.x; i < nslots; i += blockDim.x) {
     skeys[i] = 0;
     svals[i] = 0xffffffffu;
   }
@@ -105,7 +108,7 @@ __device__ __forceinline__ void collect_body(const int32_t* __restrict__ labels,
       const unsigned peers = __match_any_sync(0xffffffffu, key);
       if (!valid || (__ffs(peers) - 1) != lane) continue;
       const uint32_t row = static_cast<uint32_t>(i);
-      uint32_t h = hash32(static_cast<uint32_t>(lab[u])) & (kSmemSlots - 1);
+      uint32_t h = hash32(static_cast<uint32_t>(lab[u])) & (nslots - 1);
       bool done = false;
       for (int probe = 0; probe < 16; ++probe) {  // bounded: overflow goes global
         unsigned long long cur = skeys[h];
@@ -118,13 +121,13 @@ __device__ __forceinline__ void collect_body(const int32_t* __restrict__ labels,
           done = true;
           break;
         }
-        h = (h + 1) & (kSmemSlots - 1);
+        h = (h + 1) & (nslots - 1);
       }
       if (!done && !global_insert(gkeys, gvals, mask, epoch, lab[u], row)) atomicExch(overflow, 1);
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kSmemSlots; i += blockDim.x) {
+  for (int i = threadIdx.x; i < nslots; i += blockDim.x) {
     const unsigned long long key = skeys[i];
     if (key != 0 &&
         !global_insert(gkeys, gvals, mask, epoch, static_cast<int32_t>(static_cast<uint32_t>(key)), svals[i]))
@@ -135,9 +138,9 @@ __device__ __forceinline__ void collect_body(const int32_t* __restrict__ labels,
 __global__ void __launch_bounds__(256) densify_collect_kernel(const int32_t* __restrict__ labels, int64_t n,
                                                               int64_t chunk, unsigned long long* gkeys,
                                                               unsigned long long* gvals, uint32_t mask,
-                                                              uint32_t epoch, int* overflow) {
+                                                              uint32_t epoch, int* overflow, int nslots) {
   griddep_wait();
-  collect_body(labels, n, chunk, gkeys, gvals, mask, epoch, overflow);
+  collect_body(labels, n, chunk, gkeys, gvals, mask, epoch, overflow, nslots);
 }
 
 // Single block: compact the current-epoch slots, rank by first row, write the dense
@@ -214,15 +217,46 @@ __device__ __forceinline__ void map_body(const int32_t* __restrict__ labels, int
   // k_lim: the K the following kernels are launched for (the speculated K, or INT_MAX when
   // the host waits for the count).  An id outside [0, k_lim) -- only possible when the
   // speculation misses -- is stored as 0 and flagged, so every later kernel stays in bounds.
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int64_t slot = find_slot<coherent>(gkeys, mask, epoch, __ldg(labels + i));
-    int32_t dj = slot >= 0 ? (coherent ? __ldcg(slot_dense + slot) : slot_dense[slot]) : -1;
-    if (dj < 0 || dj >= k_lim) {
-      atomicExch(missing, 1);
-      dj = 0;
+  // Tables of <= kMapSmemSlots slots are copied to shared memory first (every lookup then
+  // probes shared memory); U rows per thread are looked up independently.
+  extern __shared__ __align__(8) unsigned long long tkeys[];
+  const bool local = mask + 1 <= static_cast<uint32_t>(kMapSmemSlots);
+  int32_t* tdense = reinterpret_cast<int32_t*>(tkeys + (mask + 1));
+  if (local) {
+    for (uint32_t i = threadIdx.x; i <= mask; i += blockDim.x) {
+      const unsigned long long key = coherent ? __ldcg(gkeys + i) : gkeys[i];
+      tkeys[i] = key;
+      if (static_cast<uint32_t>(key >> 32) == epoch) tdense[i] = coherent ? __ldcg(slot_dense + i) : slot_dense[i];
     }
-    dense[i] = dj;
+    __syncthreads();
+  }
+  constexpr int U = 4;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    int32_t lab[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      lab[u] = i < n ? __ldg(labels + i) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= n) break;
+      int32_t dj;
+      if (local) {
+        const int64_t slot = find_slot<false>(tkeys, mask, epoch, lab[u]);
+        dj = slot >= 0 ? tdense[slot] : -1;
+      } else {
+        const int64_t slot = find_slot<coherent>(gkeys, mask, epoch, lab[u]);
+        dj = slot >= 0 ? (coherent ? __ldcg(slot_dense + slot) : slot_dense[slot]) : -1;
+      }
+      if (dj < 0 || dj >= k_lim) {
+        atomicExch(missing, 1);
+        dj = 0;
+      }
+      dense[i] = dj;
+    }
   }
 }
 
@@ -349,8 +383,39 @@ void launch_collect(fsil_context* c, int64_t cap, uint32_t epoch) {
   if (c->n == 0) return;
   const int grid = grid_for(c->n, 1024, c->num_sms, 2);
   const int64_t chunk = (c->n + grid - 1) / grid;
-  launch_pdl(c, densify_collect_kernel, grid, 256, 0, c->labels, c->n, chunk, c->ht_keys.as<unsigned long long>(),
-             c->ht_vals.as<unsigned long long>(), static_cast<uint32_t>(cap - 1), epoch, c->counters.as<int>());
+  // shared-memory dedup slots: ~4x the previous call's label count (1024 .. 4096)
+  int nslots = kSmemSlots;
+  while (nslots < 4096 && nslots < 4 * c->k_last) nslots <<= 1;
+  const size_t smem = static_cast<size_t>(nslots) * (sizeof(unsigned long long) + sizeof(uint32_t));
+  static bool attr = false;
+  if (!attr) {
+    FSIL_CUDA(cudaFuncSetAttribute(densify_collect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 12));
+    attr = true;
+  }
+  launch_pdl(c, densify_collect_kernel, grid, 256, smem, c->labels, c->n, chunk, c->ht_keys.as<unsigned long long>(),
+             c->ht_vals.as<unsigned long long>(), static_cast<uint32_t>(cap - 1), epoch, c->counters.as<int>(), nslots);
+}
+
+// The map launch: a table of <= kMapSmemSlots slots is staged in shared memory by every
+// block, so the grid is persistent (two blocks per SM) to keep those copies few.
+template <typename... Args>
+void launch_map(fsil_context* c, bool pdl, int64_t cap, Args... args) {
+  const bool local = cap <= kMapSmemSlots;
+  const size_t smem = local ? static_cast<size_t>(cap) * (sizeof(unsigned long long) + sizeof(int32_t)) : 0;
+  static bool attr = false;
+  if (!attr) {
+    FSIL_CUDA(cudaFuncSetAttribute(densify_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kMapSmemSlots * 12));
+    attr = true;
+  }
+  int grid = grid_for(c->n, 256, c->num_sms, 8);
+  if (local) grid = std::min(grid, 2 * c->num_sms);
+  if (pdl) {
+    launch_pdl(c, densify_map_kernel, grid, 256, smem, args...);
+  } else {
+    densify_map_kernel<<<grid, 256, smem, c->stream>>>(args...);
+    FSIL_LAUNCHED(c);
+  }
 }
 
 }  // namespace
@@ -426,9 +491,8 @@ void densify_local(fsil_context* c) {
       FSIL_LAUNCHED(c);
     }
     if (c->n > 0) {
-      launch_pdl(c, densify_map_kernel, grid_for(c->n, 256, c->num_sms, 8), 256, 0, c->labels, c->n,
-                 c->ht_keys.as<unsigned long long>(), c->ht_dense.as<int32_t>(), mask, epoch,
-                 spec ? static_cast<int32_t>(c->k_last) : INT32_MAX, c->dense.as<int32_t>(), counters + 4);
+      launch_map(c, true, cap, c->labels, c->n, c->ht_keys.as<unsigned long long>(), c->ht_dense.as<int32_t>(), mask,
+                 epoch, spec ? static_cast<int32_t>(c->k_last) : INT32_MAX, c->dense.as<int32_t>(), counters + 4);
     }
     if (spec) {
       c->k_spec = true;
@@ -474,10 +538,8 @@ void densify_assign_and_map(fsil_context* c, const int32_t* raw_in_dense_order, 
   FSIL_LAUNCHED(c);
   FSIL_CUDA(cudaMemsetAsync(c->counters.as<int>() + 4, 0, sizeof(int), c->stream));  // missing
   if (c->n > 0) {
-    densify_map_kernel<<<grid_for(c->n, 256, c->num_sms, 8), 256, 0, c->stream>>>(
-        c->labels, c->n, c->ht_keys.as<unsigned long long>(), c->ht_dense.as<int32_t>(),
-        static_cast<uint32_t>(cap - 1), epoch, k, c->dense.as<int32_t>(), c->counters.as<int>() + 4);
-    FSIL_LAUNCHED(c);
+    launch_map(c, false, cap, c->labels, c->n, c->ht_keys.as<unsigned long long>(), c->ht_dense.as<int32_t>(),
+               static_cast<uint32_t>(cap - 1), epoch, k, c->dense.as<int32_t>(), c->counters.as<int>() + 4);
   }
   // `missing` is checked by the caller at the end of the call (no extra sync here).
 }
@@ -581,10 +643,8 @@ void densify_exchange_set(fsil_context* c, const int64_t* gathered, int nranks, 
   }
   FSIL_CUDA(cudaMemsetAsync(counters + 4, 0, sizeof(int), c->stream));  // missing
   if (c->n > 0) {
-    densify_map_kernel<<<grid_for(c->n, 256, c->num_sms, 8), 256, 0, c->stream>>>(
-        c->labels, c->n, keys, slot_dense, mask, epoch, spec ? static_cast<int32_t>(c->k_global_last) : INT32_MAX,
-        c->dense.as<int32_t>(), counters + 4);
-    FSIL_LAUNCHED(c);
+    launch_map(c, false, static_cast<int64_t>(mask) + 1, c->labels, c->n, keys, slot_dense, mask, epoch,
+               spec ? static_cast<int32_t>(c->k_global_last) : INT32_MAX, c->dense.as<int32_t>(), counters + 4);
   }
   c->ht_cap = std::max<int64_t>(c->ht_cap, 8192);
   c->n_distinct = cnt;

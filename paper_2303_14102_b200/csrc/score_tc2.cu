@@ -31,6 +31,7 @@
 // acc_full.  Remote arrivals are release.cluster; the issuer's waits acquire.cluster.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "score_tc.cuh"
@@ -90,6 +91,18 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
         : "memory");
   } while (!ok);
 }
+// Optional wait profiling (FSIL_TC_PROFILE): cycles spent in a wait, added to dbg[slot]
+#define PW(slot, call)                                                                   \
+  do {                                                                                   \
+    if (dbg) {                                                                           \
+      const long long t0__ = clock64();                                                  \
+      call;                                                                              \
+      atomicAdd(dbg + (slot), static_cast<unsigned long long>(clock64() - t0__));       \
+    } else {                                                                             \
+      call;                                                                              \
+    }                                                                                    \
+  } while (0)
+
 // 2-D tensor copy of the pair (cta_group::2): lands in this CTA's shared memory, the
 // transaction bytes complete on the barrier at cluster address `bar_caddr` (the leader's)
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_caddr, int c0,
@@ -178,6 +191,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* const myscr = tp.ascratch + static_cast<size_t>(blockIdx.x) * nkc * kStgBytes;
   const TcScale sc = *tp.scale;
+  unsigned long long* const dbg = tp.dbg;
+  const long long t_begin = dbg ? clock64() : 0;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < ns; ++i) {
@@ -217,12 +232,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row0 = static_cast<int>(st * 2 * BM + rank * BM);
         for (int xp = 0; xp < ncb; ++xp) {
           if (xp == 1) {  // the first pass converted and stored this tile: reuse it
-            mbar_wait(scr_ready, ntl & 1);
+            PW(5, mbar_wait(scr_ready, ntl & 1));
             fence_proxy_async_global();
           }
           for (int kc = 0; kc < nkc; ++kc, ++n1) {
             const int s1 = static_cast<int>(n1 % ns);
-            mbar_wait_cluster(stg_empty + s1, ((n1 / ns) & 1) ^ 1);  // (multicast commit)
+            PW(4, mbar_wait_cluster(stg_empty + s1, ((n1 / ns) & 1) ^ 1));  // (multicast commit)
             if (xp > 0) {
               const uint32_t af = mapa_u32(smem_u32(a_full + s1), 0);
               if (leader) mbar_arrive_expect_tx_cluster(af, 2 * kStgBytes);
@@ -246,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kc = 0; kc < nkc; ++kc, ++n2) {
             const int sb = static_cast<int>(n2 % nb);
             uint8_t* bs = bring + sb * 2 * kBPiece;
-            mbar_wait_cluster(b_empty + sb, ((n2 / nb) & 1) ^ 1);
+            PW(6, mbar_wait_cluster(b_empty + sb, ((n2 / nb) & 1) ^ 1));
             const uint32_t bf = mapa_u32(smem_u32(b_full + sb), 0);
             if (leader) mbar_arrive_expect_tx_cluster(bf, 4 * kBPiece);
             const int col = cb * kPairN + static_cast<int>(rank) * kHalfN;
@@ -261,13 +276,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t st = cid; st < nst; st += ncl) {
         for (int cb = 0; cb < ncb; ++cb, ++na) {
           const int ab = static_cast<int>(na & 1);
-          mbar_wait_cluster(acc_empty + ab, ((na >> 1) & 1) ^ 1);
+          PW(0, mbar_wait_cluster(acc_empty + ab, ((na >> 1) & 1) ^ 1));
           tc_fence_after();
           const uint32_t d = tmem_base + ab * kPairN;
           for (int kc = 0; kc < nkc; ++kc, ++n2, ++ia) {
             const int s1 = static_cast<int>(ia % ns), sb = static_cast<int>(n2 % nb);
-            mbar_wait_cluster(a_full + s1, (ia / ns) & 1);
-            mbar_wait_cluster(b_full + sb, (n2 / nb) & 1);
+            PW(1, mbar_wait_cluster(a_full + s1, (ia / ns) & 1));
+            PW(2, mbar_wait_cluster(b_full + sb, (n2 / nb) & 1));
             tc_fence_after();
             const int rem = p.d - kc * BK;
             const int nks = rem >= BK ? 4 : (rem + 15) / 16;
@@ -285,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_commit_pair(acc_full + ab, 0x3);
         }
       }
+      if (dbg) atomicAdd(dbg + 3, static_cast<unsigned long long>(clock64() - t_begin));
     }
   } else if (warp >= kConv0) {
     setmaxnreg_dec<72>();
@@ -300,7 +316,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int own = (hq == 0 && row < p.n) ? __ldg(p.dense + row) : -1;
       double xi = 0.0;
       for (int kc = 0; kc < nkc; ++kc, ++n1) {
-        mbar_wait(stg_full + s1, (tpar >> s1) & 1u);
+        if (tl == 0) PW(9, mbar_wait(stg_full + s1, (tpar >> s1) & 1u));
+        else mbar_wait(stg_full + s1, (tpar >> s1) & 1u);
         tpar ^= 1u << s1;
         uint8_t* sbase = stg + s1 * kStgBytes;
         float4 f[8];
@@ -381,7 +398,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t row = st * 2 * BM + rank * BM + r;
       const bool valid = row < p.n;
       const double xi_g = (tp.xi_rows && valid) ? __ldg(tp.xi_rows + row) : 0.0;
-      mbar_wait(meta_full + tb, (nt >> 1) & 1);
+      if (threadIdx.x == 32 * kEpi0) PW(8, mbar_wait(meta_full + tb, (nt >> 1) & 1));
+      else mbar_wait(meta_full + tb, (nt >> 1) & 1);
       const int own = meta_own[tb * BM + r];
       const double xi64 = tp.xi_rows ? xi_g : meta_xi[(tb * 2) * BM + r] + meta_xi[(tb * 2 + 1) * BM + r];
       const float xi = static_cast<float>(xi64);
@@ -421,7 +439,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       for (int cb = 0; cb < ncb; ++cb, ++na) {
         const int ab = static_cast<int>(na & 1);
-        mbar_wait_cluster(acc_full + ab, (na >> 1) & 1);
+        if (threadIdx.x == 32 * kEpi0) PW(7, mbar_wait_cluster(acc_full + ab, (na >> 1) & 1));
+        else mbar_wait_cluster(acc_full + ab, (na >> 1) & 1);
         tc_fence_after();
         const uint32_t tb0 = tmem_base + ab * kPairN + (static_cast<uint32_t>(quad * 32) << 16);
 #pragma unroll 1
@@ -505,10 +524,14 @@ bool pair_supported(const fsil_context* c, const TcParams& tp, int bn) {
 
 void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                     TcParams tp, int64_t ntiles, bool cos, bool t3) {
-  // stages: X/A and B rings of 32 KB each; as many as fit, at least 3 + 3, at most 8 + 8
-  int ns = 3, nb = 3;
-  while (PairSmem::bytes(ns + 1, nb) <= c->smem_optin && ns < std::min(tp.nkc, 8) && ns <= nb) ++ns;
-  while (PairSmem::bytes(ns, nb + 1) <= c->smem_optin && nb < 8) ++nb;
+  // stages: X/A and B rings of 32 KB each; 3 + 3 at 227 KB.  Measured (C5, 4M rows):
+  // 3 + 3 59.1 ms, 4 + 2 62.1 ms, 3 + 2 64.5 ms -- the issuer's A waits shrink with more
+  // A stages but its B waits grow faster
+  int nb = 3, ns = 3;
+  while (PairSmem::bytes(ns, nb) > c->smem_optin && nb > 2) --nb;
+  if (const char* e = std::getenv("FSIL_TC_PAIR_NB")) nb = std::max(2, std::min(8, std::atoi(e)));  // experiments
+  if (const char* e = std::getenv("FSIL_TC_PAIR_NS")) ns = std::max(2, std::min(8, std::atoi(e)));
+  while (PairSmem::bytes(ns, nb) > c->smem_optin && ns > 2) --ns;
   tp.ncb = (c->k + kPairN - 1) / kPairN;
   const int grid = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(2 * ((ntiles + 1) / 2), c->num_sms & ~1)));
   c->a_scratch.ensure(static_cast<size_t>(grid) * tp.nkc * kStgBytes);
@@ -539,8 +562,27 @@ void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& m
   at[1].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 2;
+  static const bool prof = std::getenv("FSIL_TC_PROFILE") != nullptr;
+  unsigned long long* dbg = nullptr;
+  if (prof) {
+    FSIL_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
+    FSIL_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), c->stream));
+  }
+  tp.dbg = dbg;
   FSIL_CUDA(cudaLaunchKernelEx(&cfg, kern, mx, mh, ml, mscr, tp, ntiles, ns, nb));
   FSIL_LAUNCHED(c);
+  if (dbg) {
+    unsigned long long h[16];
+    FSIL_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    FSIL_CUDA(cudaStreamSynchronize(c->stream));
+    const char* names[10] = {"mma acc_empty", "mma a_full", "mma b_full", "mma total", "X stg_empty",
+                             "X scr_ready", "B b_empty", "epi acc_full", "epi meta_full", "conv stg_full"};
+    const double pairs = static_cast<double>(grid / 2), ctas = static_cast<double>(grid);
+    std::fprintf(stderr, "[fsil tc pair profile] ns=%d nb=%d Mcycles per CTA (MMA rows: per pair):", ns, nb);
+    for (int i = 0; i < 10; ++i) std::fprintf(stderr, " %s=%.3f", names[i], h[i] / (i < 4 ? pairs : ctas) / 1e6);
+    std::fprintf(stderr, "\n");
+    cudaFree(dbg);
+  }
 }
 
 }  // namespace tc
