@@ -915,144 +915,164 @@ __global__ void __launch_bounds__(128) label_scatter_kernel(const int32_t* __res
 // row loads of a piece overlap instead of one row load per sub-group at a time.  The
 // per-row arithmetic and the piece layout are agg_piece_kernel's.
 template <bool COS, int CPL>
-__global__ void __launch_bounds__(256) agg_piece_ring_kernel(
+__global__ void __launch_bounds__(384) agg_piece_ring_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ rows, int64_t n, int d,
     int64_t row_offset, int k, int lpr, int R, const int64_t* __restrict__ seg_begin,
     const int64_t* __restrict__ seg_end, const int64_t* __restrict__ piece_start,
     double* __restrict__ piece_out, int64_t* checks, float* xmax, double* __restrict__ xi_out) {
   extern __shared__ __align__(128) uint8_t rsh[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
   const int64_t p0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int rpw = 32 / lpr;
   const int row_bytes = d * 4;
   const int slot_bytes = rpw * row_bytes;
   uint8_t* ring = rsh + static_cast<size_t>(w) * R * slot_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rsh + static_cast<size_t>(blockDim.x >> 5) * R * slot_bytes) + w * R;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rsh + static_cast<size_t>(nw) * R * slot_bytes) + w * R;
+  // the gathered row ids of each slot (written by fill, read by the consumers: no global
+  // load on the per-row critical path)
+  int32_t* slot_rows = reinterpret_cast<int32_t*>(reinterpret_cast<uint64_t*>(rsh + static_cast<size_t>(nw) * R * slot_bytes) + nw * R) +
+                       w * R * rpw;
   const int64_t total = piece_start[k];
   if (lane == 0)
     for (int s = 0; s < R; ++s) sm100::mbar_init(bars + s, 1);
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncwarp();
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  uint32_t used = 0;  // slot uses so far (mbarrier phases continue across pieces)
+  int cs = 0;         // consumer slot
+  uint32_t cph = 0;   // its phase parity
+  int fs = 0;         // next slot to fill (ring order; runs R uses ahead of cs)
   for (int64_t p = p0; p < total; p += nwarps) {
-  int lo = 0, hi = k - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (piece_start[mid] <= p) lo = mid;
-    else hi = mid - 1;
-  }
-  const int c = lo;
-  const int64_t b0 = seg_begin[c] + (p - piece_start[c]) * kPieceRows;
-  const int64_t b1 = min(seg_end[c], b0 + kPieceRows);
-  const int iters = static_cast<int>((b1 - b0 + rpw - 1) / rpw);
-  // slot s <- the rows of iteration it (lanes 0..rpw-1 one row each; lane 0 arms the tx)
-  auto fill = [&](int it, int s) {
-    const int64_t pos = b0 + static_cast<int64_t>(it) * rpw + lane;
-    const int nrows = static_cast<int>(min(static_cast<int64_t>(rpw), b1 - (b0 + static_cast<int64_t>(it) * rpw)));
-    if (lane == 0) sm100::mbar_arrive_expect_tx(bars + s, nrows * row_bytes);
-    if (lane < nrows) {
-      const int64_t r = __ldg(rows + pos);
-      sm100::bulk_load(ring + static_cast<size_t>(s) * slot_bytes + lane * row_bytes, X + r * d, row_bytes, bars + s);
+    int lo = 0, hi = k - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (piece_start[mid] <= p) lo = mid;
+      else hi = mid - 1;
     }
-  };
-  for (int j = 0; j < R && j < iters; ++j) fill(j, static_cast<int>((used + j) % R));
-  const int sub = lane / lpr, li = lane % lpr;
-  const int nchunks = d >> 2;
-  double acc[CPL][4];
-#pragma unroll
-  for (int q = 0; q < CPL; ++q)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) acc[q][e] = 0.0;
-  double psi = 0.0, cnt = 0.0;
-  float amax = 0.f;
-  for (int it = 0; it < iters; ++it) {
-    const uint32_t u = used + it;
-    const int s = static_cast<int>(u % R);
-    sm100::mbar_wait(bars + s, (u / R) & 1);
-    const int64_t pos = b0 + static_cast<int64_t>(it) * rpw + sub;
-    const bool valid = pos < b1;
-    const int64_t r = valid ? __ldg(rows + pos) : 0;
-    const uint8_t* srow = ring + static_cast<size_t>(s) * slot_bytes + sub * row_bytes;
-    float v[CPL][4];
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) {
-      const int ch = li + q * lpr;
-      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (valid && ch < nchunks) t = *reinterpret_cast<const float4*>(srow + ch * 16);
-      v[q][0] = t.x; v[q][1] = t.y; v[q][2] = t.z; v[q][3] = t.w;
+    const int c = lo;
+    const int64_t b0 = seg_begin[c] + (p - piece_start[c]) * kPieceRows;
+    const int64_t b1 = min(seg_end[c], b0 + kPieceRows);
+    const int iters = static_cast<int>((b1 - b0 + rpw - 1) / rpw);
+    // slot s <- the rows of iteration it (lanes 0..rpw-1 one row each; lane 0 arms the tx)
+    auto fill = [&](int it, int s) {
+      const int64_t pos = b0 + static_cast<int64_t>(it) * rpw + lane;
+      const int nrows = static_cast<int>(min(static_cast<int64_t>(rpw), b1 - (b0 + static_cast<int64_t>(it) * rpw)));
+      if (lane == 0) sm100::mbar_arrive_expect_tx(bars + s, nrows * row_bytes);
+      if (lane < nrows) {
+        const int32_t r = __ldg(rows + pos);
+        slot_rows[s * rpw + lane] = r;
+        sm100::bulk_load(ring + static_cast<size_t>(s) * slot_bytes + lane * row_bytes, X + static_cast<int64_t>(r) * d,
+                         row_bytes, bars + s);
+      }
+    };
+    for (int j = 0; j < R && j < iters; ++j) {
+      fill(j, fs);
+      if (++fs == R) fs = 0;
     }
-    __syncwarp();  // every lane has read the slot: refill it
-    if (it + R < iters) fill(it + R, s);
-    double ss = 0.0;
-    bool finite = true;
+    const int sub = lane / lpr, li = lane % lpr;
+    const int nchunks = d >> 2;
+    double acc[CPL][4];
 #pragma unroll
     for (int q = 0; q < CPL; ++q)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const double x = v[q][e];
-        ss += x * x;
-        finite = finite && isfinite(v[q][e]);
-        amax = fmaxf(amax, fabsf(v[q][e]));
+      for (int e = 0; e < 4; ++e) acc[q][e] = 0.0;
+    double psi = 0.0, cnt = 0.0;
+    float amax = 0.f;
+    for (int it = 0; it < iters; ++it) {
+      const int s = cs;
+      sm100::mbar_wait(bars + s, cph);
+      if (++cs == R) {
+        cs = 0;
+        cph ^= 1u;
       }
-    if (!finite) {
+      const int64_t pos = b0 + static_cast<int64_t>(it) * rpw + sub;
+      const bool valid = pos < b1;
+      const uint8_t* srow = ring + static_cast<size_t>(s) * slot_bytes + sub * row_bytes;
+      float v[CPL][4];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const int ch = li + q * lpr;
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid && ch < nchunks) t = *reinterpret_cast<const float4*>(srow + ch * 16);
+        v[q][0] = t.x; v[q][1] = t.y; v[q][2] = t.z; v[q][3] = t.w;
+      }
+      const int64_t r = valid ? slot_rows[s * rpw + sub] : 0;
+      __syncwarp();  // every lane has read the slot: refill it
+      if (it + R < iters) {
+        fill(it + R, fs);
+        if (++fs == R) fs = 0;
+      }
+      // ||x||^2: four independent fp64 partials per lane (short dependency chains), a fixed
+      // combination order, then the fixed xor-tree across the row's lanes
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+      bool finite = true;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double x = v[q][e];
+          s4[e] = fma(x, x, s4[e]);
+          finite = finite && isfinite(v[q][e]);
+          amax = fmaxf(amax, fabsf(v[q][e]));
+        }
+      double ss = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+      if (!finite) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int l = (li + q * lpr) * 4 + e;
+            if (l < d && !isfinite(v[q][e])) atomic_min_i64(checks, (row_offset + r) * d + l);
+          }
+      }
+      double scale = 1.0;
+      if (COS) {
+        for (int off = lpr >> 1; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off, lpr);
+        if (valid && li == 0 && xi_out) xi_out[r] = ss;
+        if (!valid) continue;
+        if (ss == 0.0) {
+          if (li == 0) atomic_min_i64(checks + 1, row_offset + r);
+          continue;
+        }
+        scale = 1.0 / sqrt(ss);
+      } else {
+        if (!valid) continue;
+        psi += ss;
+      }
+      cnt += 1.0;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          acc[q][e] += COS ? static_cast<double>(v[q][e]) * scale : static_cast<double>(v[q][e]);
+    }
+    for (int off = 16; off >= lpr; off >>= 1) {
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[q][e] += __shfl_xor_sync(0xffffffffu, acc[q][e], off);
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    }
+    if (!COS)
+      for (int off = 16; off > 0; off >>= 1) psi += __shfl_xor_sync(0xffffffffu, psi, off);
+    for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+    if (lane == 0 && amax > 0.f) atomic_max_nonneg_f32(xmax, amax);
+    const int S1 = COS ? d + 1 : d + 2;
+    double* out = piece_out + p * S1;
+    if (lane == 0) {
+      out[0] = cnt;
+      if (!COS) out[1] = psi;
+    }
+    if (sub == 0) {
+      double* sums = out + (COS ? 1 : 2);
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int l = (li + q * lpr) * 4 + e;
-          if (l < d && !isfinite(v[q][e])) atomic_min_i64(checks, (row_offset + r) * d + l);
+          if (l < d) sums[l] = acc[q][e];
         }
     }
-    double scale = 1.0;
-    if (COS) {
-      for (int off = lpr >> 1; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off, lpr);
-      if (valid && li == 0 && xi_out) xi_out[r] = ss;
-      if (!valid) continue;
-      if (ss == 0.0) {
-        if (li == 0) atomic_min_i64(checks + 1, row_offset + r);
-        continue;
-      }
-      scale = 1.0 / sqrt(ss);
-    } else {
-      if (!valid) continue;
-      psi += ss;
-    }
-    cnt += 1.0;
-#pragma unroll
-    for (int q = 0; q < CPL; ++q)
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        acc[q][e] += COS ? static_cast<double>(v[q][e]) * scale : static_cast<double>(v[q][e]);
-  }
-  for (int off = 16; off >= lpr; off >>= 1) {
-#pragma unroll
-    for (int q = 0; q < CPL; ++q)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[q][e] += __shfl_xor_sync(0xffffffffu, acc[q][e], off);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
-  }
-  if (!COS)
-    for (int off = 16; off > 0; off >>= 1) psi += __shfl_xor_sync(0xffffffffu, psi, off);
-  for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
-  if (lane == 0 && amax > 0.f) atomic_max_nonneg_f32(xmax, amax);
-  const int S1 = COS ? d + 1 : d + 2;
-  double* out = piece_out + p * S1;
-  if (lane == 0) {
-    out[0] = cnt;
-    if (!COS) out[1] = psi;
-  }
-  if (sub == 0) {
-    double* sums = out + (COS ? 1 : 2);
-#pragma unroll
-    for (int q = 0; q < CPL; ++q)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int l = (li + q * lpr) * 4 + e;
-        if (l < d) sums[l] = acc[q][e];
-      }
-  }
-  used += static_cast<uint32_t>(iters);
   }
 }
 
@@ -1429,20 +1449,20 @@ void aggregate(fsil_context* c) {
   if (x64) {
     if (cos) launch_pieces<true>(c, c->X64, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);
     else launch_pieces<false>(c, c->X64, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);
-  } else if (vec == 4 && cpl_t <= 8 && c->d >= 256 && ring_env) {
-    // wide rows (>= 1 KB): bulk-copy ring, R slots per warp (~24 KB of rows in flight per
-    // warp), persistent warps striding over the pieces.  Narrow rows keep the register
-    // ring of agg_piece_kernel (one bulk copy per small row costs more than it hides).
+  } else if (vec == 4 && cpl <= 8 && c->d >= 256 && ring_env) {
+    // wide rows (>= 1 KB): bulk-copy ring, R slots per warp, 12 persistent warps per SM
+    // striding over the pieces (one CTA per SM: ~216 KB of rows in flight).  Narrow rows
+    // keep agg_piece_kernel (one bulk copy per small row costs more than it hides).
     const int rpw = 32 / lpr;
     const int slot = rpw * c->d * 4;
-    const int R = static_cast<int>(std::max(2, std::min(16, 24576 / slot)));
-    const int W = 8;
-    const size_t rsm = static_cast<size_t>(W) * R * slot + static_cast<size_t>(W) * R * 8;
-    const int per_sm = std::max(1, static_cast<int>(std::min<size_t>(2, budget / rsm)));
+    const int W = 12;
+    const size_t avail = std::min<size_t>(budget, 220 * 1024);
+    const int R = static_cast<int>(std::max<size_t>(2, std::min<size_t>(16, avail / (static_cast<size_t>(W) * (slot + 8 + 4 * rpw)))));
+    const size_t rsm = static_cast<size_t>(W) * R * (slot + 8 + 4 * rpw);
     const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
-        1, std::min<int64_t>((max_pieces + W - 1) / W, static_cast<int64_t>(c->num_sms) * per_sm)));
+        1, std::min<int64_t>((max_pieces + W - 1) / W, static_cast<int64_t>(c->num_sms))));
 #define FSIL_AGG_RING(C)                                                                                   \
-  if (cpl_t == C) {                                                                                        \
+  if (cpl == C) {                                                                                          \
     auto kern = cos ? agg_piece_ring_kernel<true, C> : agg_piece_ring_kernel<false, C>;                    \
     FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rsm))); \
     kern<<<grid, 32 * W, rsm, c->stream>>>(c->X, srows, c->n, c->d, c->row_offset, c->k, lpr, R, seg_begin,  \
@@ -1450,7 +1470,8 @@ void aggregate(fsil_context* c) {
                                            c->xi_valid ? c->xi_rows.as<double>() : nullptr);                  \
     FSIL_LAUNCHED(c);                                                                                      \
   }
-    FSIL_AGG_RING(1) else FSIL_AGG_RING(2) else FSIL_AGG_RING(4) else FSIL_AGG_RING(8)
+    FSIL_AGG_RING(2) else FSIL_AGG_RING(3) else FSIL_AGG_RING(4) else FSIL_AGG_RING(5) else FSIL_AGG_RING(6)
+    else FSIL_AGG_RING(7) else FSIL_AGG_RING(8)
 #undef FSIL_AGG_RING
   } else {
     if (cos) launch_pieces<true>(c, c->X, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);
