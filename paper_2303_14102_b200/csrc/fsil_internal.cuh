@@ -184,6 +184,7 @@ struct fsil_context {
   cudaEvent_t ev[8] = {};
   bool ev7_recorded = false;  // ev[7] marks the scoring kernel's own launch (timing runs)
   bool pdl = true;             // programmatic dependent launch on the hot chain (FSIL_PDL=0: off)
+  bool fused_exact = false;    // this call's scoring kernel computed the certain rows' exact a, b, s
 };
 
 namespace fsil {

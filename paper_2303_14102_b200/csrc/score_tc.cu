@@ -1012,6 +1012,7 @@ int64_t tc_tiles(const fsil_context* c, int* tile_rows) {
 }
 
 void score_tc(fsil_context* c, const ScoreParams& p) {
+  c->fused_exact = false;  // set by the pair kernel's launcher when it computes the exact rows
   const bool cos = c->metric == FSIL_COSINE;
   const int bn = pick_bn(c->k);
   int ncb = (c->k + bn - 1) / bn;

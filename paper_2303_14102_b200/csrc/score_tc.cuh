@@ -52,6 +52,7 @@ struct TcParams {
   int lean;               // converters only convert; the epilogue fetches own/||x||^2 itself
   int2* pair_rows;        // T3: rows whose neighbour is one of {nb, .y} (certified pair)
   unsigned long long* pair_count;
+  int fexact;             // pair kernel: certain rows get their exact a, b, s in the kernel
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -68,7 +69,7 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 // neighbour; uncertain rows go to the fp64 refinement (flag_rows) or, T3, to the
 // certified-pair list when every other column is clearly behind.
 template <bool COS, bool T3>
-__device__ __forceinline__ void certify_row(const TcParams& tp, const TcScale& sc, int64_t row, int own,
+__device__ __forceinline__ bool certify_row(const TcParams& tp, const TcScale& sc, int64_t row, int own,
                                             float xi, float xn, float rnf, float b1, float b2, float b3,
                                             int arg, int arg2, float mu_arg_ratio) {
   const float u = 5.9604645e-8f;
@@ -103,6 +104,7 @@ __device__ __forceinline__ void certify_row(const TcParams& tp, const TcScale& s
     const unsigned long long idx = atomicAdd(tp.p.flag_count, 1ull);
     tp.p.flag_rows[idx] = static_cast<int32_t>(row);
   }
+  return !full;  // the nominated neighbour is certain
 }
 
 // Tensor maps (cuTensorMapEncodeTiled through the runtime's driver entry point).

@@ -149,7 +149,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 struct PairSmem {
   static size_t bytes(int ns, int nb) {
     return 1024 + static_cast<size_t>(ns) * kStgBytes + static_cast<size_t>(nb) * 2 * kBPiece + 64 * 8 +
-           4 * BM * 8 + 10 * BM * 4 + 2 * BM * 4 + 64;
+           4 * BM * 8 + 10 * BM * 4 + 2 * BM * 4 + 2 * BM * 4 + 64;
   }
 };
 
@@ -187,6 +187,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   double* meta_xi = reinterpret_cast<double*>(bars + 64);    // [2][2][BM]
   float* part = reinterpret_cast<float*>(meta_xi + 4 * BM);  // [2][5][BM]
   int* meta_own = reinterpret_cast<int*>(part + 10 * BM);     // [2][BM]
+  int* exl = meta_own + 2 * BM;                                // [2][BM] fused exact: certain nb, or -1
+  uint64_t* exact_full = bars + 50;  // [2] local: a tile's certified neighbours (epilogue group 0)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* const myscr = tp.ascratch + static_cast<size_t>(blockIdx.x) * nkc * kStgBytes;
@@ -211,6 +213,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(meta_empty + i, 4);
     }
     mbar_init(scr_ready, 1);
+    mbar_init(exact_full + 0, 4);
+    mbar_init(exact_full + 1, 4);
     fence_barrier_init();
     prefetch_tmap(&tmap_x);
     prefetch_tmap(&tmap_bh);
@@ -311,6 +315,59 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float2 sx2 = make_float2(sc.sx, sc.sx), neg1 = make_float2(-1.f, -1.f);
     uint32_t n1 = 0, nt = 0, tpar = 0;  // tpar bit s: parity of stage s's next X landing
     int s1 = 0;
+    // Fused exact pass: while the MMAs stream a tile's cluster blocks, the converters (idle
+    // after the tile's first pass) give the previous tile's certain rows their fp64 a_i,
+    // b_i, s_i -- the reference formulas (score_common.cuh) on the row re-read from
+    // global memory, one row per warp, lanes over D in a fixed order.  Flagged and pair
+    // rows are left to the post-scoring passes.
+    const int cw = (threadIdx.x >> 5) - kConv0;  // converter warp 0..7
+    auto exact_tile = [&](uint32_t t_idx, int64_t st_t) {
+      const int tbx = t_idx & 1;
+      mbar_wait(exact_full + tbx, (t_idx >> 1) & 1);
+      const double* sums = p.stats + (COS ? p.k : 2 * p.k);
+      const int d = p.d;
+      for (int rr = cw; rr < BM; rr += 8) {
+        const int nbr = exl[tbx * BM + rr];
+        if (nbr < 0) continue;  // warp-uniform
+        const int ownr = meta_own[tbx * BM + rr];
+        const int64_t row = st_t * 2 * BM + rank * BM + rr;
+        const float* xr = p.X + row * d;
+        const double* yo = sums + static_cast<int64_t>(ownr) * d;
+        const double* yb = sums + static_cast<int64_t>(nbr) * d;
+        double ss = 0.0, co = 0.0, cb = 0.0;
+#pragma unroll 4
+        for (int l = lane; l < d; l += 32) {
+          const double x = static_cast<double>(__ldg(xr + l));
+          ss = fma(x, x, ss);
+          co = fma(__ldg(yo + l), x, co);
+          cb = fma(__ldg(yb + l), x, cb);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          ss += __shfl_xor_sync(0xffffffffu, ss, off);
+          co += __shfl_xor_sync(0xffffffffu, co, off);
+          cb += __shfl_xor_sync(0xffffffffu, cb, off);
+        }
+        if (lane == 0) {
+          const double n_o = p.nk[ownr], n_b = p.nk[nbr];
+          const bool singleton = n_o == 1.0;
+          double a, b;
+          if (COS) {
+            const double nrm = sqrt(ss);
+            b = cos_foreign(n_b, cb / nrm);
+            a = singleton ? 0.0 : cos_own(n_o, co / nrm);
+          } else {
+            b = sq_foreign(ss, p.stats[p.k + nbr], n_b, cb);
+            a = singleton ? 0.0 : sq_own(ss, p.stats[p.k + ownr], n_o, co);
+          }
+          p.s[row] = singleton ? 0.0 : assemble_score(a, b);
+          if (p.a) p.a[row] = a;
+          if (p.b) p.b[row] = b;
+          if (p.own) p.own[row] = ownr;
+        }
+      }
+    };
+    int64_t st_prev = -1;
     for (int64_t st = cid; st < nst; st += ncl, ++nt) {
       const int64_t row = st * 2 * BM + rank * BM + r;
       const int own = (hq == 0 && row < p.n) ? __ldg(p.dense + row) : -1;
@@ -384,7 +441,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (hq == 0) meta_own[tb * BM + r] = own;
       __syncwarp();
       if (lane == 0) mbar_arrive(meta_full + tb);
+      if (tp.fexact && nt > 0) exact_tile(nt - 1, st_prev);
+      st_prev = st;
     }
+    if (tp.fexact && nt > 0) exact_tile(nt - 1, st_prev);
   } else {
     // ------------------------------------------------------------ epilogue (8 warps)
     setmaxnreg_inc<136>();
@@ -497,9 +557,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       // group 0 has read the partials and the meta slot: both may be reused
       __syncwarp();
       if (lane == 0) mbar_arrive(meta_empty + tb);
+      bool certain = false;
       if (valid)
-        certify_row<COS, T3>(tp, sc, row, own, xi, xn, rnf, b1, b2, b3, arg, arg2,
-                             arg >= 0 ? __half2float(__ldg(tp.munorm + arg)) : 1.0f);
+        certain = certify_row<COS, T3>(tp, sc, row, own, xi, xn, rnf, b1, b2, b3, arg, arg2,
+                                       arg >= 0 ? __half2float(__ldg(tp.munorm + arg)) : 1.0f);
+      if (tp.fexact) {  // the converters compute the certain rows' exact a, b, s
+        exl[tb * BM + r] = certain ? arg : -1;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(exact_full + tb);
+      }
     }
   }
 
@@ -533,6 +599,15 @@ void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& m
   if (const char* e = std::getenv("FSIL_TC_PAIR_NS")) ns = std::max(2, std::min(8, std::atoi(e)));
   while (PairSmem::bytes(ns, nb) > c->smem_optin && ns > 2) --ns;
   tp.ncb = (c->k + kPairN - 1) / kPairN;
+  // Fused exact pass (FSIL_TC_FEXACT=1): measured at C5, the post-scoring phase drops
+  // 45 -> 11 ms but the scoring kernel grows 636 -> 685 ms -- the converters' fp64 table
+  // reads (12 KB per row) compete with the A/B operand traffic in L2 -- so it is off.
+  static const bool fexact_env = [] {
+    const char* e = std::getenv("FSIL_TC_FEXACT");
+    return e && std::atoi(e) != 0;
+  }();
+  tp.fexact = fexact_env && !c->X64 ? 1 : 0;
+  c->fused_exact = tp.fexact != 0;
   const int grid = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(2 * ((ntiles + 1) / 2), c->num_sms & ~1)));
   c->a_scratch.ensure(static_cast<size_t>(grid) * tp.nkc * kStgBytes);
   tp.ascratch = c->a_scratch.as<uint8_t>();
