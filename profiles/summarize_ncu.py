@@ -49,16 +49,22 @@ SETUP_KERNELS = ("centres_kernel", "uniform_labels_kernel", "points_kernel", "ne
                  "zipf_labels_kernel", "dirichlet_labels_kernel", "shuffle_kernel", "labels_kernel")
 
 
-def raw(rep):
+def raw(rep, row=0):
     out = subprocess.run([NCU, "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
                          check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    head, units, vals = rows[0], rows[1], rows[2]
+    head, units, vals = rows[0], rows[1], rows[2 + row]
     return head, units, vals
 
 
-def summarise(rep):
-    head, units, vals = raw(rep)
+def n_kernels(rep):
+    out = subprocess.run([NCU, "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                         check=True).stdout
+    return len(list(csv.reader(io.StringIO(out)))) - 2
+
+
+def summarise(rep, row=0):
+    head, units, vals = raw(rep, row)
     col = {h: i for i, h in enumerate(head)}
     res = {"report": os.path.basename(rep), "kernel": vals[col["Kernel Name"]]}
     for key, m in METRICS.items():
