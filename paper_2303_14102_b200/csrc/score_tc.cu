@@ -849,7 +849,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // largest element are still covered).  Uncertain rows go to the fp64 refinement.
       if (valid)
         certify_row<COS, T3>(tp, sc, row, own, xi, xn, rnf, b1, b2, b3, arg, arg2,
-                             arg >= 0 ? __half2float(mn_s[arg]) : 1.0f);
+                             arg >= 0 ? __half2float(mn_s[arg]) : 1.0f,
+                             (T3 && arg2 >= 0) ? __half2float(mn_s[arg2]) : 1.0f);
       if (dbgp && warp == kEpiWarp0 && lane == 0) atomicAdd(dbgp + 13, static_cast<unsigned long long>(clock64() - tf0));
       if (quad == 0 && lane == 0) TRACE(nt, 7);
     }

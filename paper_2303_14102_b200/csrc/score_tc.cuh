@@ -53,6 +53,7 @@ struct TcParams {
   int2* pair_rows;        // T3: rows whose neighbour is one of {nb, .y} (certified pair)
   unsigned long long* pair_count;
   int fexact;             // pair kernel: certain rows get their exact a, b, s in the kernel
+  int pf;                 // pair kernel: converters prepare each tile's A scratch a tile ahead
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -71,7 +72,7 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 template <bool COS, bool T3>
 __device__ __forceinline__ bool certify_row(const TcParams& tp, const TcScale& sc, int64_t row, int own,
                                             float xi, float xn, float rnf, float b1, float b2, float b3,
-                                            int arg, int arg2, float mu_arg_ratio) {
+                                            int arg, int arg2, float mu_arg_ratio, float mu_arg2_ratio = 1.0f) {
   const float u = 5.9604645e-8f;
   const float rowc = COS ? 1.0f : xi;
   const float exi = tp.exic * u * xi;  // ||x||^2 error (fp32 blocks of 8; fp64 input rounding)
@@ -89,9 +90,17 @@ __device__ __forceinline__ bool certify_row(const TcParams& tp, const TcScale& s
   const float eps_dot1_arg = cmu * mu_arg + sc.floor_mu;
   const float eps_m_arg = COS ? (eps_dot1_arg + 4.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u)
                               : (2.0f * eps_dot1_arg * xn + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
-  // neighbour certain: clear gap, and no tie through the clamps at 0 (and 2)
-  const bool full = !((b2 - b1) > eps_m + eps_m_arg) || arg < 0 || !(rowc + b2 > eps_m) ||
-                    (COS && !(rowc + b1 < 2.0f - eps_m));
+  // neighbour certain: clear gap, and no tie through the clamps at 0 (and 2).  With the
+  // top-3 (T3) the runner-up's own norm bounds its key and every other column is at or
+  // behind b3 with the any-column bound: certain when min(b2 - e2, b3 - e_any) > b1 + e_arg.
+  bool gap_ok = (b2 - b1) > eps_m + eps_m_arg && rowc + b2 > eps_m;
+  if (T3 && arg2 >= 0) {
+    const float eps_dot1_2 = cmu * (mu_arg2_ratio * sc.mu_max) + sc.floor_mu;
+    const float eps_m_2 = COS ? (eps_dot1_2 + 4.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u)
+                              : (2.0f * eps_dot1_2 * xn + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
+    gap_ok = gap_ok || (fminf(b2 - eps_m_2, b3 - eps_m) > b1 + eps_m_arg && rowc + b2 > eps_m_2 && rowc + b3 > eps_m);
+  }
+  const bool full = !gap_ok || arg < 0 || (COS && !(rowc + b1 < 2.0f - eps_m));
   tp.p.nb[row] = arg >= 0 ? arg : (own == 0 ? 1 : 0);  // the refinement rewrites flagged rows
   // T3: the neighbour is one of the top two when every other column is clearly
   // behind the winner (third-best gap, no clamp tie) -- two fp64 means decide it

@@ -113,6 +113,43 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_caddr)
       : "memory");
 }
+// L2 eviction-priority policies for the tensor copies: the X stream is read once
+// (evict_first), the converted-A scratch and the B pieces are re-read every cluster block
+// (evict_last), so X does not push them out of L2.
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair_hint(void* dst, const CUtensorMap* map, uint32_t bar_caddr, int c0,
+                                                      int c1, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_caddr), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store_hint(void* dst, const void* src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::"l"(
+                   reinterpret_cast<uint64_t>(dst)),
+               "r"(smem_u32(src)), "r"(bytes), "l"(pol)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+
 template <uint32_t NCOLS>
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* smem_dst) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(smem_dst)),
@@ -189,9 +226,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   int* meta_own = reinterpret_cast<int*>(part + 10 * BM);     // [2][BM]
   int* exl = meta_own + 2 * BM;                                // [2][BM] fused exact: certain nb, or -1
   uint64_t* exact_full = bars + 50;  // [2] local: a tile's certified neighbours (epilogue group 0)
+  uint64_t* scr_ready2 = bars + 52;  // [2] prefetch mode: scratch buffer b holds its tile's chunks
+  uint64_t* scr_free = bars + 54;    // [2] prefetch mode: every reload of buffer b's tile consumed
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* const myscr = tp.ascratch + static_cast<size_t>(blockIdx.x) * nkc * kStgBytes;
+  // scratch: [CTA][buffer (prefetch mode: tile parity)][nkc][kStgBytes]
+  const int nbuf = tp.pf ? 2 : 1;
+  uint8_t* const myscr = tp.ascratch + static_cast<size_t>(blockIdx.x) * nbuf * nkc * kStgBytes;
   const TcScale sc = *tp.scale;
   unsigned long long* const dbg = tp.dbg;
   const long long t_begin = dbg ? clock64() : 0;
@@ -215,6 +256,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(scr_ready, 1);
     mbar_init(exact_full + 0, 4);
     mbar_init(exact_full + 1, 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(scr_ready2 + i, 1);
+      mbar_init(scr_free + i, 1);
+    }
     fence_barrier_init();
     prefetch_tmap(&tmap_x);
     prefetch_tmap(&tmap_bh);
@@ -232,34 +277,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
       // ------------------------------------------------------------ X producer
       uint32_t n1 = 0, ntl = 0;
+      const uint64_t pol_x = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
       for (int64_t st = cid; st < nst; st += ncl, ++ntl) {
         const int row0 = static_cast<int>(st * 2 * BM + rank * BM);
+        const int64_t sbase = (static_cast<int64_t>(blockIdx.x) * nbuf + (tp.pf ? (ntl & 1) : 0)) * nkc;
+        if (tp.pf) {  // the converters prepared this tile's chunks: every pass reloads them
+          PW(5, mbar_wait(scr_ready2 + (ntl & 1), (ntl >> 1) & 1));
+          fence_proxy_async_global();
+        }
         for (int xp = 0; xp < ncb; ++xp) {
-          if (xp == 1) {  // the first pass converted and stored this tile: reuse it
+          if (xp == 1 && !tp.pf) {  // the first pass converted and stored this tile: reuse it
             PW(5, mbar_wait(scr_ready, ntl & 1));
             fence_proxy_async_global();
           }
           for (int kc = 0; kc < nkc; ++kc, ++n1) {
             const int s1 = static_cast<int>(n1 % ns);
             PW(4, mbar_wait_cluster(stg_empty + s1, ((n1 / ns) & 1) ^ 1));  // (multicast commit)
-            if (xp > 0) {
+            if (xp > 0 || tp.pf) {
               const uint32_t af = mapa_u32(smem_u32(a_full + s1), 0);
               if (leader) mbar_arrive_expect_tx_cluster(af, 2 * kStgBytes);
-              tma_load_2d_pair(stg + s1 * kStgBytes, &tmap_scr, af, 0,
-                               static_cast<int>((static_cast<int64_t>(blockIdx.x) * nkc + kc) * BM));
+              tma_load_2d_pair_hint(stg + s1 * kStgBytes, &tmap_scr, af, 0, static_cast<int>((sbase + kc) * BM),
+                                    pol_keep);
               if (!leader) mbar_arrive_cluster(af);
               continue;
             }
             const int nbox = (kc * BK + 32 < p.d) ? 2 : 1;
             mbar_arrive_expect_tx(stg_full + s1, nbox * BM * 128);
             for (int b = 0; b < nbox; ++b)
-              tma_load_2d(stg + s1 * kStgBytes + b * BM * 128, &tmap_x, stg_full + s1, kc * BK + b * 32, row0);
+              tma_load_2d_hint(stg + s1 * kStgBytes + b * BM * 128, &tmap_x, stg_full + s1, kc * BK + b * 32, row0,
+                               pol_x);
           }
         }
       }
     } else if (warp == 2 && lane == 0) {
       // ------------------------------------------------------------ B producer
       uint32_t n2 = 0;
+      const uint64_t pol_b = l2_policy_evict_last();
       for (int64_t st = cid; st < nst; st += ncl) {
         for (int cb = 0; cb < ncb; ++cb) {
           for (int kc = 0; kc < nkc; ++kc, ++n2) {
@@ -269,15 +322,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t bf = mapa_u32(smem_u32(b_full + sb), 0);
             if (leader) mbar_arrive_expect_tx_cluster(bf, 4 * kBPiece);
             const int col = cb * kPairN + static_cast<int>(rank) * kHalfN;
-            tma_load_2d_pair(bs, &tmap_bh, bf, kc * BK, col);
-            tma_load_2d_pair(bs + kBPiece, &tmap_bl, bf, kc * BK, col);
+            tma_load_2d_pair_hint(bs, &tmap_bh, bf, kc * BK, col, pol_b);
+            tma_load_2d_pair_hint(bs + kBPiece, &tmap_bl, bf, kc * BK, col, pol_b);
           }
         }
       }
     } else if (warp == 1 && lane == 0 && leader) {
       // ------------------------------------------------------------ MMA issuer (the pair's)
-      uint32_t n2 = 0, ia = 0, na = 0;
-      for (int64_t st = cid; st < nst; st += ncl) {
+      uint32_t n2 = 0, ia = 0, na = 0, ntm = 0;
+      for (int64_t st = cid; st < nst; st += ncl, ++ntm) {
         for (int cb = 0; cb < ncb; ++cb, ++na) {
           const int ab = static_cast<int>(na & 1);
           PW(0, mbar_wait_cluster(acc_empty + ab, ((na >> 1) & 1) ^ 1));
@@ -303,6 +356,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           mma_commit_pair(acc_full + ab, 0x3);
         }
+        // prefetch mode: this tile's scratch buffer has been read by every reload
+        if (tp.pf) mma_commit_pair(scr_free + (ntm & 1), 0x3);
       }
       if (dbg) atomicAdd(dbg + 3, static_cast<unsigned long long>(clock64() - t_begin));
     }
@@ -368,6 +423,73 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     int64_t st_prev = -1;
+    if (tp.pf) {
+      // Prefetch mode: the converters read each tile's rows straight from global memory
+      // (two threads per row, 128 B each per chunk), split them and store the fp16 pieces
+      // in the UMMA K-major SWIZZLE_128B byte image to the tile's scratch buffer (tile
+      // parity), a tile ahead of the MMAs: no HBM latency or conversion on the tensor
+      // pipe's critical path.  A buffer is rewritten only after the MMA issuer's commit
+      // says every reload of its previous tile was consumed.
+      const float* Xg = p.X;
+      const int d = p.d;
+      for (int64_t st = cid; st < nst; st += ncl, ++nt) {
+        const int64_t row = st * 2 * BM + rank * BM + r;
+        const bool rv = row < p.n;
+        const int own = (hq == 0 && rv) ? __ldg(p.dense + row) : -1;
+        const int b = nt & 1;
+        if (nt >= 2) mbar_wait_cluster(scr_free + b, ((nt >> 1) - 1) & 1);
+        uint8_t* sb = myscr + static_cast<size_t>(b) * nkc * kStgBytes;
+        double xi = 0.0;
+        for (int kc = 0; kc < nkc; ++kc) {
+          const int c0 = kc * BK + hq * 32;
+          float4 f[8];
+          const float* xr = Xg + (rv ? row : 0) * d + c0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            f[u] = (rv && c0 + 4 * u < d) ? __ldg(reinterpret_cast<const float4*>(xr) + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+          uint8_t* hrow = sb + static_cast<size_t>(kc) * kStgBytes + r * 128;
+          uint8_t* lrow = hrow + BM * 128;
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int j = 4 * hq + jj;
+            const float v[8] = {f[2 * jj].x,     f[2 * jj].y,     f[2 * jj].z,     f[2 * jj].w,
+                                f[2 * jj + 1].x, f[2 * jj + 1].y, f[2 * jj + 1].z, f[2 * jj + 1].w};
+            if (!tp.xi_rows) {  // ||x||^2: fp32 blocks of 8 (error <= 8u each), fp64 across blocks
+              float2 bs = make_float2(0.f, 0.f);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 ve = make_float2(v[2 * e], v[2 * e + 1]);
+                bs = __ffma2_rn(ve, ve, bs);
+              }
+              xi += static_cast<double>(bs.x + bs.y);
+            }
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 xx = __fmul2_rn(make_float2(v[2 * e], v[2 * e + 1]), sx2);
+              const __half2 h = __float22half2_rn(xx);
+              const float2 res = __ffma2_rn(__half22float2(h), neg1, xx);
+              const __half2 l = __float22half2_rn(res);
+              hw[e] = *reinterpret_cast<const uint32_t*>(&h);
+              lw[e] = *reinterpret_cast<const uint32_t*>(&l);
+            }
+            const int pos = (j ^ sw) << 4;
+            *reinterpret_cast<uint4*>(hrow + pos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(lrow + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          }
+        }
+        // generic-proxy stores -> the producer's tensor copies (async proxy)
+        fence_proxy_async_global();
+        named_bar_sync(5, 256);
+        if (tl == 0) mbar_arrive(scr_ready2 + b);
+        const int tb = nt & 1;
+        mbar_wait(meta_empty + tb, ((nt >> 1) & 1) ^ 1);
+        meta_xi[(tb * 2 + hq) * BM + r] = xi;
+        if (hq == 0) meta_own[tb * BM + r] = own;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(meta_full + tb);
+      }
+    } else {
     for (int64_t st = cid; st < nst; st += ncl, ++nt) {
       const int64_t row = st * 2 * BM + rank * BM + r;
       const int own = (hq == 0 && row < p.n) ? __ldg(p.dense + row) : -1;
@@ -421,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tl == 0) {
           // the converted chunk -> scratch (read before the MMA may free the stage), then
           // this CTA's single arrival on the leader's a_full
-          bulk_store(myscr + static_cast<size_t>(kc) * kStgBytes, sbase, kStgBytes);
+          bulk_store_hint(myscr + static_cast<size_t>(kc) * kStgBytes, sbase, kStgBytes, l2_policy_evict_last());
           bulk_wait_read();
           mbar_arrive_cluster(mapa_u32(smem_u32(a_full + s1), 0));
         }
@@ -445,6 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       st_prev = st;
     }
     if (tp.fexact && nt > 0) exact_tile(nt - 1, st_prev);
+    }
   } else {
     // ------------------------------------------------------------ epilogue (8 warps)
     setmaxnreg_inc<136>();
@@ -560,7 +683,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       bool certain = false;
       if (valid)
         certain = certify_row<COS, T3>(tp, sc, row, own, xi, xn, rnf, b1, b2, b3, arg, arg2,
-                                       arg >= 0 ? __half2float(__ldg(tp.munorm + arg)) : 1.0f);
+                                       arg >= 0 ? __half2float(__ldg(tp.munorm + arg)) : 1.0f,
+                                       arg2 >= 0 ? __half2float(__ldg(tp.munorm + arg2)) : 1.0f);
       if (tp.fexact) {  // the converters compute the certain rows' exact a, b, s
         exl[tb * BM + r] = certain ? arg : -1;
         __syncwarp();
@@ -606,14 +730,24 @@ void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& m
     const char* e = std::getenv("FSIL_TC_FEXACT");
     return e && std::atoi(e) != 0;
   }();
-  tp.fexact = fexact_env && !c->X64 ? 1 : 0;
+  // Prefetch mode (FSIL_TC_PAIR_PF=1): the converters prepare each tile's scratch a tile
+  // ahead from global memory, so every pass is a reload.  Measured at C5: 636 -> 686 ms --
+  // the issuer's waits are on the reloads themselves (L2), and the double scratch (114 MB)
+  // evicts more of them -- so it is off.
+  static const bool pf_env = [] {
+    const char* e = std::getenv("FSIL_TC_PAIR_PF");
+    return e && std::atoi(e) != 0;
+  }();
+  tp.pf = pf_env ? 1 : 0;
+  tp.fexact = fexact_env && !c->X64 && !tp.pf ? 1 : 0;  // (the fused exact pass rides on pass 0)
   c->fused_exact = tp.fexact != 0;
   const int grid = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(2 * ((ntiles + 1) / 2), c->num_sms & ~1)));
-  c->a_scratch.ensure(static_cast<size_t>(grid) * tp.nkc * kStgBytes);
+  const int nbuf = tp.pf ? 2 : 1;  // prefetch mode: one buffer per tile parity
+  c->a_scratch.ensure(static_cast<size_t>(grid) * nbuf * tp.nkc * kStgBytes);
   tp.ascratch = c->a_scratch.as<uint8_t>();
   // the scratch as a 2-D tensor of 256-byte rows: one 32 KB box = one converted chunk
   const CUtensorMap mscr = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_UINT16, tp.ascratch, 128,
-                                       static_cast<uint64_t>(grid) * tp.nkc * BM, 256, 128, BM,
+                                       static_cast<uint64_t>(grid) * nbuf * tp.nkc * BM, 256, 128, BM,
                                        CU_TENSOR_MAP_SWIZZLE_NONE);
   const size_t smem = PairSmem::bytes(ns, nb);
   auto kern = cos ? (t3 ? score_tc_pair_kernel<true, true> : score_tc_pair_kernel<true, false>)
