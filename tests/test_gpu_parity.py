@@ -219,6 +219,19 @@ def test_tc_streaming_stage_counts(ctx, monkeypatch, nstg, n, d, k, metric):
     assert ctx.stats()["flagged_rows"] < n // 2
 
 
+@pytest.mark.parametrize("n,d,k,metric", [(30000, 200, 600, "cosine"), (30000, 136, 513, "sqeuclid"),
+                                          (20000, 768, 1000, "sqeuclid"), (9000, 320, 2100, "cosine"),
+                                          (3000, 192, 257, "cosine")])
+def test_tc_pair_kernel_shapes(ctx, n, d, k, metric):
+    """The CTA-pair kernel (score_tc2.cu) on streaming tables: a partial last K chunk
+    (D = 200, 136: the second fp32 box absent, the MMA's K steps stop early), K not a
+    multiple of the 256-column block (padding columns at +inf), an odd number of 128-row
+    tiles (the peer CTA of the last pair idle), several super-tiles per pair."""
+    X, L = _blobs(n, d, k, seed=n + d + k)
+    check(ctx, X, L, metric, "tcgen05", label="pair")
+    assert ctx.stats()["flagged_rows"] < n // 2
+
+
 def test_tc_cosine_mixed_norms_unit_scale(ctx):
     """Cosine is invariant to per-point scaling, so rows scaled by 1e-3..1e-5 are valid
     input.  On the three-group kernel (BN = 32, batched aggregation) the x operand is not
