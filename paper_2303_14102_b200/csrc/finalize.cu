@@ -709,69 +709,6 @@ __global__ void __launch_bounds__(kExactThreads) exact_kernel(ScoreParams p, Exa
   if (last) unit_total(ea, p.n);
 }
 
-// Fused exact pass (the CTA-pair scoring kernel gave every certain row its exact a, b, s):
-// the refined and certified-pair rows get theirs here, one warp per listed row, lanes
-// over D in the same order as the kernel's.
-template <bool COS>
-__global__ void __launch_bounds__(256) exact_list_kernel(ScoreParams p, const int2* __restrict__ pairs,
-                                                         const unsigned long long* pair_count) {
-  griddep_wait();
-  if (*p.abort) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t fc = static_cast<int64_t>(*p.flag_count);
-  const int64_t total = fc + (pair_count ? static_cast<int64_t>(*pair_count) : 0);
-  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const double* sums = p.stats + (COS ? p.k : 2 * p.k);
-  const int d = p.d;
-  for (int64_t i = w0; i < total; i += nw) {
-    const int64_t row = i < fc ? static_cast<int64_t>(p.flag_rows[i]) : static_cast<int64_t>(pairs[i - fc].x);
-    const int own = __ldg(p.dense + row), nb = p.nb[row];
-    const double* yo = sums + static_cast<int64_t>(own) * d;
-    const double* yb = sums + static_cast<int64_t>(nb) * d;
-    double ss = 0.0, co = 0.0, cb = 0.0;
-    for (int l = lane; l < d; l += 32) {
-      const double x = xval(p, row * d + l);
-      ss = fma(x, x, ss);
-      co = fma(__ldg(yo + l), x, co);
-      cb = fma(__ldg(yb + l), x, cb);
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      ss += __shfl_xor_sync(0xffffffffu, ss, off);
-      co += __shfl_xor_sync(0xffffffffu, co, off);
-      cb += __shfl_xor_sync(0xffffffffu, cb, off);
-    }
-    if (lane == 0) exact_finish<COS>(p, row, own, nb, ss, co, cb);
-  }
-}
-
-// Deterministic total over s[]: 32-row units summed by the same xor tree as the exact
-// pass's units, then the last block's fixed-order total (unit_total).
-__global__ void __launch_bounds__(kExactThreads) sum_units_kernel(ScoreParams p, ExactArgs ea) {
-  griddep_wait();
-  const bool abort = *p.abort != 0;
-  const int lane = threadIdx.x & 31;
-  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  if (!abort)
-    for (int64_t u = w0; u < ea.nunits; u += nw) {
-      const int64_t row = u * kUnitRows + lane;
-      double su = row < p.n ? p.s[row] : 0.0;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) su += __shfl_xor_sync(0xffffffffu, su, off);
-      if (lane == 0) ea.usum[u] = su;
-    }
-  __shared__ bool last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(ea.ta.ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last) unit_total(ea, p.n);
-}
-
 }  // namespace
 
 void flag_all(fsil_context* c, const ScoreParams& p, int tile_rows) {
@@ -877,28 +814,6 @@ void exact_pass(fsil_context* c, const ScoreParams& p, bool local) {
   const int64_t tab = static_cast<int64_t>(c->k) * c->d;
   const bool small = tab < 64 * 1024;
   const unsigned long long* pcount = c->pair_count.as<unsigned long long>();
-  if (c->fused_exact) {
-    // the scoring kernel wrote every certain row's a, b, s: refine the flagged rows,
-    // resolve the certified pairs, give those rows theirs, then the total
-    refine(c, p);
-    const unsigned pgrid = static_cast<unsigned>(c->num_sms * 8);
-    if (cos) pair_kernel<true><<<pgrid, 256, 0, c->stream>>>(p, c->pair_rows.as<int2>(), pcount);
-    else pair_kernel<false><<<pgrid, 256, 0, c->stream>>>(p, c->pair_rows.as<int2>(), pcount);
-    FSIL_LAUNCHED(c);
-    if (cos) exact_list_kernel<true><<<pgrid, 256, 0, c->stream>>>(p, c->pair_rows.as<int2>(), pcount);
-    else exact_list_kernel<false><<<pgrid, 256, 0, c->stream>>>(p, c->pair_rows.as<int2>(), pcount);
-    FSIL_LAUNCHED(c);
-    ExactArgs ea{};
-    ea.nunits = (c->n + kUnitRows - 1) / kUnitRows;
-    c->group_sum.ensure(std::max<int64_t>(ea.nunits, 1) * sizeof(double));
-    ea.usum = c->group_sum.as<double>();
-    ea.ta = total_args(c, p, 1, local);
-    ea.ta.group_sum = nullptr;
-    ea.ta.pair_count = pcount;
-    sum_units_kernel<<<static_cast<unsigned>(c->num_sms * 2), kExactThreads, 0, c->stream>>>(p, ea);
-    FSIL_LAUNCHED(c);
-    return;
-  }
   if (!small) {  // full refinements (tiled) and certified pairs as their own launches
     refine(c, p);
     const unsigned pgrid = static_cast<unsigned>(c->num_sms * 8);

@@ -147,6 +147,7 @@ struct fsil_context {
   fsil::DevBuf xmax;           // float: max |x| of this shard (tensor-core operand scaling)
   fsil::DevBuf tc_b;           // fp16 cluster-mean pieces + column bias (tcgen05 path)
   fsil::DevBuf nb_tmp;                   // neighbours when the caller passes no neighbour pointer
+  fsil::DevBuf sub_x, sub_i;             // two-level certificate: the level-1 uncertain rows (x, ids)
   fsil::DevBuf pair_rows, pair_count;    // tcgen05 top-3: rows resolved as a certified pair
   fsil::DevBuf a_scratch;                // tcgen05 streaming mode: per-CTA converted A chunks
   fsil::DevBuf x32;                      // fp64 front end: rounded fp32 copy for the fast pass
@@ -184,7 +185,6 @@ struct fsil_context {
   cudaEvent_t ev[8] = {};
   bool ev7_recorded = false;  // ev[7] marks the scoring kernel's own launch (timing runs)
   bool pdl = true;             // programmatic dependent launch on the hot chain (FSIL_PDL=0: off)
-  bool fused_exact = false;    // this call's scoring kernel computed the certain rows' exact a, b, s
 };
 
 namespace fsil {

@@ -987,16 +987,68 @@ int tc_stages(int bn, int kp, size_t optin) {
 
 template <int BN, bool COS, int KC = 32, int EG = 2, bool T3 = false>
 void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
-               const TcParams& tp, int64_t ntiles) {
+               const TcParams& tp, int64_t ntiles, bool rec = true) {
   auto kern = tp.dbg ? score_tc_kernel<BN, COS, true, KC, EG, T3> : score_tc_kernel<BN, COS, false, KC, EG, T3>;
   const size_t smem = tc_smem(BN, tp.ncb * BN, tp.nstg + tp.nsa);
-  if (c->timing) {  // the kernel alone, for the roofline (ms_score_kernel)
+  if (c->timing && rec) {  // the kernel alone, for the roofline (ms_score_kernel)
     FSIL_CUDA(cudaEventRecord(c->ev[7], c->stream));
     c->ev7_recorded = true;
   }
   FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int grid = static_cast<int>(std::min<int64_t>(ntiles, c->num_sms));
   launch_pdl(c, kern, grid, kThreads, smem, mx, mh, ml, tp, ntiles);
+}
+
+// ---------------------------------------------------------------- two-level certificate
+// Level 1 (the two-MMA CTA-pair pass) leaves its uncertain rows -- more than two candidate
+// neighbours within its bound -- in flag_rows.  Level 2 gathers them into a compact matrix
+// and re-scores them with this file's three-MMA kernel (split accumulators: the tight
+// bound); its neighbours go back to the original rows, its certified pairs join the pair
+// list, and only its own uncertain rows stay for the fp64 refinement.
+__global__ void gather_uncertain_kernel(const float* __restrict__ X, const int32_t* __restrict__ dense,
+                                        const int32_t* __restrict__ rows, int64_t nrows, int d,
+                                        float* __restrict__ xs, int32_t* __restrict__ ds,
+                                        unsigned long long* __restrict__ sub_counts) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x < 2) sub_counts[threadIdx.x] = 0ull;
+  for (int64_t i = w; i < nrows; i += nw) {
+    const int64_t r = rows[i];
+    const float4* src = reinterpret_cast<const float4*>(X + r * d);
+    float4* dst = reinterpret_cast<float4*>(xs + i * d);
+    for (int l = lane; l < (d >> 2); l += 32) dst[l] = __ldg(src + l);
+    if (lane == 0) ds[i] = __ldg(dense + r);
+  }
+}
+
+// nb of every re-scored row back to its row; level-2 uncertain rows -> original ids (in
+// place); level-2 certified pairs appended to the main pair list
+__global__ void remap_uncertain_kernel(const int32_t* __restrict__ rows, int64_t nrows,
+                                       const int32_t* __restrict__ sub_nb, int32_t* __restrict__ nb,
+                                       int32_t* __restrict__ sub_flag, const int2* __restrict__ sub_pairs,
+                                       const unsigned long long* __restrict__ sub_counts, int2* pairs,
+                                       unsigned long long* pair_count) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int64_t i = t0; i < nrows; i += stride) nb[rows[i]] = sub_nb[i];
+  const int64_t nf = static_cast<int64_t>(sub_counts[0]), np = static_cast<int64_t>(sub_counts[1]);
+  for (int64_t i = t0; i < nf; i += stride) sub_flag[i] = rows[sub_flag[i]];
+  for (int64_t i = t0; i < np; i += stride) {
+    const int2 pr = sub_pairs[i];
+    const unsigned long long j = atomicAdd(pair_count, 1ull);
+    pairs[j] = make_int2(rows[pr.x], pr.y);
+  }
+}
+
+// the level-2 uncertain rows become the flag list the refinement reads
+__global__ void adopt_flags_kernel(const int32_t* __restrict__ sub_flag, const unsigned long long* __restrict__ sub_counts,
+                                   int32_t* __restrict__ flag_rows, unsigned long long* flag_count) {
+  const int64_t nf = static_cast<int64_t>(sub_counts[0]);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nf; i += stride)
+    flag_rows[i] = sub_flag[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *flag_count = static_cast<unsigned long long>(nf);
 }
 
 }  // namespace
@@ -1013,7 +1065,6 @@ int64_t tc_tiles(const fsil_context* c, int* tile_rows) {
 }
 
 void score_tc(fsil_context* c, const ScoreParams& p) {
-  c->fused_exact = false;  // set by the pair kernel's launcher when it computes the exact rows
   const bool cos = c->metric == FSIL_COSINE;
   const int bn = pick_bn(c->k);
   int ncb = (c->k + bn - 1) / bn;
@@ -1148,12 +1199,75 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   tp.pair_count = c->pair_count.as<unsigned long long>();  // zeroed by agg_init
   if (pair) {
     // one fp32 accumulator (512 TMEM columns hold two 256-column buffers): the correction
-    // products share the main accumulator, 3 MMAs per K step in its rounding bound
-    tp.split = 0;
-    tp.cdot = 1.05f * (12.0f + 2.0f * kMmaUlp * 3.0f * steps + 1.0f) * u;
-    if (c->X64) tp.cdot += 1.01f * u;
+    // products share the main accumulator, 2 or 3 MMAs per K step in its rounding bound.
+    // Two-level certificate (default): level 1 is the two-MMA pass (hx.hm + hx.lm, the
+    // dropped lx.hm bounded per row by ||lx|| ||mu_k||); level 2 re-scores its uncertain rows
+    // with the three-MMA kernel below.  FSIL_TC_TWO=0: one three-MMA pair pass.
+    static const bool two_env = [] {
+      const char* e = std::getenv("FSIL_TC_TWO");
+      return !e || std::atoi(e) != 0;
+    }();
+    const bool two = two_env && !c->X64;
+    TcParams tpp = tp;
+    tpp.split = 0;
+    tpp.cdot = 1.05f * (12.0f + 2.0f * kMmaUlp * (two ? 2.0f : 3.0f) * steps + 1.0f) * u;
+    if (c->X64) tpp.cdot += 1.01f * u;
     const bool t3p = t3_env && static_cast<int64_t>(c->k) * c->d >= 64 * 1024;
-    launch_tc_pair(c, mx, mh, ml, tp, ntiles, cos, t3p);
+    launch_tc_pair(c, mx, mh, ml, tpp, ntiles, cos, t3p, two);
+    if (!two) return;
+    // ---- level 2
+    unsigned long long nf = 0;
+    FSIL_CUDA(cudaMemcpyAsync(&nf, p.flag_count, sizeof(nf), cudaMemcpyDeviceToHost, c->stream));
+    FSIL_CUDA(cudaStreamSynchronize(c->stream));
+    const int64_t F = static_cast<int64_t>(nf);
+    // (a speculation miss aborted the pass: nothing flagged; very many uncertain rows: the
+    // fp64 refinement takes them all rather than a large gathered copy)
+    const int64_t cap = std::max<int64_t>(1 << 16, std::min<int64_t>(c->n / 4, (int64_t(4) << 30) / (4 * c->d)));
+    if (F == 0 || F > cap) return;
+    c->sub_x.ensure(static_cast<size_t>(F) * c->d * sizeof(float));
+    c->sub_i.ensure(static_cast<size_t>(F) * (3 * sizeof(int32_t) + sizeof(int2)) + 64);
+    int2* sub_pairs = c->sub_i.as<int2>();
+    unsigned long long* sub_counts = reinterpret_cast<unsigned long long*>(sub_pairs + F);
+    int32_t* sub_dense = reinterpret_cast<int32_t*>(sub_counts + 2);
+    int32_t* sub_nb = sub_dense + F;
+    int32_t* sub_flag = sub_nb + F;
+    float* xs = c->sub_x.as<float>();
+    const unsigned g = static_cast<unsigned>(std::min<int64_t>((F + 7) / 8, static_cast<int64_t>(c->num_sms) * 8));
+    gather_uncertain_kernel<<<g, 256, 0, c->stream>>>(p.X, p.dense, p.flag_rows, F, c->d, xs, sub_dense, sub_counts);
+    FSIL_LAUNCHED(c);
+    ScoreParams p2 = p;
+    p2.X = xs;
+    p2.X64 = nullptr;
+    p2.dense = sub_dense;
+    p2.n = F;
+    p2.nb = sub_nb;
+    p2.flag_rows = sub_flag;
+    p2.flag_count = sub_counts;
+    TcParams t2 = tp;  // the single-CTA three-MMA parameter set (split accumulators for D > 128)
+    t2.p = p2;
+    t2.xi_rows = nullptr;  // the gathered rows' ||x||^2: formed by the converters
+    t2.exic = 8.1f;
+    t2.lean = 0;
+    t2.pair_rows = sub_pairs;
+    t2.pair_count = sub_counts + 1;
+    const int64_t nt2 = (F + BM - 1) / BM;
+    const int64_t grid2 = std::min<int64_t>(nt2, c->num_sms);
+    c->a_scratch.ensure(static_cast<size_t>(grid2) * nkc * kStgBytes);
+    t2.ascratch = c->a_scratch.as<uint8_t>();
+    const CUtensorMap mx2 = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, xs, c->d, F, c->d * 4ull, 32, BM);
+    // (ms_score_kernel spans both levels: the first level's start event is kept)
+    if (cos) {
+      if (t3p) launch_tc<128, true, 32, 2, true>(c, mx2, mh, ml, t2, nt2, false);
+      else launch_tc<128, true>(c, mx2, mh, ml, t2, nt2, false);
+    } else {
+      if (t3p) launch_tc<128, false, 32, 2, true>(c, mx2, mh, ml, t2, nt2, false);
+      else launch_tc<128, false>(c, mx2, mh, ml, t2, nt2, false);
+    }
+    remap_uncertain_kernel<<<g, 256, 0, c->stream>>>(p.flag_rows, F, sub_nb, p.nb, sub_flag, sub_pairs, sub_counts,
+                                                      tp.pair_rows, tp.pair_count);
+    FSIL_LAUNCHED(c);
+    adopt_flags_kernel<<<g, 256, 0, c->stream>>>(sub_flag, sub_counts, p.flag_rows, p.flag_count);
+    FSIL_LAUNCHED(c);
     return;
   }
   // K <= 24 at BN = 32: the epilogue scans only the first 16 / 24 columns

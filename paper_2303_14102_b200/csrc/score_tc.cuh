@@ -52,8 +52,6 @@ struct TcParams {
   int lean;               // converters only convert; the epilogue fetches own/||x||^2 itself
   int2* pair_rows;        // T3: rows whose neighbour is one of {nb, .y} (certified pair)
   unsigned long long* pair_count;
-  int fexact;             // pair kernel: certain rows get their exact a, b, s in the kernel
-  int pf;                 // pair kernel: converters prepare each tile's A scratch a tile ahead
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -72,12 +70,15 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 template <bool COS, bool T3>
 __device__ __forceinline__ bool certify_row(const TcParams& tp, const TcScale& sc, int64_t row, int own,
                                             float xi, float xn, float rnf, float b1, float b2, float b3,
-                                            int arg, int arg2, float mu_arg_ratio, float mu_arg2_ratio = 1.0f) {
+                                            int arg, int arg2, float mu_arg_ratio, float mu_arg2_ratio = 1.0f,
+                                            float x_rel = -1.0f) {
   const float u = 5.9604645e-8f;
   const float rowc = COS ? 1.0f : xi;
   const float exi = tp.exic * u * xi;  // ||x||^2 error (fp32 blocks of 8; fp64 input rounding)
   const float rx = COS ? rnf : rsqrtf(xi);  // 1/||x|| (<= 2.2u; inf for a zero row -> flagged)
-  const float cmu = tp.cdot + sc.floor_x * rx * 1.0001f;
+  // x_rel >= 0 (two-MMA first level): the dropped x piece's ||lx||/||x~||, which also covers
+  // the x pieces' fp16 subnormal floor; otherwise that floor per row
+  const float cmu = tp.cdot + (x_rel >= 0.0f ? x_rel : sc.floor_x * rx * 1.0001f);
   // key error: the dot bound (per unit ||x|| for cosine); the key's own roundings
   // (cosine: rsqrt 2.2u + product 0.5u + fma 0.5u on |m| <= 1, within 4u(|b1|+1));
   // the ||x||^2 error
@@ -125,7 +126,7 @@ CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* ptr, uint64_t inner,
 // MMA block, for streaming cluster tables.  Returns false when it does not apply.
 bool pair_supported(const fsil_context* c, const TcParams& tp, int bn);
 void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
-                    TcParams tp, int64_t ntiles, bool cos, bool t3);
+                    TcParams tp, int64_t ntiles, bool cos, bool t3, bool two);
 
 }  // namespace tc
 }  // namespace fsil

@@ -186,11 +186,15 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 struct PairSmem {
   static size_t bytes(int ns, int nb) {
     return 1024 + static_cast<size_t>(ns) * kStgBytes + static_cast<size_t>(nb) * 2 * kBPiece + 64 * 8 +
-           4 * BM * 8 + 10 * BM * 4 + 2 * BM * 4 + 2 * BM * 4 + 64;
+           4 * BM * 8 + 10 * BM * 4 + 2 * BM * 4 + 4 * BM * 4 + 64;
   }
 };
 
-template <bool COS, bool T3>
+// TWO: the first level of a two-level certificate -- two MMAs per K step, hx.hm + hx.lm
+// (the x pieces' low half dropped; its contribution is bounded per row by ||lx|| ||mu_k||,
+// lx = x~ - hx exact in fp32), A operands of 16 KB per chunk.  Rows it cannot certify are
+// re-scored at three-MMA precision (score_tc.cu, level 2).
+template <bool COS, bool T3, bool TWO>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_pair_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
                          const __grid_constant__ CUtensorMap tmap_bl, const __grid_constant__ CUtensorMap tmap_scr,
@@ -224,15 +228,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   double* meta_xi = reinterpret_cast<double*>(bars + 64);    // [2][2][BM]
   float* part = reinterpret_cast<float*>(meta_xi + 4 * BM);  // [2][5][BM]
   int* meta_own = reinterpret_cast<int*>(part + 10 * BM);     // [2][BM]
-  int* exl = meta_own + 2 * BM;                                // [2][BM] fused exact: certain nb, or -1
-  uint64_t* exact_full = bars + 50;  // [2] local: a tile's certified neighbours (epilogue group 0)
-  uint64_t* scr_ready2 = bars + 52;  // [2] prefetch mode: scratch buffer b holds its tile's chunks
-  uint64_t* scr_free = bars + 54;    // [2] prefetch mode: every reload of buffer b's tile consumed
+  float* meta_lx = reinterpret_cast<float*>(meta_own + 2 * BM);  // [2][2][BM] TWO: ||lx||^2 halves
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // scratch: [CTA][buffer (prefetch mode: tile parity)][nkc][kStgBytes]
-  const int nbuf = tp.pf ? 2 : 1;
-  uint8_t* const myscr = tp.ascratch + static_cast<size_t>(blockIdx.x) * nbuf * nkc * kStgBytes;
+  uint8_t* const myscr = tp.ascratch + static_cast<size_t>(blockIdx.x) * nkc * kStgBytes;  // [nkc][kStgBytes]
   const TcScale sc = *tp.scale;
   unsigned long long* const dbg = tp.dbg;
   const long long t_begin = dbg ? clock64() : 0;
@@ -254,12 +253,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(meta_empty + i, 4);
     }
     mbar_init(scr_ready, 1);
-    mbar_init(exact_full + 0, 4);
-    mbar_init(exact_full + 1, 4);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(scr_ready2 + i, 1);
-      mbar_init(scr_free + i, 1);
-    }
     fence_barrier_init();
     prefetch_tmap(&tmap_x);
     prefetch_tmap(&tmap_bh);
@@ -280,22 +273,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_x = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
       for (int64_t st = cid; st < nst; st += ncl, ++ntl) {
         const int row0 = static_cast<int>(st * 2 * BM + rank * BM);
-        const int64_t sbase = (static_cast<int64_t>(blockIdx.x) * nbuf + (tp.pf ? (ntl & 1) : 0)) * nkc;
-        if (tp.pf) {  // the converters prepared this tile's chunks: every pass reloads them
-          PW(5, mbar_wait(scr_ready2 + (ntl & 1), (ntl >> 1) & 1));
-          fence_proxy_async_global();
-        }
+        const int64_t sbase = static_cast<int64_t>(blockIdx.x) * nkc;
         for (int xp = 0; xp < ncb; ++xp) {
-          if (xp == 1 && !tp.pf) {  // the first pass converted and stored this tile: reuse it
+          if (xp == 1) {  // the first pass converted and stored this tile: reuse it
             PW(5, mbar_wait(scr_ready, ntl & 1));
             fence_proxy_async_global();
           }
           for (int kc = 0; kc < nkc; ++kc, ++n1) {
             const int s1 = static_cast<int>(n1 % ns);
             PW(4, mbar_wait_cluster(stg_empty + s1, ((n1 / ns) & 1) ^ 1));  // (multicast commit)
-            if (xp > 0 || tp.pf) {
+            if (xp > 0) {
               const uint32_t af = mapa_u32(smem_u32(a_full + s1), 0);
-              if (leader) mbar_arrive_expect_tx_cluster(af, 2 * kStgBytes);
+              if (leader) mbar_arrive_expect_tx_cluster(af, 2 * (TWO ? kABytes : kStgBytes));
+              // (TWO: the map's box is the 16 KB hx piece at the start of each 32 KB chunk)
               tma_load_2d_pair_hint(stg + s1 * kStgBytes, &tmap_scr, af, 0, static_cast<int>((sbase + kc) * BM),
                                     pol_keep);
               if (!leader) mbar_arrive_cluster(af);
@@ -329,8 +319,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     } else if (warp == 1 && lane == 0 && leader) {
       // ------------------------------------------------------------ MMA issuer (the pair's)
-      uint32_t n2 = 0, ia = 0, na = 0, ntm = 0;
-      for (int64_t st = cid; st < nst; st += ncl, ++ntm) {
+      uint32_t n2 = 0, ia = 0, na = 0;
+      for (int64_t st = cid; st < nst; st += ncl) {
         for (int cb = 0; cb < ncb; ++cb, ++na) {
           const int ab = static_cast<int>(na & 1);
           PW(0, mbar_wait_cluster(acc_empty + ab, ((na >> 1) & 1) ^ 1));
@@ -349,15 +339,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
               mma_f16_pair(d, dah + 2 * ks, dbh + 2 * ks, kIdesc, acc0);
               mma_f16_pair(d, dah + 2 * ks, dbl + 2 * ks, kIdesc, 1u);
-              mma_f16_pair(d, dal + 2 * ks, dbh + 2 * ks, kIdesc, 1u);
+              if (!TWO) mma_f16_pair(d, dal + 2 * ks, dbh + 2 * ks, kIdesc, 1u);
             }
             mma_commit_pair(b_empty + sb, 0x3);
             mma_commit_pair(stg_empty + s1, 0x3);
           }
           mma_commit_pair(acc_full + ab, 0x3);
         }
-        // prefetch mode: this tile's scratch buffer has been read by every reload
-        if (tp.pf) mma_commit_pair(scr_free + (ntm & 1), 0x3);
       }
       if (dbg) atomicAdd(dbg + 3, static_cast<unsigned long long>(clock64() - t_begin));
     }
@@ -370,130 +358,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float2 sx2 = make_float2(sc.sx, sc.sx), neg1 = make_float2(-1.f, -1.f);
     uint32_t n1 = 0, nt = 0, tpar = 0;  // tpar bit s: parity of stage s's next X landing
     int s1 = 0;
-    // Fused exact pass: while the MMAs stream a tile's cluster blocks, the converters (idle
-    // after the tile's first pass) give the previous tile's certain rows their fp64 a_i,
-    // b_i, s_i -- the reference formulas (score_common.cuh) on the row re-read from
-    // global memory, one row per warp, lanes over D in a fixed order.  Flagged and pair
-    // rows are left to the post-scoring passes.
-    const int cw = (threadIdx.x >> 5) - kConv0;  // converter warp 0..7
-    auto exact_tile = [&](uint32_t t_idx, int64_t st_t) {
-      const int tbx = t_idx & 1;
-      mbar_wait(exact_full + tbx, (t_idx >> 1) & 1);
-      const double* sums = p.stats + (COS ? p.k : 2 * p.k);
-      const int d = p.d;
-      for (int rr = cw; rr < BM; rr += 8) {
-        const int nbr = exl[tbx * BM + rr];
-        if (nbr < 0) continue;  // warp-uniform
-        const int ownr = meta_own[tbx * BM + rr];
-        const int64_t row = st_t * 2 * BM + rank * BM + rr;
-        const float* xr = p.X + row * d;
-        const double* yo = sums + static_cast<int64_t>(ownr) * d;
-        const double* yb = sums + static_cast<int64_t>(nbr) * d;
-        double ss = 0.0, co = 0.0, cb = 0.0;
-#pragma unroll 4
-        for (int l = lane; l < d; l += 32) {
-          const double x = static_cast<double>(__ldg(xr + l));
-          ss = fma(x, x, ss);
-          co = fma(__ldg(yo + l), x, co);
-          cb = fma(__ldg(yb + l), x, cb);
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          ss += __shfl_xor_sync(0xffffffffu, ss, off);
-          co += __shfl_xor_sync(0xffffffffu, co, off);
-          cb += __shfl_xor_sync(0xffffffffu, cb, off);
-        }
-        if (lane == 0) {
-          const double n_o = p.nk[ownr], n_b = p.nk[nbr];
-          const bool singleton = n_o == 1.0;
-          double a, b;
-          if (COS) {
-            const double nrm = sqrt(ss);
-            b = cos_foreign(n_b, cb / nrm);
-            a = singleton ? 0.0 : cos_own(n_o, co / nrm);
-          } else {
-            b = sq_foreign(ss, p.stats[p.k + nbr], n_b, cb);
-            a = singleton ? 0.0 : sq_own(ss, p.stats[p.k + ownr], n_o, co);
-          }
-          p.s[row] = singleton ? 0.0 : assemble_score(a, b);
-          if (p.a) p.a[row] = a;
-          if (p.b) p.b[row] = b;
-          if (p.own) p.own[row] = ownr;
-        }
-      }
-    };
-    int64_t st_prev = -1;
-    if (tp.pf) {
-      // Prefetch mode: the converters read each tile's rows straight from global memory
-      // (two threads per row, 128 B each per chunk), split them and store the fp16 pieces
-      // in the UMMA K-major SWIZZLE_128B byte image to the tile's scratch buffer (tile
-      // parity), a tile ahead of the MMAs: no HBM latency or conversion on the tensor
-      // pipe's critical path.  A buffer is rewritten only after the MMA issuer's commit
-      // says every reload of its previous tile was consumed.
-      const float* Xg = p.X;
-      const int d = p.d;
-      for (int64_t st = cid; st < nst; st += ncl, ++nt) {
-        const int64_t row = st * 2 * BM + rank * BM + r;
-        const bool rv = row < p.n;
-        const int own = (hq == 0 && rv) ? __ldg(p.dense + row) : -1;
-        const int b = nt & 1;
-        if (nt >= 2) mbar_wait_cluster(scr_free + b, ((nt >> 1) - 1) & 1);
-        uint8_t* sb = myscr + static_cast<size_t>(b) * nkc * kStgBytes;
-        double xi = 0.0;
-        for (int kc = 0; kc < nkc; ++kc) {
-          const int c0 = kc * BK + hq * 32;
-          float4 f[8];
-          const float* xr = Xg + (rv ? row : 0) * d + c0;
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            f[u] = (rv && c0 + 4 * u < d) ? __ldg(reinterpret_cast<const float4*>(xr) + u) : make_float4(0.f, 0.f, 0.f, 0.f);
-          uint8_t* hrow = sb + static_cast<size_t>(kc) * kStgBytes + r * 128;
-          uint8_t* lrow = hrow + BM * 128;
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int j = 4 * hq + jj;
-            const float v[8] = {f[2 * jj].x,     f[2 * jj].y,     f[2 * jj].z,     f[2 * jj].w,
-                                f[2 * jj + 1].x, f[2 * jj + 1].y, f[2 * jj + 1].z, f[2 * jj + 1].w};
-            if (!tp.xi_rows) {  // ||x||^2: fp32 blocks of 8 (error <= 8u each), fp64 across blocks
-              float2 bs = make_float2(0.f, 0.f);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 ve = make_float2(v[2 * e], v[2 * e + 1]);
-                bs = __ffma2_rn(ve, ve, bs);
-              }
-              xi += static_cast<double>(bs.x + bs.y);
-            }
-            uint32_t hw[4], lw[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 xx = __fmul2_rn(make_float2(v[2 * e], v[2 * e + 1]), sx2);
-              const __half2 h = __float22half2_rn(xx);
-              const float2 res = __ffma2_rn(__half22float2(h), neg1, xx);
-              const __half2 l = __float22half2_rn(res);
-              hw[e] = *reinterpret_cast<const uint32_t*>(&h);
-              lw[e] = *reinterpret_cast<const uint32_t*>(&l);
-            }
-            const int pos = (j ^ sw) << 4;
-            *reinterpret_cast<uint4*>(hrow + pos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-            *reinterpret_cast<uint4*>(lrow + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-          }
-        }
-        // generic-proxy stores -> the producer's tensor copies (async proxy)
-        fence_proxy_async_global();
-        named_bar_sync(5, 256);
-        if (tl == 0) mbar_arrive(scr_ready2 + b);
-        const int tb = nt & 1;
-        mbar_wait(meta_empty + tb, ((nt >> 1) & 1) ^ 1);
-        meta_xi[(tb * 2 + hq) * BM + r] = xi;
-        if (hq == 0) meta_own[tb * BM + r] = own;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(meta_full + tb);
-      }
-    } else {
     for (int64_t st = cid; st < nst; st += ncl, ++nt) {
       const int64_t row = st * 2 * BM + rank * BM + r;
       const int own = (hq == 0 && row < p.n) ? __ldg(p.dense + row) : -1;
       double xi = 0.0;
+      float lx2 = 0.0f;  // TWO: sum of lx^2 (lx = x~ - hx, exact in fp32; tiny, fp32 sum + margin)
       for (int kc = 0; kc < nkc; ++kc, ++n1) {
         if (tl == 0) PW(9, mbar_wait(stg_full + s1, (tpar >> s1) & 1u));
         else mbar_wait(stg_full + s1, (tpar >> s1) & 1u);
@@ -530,20 +399,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float2 xx = __fmul2_rn(make_float2(v[2 * e], v[2 * e + 1]), sx2);
             const __half2 h = __float22half2_rn(xx);
             const float2 res = __ffma2_rn(__half22float2(h), neg1, xx);
-            const __half2 l = __float22half2_rn(res);
+            if (TWO) {
+              lx2 = fmaf(res.x, res.x, fmaf(res.y, res.y, lx2));
+            } else {
+              const __half2 l = __float22half2_rn(res);
+              lw[e] = *reinterpret_cast<const uint32_t*>(&l);
+            }
             hw[e] = *reinterpret_cast<const uint32_t*>(&h);
-            lw[e] = *reinterpret_cast<const uint32_t*>(&l);
           }
           const int pos = (j ^ sw) << 4;
           *reinterpret_cast<uint4*>(hrow + pos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-          *reinterpret_cast<uint4*>(lrow + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          if (!TWO) *reinterpret_cast<uint4*>(lrow + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
         }
         fence_proxy_async_smem();
         named_bar_sync(5, 256);
         if (tl == 0) {
           // the converted chunk -> scratch (read before the MMA may free the stage), then
           // this CTA's single arrival on the leader's a_full
-          bulk_store_hint(myscr + static_cast<size_t>(kc) * kStgBytes, sbase, kStgBytes, l2_policy_evict_last());
+          bulk_store_hint(myscr + static_cast<size_t>(kc) * kStgBytes, sbase, TWO ? kABytes : kStgBytes,
+                          l2_policy_evict_last());
           bulk_wait_read();
           mbar_arrive_cluster(mapa_u32(smem_u32(a_full + s1), 0));
         }
@@ -560,13 +434,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tb = nt & 1;
       mbar_wait(meta_empty + tb, ((nt >> 1) & 1) ^ 1);
       meta_xi[(tb * 2 + hq) * BM + r] = xi;
+      if (TWO) meta_lx[(tb * 2 + hq) * BM + r] = lx2;
       if (hq == 0) meta_own[tb * BM + r] = own;
       __syncwarp();
       if (lane == 0) mbar_arrive(meta_full + tb);
-      if (tp.fexact && nt > 0) exact_tile(nt - 1, st_prev);
-      st_prev = st;
-    }
-    if (tp.fexact && nt > 0) exact_tile(nt - 1, st_prev);
     }
   } else {
     // ------------------------------------------------------------ epilogue (8 warps)
@@ -589,6 +460,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float xn = COS ? 0.0f : sqrtf(xi);
       const float rnf = COS ? rsqrtf(xi) : 0.0f;
       const float rowm = COS ? -(sc.smul * rnf) : -2.0f * sc.smul;
+      // TWO: ||lx|| / ||x~|| (the dropped piece, relative to the row; fp32 sums of squares
+      // of numbers ~2^-11 |x| carry < 1e-4 relative error: x 1.001 margin; rsqrt <= 2.2u)
+      const float lx_rel = TWO ? sqrtf(meta_lx[(tb * 2) * BM + r] + meta_lx[(tb * 2 + 1) * BM + r]) * rsqrtf(xi) /
+                                     sc.sx * 1.001f
+                               : -1.0f;
       float b1 = INFINITY, b2 = INFINITY, b3 = INFINITY;
       int arg = -1, arg2 = -1;
       // one 32-column chunk: ranking keys (own column excluded), running top-2 / top-3
@@ -680,16 +556,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // group 0 has read the partials and the meta slot: both may be reused
       __syncwarp();
       if (lane == 0) mbar_arrive(meta_empty + tb);
-      bool certain = false;
       if (valid)
-        certain = certify_row<COS, T3>(tp, sc, row, own, xi, xn, rnf, b1, b2, b3, arg, arg2,
+        certify_row<COS, T3>(tp, sc, row, own, xi, xn, rnf, b1, b2, b3, arg, arg2,
                                        arg >= 0 ? __half2float(__ldg(tp.munorm + arg)) : 1.0f,
-                                       arg2 >= 0 ? __half2float(__ldg(tp.munorm + arg2)) : 1.0f);
-      if (tp.fexact) {  // the converters compute the certain rows' exact a, b, s
-        exl[tb * BM + r] = certain ? arg : -1;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(exact_full + tb);
-      }
+                                       arg2 >= 0 ? __half2float(__ldg(tp.munorm + arg2)) : 1.0f, lx_rel);
     }
   }
 
@@ -713,7 +583,7 @@ bool pair_supported(const fsil_context* c, const TcParams& tp, int bn) {
 }
 
 void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
-                    TcParams tp, int64_t ntiles, bool cos, bool t3) {
+                    TcParams tp, int64_t ntiles, bool cos, bool t3, bool two) {
   // stages: X/A and B rings of 32 KB each; 3 + 3 at 227 KB.  Measured (C5, 4M rows):
   // 3 + 3 59.1 ms, 4 + 2 62.1 ms, 3 + 2 64.5 ms -- the issuer's A waits shrink with more
   // A stages but its B waits grow faster
@@ -723,35 +593,23 @@ void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& m
   if (const char* e = std::getenv("FSIL_TC_PAIR_NS")) ns = std::max(2, std::min(8, std::atoi(e)));
   while (PairSmem::bytes(ns, nb) > c->smem_optin && ns > 2) --ns;
   tp.ncb = (c->k + kPairN - 1) / kPairN;
-  // Fused exact pass (FSIL_TC_FEXACT=1): measured at C5, the post-scoring phase drops
-  // 45 -> 11 ms but the scoring kernel grows 636 -> 685 ms -- the converters' fp64 table
-  // reads (12 KB per row) compete with the A/B operand traffic in L2 -- so it is off.
-  static const bool fexact_env = [] {
-    const char* e = std::getenv("FSIL_TC_FEXACT");
-    return e && std::atoi(e) != 0;
-  }();
-  // Prefetch mode (FSIL_TC_PAIR_PF=1): the converters prepare each tile's scratch a tile
-  // ahead from global memory, so every pass is a reload.  Measured at C5: 636 -> 686 ms --
-  // the issuer's waits are on the reloads themselves (L2), and the double scratch (114 MB)
-  // evicts more of them -- so it is off.
-  static const bool pf_env = [] {
-    const char* e = std::getenv("FSIL_TC_PAIR_PF");
-    return e && std::atoi(e) != 0;
-  }();
-  tp.pf = pf_env ? 1 : 0;
-  tp.fexact = fexact_env && !c->X64 && !tp.pf ? 1 : 0;  // (the fused exact pass rides on pass 0)
-  c->fused_exact = tp.fexact != 0;
+  // (Measured and removed: a fused exact pass in the converters -- the post pass 45 -> 11 ms
+  // but the kernel 636 -> 685 ms, fp64 table reads competing with the operand stream in L2 --
+  // and converter-prefetched double-buffered scratch -- 686 ms: the issuer waits on the
+  // reloads themselves, and a 114 MB scratch evicts more of them.  DESIGN.md 4.5.)
   const int grid = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(2 * ((ntiles + 1) / 2), c->num_sms & ~1)));
-  const int nbuf = tp.pf ? 2 : 1;  // prefetch mode: one buffer per tile parity
-  c->a_scratch.ensure(static_cast<size_t>(grid) * nbuf * tp.nkc * kStgBytes);
+  c->a_scratch.ensure(static_cast<size_t>(grid) * tp.nkc * kStgBytes);
   tp.ascratch = c->a_scratch.as<uint8_t>();
-  // the scratch as a 2-D tensor of 256-byte rows: one 32 KB box = one converted chunk
+  // the scratch as a 2-D tensor of 256-byte rows: one 32 KB box = one converted chunk (two-
+  // MMA level: the 16 KB hx piece at the start of each chunk, a box of 64 such rows)
   const CUtensorMap mscr = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_UINT16, tp.ascratch, 128,
-                                       static_cast<uint64_t>(grid) * nbuf * tp.nkc * BM, 256, 128, BM,
+                                       static_cast<uint64_t>(grid) * tp.nkc * BM, 256, 128, two ? BM / 2 : BM,
                                        CU_TENSOR_MAP_SWIZZLE_NONE);
   const size_t smem = PairSmem::bytes(ns, nb);
-  auto kern = cos ? (t3 ? score_tc_pair_kernel<true, true> : score_tc_pair_kernel<true, false>)
-                  : (t3 ? score_tc_pair_kernel<false, true> : score_tc_pair_kernel<false, false>);
+  auto kern = two ? (cos ? (t3 ? score_tc_pair_kernel<true, true, true> : score_tc_pair_kernel<true, false, true>)
+                        : (t3 ? score_tc_pair_kernel<false, true, true> : score_tc_pair_kernel<false, false, true>))
+                  : (cos ? (t3 ? score_tc_pair_kernel<true, true, false> : score_tc_pair_kernel<true, false, false>)
+                         : (t3 ? score_tc_pair_kernel<false, true, false> : score_tc_pair_kernel<false, false, false>));
   FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   if (c->timing) {  // the kernel alone, for the roofline (ms_score_kernel)
     FSIL_CUDA(cudaEventRecord(c->ev[7], c->stream));
