@@ -332,14 +332,20 @@ class Runner:
             else:
                 traffic = j.get("dram_bytes_per_launch")
         if self.config in TENSOR_CONFIGS:
-            # fp32-faithful split-precision rate: 3 fp16 MMAs per product,
-            # the sustained bf16 figure for a kernel inside a long step
-            peak = pk["tc_sustained"] / 3.0
+            # split-precision rate: m fp16 MMAs per product, the sustained bf16 figure for a
+            # kernel inside a long step.  m = 3 (fp16x3) or 2 (the two-level
+            # certificate's first level, which scores every row; its three-MMA re-score of
+            # the uncertain rows is inside the timed kernel window)
+            mmas = int(self.st.get("tc_mmas", 0) or 3)
+            peak = pk["tc_sustained"] / mmas
             flops = 2.0 * self.K * self.D * self.n
             achieved = flops / (score_ms / 1e3) / 1e12
             rf.update({"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                        "frac": achieved / peak, "traffic": traffic, "algorithmic_flops_per_point": 2 * self.K * self.D,
-                       "peak_note": "P_tc = bf16_tflops_sustained / 3 (split-precision fp16x3)"})
+                       "mmas_per_product": mmas,
+                       "rescored_rows": int(self.st.get("rescored_rows", 0)),
+                       "peak_note": f"P_tc = bf16_tflops_sustained / {mmas} (split precision, {mmas} fp16 MMAs "
+                                    f"per K step of the pass that scores every row)"})
         else:
             bpp = bytes_per_point(self.D)
             achieved = (self.n * bpp) / (score_ms / 1e3) / 1e9

@@ -82,6 +82,10 @@ typedef struct {
   float ms_densify, ms_aggregate, ms_score, ms_refine, ms_finalize; /* device time, 0 unless timing on */
   float ms_score_kernel;   /* the scoring kernel alone (ms_score minus its operand preparation) */
   int64_t pair_rows;       /* rows whose neighbour was one of two certified candidates, decided in fp64 */
+  int32_t tc_mmas;         /* tensor-core MMAs per 16-deep K step of the pass that scored every row:
+                              3 (fp16x3), 2 (the two-level certificate's first level); 0 otherwise */
+  int32_t pad0;
+  int64_t rescored_rows;   /* two-level certificate: rows re-scored at three-MMA precision */
 } fsil_stats;
 
 fsil_status fsil_create(fsil_context** ctx, int device);

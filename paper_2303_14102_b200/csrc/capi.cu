@@ -92,6 +92,8 @@ void setup(fsil_context* c, int metric, const void* dX, bool x64, const int32_t*
   c->k_spec = false;
   c->spec_missed = false;
   c->stats = fsil_stats{};
+  c->tc_mmas = 0;
+  c->rescored = 0;
   record(c, 0);
 }
 
@@ -304,6 +306,8 @@ double finish(fsil_context* c, double* flagged_out) {
   c->stats.flagged_rows = static_cast<int64_t>(res[1]);
   c->stats.exact_rows = static_cast<int64_t>(res[2]);
   c->stats.pair_rows = static_cast<int64_t>(res[3]);
+  c->stats.tc_mmas = c->tc_mmas;
+  c->stats.rescored_rows = c->rescored;
   c->stats.kernel_launches = c->launches;
   if (c->timing) {
     float* ms[5] = {&c->stats.ms_densify, &c->stats.ms_aggregate, &c->stats.ms_score,

@@ -148,6 +148,8 @@ struct fsil_context {
   fsil::DevBuf tc_b;           // fp16 cluster-mean pieces + column bias (tcgen05 path)
   fsil::DevBuf nb_tmp;                   // neighbours when the caller passes no neighbour pointer
   fsil::DevBuf sub_x, sub_i;             // two-level certificate: the level-1 uncertain rows (x, ids)
+  int32_t tc_mmas = 0;                   // MMAs per K step of this call's tensor-core pass (stats)
+  int64_t rescored = 0;                  // two-level certificate: rows re-scored at three MMAs
   fsil::DevBuf pair_rows, pair_count;    // tcgen05 top-3: rows resolved as a certified pair
   fsil::DevBuf a_scratch;                // tcgen05 streaming mode: per-CTA converted A chunks
   fsil::DevBuf x32;                      // fp64 front end: rounded fp32 copy for the fast pass

@@ -1214,6 +1214,7 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     if (c->X64) tpp.cdot += 1.01f * u;
     const bool t3p = t3_env && static_cast<int64_t>(c->k) * c->d >= 64 * 1024;
     launch_tc_pair(c, mx, mh, ml, tpp, ntiles, cos, t3p, two);
+    c->tc_mmas = two ? 2 : 3;
     if (!two) return;
     // ---- level 2
     unsigned long long nf = 0;
@@ -1224,6 +1225,7 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     // fp64 refinement takes them all rather than a large gathered copy)
     const int64_t cap = std::max<int64_t>(1 << 16, std::min<int64_t>(c->n / 4, (int64_t(4) << 30) / (4 * c->d)));
     if (F == 0 || F > cap) return;
+    c->rescored = F;
     c->sub_x.ensure(static_cast<size_t>(F) * c->d * sizeof(float));
     c->sub_i.ensure(static_cast<size_t>(F) * (3 * sizeof(int32_t) + sizeof(int2)) + 64);
     int2* sub_pairs = c->sub_i.as<int2>();
@@ -1270,6 +1272,7 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     FSIL_LAUNCHED(c);
     return;
   }
+  c->tc_mmas = 3;
   // K <= 24 at BN = 32: the epilogue scans only the first 16 / 24 columns
   const int kc_scan = bn == 32 && c->k <= 16 ? 16 : bn == 32 && c->k <= 24 ? 24 : 32;
   if (cos) {
