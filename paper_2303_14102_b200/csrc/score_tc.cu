@@ -913,7 +913,7 @@ __device__ __forceinline__ int scale_exp(float m) { return m > 0.f ? ilogbf(m) -
 __global__ void prep_b_kernel(const double* __restrict__ stats, const float* __restrict__ bound,
                               const float* __restrict__ xmax, int k, int d, int kp, int dp, bool cos,
                               __half* bh, __half* bl, float* colbias, __half* munorm,
-                              TcScale* scale, const int* abort, bool unit_ok) {
+                              TcScale* scale, const int* abort, bool unit_ok, float* lmnorm, float* lmmax) {
   griddep_wait();
   if (*abort) return;
   const int c = blockIdx.x;
@@ -940,6 +940,7 @@ __global__ void prep_b_kernel(const double* __restrict__ stats, const float* __r
   }
   const double n = c < k ? fmax(stats[c], 1.0) : 1.0;
   const double* sums = stats + (cos ? k : 2 * k) + static_cast<int64_t>(c) * d;
+  double lm2 = 0.0;  // ||mu~ - hm||^2: what a hm-only product leaves out (scaled units)
   for (int l = threadIdx.x; l < dp; l += blockDim.x) {
     float h = 0.f, lo = 0.f;
     if (c < k && l < d) {
@@ -947,11 +948,16 @@ __global__ void prep_b_kernel(const double* __restrict__ stats, const float* __r
       const __half hh = __double2half(mu);
       h = __half2float(hh);
       lo = static_cast<float>(mu - static_cast<double>(h));
+      const double rem = mu - static_cast<double>(h);
+      lm2 = fma(rem, rem, lm2);
     }
     bh[static_cast<int64_t>(c) * dp + l] = __float2half_rn(h);
     bl[static_cast<int64_t>(c) * dp + l] = __float2half_rn(lo);
   }
   __shared__ double red[4];
+  __shared__ double red2[4];
+  for (int off = 16; off > 0; off >>= 1) lm2 += __shfl_xor_sync(0xffffffffu, lm2, off);
+  if ((threadIdx.x & 31) == 0) red2[threadIdx.x >> 5] = lm2;
   double sq = 0.0;
   if (c < k)
     for (int l = threadIdx.x; l < d; l += blockDim.x) {
@@ -966,6 +972,11 @@ __global__ void prep_b_kernel(const double* __restrict__ stats, const float* __r
     const double nrm = sqrt(red[0] + red[1] + red[2] + red[3]) * (1.0 + 1e-12);
     // bound[0] = max ||mu_k|| rounded up, so the ratio is <= 1; every rounding upward
     munorm[c] = __float2half_ru(__double2float_ru(__ddiv_ru(nrm, fmax(static_cast<double>(bound[0]), 1e-300))));
+    // ||mu - hm|| in mu units, rounded up (0 for padding columns)
+    const double lmn = sqrt(red2[0] + red2[1] + red2[2] + red2[3]) * (1.0 + 1e-9) / static_cast<double>(smu);
+    const float lmf = c < k ? __double2float_ru(lmn) : 0.0f;
+    lmnorm[c] = lmf;
+    atomicMax(reinterpret_cast<int*>(lmmax), __float_as_int(lmf));  // non-negative floats order as ints
   }
 }
 
@@ -1082,12 +1093,15 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     if (pair) ncb = (c->k + 255) / 256 * 2;
   }
   const int kp = ncb * bn;
-  c->tc_b.ensure(2ull * kp * dp * sizeof(__half) + kp * (sizeof(float) + sizeof(__half)) + sizeof(TcScale) + 64);
+  c->tc_b.ensure(2ull * kp * dp * sizeof(__half) + kp * (2 * sizeof(float) + sizeof(__half)) + sizeof(TcScale) + 96);
   __half* bh = c->tc_b.as<__half>();
   __half* bl = bh + static_cast<size_t>(kp) * dp;
   float* colbias = reinterpret_cast<float*>(bl + static_cast<size_t>(kp) * dp);
-  __half* munorm = reinterpret_cast<__half*>(colbias + kp);
+  float* lmnorm = colbias + kp;  // ||mu_k - hm_k|| (mu units, rounded up): the one-MMA level's bound
+  __half* munorm = reinterpret_cast<__half*>(lmnorm + kp);
   TcScale* scale = reinterpret_cast<TcScale*>((reinterpret_cast<uintptr_t>(munorm + kp) + 31) & ~uintptr_t(31));
+  float* lmmax = reinterpret_cast<float*>(scale + 1);  // max_k lmnorm (atomic max in prep_b)
+  FSIL_CUDA(cudaMemsetAsync(lmmax, 0, sizeof(float), c->stream));
   TcParams tp{};
   tp.p = p;
   tp.ncb = ncb;
@@ -1128,7 +1142,9 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   // three-group kernel); its subnormal floor is bounded per row (floor_x / ||x||)
   const bool unit_ok = eg3;
   launch_pdl(c, prep_b_kernel, kp, 128, 0, p.stats, c->bound.as<float>(), c->xmax.as<float>(), c->k, c->d, kp, dp,
-             cos, bh, bl, colbias, munorm, scale, p.abort, unit_ok);
+             cos, bh, bl, colbias, munorm, scale, p.abort, unit_ok, lmnorm, lmmax);
+  tp.lmnorm = lmnorm;
+  tp.lmmax = lmmax;
   const CUtensorMap mx = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, c->X, c->d, c->n, c->d * 4ull, 32, BM);
   const CUtensorMap mh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, bh, dp, kp, dp * 2ull, BK, bn);
   const CUtensorMap ml = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, bl, dp, kp, dp * 2ull, BK, bn);
@@ -1203,18 +1219,23 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     // Two-level certificate (default): level 1 is the two-MMA pass (hx.hm + hx.lm, the
     // dropped lx.hm bounded per row by ||lx|| ||mu_k||); level 2 re-scores its uncertain rows
     // with the three-MMA kernel below.  FSIL_TC_TWO=0: one three-MMA pair pass.
-    static const bool two_env = [] {
-      const char* e = std::getenv("FSIL_TC_TWO");
-      return !e || std::atoi(e) != 0;
+    // FSIL_TC_L1 = 1 (default: one MMA per K step, hx.hm), 2 (hx.hm + hx.lm) or 3 (one
+    // three-MMA pass, no second level; FSIL_TC_TWO=0 is the same)
+    static const int l1_env = [] {
+      const char* e = std::getenv("FSIL_TC_L1");
+      const char* t = std::getenv("FSIL_TC_TWO");
+      if (t && std::atoi(t) == 0) return 3;
+      return e ? std::max(1, std::min(3, std::atoi(e))) : 1;
     }();
-    const bool two = two_env && !c->X64;
+    const int l1 = c->X64 ? 3 : l1_env;
+    const bool two = l1 < 3;
     TcParams tpp = tp;
     tpp.split = 0;
-    tpp.cdot = 1.05f * (12.0f + 2.0f * kMmaUlp * (two ? 2.0f : 3.0f) * steps + 1.0f) * u;
+    tpp.cdot = 1.05f * (12.0f + 2.0f * kMmaUlp * static_cast<float>(l1) * steps + 1.0f) * u;
     if (c->X64) tpp.cdot += 1.01f * u;
     const bool t3p = t3_env && static_cast<int64_t>(c->k) * c->d >= 64 * 1024;
-    launch_tc_pair(c, mx, mh, ml, tpp, ntiles, cos, t3p, two);
-    c->tc_mmas = two ? 2 : 3;
+    launch_tc_pair(c, mx, mh, ml, tpp, ntiles, cos, t3p, l1);
+    c->tc_mmas = l1;
     if (!two) return;
     // ---- level 2
     unsigned long long nf = 0;

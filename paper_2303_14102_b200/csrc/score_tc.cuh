@@ -52,6 +52,8 @@ struct TcParams {
   int lean;               // converters only convert; the epilogue fetches own/||x||^2 itself
   int2* pair_rows;        // T3: rows whose neighbour is one of {nb, .y} (certified pair)
   unsigned long long* pair_count;
+  const float* lmnorm;    // [ncb*BN] ||mu_k - hm_k|| (mu units, rounded up): one-MMA level bound
+  const float* lmmax;     // max_k lmnorm
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) {
@@ -71,7 +73,8 @@ template <bool COS, bool T3>
 __device__ __forceinline__ bool certify_row(const TcParams& tp, const TcScale& sc, int64_t row, int own,
                                             float xi, float xn, float rnf, float b1, float b2, float b3,
                                             int arg, int arg2, float mu_arg_ratio, float mu_arg2_ratio = 1.0f,
-                                            float x_rel = -1.0f) {
+                                            float x_rel = -1.0f, float lm_arg = 0.0f, float lm_arg2 = 0.0f,
+                                            float lm_any = 0.0f) {
   const float u = 5.9604645e-8f;
   const float rowc = COS ? 1.0f : xi;
   const float exi = tp.exic * u * xi;  // ||x||^2 error (fp32 blocks of 8; fp64 input rounding)
@@ -82,13 +85,16 @@ __device__ __forceinline__ bool certify_row(const TcParams& tp, const TcScale& s
   // key error: the dot bound (per unit ||x|| for cosine); the key's own roundings
   // (cosine: rsqrt 2.2u + product 0.5u + fma 0.5u on |m| <= 1, within 4u(|b1|+1));
   // the ||x||^2 error
-  const float eps_dot1 = cmu * sc.mu_max + sc.floor_mu;  // any column, per unit ||x||
+  // one-MMA level (lm_* > 0): the dropped hx.lm piece, ||hx|| ||mu_k - hm_k||, ||hx|| <=
+  // (1 + x_rel) ||x~||, per column (the winner, the runner-up) or its maximum (any column)
+  const float lmf = 1.0f + fmaxf(x_rel, 0.0f);
+  const float eps_dot1 = cmu * sc.mu_max + sc.floor_mu + lmf * lm_any;  // any column, per unit ||x||
   const float eps_m = COS ? (eps_dot1 + 4.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u)
                           : (2.0f * eps_dot1 * xn + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
   // the winner's key error uses its own cluster norm (the runner-up's column is
   // not tracked: any-column bound eps_m)
   const float mu_arg = mu_arg_ratio * sc.mu_max;
-  const float eps_dot1_arg = cmu * mu_arg + sc.floor_mu;
+  const float eps_dot1_arg = cmu * mu_arg + sc.floor_mu + lmf * lm_arg;
   const float eps_m_arg = COS ? (eps_dot1_arg + 4.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u)
                               : (2.0f * eps_dot1_arg * xn + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
   // neighbour certain: clear gap, and no tie through the clamps at 0 (and 2).  With the
@@ -96,7 +102,7 @@ __device__ __forceinline__ bool certify_row(const TcParams& tp, const TcScale& s
   // behind b3 with the any-column bound: certain when min(b2 - e2, b3 - e_any) > b1 + e_arg.
   bool gap_ok = (b2 - b1) > eps_m + eps_m_arg && rowc + b2 > eps_m;
   if (T3 && arg2 >= 0) {
-    const float eps_dot1_2 = cmu * (mu_arg2_ratio * sc.mu_max) + sc.floor_mu;
+    const float eps_dot1_2 = cmu * (mu_arg2_ratio * sc.mu_max) + sc.floor_mu + lmf * lm_arg2;
     const float eps_m_2 = COS ? (eps_dot1_2 + 4.0f * u * (fabsf(b1) + 1.0f) + tp.exic * u)
                               : (2.0f * eps_dot1_2 * xn + 3.0f * u * (fabsf(b1) + sc.p_max + 2.0f * xn * sc.mu_max) + exi);
     gap_ok = gap_ok || (fminf(b2 - eps_m_2, b3 - eps_m) > b1 + eps_m_arg && rowc + b2 > eps_m_2 && rowc + b3 > eps_m);
@@ -126,7 +132,7 @@ CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* ptr, uint64_t inner,
 // MMA block, for streaming cluster tables.  Returns false when it does not apply.
 bool pair_supported(const fsil_context* c, const TcParams& tp, int bn);
 void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
-                    TcParams tp, int64_t ntiles, bool cos, bool t3, bool two);
+                    TcParams tp, int64_t ntiles, bool cos, bool t3, int l1);
 
 }  // namespace tc
 }  // namespace fsil

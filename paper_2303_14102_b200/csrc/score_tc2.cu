@@ -194,11 +194,14 @@ struct PairSmem {
 // (the x pieces' low half dropped; its contribution is bounded per row by ||lx|| ||mu_k||,
 // lx = x~ - hx exact in fp32), A operands of 16 KB per chunk.  Rows it cannot certify are
 // re-scored at three-MMA precision (score_tc.cu, level 2).
-template <bool COS, bool T3, bool TWO>
+// L1 = 1: the first level is a single MMA per K step, hx.hm: the dropped hx.lm is bounded per
+// column by ||hx|| ||mu_k - hm_k|| (prep_b's lmnorm table), and only hm is loaded for B.
+template <bool COS, bool T3, int L1>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_pair_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
                          const __grid_constant__ CUtensorMap tmap_bl, const __grid_constant__ CUtensorMap tmap_scr,
                          TcParams tp, int64_t ntiles, int ns, int nb) {
+  constexpr bool TWO = L1 < 3;  // a first level of the two-level certificate (x lo dropped)
   griddep_wait();           // (PDL) prep_b's operands and every earlier phase are visible
   if (*tp.p.abort) return;  // K speculation missed: the call is repeated (both CTAs return)
   const ScoreParams& p = tp.p;
@@ -310,10 +313,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint8_t* bs = bring + sb * 2 * kBPiece;
             PW(6, mbar_wait_cluster(b_empty + sb, ((n2 / nb) & 1) ^ 1));
             const uint32_t bf = mapa_u32(smem_u32(b_full + sb), 0);
-            if (leader) mbar_arrive_expect_tx_cluster(bf, 4 * kBPiece);
+            if (leader) mbar_arrive_expect_tx_cluster(bf, (L1 == 1 ? 2 : 4) * kBPiece);
             const int col = cb * kPairN + static_cast<int>(rank) * kHalfN;
             tma_load_2d_pair_hint(bs, &tmap_bh, bf, kc * BK, col, pol_b);
-            tma_load_2d_pair_hint(bs + kBPiece, &tmap_bl, bf, kc * BK, col, pol_b);
+            if (L1 > 1) tma_load_2d_pair_hint(bs + kBPiece, &tmap_bl, bf, kc * BK, col, pol_b);
           }
         }
       }
@@ -338,8 +341,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int ks = 0; ks < nks; ++ks) {
               const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
               mma_f16_pair(d, dah + 2 * ks, dbh + 2 * ks, kIdesc, acc0);
-              mma_f16_pair(d, dah + 2 * ks, dbl + 2 * ks, kIdesc, 1u);
-              if (!TWO) mma_f16_pair(d, dal + 2 * ks, dbh + 2 * ks, kIdesc, 1u);
+              if (L1 > 1) mma_f16_pair(d, dah + 2 * ks, dbl + 2 * ks, kIdesc, 1u);
+              if (L1 > 2) mma_f16_pair(d, dal + 2 * ks, dbh + 2 * ks, kIdesc, 1u);
             }
             mma_commit_pair(b_empty + sb, 0x3);
             mma_commit_pair(stg_empty + s1, 0x3);
@@ -559,7 +562,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (valid)
         certify_row<COS, T3>(tp, sc, row, own, xi, xn, rnf, b1, b2, b3, arg, arg2,
                                        arg >= 0 ? __half2float(__ldg(tp.munorm + arg)) : 1.0f,
-                                       arg2 >= 0 ? __half2float(__ldg(tp.munorm + arg2)) : 1.0f, lx_rel);
+                                       arg2 >= 0 ? __half2float(__ldg(tp.munorm + arg2)) : 1.0f, lx_rel,
+                                       L1 == 1 && arg >= 0 ? __ldg(tp.lmnorm + arg) : 0.0f,
+                                       L1 == 1 && arg2 >= 0 ? __ldg(tp.lmnorm + arg2) : 0.0f,
+                                       L1 == 1 ? __ldg(tp.lmmax) : 0.0f);
     }
   }
 
@@ -583,7 +589,8 @@ bool pair_supported(const fsil_context* c, const TcParams& tp, int bn) {
 }
 
 void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
-                    TcParams tp, int64_t ntiles, bool cos, bool t3, bool two) {
+                    TcParams tp, int64_t ntiles, bool cos, bool t3, int l1) {
+  const bool two = l1 < 3;
   // stages: X/A and B rings of 32 KB each; 3 + 3 at 227 KB.  Measured (C5, 4M rows):
   // 3 + 3 59.1 ms, 4 + 2 62.1 ms, 3 + 2 64.5 ms -- the issuer's A waits shrink with more
   // A stages but its B waits grow faster
@@ -606,10 +613,10 @@ void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& m
                                        static_cast<uint64_t>(grid) * tp.nkc * BM, 256, 128, two ? BM / 2 : BM,
                                        CU_TENSOR_MAP_SWIZZLE_NONE);
   const size_t smem = PairSmem::bytes(ns, nb);
-  auto kern = two ? (cos ? (t3 ? score_tc_pair_kernel<true, true, true> : score_tc_pair_kernel<true, false, true>)
-                        : (t3 ? score_tc_pair_kernel<false, true, true> : score_tc_pair_kernel<false, false, true>))
-                  : (cos ? (t3 ? score_tc_pair_kernel<true, true, false> : score_tc_pair_kernel<true, false, false>)
-                         : (t3 ? score_tc_pair_kernel<false, true, false> : score_tc_pair_kernel<false, false, false>));
+#define FSIL_PAIR_K(L) (cos ? (t3 ? score_tc_pair_kernel<true, true, L> : score_tc_pair_kernel<true, false, L>) \
+                           : (t3 ? score_tc_pair_kernel<false, true, L> : score_tc_pair_kernel<false, false, L>))
+  auto kern = l1 == 1 ? FSIL_PAIR_K(1) : l1 == 2 ? FSIL_PAIR_K(2) : FSIL_PAIR_K(3);
+#undef FSIL_PAIR_K
   FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   if (c->timing) {  // the kernel alone, for the roofline (ms_score_kernel)
     FSIL_CUDA(cudaEventRecord(c->ev[7], c->stream));
