@@ -331,7 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t d = tmem_base + ab * kPairN;
           for (int kc = 0; kc < nkc; ++kc, ++n2, ++ia) {
             const int s1 = static_cast<int>(ia % ns), sb = static_cast<int>(n2 % nb);
-            PW(1, mbar_wait_cluster(a_full + s1, (ia / ns) & 1));
+            if (cb == 0) PW(10, mbar_wait_cluster(a_full + s1, (ia / ns) & 1));  // converted in this pass
+            else PW(1, mbar_wait_cluster(a_full + s1, (ia / ns) & 1));           // reloaded from scratch
             PW(2, mbar_wait_cluster(b_full + sb, (n2 / nb) & 1));
             tc_fence_after();
             const int rem = p.d - kc * BK;
@@ -649,11 +650,13 @@ void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& m
     unsigned long long h[16];
     FSIL_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     FSIL_CUDA(cudaStreamSynchronize(c->stream));
-    const char* names[10] = {"mma acc_empty", "mma a_full", "mma b_full", "mma total", "X stg_empty",
-                             "X scr_ready", "B b_empty", "epi acc_full", "epi meta_full", "conv stg_full"};
+    const char* names[11] = {"mma acc_empty", "mma a_full(reload)", "mma b_full", "mma total", "X stg_empty",
+                             "X scr_ready", "B b_empty", "epi acc_full", "epi meta_full", "conv stg_full",
+                             "mma a_full(pass0)"};
     const double pairs = static_cast<double>(grid / 2), ctas = static_cast<double>(grid);
     std::fprintf(stderr, "[fsil tc pair profile] ns=%d nb=%d Mcycles per CTA (MMA rows: per pair):", ns, nb);
-    for (int i = 0; i < 10; ++i) std::fprintf(stderr, " %s=%.3f", names[i], h[i] / (i < 4 ? pairs : ctas) / 1e6);
+    for (int i = 0; i < 11; ++i)
+      std::fprintf(stderr, " %s=%.3f", names[i], h[i] / (i < 4 || i == 10 ? pairs : ctas) / 1e6);
     std::fprintf(stderr, "\n");
     cudaFree(dbg);
   }
