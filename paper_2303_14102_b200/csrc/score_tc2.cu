@@ -202,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                          const __grid_constant__ CUtensorMap tmap_bl, const __grid_constant__ CUtensorMap tmap_scr,
                          TcParams tp, int64_t ntiles, int ns, int nb) {
   constexpr bool TWO = L1 < 3;  // a first level of the two-level certificate (x lo dropped)
+  constexpr int BCH = L1 == 1 ? 2 : 1;  // K chunks per B stage (hm only: two fit a stage)
   griddep_wait();           // (PDL) prep_b's operands and every earlier phase are visible
   if (*tp.p.abort) return;  // K speculation missed: the call is repeated (both CTAs return)
   const ScoreParams& p = tp.p;
@@ -308,45 +309,68 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_b = l2_policy_evict_last();
       for (int64_t st = cid; st < nst; st += ncl) {
         for (int cb = 0; cb < ncb; ++cb) {
-          for (int kc = 0; kc < nkc; ++kc, ++n2) {
+          for (int kc = 0; kc < nkc; kc += BCH, ++n2) {
             const int sb = static_cast<int>(n2 % nb);
             uint8_t* bs = bring + sb * 2 * kBPiece;
             PW(6, mbar_wait_cluster(b_empty + sb, ((n2 / nb) & 1) ^ 1));
             const uint32_t bf = mapa_u32(smem_u32(b_full + sb), 0);
-            if (leader) mbar_arrive_expect_tx_cluster(bf, (L1 == 1 ? 2 : 4) * kBPiece);
             const int col = cb * kPairN + static_cast<int>(rank) * kHalfN;
-            tma_load_2d_pair_hint(bs, &tmap_bh, bf, kc * BK, col, pol_b);
-            if (L1 > 1) tma_load_2d_pair_hint(bs + kBPiece, &tmap_bl, bf, kc * BK, col, pol_b);
+            if (L1 == 1) {  // hm of two consecutive chunks per stage (B lookahead doubles)
+              const int nch = min(2, nkc - kc);
+              if (leader) mbar_arrive_expect_tx_cluster(bf, nch * 2 * kBPiece);
+              for (int h = 0; h < nch; ++h)
+                tma_load_2d_pair_hint(bs + h * kBPiece, &tmap_bh, bf, (kc + h) * BK, col, pol_b);
+            } else {
+              if (leader) mbar_arrive_expect_tx_cluster(bf, 4 * kBPiece);
+              tma_load_2d_pair_hint(bs, &tmap_bh, bf, kc * BK, col, pol_b);
+              tma_load_2d_pair_hint(bs + kBPiece, &tmap_bl, bf, kc * BK, col, pol_b);
+            }
           }
         }
       }
     } else if (warp == 1 && lane == 0 && leader) {
       // ------------------------------------------------------------ MMA issuer (the pair's)
-      uint32_t n2 = 0, ia = 0, na = 0;
+      uint32_t na = 0;
+      // ring positions advance incrementally (no runtime division on the issue path)
+      int s1 = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
       for (int64_t st = cid; st < nst; st += ncl) {
         for (int cb = 0; cb < ncb; ++cb, ++na) {
           const int ab = static_cast<int>(na & 1);
           PW(0, mbar_wait_cluster(acc_empty + ab, ((na >> 1) & 1) ^ 1));
           tc_fence_after();
           const uint32_t d = tmem_base + ab * kPairN;
-          for (int kc = 0; kc < nkc; ++kc, ++n2, ++ia) {
-            const int s1 = static_cast<int>(ia % ns), sb = static_cast<int>(n2 % nb);
-            if (cb == 0) PW(10, mbar_wait_cluster(a_full + s1, (ia / ns) & 1));  // converted in this pass
-            else PW(1, mbar_wait_cluster(a_full + s1, (ia / ns) & 1));           // reloaded from scratch
-            PW(2, mbar_wait_cluster(b_full + sb, (n2 / nb) & 1));
+          for (int kc = 0; kc < nkc; ++kc) {
+            // cluster-scope acquire only where the peer's converters wrote shared memory with
+            // generic stores (the converted pass); the tensor copies' completions (reloads, B)
+            // make their bytes visible to the async proxy through the barrier itself
+            if (cb == 0) PW(10, mbar_wait_cluster(a_full + s1, pa));
+            else PW(1, mbar_wait(a_full + s1, pa));
+            const int bh = BCH == 2 ? (kc & 1) : 0;  // chunk's half of the B stage
+            if (bh == 0) PW(2, mbar_wait(b_full + sb, pb));
             tc_fence_after();
             const int rem = p.d - kc * BK;
             const int nks = rem >= BK ? 4 : (rem + 15) / 16;
             const uint64_t dah = desc_k_sw128(smem_u32(stg + s1 * kStgBytes)), dal = dah + (kABytes >> 4);
-            const uint64_t dbh = desc_k_sw128(smem_u32(bring + sb * 2 * kBPiece)), dbl = dbh + (kBPiece >> 4);
+            const uint64_t dbh = desc_k_sw128(smem_u32(bring + sb * 2 * kBPiece + bh * kBPiece)),
+                           dbl = dbh + (kBPiece >> 4);
             for (int ks = 0; ks < nks; ++ks) {
               const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
               mma_f16_pair(d, dah + 2 * ks, dbh + 2 * ks, kIdesc, acc0);
               if (L1 > 1) mma_f16_pair(d, dah + 2 * ks, dbl + 2 * ks, kIdesc, 1u);
               if (L1 > 2) mma_f16_pair(d, dal + 2 * ks, dbh + 2 * ks, kIdesc, 1u);
             }
-            mma_commit_pair(b_empty + sb, 0x3);
+            const bool b_done = BCH == 1 || bh == 1 || kc + 1 == nkc;  // the stage's last chunk
+            if (b_done) mma_commit_pair(b_empty + sb, 0x3);
             mma_commit_pair(stg_empty + s1, 0x3);
+            if (++s1 == ns) {
+              s1 = 0;
+              pa ^= 1u;
+            }
+            if (b_done && ++sb == nb) {
+              sb = 0;
+              pb ^= 1u;
+            }
           }
           mma_commit_pair(acc_full + ab, 0x3);
         }
