@@ -74,9 +74,16 @@ __device__ __forceinline__ void cluster_sync_all() {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(caddr) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t caddr, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;\n" ::"r"(caddr),
-               "r"(bytes)
+// tx bytes expected on a local barrier without arriving (the leader's reload items)
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// `count` arrivals at once on a local barrier (the leader arrives for both CTAs of the pair
+// on reload items: neither CTA wrote the stage with generic stores, so the peer's arrival
+// would publish nothing and its cluster-scope release fence is pure latency)
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
                : "memory");
 }
 // wait with cluster-scope acquire: the phase may have been completed by the peer CTA
@@ -288,11 +295,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             PW(4, mbar_wait_cluster(stg_empty + s1, ((n1 / ns) & 1) ^ 1));  // (multicast commit)
             if (xp > 0) {
               const uint32_t af = mapa_u32(smem_u32(a_full + s1), 0);
-              if (leader) mbar_arrive_expect_tx_cluster(af, 2 * (TWO ? kABytes : kStgBytes));
+              if (leader) mbar_expect_tx(a_full + s1, 2 * (TWO ? kABytes : kStgBytes));
               // (TWO: the map's box is the 16 KB hx piece at the start of each 32 KB chunk)
               tma_load_2d_pair_hint(stg + s1 * kStgBytes, &tmap_scr, af, 0, static_cast<int>((sbase + kc) * BM),
                                     pol_keep);
-              if (!leader) mbar_arrive_cluster(af);
+              if (leader) mbar_arrive_cnt(a_full + s1, 2);
               continue;
             }
             const int nbox = (kc * BK + 32 < p.d) ? 2 : 1;
@@ -317,11 +324,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int col = cb * kPairN + static_cast<int>(rank) * kHalfN;
             if (L1 == 1) {  // hm of two consecutive chunks per stage (B lookahead doubles)
               const int nch = min(2, nkc - kc);
-              if (leader) mbar_arrive_expect_tx_cluster(bf, nch * 2 * kBPiece);
+              if (leader) mbar_arrive_expect_tx(b_full + sb, nch * 2 * kBPiece);
               for (int h = 0; h < nch; ++h)
                 tma_load_2d_pair_hint(bs + h * kBPiece, &tmap_bh, bf, (kc + h) * BK, col, pol_b);
             } else {
-              if (leader) mbar_arrive_expect_tx_cluster(bf, 4 * kBPiece);
+              if (leader) mbar_arrive_expect_tx(b_full + sb, 4 * kBPiece);
               tma_load_2d_pair_hint(bs, &tmap_bh, bf, kc * BK, col, pol_b);
               tma_load_2d_pair_hint(bs + kBPiece, &tmap_bl, bf, kc * BK, col, pol_b);
             }
