@@ -45,6 +45,7 @@ constexpr int kHalfN = 128;                // B columns held by each CTA
 constexpr int kBPiece = kHalfN * 128;      // one B piece (hi or lo) per stage per CTA: 16 KB
 constexpr uint32_t kPairCols = 512;        // TMEM columns: two 256-column accumulators
 constexpr int kEpi0 = 4, kConv0 = 12;
+constexpr int kScanG = 4;  // epilogue filter group (keys)
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -73,6 +74,12 @@ __device__ __forceinline__ void cluster_sync_all() {
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(caddr) : "memory");
+}
+// arrival on a barrier of another CTA of the cluster without a cluster-scope release: for
+// signals that publish no memory (the epilogue's TMEM reads have completed -- tcgen05.wait::ld
+// -- before it frees the accumulator), the release fence would only add latency
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(caddr) : "memory");
 }
 // tx bytes expected on a local barrier without arriving (the leader's reload items)
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -184,6 +191,13 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// one lane of a converged warp (the issuing lane of a warp-wide loop)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
@@ -210,6 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                          TcParams tp, int64_t ntiles, int ns, int nb) {
   constexpr bool TWO = L1 < 3;  // a first level of the two-level certificate (x lo dropped)
   constexpr int BCH = L1 == 1 ? 2 : 1;  // K chunks per B stage (hm only: two fit a stage)
+  constexpr int ACH = TWO ? 2 : 1;      // K chunks per reloaded A stage (hx only: two fit a stage)
   griddep_wait();           // (PDL) prep_b's operands and every earlier phase are visible
   if (*tp.p.abort) return;  // K speculation missed: the call is repeated (both CTAs return)
   const ScoreParams& p = tp.p;
@@ -290,15 +305,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             PW(5, mbar_wait(scr_ready, ntl & 1));
             fence_proxy_async_global();
           }
-          for (int kc = 0; kc < nkc; ++kc, ++n1) {
+          for (int kc = 0; kc < nkc; kc += (xp > 0 ? ACH : 1), ++n1) {
             const int s1 = static_cast<int>(n1 % ns);
-            PW(4, mbar_wait_cluster(stg_empty + s1, ((n1 / ns) & 1) ^ 1));  // (multicast commit)
+            PW(4, mbar_wait(stg_empty + s1, ((n1 / ns) & 1) ^ 1));  // (multicast MMA commit)
             if (xp > 0) {
+              // a reload item: ACH chunks' A pieces side by side in one stage
               const uint32_t af = mapa_u32(smem_u32(a_full + s1), 0);
-              if (leader) mbar_expect_tx(a_full + s1, 2 * (TWO ? kABytes : kStgBytes));
+              const int nch = min(ACH, nkc - kc);
+              if (leader) mbar_expect_tx(a_full + s1, 2 * nch * (TWO ? kABytes : kStgBytes));
               // (TWO: the map's box is the 16 KB hx piece at the start of each 32 KB chunk)
-              tma_load_2d_pair_hint(stg + s1 * kStgBytes, &tmap_scr, af, 0, static_cast<int>((sbase + kc) * BM),
-                                    pol_keep);
+              for (int h = 0; h < nch; ++h)
+                tma_load_2d_pair_hint(stg + s1 * kStgBytes + h * kABytes, &tmap_scr, af, 0,
+                                      static_cast<int>((sbase + kc + h) * BM), pol_keep);
               if (leader) mbar_arrive_cnt(a_full + s1, 2);
               continue;
             }
@@ -319,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kc = 0; kc < nkc; kc += BCH, ++n2) {
             const int sb = static_cast<int>(n2 % nb);
             uint8_t* bs = bring + sb * 2 * kBPiece;
-            PW(6, mbar_wait_cluster(b_empty + sb, ((n2 / nb) & 1) ^ 1));
+            PW(6, mbar_wait(b_empty + sb, ((n2 / nb) & 1) ^ 1));
             const uint32_t bf = mapa_u32(smem_u32(b_full + sb), 0);
             const int col = cb * kPairN + static_cast<int>(rank) * kHalfN;
             if (L1 == 1) {  // hm of two consecutive chunks per stage (B lookahead doubles)
@@ -335,51 +353,118 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-    } else if (warp == 1 && lane == 0 && leader) {
+    } else if (warp == 1 && leader) {
       // ------------------------------------------------------------ MMA issuer (the pair's)
+      // The whole warp runs the loop (every value on it warp-uniform, so descriptors live in
+      // uniform registers) and one elected lane issues: a single-thread loop paid a
+      // uniform-register waterfall per MMA and could not keep the tensor pipe fed.
+      unsigned long long* const dbg = lane == 0 ? tp.dbg : nullptr;
+      const bool nomma = tp.dbg && tp.dbg[15] != 0;  // FSIL_TC_PROFILE=2 diagnostic: the pipeline without MMAs
       uint32_t na = 0;
       // ring positions advance incrementally (no runtime division on the issue path)
       int s1 = 0, sb = 0;
       uint32_t pa = 0, pb = 0;
+      const int nkfull = p.d / BK;  // full 64-wide K chunks
+      const uint64_t da0 = desc_k_sw128(smem_u32(stg)), db0 = desc_k_sw128(smem_u32(bring));
       for (int64_t st = cid; st < nst; st += ncl) {
         for (int cb = 0; cb < ncb; ++cb, ++na) {
           const int ab = static_cast<int>(na & 1);
-          PW(0, mbar_wait_cluster(acc_empty + ab, ((na >> 1) & 1) ^ 1));
+          PW(0, mbar_wait(acc_empty + ab, ((na >> 1) & 1) ^ 1));
           tc_fence_after();
           const uint32_t d = tmem_base + ab * kPairN;
-          for (int kc = 0; kc < nkc; ++kc) {
+          const int ach = cb == 0 ? 1 : ACH;  // chunks per A item: converted pass 1, reloads ACH
+          const long long tcb0 = dbg ? clock64() : 0;
+          for (int kc0 = 0; kc0 < nkc; kc0 += ach) {
+            const long long tit0 = dbg ? clock64() : 0;
+            if (L1 == 1 && cb > 0 && kc0 + 2 <= nkfull) {
+              // the steady state: a reload item of two full chunks against the B stage of the
+              // same two chunks -- two waits, eight MMAs, two commits, straight-line
+              PW(1, mbar_wait(a_full + s1, pa));
+              PW(2, mbar_wait(b_full + sb, pb));
+              tc_fence_after();
+              if (elect_one()) {
+                const uint64_t da = da0 + static_cast<uint32_t>(s1 * (kStgBytes >> 4)),
+                               db = db0 + static_cast<uint32_t>(sb * (2 * kBPiece >> 4));
+                if (!nomma) {
+#pragma unroll
+                  for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                      mma_f16_pair(d, da + h * (kABytes >> 4) + 2 * ks, db + h * (kBPiece >> 4) + 2 * ks, kIdesc,
+                                   (h | ks | kc0) ? 1u : 0u);
+                }
+                mma_commit_pair(b_empty + sb, 0x3);
+                mma_commit_pair(stg_empty + s1, 0x3);
+              }
+              __syncwarp();
+              if (++sb == nb) {
+                sb = 0;
+                pb ^= 1u;
+              }
+              if (++s1 == ns) {
+                s1 = 0;
+                pa ^= 1u;
+              }
+              if (dbg) atomicAdd(dbg + 12, static_cast<unsigned long long>(clock64() - tit0));
+              continue;
+            }
             // cluster-scope acquire only where the peer's converters wrote shared memory with
             // generic stores (the converted pass); the tensor copies' completions (reloads, B)
             // make their bytes visible to the async proxy through the barrier itself
             if (cb == 0) PW(10, mbar_wait_cluster(a_full + s1, pa));
             else PW(1, mbar_wait(a_full + s1, pa));
-            const int bh = BCH == 2 ? (kc & 1) : 0;  // chunk's half of the B stage
-            if (bh == 0) PW(2, mbar_wait(b_full + sb, pb));
-            tc_fence_after();
-            const int rem = p.d - kc * BK;
-            const int nks = rem >= BK ? 4 : (rem + 15) / 16;
-            const uint64_t dah = desc_k_sw128(smem_u32(stg + s1 * kStgBytes)), dal = dah + (kABytes >> 4);
-            const uint64_t dbh = desc_k_sw128(smem_u32(bring + sb * 2 * kBPiece + bh * kBPiece)),
-                           dbl = dbh + (kBPiece >> 4);
-            for (int ks = 0; ks < nks; ++ks) {
-              const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
-              mma_f16_pair(d, dah + 2 * ks, dbh + 2 * ks, kIdesc, acc0);
-              if (L1 > 1) mma_f16_pair(d, dah + 2 * ks, dbl + 2 * ks, kIdesc, 1u);
-              if (L1 > 2) mma_f16_pair(d, dal + 2 * ks, dbh + 2 * ks, kIdesc, 1u);
+            const int nch = min(ach, nkc - kc0);
+            for (int h = 0; h < nch; ++h) {
+              const int kc = kc0 + h;
+              const int bh = BCH == 2 ? (kc & 1) : 0;  // chunk's half of the B stage
+              if (bh == 0) PW(2, mbar_wait(b_full + sb, pb));
+              tc_fence_after();
+              const int rem = p.d - kc * BK;
+              const int nks = rem >= BK ? 4 : (rem + 15) / 16;
+              const uint64_t dah = desc_k_sw128(smem_u32(stg + s1 * kStgBytes + h * kABytes)),
+                             dal = dah + (kABytes >> 4);
+              const uint64_t dbh = desc_k_sw128(smem_u32(bring + sb * 2 * kBPiece + bh * kBPiece)),
+                             dbl = dbh + (kBPiece >> 4);
+              const bool b_done = BCH == 1 || bh == 1 || kc + 1 == nkc;  // the B stage's last chunk
+              const bool a_done = h + 1 == nch;                          // the A item's last chunk
+              if (elect_one()) {
+                const long long ti0 = dbg ? clock64() : 0;
+                if (nomma) {
+                } else if (nks == 4) {
+#pragma unroll
+                  for (int ks = 0; ks < 4; ++ks) {
+                    const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
+                    mma_f16_pair(d, dah + 2 * ks, dbh + 2 * ks, kIdesc, acc0);
+                    if (L1 > 1) mma_f16_pair(d, dah + 2 * ks, dbl + 2 * ks, kIdesc, 1u);
+                    if (L1 > 2) mma_f16_pair(d, dal + 2 * ks, dbh + 2 * ks, kIdesc, 1u);
+                  }
+                } else {
+                  for (int ks = 0; ks < nks; ++ks) {
+                    const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
+                    mma_f16_pair(d, dah + 2 * ks, dbh + 2 * ks, kIdesc, acc0);
+                    if (L1 > 1) mma_f16_pair(d, dah + 2 * ks, dbl + 2 * ks, kIdesc, 1u);
+                    if (L1 > 2) mma_f16_pair(d, dal + 2 * ks, dbh + 2 * ks, kIdesc, 1u);
+                  }
+                }
+                if (b_done) mma_commit_pair(b_empty + sb, 0x3);
+                if (a_done) mma_commit_pair(stg_empty + s1, 0x3);
+                if (dbg) atomicAdd(dbg + 11, static_cast<unsigned long long>(clock64() - ti0));
+              }
+              __syncwarp();
+              if (b_done && ++sb == nb) {
+                sb = 0;
+                pb ^= 1u;
+              }
             }
-            const bool b_done = BCH == 1 || bh == 1 || kc + 1 == nkc;  // the stage's last chunk
-            if (b_done) mma_commit_pair(b_empty + sb, 0x3);
-            mma_commit_pair(stg_empty + s1, 0x3);
             if (++s1 == ns) {
               s1 = 0;
               pa ^= 1u;
             }
-            if (b_done && ++sb == nb) {
-              sb = 0;
-              pb ^= 1u;
-            }
+            if (dbg) atomicAdd(dbg + 12, static_cast<unsigned long long>(clock64() - tit0));
           }
-          mma_commit_pair(acc_full + ab, 0x3);
+          if (elect_one()) mma_commit_pair(acc_full + ab, 0x3);
+          __syncwarp();
+          if (dbg) atomicAdd(dbg + 13, static_cast<unsigned long long>(clock64() - tcb0));
         }
       }
       if (dbg) atomicAdd(dbg + 3, static_cast<unsigned long long>(clock64() - t_begin));
@@ -462,8 +547,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         bulk_wait_all();
         mbar_arrive(scr_ready);
       }
-      // the reload passes (ncb - 1 of nkc chunks each) go through the same stages
-      n1 += static_cast<uint32_t>((ncb - 1) * nkc);
+      // the reload passes (ncb - 1 of ceil(nkc / ACH) items each) go through the same stages
+      n1 += static_cast<uint32_t>((ncb - 1) * ((nkc + ACH - 1) / ACH));
       s1 = static_cast<int>(n1 % ns);
       // ||x||^2 halves and the own cluster to the epilogue
       const int tb = nt & 1;
@@ -502,39 +587,56 @@ __global__ void __launch_bounds__(kThreads, 1)
                                : -1.0f;
       float b1 = INFINITY, b2 = INFINITY, b3 = INFINITY;
       int arg = -1, arg2 = -1;
-      // one 32-column chunk: ranking keys (own column excluded), running top-2 / top-3
+      // one 32-column chunk: ranking keys (own column excluded), running top-2 / top-3.
+      // The ALU pipe (compares, selects, min/max: half rate) bounds this loop, so the chunk
+      // goes in groups of kScanG keys: the group's minimum against the running threshold
+      // (b3 -- b2 without T3) and the full update only when some row of the warp has a key
+      // below it.  Skipping is exact: a key >= the threshold changes none of b1..b3 / args.
       auto scan32 = [&](const uint32_t(&v)[32], int k0) {
         const int ownrel = own - k0;
         int argc = -1;
         const float4* cb4 = reinterpret_cast<const float4*>(tp.colbias + k0);
+        float bj[32];
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
           const float4 bias = __ldg(cb4 + j4);
-          const float bj[4] = {bias.x, bias.y, bias.z, bias.w};
+          bj[4 * j4] = bias.x;
+          bj[4 * j4 + 1] = bias.y;
+          bj[4 * j4 + 2] = bias.z;
+          bj[4 * j4 + 3] = bias.w;
+        }
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int j = 4 * j4 + e;
-            float m = fmaf(__uint_as_float(v[j]), rowm, bj[e]);
-            m = j == ownrel ? INFINITY : m;
-            const bool lt = m < b1;  // strict: the lowest index keeps ties
+        for (int g = 0; g < 32 / kScanG; ++g) {
+          float m[kScanG];
+#pragma unroll
+          for (int e = 0; e < kScanG; ++e) m[e] = fmaf(__uint_as_float(v[g * kScanG + e]), rowm, bj[g * kScanG + e]);
+          float gmin = m[0];
+#pragma unroll
+          for (int e = 1; e < kScanG; ++e) gmin = fminf(gmin, m[e]);
+          if (!__any_sync(0xffffffffu, gmin < (T3 ? b3 : b2))) continue;
+#pragma unroll
+          for (int e = 0; e < kScanG; ++e) {
+            const int j = g * kScanG + e;
+            const float mm = j == ownrel ? INFINITY : m[e];
+            const bool lt = mm < b1;  // strict: the lowest index keeps ties
             if (T3) {
-              const bool lt2 = m < b2;
+              const bool lt2 = mm < b2;
               arg2 = lt ? arg : (lt2 ? k0 + j : arg2);
               arg = lt ? k0 + j : arg;
-              b3 = fminf(b3, fmaxf(b2, m));
+              b3 = fminf(b3, fmaxf(b2, mm));
             } else {
               argc = lt ? j : argc;
             }
-            b2 = fminf(b2, fmaxf(b1, m));
-            b1 = fminf(b1, m);
+            b2 = fminf(b2, fmaxf(b1, mm));
+            b1 = fminf(b1, mm);
           }
         }
         if (!T3 && argc >= 0) arg = k0 + argc;
       };
       for (int cb = 0; cb < ncb; ++cb, ++na) {
         const int ab = static_cast<int>(na & 1);
-        if (threadIdx.x == 32 * kEpi0) PW(7, mbar_wait_cluster(acc_full + ab, (na >> 1) & 1));
-        else mbar_wait_cluster(acc_full + ab, (na >> 1) & 1);
+        if (threadIdx.x == 32 * kEpi0) PW(7, mbar_wait(acc_full + ab, (na >> 1) & 1));
+        else mbar_wait(acc_full + ab, (na >> 1) & 1);
         tc_fence_after();
         const uint32_t tb0 = tmem_base + ab * kPairN + (static_cast<uint32_t>(quad * 32) << 16);
 #pragma unroll 1
@@ -548,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(mapa_u32(smem_u32(acc_empty + ab), 0));
+        if (lane == 0) mbar_arrive_remote(mapa_u32(smem_u32(acc_empty + ab), 0));
       }
       // ---- merge the two column halves (group 1 -> smem -> group 0)
       float* pt = part + tb * 5 * BM;
@@ -673,6 +775,7 @@ void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& m
   if (prof) {
     FSIL_CUDA(cudaMalloc(&dbg, 16 * sizeof(unsigned long long)));
     FSIL_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), c->stream));
+    if (std::atoi(std::getenv("FSIL_TC_PROFILE")) == 2) FSIL_CUDA(cudaMemsetAsync(dbg + 15, 1, 1, c->stream));
   }
   tp.dbg = dbg;
   FSIL_CUDA(cudaLaunchKernelEx(&cfg, kern, mx, mh, ml, mscr, tp, ntiles, ns, nb));
@@ -681,13 +784,13 @@ void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& m
     unsigned long long h[16];
     FSIL_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     FSIL_CUDA(cudaStreamSynchronize(c->stream));
-    const char* names[11] = {"mma acc_empty", "mma a_full(reload)", "mma b_full", "mma total", "X stg_empty",
+    const char* names[14] = {"mma acc_empty", "mma a_full(reload)", "mma b_full", "mma total", "X stg_empty",
                              "X scr_ready", "B b_empty", "epi acc_full", "epi meta_full", "conv stg_full",
-                             "mma a_full(pass0)"};
+                             "mma a_full(pass0)", "mma issue", "mma items", "mma cbs"};
     const double pairs = static_cast<double>(grid / 2), ctas = static_cast<double>(grid);
     std::fprintf(stderr, "[fsil tc pair profile] ns=%d nb=%d Mcycles per CTA (MMA rows: per pair):", ns, nb);
-    for (int i = 0; i < 11; ++i)
-      std::fprintf(stderr, " %s=%.3f", names[i], h[i] / (i < 4 || i == 10 ? pairs : ctas) / 1e6);
+    for (int i = 0; i < 14; ++i)
+      std::fprintf(stderr, " %s=%.3f", names[i], h[i] / (i < 4 || i >= 10 ? pairs : ctas) / 1e6);
     std::fprintf(stderr, "\n");
     cudaFree(dbg);
   }
