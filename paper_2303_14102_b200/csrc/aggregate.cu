@@ -978,6 +978,16 @@ __global__ void __launch_bounds__(384) agg_piece_ring_kernel(
       for (int e = 0; e < 4; ++e) acc[q][e] = 0.0;
     double psi = 0.0, cnt = 0.0;
     float amax = 0.f;
+    // Cosine is software-pipelined by one row: row it's norm reduction across its lanes
+    // (five dependent shuffle steps, then a reciprocal square root) overlaps the
+    // accumulation of row it - 1, whose scale is known by then.  pv/pscale start at zero:
+    // the first step adds exact zeros.  The per-lane accumulation order is unchanged.
+    float pv[CPL][4];
+    double pscale = 0.0;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) pv[q][e] = 0.f;
     for (int it = 0; it < iters; ++it) {
       const int s = cs;
       sm100::mbar_wait(bars + s, cph);
@@ -1012,11 +1022,14 @@ __global__ void __launch_bounds__(384) agg_piece_ring_kernel(
         for (int e = 0; e < 4; ++e) {
           const double x = v[q][e];
           s4[e] = fma(x, x, s4[e]);
-          finite = finite && isfinite(v[q][e]);
+          if (!COS) finite = finite && isfinite(v[q][e]);
           amax = fmaxf(amax, fabsf(v[q][e]));
         }
       double ss = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-      if (!finite) {
+      // cosine: squares of finite floats cannot overflow fp64, so a non-finite lane sum
+      // flags the lane (one test per row instead of one per element)
+      if (COS) finite = isfinite(ss);
+      if (!COS && !finite) {
 #pragma unroll
         for (int q = 0; q < CPL; ++q)
 #pragma unroll
@@ -1025,26 +1038,46 @@ __global__ void __launch_bounds__(384) agg_piece_ring_kernel(
             if (l < d && !isfinite(v[q][e])) atomic_min_i64(checks, (row_offset + r) * d + l);
           }
       }
-      double scale = 1.0;
       if (COS) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[q][e] += static_cast<double>(pv[q][e]) * pscale;
         for (int off = lpr >> 1; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off, lpr);
-        if (valid && li == 0 && xi_out) xi_out[r] = ss;
-        if (!valid) continue;
-        if (ss == 0.0) {
-          if (li == 0) atomic_min_i64(checks + 1, row_offset + r);
-          continue;
+        const bool ok = valid && ss != 0.0;
+        pscale = ok ? 1.0 / sqrt(ss) : 0.0;
+        cnt += ok ? 1.0 : 0.0;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) pv[q][e] = v[q][e];
+        if (valid && li == 0) {
+          if (xi_out) xi_out[r] = ss;
+          if (ss == 0.0) atomic_min_i64(checks + 1, row_offset + r);
         }
-        scale = 1.0 / sqrt(ss);
-      } else {
-        if (!valid) continue;
+      } else if (valid) {
         psi += ss;
+        cnt += 1.0;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[q][e] += static_cast<double>(v[q][e]);
       }
-      cnt += 1.0;
+      if (COS && !finite) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int l = (li + q * lpr) * 4 + e;
+            if (l < d && !isfinite(v[q][e])) atomic_min_i64(checks, (row_offset + r) * d + l);
+          }
+      }
+    }
+    if (COS) {
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          acc[q][e] += COS ? static_cast<double>(v[q][e]) * scale : static_cast<double>(v[q][e]);
+        for (int e = 0; e < 4; ++e) acc[q][e] += static_cast<double>(pv[q][e]) * pscale;
     }
     for (int off = 16; off >= lpr; off >>= 1) {
 #pragma unroll

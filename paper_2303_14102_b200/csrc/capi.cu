@@ -460,7 +460,7 @@ void fsil_destroy(fsil_context* c) {
                           &c->piece_start, &c->mu32, &c->p32, &c->nk, &c->bound, &c->s_tmp,
                           &c->tile_sum, &c->tile_flag, &c->flag_rows, &c->flag_count, &c->result,
                           &c->group_sum, &c->xmax, &c->tc_b, &c->nb_tmp, &c->pair_rows, &c->pair_count, &c->a_scratch, &c->x32, &c->xbuf, &c->xt_keys, &c->xt_vals, &c->xt_dense, &c->hX, &c->hL, &c->o_s, &c->o_nb, &c->o_own, &c->o_a,
-                          &c->o_b};
+                          &c->o_b, &c->refine_part, &c->refine_cnt, &c->sub_x, &c->sub_i, &c->xi_rows};
   for (auto* b : bufs) b->release();
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);

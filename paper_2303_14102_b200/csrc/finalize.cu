@@ -121,20 +121,41 @@ __global__ void __launch_bounds__(256) refine_kernel(ScoreParams p) {
 // per 32 rows instead of once per row).  Thread (ty, tx) owns rows 2ty, 2ty+1 and
 // clusters tx + 16 j of each tile: ascending per thread, strict < -- then the 16
 // threads of a row merge with ties to the lowest k (the reference's rule).
+//
+// Few flagged rows (C5: ~1e2 of 1e7) would leave most of the grid idle, one block walking
+// all K clusters per 32 rows: the cluster range is then split into nsl slices (units =
+// row tiles x slices, nsl chosen on the device from the flagged count so the units cover
+// the grid).  A unit writes its rows' slice minimum (ties already at the lowest k); the
+// last unit of a row tile to finish (ticket) merges the slices in ascending order -- strict
+// <, so the lowest k keeps ties across slices too -- and finalises the rows.
 constexpr int kRT = 32, kCT = 64, kDC = 32;
+struct RefineSplit {
+  double* best;   // [row tiles * 32][nsl] slice minima (nsl > 1 only: < 2 * grid * 32 entries)
+  int* arg;
+  unsigned* cnt;  // [grid] per-row-tile tickets, zero between launches (the merger resets)
+};
 template <bool COS>
-__global__ void __launch_bounds__(256) refine_tiled_kernel(ScoreParams p) {
+__global__ void __launch_bounds__(256) refine_tiled_kernel(ScoreParams p, RefineSplit rs) {
   if (*p.abort) return;
   __shared__ double xs[kRT][kDC + 1];
   __shared__ double ys[kCT][kDC + 1];
   __shared__ double s_ss[kRT], s_co[kRT], s_best[kRT][17];
   __shared__ int s_arg[kRT][17], s_own[kRT];
   __shared__ int64_t s_row[kRT];
+  __shared__ bool s_last;
   const int64_t count = static_cast<int64_t>(*p.flag_count);
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4, lane = tid & 31, warp = tid >> 5;
   const double* sums = p.stats + (COS ? p.k : 2 * p.k);
   const int d = p.d, K = p.k;
-  for (int64_t t0 = static_cast<int64_t>(blockIdx.x) * kRT; t0 < count; t0 += static_cast<int64_t>(gridDim.x) * kRT) {
+  const int64_t rtiles = (count + kRT - 1) / kRT;
+  const int nct = (K + kCT - 1) / kCT;
+  const int nsl = rtiles >= static_cast<int64_t>(gridDim.x) ? 1 : static_cast<int>(min(static_cast<int64_t>(nct), (static_cast<int64_t>(gridDim.x) + rtiles - 1) / rtiles));
+  const int64_t nunits = rtiles * nsl;
+  for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+    const int64_t tile = u / nsl;
+    const int sl = static_cast<int>(u % nsl);
+    const int64_t t0 = tile * kRT;
+    const int c_lo = (sl * nct / nsl) * kCT, c_hi = min(K, ((sl + 1) * nct / nsl) * kCT);
     __syncthreads();
     if (tid < kRT) {
       const int64_t i = t0 + tid;
@@ -172,7 +193,7 @@ __global__ void __launch_bounds__(256) refine_tiled_kernel(ScoreParams p) {
     const int own0 = s_own[r0], own1 = s_own[r1];
     double best0 = INFINITY, best1 = INFINITY;
     int arg0 = -1, arg1 = -1;
-    for (int c0 = 0; c0 < K; c0 += kCT) {
+    for (int c0 = c_lo; c0 < c_hi; c0 += kCT) {
       double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
       for (int l0 = 0; l0 < d; l0 += kDC) {
         __syncthreads();
@@ -223,20 +244,47 @@ __global__ void __launch_bounds__(256) refine_tiled_kernel(ScoreParams p) {
     s_best[r1][tx] = best1;
     s_arg[r1][tx] = arg1;
     __syncthreads();
+    double best = INFINITY;
+    int arg = -1;
     if (tid < kRT) {
-      const int r = tid;
-      const int64_t row = s_row[r];
-      if (row >= 0) {
-        double best = INFINITY;
-        int arg = -1;
-        for (int j = 0; j < 16; ++j) {  // lowest k among equal minima
-          const double b = s_best[r][j];
-          const int a = s_arg[r][j];
-          if (a >= 0 && (arg < 0 || b < best || (b == best && a < arg))) {
+      for (int j = 0; j < 16; ++j) {  // lowest k among equal minima
+        const double b = s_best[tid][j];
+        const int a = s_arg[tid][j];
+        if (a >= 0 && (arg < 0 || b < best || (b == best && a < arg))) {
+          best = b;
+          arg = a;
+        }
+      }
+    }
+    if (nsl > 1) {
+      if (tid < kRT) {
+        rs.best[(t0 + tid) * nsl + sl] = best;
+        rs.arg[(t0 + tid) * nsl + sl] = arg;
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) s_last = atomicAdd(rs.cnt + tile, 1u) == static_cast<unsigned>(nsl - 1);
+      __syncthreads();
+      if (!s_last) continue;
+      __threadfence();
+      if (tid == 0) rs.cnt[tile] = 0u;  // ready for the next launch
+      if (tid < kRT) {
+        best = INFINITY;
+        arg = -1;
+        for (int q = 0; q < nsl; ++q) {  // ascending slices: strict < keeps the lowest k
+          const double b = __ldcg(rs.best + (t0 + tid) * nsl + q);
+          const int a = __ldcg(rs.arg + (t0 + tid) * nsl + q);
+          if (a >= 0 && (arg < 0 || b < best)) {
             best = b;
             arg = a;
           }
         }
+      }
+    }
+    if (tid < kRT) {
+      const int r = tid;
+      const int64_t row = s_row[r];
+      if (row >= 0) {
         const int own = s_own[r];
         const double n_o = p.nk[own];
         const bool singleton = n_o == 1.0;
@@ -723,8 +771,16 @@ void flag_all(fsil_context* c, const ScoreParams& p, int tile_rows) {
 void refine(fsil_context* c, const ScoreParams& p) {
   if (static_cast<int64_t>(c->k) * c->d >= 64 * 1024) {
     const int grid = c->num_sms * 4;
-    if (c->metric == FSIL_COSINE) refine_tiled_kernel<true><<<grid, 256, 0, c->stream>>>(p);
-    else refine_tiled_kernel<false><<<grid, 256, 0, c->stream>>>(p);
+    const size_t entries = static_cast<size_t>(2) * grid * kRT;
+    if (c->refine_cnt.bytes < grid * sizeof(unsigned)) {
+      c->refine_cnt.ensure(grid * sizeof(unsigned));
+      FSIL_CUDA(cudaMemsetAsync(c->refine_cnt.p, 0, c->refine_cnt.bytes, c->stream));
+    }
+    c->refine_part.ensure(entries * (sizeof(double) + sizeof(int)));
+    const RefineSplit rs{c->refine_part.as<double>(), reinterpret_cast<int*>(c->refine_part.as<double>() + entries),
+                         c->refine_cnt.as<unsigned>()};
+    if (c->metric == FSIL_COSINE) refine_tiled_kernel<true><<<grid, 256, 0, c->stream>>>(p, rs);
+    else refine_tiled_kernel<false><<<grid, 256, 0, c->stream>>>(p, rs);
     FSIL_LAUNCHED(c);
     return;
   }

@@ -142,6 +142,7 @@ struct fsil_context {
   fsil::DevBuf mu32, p32, nk, bound;
   fsil::DevBuf s_tmp;          // s when the caller passes no s pointer
   fsil::DevBuf tile_sum, tile_flag, flag_rows, flag_count;
+  fsil::DevBuf refine_part, refine_cnt;  // split tiled refinement: slice minima, row-tile tickets
   fsil::DevBuf result;         // double[4]: sum_s, flagged, ... (shard partial)
   fsil::DevBuf group_sum;
   fsil::DevBuf xmax;           // float: max |x| of this shard (tensor-core operand scaling)
