@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "device_util.cuh"
 #include "fsil_internal.cuh"
@@ -29,6 +30,7 @@ namespace fsil {
 namespace {
 
 constexpr int kPieceRows = 2048;
+constexpr int kRingWarps = 8;  // row-ring aggregation: warps per CTA (one CTA per SM)
 
 // ---------------------------------------------------------------- path 1 ----
 // Warp-per-row streaming with the (warp-uniform) label of each row: lanes hold
@@ -915,7 +917,7 @@ __global__ void __launch_bounds__(128) label_scatter_kernel(const int32_t* __res
 // row loads of a piece overlap instead of one row load per sub-group at a time.  The
 // per-row arithmetic and the piece layout are agg_piece_kernel's.
 template <bool COS, int CPL>
-__global__ void __launch_bounds__(384) agg_piece_ring_kernel(
+__global__ void __launch_bounds__(kRingWarps * 32) agg_piece_ring_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ rows, int64_t n, int d,
     int64_t row_offset, int k, int lpr, int R, const int64_t* __restrict__ seg_begin,
     const int64_t* __restrict__ seg_end, const int64_t* __restrict__ piece_start,
@@ -978,107 +980,128 @@ __global__ void __launch_bounds__(384) agg_piece_ring_kernel(
       for (int e = 0; e < 4; ++e) acc[q][e] = 0.0;
     double psi = 0.0, cnt = 0.0;
     float amax = 0.f;
-    // Cosine is software-pipelined by one row: row it's norm reduction across its lanes
-    // (five dependent shuffle steps, then a reciprocal square root) overlaps the
-    // accumulation of row it - 1, whose scale is known by then.  pv/pscale start at zero:
-    // the first step adds exact zeros.  The per-lane accumulation order is unchanged.
-    float pv[CPL][4];
-    double pscale = 0.0;
+    // Two slots (rows) per step: their norm reductions across the row's lanes (five
+    // dependent shuffle steps, then a reciprocal square root for cosine) run side by
+    // side and the per-step ring bookkeeping is paid once per two rows.  Rows are still
+    // accumulated one after the other, so each lane's summation order is unchanged.
+    constexpr int NR = CPL <= 6 ? 2 : 1;  // (wider rows: register budget)
+    const bool full_lanes = nchunks == lpr * CPL;  // every lane's CPL chunks inside the row
+    // one step of NR rows; FAST: all NR rows present and every chunk inside the row (no
+    // per-element predicates, no zero fill)
+    auto step = [&](int it, auto fast_tag) {
+      constexpr bool FAST = decltype(fast_tag)::value;
+      float v[NR][CPL][4];
+      int64_t rr[NR];
+      bool valid[NR];
 #pragma unroll
-    for (int q = 0; q < CPL; ++q)
+      for (int h = 0; h < NR; ++h) {
+        const int64_t pos = b0 + static_cast<int64_t>(it + h) * rpw + sub;
+        valid[h] = FAST || (it + h < iters && pos < b1);
+        rr[h] = 0;
+        if (!FAST) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) pv[q][e] = 0.f;
-    for (int it = 0; it < iters; ++it) {
-      const int s = cs;
-      sm100::mbar_wait(bars + s, cph);
-      if (++cs == R) {
-        cs = 0;
-        cph ^= 1u;
-      }
-      const int64_t pos = b0 + static_cast<int64_t>(it) * rpw + sub;
-      const bool valid = pos < b1;
-      const uint8_t* srow = ring + static_cast<size_t>(s) * slot_bytes + sub * row_bytes;
-      float v[CPL][4];
+          for (int q = 0; q < CPL; ++q)
 #pragma unroll
-      for (int q = 0; q < CPL; ++q) {
-        const int ch = li + q * lpr;
-        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid && ch < nchunks) t = *reinterpret_cast<const float4*>(srow + ch * 16);
-        v[q][0] = t.x; v[q][1] = t.y; v[q][2] = t.z; v[q][3] = t.w;
+            for (int e = 0; e < 4; ++e) v[h][q][e] = 0.f;
+        }
+        if (FAST || it + h < iters) {
+          const int s = cs;
+          sm100::mbar_wait(bars + s, cph);
+          if (++cs == R) {
+            cs = 0;
+            cph ^= 1u;
+          }
+          const uint8_t* srow = ring + static_cast<size_t>(s) * slot_bytes + sub * row_bytes;
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) {
+            const int ch = li + q * lpr;
+            if (FAST || (valid[h] && ch < nchunks)) {
+              const float4 t = *reinterpret_cast<const float4*>(srow + ch * 16);
+              v[h][q][0] = t.x; v[h][q][1] = t.y; v[h][q][2] = t.z; v[h][q][3] = t.w;
+            }
+          }
+          if (valid[h]) rr[h] = slot_rows[s * rpw + sub];
+        }
       }
-      const int64_t r = valid ? slot_rows[s * rpw + sub] : 0;
-      __syncwarp();  // every lane has read the slot: refill it
-      if (it + R < iters) {
-        fill(it + R, fs);
-        if (++fs == R) fs = 0;
-      }
+      __syncwarp();  // every lane has read both slots: refill them
+#pragma unroll
+      for (int h = 0; h < NR; ++h)
+        if (it + h + R < iters) {
+          fill(it + h + R, fs);
+          if (++fs == R) fs = 0;
+        }
       // ||x||^2: four independent fp64 partials per lane (short dependency chains), a fixed
       // combination order, then the fixed xor-tree across the row's lanes
-      double s4[4] = {0.0, 0.0, 0.0, 0.0};
-      bool finite = true;
+      double ss[NR];
+      bool finite[NR];
 #pragma unroll
-      for (int q = 0; q < CPL; ++q)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const double x = v[q][e];
-          s4[e] = fma(x, x, s4[e]);
-          if (!COS) finite = finite && isfinite(v[q][e]);
-          amax = fmaxf(amax, fabsf(v[q][e]));
-        }
-      double ss = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-      // cosine: squares of finite floats cannot overflow fp64, so a non-finite lane sum
-      // flags the lane (one test per row instead of one per element)
-      if (COS) finite = isfinite(ss);
-      if (!COS && !finite) {
+      for (int h = 0; h < NR; ++h) {
+        double s4[4] = {0.0, 0.0, 0.0, 0.0};
+        finite[h] = true;
 #pragma unroll
         for (int q = 0; q < CPL; ++q)
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int l = (li + q * lpr) * 4 + e;
-            if (l < d && !isfinite(v[q][e])) atomic_min_i64(checks, (row_offset + r) * d + l);
+            const double x = v[h][q][e];
+            s4[e] = fma(x, x, s4[e]);
+            if (!COS) finite[h] = finite[h] && isfinite(v[h][q][e]);
+            amax = fmaxf(amax, fabsf(v[h][q][e]));
           }
+        ss[h] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+        // cosine: squares of finite floats cannot overflow fp64, so a non-finite lane sum
+        // flags the lane (one test per row instead of one per element)
+        if (COS) finite[h] = isfinite(ss[h]);
       }
+#pragma unroll
+      for (int h = 0; h < NR; ++h)
+        if (!finite[h]) {
+#pragma unroll
+          for (int q = 0; q < CPL; ++q)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int l = (li + q * lpr) * 4 + e;
+              if (l < d && !isfinite(v[h][q][e])) atomic_min_i64(checks, (row_offset + rr[h]) * d + l);
+            }
+        }
       if (COS) {
+        for (int off = lpr >> 1; off > 0; off >>= 1) {
 #pragma unroll
-        for (int q = 0; q < CPL; ++q)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[q][e] += static_cast<double>(pv[q][e]) * pscale;
-        for (int off = lpr >> 1; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off, lpr);
-        const bool ok = valid && ss != 0.0;
-        pscale = ok ? 1.0 / sqrt(ss) : 0.0;
-        cnt += ok ? 1.0 : 0.0;
-#pragma unroll
-        for (int q = 0; q < CPL; ++q)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) pv[q][e] = v[q][e];
-        if (valid && li == 0) {
-          if (xi_out) xi_out[r] = ss;
-          if (ss == 0.0) atomic_min_i64(checks + 1, row_offset + r);
+          for (int h = 0; h < NR; ++h) ss[h] += __shfl_xor_sync(0xffffffffu, ss[h], off, lpr);
         }
-      } else if (valid) {
-        psi += ss;
-        cnt += 1.0;
+        double scale[NR];
 #pragma unroll
-        for (int q = 0; q < CPL; ++q)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[q][e] += static_cast<double>(v[q][e]);
-      }
-      if (COS && !finite) {
-#pragma unroll
-        for (int q = 0; q < CPL; ++q)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int l = (li + q * lpr) * 4 + e;
-            if (l < d && !isfinite(v[q][e])) atomic_min_i64(checks, (row_offset + r) * d + l);
+        for (int h = 0; h < NR; ++h) {
+          const bool ok = valid[h] && ss[h] != 0.0;
+          scale[h] = ok ? 1.0 / sqrt(ss[h]) : 0.0;
+          cnt += ok ? 1.0 : 0.0;
+          if (valid[h] && li == 0) {
+            if (xi_out) xi_out[rr[h]] = ss[h];
+            if (ss[h] == 0.0) atomic_min_i64(checks + 1, row_offset + rr[h]);
           }
+        }
+#pragma unroll
+        for (int h = 0; h < NR; ++h)  // row order (invalid rows add exact zeros)
+#pragma unroll
+          for (int q = 0; q < CPL; ++q)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[q][e] += static_cast<double>(v[h][q][e]) * scale[h];
+      } else {
+#pragma unroll
+        for (int h = 0; h < NR; ++h) {
+          if (!FAST && !valid[h]) continue;
+          psi += ss[h];
+          cnt += 1.0;
+#pragma unroll
+          for (int q = 0; q < CPL; ++q)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[q][e] += static_cast<double>(v[h][q][e]);
+        }
       }
-    }
-    if (COS) {
-#pragma unroll
-      for (int q = 0; q < CPL; ++q)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[q][e] += static_cast<double>(pv[q][e]) * pscale;
-    }
+    };
+    int it = 0;
+    if (full_lanes)
+      for (; it + NR <= iters; it += NR) step(it, std::true_type{});
+    for (; it < iters; it += NR) step(it, std::false_type{});
     for (int off = 16; off >= lpr; off >>= 1) {
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
@@ -1488,7 +1511,7 @@ void aggregate(fsil_context* c) {
     // keep agg_piece_kernel (one bulk copy per small row costs more than it hides).
     const int rpw = 32 / lpr;
     const int slot = rpw * c->d * 4;
-    const int W = 12;
+    const int W = kRingWarps;
     const size_t avail = std::min<size_t>(budget, 220 * 1024);
     const int R = static_cast<int>(std::max<size_t>(2, std::min<size_t>(16, avail / (static_cast<size_t>(W) * (slot + 8 + 4 * rpw)))));
     const size_t rsm = static_cast<size_t>(W) * R * (slot + 8 + 4 * rpw);
