@@ -30,7 +30,7 @@ namespace fsil {
 namespace {
 
 constexpr int kPieceRows = 2048;
-constexpr int kRingWarps = 8;  // row-ring aggregation: warps per CTA (one CTA per SM)
+constexpr int kRingWarps = 12, kRingCtas = 1;  // row-ring aggregation: warps per CTA, CTAs per SM
 
 // ---------------------------------------------------------------- path 1 ----
 // Warp-per-row streaming with the (warp-uniform) label of each row: lanes hold
@@ -917,7 +917,7 @@ __global__ void __launch_bounds__(128) label_scatter_kernel(const int32_t* __res
 // row loads of a piece overlap instead of one row load per sub-group at a time.  The
 // per-row arithmetic and the piece layout are agg_piece_kernel's.
 template <bool COS, int CPL>
-__global__ void __launch_bounds__(kRingWarps * 32) agg_piece_ring_kernel(
+__global__ void __launch_bounds__(kRingWarps * 32, kRingCtas) agg_piece_ring_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ rows, int64_t n, int d,
     int64_t row_offset, int k, int lpr, int R, const int64_t* __restrict__ seg_begin,
     const int64_t* __restrict__ seg_end, const int64_t* __restrict__ piece_start,
@@ -984,7 +984,7 @@ __global__ void __launch_bounds__(kRingWarps * 32) agg_piece_ring_kernel(
     // dependent shuffle steps, then a reciprocal square root for cosine) run side by
     // side and the per-step ring bookkeeping is paid once per two rows.  Rows are still
     // accumulated one after the other, so each lane's summation order is unchanged.
-    constexpr int NR = CPL <= 6 ? 2 : 1;  // (wider rows: register budget)
+    constexpr int NR = CPL <= 3 ? 2 : 1;  // (wider rows: register budget)
     const bool full_lanes = nchunks == lpr * CPL;  // every lane's CPL chunks inside the row
     // one step of NR rows; FAST: all NR rows present and every chunk inside the row (no
     // per-element predicates, no zero fill)
@@ -1506,17 +1506,19 @@ void aggregate(fsil_context* c) {
     if (cos) launch_pieces<true>(c, c->X64, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);
     else launch_pieces<false>(c, c->X64, vec, cpl_t, max_pieces, lpr, srows, seg_begin, seg_end, piece_start, pout, checks);
   } else if (vec == 4 && cpl <= 8 && c->d >= 256 && ring_env) {
-    // wide rows (>= 1 KB): bulk-copy ring, R slots per warp, 12 persistent warps per SM
-    // striding over the pieces (one CTA per SM: ~216 KB of rows in flight).  Narrow rows
-    // keep agg_piece_kernel (one bulk copy per small row costs more than it hides).
+    // wide rows (>= 1 KB): bulk-copy ring, R slots per warp, kRingCtas x kRingWarps
+    // persistent warps per SM striding over the pieces.  The per-row arithmetic (fp64,
+    // latency-bound) wants warps more than slots: random 3 KB row gathers reach HBM speed
+    // with 16 rows in flight per SM (tools/gather_bench.cu).  Narrow rows keep
+    // agg_piece_kernel (one bulk copy per small row costs more than it hides).
     const int rpw = 32 / lpr;
     const int slot = rpw * c->d * 4;
     const int W = kRingWarps;
-    const size_t avail = std::min<size_t>(budget, 220 * 1024);
+    const size_t avail = std::min<size_t>(budget, 220 * 1024) / kRingCtas;
     const int R = static_cast<int>(std::max<size_t>(2, std::min<size_t>(16, avail / (static_cast<size_t>(W) * (slot + 8 + 4 * rpw)))));
     const size_t rsm = static_cast<size_t>(W) * R * (slot + 8 + 4 * rpw);
     const unsigned grid = static_cast<unsigned>(std::max<int64_t>(
-        1, std::min<int64_t>((max_pieces + W - 1) / W, static_cast<int64_t>(c->num_sms))));
+        1, std::min<int64_t>((max_pieces + W - 1) / W, static_cast<int64_t>(kRingCtas) * c->num_sms)));
 #define FSIL_AGG_RING(C)                                                                                   \
   if (cpl == C) {                                                                                          \
     auto kern = cos ? agg_piece_ring_kernel<true, C> : agg_piece_ring_kernel<false, C>;                    \
