@@ -996,6 +996,18 @@ int tc_stages(int bn, int kp, size_t optin) {
   return ns;
 }
 
+// First-level MMAs per K step of the pair pass: FSIL_TC_L1 = 1 (default: hx.hm), 2 (hx.hm +
+// hx.lm) or 3 (one three-MMA pass, no second level; FSIL_TC_TWO=0 is the same); fp64 inputs 3
+static int pair_l1(const fsil_context* c) {
+  static const int l1_env = [] {
+    const char* e = std::getenv("FSIL_TC_L1");
+    const char* t = std::getenv("FSIL_TC_TWO");
+    if (t && std::atoi(t) == 0) return 3;
+    return e ? std::max(1, std::min(3, std::atoi(e))) : 1;
+  }();
+  return c->X64 ? 3 : l1_env;
+}
+
 template <int BN, bool COS, int KC = 32, int EG = 2, bool T3 = false>
 void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                const TcParams& tp, int64_t ntiles, bool rec = true) {
@@ -1089,7 +1101,9 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     probe.nkc = nkc;
     const int nstg_ = tc_stages(bn, ncb * bn, c->smem_optin);
     const bool streaming = ncb > 1 && !(2 * nkc <= nstg_) && nkc >= nstg_;
-    pair = streaming && pair_supported(c, probe, bn);
+    // (the pair kernel is a first level of one or two MMAs per K step; a single three-MMA
+    // pass -- FSIL_TC_L1=3 / FSIL_TC_TWO=0 experiments -- runs on the single-CTA kernel)
+    pair = streaming && pair_supported(c, probe, bn) && pair_l1(c) < 3;
     if (pair) ncb = (c->k + 255) / 256 * 2;
   }
   const int kp = ncb * bn;
@@ -1221,13 +1235,7 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     // with the three-MMA kernel below.  FSIL_TC_TWO=0: one three-MMA pair pass.
     // FSIL_TC_L1 = 1 (default: one MMA per K step, hx.hm), 2 (hx.hm + hx.lm) or 3 (one
     // three-MMA pass, no second level; FSIL_TC_TWO=0 is the same)
-    static const int l1_env = [] {
-      const char* e = std::getenv("FSIL_TC_L1");
-      const char* t = std::getenv("FSIL_TC_TWO");
-      if (t && std::atoi(t) == 0) return 3;
-      return e ? std::max(1, std::min(3, std::atoi(e))) : 1;
-    }();
-    const int l1 = c->X64 ? 3 : l1_env;
+    const int l1 = pair_l1(c);
     const bool two = l1 < 3;
     TcParams tpp = tp;
     tpp.split = 0;

@@ -46,6 +46,7 @@ constexpr int kBPiece = kHalfN * 128;      // one B piece (hi or lo) per stage p
 constexpr uint32_t kPairCols = 512;        // TMEM columns: two 256-column accumulators
 constexpr int kEpi0 = 4, kConv0 = 12;
 constexpr int kScanG = 4;  // epilogue filter group (keys)
+constexpr int kXBox = BM * 128;            // one X box: 128 rows x 32 fp32 columns (16 KB)
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -164,6 +165,17 @@ __device__ __forceinline__ void bulk_store_hint(void* dst, const void* src, uint
   asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
 }
 
+// 2-D tensor store from this CTA's shared memory (bulk group: commit here, the caller waits)
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const void* src, int c0, int c1,
+                                                  uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;\n" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+
 template <uint32_t NCOLS>
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* smem_dst) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(smem_dst)),
@@ -205,9 +217,9 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 // Shared memory (identical offsets in both CTAs: the MMA addresses the peer's operands
 // through the leader's descriptors)
 struct PairSmem {
-  static size_t bytes(int ns, int nb) {
-    return 1024 + static_cast<size_t>(ns) * kStgBytes + static_cast<size_t>(nb) * 2 * kBPiece + 64 * 8 +
-           4 * BM * 8 + 10 * BM * 4 + 2 * BM * 4 + 4 * BM * 4 + 64;
+  static size_t bytes(int ns, int nb, int nx) {
+    return 1024 + static_cast<size_t>(ns) * kStgBytes + static_cast<size_t>(nb) * 2 * kBPiece +
+           static_cast<size_t>(nx) * kXBox + 64 * 8 + 4 * BM * 8 + 10 * BM * 4 + 2 * BM * 4 + 4 * BM * 4 + 64;
   }
 };
 
@@ -221,10 +233,11 @@ template <bool COS, bool T3, int L1>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_pair_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
                          const __grid_constant__ CUtensorMap tmap_bl, const __grid_constant__ CUtensorMap tmap_scr,
-                         TcParams tp, int64_t ntiles, int ns, int nb) {
-  constexpr bool TWO = L1 < 3;  // a first level of the two-level certificate (x lo dropped)
+                         const __grid_constant__ CUtensorMap tmap_scst, TcParams tp, int64_t ntiles, int ns, int nb,
+                         int nx) {
+  static_assert(L1 == 1 || L1 == 2, "the pair kernel is the first level of the two-level certificate");
   constexpr int BCH = L1 == 1 ? 2 : 1;  // K chunks per B stage (hm only: two fit a stage)
-  constexpr int ACH = TWO ? 2 : 1;      // K chunks per reloaded A stage (hx only: two fit a stage)
+  constexpr int ACH = 2;                // K chunks per A stage (hx only: two fit a stage)
   griddep_wait();           // (PDL) prep_b's operands and every earlier phase are visible
   if (*tp.p.abort) return;  // K speculation missed: the call is repeated (both CTAs return)
   const ScoreParams& p = tp.p;
@@ -237,34 +250,38 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* stg = base;                               // [ns][kStgBytes]: X fp32 -> A hi | lo in place
-  uint8_t* bring = stg + ns * kStgBytes;             // [nb][B hi | B lo] (this CTA's 128 columns)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + nb * 2 * kBPiece);
-  uint64_t* stg_full = bars;         // [ns <= 8] local: X landed (first pass)
-  uint64_t* stg_empty = bars + 8;    // [ns] local: stage free (multicast MMA commit)
-  uint64_t* a_full = bars + 16;      // [ns] leader: converted / reloaded chunk of both CTAs
-  uint64_t* b_full = bars + 24;      // [nb <= 8] leader: B of both CTAs
-  uint64_t* b_empty = bars + 32;     // [nb] local (multicast commit)
-  uint64_t* acc_full = bars + 40;    // [2] local (multicast commit)
-  uint64_t* acc_empty = bars + 42;   // [2] leader: 8 epilogue warps x 2 CTAs
-  uint64_t* meta_full = bars + 44;   // [2] local
-  uint64_t* meta_empty = bars + 46;  // [2] local
-  uint64_t* scr_ready = bars + 48;   // [1] local: a tile's converted chunks are in scratch
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 49);
+  uint8_t* stg = base;                               // [ns][2 x 16 KB]: A items (hx of two K chunks)
+  uint8_t* bring = stg + ns * kStgBytes;             // [nb][2 x 16 KB]: B (this CTA's 128 columns)
+  uint8_t* xst = bring + nb * 2 * kBPiece;           // [nx][16 KB]: X fp32 boxes (32 columns)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xst + nx * kXBox);
+  uint64_t* stg_empty = bars;        // [ns <= 8] local: A stage free (multicast MMA commit)
+  uint64_t* a_full = bars + 8;       // [ns] leader: both CTAs' reloaded chunks landed
+  uint64_t* b_full = bars + 16;      // [nb <= 8] leader: B of both CTAs
+  uint64_t* b_empty = bars + 24;     // [nb] local (multicast commit)
+  uint64_t* acc_full = bars + 32;    // [2] local (multicast commit)
+  uint64_t* acc_empty = bars + 34;   // [2] leader: 8 epilogue warps x 2 CTAs
+  uint64_t* meta_full = bars + 36;   // [2] local
+  uint64_t* meta_empty = bars + 38;  // [2] local
+  uint64_t* scr_ready = bars + 40;   // [2] local: a tile's converted chunks are in scratch buffer b
+  uint64_t* scr_free = bars + 42;    // [2] local: the issuer is past every reload of buffer b's tile
+  uint64_t* xs_full = bars + 44;     // [nx <= 4] local: X box landed
+  uint64_t* xs_empty = bars + 48;    // [nx] local: X box converted and stored
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 52);
   double* meta_xi = reinterpret_cast<double*>(bars + 64);    // [2][2][BM]
   float* part = reinterpret_cast<float*>(meta_xi + 4 * BM);  // [2][5][BM]
   int* meta_own = reinterpret_cast<int*>(part + 10 * BM);     // [2][BM]
-  float* meta_lx = reinterpret_cast<float*>(meta_own + 2 * BM);  // [2][2][BM] TWO: ||lx||^2 halves
+  float* meta_lx = reinterpret_cast<float*>(meta_own + 2 * BM);  // [2][2][BM] ||lx||^2 halves
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* const myscr = tp.ascratch + static_cast<size_t>(blockIdx.x) * nkc * kStgBytes;  // [nkc][kStgBytes]
+  // this CTA's scratch: [2 buffers][nkc chunks][BM rows][64 fp16], rows of the 2-D map
+  const int64_t scr_row0 = static_cast<int64_t>(blockIdx.x) * 2 * nkc * BM;
+  const int nbx = (p.d + 31) / 32;  // X boxes (32 fp32 columns) per tile
   const TcScale sc = *tp.scale;
   unsigned long long* const dbg = tp.dbg;
   const long long t_begin = dbg ? clock64() : 0;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < ns; ++i) {
-      mbar_init(stg_full + i, 1);
       mbar_init(stg_empty + i, 1);
       mbar_init(a_full + i, 2);
     }
@@ -277,13 +294,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(acc_empty + i, 16);
       mbar_init(meta_full + i, 8);
       mbar_init(meta_empty + i, 4);
+      mbar_init(scr_ready + i, 1);
+      mbar_init(scr_free + i, 1);
     }
-    mbar_init(scr_ready, 1);
+    for (int i = 0; i < nx; ++i) {
+      mbar_init(xs_full + i, 1);
+      mbar_init(xs_empty + i, 1);
+    }
     fence_barrier_init();
     prefetch_tmap(&tmap_x);
     prefetch_tmap(&tmap_bh);
     prefetch_tmap(&tmap_bl);
     prefetch_tmap(&tmap_scr);
+    prefetch_tmap(&tmap_scst);
   }
   if (warp == 1) tmem_alloc_pair<kPairCols>(tmem_slot);
   tc_fence_before();
@@ -294,38 +317,42 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < kEpi0) {
     setmaxnreg_dec<64>();
     if (warp == 0 && lane == 0) {
-      // ------------------------------------------------------------ X producer
+      // ------------------------------------------------------------ A producer
+      // every pass over a tile (all ncb cluster blocks) reloads its converted chunks from
+      // this CTA's scratch buffer, two chunks per stage, completing on the leader's a_full
       uint32_t n1 = 0, ntl = 0;
-      const uint64_t pol_x = l2_policy_evict_first(), pol_keep = l2_policy_evict_last();
+      const uint64_t pol_keep = l2_policy_evict_last();
       for (int64_t st = cid; st < nst; st += ncl, ++ntl) {
-        const int row0 = static_cast<int>(st * 2 * BM + rank * BM);
-        const int64_t sbase = static_cast<int64_t>(blockIdx.x) * nkc;
-        for (int xp = 0; xp < ncb; ++xp) {
-          if (xp == 1) {  // the first pass converted and stored this tile: reuse it
-            PW(5, mbar_wait(scr_ready, ntl & 1));
-            fence_proxy_async_global();
-          }
-          for (int kc = 0; kc < nkc; kc += (xp > 0 ? ACH : 1), ++n1) {
+        const int64_t srow = scr_row0 + static_cast<int64_t>(ntl & 1) * nkc * BM;
+        PW(5, mbar_wait(scr_ready + (ntl & 1), (ntl >> 1) & 1));
+        fence_proxy_async_global();
+        for (int cb = 0; cb < ncb; ++cb) {
+          for (int kc = 0; kc < nkc; kc += ACH, ++n1) {
             const int s1 = static_cast<int>(n1 % ns);
             PW(4, mbar_wait(stg_empty + s1, ((n1 / ns) & 1) ^ 1));  // (multicast MMA commit)
-            if (xp > 0) {
-              // a reload item: ACH chunks' A pieces side by side in one stage
-              const uint32_t af = mapa_u32(smem_u32(a_full + s1), 0);
-              const int nch = min(ACH, nkc - kc);
-              if (leader) mbar_expect_tx(a_full + s1, 2 * nch * (TWO ? kABytes : kStgBytes));
-              // (TWO: the map's box is the 16 KB hx piece at the start of each 32 KB chunk)
-              for (int h = 0; h < nch; ++h)
-                tma_load_2d_pair_hint(stg + s1 * kStgBytes + h * kABytes, &tmap_scr, af, 0,
-                                      static_cast<int>((sbase + kc + h) * BM), pol_keep);
-              if (leader) mbar_arrive_cnt(a_full + s1, 2);
-              continue;
-            }
-            const int nbox = (kc * BK + 32 < p.d) ? 2 : 1;
-            mbar_arrive_expect_tx(stg_full + s1, nbox * BM * 128);
-            for (int b = 0; b < nbox; ++b)
-              tma_load_2d_hint(stg + s1 * kStgBytes + b * BM * 128, &tmap_x, stg_full + s1, kc * BK + b * 32, row0,
-                               pol_x);
+            const uint32_t af = mapa_u32(smem_u32(a_full + s1), 0);
+            const int nch = min(ACH, nkc - kc);
+            if (leader) mbar_expect_tx(a_full + s1, 2 * nch * kABytes);
+            for (int h = 0; h < nch; ++h)
+              tma_load_2d_pair_hint(stg + s1 * kStgBytes + h * kABytes, &tmap_scr, af, 0,
+                                    static_cast<int>(srow + (kc + h) * BM), pol_keep);
+            if (leader) mbar_arrive_cnt(a_full + s1, 2);
           }
+        }
+      }
+    } else if (warp == 3 && lane == 0) {
+      // ------------------------------------------------------------ X producer
+      // this CTA's 128 rows of each tile, one 32-column box per stage; runs up to the X ring
+      // ahead, so the next tile's rows stream in while the current tile is scored
+      uint32_t nxb = 0;
+      const uint64_t pol_x = l2_policy_evict_first();
+      for (int64_t st = cid; st < nst; st += ncl) {
+        const int row0 = static_cast<int>(st * 2 * BM + rank * BM);
+        for (int bx = 0; bx < nbx; ++bx, ++nxb) {
+          const int sx = static_cast<int>(nxb % nx);
+          mbar_wait(xs_empty + sx, ((nxb / nx) & 1) ^ 1);
+          mbar_arrive_expect_tx(xs_full + sx, kXBox);
+          tma_load_2d_hint(xst + sx * kXBox, &tmap_x, xs_full + sx, bx * 32, row0, pol_x);
         }
       }
     } else if (warp == 2 && lane == 0) {
@@ -366,17 +393,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t pa = 0, pb = 0;
       const int nkfull = p.d / BK;  // full 64-wide K chunks
       const uint64_t da0 = desc_k_sw128(smem_u32(stg)), db0 = desc_k_sw128(smem_u32(bring));
-      for (int64_t st = cid; st < nst; st += ncl) {
+      uint32_t ntl = 0;
+      for (int64_t st = cid; st < nst; st += ncl, ++ntl) {
         for (int cb = 0; cb < ncb; ++cb, ++na) {
           const int ab = static_cast<int>(na & 1);
           PW(0, mbar_wait(acc_empty + ab, ((na >> 1) & 1) ^ 1));
           tc_fence_after();
           const uint32_t d = tmem_base + ab * kPairN;
-          const int ach = cb == 0 ? 1 : ACH;  // chunks per A item: converted pass 1, reloads ACH
+          constexpr int ach = ACH;  // chunks per A item
           const long long tcb0 = dbg ? clock64() : 0;
           for (int kc0 = 0; kc0 < nkc; kc0 += ach) {
             const long long tit0 = dbg ? clock64() : 0;
-            if (L1 == 1 && cb > 0 && kc0 + 2 <= nkfull) {
+            if (L1 == 1 && kc0 + 2 <= nkfull) {
               // the steady state: a reload item of two full chunks against the B stage of the
               // same two chunks -- two waits, eight MMAs, two commits, straight-line
               PW(1, mbar_wait(a_full + s1, pa));
@@ -408,11 +436,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (dbg) atomicAdd(dbg + 12, static_cast<unsigned long long>(clock64() - tit0));
               continue;
             }
-            // cluster-scope acquire only where the peer's converters wrote shared memory with
-            // generic stores (the converted pass); the tensor copies' completions (reloads, B)
-            // make their bytes visible to the async proxy through the barrier itself
-            if (cb == 0) PW(10, mbar_wait_cluster(a_full + s1, pa));
-            else PW(1, mbar_wait(a_full + s1, pa));
+            // (the tensor copies' completions make their bytes visible to the async proxy
+            // through the barrier itself: CTA-scope waits)
+            PW(1, mbar_wait(a_full + s1, pa));
             const int nch = min(ach, nkc - kc0);
             for (int h = 0; h < nch; ++h) {
               const int kc = kc0 + h;
@@ -466,95 +492,91 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (dbg) atomicAdd(dbg + 13, static_cast<unsigned long long>(clock64() - tcb0));
         }
+        // every reload of this tile's scratch buffer has landed (its a_full waits are
+        // behind us): both CTAs' converters may overwrite the buffer with the tile after next
+        if (elect_one()) {
+          mbar_arrive(scr_free + (ntl & 1));
+          mbar_arrive_remote(mapa_u32(smem_u32(scr_free + (ntl & 1)), 1));
+        }
+        __syncwarp();
       }
       if (dbg) atomicAdd(dbg + 3, static_cast<unsigned long long>(clock64() - t_begin));
     }
   } else if (warp >= kConv0) {
     setmaxnreg_dec<72>();
     // ------------------------------------------------------------ converters
+    // One X box (32 fp32 columns x 128 rows) at a time, two threads per row (16 columns
+    // each): scale (exact), fp16 hx, the residual lx = x~ - hx (exact) into ||lx||^2; hx is
+    // written in place as a compact [128 rows][64 B] half chunk and tensor-stored to this
+    // CTA's scratch buffer of the tile.  Converting runs a tile ahead of the MMAs (double-
+    // buffered scratch): no pass over a tile waits on HBM or on the conversion.
     const int tl = threadIdx.x - kConv0 * 32;
     const int r = tl & (BM - 1), hq = tl >> 7;
     const int sw = r & 7;
     const float2 sx2 = make_float2(sc.sx, sc.sx), neg1 = make_float2(-1.f, -1.f);
-    uint32_t n1 = 0, nt = 0, tpar = 0;  // tpar bit s: parity of stage s's next X landing
-    int s1 = 0;
+    const uint64_t pol_keep = l2_policy_evict_last();
+    uint32_t nxb = 0, nt = 0;
     for (int64_t st = cid; st < nst; st += ncl, ++nt) {
       const int64_t row = st * 2 * BM + rank * BM + r;
       const int own = (hq == 0 && row < p.n) ? __ldg(p.dense + row) : -1;
+      const int b = static_cast<int>(nt & 1);
+      const int64_t srow = scr_row0 + static_cast<int64_t>(b) * nkc * BM;
       double xi = 0.0;
-      float lx2 = 0.0f;  // TWO: sum of lx^2 (lx = x~ - hx, exact in fp32; tiny, fp32 sum + margin)
-      for (int kc = 0; kc < nkc; ++kc, ++n1) {
-        if (tl == 0) PW(9, mbar_wait(stg_full + s1, (tpar >> s1) & 1u));
-        else mbar_wait(stg_full + s1, (tpar >> s1) & 1u);
-        tpar ^= 1u << s1;
-        uint8_t* sbase = stg + s1 * kStgBytes;
-        float4 f[8];
-        const uint8_t* srow = sbase + hq * (BM * 128) + r * 128;
+      float lx2 = 0.0f;  // sum of lx^2 (exact residuals; tiny, fp32 sum + margin)
+      for (int bx = 0; bx < nbx; ++bx, ++nxb) {
+        const int sx = static_cast<int>(nxb % nx);
+        if (tl == 0) PW(9, mbar_wait(xs_full + sx, (nxb / nx) & 1));
+        else mbar_wait(xs_full + sx, (nxb / nx) & 1);
+        uint8_t* xb = xst + sx * kXBox;
+        float4 f[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) f[u] = *reinterpret_cast<const float4*>(srow + ((u ^ sw) << 4));
-        if (hq == 1 && kc * BK + 32 >= p.d) {
+        for (int u = 0; u < 4; ++u) f[u] = *reinterpret_cast<const float4*>(xb + r * 128 + (((4 * hq + u) ^ sw) << 4));
+        named_bar_sync(5, 256);  // every read of the box precedes the in-place writes
+        const float v[16] = {f[0].x, f[0].y, f[0].z, f[0].w, f[1].x, f[1].y, f[1].z, f[1].w,
+                             f[2].x, f[2].y, f[2].z, f[2].w, f[3].x, f[3].y, f[3].z, f[3].w};
+        if (!tp.xi_rows) {  // ||x||^2: fp32 blocks of 8 (error <= 8u each), fp64 across blocks
 #pragma unroll
-          for (int u = 0; u < 8; ++u) f[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        named_bar_sync(5, 256);  // every read of the stage precedes the in-place writes
-        uint8_t* hrow = sbase + r * 128;
-        uint8_t* lrow = hrow + BM * 128;
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const int j = 4 * hq + jj;
-          const float v[8] = {f[2 * jj].x,     f[2 * jj].y,     f[2 * jj].z,     f[2 * jj].w,
-                              f[2 * jj + 1].x, f[2 * jj + 1].y, f[2 * jj + 1].z, f[2 * jj + 1].w};
-          if (!tp.xi_rows) {  // ||x||^2: fp32 blocks of 8 (error <= 8u each), fp64 across blocks
+          for (int blk = 0; blk < 2; ++blk) {
             float2 bs = make_float2(0.f, 0.f);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float2 ve = make_float2(v[2 * e], v[2 * e + 1]);
+              const float2 ve = make_float2(v[8 * blk + 2 * e], v[8 * blk + 2 * e + 1]);
               bs = __ffma2_rn(ve, ve, bs);
             }
             xi += static_cast<double>(bs.x + bs.y);
           }
-          uint32_t hw[4], lw[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {  // packed f32x2: scale (exact), hi, residual (exact), lo
-            const float2 xx = __fmul2_rn(make_float2(v[2 * e], v[2 * e + 1]), sx2);
-            const __half2 h = __float22half2_rn(xx);
-            const float2 res = __ffma2_rn(__half22float2(h), neg1, xx);
-            if (TWO) {
-              lx2 = fmaf(res.x, res.x, fmaf(res.y, res.y, lx2));
-            } else {
-              const __half2 l = __float22half2_rn(res);
-              lw[e] = *reinterpret_cast<const uint32_t*>(&l);
-            }
-            hw[e] = *reinterpret_cast<const uint32_t*>(&h);
-          }
-          const int pos = (j ^ sw) << 4;
-          *reinterpret_cast<uint4*>(hrow + pos) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-          if (!TWO) *reinterpret_cast<uint4*>(lrow + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
         }
+        uint32_t hw[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {  // packed f32x2: scale (exact), hi, residual (exact)
+          const float2 xx = __fmul2_rn(make_float2(v[2 * e], v[2 * e + 1]), sx2);
+          const __half2 h = __float22half2_rn(xx);
+          const float2 res = __ffma2_rn(__half22float2(h), neg1, xx);
+          lx2 = fmaf(res.x, res.x, fmaf(res.y, res.y, lx2));
+          hw[e] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        uint8_t* hrow = xb + r * 64 + hq * 32;
+        *reinterpret_cast<uint4*>(hrow) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(hrow + 16) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
         fence_proxy_async_smem();
         named_bar_sync(5, 256);
         if (tl == 0) {
-          // the converted chunk -> scratch (read before the MMA may free the stage), then
-          // this CTA's single arrival on the leader's a_full
-          bulk_store_hint(myscr + static_cast<size_t>(kc) * kStgBytes, sbase, TWO ? kABytes : kStgBytes,
-                          l2_policy_evict_last());
+          // the buffer last held the tile before last: the issuer must be past its reloads
+          if (bx == 0 && nt >= 2) PW(14, mbar_wait(scr_free + b, ((nt >> 1) & 1) ^ 1));
+          tma_store_2d_hint(&tmap_scst, xb, (bx & 1) * 32, static_cast<int>(srow + (bx >> 1) * BM), pol_keep);
           bulk_wait_read();
-          mbar_arrive_cluster(mapa_u32(smem_u32(a_full + s1), 0));
+          mbar_arrive(xs_empty + sx);
         }
-        if (++s1 == ns) s1 = 0;
       }
       if (tl == 0) {  // this tile's chunks are all in global memory
         bulk_wait_all();
-        mbar_arrive(scr_ready);
+        mbar_arrive(scr_ready + b);
       }
-      // the reload passes (ncb - 1 of ceil(nkc / ACH) items each) go through the same stages
-      n1 += static_cast<uint32_t>((ncb - 1) * ((nkc + ACH - 1) / ACH));
-      s1 = static_cast<int>(n1 % ns);
-      // ||x||^2 halves and the own cluster to the epilogue
+      // ||x||^2 halves, ||lx||^2 halves and the own cluster to the epilogue
       const int tb = nt & 1;
       mbar_wait(meta_empty + tb, ((nt >> 1) & 1) ^ 1);
       meta_xi[(tb * 2 + hq) * BM + r] = xi;
-      if (TWO) meta_lx[(tb * 2 + hq) * BM + r] = lx2;
+      meta_lx[(tb * 2 + hq) * BM + r] = lx2;
       if (hq == 0) meta_own[tb * BM + r] = own;
       __syncwarp();
       if (lane == 0) mbar_arrive(meta_full + tb);
@@ -580,11 +602,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float xn = COS ? 0.0f : sqrtf(xi);
       const float rnf = COS ? rsqrtf(xi) : 0.0f;
       const float rowm = COS ? -(sc.smul * rnf) : -2.0f * sc.smul;
-      // TWO: ||lx|| / ||x~|| (the dropped piece, relative to the row; fp32 sums of squares
-      // of numbers ~2^-11 |x| carry < 1e-4 relative error: x 1.001 margin; rsqrt <= 2.2u)
-      const float lx_rel = TWO ? sqrtf(meta_lx[(tb * 2) * BM + r] + meta_lx[(tb * 2 + 1) * BM + r]) * rsqrtf(xi) /
-                                     sc.sx * 1.001f
-                               : -1.0f;
+      // ||lx|| / ||x~|| (the dropped piece, relative to the row; fp32 sums of squares of
+      // numbers ~2^-11 |x| carry < 1e-4 relative error: x 1.001 margin; rsqrt <= 2.2u)
+      const float lx_rel =
+          sqrtf(meta_lx[(tb * 2) * BM + r] + meta_lx[(tb * 2 + 1) * BM + r]) * rsqrtf(xi) / sc.sx * 1.001f;
       float b1 = INFINITY, b2 = INFINITY, b3 = INFINITY;
       int arg = -1, arg2 = -1;
       // one 32-column chunk: ranking keys (own column excluded), running top-2 / top-3.
@@ -716,40 +737,45 @@ bool pair_supported(const fsil_context* c, const TcParams& tp, int bn) {
     return !e || std::atoi(e) != 0;
   }();
   // streaming regime only (several 256-column blocks, a tile's chunks too many to keep),
-  // an even grid of one CTA per SM, and the 8 (X) + 8 (B) barrier slots
+  // an even grid of one CTA per SM
   const int ncb2 = (c->k + kPairN - 1) / kPairN;
   return env && bn == 128 && ncb2 >= 2 && tp.nkc >= 3 && c->num_sms >= 2 && !c->X64 &&
-         PairSmem::bytes(3, 3) <= c->smem_optin;
+         PairSmem::bytes(3, 3, 1) <= c->smem_optin;
 }
 
 void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                     TcParams tp, int64_t ntiles, bool cos, bool t3, int l1) {
-  const bool two = l1 < 3;
-  // stages: X/A and B rings of 32 KB each; 3 + 3 at 227 KB.  Measured (C5, 4M rows):
-  // 3 + 3 59.1 ms, 4 + 2 62.1 ms, 3 + 2 64.5 ms -- the issuer's A waits shrink with more
-  // A stages but its B waits grow faster
-  int nb = 3, ns = 3;
-  while (PairSmem::bytes(ns, nb) > c->smem_optin && nb > 2) --nb;
+  if (l1 < 1 || l1 > 2) fail(FSIL_ERR_INTERNAL, "pair kernel: first level of 1 or 2 MMAs per K step");
+  // stages: A (two reloaded chunks) and B rings of 32 KB, X boxes of 16 KB.  Measured (C5,
+  // 1M rows, Mcycles per CTA): 3/3/1 6.62, 3/2/2 7.32, 2/3/2 7.85 -- the converters run a
+  // tile ahead and need no X lookahead; the MMA needs both operand rings deep
+  int ns = 3, nb = 3, nx = 1;
   if (const char* e = std::getenv("FSIL_TC_PAIR_NB")) nb = std::max(2, std::min(8, std::atoi(e)));  // experiments
   if (const char* e = std::getenv("FSIL_TC_PAIR_NS")) ns = std::max(2, std::min(8, std::atoi(e)));
-  while (PairSmem::bytes(ns, nb) > c->smem_optin && ns > 2) --ns;
+  if (const char* e = std::getenv("FSIL_TC_PAIR_NX")) nx = std::max(1, std::min(4, std::atoi(e)));
+  while (PairSmem::bytes(ns, nb, nx) > c->smem_optin && ns > 2) --ns;
+  while (PairSmem::bytes(ns, nb, nx) > c->smem_optin && nb > 2) --nb;
+  while (PairSmem::bytes(ns, nb, nx) > c->smem_optin && nx > 1) --nx;
   tp.ncb = (c->k + kPairN - 1) / kPairN;
   // (Measured and removed: a fused exact pass in the converters -- the post pass 45 -> 11 ms
-  // but the kernel 636 -> 685 ms, fp64 table reads competing with the operand stream in L2 --
-  // and converter-prefetched double-buffered scratch -- 686 ms: the issuer waits on the
-  // reloads themselves, and a 114 MB scratch evicts more of them.  DESIGN.md 4.5.)
+  // but the kernel 636 -> 685 ms, fp64 table reads competing with the operand stream in L2.
+  // DESIGN.md 4.5.)
   const int grid = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(2 * ((ntiles + 1) / 2), c->num_sms & ~1)));
-  c->a_scratch.ensure(static_cast<size_t>(grid) * tp.nkc * kStgBytes);
+  // scratch: per CTA two buffers (the tile being scored, the next being converted) of nkc
+  // chunks x 128 rows x 64 fp16 -- a 2-D tensor of 128-byte rows, reloaded in 64 x 128
+  // boxes with the 128-byte swizzle the MMA descriptors expect, stored by the converters
+  // in unswizzled 32 x 128 half chunks
+  const uint64_t srows = static_cast<uint64_t>(grid) * 2 * tp.nkc * BM;
+  c->a_scratch.ensure(srows * 128);
   tp.ascratch = c->a_scratch.as<uint8_t>();
-  // the scratch as a 2-D tensor of 256-byte rows: one 32 KB box = one converted chunk (two-
-  // MMA level: the 16 KB hx piece at the start of each chunk, a box of 64 such rows)
-  const CUtensorMap mscr = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_UINT16, tp.ascratch, 128,
-                                       static_cast<uint64_t>(grid) * tp.nkc * BM, 256, 128, two ? BM / 2 : BM,
-                                       CU_TENSOR_MAP_SWIZZLE_NONE);
-  const size_t smem = PairSmem::bytes(ns, nb);
+  const CUtensorMap mscr = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, tp.ascratch, 64, srows, 128, 64, BM,
+                                       CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap mscst = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, tp.ascratch, 64, srows, 128, 32, BM,
+                                        CU_TENSOR_MAP_SWIZZLE_NONE);
+  const size_t smem = PairSmem::bytes(ns, nb, nx);
 #define FSIL_PAIR_K(L) (cos ? (t3 ? score_tc_pair_kernel<true, true, L> : score_tc_pair_kernel<true, false, L>) \
                            : (t3 ? score_tc_pair_kernel<false, true, L> : score_tc_pair_kernel<false, false, L>))
-  auto kern = l1 == 1 ? FSIL_PAIR_K(1) : l1 == 2 ? FSIL_PAIR_K(2) : FSIL_PAIR_K(3);
+  auto kern = l1 == 1 ? FSIL_PAIR_K(1) : FSIL_PAIR_K(2);
 #undef FSIL_PAIR_K
   FSIL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   if (c->timing) {  // the kernel alone, for the roofline (ms_score_kernel)
@@ -778,19 +804,19 @@ void launch_tc_pair(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& m
     if (std::atoi(std::getenv("FSIL_TC_PROFILE")) == 2) FSIL_CUDA(cudaMemsetAsync(dbg + 15, 1, 1, c->stream));
   }
   tp.dbg = dbg;
-  FSIL_CUDA(cudaLaunchKernelEx(&cfg, kern, mx, mh, ml, mscr, tp, ntiles, ns, nb));
+  FSIL_CUDA(cudaLaunchKernelEx(&cfg, kern, mx, mh, ml, mscr, mscst, tp, ntiles, ns, nb, nx));
   FSIL_LAUNCHED(c);
   if (dbg) {
     unsigned long long h[16];
     FSIL_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     FSIL_CUDA(cudaStreamSynchronize(c->stream));
-    const char* names[14] = {"mma acc_empty", "mma a_full(reload)", "mma b_full", "mma total", "X stg_empty",
-                             "X scr_ready", "B b_empty", "epi acc_full", "epi meta_full", "conv stg_full",
-                             "mma a_full(pass0)", "mma issue", "mma items", "mma cbs"};
+    const char* names[15] = {"mma acc_empty", "mma a_full", "mma b_full", "mma total", "A stg_empty",
+                             "A scr_ready", "B b_empty", "epi acc_full", "epi meta_full", "conv xs_full",
+                             "(unused)", "mma issue", "mma items", "mma cbs", "conv scr_free"};
     const double pairs = static_cast<double>(grid / 2), ctas = static_cast<double>(grid);
-    std::fprintf(stderr, "[fsil tc pair profile] ns=%d nb=%d Mcycles per CTA (MMA rows: per pair):", ns, nb);
-    for (int i = 0; i < 14; ++i)
-      std::fprintf(stderr, " %s=%.3f", names[i], h[i] / (i < 4 || i >= 10 ? pairs : ctas) / 1e6);
+    std::fprintf(stderr, "[fsil tc pair profile] ns=%d nb=%d nx=%d Mcycles per CTA (MMA rows: per pair):", ns, nb, nx);
+    for (int i = 0; i < 15; ++i)
+      std::fprintf(stderr, " %s=%.3f", names[i], h[i] / ((i < 4 || (i >= 10 && i < 14)) ? pairs : ctas) / 1e6);
     std::fprintf(stderr, "\n");
     cudaFree(dbg);
   }
