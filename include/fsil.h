@@ -84,7 +84,7 @@ typedef struct {
   int64_t pair_rows;       /* rows whose neighbour was one of two certified candidates, decided in fp64 */
   int32_t tc_mmas;         /* tensor-core MMAs per 16-deep K step of the pass that scored every row:
                               3 (fp16x3), 2 (the two-level certificate's first level); 0 otherwise */
-  int32_t pad0;
+  int32_t tc_threshold;    /* 1: the tensor-core pass ran in threshold mode (comparison inside the MMA) */
   int64_t rescored_rows;   /* two-level certificate: rows re-scored at three-MMA precision */
 } fsil_stats;
 

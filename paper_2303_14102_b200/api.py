@@ -98,7 +98,7 @@ class fsil_stats(ctypes.Structure):
                 ("flagged_rows", _I64), ("exact_rows", _I64), ("kernel_launches", _I64), ("ms_densify", ctypes.c_float),
                 ("ms_aggregate", ctypes.c_float), ("ms_score", ctypes.c_float),
                 ("ms_refine", ctypes.c_float), ("ms_finalize", ctypes.c_float),
-                ("ms_score_kernel", ctypes.c_float), ("pair_rows", _I64), ("tc_mmas", _I32), ("pad0", _I32),
+                ("ms_score_kernel", ctypes.c_float), ("pair_rows", _I64), ("tc_mmas", _I32), ("tc_threshold", _I32),
                 ("rescored_rows", _I64)]
 
 

@@ -1227,7 +1227,8 @@ __global__ void agg_init_kernel(double* stats, int64_t S, int64_t* checks, float
     // the scoring phase's counters and partial result (no separate memsets per call)
     for (int i = 0; i < 4; ++i) result[i] = 0.0;
     *flag_count = 0ull;
-    *pair_count = 0ull;
+    pair_count[0] = 0ull;
+    pair_count[1] = 0ull;  // threshold mode's candidate records
   }
 }
 
@@ -1319,7 +1320,7 @@ void aggregate(fsil_context* c) {
   c->bound.ensure(4 * sizeof(float));
   c->result.ensure(4 * sizeof(double));
   c->flag_count.ensure(sizeof(unsigned long long));
-  c->pair_count.ensure(sizeof(unsigned long long));
+  c->pair_count.ensure(2 * sizeof(unsigned long long));
   launch_pdl(c, agg_init_kernel, static_cast<unsigned>(std::min<int64_t>((S + 255) / 256 + 1, 1024)), 256, 0, stats,
              S, checks, c->xmax.as<float>(), c->bound.as<float>(), c->result.as<double>(),
              c->flag_count.as<unsigned long long>(), c->pair_count.as<unsigned long long>());

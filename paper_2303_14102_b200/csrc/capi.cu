@@ -93,6 +93,7 @@ void setup(fsil_context* c, int metric, const void* dX, bool x64, const int32_t*
   c->spec_missed = false;
   c->stats = fsil_stats{};
   c->tc_mmas = 0;
+  c->tc_thr = 0;
   c->rescored = 0;
   record(c, 0);
 }
@@ -307,6 +308,7 @@ double finish(fsil_context* c, double* flagged_out) {
   c->stats.exact_rows = static_cast<int64_t>(res[2]);
   c->stats.pair_rows = static_cast<int64_t>(res[3]);
   c->stats.tc_mmas = c->tc_mmas;
+  c->stats.tc_threshold = c->tc_thr;
   c->stats.rescored_rows = c->rescored;
   c->stats.kernel_launches = c->launches;
   if (c->timing) {
@@ -459,7 +461,7 @@ void fsil_destroy(fsil_context* c) {
                           &c->sort_tmp, &c->sort_keys, &c->sort_vals, &c->iota, &c->seg_start,
                           &c->piece_start, &c->mu32, &c->p32, &c->nk, &c->bound, &c->s_tmp,
                           &c->tile_sum, &c->tile_flag, &c->flag_rows, &c->flag_count, &c->result,
-                          &c->group_sum, &c->xmax, &c->tc_b, &c->nb_tmp, &c->pair_rows, &c->pair_count, &c->a_scratch, &c->x32, &c->xbuf, &c->xt_keys, &c->xt_vals, &c->xt_dense, &c->hX, &c->hL, &c->o_s, &c->o_nb, &c->o_own, &c->o_a,
+                          &c->group_sum, &c->xmax, &c->tc_b, &c->nb_tmp, &c->pair_rows, &c->pair_count, &c->thr_nn, &c->thr_t, &c->cand_rows, &c->a_scratch, &c->x32, &c->xbuf, &c->xt_keys, &c->xt_vals, &c->xt_dense, &c->hX, &c->hL, &c->o_s, &c->o_nb, &c->o_own, &c->o_a,
                           &c->o_b, &c->refine_part, &c->refine_cnt, &c->sub_x, &c->sub_i, &c->xi_rows};
   for (auto* b : bufs) b->release();
   for (auto& e : c->ev)

@@ -650,7 +650,8 @@ __device__ __forceinline__ void unit_total(const ExactArgs& ea, int64_t exact_ro
     const TotalArgs& ta = ea.ta;
     const double flagged = static_cast<double>(*ta.flag_count);
     const double exact = static_cast<double>(exact_rows);
-    const double pairs = ta.pair_count ? static_cast<double>(*ta.pair_count) : 0.0;
+    // (certified pairs + the threshold mode's three/four-candidate records)
+    const double pairs = ta.pair_count ? static_cast<double>(ta.pair_count[0] + ta.pair_count[1]) : 0.0;
     ta.result[0] = red[0];
     ta.result[1] = flagged;
     ta.result[2] = exact;
@@ -709,6 +710,80 @@ __device__ __forceinline__ void pair_rows_body(const ScoreParams& p, const int2*
       p.nb[row] = (m2 < m1 || (m2 == m1 && c2 < c1)) ? c2 : c1;
     }
   }
+}
+
+// Threshold mode's resolution pass.  The scoring epilogue left in the top bits of nb[row]:
+// 0 the neighbour is certain; 2..4 the neighbour is one of that many columns -- nb[row] and
+// cand[row].{x,y,z}; 1 no usable candidate set.  This pass scans nb (one row per lane), and
+// the warp resolves its marked rows one after another: the candidates' fp64 foreign means
+// with the reference formula, clamp included, then the reference's rule -- strict <, equal
+// means keep the lowest index (squared_euclidean.cpp:94-103) -- or, for code 1, the row
+// joins the fp64 refinement's list.  counts[1] += rows resolved here (statistics).
+template <bool COS>
+__global__ void __launch_bounds__(256) thr_resolve_kernel(ScoreParams p, const int4* __restrict__ cand,
+                                                          unsigned long long* counts) {
+  griddep_wait();
+  if (*p.abort) return;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const double* sums = p.stats + (COS ? p.k : 2 * p.k);
+  const int d = p.d;
+  unsigned long long resolved = 0;
+  for (int64_t base = warp * 32; base < p.n; base += nwarps * 32) {
+    const int64_t mine = base + lane;
+    const uint32_t v = mine < p.n ? static_cast<uint32_t>(p.nb[mine]) : 0u;
+    uint32_t todo = __ballot_sync(0xffffffffu, (v >> 28) != 0u);
+    while (todo) {
+      const int l = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t vv = __shfl_sync(0xffffffffu, v, l);
+      const int64_t row = base + l;
+      const int code = static_cast<int>(vv >> 28);
+      const int c1 = static_cast<int>(vv & 0x0fffffffu);
+      if (code == 1) {
+        if (lane == 0) {
+          p.nb[row] = c1;
+          const unsigned long long idx = atomicAdd(p.flag_count, 1ull);
+          p.flag_rows[idx] = static_cast<int32_t>(row);
+        }
+        continue;
+      }
+      const int4 rec = cand[row];
+      const int cs[4] = {c1, rec.x, code >= 3 ? rec.y : -1, code >= 4 ? rec.z : -1};
+      double ss = 0.0, dt[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int e = lane; e < d; e += 32) {
+        const double x = xval(p, row * d + e);
+        ss = fma(x, x, ss);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (cs[j] >= 0) dt[j] = fma(sums[static_cast<int64_t>(cs[j]) * d + e], x, dt[j]);
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        ss += __shfl_xor_sync(0xffffffffu, ss, off);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dt[j] += __shfl_xor_sync(0xffffffffu, dt[j], off);
+      }
+      if (lane == 0) {
+        const double nrm = sqrt(ss);
+        double best = 0.0;
+        int arg = -1;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = cs[j];
+          if (c < 0) continue;
+          const double m = COS ? cos_foreign(p.nk[c], dt[j] / nrm) : sq_foreign(ss, p.stats[p.k + c], p.nk[c], dt[j]);
+          if (arg < 0 || m < best || (m == best && c < arg)) {
+            best = m;
+            arg = c;
+          }
+        }
+        p.nb[row] = arg;
+        ++resolved;
+      }
+    }
+  }
+  if (lane == 0 && resolved) atomicAdd(counts + 1, resolved);
 }
 
 template <bool COS>
@@ -870,6 +945,12 @@ void exact_pass(fsil_context* c, const ScoreParams& p, bool local) {
   const int64_t tab = static_cast<int64_t>(c->k) * c->d;
   const bool small = tab < 64 * 1024;
   const unsigned long long* pcount = c->pair_count.as<unsigned long long>();
+  if (c->tc_thr) {  // threshold mode: rows with two to four candidate neighbours, rows with none
+    const unsigned cgrid = static_cast<unsigned>(c->num_sms * 8);
+    unsigned long long* counts = c->pair_count.as<unsigned long long>();
+    if (cos) launch_pdl(c, thr_resolve_kernel<true>, cgrid, 256, 0, p, c->cand_rows.as<int4>(), counts);
+    else launch_pdl(c, thr_resolve_kernel<false>, cgrid, 256, 0, p, c->cand_rows.as<int4>(), counts);
+  }
   if (!small) {  // full refinements (tiled) and certified pairs as their own launches
     refine(c, p);
     const unsigned pgrid = static_cast<unsigned>(c->num_sms * 8);

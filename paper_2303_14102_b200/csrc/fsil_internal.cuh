@@ -149,6 +149,9 @@ struct fsil_context {
   fsil::DevBuf tc_b;           // fp16 cluster-mean pieces + column bias (tcgen05 path)
   fsil::DevBuf nb_tmp;                   // neighbours when the caller passes no neighbour pointer
   fsil::DevBuf sub_x, sub_i;             // two-level certificate: the level-1 uncertain rows (x, ids)
+  fsil::DevBuf cand_rows;                // threshold mode: rows with 3-4 candidate neighbours (int4 records)
+  fsil::DevBuf thr_nn, thr_t;            // threshold mode: candidate clusters per cluster, t slots per row
+  int32_t tc_thr = 0;                    // this call's tensor-core pass ran in threshold mode (stats)
   int32_t tc_mmas = 0;                   // MMAs per K step of this call's tensor-core pass (stats)
   int64_t rescored = 0;                  // two-level certificate: rows re-scored at three MMAs
   fsil::DevBuf pair_rows, pair_count;    // tcgen05 top-3: rows resolved as a certified pair

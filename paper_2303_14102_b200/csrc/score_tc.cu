@@ -72,6 +72,12 @@ struct TcCfg {
 //   warpgroups 1-2 (warps 4..11): epilogue, two groups of four -- 120 registers
 //   warpgroups 3-4 (warps 12..19): converters -- 96 registers
 constexpr int kEpiWarp0 = 4, kConvWarp0 = 12;
+
+__device__ __forceinline__ bool elect_one_sync() {
+  uint32_t pred;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(pred));
+  return pred != 0;
+}
 #ifndef FSIL_EPI_REGS
 #define FSIL_EPI_REGS 136
 #endif
@@ -91,14 +97,22 @@ static_assert(4 * FSIL_WG0_REGS + 8 * FSIL_EPI_REGS + 8 * FSIL_CONV_REGS <= 20 *
 // T3: the epilogue also tracks the third-best key and the runner-up's column, so a row
 // whose top-2 is uncertain but whose third-best is clear resolves as a certified pair (two
 // fp64 foreign means) instead of a full K x D refinement (large cluster tables, C5).
-template <int BN, bool COS, bool PROF, int KC, int EG = 2, bool T3 = false>
+// THR: threshold mode (see "threshold mode" below): one extra K step per cluster block, the
+// converters add the row's t slots, the epilogue only harvests sign bits.
+template <int BN, bool COS, bool PROF, int KC, int EG = 2, bool T3 = false, bool THR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_bh,
                     const __grid_constant__ CUtensorMap tmap_bl, TcParams tp, int64_t ntiles) {
   griddep_wait();           // (PDL) prep_b's operands and every earlier phase are visible
   if (*tp.p.abort) return;  // K speculation missed: the call is repeated
   using C = TcCfg<BN>;
-  constexpr int NB = C::kBStg;
+  // B operand stages: the block-size default, or (threshold mode) more of them -- there a
+  // cluster block is a handful of MMAs, so the ring must cover the L2 latency of its refills
+  // (one-MMA threshold level: only the hi piece is staged, so the same ring space holds
+  // twice the stages at half the stride)
+  const int bstr = (THR && tp.thr_l1 == 1) ? C::kBBytes : 2 * C::kBBytes;
+  const int NB = THR && tp.nbs ? tp.nbs * (2 * C::kBBytes / bstr) : C::kBStg;
+  const int nbring = THR && tp.nbs ? tp.nbs : C::kBStg;  // ring space in (hi + lo) stage units
   // X stages: a TMA-filled fp32 box pair that the converters overwrite in place with
   // the fp16 A pieces (hi over box 0, lo over box 1), freed by the MMA commit
   const int NS = tp.nstg;
@@ -115,7 +129,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // group's buffers).  Otherwise the groups split the column chunks of every tile,
   // cycling through `nacc` buffers (4 when they fit the 512 TMEM columns).
   const uint32_t astride = tp.split ? 2 * BN : BN;  // TMEM columns per accumulator buffer
-  const bool TS = tp.ncb <= 2 && 4 * astride <= 512;
+  // (threshold mode: always alternate tiles -- its issuer interleaves the cluster blocks of
+  // two tiles, one per group, so neither group's buffer pair serialises the MMA stream)
+  const bool TS = THR || (tp.ncb <= 2 && 4 * astride <= 512);
   const uint32_t nacc = 4 * astride <= 512 ? 4 : 2;
   // A-resident: a tile's converted A chunks stay in their stages for every cluster
   // block (X read and converted once per tile); otherwise re-staged per block
@@ -140,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* stg = base;                      // [NS][kStgBytes]
   uint8_t* aslot = stg + NS * kStgBytes;    // [NSA][kStgBytes] decoupled A operand slots
   uint8_t* bring = aslot + NSA * kStgBytes; // [NB][b_hi | b_lo]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + NB * 2 * C::kBBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + nbring * 2 * C::kBBytes);
   uint64_t* stg_full = bars;               // [NS <= 8] X landed (TMA)
   uint64_t* stg_empty = bars + 8;          // [NS] stage free (MMA commit)
   uint64_t* a_full = bars + 16;            // [NS] A pieces written (converters) -- [NSA] decoupled
@@ -231,18 +247,106 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 2 && lane == 0) {
       // ---------------------------------------------------------- TMA producer: B pieces
       uint32_t n2 = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      // (threshold mode: a B block serves two tiles, see the issuer)
+      for (int64_t t = blockIdx.x; t < ntiles; t += (THR ? 2 : 1) * static_cast<int64_t>(gridDim.x)) {
         for (int cb = 0; cb < ncb; ++cb) {
           for (int kc = 0; kc < nkc; ++kc, ++n2) {
             const int sb = n2 % NB;
-            uint8_t* bs = bring + sb * 2 * C::kBBytes;
+            uint8_t* bs = bring + sb * bstr;
             TW(1, b_empty + sb, ((n2 / NB) & 1) ^ 1);
+            if (THR && tp.thr_l1 == 1) {  // one-MMA threshold level: the hi piece only
+              mbar_arrive_expect_tx(b_full + sb, C::kBBytes);
+              tma_load_2d(bs, &tmap_bh, b_full + sb, kc * BK, cb * BN);
+              continue;
+            }
             mbar_arrive_expect_tx(b_full + sb, 2 * C::kBBytes);
             tma_load_2d(bs, &tmap_bh, b_full + sb, kc * BK, cb * BN);
             tma_load_2d(bs + C::kBBytes, &tmap_bl, b_full + sb, kc * BK, cb * BN);
             TRACE((t - blockIdx.x) / gridDim.x, 8);
           }
         }
+      }
+    } else if (THR && warp == 1) {
+      // ---------------------------------------------------------- MMA issuer, threshold mode:
+      // one K chunk, A-resident tiles; a cluster block is D/16 + 1 (or 3 D/16 + 1) MMAs, so
+      // the issue path itself must stay short -- incremental ring positions (no division),
+      // operand descriptors by offset from one base per ring.  The whole warp runs the loop
+      // (every value warp-uniform: descriptors stay in uniform registers) and one elected
+      // lane issues.  Two tiles at a time, their cluster blocks interleaved: each B block is
+      // loaded once for both, tile 2i feeds epilogue group 0's buffer pair and tile 2i + 1
+      // group 1's, so both groups scan concurrently with no merge between them.
+      const int nks = (p.d + 15) >> 4;
+      const uint64_t da0 = desc_k_sw128(smem_u32(stg)), db0 = desc_k_sw128(smem_u32(bring));
+      const uint32_t xo = static_cast<uint32_t>(tp.thr) >> 3;  // the extra K step, in descriptor units (16 B)
+      const int l1 = tp.thr_l1;
+      int s1 = 0, sb = 0;
+      uint32_t ph1 = 0, phb = 0, ng0 = 0, ng1 = 0;
+      const int64_t nmine = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+      for (int64_t i = 0; i < nmine; i += 2) {
+        const bool two = i + 1 < nmine;
+        int s2 = s1 + 1;
+        uint32_t ph2 = ph1;
+        if (s2 == NS) {
+          s2 = 0;
+          ph2 ^= 1u;
+        }
+        const uint64_t dah0 = da0 + static_cast<uint32_t>(s1) * (kStgBytes >> 4);
+        const uint64_t dah1 = da0 + static_cast<uint32_t>(s2) * (kStgBytes >> 4);
+        TW(3, a_full + s1, ph1);
+        if (two) TW(3, a_full + s2, ph2);
+        for (int cb = 0; cb < ncb; ++cb) {
+          TW(3, b_full + sb, phb);
+          const uint64_t dbh = db0 + static_cast<uint32_t>(sb) * (static_cast<uint32_t>(bstr) >> 4), dbl = dbh + (C::kBBytes >> 4);
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            if (g == 1 && !two) break;
+            const uint32_t cntg = g ? ng1 : ng0;
+            const int ab = 2 * g + static_cast<int>(cntg & 1u);
+            TW(2, acc_empty + ab, ((cntg >> 1) & 1u) ^ 1u);
+            tc_fence_after();
+            const uint64_t dah = g ? dah1 : dah0, dal = dah + (kABytes >> 4);
+            const uint32_t dacc = tmem_base + ab * astride;
+            if (elect_one_sync()) {
+              if (l1 == 1) {  // hx.hm only
+                if (nks == 2) {
+                  mma_f16(dacc, dah, dbh, kIdesc, 0u);
+                  mma_f16(dacc, dah + 2, dbh + 2, kIdesc, 1u);
+                } else {
+                  for (int ks = 0; ks < nks; ++ks) mma_f16(dacc, dah + 2 * ks, dbh + 2 * ks, kIdesc, ks > 0 ? 1u : 0u);
+                }
+              } else {
+                for (int ks = 0; ks < nks; ++ks) {
+                  mma_f16(dacc, dah + 2 * ks, dbh + 2 * ks, kIdesc, ks > 0 ? 1u : 0u);
+                  mma_f16(dacc, dah + 2 * ks, dbl + 2 * ks, kIdesc, 1u);
+                  mma_f16(dacc, dal + 2 * ks, dbh + 2 * ks, kIdesc, 1u);
+                }
+              }
+              mma_f16(dacc, dah + xo, dbh + xo, kIdesc, 1u);  // + t_row + q_k
+              mma_commit(acc_full + ab);
+            }
+            __syncwarp();
+            if (g) ++ng1;
+            else ++ng0;
+          }
+          if (elect_one_sync()) {
+            mma_commit(b_empty + sb);
+            if (cb == ncb - 1) {
+              mma_commit(stg_empty + s1);
+              if (two) mma_commit(stg_empty + s2);
+            }
+          }
+          __syncwarp();
+          if (++sb == NB) {
+            sb = 0;
+            phb ^= 1u;
+          }
+        }
+        const int adv = two ? 2 : 1;
+        for (int a = 0; a < adv; ++a)
+          if (++s1 == NS) {
+            s1 = 0;
+            ph1 ^= 1u;
+          }
       }
     } else if (warp == 1 && lane == 0 && !(TS && NSA)) {
       // ---------------------------------------------------------- MMA issuer (column-split
@@ -287,6 +391,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               mma_f16(d_corr, desc_k_sw128(ah + off), desc_k_sw128(bl + off), kIdesc, tp.split ? acc0 : 1u);
               mma_f16(d_corr, desc_k_sw128(al + off), desc_k_sw128(bh + off), kIdesc, 1u);
             }
+            // threshold mode: the extra K step (hi pieces only) adds t_row + q_k
+            if (THR && kc == nkc - 1)
+              mma_f16(d_main, desc_k_sw128(ah + 2 * tp.thr), desc_k_sw128(bh + 2 * tp.thr), kIdesc, 1u);
             mma_commit(b_empty + sb);                               // B stage free when these retire
             if (!ares || cb == ncb - 1) mma_commit(stg_empty + s1);  // A stage: after its last use
           }
@@ -523,6 +630,58 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+    } else if (THR) {
+      // threshold mode (one K chunk, A-resident): the lean loop below, plus the extra K
+      // step's A slots -- chunk jx = the row's t slots (thr_kernel), chunk jx + 1 = 2^g --
+      // written by the thread whose half of the row holds those chunks
+      const uint32_t rd = hq * (BM * 128) + r * 128, wr = r * 128;
+      const bool tail_box = hq == 1;
+      const int jx = tp.thr >> 3;
+      const bool mine = (jx >> 2) == hq;
+      const uint32_t g1 = static_cast<uint32_t>(sc.thr_g + 15) << 10, g2 = g1 | (g1 << 16);  // fp16 2^g, twice
+      const bool hi_only = tp.thr_l1 == 1;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t row = t * BM + r;
+        const uint4 tsl = (mine && row < p.n) ? __ldg(tp.thr_t + row) : make_uint4(0u, 0u, 0u, 0u);
+        mbar_wait(stg_full + s1, ph1);
+        uint8_t* sbase = stg + s1 * kStgBytes;
+        float4 f[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) f[u] = *reinterpret_cast<const float4*>(sbase + rd + ((u ^ sw) << 4));
+        if (tail_box && 32 >= p.d) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) f[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        named_bar(5, 256);  // every read of the stage precedes the in-place writes
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const float v[8] = {f[2 * jj].x,     f[2 * jj].y,     f[2 * jj].z,     f[2 * jj].w,
+                              f[2 * jj + 1].x, f[2 * jj + 1].y, f[2 * jj + 1].z, f[2 * jj + 1].w};
+          uint32_t hw[4], lw[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 xx = __fmul2_rn(make_float2(v[2 * e], v[2 * e + 1]), sx2);
+            const __half2 h = __float22half2_rn(xx);
+            const float2 res = __ffma2_rn(__half22float2(h), neg1, xx);  // exact
+            const __half2 l = __float22half2_rn(res);
+            hw[e] = *reinterpret_cast<const uint32_t*>(&h);
+            lw[e] = *reinterpret_cast<const uint32_t*>(&l);
+          }
+          const uint32_t pos = wr + (((4 * hq + jj) ^ sw) << 4);
+          uint4 hv = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+          if (mine && 4 * hq + jj == jx) hv = tsl;
+          if (mine && 4 * hq + jj == jx + 1) hv = make_uint4(g2, g2, g2, g2);
+          *reinterpret_cast<uint4*>(sbase + pos) = hv;
+          if (!hi_only) *reinterpret_cast<uint4*>(sbase + BM * 128 + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full + s1);
+        if (++s1 == NS) {
+          s1 = 0;
+          ph1 ^= 1;
+        }
+      }
     } else if (ext && !myscr && xpasses == 1) {
       // lean loop (every stage converted exactly once, nothing else): the per-thread
       // swizzled offsets are loop invariant
@@ -674,6 +833,141 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int grp = (warp - kEpiWarp0) >> 2;  // epilogue group 0 / 1
     uint32_t na = 0, nt = 0, ng = 0;
     constexpr int NQ = BN / 32;
+    if (THR) {
+      // ---- threshold mode: acc'' = x~.mu~_k + t_row + q_k; a clear sign bit = column k is
+      // within the row's certified threshold.  Sign bits of a 32-column chunk are packed by
+      // funnel shifts (four independent chains), then only the set bits are walked.
+      const int64_t tstep = (TS ? EG : 1) * static_cast<int64_t>(gridDim.x);
+      auto fetch_own = [&](int64_t tt) {
+        const int64_t rr = tt * BM + r;
+        return (tt < ntiles && rr < p.n) ? __ldg(p.dense + rr) : -1;
+      };
+      int own_n = fetch_own(blockIdx.x + (TS ? grp : 0) * static_cast<int64_t>(gridDim.x));
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
+        const int tb = nt & 1;
+        if (TS && static_cast<int>(nt % EG) != grp) continue;  // another group takes this tile
+        const int64_t row = t * BM + r;
+        const bool valid = row < p.n;
+        const int own = own_n;
+        own_n = fetch_own(t + tstep);
+        // per row: up to four (chunk base, hit mask) slots, filled without branches; the
+        // masks are decoded into columns once per tile
+        int nh = 0, k1 = 0, k2 = 0, k3 = 0, k4 = 0;
+        uint32_t h1 = 0, h2 = 0, h3 = 0, h4 = 0;
+        for (int cb = 0; cb < ncb; ++cb) {
+          int ab;
+          uint32_t ph;
+          if (TS) {
+            ab = 2 * grp + (ng & 1);
+            ph = (ng >> 1) & 1;
+            ++ng;
+          } else {  // (BN = 128, one accumulator per block: four buffers)
+            ab = na & 3;
+            ph = (na >> 2) & 1;
+            ++na;
+          }
+          TW(8, acc_full + ab, ph);
+          const long long ts0 = dbgp ? clock64() : 0;
+          tc_fence_after();
+          auto harvest = [&](const uint32_t(&v)[32], int k0) {
+            uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              m0 = __funnelshift_l(v[j], m0, 1);  // (m << 1) | sign
+              m1 = __funnelshift_l(v[8 + j], m1, 1);
+              m2 = __funnelshift_l(v[16 + j], m2, 1);
+              m3 = __funnelshift_l(v[24 + j], m3, 1);
+            }
+            uint32_t hits = ~((m0 << 24) | (m1 << 16) | (m2 << 8) | m3);  // bit 31 - j: element j
+            const uint32_t orel = static_cast<uint32_t>(own - k0);          // the own column never counts
+            hits &= ~(orel < 32u ? 0x80000000u >> orel : 0u);
+            const bool any = hits != 0u;
+            h4 = (any && nh == 3) ? hits : h4;
+            k4 = (any && nh == 3) ? k0 : k4;
+            h3 = (any && nh == 2) ? hits : h3;
+            k3 = (any && nh == 2) ? k0 : k3;
+            h2 = (any && nh == 1) ? hits : h2;
+            k2 = (any && nh == 1) ? k0 : k2;
+            h1 = (any && nh == 0) ? hits : h1;
+            k1 = (any && nh == 0) ? k0 : k1;
+            nh += any ? 1 : 0;
+          };
+          const int q0 = TS ? 0 : grp, qs = TS ? 1 : 2;
+          const uint32_t tb0 = tmem_base + ab * astride + (static_cast<uint32_t>(quad * 32) << 16);
+#pragma unroll 1
+          for (int q = q0; q < NQ; q += 2 * qs) {  // two chunks per TMEM wait
+            uint32_t v[32], w[32];
+            const bool two = q + qs < NQ;
+            tmem_ld32_issue(tb0 + q * 32, v);
+            if (two) tmem_ld32_issue(tb0 + (q + qs) * 32, w);
+            tmem_ld_wait2(v, w);
+            harvest(v, cb * BN + q * 32);
+            if (two) harvest(w, cb * BN + (q + qs) * 32);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_empty + ab);
+          if (dbgp && warp == kEpiWarp0 && lane == 0) atomicAdd(dbgp + 12, static_cast<unsigned long long>(clock64() - ts0));
+        }
+        // decode: columns of the set bits in ascending order (slots are in scan order), the
+        // padding columns >= K dropped; more than four chunks with hits -> "more than four"
+        int cnt = 0, c1 = -1, c2 = -1, c3 = -1, c4 = -1;
+        {
+          auto decode = [&](uint32_t hm, int kb) {
+            while (hm) {
+              const int j = __clz(hm);
+              hm &= ~(0x80000000u >> j);
+              const int col = kb + j;
+              if (col < p.k) {
+                c4 = cnt == 3 ? col : c4;
+                c3 = cnt == 2 ? col : c3;
+                c2 = cnt == 1 ? col : c2;
+                c1 = cnt == 0 ? col : c1;
+                ++cnt;
+              }
+            }
+          };
+          decode(h1, k1);
+          decode(h2, k2);
+          decode(h3, k3);
+          decode(h4, k4);
+          if (nh > 4) cnt = 5;
+        }
+        if (!TS) {  // merge the two column halves (group 1 -> smem -> group 0)
+          int* pt = reinterpret_cast<int*>(part + tb * 5 * BM);  // double-buffered by tile parity
+          if (grp == 1) {
+            pt[0 * BM + r] = cnt;
+            pt[1 * BM + r] = c1;
+            pt[2 * BM + r] = c2;
+            pt[3 * BM + r] = c3;
+            pt[4 * BM + r] = c4;
+          }
+          named_bar(1, 256);
+          if (grp == 1) continue;
+          const int ocnt = pt[0 * BM + r];
+          const int os[4] = {pt[1 * BM + r], pt[2 * BM + r], pt[3 * BM + r], pt[4 * BM + r]};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {  // the other half's hits follow this half's
+            const int pos = cnt + i;
+            c1 = pos == 0 ? os[i] : c1;
+            c2 = pos == 1 ? os[i] : c2;
+            c3 = pos == 2 ? os[i] : c3;
+            c4 = pos == 3 ? os[i] : c4;
+          }
+          cnt += ocnt;
+        }
+        if (valid) {
+          // the reference's neighbour is among the hits.  One -> certain.  Two to four ->
+          // their columns go to cand_rows[row] and the count into the top bits of nb[row];
+          // none (a row outside the slot range) or more -> code 1.  thr_resolve_kernel
+          // (finalize.cu) scans nb afterwards: fp64 means of the candidates, or the fp64
+          // refinement over all K for code 1 -- no atomics on this path.
+          const int code = cnt == 1 ? 0 : (cnt >= 2 && cnt <= 4) ? cnt : 1;
+          p.nb[row] = (cnt >= 1 ? c1 : (own == 0 ? 1 : 0)) | (code << 28);
+          if (code >= 2) tp.cand_rows[row] = make_int4(c2, c3, c4, 0);
+        }
+      }
+    } else {
     // Per-row inputs (own cluster; ||x||^2 when the aggregation pass provides it) are
     // fetched from global memory one tile ahead of their use, so their DRAM latency
     // overlaps the current tile instead of serialising with it.
@@ -854,6 +1148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (dbgp && warp == kEpiWarp0 && lane == 0) atomicAdd(dbgp + 13, static_cast<unsigned long long>(clock64() - tf0));
       if (quad == 0 && lane == 0) TRACE(nt, 7);
     }
+    }  // !THR
   }
 
   if (dbgp && lane == 0) {
@@ -905,7 +1200,26 @@ namespace {
 // ---------------------------------------------------------------- prep --------
 // Global power-of-two scalings chosen so max|x~| and max|mu~| lie in [2^14, 2^15):
 // ex from max|x| of the shard, em from max|mu_kl| (derive's bound[2]).
-__device__ __forceinline__ int scale_exp(float m) { return m > 0.f ? ilogbf(m) - 14 : 0; }
+__device__ __forceinline__ int scale_exp(float m, int target = 14) { return m > 0.f ? ilogbf(m) - target : 0; }
+
+// fp16 slots of the threshold mode's extra K step: a value v (accumulator units) is carried
+// as 6 equal high slots + a middle + a low slot, each times 2^g from the other operand:
+// v ~ (6 h + m + l) 2^g, residuals exact in fp64, the low slot rounded up (so the carried
+// value is >= v up to the slot's subnormal quantum).  |v| <= 6 * 65504 * 2^g or *ok = false.
+__device__ __forceinline__ void thr_slots(double v, int g, __half (&out)[8], bool* ok) {
+  const double s = ldexp(1.0, g);
+  const double h0 = v / (6.0 * s);
+  *ok = fabs(h0) <= 65504.0;
+  const __half h = __double2half(h0);
+  const double r1 = v - 6.0 * s * static_cast<double>(__half2float(h));
+  const __half m = __double2half(r1 / s);
+  const double r2 = r1 - s * static_cast<double>(__half2float(m));
+  const __half l = __float2half_ru(__double2float_ru(r2 / s));
+#pragma unroll
+  for (int i = 0; i < 6; ++i) out[i] = h;
+  out[6] = m;
+  out[7] = l;
+}
 
 // B pieces: mu~ = mu * 2^-em split into fp16 hi + lo, [Kp][Dp] zero padded; column
 // bias for the ranking (sqeuclid p_k, cosine 0, padding +inf); per-cluster norms (the
@@ -913,19 +1227,33 @@ __device__ __forceinline__ int scale_exp(float m) { return m > 0.f ? ilogbf(m) -
 __global__ void prep_b_kernel(const double* __restrict__ stats, const float* __restrict__ bound,
                               const float* __restrict__ xmax, int k, int d, int kp, int dp, bool cos,
                               __half* bh, __half* bl, float* colbias, __half* munorm,
-                              TcScale* scale, const int* abort, bool unit_ok, float* lmnorm, float* lmmax) {
+                              TcScale* scale, const int* abort, bool unit_ok, float* lmnorm, float* lmmax,
+                              int thr_dx) {
   griddep_wait();
   if (*abort) return;
   const int c = blockIdx.x;
-  const int em = scale_exp(bound[2]);
+  // threshold mode: operands scaled to [2^12, 2^13) so dots (<= D 2^26) and the extra K
+  // step's t and q slots stay within the fp16 slot range; em is raised further when p_max
+  // alone would push |q| = p/2^(ex+em+1) past 2^32 (the mu pieces' floor term grows with it)
+  const int tgt = thr_dx ? 12 : 14;
+  int em = scale_exp(bound[2], tgt);
+  const float xm = *xmax;
+  // x needs no scaling when max|x| lies in [0.5, 2^14): x~ = x stays below fp16's max
+  // and the subnormal floor of the small elements is in the per-row bound (floor_x);
+  // the multiply-free converters then skip the multiply
+  const int ex = (unit_ok && xm >= 0.5f && xm < 16384.f) ? 0 : scale_exp(xm, tgt);
+  int thr_g = 0;
+  if (thr_dx) {
+    const float pm = bound[1];
+    if (pm > 0.f) em = max(em, ilogbf(pm) + 1 - 33 - ex);
+    const float qmax = ldexpf(pm, -(ex + em + 1));
+    const float rmax = fmaxf(qmax, ldexpf(static_cast<float>(d), 26));
+    thr_g = min(15, max(0, ilogbf(rmax) + 2 - 18));
+  }
   const float smu = ldexpf(1.0f, -em);
   if (c == 0 && threadIdx.x == 0) {
-    const float xm = *xmax;
-    // x needs no scaling when max|x| lies in [0.5, 2^14): x~ = x stays below fp16's max
-    // and the subnormal floor of the small elements is in the per-row bound (floor_x);
-    // the multiply-free converters then skip the multiply
-    const int ex = (unit_ok && xm >= 0.5f && xm < 16384.f) ? 0 : scale_exp(xm);
     TcScale t;
+    t.thr_g = thr_g;
     t.sx = ldexpf(1.0f, -ex);
     t.smul = ldexpf(1.0f, ex + em);
     t.smul64 = ldexp(1.0, ex + em);
@@ -950,6 +1278,22 @@ __global__ void prep_b_kernel(const double* __restrict__ stats, const float* __r
       lo = static_cast<float>(mu - static_cast<double>(h));
       const double rem = mu - static_cast<double>(h);
       lm2 = fma(rem, rem, lm2);
+    }
+    if (thr_dx && l >= thr_dx && l < thr_dx + 16) {
+      // extra K step (hi piece only): columns dx..dx+7 meet the row's t slots -> 2^g;
+      // columns dx+8..dx+15 carry q_k = -p_k / 2^(ex+em+1) against the A side's 2^g
+      // (padding clusters: the most negative value, never within a threshold)
+      const int i = l - thr_dx;
+      if (i < 8) {
+        h = ldexpf(1.0f, thr_g);
+      } else if (c < k) {
+        __half qs[8];
+        bool ok;
+        thr_slots(-(stats[k + c] / n) * ldexp(1.0, -(ex + em + 1)), thr_g, qs, &ok);
+        h = __half2float(qs[i - 8]);
+      } else {
+        h = -65504.0f;
+      }
     }
     bh[static_cast<int64_t>(c) * dp + l] = __float2half_rn(h);
     bl[static_cast<int64_t>(c) * dp + l] = __float2half_rn(lo);
@@ -980,12 +1324,215 @@ __global__ void prep_b_kernel(const double* __restrict__ stats, const float* __r
   }
 }
 
+// ---------------------------------------------------------------- threshold mode ----
+// (sqeuclid, D <= 48, several cluster blocks: C4.)  The scan's per-element work -- key,
+// own-column exclusion, running top-2, argmin: 1 FFMA + 7 ALU operations -- paces the
+// single-CTA kernel there (ncu: ALU pipe 77 %, tensor pipe 15 %).  Threshold mode moves the
+// comparison into the tensor core.  Per row, thr_kernel evaluates in fp64 the ranking key
+// m'_k = p_k - 2 x.mu_k of a few clusters near the row's own (nn_list_kernel: the centroid's
+// nearest centroids); their minimum T is an upper bound of the row's true minimum over
+// k != own.  One extra K step adds t_row = (T + margin) / 2^(ex+em+1) and q_k = -p_k /
+// 2^(ex+em+1) to the accumulator x~.mu~_k, so
+//     acc'' >= 0   <=>   m'_k (as the tensor core sees it) <= T + margin,
+// and with `margin` = the certified error of that comparison every column that can be the
+// reference's neighbour has a clear sign bit.  The epilogue packs the 32 sign bits of a chunk
+// with one funnel shift per element and only walks the set bits: one hit -> that column is
+// the neighbour, certain; two -> a certified pair (two fp64 means decide, pair_kernel); none
+// or more -> the fp64 refinement over all K.  a_i, b_i, s_i come from the exact pass as
+// always.  Which clusters enter T only affects how many rows have a single hit.
+constexpr int kThrM = 16;  // candidate clusters per row
+constexpr int kPieceRowsTc = 2048;  // = aggregate.cu's kPieceRows (rows per label-sorted piece)
+
+// One block per cluster c: the kThrM clusters k != c with the smallest p_k - 2 mu_c.mu_k
+// (fp32: a heuristic choice, no bound depends on it); fewer than kThrM others: repeated.
+__global__ void __launch_bounds__(256) nn_list_kernel(const float* __restrict__ mu32, const float* __restrict__ p32,
+                                                      int k, int d, int dp, int32_t* __restrict__ nn,
+                                                      const int* abort) {
+  griddep_wait();
+  if (*abort) return;
+  extern __shared__ float nsm[];  // [dp] mu_c, [k] keys
+  float* muc = nsm;
+  float* key = nsm + dp;
+  __shared__ float rk[8];
+  __shared__ int ri[8];
+  const int c = blockIdx.x;
+  for (int l = threadIdx.x; l < dp; l += blockDim.x) muc[l] = mu32[static_cast<int64_t>(c) * dp + l];
+  __syncthreads();
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    const float* mj = mu32 + static_cast<int64_t>(j) * dp;
+    float dot = 0.f;
+    for (int l = 0; l < d; ++l) dot = fmaf(muc[l], mj[l], dot);
+    key[j] = j == c ? INFINITY : p32[j] - 2.0f * dot;
+  }
+  __syncthreads();
+  int last = c == 0 ? 1 : 0;
+  for (int r = 0; r < kThrM; ++r) {
+    float bk = INFINITY;
+    int bi = -1;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+      const float v = key[j];
+      if (v < bk) {
+        bk = v;
+        bi = j;
+      }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ok = __shfl_xor_sync(0xffffffffu, bk, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (oi >= 0 && (bi < 0 || ok < bk || (ok == bk && oi < bi))) {
+        bk = ok;
+        bi = oi;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      rk[threadIdx.x >> 5] = bk;
+      ri[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < 8; ++w)
+        if (ri[w] >= 0 && (bi < 0 || rk[w] < bk || (rk[w] == bk && ri[w] < bi))) {
+          bk = rk[w];
+          bi = ri[w];
+        }
+      if (bi < 0) bi = last;  // fewer than kThrM other clusters (or non-finite keys): repeat
+      last = bi;
+      nn[c * kThrM + r] = bi;
+      key[bi] = INFINITY;
+    }
+    __syncthreads();
+  }
+}
+
+// Per row: T = min over the own cluster's candidate list of the key p_k - 2 x.mu_k (fp32, its
+// rounding bounded below), the certified margin of the tensor-core comparison, and the 8 fp16
+// A slots of t_row.  One warp per piece of the label-sorted rows (<= 2048 rows of one
+// cluster): the candidates' means sit in shared memory (broadcast reads), one row per lane.
+template <int D>
+__global__ void __launch_bounds__(256) thr_kernel(const float* __restrict__ X, const int32_t* __restrict__ rows,
+                                                  int k, const int64_t* __restrict__ seg_begin,
+                                                  const int64_t* __restrict__ seg_end,
+                                                  const int64_t* __restrict__ piece_start, int piece_rows,
+                                                  const float* __restrict__ mu32, const float* __restrict__ p32,
+                                                  int dp, const int32_t* __restrict__ nn,
+                                                  const TcScale* __restrict__ scale, float cdot,
+                                                  const float* __restrict__ lmmax, uint4* __restrict__ thr_t,
+                                                  const int* abort) {
+  griddep_wait();
+  if (*abort) return;
+  __shared__ __align__(16) float cm[8][kThrM][D];  // per warp: candidate means (fp32 roundings)
+  __shared__ float cp[8][kThrM];                   // ... and their p_k
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t total = piece_start[k];
+  const TcScale sc = *scale;
+  const double u = 5.9604645e-8;
+  const double inv2s = 1.0 / (2.0 * sc.smul64);
+  const double quantum = ldexp(1.0, sc.thr_g - 23) / inv2s;  // the slots' subnormal quantum, key units
+  // one-MMA level (lmmax given): max_k ||mu_k - hm_k|| in mu units
+  const double lm_any = lmmax ? static_cast<double>(*lmmax) * (1.0 + 1e-6) : -1.0;
+  const float2 sx2 = make_float2(sc.sx, sc.sx), neg1 = make_float2(-1.f, -1.f);
+  for (int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; p < total; p += nw) {
+    int lo = 0, hi = k - 1;  // cluster owning piece p: largest c with piece_start[c] <= p
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (piece_start[mid] <= p) lo = mid;
+      else hi = mid - 1;
+    }
+    const int c = lo;
+    const int64_t b0 = seg_begin[c] + (p - piece_start[c]) * piece_rows;
+    const int64_t b1 = min(seg_end[c], b0 + piece_rows);
+    __syncwarp();
+    for (int j = 0; j < kThrM; ++j) {
+      const int kk = nn[c * kThrM + j];
+      for (int l = lane; l < D; l += 32) cm[wib][j][l] = mu32[static_cast<int64_t>(kk) * dp + l];
+      if (lane == 0) cp[wib][j] = p32[kk];
+    }
+    __syncwarp();
+    for (int64_t pos = b0 + lane; pos < b1; pos += 32) {
+      const int64_t r = rows[pos];
+      const float4* xr = reinterpret_cast<const float4*>(X + r * D);
+      float2 x[D / 2];
+      float2 ss2 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < D / 4; ++q) {
+        const float4 f = ldg_stream(xr + q);
+        x[2 * q] = make_float2(f.x, f.y);
+        x[2 * q + 1] = make_float2(f.z, f.w);
+        ss2 = __ffma2_rn(x[2 * q], x[2 * q], ss2);
+        ss2 = __ffma2_rn(x[2 * q + 1], x[2 * q + 1], ss2);
+      }
+      // one-MMA level: ||lx||^2, lx = x~ - fp16(x~) (exact in fp32), in scaled units
+      float2 ll2 = make_float2(0.f, 0.f);
+      if (lm_any >= 0.0) {
+#pragma unroll
+        for (int q = 0; q < D / 2; ++q) {
+          const float2 xx = __fmul2_rn(x[q], sx2);
+          const float2 res = __ffma2_rn(__half22float2(__float22half2_rn(xx)), neg1, xx);
+          ll2 = __ffma2_rn(res, res, ll2);
+        }
+      }
+      float T = INFINITY;
+#pragma unroll 4
+      for (int j = 0; j < kThrM; ++j) {
+        float2 a = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < D / 4; ++q) {
+          const float4 m = *reinterpret_cast<const float4*>(&cm[wib][j][4 * q]);
+          a = __ffma2_rn(x[2 * q], make_float2(m.x, m.y), a);
+          a = __ffma2_rn(x[2 * q + 1], make_float2(m.z, m.w), a);
+        }
+        T = fminf(T, fmaf(-2.0f, a.x + a.y, cp[wib][j]));
+      }
+      const double ss = static_cast<double>(ss2.x + ss2.y);
+      const double xn = sqrt(ss) * (1.0 + (D + 4) * u);  // >= ||x||
+      // columns whose mean distance clamps to 0 tie with a clamped minimum: keep every
+      // key <= -||x||^2 within the threshold too (squared_euclidean.cpp:81)
+      const double Tm = fmax(static_cast<double>(T), -ss * (1.0 - (D + 4) * u));
+      // T's own rounding: fp32 means (u each), the D-term fp32 dot (gamma_D), p_k (u), the
+      // final fma (u) -- (2D + 5) u ||x|| max||mu|| + 3u max p.  The comparison: the three-MMA
+      // dot bound (score_tc's cdot, the pieces' subnormal floors); the extra K step -- one
+      // more MMA over |acc| + |t| + |q| (10.5u), the t and q slots' representation (2^-31
+      // relative, their subnormal quantum) -- 24u of the magnitudes
+      const double xm = xn * static_cast<double>(sc.mu_max);
+      const double mag = fabs(Tm) + static_cast<double>(sc.p_max) + 2.0 * xm;
+      const double edot = static_cast<double>(cdot) * xm + static_cast<double>(sc.floor_x) * sc.mu_max +
+                          static_cast<double>(sc.floor_mu) * xn;
+      const double e_t = (2.0 * D + 5.0) * u * xm + 3.0 * u * static_cast<double>(sc.p_max);
+      // one-MMA level: x~.mu~ - hx.hm = hx.Lm + lx.mu~ with mu~ = hm + Lm, so per column
+      // |dropped| <= (||x|| + ||lx||) ||Lm_k|| + ||lx|| ||mu_k|| (x and mu units)
+      double e_drop = 0.0;
+      if (lm_any >= 0.0) {
+        const double lxn = sqrt(static_cast<double>(ll2.x + ll2.y)) * (1.0 + (D + 4) * u) / static_cast<double>(sc.sx);
+        e_drop = (xn + lxn) * lm_any + lxn * static_cast<double>(sc.mu_max);
+      }
+      const double margin = 1.01 * (2.0 * (edot + e_drop) + e_t + 24.0 * u * mag + 4.0 * quantum);
+      __half sl[8];
+      bool ok;
+      thr_slots((Tm + margin) * inv2s, sc.thr_g, sl, &ok);
+      if (!ok || !(ss < INFINITY)) {
+        // outside the slot range (or a non-finite row): no column can hit, so the row
+        // goes to the fp64 refinement
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sl[i] = __float2half_rn(-65504.0f);
+      }
+      uint4 o;
+      o.x = static_cast<uint32_t>(__half_as_ushort(sl[0])) | (static_cast<uint32_t>(__half_as_ushort(sl[1])) << 16);
+      o.y = static_cast<uint32_t>(__half_as_ushort(sl[2])) | (static_cast<uint32_t>(__half_as_ushort(sl[3])) << 16);
+      o.z = static_cast<uint32_t>(__half_as_ushort(sl[4])) | (static_cast<uint32_t>(__half_as_ushort(sl[5])) << 16);
+      o.w = static_cast<uint32_t>(__half_as_ushort(sl[6])) | (static_cast<uint32_t>(__half_as_ushort(sl[7])) << 16);
+      thr_t[r] = o;
+    }
+  }
+}
+
 int pick_bn(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : 128; }
 
 // Shared memory with `nstg` X staging stages: operand ring, staging ring, barriers,
 // meta_xi, merge partials, own clusters, column bias (fp32) and norms (fp16).
-size_t tc_smem(int bn, int kp, int nstg) {
-  const size_t bring = bn <= 32 ? TcCfg<32>::kBRing : bn <= 64 ? TcCfg<64>::kBRing : TcCfg<128>::kBRing;
+size_t tc_smem(int bn, int kp, int nstg, int nbs = 0) {
+  size_t bring = bn <= 32 ? TcCfg<32>::kBRing : bn <= 64 ? TcCfg<64>::kBRing : TcCfg<128>::kBRing;
+  if (nbs) bring = static_cast<size_t>(nbs) * 2 * bn * 128;
   return 1024 + bring + static_cast<size_t>(nstg) * kStgBytes + 50 * 8 + 4 * BM * 8 + 10 * BM * 4 + 2 * BM * 4 +
          static_cast<size_t>(ncb_bn_pad(kp)) * 4 + static_cast<size_t>(kp) * 2 + 16;
 }
@@ -1008,11 +1555,11 @@ static int pair_l1(const fsil_context* c) {
   return c->X64 ? 3 : l1_env;
 }
 
-template <int BN, bool COS, int KC = 32, int EG = 2, bool T3 = false>
+template <int BN, bool COS, int KC = 32, int EG = 2, bool T3 = false, bool THR = false>
 void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                const TcParams& tp, int64_t ntiles, bool rec = true) {
-  auto kern = tp.dbg ? score_tc_kernel<BN, COS, true, KC, EG, T3> : score_tc_kernel<BN, COS, false, KC, EG, T3>;
-  const size_t smem = tc_smem(BN, tp.ncb * BN, tp.nstg + tp.nsa);
+  auto kern = tp.dbg ? score_tc_kernel<BN, COS, true, KC, EG, T3, THR> : score_tc_kernel<BN, COS, false, KC, EG, T3, THR>;
+  const size_t smem = tc_smem(BN, tp.ncb * BN, tp.nstg + tp.nsa, THR ? tp.nbs : 0);
   if (c->timing && rec) {  // the kernel alone, for the roofline (ms_score_kernel)
     FSIL_CUDA(cudaEventRecord(c->ev[7], c->stream));
     c->ev7_recorded = true;
@@ -1155,8 +1702,17 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
   // unit x scale exactly where the converters take the multiply-free path (the
   // three-group kernel); its subnormal floor is bounded per row (floor_x / ||x||)
   const bool unit_ok = eg3;
+  // threshold mode (see "threshold mode" above): squared Euclidean, one K chunk with a free
+  // 16-column K step (D in {16, 32, 48}), several cluster blocks (A-resident tiles), the
+  // label-sorted aggregation's row order for thr_kernel; FSIL_TC_THR=0 turns it off
+  static const bool thr_env = [] {
+    const char* e = std::getenv("FSIL_TC_THR");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool thr = thr_env && !cos && !pair && bn == 128 && ncb > 1 && nkc == 1 && c->d % 16 == 0 && c->d <= 48 &&
+                   c->agg_path == 2 && !c->X64 && tp.nstg >= 2 && c->k <= 8192;
   launch_pdl(c, prep_b_kernel, kp, 128, 0, p.stats, c->bound.as<float>(), c->xmax.as<float>(), c->k, c->d, kp, dp,
-             cos, bh, bl, colbias, munorm, scale, p.abort, unit_ok, lmnorm, lmmax);
+             cos, bh, bl, colbias, munorm, scale, p.abort, unit_ok, lmnorm, lmmax, thr ? c->d : 0);
   tp.lmnorm = lmnorm;
   tp.lmmax = lmmax;
   const CUtensorMap mx = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, c->X, c->d, c->n, c->d * 4ull, 32, BM);
@@ -1302,9 +1858,58 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     return;
   }
   c->tc_mmas = 3;
+  if (thr) {
+    c->thr_nn.ensure(static_cast<size_t>(c->k) * kThrM * sizeof(int32_t));
+    c->thr_t.ensure(static_cast<size_t>(c->n) * sizeof(uint4));
+    int32_t* nn = c->thr_nn.as<int32_t>();
+    launch_pdl(c, nn_list_kernel, c->k, 256, (static_cast<size_t>(c->dp) + c->k) * sizeof(float), p.mu32, p.p32, c->k,
+               c->d, static_cast<int>(c->dp), nn, p.abort);
+    const int64_t* seg_begin = c->seg_start.as<int64_t>();
+    const int64_t* seg_end = seg_begin + c->k + 1;
+    const int64_t* piece_start = c->piece_start.as<int64_t>() + c->k + 2;
+    const int tgrid = c->num_sms * 8;
+    uint4* tt = c->thr_t.as<uint4>();
+    // MMAs per K step: 1 (default: hx.hm; the dropped pieces, ~2^-11 relative, widen each
+    // row's margin -- a few more two-candidate rows, a third of the tensor and operand
+    // traffic) or 3 (FSIL_THR_L1=3: fp16x3)
+    static const int thr_l1_env = [] { const char* e = std::getenv("FSIL_THR_L1"); return e && std::atoi(e) == 3 ? 3 : 1; }();
+    tp.thr_l1 = thr_l1_env;
+    if (tp.thr_l1 == 1) {
+      tp.cdot = 1.05f * (12.0f + 2.0f * kMmaUlp * steps + 1.0f) * u;
+      c->tc_mmas = 1;
+    }
+#define FSIL_THR_K(DD)                                                                                            \
+  launch_pdl(c, thr_kernel<DD>, tgrid, 256, 0, p.X, c->sort_vals.as<int32_t>(), c->k, seg_begin, seg_end,       \
+             piece_start, kPieceRowsTc, p.mu32, p.p32, static_cast<int>(c->dp), nn, scale, tp.cdot,           \
+             tp.thr_l1 == 1 ? lmmax : nullptr, tt, p.abort)
+    if (c->d == 16) FSIL_THR_K(16);
+    else if (c->d == 32) FSIL_THR_K(32);
+    else FSIL_THR_K(48);
+#undef FSIL_THR_K
+    tp.thr = c->d;
+    tp.thr_t = tt;
+    tp.lean = 1;  // the threshold epilogue fetches the own cluster itself; no hand-off
+    // stages: a tile is one A stage for all its cluster blocks, so two or three suffice;
+    // the B ring takes the rest (FSIL_THR_NB / FSIL_THR_NS: experiments)
+    {
+      static const int nb_env = [] { const char* e = std::getenv("FSIL_THR_NB"); return e ? std::atoi(e) : 2; }();
+      static const int ns_env = [] { const char* e = std::getenv("FSIL_THR_NS"); return e ? std::atoi(e) : 4; }();
+      // (ring space in hi + lo stage units: the one-MMA level fits two hi-only stages in each,
+      // and the barrier arrays hold four B stages)
+      int nbs = std::max(1, std::min(thr_l1_env == 1 ? 2 : 4, nb_env)), ns = std::max(2, std::min(tp.nstg, ns_env));
+      while (nbs > 1 && tc_smem(bn, kp, ns, nbs) > c->smem_optin) --nbs;
+      tp.nbs = nbs;
+      tp.nstg = ns;
+    }
+    c->tc_thr = 1;
+    c->cand_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int4));
+    tp.cand_rows = c->cand_rows.as<int4>();
+    launch_tc<128, false, 32, 2, false, true>(c, mx, mh, ml, tp, ntiles);
+  }
   // K <= 24 at BN = 32: the epilogue scans only the first 16 / 24 columns
   const int kc_scan = bn == 32 && c->k <= 16 ? 16 : bn == 32 && c->k <= 24 ? 24 : 32;
-  if (cos) {
+  if (thr) {
+  } else if (cos) {
     if (eg3 && kc_scan == 16) launch_tc<32, true, 16, 3>(c, mx, mh, ml, tp, ntiles);
     else if (eg3 && kc_scan == 24) launch_tc<32, true, 24, 3>(c, mx, mh, ml, tp, ntiles);
     else if (eg3) launch_tc<32, true, 32, 3>(c, mx, mh, ml, tp, ntiles);

@@ -31,6 +31,7 @@ struct TcScale {
   float floor_x;          // fp16 subnormal floor of the x pieces, per unit ||mu|| (absolute in x)
   float mu_max;           // max ||mu_k||
   float p_max;            // max p_k (sqeuclid)
+  int thr_g;              // threshold mode: the extra K step's power-of-two slot exponent g
 };
 
 struct TcParams {
@@ -54,6 +55,14 @@ struct TcParams {
   unsigned long long* pair_count;
   const float* lmnorm;    // [ncb*BN] ||mu_k - hm_k|| (mu units, rounded up): one-MMA level bound
   const float* lmmax;     // max_k lmnorm
+  // threshold mode (sqeuclid, D <= 48, several cluster blocks; score_tc.cu "threshold scan"):
+  // one extra K step adds t_row + q_k to every accumulator, so the sign bit alone says
+  // whether column k is within the row's certified threshold
+  int thr;                // 0 off; else the first fp16 column of the extra K step (16 ceil(D/16))
+  const uint4* thr_t;     // [n] per row: the 8 fp16 A slots of t_row (thr_kernel)
+  int nbs;                // threshold mode: B operand stages (0: the block-size default)
+  int thr_l1;             // threshold mode: MMAs per K step -- 3 (fp16x3) or 1 (hx.hm only; the dropped pieces are in the row's margin)
+  int4* cand_rows;        // [n] threshold mode: a row's second to fourth candidate columns (when nb[row]'s top bits say 2..4)
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) {
