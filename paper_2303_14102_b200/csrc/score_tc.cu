@@ -153,10 +153,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 1024-byte alignment by a pointer offset (keeps the shared address space visible to
   // the compiler: LDS/STS rather than generic accesses)
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* stg = base;                      // [NS][kStgBytes]
-  uint8_t* aslot = stg + NS * kStgBytes;    // [NSA][kStgBytes] decoupled A operand slots
+  // (threshold mode at D <= 32 with the hi piece only: a stage is one 16 KB box)
+  const int stgb = THR ? tp.astg : kStgBytes;
+  const bool bres = THR && tp.bres;  // the whole hi-piece table resident: [ncb][kBBytes], loaded once
+  uint8_t* stg = base;                      // [NS][stgb]
+  uint8_t* aslot = stg + NS * stgb;         // [NSA][kStgBytes] decoupled A operand slots
   uint8_t* bring = aslot + NSA * kStgBytes; // [NB][b_hi | b_lo]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + nbring * 2 * C::kBBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + (bres ? tp.ncb * C::kBBytes : nbring * 2 * C::kBBytes));
   uint64_t* stg_full = bars;               // [NS <= 8] X landed (TMA)
   uint64_t* stg_empty = bars + 8;          // [NS] stage free (MMA commit)
   uint64_t* a_full = bars + 16;            // [NS] A pieces written (converters) -- [NSA] decoupled
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < NSA; ++i) mbar_init(a_empty + i, 1);
     for (int i = 0; i < NB; ++i) {
       mbar_init(b_full + i, 1);
-      mbar_init(b_empty + i, 1);
+      mbar_init(b_empty + i, THR ? 2 : 1);  // (threshold mode: both issuers release a stage)
     }
     for (int i = 0; i < 2 * EG; ++i) {
       mbar_init(acc_full + i, 1);
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             mbar_arrive_expect_tx(stg_full + s1, nbox * BM * 128);
             for (int b = 0; b < nbox; ++b)
-              tma_load_2d(stg + s1 * kStgBytes + b * BM * 128, &tmap_x, stg_full + s1, kc * BK + b * 32, row0);
+              tma_load_2d(stg + s1 * stgb + b * BM * 128, &tmap_x, stg_full + s1, kc * BK + b * 32, row0);
             TRACE(ntl, 0);
           }
         }
@@ -247,8 +250,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 2 && lane == 0) {
       // ---------------------------------------------------------- TMA producer: B pieces
       uint32_t n2 = 0;
+      if (bres) {  // the table once: every block's hi piece, one barrier
+        mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(ncb) * C::kBBytes);
+        for (int cb = 0; cb < ncb; ++cb) tma_load_2d(bring + cb * C::kBBytes, &tmap_bh, b_full, 0, cb * BN);
+      }
       // (threshold mode: a B block serves two tiles, see the issuer)
-      for (int64_t t = blockIdx.x; t < ntiles; t += (THR ? 2 : 1) * static_cast<int64_t>(gridDim.x)) {
+      for (int64_t t = blockIdx.x; t < ntiles && !bres; t += (THR ? 2 : 1) * static_cast<int64_t>(gridDim.x)) {
         for (int cb = 0; cb < ncb; ++cb) {
           for (int kc = 0; kc < nkc; ++kc, ++n2) {
             const int sb = n2 % NB;
@@ -266,45 +273,69 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-    } else if (THR && warp == 1) {
-      // ---------------------------------------------------------- MMA issuer, threshold mode:
+    } else if (THR && (warp == 1 || warp == 3)) {
+      // ---------------------------------------------------------- MMA issuers, threshold mode:
       // one K chunk, A-resident tiles; a cluster block is D/16 + 1 (or 3 D/16 + 1) MMAs, so
       // the issue path itself must stay short -- incremental ring positions (no division),
-      // operand descriptors by offset from one base per ring.  The whole warp runs the loop
-      // (every value warp-uniform: descriptors stay in uniform registers) and one elected
-      // lane issues.  Two tiles at a time, their cluster blocks interleaved: each B block is
-      // loaded once for both, tile 2i feeds epilogue group 0's buffer pair and tile 2i + 1
-      // group 1's, so both groups scan concurrently with no merge between them.
+      // operand descriptors by offset from one base per ring, and the whole warp runs the
+      // loop (every value warp-uniform: descriptors stay in uniform registers) while one
+      // elected lane issues.  Two tiles at a time: each B block is loaded once for both;
+      // warp 1 issues tile 2i into epilogue group 0's buffer pair, warp 3 tile 2i + 1 into
+      // group 1's, so the two issue streams (whose per-block waits are latency, not work)
+      // overlap, and both groups scan concurrently with no merge between them.  A B stage is
+      // free when both issuers' MMAs on it retired (b_empty counts two).
+      const int g = warp == 3 ? 1 : 0;
       const int nks = (p.d + 15) >> 4;
       const uint64_t da0 = desc_k_sw128(smem_u32(stg)), db0 = desc_k_sw128(smem_u32(bring));
       const uint32_t xo = static_cast<uint32_t>(tp.thr) >> 3;  // the extra K step, in descriptor units (16 B)
       const int l1 = tp.thr_l1;
       int s1 = 0, sb = 0;
-      uint32_t ph1 = 0, phb = 0, ng0 = 0, ng1 = 0;
+      uint32_t ph1 = 0, phb = 0, ngc = 0;
+      auto adv_a = [&](int k) {
+        s1 += k;
+        while (s1 >= NS) {
+          s1 -= NS;
+          ph1 ^= 1u;
+        }
+      };
+      if (g) adv_a(1);
       const int64_t nmine = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
       for (int64_t i = 0; i < nmine; i += 2) {
-        const bool two = i + 1 < nmine;
-        int s2 = s1 + 1;
-        uint32_t ph2 = ph1;
-        if (s2 == NS) {
-          s2 = 0;
-          ph2 ^= 1u;
-        }
-        const uint64_t dah0 = da0 + static_cast<uint32_t>(s1) * (kStgBytes >> 4);
-        const uint64_t dah1 = da0 + static_cast<uint32_t>(s2) * (kStgBytes >> 4);
-        TW(3, a_full + s1, ph1);
-        if (two) TW(3, a_full + s2, ph2);
+        const bool have = i + g < nmine;  // (the last pair may lack its second tile)
+        const uint64_t dah = da0 + static_cast<uint32_t>(s1) * (static_cast<uint32_t>(stgb) >> 4), dal = dah + (kABytes >> 4);
+        if (have) TW(5, a_full + s1, ph1);
+        if (bres && i == 0) TW(3, b_full, 0u);  // the resident table has landed
         for (int cb = 0; cb < ncb; ++cb) {
+          if (bres) {
+            if (have) {
+              const uint64_t dbh = db0 + static_cast<uint32_t>(cb) * (C::kBBytes >> 4);
+              const int ab = 2 * g + static_cast<int>(ngc & 1u);
+              TW(2, acc_empty + ab, ((ngc >> 1) & 1u) ^ 1u);
+              ++ngc;
+              tc_fence_after();
+              const uint32_t dacc = tmem_base + ab * astride;
+              if (elect_one_sync()) {
+                if (nks == 2) {
+                  mma_f16(dacc, dah, dbh, kIdesc, 0u);
+                  mma_f16(dacc, dah + 2, dbh + 2, kIdesc, 1u);
+                } else {
+                  for (int ks = 0; ks < nks; ++ks) mma_f16(dacc, dah + 2 * ks, dbh + 2 * ks, kIdesc, ks > 0 ? 1u : 0u);
+                }
+                mma_f16(dacc, dah + xo, dbh + xo, kIdesc, 1u);  // + t_row + q_k
+                mma_commit(acc_full + ab);
+                if (cb == ncb - 1) mma_commit(stg_empty + s1);
+              }
+              __syncwarp();
+            }
+            continue;
+          }
           TW(3, b_full + sb, phb);
-          const uint64_t dbh = db0 + static_cast<uint32_t>(sb) * (static_cast<uint32_t>(bstr) >> 4), dbl = dbh + (C::kBBytes >> 4);
-#pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            if (g == 1 && !two) break;
-            const uint32_t cntg = g ? ng1 : ng0;
-            const int ab = 2 * g + static_cast<int>(cntg & 1u);
-            TW(2, acc_empty + ab, ((cntg >> 1) & 1u) ^ 1u);
+          if (have) {
+            const uint64_t dbh = db0 + static_cast<uint32_t>(sb) * (static_cast<uint32_t>(bstr) >> 4), dbl = dbh + (C::kBBytes >> 4);
+            const int ab = 2 * g + static_cast<int>(ngc & 1u);
+            TW(2, acc_empty + ab, ((ngc >> 1) & 1u) ^ 1u);
+            ++ngc;
             tc_fence_after();
-            const uint64_t dah = g ? dah1 : dah0, dal = dah + (kABytes >> 4);
             const uint32_t dacc = tmem_base + ab * astride;
             if (elect_one_sync()) {
               if (l1 == 1) {  // hx.hm only
@@ -323,17 +354,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               mma_f16(dacc, dah + xo, dbh + xo, kIdesc, 1u);  // + t_row + q_k
               mma_commit(acc_full + ab);
+              mma_commit(b_empty + sb);
+              if (cb == ncb - 1) mma_commit(stg_empty + s1);
             }
-            __syncwarp();
-            if (g) ++ng1;
-            else ++ng0;
-          }
-          if (elect_one_sync()) {
-            mma_commit(b_empty + sb);
-            if (cb == ncb - 1) {
-              mma_commit(stg_empty + s1);
-              if (two) mma_commit(stg_empty + s2);
-            }
+          } else if (elect_one_sync()) {
+            mbar_arrive(b_empty + sb);  // nothing of this stage is read by this issuer
           }
           __syncwarp();
           if (++sb == NB) {
@@ -341,12 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             phb ^= 1u;
           }
         }
-        const int adv = two ? 2 : 1;
-        for (int a = 0; a < adv; ++a)
-          if (++s1 == NS) {
-            s1 = 0;
-            ph1 ^= 1u;
-          }
+        adv_a(2);
       }
     } else if (warp == 1 && lane == 0 && !(TS && NSA)) {
       // ---------------------------------------------------------- MMA issuer (column-split
@@ -643,14 +663,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int64_t row = t * BM + r;
         const uint4 tsl = (mine && row < p.n) ? __ldg(tp.thr_t + row) : make_uint4(0u, 0u, 0u, 0u);
-        mbar_wait(stg_full + s1, ph1);
-        uint8_t* sbase = stg + s1 * kStgBytes;
+        TW(4, stg_full + s1, ph1);
+        uint8_t* sbase = stg + s1 * stgb;
         float4 f[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) f[u] = *reinterpret_cast<const float4*>(sbase + rd + ((u ^ sw) << 4));
-        if (tail_box && 32 >= p.d) {
+        if (tail_box && 32 >= p.d) {  // box 1 absent (and, with 16 KB stages, not this stage's memory)
 #pragma unroll
           for (int u = 0; u < 8; ++u) f[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) f[u] = *reinterpret_cast<const float4*>(sbase + rd + ((u ^ sw) << 4));
         }
         named_bar(5, 256);  // every read of the stage precedes the in-place writes
 #pragma unroll
@@ -1406,8 +1427,9 @@ __global__ void __launch_bounds__(256) nn_list_kernel(const float* __restrict__ 
 
 // Per row: T = min over the own cluster's candidate list of the key p_k - 2 x.mu_k (fp32, its
 // rounding bounded below), the certified margin of the tensor-core comparison, and the 8 fp16
-// A slots of t_row.  One warp per piece of the label-sorted rows (<= 2048 rows of one
-// cluster): the candidates' means sit in shared memory (broadcast reads), one row per lane.
+// A slots of t_row.  One block per piece of the label-sorted rows (<= 2048 rows of one
+// cluster; a persistent grid strides the pieces): the candidates' means sit in shared memory
+// (broadcast reads), one row per thread.
 template <int D>
 __global__ void __launch_bounds__(256) thr_kernel(const float* __restrict__ X, const int32_t* __restrict__ rows,
                                                   int k, const int64_t* __restrict__ seg_begin,
@@ -1420,10 +1442,8 @@ __global__ void __launch_bounds__(256) thr_kernel(const float* __restrict__ X, c
                                                   const int* abort) {
   griddep_wait();
   if (*abort) return;
-  __shared__ __align__(16) float cm[8][kThrM][D];  // per warp: candidate means (fp32 roundings)
-  __shared__ float cp[8][kThrM];                   // ... and their p_k
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  __shared__ __align__(16) float cm[kThrM][D];  // candidate means (fp32 roundings)
+  __shared__ float cp[kThrM];                   // ... and their p_k
   const int64_t total = piece_start[k];
   const TcScale sc = *scale;
   const double u = 5.9604645e-8;
@@ -1432,7 +1452,7 @@ __global__ void __launch_bounds__(256) thr_kernel(const float* __restrict__ X, c
   // one-MMA level (lmmax given): max_k ||mu_k - hm_k|| in mu units
   const double lm_any = lmmax ? static_cast<double>(*lmmax) * (1.0 + 1e-6) : -1.0;
   const float2 sx2 = make_float2(sc.sx, sc.sx), neg1 = make_float2(-1.f, -1.f);
-  for (int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; p < total; p += nw) {
+  for (int64_t p = blockIdx.x; p < total; p += gridDim.x) {
     int lo = 0, hi = k - 1;  // cluster owning piece p: largest c with piece_start[c] <= p
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -1442,14 +1462,14 @@ __global__ void __launch_bounds__(256) thr_kernel(const float* __restrict__ X, c
     const int c = lo;
     const int64_t b0 = seg_begin[c] + (p - piece_start[c]) * piece_rows;
     const int64_t b1 = min(seg_end[c], b0 + piece_rows);
-    __syncwarp();
-    for (int j = 0; j < kThrM; ++j) {
-      const int kk = nn[c * kThrM + j];
-      for (int l = lane; l < D; l += 32) cm[wib][j][l] = mu32[static_cast<int64_t>(kk) * dp + l];
-      if (lane == 0) cp[wib][j] = p32[kk];
+    __syncthreads();  // the previous piece's reads of cm / cp are done
+    for (int e = threadIdx.x; e < kThrM * D; e += blockDim.x) {
+      const int j = e / D, l = e - j * D;
+      cm[j][l] = mu32[static_cast<int64_t>(nn[c * kThrM + j]) * dp + l];
     }
-    __syncwarp();
-    for (int64_t pos = b0 + lane; pos < b1; pos += 32) {
+    if (threadIdx.x < kThrM) cp[threadIdx.x] = p32[nn[c * kThrM + threadIdx.x]];
+    __syncthreads();
+    for (int64_t pos = b0 + threadIdx.x; pos < b1; pos += blockDim.x) {
       const int64_t r = rows[pos];
       const float4* xr = reinterpret_cast<const float4*>(X + r * D);
       float2 x[D / 2];
@@ -1478,11 +1498,11 @@ __global__ void __launch_bounds__(256) thr_kernel(const float* __restrict__ X, c
         float2 a = make_float2(0.f, 0.f);
 #pragma unroll
         for (int q = 0; q < D / 4; ++q) {
-          const float4 m = *reinterpret_cast<const float4*>(&cm[wib][j][4 * q]);
+          const float4 m = *reinterpret_cast<const float4*>(&cm[j][4 * q]);
           a = __ffma2_rn(x[2 * q], make_float2(m.x, m.y), a);
           a = __ffma2_rn(x[2 * q + 1], make_float2(m.z, m.w), a);
         }
-        T = fminf(T, fmaf(-2.0f, a.x + a.y, cp[wib][j]));
+        T = fminf(T, fmaf(-2.0f, a.x + a.y, cp[j]));
       }
       const double ss = static_cast<double>(ss2.x + ss2.y);
       const double xn = sqrt(ss) * (1.0 + (D + 4) * u);  // >= ||x||
@@ -1530,10 +1550,11 @@ int pick_bn(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : 128; }
 
 // Shared memory with `nstg` X staging stages: operand ring, staging ring, barriers,
 // meta_xi, merge partials, own clusters, column bias (fp32) and norms (fp16).
-size_t tc_smem(int bn, int kp, int nstg, int nbs = 0) {
+size_t tc_smem(int bn, int kp, int nstg, int nbs = 0, int astg = kStgBytes, size_t bres_bytes = 0) {
   size_t bring = bn <= 32 ? TcCfg<32>::kBRing : bn <= 64 ? TcCfg<64>::kBRing : TcCfg<128>::kBRing;
   if (nbs) bring = static_cast<size_t>(nbs) * 2 * bn * 128;
-  return 1024 + bring + static_cast<size_t>(nstg) * kStgBytes + 50 * 8 + 4 * BM * 8 + 10 * BM * 4 + 2 * BM * 4 +
+  if (bres_bytes) bring = bres_bytes;
+  return 1024 + bring + static_cast<size_t>(nstg) * astg + 50 * 8 + 4 * BM * 8 + 10 * BM * 4 + 2 * BM * 4 +
          static_cast<size_t>(ncb_bn_pad(kp)) * 4 + static_cast<size_t>(kp) * 2 + 16;
 }
 constexpr int kMaxStg = 8;
@@ -1559,7 +1580,8 @@ template <int BN, bool COS, int KC = 32, int EG = 2, bool T3 = false, bool THR =
 void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                const TcParams& tp, int64_t ntiles, bool rec = true) {
   auto kern = tp.dbg ? score_tc_kernel<BN, COS, true, KC, EG, T3, THR> : score_tc_kernel<BN, COS, false, KC, EG, T3, THR>;
-  const size_t smem = tc_smem(BN, tp.ncb * BN, tp.nstg + tp.nsa, THR ? tp.nbs : 0);
+  const size_t smem = THR ? tc_smem(BN, tp.ncb * BN, tp.nstg, tp.nbs, tp.astg, tp.bres ? static_cast<size_t>(tp.ncb) * BN * 128 : 0)
+                          : tc_smem(BN, tp.ncb * BN, tp.nstg + tp.nsa);
   if (c->timing && rec) {  // the kernel alone, for the roofline (ms_score_kernel)
     FSIL_CUDA(cudaEventRecord(c->ev[7], c->stream));
     c->ev7_recorded = true;
@@ -1867,7 +1889,7 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     const int64_t* seg_begin = c->seg_start.as<int64_t>();
     const int64_t* seg_end = seg_begin + c->k + 1;
     const int64_t* piece_start = c->piece_start.as<int64_t>() + c->k + 2;
-    const int tgrid = c->num_sms * 8;
+    const int tgrid = c->num_sms * 6;  // (blocks stride the pieces)
     uint4* tt = c->thr_t.as<uint4>();
     // MMAs per K step: 1 (default: hx.hm; the dropped pieces, ~2^-11 relative, widen each
     // row's margin -- a few more two-candidate rows, a third of the tensor and operand
@@ -1900,6 +1922,21 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
       while (nbs > 1 && tc_smem(bn, kp, ns, nbs) > c->smem_optin) --nbs;
       tp.nbs = nbs;
       tp.nstg = ns;
+      // one-MMA level at D <= 32: a stage is box 0 alone (16 KB: the fp32 box, converted in
+      // place to the hi piece), and when the whole hi-piece table (Kp x 128 B) fits beside
+      // four such stages it stays resident -- no B ring, no per-block L2 reads
+      // (FSIL_THR_BRES=0: ring)
+      tp.astg = (tp.thr_l1 == 1 && c->d <= 32) ? kStgBytes / 2 : kStgBytes;
+      static const bool bres_env = [] { const char* e = std::getenv("FSIL_THR_BRES"); return !e || std::atoi(e) != 0; }();
+      const size_t tab = static_cast<size_t>(kp) * 128;
+      if (bres_env && tp.thr_l1 == 1) {
+        int nsr = std::min(6, std::max(2, ns_env));
+        while (nsr > 2 && tc_smem(bn, kp, nsr, nbs, tp.astg, tab) > c->smem_optin) --nsr;
+        if (tc_smem(bn, kp, nsr, nbs, tp.astg, tab) <= c->smem_optin) {
+          tp.bres = 1;
+          tp.nstg = nsr;
+        }
+      }
     }
     c->tc_thr = 1;
     c->cand_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int4));

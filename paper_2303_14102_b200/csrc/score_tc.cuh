@@ -61,6 +61,8 @@ struct TcParams {
   int thr;                // 0 off; else the first fp16 column of the extra K step (16 ceil(D/16))
   const uint4* thr_t;     // [n] per row: the 8 fp16 A slots of t_row (thr_kernel)
   int nbs;                // threshold mode: B operand stages (0: the block-size default)
+  int astg;               // threshold mode: bytes per A stage (16 KB when only box 0 / the hi piece is staged; else 32 KB)
+  int bres;               // threshold mode: the whole hi-piece table stays in shared memory (no B ring)
   int thr_l1;             // threshold mode: MMAs per K step -- 3 (fp16x3) or 1 (hx.hm only; the dropped pieces are in the row's margin)
   int4* cand_rows;        // [n] threshold mode: a row's second to fourth candidate columns (when nb[row]'s top bits say 2..4)
 };

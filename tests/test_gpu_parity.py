@@ -247,6 +247,52 @@ def test_tc_cosine_mixed_norms_unit_scale(ctx):
     assert np.array_equal(got.neighbour[small], ref.neighbour[small])
 
 
+def _nearest_centre_blobs(n, d, k, spread, seed, offset=0.0):
+    """Gaussian blobs relabelled by nearest centre: overlapping, uneven clusters (C4's recipe)."""
+    rng = np.random.default_rng(seed)
+    cen = rng.normal(size=(k, d)) * spread
+    X = (cen[rng.integers(0, k, n)] + rng.normal(size=(n, d))).astype(np.float32)
+    x64 = X.astype(np.float64)
+    d2 = (x64 ** 2).sum(1)[:, None] - 2 * x64 @ cen.T + (cen ** 2).sum(1)[None]
+    return X + np.float32(offset), d2.argmin(1)
+
+
+@pytest.mark.parametrize("name,n,d,k,spread,offset", [
+    ("overlap d32", 120_000, 32, 700, 1.0, 0.0),     # heavy overlap: many rows with 2-4 candidates
+    ("separated d32", 120_000, 32, 1000, 3.0, 0.0),  # C4-like: almost every row certified outright
+    ("d16", 150_000, 16, 600, 1.5, 0.0),             # one K step + the threshold step
+    ("d48", 100_000, 48, 300, 2.0, 0.0),             # two fp32 boxes, 32 KB stages, B ring
+    ("k257", 80_000, 32, 257, 2.0, 0.0),             # one column into the third cluster block
+    ("k2100", 40_000, 32, 2100, 2.0, 0.0),           # table too large to stay resident: B ring
+    ("offset", 100_000, 32, 500, 2.0, 500.0),        # ||x|| >> spread: no row certifies, all refined
+])
+def test_tc_threshold_mode(ctx, name, n, d, k, spread, offset):
+    """Threshold mode of the single-CTA tcgen05 kernel (sqeuclid, D <= 48, several cluster
+    blocks, label-sorted aggregation): the comparison against the per-row certified threshold
+    runs inside the MMA and the epilogue harvests sign bits.  Every row's neighbour must be
+    the oracle's (candidate rows are resolved in fp64), a/b/s at fp64 noise."""
+    X, L = _nearest_centre_blobs(n, d, k, spread, seed=5 + d + k, offset=offset)
+    got, ref = check(ctx, X, L, "sqeuclid", "tcgen05", label=name)
+    st = ctx.stats()
+    assert st["tc_threshold"] == 1, (name, st)
+    if offset == 0.0:
+        assert st["flagged_rows"] < n // 4, (name, st)
+
+
+def test_tc_threshold_mode_switch(ctx):
+    """FSIL_THR_BRES / FSIL_THR_L1 are read once per process, so the ring variants are covered
+    by shapes (d48, k2100 above); here: the threshold scan and the classic scan agree row for
+    row on the same input (the classic scan is what K <= 128 or D > 48 shapes take)."""
+    X, L = _nearest_centre_blobs(90_000, 32, 400, 2.0, seed=77)
+    got, _ = check(ctx, X, L, "sqeuclid", "tcgen05", label="thr")
+    assert ctx.stats()["tc_threshold"] == 1
+    X2 = np.concatenate([X, np.zeros((X.shape[0], 32), np.float32)], axis=1)  # D = 64: classic scan
+    got2, _ = check(ctx, X2, L, "sqeuclid", "tcgen05", label="classic")
+    assert ctx.stats()["tc_threshold"] == 0
+    assert np.array_equal(got.neighbour, got2.neighbour)
+    assert np.abs(got.s - got2.s).max() <= 1e-12
+
+
 @pytest.mark.parametrize("metric", ["sqeuclid", "cosine"])
 @pytest.mark.parametrize("k_pad,d", [(0, 64), (97, 64), (290, 64), (290, 256)])
 def test_tc_certificate_adversarial_near_ties(ctx, metric, k_pad, d):
