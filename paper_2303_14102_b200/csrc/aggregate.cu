@@ -763,7 +763,7 @@ __global__ void __launch_bounds__(256) agg_piece_kernel(
 // ---------------------------------------------------------------- path 2 ----
 // Hand-written stable counting sort of the rows by dense label (no library sort):
 //   count   : G warp-chunks of L consecutive rows; each warp histograms its chunk in
-//             shared memory (match_any groups equal labels) -> hist[c][g]
+//             shared memory (atomics; match_any groups equal labels when K is small) -> hist[c][g]
 //   offsets : per label, an exclusive scan over the chunks (a row of chunk g lands
 //             after every row of chunks < g with the same label) + the label's total
 //   starts  : one block scans the K totals -> segment bounds, pieces per cluster and
@@ -790,13 +790,20 @@ __global__ void __launch_bounds__(128) label_count_kernel(const int32_t* __restr
       const int64_t i = base + u * 32 + lane;
       lab[u] = i < b1 ? __ldg(dense + i) : -1;
     }
+    if (k >= 64) {  // equal labels in a 32-row group are rare: shared-memory atomics
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const unsigned peers = __match_any_sync(0xffffffffu, lab[u]);
-      if (lab[u] >= 0 && lane == __ffs(peers) - 1) h[lab[u]] += __popc(peers);
-      __syncwarp();
+      for (int u = 0; u < U; ++u)
+        if (lab[u] >= 0) atomicAdd(h + lab[u], 1);
+    } else {  // few labels: one add per distinct label of the group
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned peers = __match_any_sync(0xffffffffu, lab[u]);
+        if (lab[u] >= 0 && lane == __ffs(peers) - 1) h[lab[u]] += __popc(peers);
+        __syncwarp();
+      }
     }
   }
+  __syncwarp();
   for (int c = lane; c < k; c += 32) hist[static_cast<size_t>(c) * G + g] = h[c];
 }
 

@@ -75,8 +75,7 @@ __device__ int64_t find_slot(const unsigned long long* keys, uint32_t mask, uint
   return -1;
 }
 
-// Per-block shared-memory dedup of a contiguous row range; only the lowest lane of
-// each run of equal labels in a warp touches the table.
+// Per-block shared-memory dedup of a contiguous row range.
 __device__ __forceinline__ void collect_body(const int32_t* __restrict__ labels, int64_t n, int64_t chunk,
                                              unsigned long long* gkeys, unsigned long long* gvals, uint32_t mask,
                                              uint32_t epoch, int* overflow, int nslots) {
@@ -89,7 +88,6 @@ __device__ __forceinline__ void collect_body(const int32_t* __restrict__ labels,
     svals[i] = 0xffffffffu;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * chunk;
   const int64_t r1 = min(n, r0 + chunk);
   constexpr int U = 4;
@@ -104,20 +102,22 @@ __device__ __forceinline__ void collect_body(const int32_t* __restrict__ labels,
     for (int u = 0; u < U; ++u) {
       const int64_t i = base + u * blockDim.x + threadIdx.x;
       const bool valid = i < r1;
-      const unsigned long long key = valid ? label_key(lab[u]) : 0ull;
-      const unsigned peers = __match_any_sync(0xffffffffu, key);
-      if (!valid || (__ffs(peers) - 1) != lane) continue;
+      if (!valid) continue;
+      // every lane probes for itself: once a label sits in the block's table with a first row
+      // below this one (always, after the chunk's first few rows) the lookup is two shared
+      // loads and no atomic; lanes with equal labels read the same words (broadcast)
+      const unsigned long long key = label_key(lab[u]);
       const uint32_t row = static_cast<uint32_t>(i);
       uint32_t h = hash32(static_cast<uint32_t>(lab[u])) & (nslots - 1);
       bool done = false;
       for (int probe = 0; probe < 16; ++probe) {  // bounded: overflow goes global
-        unsigned long long cur = skeys[h];
+        unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(skeys + h);
         if (cur == 0) {
           const unsigned long long prev = atomicCAS(skeys + h, 0ull, key);
           cur = prev == 0 ? key : prev;
         }
         if (cur == key) {
-          if (row < svals[h]) atomicMin(svals + h, row);
+          if (row < *reinterpret_cast<volatile uint32_t*>(svals + h)) atomicMin(svals + h, row);
           done = true;
           break;
         }

@@ -519,7 +519,91 @@ __device__ __forceinline__ void exact_units(const ScoreParams& p, const double* 
   const int d = p.d, d2 = p.d >> 1;
   const T* X = sizeof(T) == 8 ? reinterpret_cast<const T*>(p.X64) : reinterpret_cast<const T*>(p.X);
   if (wid >= nunits) return;
-  if constexpr (CPL > 0) {
+  if constexpr (CPL > 0 && CPL <= 4 && LPR <= 8) {
+    // Narrow rows (D <= 64: LPR <= 8 lanes per row and passes per unit, at most four pairs per
+    // lane; measured at D = 128 the 48 live partials spill and the plain ring below wins).  Same rolling register ring
+    // as below, but the LPR lanes' partial dots of every pass are kept until the unit ends and
+    // reduced by a transposing butterfly: at each step a lane hands half of its passes to its
+    // partner and keeps the other half, so after log2(LPR) steps lane (sub, li) holds the full
+    // sums of pass li's row -- (LPR - 1) 64-bit exchanges per quantity and unit instead of
+    // PPU log2(LPR) + PPU (the pass was shuffle- and issue-bound at D <= 128, not HBM-bound).
+    // The pairing (li ^ LPR/2, ..., li ^ 1) is the plain butterfly's, so each row's sums are
+    // bit-identical to it.
+    constexpr int DEPTH = 4;
+    static_assert(PPU % DEPTH == 0 && PPU == LPR, "a unit must end on a ring boundary");
+    const int64_t npass = ((nunits - 1 - wid) / nw + 1) * PPU;
+    V buf[DEPTH][CPL];
+    int bown[DEPTH], bnb[DEPTH];
+    auto row_of = [&](int64_t j) { return (wid + (j / PPU) * nw) * kUnitRows + (j % PPU) * RPP + sub; };
+    auto load = [&](int64_t j, V (&b)[CPL], int& o, int& nb) {
+      const int64_t pos = row_of(j);
+      const bool ok = j < npass && pos < p.n;
+      const V* xr = reinterpret_cast<const V*>(X + (ok ? pos : 0) * d);
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) b[c] = xr[li + LPR * c];
+      o = ok ? __ldg(p.dense + pos) : 0;
+      nb = ok ? p.nb[pos] : 0;
+    };
+#pragma unroll
+    for (int h = 0; h < DEPTH; ++h) load(h, buf[h], bown[h], bnb[h]);
+    for (int64_t j0 = 0; j0 < npass; j0 += PPU) {
+      double pss[PPU], pco[PPU], pcb[PPU];
+      int rown = 0, rnb = 0;
+#pragma unroll
+      for (int ps = 0; ps < PPU; ++ps) {
+        constexpr int kD = DEPTH;
+        const int h = ps % kD;
+        const int own = bown[h], nb = bnb[h];
+        const double* yo = ytab + static_cast<int64_t>(own) * d;
+        const double* yb = ytab + static_cast<int64_t>(nb) * d;
+        double ss = 0.0, co = 0.0, cb = 0.0;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int q = li + LPR * c;
+          const double2 o = *reinterpret_cast<const double2*>(yo + 2 * q);
+          const double2 b = *reinterpret_cast<const double2*>(yb + 2 * q);
+          const double x0 = static_cast<double>(buf[h][c].x), x1 = static_cast<double>(buf[h][c].y);
+          ss = fma(x0, x0, ss);
+          ss = fma(x1, x1, ss);
+          co = fma(o.x, x0, co);
+          co = fma(o.y, x1, co);
+          cb = fma(b.x, x0, cb);
+          cb = fma(b.y, x1, cb);
+        }
+        pss[ps] = ss;
+        pco[ps] = co;
+        pcb[ps] = cb;
+        if (li == ps) {  // (every lane of the row's group loaded its own / neighbour ids)
+          rown = own;
+          rnb = nb;
+        }
+        load(j0 + ps + DEPTH, buf[h], bown[h], bnb[h]);  // refill the slot just consumed
+      }
+      // transposing butterfly: `half` passes survive each step; the lane keeps the passes whose
+      // bit matches its own li bit
+#pragma unroll
+      for (int half = LPR >> 1; half > 0; half >>= 1) {
+        const bool up = (li & half) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+          const double s0 = up ? pss[i] : pss[i + half], s1 = up ? pco[i] : pco[i + half],
+                       s2 = up ? pcb[i] : pcb[i + half];
+          const double k0 = up ? pss[i + half] : pss[i], k1 = up ? pco[i + half] : pco[i],
+                       k2 = up ? pcb[i + half] : pcb[i];
+          pss[i] = k0 + __shfl_xor_sync(0xffffffffu, s0, half);
+          pco[i] = k1 + __shfl_xor_sync(0xffffffffu, s1, half);
+          pcb[i] = k2 + __shfl_xor_sync(0xffffffffu, s2, half);
+        }
+      }
+      // lane (sub, li) holds row li * RPP + sub of the unit; fixed-order tree over the lanes
+      const int64_t u = wid + (j0 / PPU) * nw;
+      const int64_t pos = u * kUnitRows + li * RPP + sub;
+      double su = pos < p.n ? exact_finish<COS>(p, pos, rown, rnb, pss[0], pco[0], pcb[0]) : 0.0;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) su += __shfl_xor_sync(0xffffffffu, su, off);
+      if (lane == 0) usum[u] = su;
+    }
+  } else if constexpr (CPL > 0) {
     // The warp's passes (units wid, wid + nw, ...; PPU passes each) form one stream with a
     // rolling register ring: pass j + DEPTH is loaded while pass j is reduced, so DEPTH
     // passes' rows are always in flight (the pass is HBM-latency bound otherwise).
