@@ -1361,7 +1361,10 @@ __global__ void prep_b_kernel(const double* __restrict__ stats, const float* __r
 // the neighbour, certain; two -> a certified pair (two fp64 means decide, pair_kernel); none
 // or more -> the fp64 refinement over all K.  a_i, b_i, s_i come from the exact pass as
 // always.  Which clusters enter T only affects how many rows have a single hit.
-constexpr int kThrM = 16;  // candidate clusters per row
+#ifndef FSIL_THR_M
+#define FSIL_THR_M 16
+#endif
+constexpr int kThrM = FSIL_THR_M;  // candidate clusters per row
 constexpr int kPieceRowsTc = 2048;  // = aggregate.cu's kPieceRows (rows per label-sorted piece)
 
 // One block per cluster c: the kThrM clusters k != c with the smallest p_k - 2 mu_c.mu_k

@@ -7,7 +7,7 @@ tag=$1; shift
 mkdir -p ab/obj_$tag
 C=paper_2303_14102_b200/csrc
 objs=()
-for f in densify aggregate score_ffma score_tc naive finalize capi; do
+for f in densify aggregate score_ffma score_tc score_tc2 naive finalize capi; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -O3 \
     -Iinclude -I$C "$@" -c $C/$f.cu -o ab/obj_$tag/$f.o &
   objs+=(ab/obj_$tag/$f.o)
