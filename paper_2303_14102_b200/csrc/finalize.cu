@@ -798,8 +798,8 @@ __device__ __forceinline__ void pair_rows_body(const ScoreParams& p, const int2*
 
 // Threshold mode's resolution pass.  The scoring epilogue left in the top bits of nb[row]:
 // 0 the neighbour is certain; 2..4 the neighbour is one of that many columns -- nb[row] and
-// cand[row].{x,y,z}; 1 no usable candidate set.  This pass scans nb (one row per lane), and
-// the warp resolves its marked rows one after another: the candidates' fp64 foreign means
+// cand[row].{x,y,z}; 1 no usable candidate set.  This pass scans nb (128 rows per warp step), and
+// the warp resolves its marked rows four at a time (eight lanes each): the candidates' fp64 foreign means
 // with the reference formula, clamp included, then the reference's rule -- strict <, equal
 // means keep the lowest index (squared_euclidean.cpp:94-103) -- or, for code 1, the row
 // joins the fp64 refinement's list.  counts[1] += rows resolved here (statistics).
@@ -810,45 +810,76 @@ __global__ void __launch_bounds__(256) thr_resolve_kernel(ScoreParams p, const i
   if (*p.abort) return;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, sub = lane >> 3, li = lane & 7;
   const double* sums = p.stats + (COS ? p.k : 2 * p.k);
   const int d = p.d;
   unsigned long long resolved = 0;
-  for (int64_t base = warp * 32; base < p.n; base += nwarps * 32) {
-    const int64_t mine = base + lane;
-    const uint32_t v = mine < p.n ? static_cast<uint32_t>(p.nb[mine]) : 0u;
-    uint32_t todo = __ballot_sync(0xffffffffu, (v >> 28) != 0u);
-    while (todo) {
-      const int l = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const uint32_t vv = __shfl_sync(0xffffffffu, v, l);
-      const int64_t row = base + l;
-      const int code = static_cast<int>(vv >> 28);
-      const int c1 = static_cast<int>(vv & 0x0fffffffu);
-      if (code == 1) {
-        if (lane == 0) {
-          p.nb[row] = c1;
-          const unsigned long long idx = atomicAdd(p.flag_count, 1ull);
-          p.flag_rows[idx] = static_cast<int32_t>(row);
-        }
-        continue;
-      }
-      const int4 rec = cand[row];
-      const int cs[4] = {c1, rec.x, code >= 3 ? rec.y : -1, code >= 4 ? rec.z : -1};
-      double ss = 0.0, dt[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int e = lane; e < d; e += 32) {
-        const double x = xval(p, row * d + e);
-        ss = fma(x, x, ss);
+  // 128 consecutive rows per warp step (four nb loads in flight); their marked rows are
+  // resolved four at a time, eight lanes each: the chain per row -- record, row and candidate
+  // sums loads, reduction, fp64 finish -- is latency, so rows overlap
+  for (int64_t base = warp * 128; base < p.n; base += nwarps * 128) {
+    uint32_t v[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (cs[j] >= 0) dt[j] = fma(sums[static_cast<int64_t>(cs[j]) * d + e], x, dt[j]);
+    for (int g = 0; g < 4; ++g) {
+      const int64_t mine = base + g * 32 + lane;
+      v[g] = mine < p.n ? static_cast<uint32_t>(p.nb[mine]) : 0u;
+    }
+    unsigned long long todo_lo = __ballot_sync(0xffffffffu, (v[0] >> 28) != 0u) |
+                                 (static_cast<unsigned long long>(__ballot_sync(0xffffffffu, (v[1] >> 28) != 0u)) << 32);
+    unsigned long long todo_hi = __ballot_sync(0xffffffffu, (v[2] >> 28) != 0u) |
+                                 (static_cast<unsigned long long>(__ballot_sync(0xffffffffu, (v[3] >> 28) != 0u)) << 32);
+    while (todo_lo | todo_hi) {
+      int l = -1;  // position within the 128 rows
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int f = -1;
+        if (todo_lo) {
+          f = __ffsll(static_cast<long long>(todo_lo)) - 1;
+          todo_lo &= todo_lo - 1;
+        } else if (todo_hi) {
+          f = 64 + __ffsll(static_cast<long long>(todo_hi)) - 1;
+          todo_hi &= todo_hi - 1;
+        }
+        if (q == sub) l = f;
       }
-      for (int off = 16; off > 0; off >>= 1) {
+      const int src = l < 0 ? 0 : (l & 31), gsel = l < 0 ? 0 : (l >> 5);
+      const uint32_t w0 = __shfl_sync(0xffffffffu, v[0], src), w1 = __shfl_sync(0xffffffffu, v[1], src),
+                     w2 = __shfl_sync(0xffffffffu, v[2], src), w3 = __shfl_sync(0xffffffffu, v[3], src);
+      const uint32_t vv = gsel == 0 ? w0 : gsel == 1 ? w1 : gsel == 2 ? w2 : w3;
+      const int64_t row = base + (l < 0 ? 0 : l);
+      const int code = l < 0 ? 0 : static_cast<int>(vv >> 28);
+      const int c1 = static_cast<int>(vv & 0x0fffffffu);
+      if (code == 1 && li == 0) {
+        p.nb[row] = c1;
+        const unsigned long long idx = atomicAdd(p.flag_count, 1ull);
+        p.flag_rows[idx] = static_cast<int32_t>(row);
+      }
+      const bool work = code >= 2;
+      int cs[4] = {-1, -1, -1, -1};
+      if (work) {
+        const int4 rec = cand[row];
+        cs[0] = c1;
+        cs[1] = rec.x;
+        cs[2] = code >= 3 ? rec.y : -1;
+        cs[3] = code >= 4 ? rec.z : -1;
+      }
+      double ss = 0.0, dt[4] = {0.0, 0.0, 0.0, 0.0};
+      if (work) {
+        for (int e = li; e < d; e += 8) {
+          const double x = xval(p, row * d + e);
+          ss = fma(x, x, ss);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (cs[j] >= 0) dt[j] = fma(sums[static_cast<int64_t>(cs[j]) * d + e], x, dt[j]);
+        }
+      }
+#pragma unroll
+      for (int off = 4; off > 0; off >>= 1) {
         ss += __shfl_xor_sync(0xffffffffu, ss, off);
 #pragma unroll
         for (int j = 0; j < 4; ++j) dt[j] += __shfl_xor_sync(0xffffffffu, dt[j], off);
       }
-      if (lane == 0) {
+      if (li == 0 && work) {
         const double nrm = sqrt(ss);
         double best = 0.0;
         int arg = -1;
@@ -867,6 +898,7 @@ __global__ void __launch_bounds__(256) thr_resolve_kernel(ScoreParams p, const i
       }
     }
   }
+  for (int off = 16; off > 0; off >>= 1) resolved += __shfl_xor_sync(0xffffffffu, resolved, off);
   if (lane == 0 && resolved) atomicAdd(counts + 1, resolved);
 }
 

@@ -294,7 +294,7 @@ def test_tc_threshold_mode_switch(ctx):
 
 
 @pytest.mark.parametrize("metric", ["sqeuclid", "cosine"])
-@pytest.mark.parametrize("k_pad,d", [(0, 64), (97, 64), (290, 64), (290, 256)])
+@pytest.mark.parametrize("k_pad,d", [(0, 64), (97, 64), (290, 64), (290, 256), (290, 32), (290, 48)])
 def test_tc_certificate_adversarial_near_ties(ctx, metric, k_pad, d):
     """Pins the neighbour certificate: rows placed at controlled distances from the
     bisector of two mirror clusters A (dense id 1) and B (dense id 2), so their top-2 gap
@@ -334,6 +334,49 @@ def test_tc_certificate_adversarial_near_ties(ctx, metric, k_pad, d):
     # both candidates really occur, and a good share of rows is decided on the fast pass
     assert set(np.unique(ref.neighbour[:n_rows])) >= {1, 2}
     assert ctx.stats()["flagged_rows"] < n_rows
+    if metric == "sqeuclid" and d <= 48:  # the threshold scan (comparison inside the MMA)
+        assert ctx.stats()["tc_threshold"] == 1
+
+
+def test_tc_threshold_mode_edge_cases(ctx):
+    """The reference's edge cases on the threshold scan (D = 32, K > 256): singleton clusters
+    (s = 0, report.cpp:18-21), a two-point cluster, exact duplicates of other rows, a cluster of
+    identical points (a = 0), and two clusters with identical members under different labels --
+    every row's distance to them ties exactly, so the lowest dense id must win
+    (squared_euclidean.cpp:94-103) wherever one of them is the neighbour."""
+    X, L = _nearest_centre_blobs(60_000, 32, 300, 3.0, seed=91)
+    L = L.astype(np.int64)
+    rng = np.random.default_rng(92)
+    extra_x, extra_l = [], []
+    nxt = int(L.max()) + 1
+    for _ in range(3):  # singletons, far from and close to other clusters
+        extra_x.append(X[rng.integers(0, X.shape[0])][None] + rng.normal(size=(1, 32)).astype(np.float32) * 0.5)
+        extra_l.append([nxt])
+        nxt += 1
+    extra_x.append(X[:2] + np.float32(0.25))  # a two-point cluster
+    extra_l.append([nxt, nxt])
+    nxt += 1
+    dup = rng.choice(X.shape[0], 500, replace=False)  # exact duplicates keep their labels
+    extra_x.append(X[dup])
+    extra_l.append(L[dup])
+    extra_x.append(np.repeat(X[7][None] + np.float32(1.0), 40, axis=0))  # identical points
+    extra_l.append([nxt] * 40)
+    nxt += 1
+    twin = X[L == L[11]][:200] + np.float32(0.5)  # twin clusters: the same members twice
+    extra_x += [twin, twin]
+    extra_l += [[nxt] * twin.shape[0], [nxt + 1] * twin.shape[0]]
+    X = np.concatenate([X] + extra_x).astype(np.float32)
+    L = np.concatenate([L] + [np.asarray(e, np.int64) for e in extra_l])
+    got, ref = check(ctx, X, L, "sqeuclid", "tcgen05", label="thr edge")
+    assert ctx.stats()["tc_threshold"] == 1
+    assert np.array_equal(got.neighbour, ref.neighbour)
+    single = np.isin(L, np.arange(int(L.max()) - 6, int(L.max()) - 3))
+    assert single.sum() == 3 and np.all(got.s[single] == 0.0) and np.all(got.a[single] == 0.0)
+    # rows whose neighbour is a twin carry the lower of the two dense ids
+    t0, t1 = np.flatnonzero(np.asarray(ref.dense_to_raw) == nxt)[0], np.flatnonzero(np.asarray(ref.dense_to_raw) == nxt + 1)[0]
+    assert np.any(got.neighbour == min(t0, t1))
+    other = ~np.isin(got.own, [t0, t1])
+    assert not np.any(got.neighbour[other] == max(t0, t1))
 
 
 def test_validation_errors_match_reference(ctx):
