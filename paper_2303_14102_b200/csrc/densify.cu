@@ -464,6 +464,11 @@ void densify_local(fsil_context* c) {
   // and the call is redone without speculation when it differs.
   const bool spec = c->speculate && !c->spec_block_once && c->k_last >= 2;
   c->spec_block_once = false;
+  // A small speculated dictionary gets a 1024-slot table (12 KB): every map block stages the
+  // table in shared memory and finish scans all of it, so its size is most of their cost when
+  // N is small (C1, C2).  More labels than expected: the speculation misses and the repeat
+  // takes the full-size table.
+  if (spec && c->k_last <= 256) cap = 1024;
   for (;;) {
     const uint32_t epoch = prepare_table(c, cap);
     c->dict_sorted.ensure(cap * (2 * sizeof(int32_t)));

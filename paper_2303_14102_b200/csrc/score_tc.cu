@@ -178,11 +178,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* cb_s = reinterpret_cast<float*>(meta_own + 2 * BM);  // [ncb*BN] column bias
   __half* mn_s = reinterpret_cast<__half*>(cb_s + ncb_bn_pad(tp.ncb * BN));  // [ncb*BN] ||mu_k||/mu_max, rounded up
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Role ids rotated by tp.wshift warps (a multiple of 4: the setmaxnreg warpgroups and the
+  // epilogue's TMEM lane quadrants keep their alignment): an experiment switch that puts the
+  // producers and MMA issuers (logical warps 0-3) on the physical warps 16-19.
+  const int tid = tp.wshift ? static_cast<int>((threadIdx.x + 32u * tp.wshift) % kThreads) : static_cast<int>(threadIdx.x);
+  const int warp = tid >> 5, lane = tid & 31;
   const int ncb = tp.ncb, nkc = tp.nkc;
   unsigned long long* const dbgp = PROF ? tp.dbg : nullptr;  // compiled out unless profiling
   const long long t_start = dbgp ? clock64() : 0;
-  for (int j = threadIdx.x; j < ncb * BN; j += blockDim.x) {
+  for (int j = tid; j < ncb * BN; j += blockDim.x) {
     cb_s[j] = tp.colbias[j];
     mn_s[j] = tp.munorm[j];
   }
@@ -529,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // two threads per row; thread half hq reads fp32 box hq of the stage, then -- after
     // the whole group has read -- writes A chunks 4hq..4hq+3 of hi (over box 0) and lo
     // (over box 1))
-    const int tl = threadIdx.x - kConv0 * 32;
+    const int tl = tid - kConv0 * 32;
     const int r = tl & (BM - 1), hq = tl >> 7;  // row in tile, box / chunk half
     const int sw = r & 7;
     const float2 sx2 = make_float2(sc.sx, sc.sx), neg1 = make_float2(-1.f, -1.f);
@@ -864,6 +868,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         return (tt < ntiles && rr < p.n) ? __ldg(p.dense + rr) : -1;
       };
       int own_n = fetch_own(blockIdx.x + (TS ? grp : 0) * static_cast<int64_t>(gridDim.x));
+      // per row: four (hit mask, chunk base) slots in shared memory, [grp][slot][row] (the
+      // meta_xi / part regions, unused in this mode); written and read by the row's own thread
+      constexpr uint32_t kHitStride = BM * 8;
+      static_assert(2 * 4 * kHitStride <= (4 * BM * 8 + 10 * BM * 4), "hit slots exceed the reused regions");
+      const uint32_t hs0 = smem_u32(meta_xi) + static_cast<uint32_t>(grp) * 4u * kHitStride + static_cast<uint32_t>(r) * 8u;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
         const int tb = nt & 1;
         if (TS && static_cast<int>(nt % EG) != grp) continue;  // another group takes this tile
@@ -873,8 +882,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         own_n = fetch_own(t + tstep);
         // per row: up to four (chunk base, hit mask) slots, filled without branches; the
         // masks are decoded into columns once per tile
-        int nh = 0, k1 = 0, k2 = 0, k3 = 0, k4 = 0;
-        uint32_t h1 = 0, h2 = 0, h3 = 0, h4 = 0;
+        uint32_t sp = 0;  // byte offset of the row's next (hit mask, chunk base) slot
+        // the own column's chunk base and its cleared bit (own = -1: no chunk matches)
+        const int okb = own & ~31;
+        const uint32_t onot = ~(1u << (8 * (own & 3) + ((own & 31) >> 2)));
+        auto harvest = [&](const uint32_t(&v)[32], int k0) {
+          // sign bytes by byte permutes in sign-replication mode (0xff where the accumulator
+          // is negative), four elements per word; word i contributes bit i of each byte:
+          // bit 8c + i of `neg` <-> element 4i + c.  No shifts, no dependent chain longer
+          // than the four-deep OR.
+          uint32_t n0 = 0, n1 = 0;
+#pragma unroll
+          for (int i = 0; i < 8; i += 2) {
+            const uint32_t w0 = prmt(prmt(v[4 * i], v[4 * i + 1], 0xfbfbu), prmt(v[4 * i + 2], v[4 * i + 3], 0xfbfbu), 0x5410u);
+            const uint32_t w1 = prmt(prmt(v[4 * i + 4], v[4 * i + 5], 0xfbfbu), prmt(v[4 * i + 6], v[4 * i + 7], 0xfbfbu), 0x5410u);
+            n0 |= w0 & (0x01010101u << i);
+            n1 |= w1 & (0x01010101u << (i + 1));
+          }
+          uint32_t hits = ~(n0 | n1);
+          if (k0 == okb) hits &= onot;  // the own column never counts
+          // a chunk with hits (rare) is appended to the row's shared-memory slots by a
+          // predicated store: no branch, no vote, nothing else on the common path
+          const bool hit = hits != 0u;
+          if (hit && sp < 4u * kHitStride) st_shared_v2(hs0 + sp, hits, static_cast<uint32_t>(k0));
+          sp += hit ? kHitStride : 0u;
+        };
+        uint32_t v[32], w[32];
+        int pend_k0 = -1;  // chunk (in w) whose scan is still owed: the previous block's last
         for (int cb = 0; cb < ncb; ++cb) {
           int ab;
           uint32_t ph;
@@ -890,46 +924,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           TW(8, acc_full + ab, ph);
           const long long ts0 = dbgp ? clock64() : 0;
           tc_fence_after();
-          auto harvest = [&](const uint32_t(&v)[32], int k0) {
-            uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              m0 = __funnelshift_l(v[j], m0, 1);  // (m << 1) | sign
-              m1 = __funnelshift_l(v[8 + j], m1, 1);
-              m2 = __funnelshift_l(v[16 + j], m2, 1);
-              m3 = __funnelshift_l(v[24 + j], m3, 1);
-            }
-            uint32_t hits = ~((m0 << 24) | (m1 << 16) | (m2 << 8) | m3);  // bit 31 - j: element j
-            const uint32_t orel = static_cast<uint32_t>(own - k0);          // the own column never counts
-            hits &= ~(orel < 32u ? 0x80000000u >> orel : 0u);
-            const bool any = hits != 0u;
-            h4 = (any && nh == 3) ? hits : h4;
-            k4 = (any && nh == 3) ? k0 : k4;
-            h3 = (any && nh == 2) ? hits : h3;
-            k3 = (any && nh == 2) ? k0 : k3;
-            h2 = (any && nh == 1) ? hits : h2;
-            k2 = (any && nh == 1) ? k0 : k2;
-            h1 = (any && nh == 0) ? hits : h1;
-            k1 = (any && nh == 0) ? k0 : k1;
-            nh += any ? 1 : 0;
-          };
-          const int q0 = TS ? 0 : grp, qs = TS ? 1 : 2;
+          // The block's four 32-column chunks, software-pipelined: chunk q + 1 is in flight
+          // while chunk q is scanned (tcgen05.wait::ld waits for every outstanding load, so
+          // the overlap is load-vs-scan, one chunk deep), the previous block's last chunk is
+          // scanned under this block's first load, and the accumulator goes back to the
+          // issuer as soon as its last chunk is in registers.
+          static_assert(!THR || BN == 128, "threshold scan: 128-column blocks");
           const uint32_t tb0 = tmem_base + ab * astride + (static_cast<uint32_t>(quad * 32) << 16);
-#pragma unroll 1
-          for (int q = q0; q < NQ; q += 2 * qs) {  // two chunks per TMEM wait
-            uint32_t v[32], w[32];
-            const bool two = q + qs < NQ;
-            tmem_ld32_issue(tb0 + q * 32, v);
-            if (two) tmem_ld32_issue(tb0 + (q + qs) * 32, w);
-            tmem_ld_wait2(v, w);
-            harvest(v, cb * BN + q * 32);
-            if (two) harvest(w, cb * BN + (q + qs) * 32);
-          }
+          const int kb0 = cb * BN;
+          tmem_ld32_issue(tb0, v);
+          if (pend_k0 >= 0) harvest(w, pend_k0);
+          tmem_ld_wait(v);
+          tmem_ld32_issue(tb0 + 32, w);
+          harvest(v, kb0);
+          tmem_ld_wait(w);
+          tmem_ld32_issue(tb0 + 64, v);
+          harvest(w, kb0 + 32);
+          tmem_ld_wait(v);
+          tmem_ld32_issue(tb0 + 96, w);
+          harvest(v, kb0 + 64);
+          tmem_ld_wait(w);
+          pend_k0 = kb0 + 96;
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(acc_empty + ab);
           if (dbgp && warp == kEpiWarp0 && lane == 0) atomicAdd(dbgp + 12, static_cast<unsigned long long>(clock64() - ts0));
         }
+        if (pend_k0 >= 0) harvest(w, pend_k0);
         // decode: columns of the set bits in ascending order (slots are in scan order), the
         // padding columns >= K dropped; more than four chunks with hits -> "more than four"
         int cnt = 0, c1 = -1, c2 = -1, c3 = -1, c4 = -1;
@@ -948,11 +969,19 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           };
-          decode(h1, k1);
-          decode(h2, k2);
-          decode(h3, k3);
-          decode(h4, k4);
-          if (nh > 4) cnt = 5;
+          const uint32_t nh = sp / kHitStride;
+          for (uint32_t i = 0; i < (nh < 4u ? nh : 4u); ++i) {
+            uint32_t hm, kb;
+            ld_shared_v2(hs0 + i * kHitStride, hm, kb);
+            uint32_t nat = 0;  // back to scan order: bit 31 - e <-> element e
+            while (hm) {
+              const int b = __ffs(hm) - 1;
+              hm &= hm - 1;
+              nat |= 0x80000000u >> (4 * (b & 7) + (b >> 3));
+            }
+            decode(nat, static_cast<int>(kb));
+          }
+          if (nh > 4u) cnt = 5;
         }
         if (!TS) {  // merge the two column halves (group 1 -> smem -> group 0)
           int* pt = reinterpret_cast<int*>(part + tb * 5 * BM);  // double-buffered by tile parity
@@ -1941,6 +1970,10 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
         }
       }
     }
+    // role rotation (see the kernel's `tid`; FSIL_TC_WSHIFT=4: issuers and producers on the
+    // highest warp ids).  Measured at C4: no effect (2.79 ms either way), so off by default.
+    static const int wshift_env = [] { const char* e = std::getenv("FSIL_TC_WSHIFT"); return e ? std::atoi(e) : 0; }();
+    tp.wshift = (wshift_env > 0 && wshift_env % 4 == 0 && wshift_env < kThreads / 32) ? wshift_env : 0;
     c->tc_thr = 1;
     c->cand_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int4));
     tp.cand_rows = c->cand_rows.as<int4>();

@@ -63,6 +63,7 @@ struct TcParams {
   int nbs;                // threshold mode: B operand stages (0: the block-size default)
   int astg;               // threshold mode: bytes per A stage (16 KB when only box 0 / the hi piece is staged; else 32 KB)
   int bres;               // threshold mode: the whole hi-piece table stays in shared memory (no B ring)
+  int wshift;             // role ids rotated by this many warps (0 or a multiple of 4): logical warp = (physical + wshift) % 20
   int thr_l1;             // threshold mode: MMAs per K step -- 3 (fp16x3) or 1 (hx.hm only; the dropped pieces are in the row's margin)
   int4* cand_rows;        // [n] threshold mode: a row's second to fourth candidate columns (when nb[row]'s top bits say 2..4)
 };
