@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-    } else if (warp == 2 && lane == 0) {
+    } else if (warp == 2 && lane == 0 && !(THR && EG == 3)) {
       // ---------------------------------------------------------- TMA producer: B pieces
       uint32_t n2 = 0;
       if (bres) {  // the table once: every block's hi piece, one barrier
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-    } else if (THR && (warp == 1 || warp == 3)) {
+    } else if (THR && (warp == 1 || warp == 3 || (EG == 3 && warp == 2))) {
       // ---------------------------------------------------------- MMA issuers, threshold mode:
       // one K chunk, A-resident tiles; a cluster block is D/16 + 1 (or 3 D/16 + 1) MMAs, so
       // the issue path itself must stay short -- incremental ring positions (no division),
@@ -288,7 +288,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       // group 1's, so the two issue streams (whose per-block waits are latency, not work)
       // overlap, and both groups scan concurrently with no merge between them.  A B stage is
       // free when both issuers' MMAs on it retired (b_empty counts two).
-      const int g = warp == 3 ? 1 : 0;
+      // Three groups (EG = 3; only with the resident table, so warp 2 has no B ring to feed:
+      // it loads the table once and issues for group 2): three tiles at a time, ONE
+      // accumulator per group -- a group's MMAs and scan alternate, the three groups overlap.
+      const int g = warp == 1 ? 0 : warp == 3 ? 1 : 2;
+      if (EG == 3 && warp == 2) {
+        if (lane == 0) {
+          mbar_arrive_expect_tx(b_full, static_cast<uint32_t>(ncb) * C::kBBytes);
+          for (int cb = 0; cb < ncb; ++cb) tma_load_2d(bring + cb * C::kBBytes, &tmap_bh, b_full, 0, cb * BN);
+        }
+        __syncwarp();
+      }
       const int nks = (p.d + 15) >> 4;
       const uint64_t da0 = desc_k_sw128(smem_u32(stg)), db0 = desc_k_sw128(smem_u32(bring));
       const uint32_t xo = static_cast<uint32_t>(tp.thr) >> 3;  // the extra K step, in descriptor units (16 B)
@@ -302,9 +312,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           ph1 ^= 1u;
         }
       };
-      if (g) adv_a(1);
+      if (g) adv_a(g);
       const int64_t nmine = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-      for (int64_t i = 0; i < nmine; i += 2) {
+      for (int64_t i = 0; i < nmine; i += EG) {
         const bool have = i + g < nmine;  // (the last pair may lack its second tile)
         const uint64_t dah = da0 + static_cast<uint32_t>(s1) * (static_cast<uint32_t>(stgb) >> 4), dal = dah + (kABytes >> 4);
         if (have) TW(5, a_full + s1, ph1);
@@ -313,8 +323,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (bres) {
             if (have) {
               const uint64_t dbh = db0 + static_cast<uint32_t>(cb) * (C::kBBytes >> 4);
-              const int ab = 2 * g + static_cast<int>(ngc & 1u);
-              TW(2, acc_empty + ab, ((ngc >> 1) & 1u) ^ 1u);
+              const int ab = EG == 3 ? g : 2 * g + static_cast<int>(ngc & 1u);
+              TW(2, acc_empty + ab, (EG == 3 ? (ngc & 1u) : ((ngc >> 1) & 1u)) ^ 1u);
               ++ngc;
               tc_fence_after();
               const uint32_t dacc = tmem_base + ab * astride;
@@ -370,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             phb ^= 1u;
           }
         }
-        adv_a(2);
+        adv_a(EG);
       }
     } else if (warp == 1 && lane == 0 && !(TS && NSA)) {
       // ---------------------------------------------------------- MMA issuer (column-split
@@ -526,7 +536,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= kConv0) {
-    constexpr int kConvRegs = EG == 3 ? 56 : FSIL_CONV_REGS;
+    // (threshold mode with three groups: its converter loop is the two-group one, 80 registers,
+    // and its scan needs fewer than the classic epilogue: 4 x 64 + 12 x 112 + 4 x 80 = the pool)
+    constexpr int kConvRegs = EG == 3 ? (THR ? 80 : 56) : FSIL_CONV_REGS;
     static_assert(4 * FSIL_WG0_REGS + 12 * 120 + 4 * 56 <= 20 * 96, "EG = 3 register split exceeds the pool");
     if (kConvRegs != 96) setmaxnreg_dec<kConvRegs>();
     // ------------------------------------------------------------ converters (8 warps:
@@ -544,7 +556,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ext: ||x||^2 comes from the aggregation pass and the epilogue fetches its per-row
     // inputs itself -- the converters only convert (no norm, no meta hand-off)
     const bool ext = tp.lean != 0;
-    if (EG == 3) {
+    if (EG == 3 && !THR) {
       // decoupled, four converter warps (one thread per row, both 32-column boxes in
       // turn, two 16-byte units at a time -- 56 registers): wait for the stage and a free
       // A slot, convert, then free the stage and publish the slot
@@ -661,7 +673,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t rd = hq * (BM * 128) + r * 128, wr = r * 128;
       const bool tail_box = hq == 1;
       const int jx = tp.thr >> 3;
-      const bool mine = (jx >> 2) == hq;
+      // (three epilogue groups leave four converter warps: one thread per row, D <= 32, so the
+      // row's second half holds nothing but the extra K step's slots -- written below)
+      constexpr bool HALF = kConvWarps == 4;
+      const bool mine = HALF || (jx >> 2) == hq;
       const uint32_t g1 = static_cast<uint32_t>(sc.thr_g + 15) << 10, g2 = g1 | (g1 << 16);  // fp16 2^g, twice
       const bool hi_only = tp.thr_l1 == 1;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -677,7 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int u = 0; u < 8; ++u) f[u] = *reinterpret_cast<const float4*>(sbase + rd + ((u ^ sw) << 4));
         }
-        named_bar(5, 256);  // every read of the stage precedes the in-place writes
+        named_bar(5, HALF ? 128 : 256);  // every read of the stage precedes the in-place writes
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
           const float v[8] = {f[2 * jj].x,     f[2 * jj].y,     f[2 * jj].z,     f[2 * jj].w,
@@ -698,6 +713,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (mine && 4 * hq + jj == jx + 1) hv = make_uint4(g2, g2, g2, g2);
           *reinterpret_cast<uint4*>(sbase + pos) = hv;
           if (!hi_only) *reinterpret_cast<uint4*>(sbase + BM * 128 + pos) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        }
+        if (HALF && jx >= 4) {  // D = 32: the slots are chunks 4 and 5 of the row
+          *reinterpret_cast<uint4*>(sbase + wr + ((jx ^ sw) << 4)) = tsl;
+          *reinterpret_cast<uint4*>(sbase + wr + (((jx + 1) ^ sw) << 4)) = make_uint4(g2, g2, g2, g2);
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -852,7 +871,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue (8 warps)
-    setmaxnreg_inc<EG == 3 ? 120 : FSIL_EPI_REGS>();  // CTA pool: see the static_asserts
+    setmaxnreg_inc<EG == 3 ? (THR ? 112 : 120) : FSIL_EPI_REGS>();  // CTA pool: see the static_asserts
     const int quad = warp & 3;                // TMEM lane quadrant of this warp
     const int r = quad * 32 + lane;           // row in tile
     const int grp = (warp - kEpiWarp0) >> 2;  // epilogue group 0 / 1
@@ -868,11 +887,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         return (tt < ntiles && rr < p.n) ? __ldg(p.dense + rr) : -1;
       };
       int own_n = fetch_own(blockIdx.x + (TS ? grp : 0) * static_cast<int64_t>(gridDim.x));
-      // per row: four (hit mask, chunk base) slots in shared memory, [grp][slot][row] (the
-      // meta_xi / part regions, unused in this mode); written and read by the row's own thread
+      // per row: four (hit mask, chunk base) slots in shared memory, [grp][slot][row] (two groups:
+      // the meta_xi / part regions, unused in this mode); written and read by the row's own thread
       constexpr uint32_t kHitStride = BM * 8;
-      static_assert(2 * 4 * kHitStride <= (4 * BM * 8 + 10 * BM * 4), "hit slots exceed the reused regions");
-      const uint32_t hs0 = smem_u32(meta_xi) + static_cast<uint32_t>(grp) * 4u * kHitStride + static_cast<uint32_t>(r) * 8u;
+      static_assert(EG == 3 || 2 * 4 * kHitStride <= (4 * BM * 8 + 10 * BM * 4), "hit slots exceed the reused regions");
+      // (three groups: 12 KB after the column norms, see tc_smem)
+      const uint32_t hsb = EG == 3 ? ((smem_u32(mn_s + tp.ncb * BN) + 15u) & ~15u) : smem_u32(meta_xi);
+      const uint32_t hs0 = hsb + static_cast<uint32_t>(grp) * 4u * kHitStride + static_cast<uint32_t>(r) * 8u;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
         const int tb = nt & 1;
         if (TS && static_cast<int>(nt % EG) != grp) continue;  // another group takes this tile
@@ -912,7 +933,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int cb = 0; cb < ncb; ++cb) {
           int ab;
           uint32_t ph;
-          if (TS) {
+          if (TS && EG == 3) {  // (three groups: one accumulator each)
+            ab = grp;
+            ph = ng & 1;
+            ++ng;
+          } else if (TS) {
             ab = 2 * grp + (ng & 1);
             ph = (ng >> 1) & 1;
             ++ng;
@@ -1582,14 +1607,15 @@ int pick_bn(int k) { return k <= 32 ? 32 : k <= 64 ? 64 : 128; }
 
 // Shared memory with `nstg` X staging stages: operand ring, staging ring, barriers,
 // meta_xi, merge partials, own clusters, column bias (fp32) and norms (fp16).
-size_t tc_smem(int bn, int kp, int nstg, int nbs = 0, int astg = kStgBytes, size_t bres_bytes = 0) {
+size_t tc_smem(int bn, int kp, int nstg, int nbs = 0, int astg = kStgBytes, size_t bres_bytes = 0, size_t extra = 0) {
   size_t bring = bn <= 32 ? TcCfg<32>::kBRing : bn <= 64 ? TcCfg<64>::kBRing : TcCfg<128>::kBRing;
   if (nbs) bring = static_cast<size_t>(nbs) * 2 * bn * 128;
   if (bres_bytes) bring = bres_bytes;
   return 1024 + bring + static_cast<size_t>(nstg) * astg + 50 * 8 + 4 * BM * 8 + 10 * BM * 4 + 2 * BM * 4 +
-         static_cast<size_t>(ncb_bn_pad(kp)) * 4 + static_cast<size_t>(kp) * 2 + 16;
+         static_cast<size_t>(ncb_bn_pad(kp)) * 4 + static_cast<size_t>(kp) * 2 + 16 + extra;
 }
 constexpr int kMaxStg = 8;
+constexpr size_t kHitSlots3 = 3 * 4 * BM * 8 + 16;  // threshold mode, three groups: the rows' hit slots
 int tc_stages(int bn, int kp, size_t optin) {
   int ns = kMaxStg;
   while (ns > 2 && tc_smem(bn, kp, ns) > optin) --ns;
@@ -1612,7 +1638,8 @@ template <int BN, bool COS, int KC = 32, int EG = 2, bool T3 = false, bool THR =
 void launch_tc(fsil_context* c, const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                const TcParams& tp, int64_t ntiles, bool rec = true) {
   auto kern = tp.dbg ? score_tc_kernel<BN, COS, true, KC, EG, T3, THR> : score_tc_kernel<BN, COS, false, KC, EG, T3, THR>;
-  const size_t smem = THR ? tc_smem(BN, tp.ncb * BN, tp.nstg, tp.nbs, tp.astg, tp.bres ? static_cast<size_t>(tp.ncb) * BN * 128 : 0)
+  const size_t smem = THR ? tc_smem(BN, tp.ncb * BN, tp.nstg, tp.nbs, tp.astg, tp.bres ? static_cast<size_t>(tp.ncb) * BN * 128 : 0,
+                                  EG == 3 ? kHitSlots3 : 0)
                           : tc_smem(BN, tp.ncb * BN, tp.nstg + tp.nsa);
   if (c->timing && rec) {  // the kernel alone, for the roofline (ms_score_kernel)
     FSIL_CUDA(cudaEventRecord(c->ev[7], c->stream));
@@ -1912,6 +1939,7 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     return;
   }
   c->tc_mmas = 3;
+  bool thr_eg3 = false;
   if (thr) {
     c->thr_nn.ensure(static_cast<size_t>(c->k) * kThrM * sizeof(int32_t));
     c->thr_t.ensure(static_cast<size_t>(c->n) * sizeof(uint4));
@@ -1968,6 +1996,18 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
           tp.bres = 1;
           tp.nstg = nsr;
         }
+        // three epilogue groups (three tiles in flight, one accumulator each; four converter
+        // warps): resident table, D <= 32, and room for three stages + the hit slots
+        // (FSIL_THR_EG3=0: two groups)
+        static const bool eg3t_env = [] { const char* e = std::getenv("FSIL_THR_EG3"); return !e || std::atoi(e) != 0; }();
+        if (tp.bres && eg3t_env && c->d <= 32) {
+          int ns3 = 6;
+          while (ns3 > 3 && tc_smem(bn, kp, ns3, nbs, tp.astg, tab, kHitSlots3) > c->smem_optin) --ns3;
+          if (tc_smem(bn, kp, ns3, nbs, tp.astg, tab, kHitSlots3) <= c->smem_optin) {
+            thr_eg3 = true;
+            tp.nstg = ns3;
+          }
+        }
       }
     }
     // role rotation (see the kernel's `tid`; FSIL_TC_WSHIFT=4: issuers and producers on the
@@ -1977,7 +2017,8 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     c->tc_thr = 1;
     c->cand_rows.ensure(std::max<int64_t>(c->n, 1) * sizeof(int4));
     tp.cand_rows = c->cand_rows.as<int4>();
-    launch_tc<128, false, 32, 2, false, true>(c, mx, mh, ml, tp, ntiles);
+    if (thr_eg3) launch_tc<128, false, 32, 3, false, true>(c, mx, mh, ml, tp, ntiles);
+    else launch_tc<128, false, 32, 2, false, true>(c, mx, mh, ml, tp, ntiles);
   }
   // K <= 24 at BN = 32: the epilogue scans only the first 16 / 24 columns
   const int kc_scan = bn == 32 && c->k <= 16 ? 16 : bn == 32 && c->k <= 24 ? 24 : 32;
