@@ -258,11 +258,12 @@ def _nearest_centre_blobs(n, d, k, spread, seed, offset=0.0):
 
 
 @pytest.mark.parametrize("name,n,d,k,spread,offset", [
-    ("overlap d32", 120_000, 32, 700, 1.0, 0.0),     # heavy overlap: many rows with 2-4 candidates
+    ("overlap d32", 120_000, 32, 700, 1.0, 0.0),     # heavy overlap: many rows with 2-4 candidates (three groups)
     ("separated d32", 120_000, 32, 1000, 3.0, 0.0),  # C4-like: almost every row certified outright
     ("d16", 150_000, 16, 600, 1.5, 0.0),             # one K step + the threshold step
     ("d48", 100_000, 48, 300, 2.0, 0.0),             # two fp32 boxes, 32 KB stages, B ring
     ("k257", 80_000, 32, 257, 2.0, 0.0),             # one column into the third cluster block
+    ("k1200", 50_000, 32, 1200, 2.0, 0.0),           # resident table, no room for the third group's stages: two groups
     ("k2100", 40_000, 32, 2100, 2.0, 0.0),           # table too large to stay resident: B ring
     ("offset", 100_000, 32, 500, 2.0, 500.0),        # ||x|| >> spread: no row certifies, all refined
 ])
