@@ -540,6 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // and its scan needs fewer than the classic epilogue: 4 x 64 + 12 x 112 + 4 x 80 = the pool)
     constexpr int kConvRegs = EG == 3 ? (THR ? 80 : 56) : FSIL_CONV_REGS;
     static_assert(4 * FSIL_WG0_REGS + 12 * 120 + 4 * 56 <= 20 * 96, "EG = 3 register split exceeds the pool");
+    static_assert(4 * FSIL_WG0_REGS + 12 * 112 + 4 * 80 <= 20 * 96, "threshold mode, EG = 3: register split exceeds the pool");
     if (kConvRegs != 96) setmaxnreg_dec<kConvRegs>();
     // ------------------------------------------------------------ converters (8 warps:
     // two threads per row; thread half hq reads fp32 box hq of the stage, then -- after
