@@ -1489,7 +1489,7 @@ __global__ void __launch_bounds__(256) nn_list_kernel(const float* __restrict__ 
 // cluster; a persistent grid strides the pieces): the candidates' means sit in shared memory
 // (broadcast reads), one row per thread.
 template <int D>
-__global__ void __launch_bounds__(256) thr_kernel(const float* __restrict__ X, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256, 4) thr_kernel(const float* __restrict__ X, const int32_t* __restrict__ rows,
                                                   int k, const int64_t* __restrict__ seg_begin,
                                                   const int64_t* __restrict__ seg_end,
                                                   const int64_t* __restrict__ piece_start, int piece_rows,
@@ -1950,7 +1950,7 @@ void score_tc(fsil_context* c, const ScoreParams& p) {
     const int64_t* seg_begin = c->seg_start.as<int64_t>();
     const int64_t* seg_end = seg_begin + c->k + 1;
     const int64_t* piece_start = c->piece_start.as<int64_t>() + c->k + 2;
-    const int tgrid = c->num_sms * 6;  // (blocks stride the pieces)
+    const int tgrid = c->num_sms * 8;  // (blocks stride the pieces; four resident per SM)
     uint4* tt = c->thr_t.as<uint4>();
     // MMAs per K step: 1 (default: hx.hm; the dropped pieces, ~2^-11 relative, widen each
     // row's margin -- a few more two-candidate rows, a third of the tensor and operand
