@@ -673,22 +673,40 @@ __global__ void __launch_bounds__(256) agg_piece_kernel(
     for (int e = 0; e < VEC; ++e) acc[q][e] = 0.0;
   double psi = 0.0, cnt = 0.0;
   float amax = 0.f;
-  for (int64_t base = b0; base < b1; base += rpw) {
-    const int64_t pos = base + sub;  // warp-uniform trip count
-    const bool valid = pos < b1;
-    const int64_t r = valid ? rows[pos] : 0;
-    T v[CPL][VEC];
+  // U row groups per step: their index loads, then their row loads, are issued together (the
+  // walk is a chain of two dependent loads per row otherwise -- latency-bound); the rows are
+  // still accumulated one after the other, so every sum keeps its order.
+  constexpr int U = CPL == 1 ? 4 : 1;  // (wider lanes: the row registers would spill)
+  for (int64_t base0 = b0; base0 < b1; base0 += U * rpw) {
+    int64_t ru[U];
+    bool validu[U];
+    T vu[U][CPL][VEC];
 #pragma unroll
-    for (int q = 0; q < CPL; ++q) {
-      const int ch = li + q * lpr;
-      if constexpr (VEC == 4) {  // float input only
-        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid && ch < nchunks) t = ldg_stream(reinterpret_cast<const float4*>(X + r * d) + ch);
-        v[q][0] = t.x; v[q][1] = t.y; v[q][2] = t.z; v[q][3] = t.w;
-      } else {
-        v[q][0] = (valid && ch < nchunks) ? __ldg(X + r * d + ch) : T(0);
+    for (int u = 0; u < U; ++u) {
+      const int64_t pos = base0 + u * rpw + sub;  // warp-uniform trip count
+      validu[u] = pos < b1;
+      ru[u] = validu[u] ? rows[pos] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const int ch = li + q * lpr;
+        if constexpr (VEC == 4) {  // float input only
+          float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (validu[u] && ch < nchunks) t = ldg_stream(reinterpret_cast<const float4*>(X + ru[u] * d) + ch);
+          vu[u][q][0] = t.x; vu[u][q][1] = t.y; vu[u][q][2] = t.z; vu[u][q][3] = t.w;
+        } else {
+          vu[u][q][0] = (validu[u] && ch < nchunks) ? __ldg(X + ru[u] * d + ch) : T(0);
+        }
       }
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+    if (base0 + u * rpw >= b1) break;  // (warp-uniform: groups past the piece's end)
+    const bool valid = validu[u];
+    const int64_t r = ru[u];
+    T (&v)[CPL][VEC] = vu[u];
     double ss = 0.0;
     bool finite = true;
 #pragma unroll
@@ -729,6 +747,7 @@ __global__ void __launch_bounds__(256) agg_piece_kernel(
 #pragma unroll
       for (int e = 0; e < VEC; ++e)
         acc[q][e] += COS ? static_cast<double>(v[q][e]) * scale : static_cast<double>(v[q][e]);
+    }
   }
   // Combine row sub-groups (fixed xor order) so sub-group 0 holds the piece sums.
   for (int off = 16; off >= lpr; off >>= 1) {
