@@ -381,7 +381,7 @@ uint32_t prepare_table(fsil_context* c, int64_t cap) {
 
 void launch_collect(fsil_context* c, int64_t cap, uint32_t epoch) {
   if (c->n == 0) return;
-  const int grid = grid_for(c->n, 1024, c->num_sms, 2);
+  const int grid = grid_for(c->n, 1024, c->num_sms, 4);
   const int64_t chunk = (c->n + grid - 1) / grid;
   // shared-memory dedup slots: ~4x the previous call's label count (1024 .. 4096)
   int nslots = kSmemSlots;
