@@ -763,6 +763,8 @@ __device__ __forceinline__ void pair_rows_body(const ScoreParams& p, const int2*
                                                int64_t nwarps, int lane) {
   const int64_t cnt = static_cast<int64_t>(*count);
   const int d = p.d;
+  // fp32 rows and fp64 sums in 16-byte units: D a multiple of 4 and both bases aligned
+  const bool vec = p.X64 == nullptr && (d & 3) == 0 && ((reinterpret_cast<uintptr_t>(p.X) | reinterpret_cast<uintptr_t>(sums)) & 15) == 0;
   for (int64_t i = warp; i < cnt; i += nwarps) {
     const int2 pr = pairs[i];
     const int64_t row = pr.x;
@@ -770,11 +772,35 @@ __device__ __forceinline__ void pair_rows_body(const ScoreParams& p, const int2*
     const double* y1 = sums + static_cast<int64_t>(c1) * d;
     const double* y2 = sums + static_cast<int64_t>(c2) * d;
     double ss = 0.0, d1 = 0.0, d2 = 0.0;
-    for (int l = lane; l < d; l += 32) {
-      const double v = xval(p, row * d + l);
-      ss = fma(v, v, ss);
-      d1 = fma(y1[l], v, d1);
-      d2 = fma(y2[l], v, d2);
+    if (vec) {  // 16-byte loads, four elements per lane and step (wide rows: the loads in flight
+                // set this pass's time, 15 KB per pair from L2)
+      const float* xr = p.X + row * d;
+#pragma unroll 2
+      for (int l = lane * 4; l < d; l += 128) {
+        const float4 xv = *reinterpret_cast<const float4*>(xr + l);
+        const double2 a0 = *reinterpret_cast<const double2*>(y1 + l), a1 = *reinterpret_cast<const double2*>(y1 + l + 2);
+        const double2 b0 = *reinterpret_cast<const double2*>(y2 + l), b1 = *reinterpret_cast<const double2*>(y2 + l + 2);
+        const double x0 = xv.x, x1 = xv.y, x2 = xv.z, x3 = xv.w;
+        ss = fma(x0, x0, ss);
+        ss = fma(x1, x1, ss);
+        ss = fma(x2, x2, ss);
+        ss = fma(x3, x3, ss);
+        d1 = fma(a0.x, x0, d1);
+        d1 = fma(a0.y, x1, d1);
+        d1 = fma(a1.x, x2, d1);
+        d1 = fma(a1.y, x3, d1);
+        d2 = fma(b0.x, x0, d2);
+        d2 = fma(b0.y, x1, d2);
+        d2 = fma(b1.x, x2, d2);
+        d2 = fma(b1.y, x3, d2);
+      }
+    } else {
+      for (int l = lane; l < d; l += 32) {
+        const double v = xval(p, row * d + l);
+        ss = fma(v, v, ss);
+        d1 = fma(y1[l], v, d1);
+        d2 = fma(y2[l], v, d2);
+      }
     }
     for (int off = 16; off > 0; off >>= 1) {
       ss += __shfl_xor_sync(0xffffffffu, ss, off);
