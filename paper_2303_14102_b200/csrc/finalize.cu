@@ -839,6 +839,7 @@ __global__ void __launch_bounds__(256) thr_resolve_kernel(ScoreParams p, const i
   const int lane = threadIdx.x & 31, sub = lane >> 3, li = lane & 7;
   const double* sums = p.stats + (COS ? p.k : 2 * p.k);
   const int d = p.d;
+  const bool vec = p.X64 == nullptr && (d & 3) == 0 && ((reinterpret_cast<uintptr_t>(p.X) | reinterpret_cast<uintptr_t>(sums)) & 15) == 0;
   unsigned long long resolved = 0;
   // 128 consecutive rows per warp step (four nb loads in flight); their marked rows are
   // resolved four at a time, eight lanes each: the chain per row -- record, row and candidate
@@ -890,7 +891,27 @@ __global__ void __launch_bounds__(256) thr_resolve_kernel(ScoreParams p, const i
         cs[3] = code >= 4 ? rec.z : -1;
       }
       double ss = 0.0, dt[4] = {0.0, 0.0, 0.0, 0.0};
-      if (work) {
+      if (work && vec) {  // 16-byte loads: four elements per lane and step
+        const float* xr = p.X + row * d;
+        for (int e = 4 * li; e < d; e += 32) {
+          const float4 xv = *reinterpret_cast<const float4*>(xr + e);
+          const double x0 = xv.x, x1 = xv.y, x2 = xv.z, x3 = xv.w;
+          ss = fma(x0, x0, ss);
+          ss = fma(x1, x1, ss);
+          ss = fma(x2, x2, ss);
+          ss = fma(x3, x3, ss);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (cs[j] >= 0) {
+              const double* y = sums + static_cast<int64_t>(cs[j]) * d + e;
+              const double2 a0 = *reinterpret_cast<const double2*>(y), a1 = *reinterpret_cast<const double2*>(y + 2);
+              dt[j] = fma(a0.x, x0, dt[j]);
+              dt[j] = fma(a0.y, x1, dt[j]);
+              dt[j] = fma(a1.x, x2, dt[j]);
+              dt[j] = fma(a1.y, x3, dt[j]);
+            }
+        }
+      } else if (work) {
         for (int e = li; e < d; e += 8) {
           const double x = xval(p, row * d + e);
           ss = fma(x, x, ss);
